@@ -1,0 +1,1337 @@
+// engine.cpp — host side of the B200 FOFSE library behind include/fofse.h.
+//
+// Replaces, for the hot path, the reference's host code:
+//   src/pipeline.cpp:34-38,123-132  ConcealConfig::validate, check_pattern_fits
+//   src/pattern.cpp:55-69           validate_pattern (same messages, O(n) grid check)
+//   src/pipeline.cpp:80-121         build_window / lost_map -> window-mask CLASSES
+//   src/grid.cpp:75-92              build_isotropic_weight (exact libm formula, once)
+//   src/pipeline.cpp:136-162        parallel_blocks -> one batched GPU launch set
+//   src/pipeline.cpp:205-262        conceal (write-back, PSNR over MISSING samples)
+//
+// Design: every lost block's window mask is determined by its geometry (image
+// clip + other lost blocks inside the window). Blocks with identical masks
+// share one weight field w and one weight spectrum W ("class"), so W is
+// transformed once per class on the GPU instead of once per block
+// (engine_spectral.cpp:176 recomputes it per block). Blocks are sorted by
+// (K2 path, class) and cut into tiles; each K2 CTA stages its class's W once.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <functional>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <numeric>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/fofse.h"
+#include "kernels.h"
+#include "layout.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Unsupported : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct CudaFailure : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw CudaFailure(std::string(what) + ": " + cudaGetErrorString(e));
+}
+void ck(int e, const char* what) { ck(static_cast<cudaError_t>(e), what); }
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return FOFSE_OK;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return FOFSE_EINVAL;
+    } catch (const Unsupported& e) {
+        g_err = e.what();
+        return FOFSE_EUNSUPPORTED;
+    } catch (const CudaFailure& e) {
+        g_err = e.what();
+        return FOFSE_ECUDA;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return FOFSE_ERUNTIME;
+    }
+}
+
+unsigned host_threads() {
+    const unsigned n = std::thread::hardware_concurrency();
+    return n ? n : 1;
+}
+
+template <class F>
+void parallel_for(int64_t n, F&& fn) {
+    const int64_t nt = std::min<int64_t>(host_threads(), std::max<int64_t>(1, n / 4));
+    if (nt <= 1) {
+        for (int64_t i = 0; i < n; ++i) fn(i);
+        return;
+    }
+    std::atomic<int64_t> next{0};
+    std::vector<std::thread> pool;
+    for (int64_t t = 0; t < nt; ++t)
+        pool.emplace_back([&] {
+            for (;;) {
+                const int64_t i = next.fetch_add(1);
+                if (i >= n) return;
+                fn(i);
+            }
+        });
+    for (auto& th : pool) th.join();
+}
+
+// ---------------------------------------------------------------------------
+// device buffers
+// ---------------------------------------------------------------------------
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    void* get(size_t bytes) {
+        if (bytes == 0) bytes = 16;
+        if (bytes > cap) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            cap = 0;
+            ck(cudaMalloc(&p, bytes), "cudaMalloc");
+            cap = bytes;
+        }
+        return p;
+    }
+    template <class T>
+    T* as(size_t count) {
+        return static_cast<T*>(get(count * sizeof(T)));
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+}  // namespace
+
+struct fofse_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    std::map<std::string, DevBuf> bufs;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    int64_t launches = 0;
+
+    DevBuf& buf(const std::string& name) { return bufs[name]; }
+    void activate() { ck(cudaSetDevice(device), "cudaSetDevice"); }
+};
+
+namespace {
+
+using fofse::BlockDesc;
+using fofse::Tile;
+
+// ---------------------------------------------------------------------------
+// validation — exact reference messages
+// ---------------------------------------------------------------------------
+struct Cfg {
+    int algorithm;
+    double gamma;
+    int iterations, T;
+    double rho;
+    int S, threads, traces, precision;
+    double tau;
+};
+
+Cfg to_cfg(const fofse_params* p) {
+    if (!p) throw std::invalid_argument("params must not be NULL");
+    Cfg c{p->algorithm,      p->gamma,     p->iterations,    p->transform_size,
+          p->rho_hat,        p->support_width, p->threads,   p->record_traces,
+          p->precision,      p->guard_tau};
+    return c;
+}
+
+// engine_spatial.cpp:8-15 ExtrapolationConfig::validate + pipeline.cpp:34-38
+void validate_config(const Cfg& c) {
+    if (c.algorithm < FOFSE_ALGO_FSE || c.algorithm > FOFSE_ALGO_FOFSE)
+        throw std::invalid_argument("unknown algorithm (expected fse, ofse or fofse)");
+    if (c.iterations < 0) throw std::invalid_argument("config: iterations must be >= 0");
+    if (c.T < 1) throw std::invalid_argument("config: transform size must be >= 1");
+    if (!(c.rho > 0.0) || !(c.rho < 1.0))
+        throw std::invalid_argument("config: rho_hat must lie in (0, 1)");
+    if (c.algorithm == FOFSE_ALGO_FOFSE && (!(c.gamma > 0.0) || c.gamma > 1.0))
+        throw std::invalid_argument("config: gamma must lie in (0, 1]");
+    if (c.S < 1) throw std::invalid_argument("config: support width must be >= 1");
+    if (c.threads < 1) throw std::invalid_argument("config: thread count must be >= 1");
+    if (c.precision != FOFSE_PREC_FP64 && c.precision != FOFSE_PREC_FP32)
+        throw std::invalid_argument("config: precision must be FOFSE_PREC_FP64 or FOFSE_PREC_FP32");
+}
+
+void check_gpu_support(const Cfg& c) {
+    if (c.algorithm == FOFSE_ALGO_OFSE)
+        throw Unsupported("ofse (full-OD compensation) is not part of this build's GPU path");
+    if (!(c.T == 8 || c.T == 16 || c.T == 32 || c.T == 64 || c.T == 128))
+        throw Unsupported("transform_size must be a power of two in [8, 128] on the GPU path");
+}
+
+double effective_gamma(const Cfg& c) { return c.algorithm == FOFSE_ALGO_FSE ? 1.0 : c.gamma; }
+double effective_tau(const Cfg& c) {
+    if (c.precision != FOFSE_PREC_FP32) return 0.0;
+    return c.tau < 0.0 ? 5e-5 : c.tau;
+}
+
+// Per-frame occupancy grid: cell (row/bh, col/bw) -> index of the block whose
+// top-left corner lies in it. Non-overlapping equal-size blocks never share a
+// cell, so each cell holds at most one block.
+struct CellGrid {
+    int gh = 0, gw = 0, bh = 1, bw = 1;
+    std::vector<int32_t> cell;
+    void reset(int W, int H, int bh_, int bw_) {
+        bh = bh_;
+        bw = bw_;
+        gh = H / bh + 2;
+        gw = W / bw + 2;
+        cell.assign(static_cast<size_t>(gh) * gw, -1);
+    }
+    int32_t& at(int cr, int cc) { return cell[static_cast<size_t>(cr) * gw + cc]; }
+};
+
+bool overlap(const fofse_rect& a, const fofse_rect& b) {
+    return a.row < b.row + b.height && b.row < a.row + a.height && a.col < b.col + b.width &&
+           b.col < a.col + a.width;
+}
+
+// pattern.cpp:55-69 validate_pattern (first failing block, lowest partner j),
+// leaving `g` filled with the (valid) pattern.
+void validate_pattern(const fofse_rect* blocks, int64_t n, int bh, int bw, int W, int H,
+                      CellGrid& g) {
+    g.reset(W, H, std::max(bh, 1), std::max(bw, 1));
+    for (int64_t i = 0; i < n; ++i) {
+        const fofse_rect& b = blocks[i];
+        if (b.height != bh || b.width != bw)
+            throw std::invalid_argument("pattern: blocks must share one size");
+        if (b.row < 0 || b.col < 0 || b.height < 1 || b.width < 1 || b.row + b.height > H ||
+            b.col + b.width > W)
+            throw std::invalid_argument("pattern: block " + std::to_string(i) +
+                                        " exceeds image bounds");
+        const int cr = b.row / bh, cc = b.col / bw;
+        int64_t jmin = -1;
+        for (int r = std::max(0, cr - 1); r <= std::min(g.gh - 1, cr + 1); ++r)
+            for (int c = std::max(0, cc - 1); c <= std::min(g.gw - 1, cc + 1); ++c) {
+                const int32_t j = g.at(r, c);
+                if (j >= 0 && overlap(b, blocks[j]) && (jmin < 0 || j < jmin)) jmin = j;
+            }
+        if (jmin >= 0)
+            throw std::invalid_argument("pattern: blocks " + std::to_string(jmin) + " and " +
+                                        std::to_string(i) + " overlap");
+        g.at(cr, cc) = static_cast<int32_t>(i);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// window-mask classes
+// ---------------------------------------------------------------------------
+struct Geometry {
+    int T, bh, bw, S, Lh, Lw;
+};
+
+// grid.cpp:75-92: w = rho^hypot(r - (h-1)/2, c - (w-1)/2) (support mask applied later)
+std::vector<double> full_weight(int Lh, int Lw, double rho) {
+    std::vector<double> w(static_cast<size_t>(Lh) * Lw);
+    const double cr = (Lh - 1) / 2.0, cc = (Lw - 1) / 2.0;
+    for (int r = 0; r < Lh; ++r)
+        for (int c = 0; c < Lw; ++c)
+            w[static_cast<size_t>(r) * Lw + c] = std::pow(rho, std::hypot(r - cr, c - cc));
+    return w;
+}
+
+struct KeyHash {
+    size_t operator()(const std::vector<int32_t>& k) const {
+        uint64_t h = 1469598103934665603ull;
+        for (int32_t v : k) {
+            h ^= static_cast<uint32_t>(v);
+            h *= 1099511628211ull;
+        }
+        return static_cast<size_t>(h);
+    }
+};
+
+struct ClassTable {
+    std::unordered_map<std::vector<int32_t>, int32_t, KeyHash> ids;
+    std::vector<std::vector<uint8_t>> labels;  // per class, Lh*Lw fse::Region bytes
+    int32_t intern(std::vector<int32_t>&& key, const std::function<std::vector<uint8_t>()>& mk) {
+        auto it = ids.find(key);
+        if (it != ids.end()) return it->second;
+        const int32_t id = static_cast<int32_t>(labels.size());
+        labels.push_back(mk());
+        ids.emplace(std::move(key), id);
+        return id;
+    }
+};
+
+// Label mask of a window from its geometry key: pipeline.cpp:95-110 semantics.
+std::vector<uint8_t> labels_from_key(const Geometry& g, const std::vector<int32_t>& key) {
+    std::vector<uint8_t> lab(static_cast<size_t>(g.Lh) * g.Lw, FOFSE_SUPPORT);
+    const int top = key[0], bottom = key[1], left = key[2], right = key[3];
+    for (int r = 0; r < g.Lh; ++r)
+        for (int c = 0; c < g.Lw; ++c) {
+            uint8_t l = FOFSE_SUPPORT;
+            if (r >= g.S && r < g.S + g.bh && c >= g.S && c < g.S + g.bw)
+                l = FOFSE_MISSING;
+            else if (r < top || r >= g.Lh - bottom || c < left || c >= g.Lw - right)
+                l = FOFSE_OUTSIDE;
+            lab[static_cast<size_t>(r) * g.Lw + c] = l;
+        }
+    const int nn = key[4];
+    for (int i = 0; i < nn; ++i) {
+        const int r0 = key[5 + 4 * i], c0 = key[6 + 4 * i], r1 = key[7 + 4 * i], c1 = key[8 + 4 * i];
+        for (int r = r0; r < r1; ++r)
+            for (int c = c0; c < c1; ++c) {
+                uint8_t& l = lab[static_cast<size_t>(r) * g.Lw + c];
+                if (l == FOFSE_SUPPORT) l = FOFSE_OUTSIDE;
+            }
+    }
+    return lab;
+}
+
+bool point_symmetric(const std::vector<uint8_t>& lab, int Lh, int Lw) {
+    for (int r = 0; r < Lh; ++r)
+        for (int c = 0; c < Lw; ++c) {
+            const bool a = lab[static_cast<size_t>(r) * Lw + c] == FOFSE_SUPPORT;
+            const bool b = lab[static_cast<size_t>(Lh - 1 - r) * Lw + (Lw - 1 - c)] == FOFSE_SUPPORT;
+            if (a != b) return false;
+        }
+    return true;
+}
+
+// A batch of lost blocks ready for the device.
+struct Job {
+    Geometry geo;
+    int path_hi = fofse::PATH_F64_STRICT;  // precision choice
+    std::vector<BlockDesc> blocks;          // caller order
+    std::vector<std::vector<uint8_t>> cls_labels;
+    std::vector<double> wfull;
+};
+
+// Image-mode classes: key = (clip top/bottom/left/right, other lost blocks
+// inside the window as relative rects).
+void classify_frames(Job& job, const fofse_rect* blocks, const int64_t* offs, int nframes, int W,
+                     int H, std::vector<CellGrid>& grids) {
+    const Geometry& g = job.geo;
+    const int64_t n = offs[nframes];
+    job.blocks.resize(static_cast<size_t>(n));
+    std::vector<std::vector<int32_t>> keys(static_cast<size_t>(n));
+    std::vector<uint8_t> interior(static_cast<size_t>(n), 0);
+    parallel_for(nframes, [&](int64_t f) {
+        CellGrid& cg = grids[static_cast<size_t>(f)];
+        for (int64_t i = offs[f]; i < offs[f + 1]; ++i) {
+            const fofse_rect& b = blocks[i];
+            const int r0 = b.row - g.S, c0 = b.col - g.S;
+            BlockDesc d;
+            d.frame = static_cast<int32_t>(f);
+            d.row0 = r0;
+            d.col0 = c0;
+            d.cls = -1;
+            job.blocks[static_cast<size_t>(i)] = d;
+            const int top = std::max(0, -r0), left = std::max(0, -c0);
+            const int bottom = std::max(0, r0 + g.Lh - H), right = std::max(0, c0 + g.Lw - W);
+            std::vector<int32_t> nb;
+            const int cr0 = std::max(0, (std::max(r0, 0)) / g.bh - 1);
+            const int cr1 = std::min(cg.gh - 1, (std::min(r0 + g.Lh, H) - 1) / g.bh);
+            const int cc0 = std::max(0, (std::max(c0, 0)) / g.bw - 1);
+            const int cc1 = std::min(cg.gw - 1, (std::min(c0 + g.Lw, W) - 1) / g.bw);
+            for (int cr = cr0; cr <= cr1; ++cr)
+                for (int cc = cc0; cc <= cc1; ++cc) {
+                    const int32_t j = cg.at(cr, cc);
+                    if (j < 0 || j == static_cast<int32_t>(i - offs[f])) continue;
+                    const fofse_rect& o = blocks[offs[f] + j];
+                    const int a0 = std::max(o.row - r0, 0), a1 = std::min(o.row + o.height - r0, g.Lh);
+                    const int b0 = std::max(o.col - c0, 0), b1 = std::min(o.col + o.width - c0, g.Lw);
+                    if (a0 >= a1 || b0 >= b1) continue;
+                    nb.insert(nb.end(), {a0, b0, a1, b1});
+                }
+            if (!top && !left && !bottom && !right && nb.empty()) {
+                interior[static_cast<size_t>(i)] = 1;
+                continue;
+            }
+            // canonical order of the neighbour rects
+            std::vector<std::array<int32_t, 4>> rects;
+            for (size_t k = 0; k < nb.size(); k += 4) rects.push_back({nb[k], nb[k + 1], nb[k + 2], nb[k + 3]});
+            std::sort(rects.begin(), rects.end());
+            std::vector<int32_t> key = {top, bottom, left, right, static_cast<int32_t>(rects.size())};
+            for (auto& r : rects) key.insert(key.end(), r.begin(), r.end());
+            keys[static_cast<size_t>(i)] = std::move(key);
+        }
+    });
+    ClassTable tab;
+    const std::vector<int32_t> interior_key = {0, 0, 0, 0, 0};
+    int32_t interior_id = -1;
+    for (int64_t i = 0; i < n; ++i) {
+        std::vector<int32_t> key = interior[static_cast<size_t>(i)] ? interior_key
+                                                                    : std::move(keys[static_cast<size_t>(i)]);
+        int32_t id;
+        if (interior[static_cast<size_t>(i)] && interior_id >= 0) {
+            id = interior_id;
+        } else {
+            const std::vector<int32_t> kcopy = key;
+            id = tab.intern(std::move(key), [&] { return labels_from_key(g, kcopy); });
+            if (interior[static_cast<size_t>(i)]) interior_id = id;
+        }
+        job.blocks[static_cast<size_t>(i)].cls = id;
+    }
+    job.cls_labels = std::move(tab.labels);
+}
+
+// Window-mode classes: key = the label bytes themselves.
+void classify_windows(Job& job, const uint8_t* labels, int64_t n) {
+    const Geometry& g = job.geo;
+    const size_t L = static_cast<size_t>(g.Lh) * g.Lw;
+    ClassTable tab;
+    job.blocks.resize(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) {
+        const uint8_t* lab = labels + static_cast<size_t>(i) * L;
+        std::vector<int32_t> key(lab, lab + L);
+        const int32_t id = tab.intern(std::move(key), [&] { return std::vector<uint8_t>(lab, lab + L); });
+        job.blocks[static_cast<size_t>(i)] = BlockDesc{static_cast<int32_t>(i), 0, 0, id};
+    }
+    job.cls_labels = std::move(tab.labels);
+}
+
+std::vector<double2> twiddles(int T, int sign) {
+    std::vector<double2> tw(static_cast<size_t>(T));
+    const double two_pi = 6.283185307179586476925286766559;
+    for (int k = 0; k < T; ++k) {
+        const double a = sign * two_pi * k / T;
+        tw[static_cast<size_t>(k)] = make_double2(std::cos(a), std::sin(a));
+    }
+    return tw;
+}
+
+template <class T>
+T* upload(fofse_ctx* ctx, const std::string& name, const T* host, size_t count) {
+    T* d = ctx->buf(name).as<T>(count);
+    if (count)
+        ck(cudaMemcpyAsync(d, host, count * sizeof(T), cudaMemcpyHostToDevice, ctx->stream), "H2D");
+    return d;
+}
+
+// Positions [begin, end) (grouped by class) cut into tiles of NG blocks,
+// one lost block per block-group per tile.
+std::vector<Tile> make_tiles(int64_t begin, int64_t end, const std::vector<BlockDesc>& by_pos, int ng) {
+    std::vector<Tile> tiles;
+    int64_t i = begin;
+    while (i < end) {
+        const int32_t cls = by_pos[static_cast<size_t>(i)].cls;
+        int64_t j = i;
+        while (j < end && by_pos[static_cast<size_t>(j)].cls == cls && j - i < ng) ++j;
+        tiles.push_back(Tile{cls, static_cast<int32_t>(i), static_cast<int32_t>(j - i), 0});
+        i = j;
+    }
+    return tiles;
+}
+
+struct RunOut {
+    double init_ms = 0, iter_ms = 0, total_ms = 0;
+    int64_t reruns = 0, converged = 0;
+};
+
+// Device run of a job. frames_dev: source (and destination) frames on device.
+// synth: SYN_IMAGE (write-back into frames + block_sq) or SYN_WINDOW (models).
+RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int synth,
+               double* d_block_sq, double* d_models, fofse_record* d_trace, int32_t* d_trace_count) {
+    using namespace fofse;
+    const Geometry& g = job.geo;
+    const int T = g.T;
+    const int64_t n = static_cast<int64_t>(job.blocks.size());
+    const int ncls = static_cast<int>(job.cls_labels.size());
+    RunOut out;
+    cudaStream_t st = ctx->stream;
+    for (auto& e : ctx->ev)
+        if (!e) ck(cudaEventCreate(&e), "cudaEventCreate");
+    ck(cudaEventRecord(ctx->ev[0], st), "event");
+
+    // ---- class tables (w on support, exact reference weights) ----
+    const size_t L = static_cast<size_t>(g.Lh) * g.Lw;
+    std::vector<double> wcls(static_cast<size_t>(ncls) * L, 0.0);
+    std::vector<uint8_t> sym(static_cast<size_t>(ncls), 0);
+    for (int c = 0; c < ncls; ++c) {
+        const auto& lab = job.cls_labels[static_cast<size_t>(c)];
+        for (size_t i = 0; i < L; ++i)
+            if (lab[i] == FOFSE_SUPPORT) wcls[static_cast<size_t>(c) * L + i] = job.wfull[i];
+        sym[static_cast<size_t>(c)] = point_symmetric(lab, g.Lh, g.Lw) ? 1 : 0;
+    }
+    const bool fp32 = cfg.precision == FOFSE_PREC_FP32;
+    auto path_of = [&](int cls) {
+        if (!fp32) return (int)PATH_F64_STRICT;
+        return sym[static_cast<size_t>(cls)] ? (int)PATH_F32_REAL : (int)PATH_F32_COMPLEX;
+    };
+
+    const auto twf = twiddles(T, -1), twi = twiddles(T, +1);
+    double2* d_twf = upload(ctx, "twf", twf.data(), twf.size());
+    double2* d_twi = upload(ctx, "twi", twi.data(), twi.size());
+    double* d_wcls = upload(ctx, "wcls", wcls.data(), wcls.size());
+
+    const int seg64 = seg_of(T, PATH_F64_STRICT), seg32 = seg_of(T, PATH_F32_REAL);
+    const int sr64 = T + seg64 + 1, sr32 = T + seg32 + 1;
+    double2* d_wimg64 = ctx->buf("wimg64").as<double2>(static_cast<size_t>(ncls) * T * sr64);
+    float2* d_wimg32 = fp32 ? ctx->buf("wimg32").as<float2>(static_cast<size_t>(ncls) * T * sr32) : nullptr;
+    float* d_vimg32 = fp32 ? ctx->buf("vimg32").as<float>(static_cast<size_t>(ncls) * T * sr32) : nullptr;
+    double* d_w0 = ctx->buf("w0").as<double>(static_cast<size_t>(ncls));
+    {
+        K1Args a{};
+        a.T = T;
+        a.Lh = g.Lh;
+        a.Lw = g.Lw;
+        a.n = ncls;
+        a.wcls = d_wcls;
+        a.mode = K1_CLASS;
+        a.wimg64 = d_wimg64;
+        a.wimg32 = d_wimg32;
+        a.vimg32 = d_vimg32;
+        a.w0 = d_w0;
+        a.twid = d_twf;
+        ck(k1_launch(a, st), "K1 class spectra");
+        ++ctx->launches;
+    }
+
+    // ---- blocks grouped by (path, class); stable within a class ----
+    std::vector<int32_t> ids(static_cast<size_t>(n));
+    std::iota(ids.begin(), ids.end(), 0);
+    std::stable_sort(ids.begin(), ids.end(), [&](int32_t x, int32_t y) {
+        const int px = path_of(job.blocks[x].cls), py = path_of(job.blocks[y].cls);
+        if (px != py) return px < py;
+        return job.blocks[x].cls < job.blocks[y].cls;
+    });
+    std::vector<BlockDesc> sorted(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) sorted[static_cast<size_t>(i)] = job.blocks[ids[static_cast<size_t>(i)]];
+    BlockDesc* d_sorted = upload(ctx, "sorted", sorted.data(), sorted.size());
+    int32_t* d_ids = upload(ctx, "ids", ids.data(), ids.size());
+
+    // residual buffers per position (size of the widest slot type)
+    const BinLayout L64 = BinLayout::make(T, seg64), L32 = BinLayout::make(T, seg32);
+    const size_t slot_bytes = fp32 ? sizeof(float2) * L32.SLOTS : sizeof(double2) * L64.SLOTS;
+    char* d_R = ctx->buf("R").as<char>(static_cast<size_t>(n) * slot_bytes);
+    double* d_e0 = ctx->buf("e0").as<double>(static_cast<size_t>(n));
+    double* d_imax = ctx->buf("imax").as<double>(static_cast<size_t>(n));
+    int32_t* d_flags = fp32 ? ctx->buf("flags").as<int32_t>(static_cast<size_t>(n)) : nullptr;
+    int32_t* d_conv = ctx->buf("conv").as<int32_t>(static_cast<size_t>(n));
+
+    // path ranges over the sorted positions
+    int64_t p0 = 0;
+    struct Range { int path; int64_t begin, end; };
+    std::vector<Range> ranges;
+    while (p0 < n) {
+        const int p = path_of(sorted[static_cast<size_t>(p0)].cls);
+        int64_t p1 = p0;
+        while (p1 < n && path_of(sorted[static_cast<size_t>(p1)].cls) == p) ++p1;
+        ranges.push_back({p, p0, p1});
+        p0 = p1;
+    }
+    // K1 per path range (output packed in that path's precision/rotation)
+    for (const Range& r : ranges) {
+        K1Args a{};
+        a.T = T;
+        a.Lh = g.Lh;
+        a.Lw = g.Lw;
+        a.n = static_cast<int32_t>(r.end - r.begin);
+        a.blocks = d_sorted + r.begin;
+        a.fr = fr;
+        a.wcls = d_wcls;
+        a.mode = K1_PACKED;
+        a.path = r.path;
+        a.seg = seg_of(T, r.path);
+        a.out = d_R + static_cast<size_t>(r.begin) * slot_bytes;
+        // K1 indexes its outputs from 0: shift the packed base per range
+        a.energy = d_e0 + r.begin;
+        a.init_max = d_imax + r.begin;
+        a.twid = d_twf;
+        // packed output stride equals the path's slot size; fp32 ranges use
+        // float2 slots, fp64 double2 — both fit in slot_bytes.
+        if (r.path != PATH_F64_STRICT && slot_bytes != sizeof(float2) * L32.SLOTS)
+            throw std::logic_error("slot size mismatch");
+        ck(k1_launch(a, st), "K1 residual spectra");
+        ++ctx->launches;
+    }
+    ck(cudaEventRecord(ctx->ev[1], st), "event");
+
+    // ---- K2 per path range ----
+    std::vector<Tile> all_tiles;
+    struct Launch { int path; int64_t t0, t1; };
+    std::vector<Launch> launches;
+    for (const Range& r : ranges) {
+        std::vector<Tile> tl = make_tiles(r.begin, r.end, sorted, k2_groups_per_cta(T, r.path));
+        const int64_t t0 = static_cast<int64_t>(all_tiles.size());
+        all_tiles.insert(all_tiles.end(), tl.begin(), tl.end());
+        launches.push_back({r.path, t0, static_cast<int64_t>(all_tiles.size())});
+    }
+    Tile* d_tiles = upload(ctx, "tiles", all_tiles.data(), all_tiles.size());
+    int32_t* d_rec_u = nullptr;
+    double2* d_rec_c = nullptr;
+    if (cfg.iterations > k2_smem_rec_cap(T, 0)) {
+        d_rec_u = ctx->buf("rec_u").as<int32_t>(static_cast<size_t>(n) * cfg.iterations);
+        d_rec_c = ctx->buf("rec_c").as<double2>(static_cast<size_t>(n) * cfg.iterations);
+    }
+    auto base_args = [&]() {
+        K2Args a{};
+        a.T = T;
+        a.Lh = g.Lh;
+        a.Lw = g.Lw;
+        a.iterations = cfg.iterations;
+        a.gamma = effective_gamma(cfg);
+        a.w0 = d_w0;
+        a.synth = synth;
+        a.fr = fr;
+        a.reg_r0 = synth == SYN_IMAGE ? g.S : 0;
+        a.reg_c0 = synth == SYN_IMAGE ? g.S : 0;
+        a.reg_nr = synth == SYN_IMAGE ? g.bh : g.Lh;
+        a.reg_nc = synth == SYN_IMAGE ? g.bw : g.Lw;
+        a.models = d_models;
+        a.block_sq = d_block_sq;
+        a.twid_inv = d_twi;
+        a.rec_u_g = d_rec_u;
+        a.rec_c_g = d_rec_c;
+        a.trace = d_trace;
+        a.trace_count = d_trace_count;
+        return a;
+    };
+    for (const Launch& l : launches) {
+        K2Args a = base_args();
+        a.path = l.path;
+        a.seg = seg_of(T, l.path);
+        a.tau = l.path == PATH_F64_STRICT ? 0.0 : effective_tau(cfg);
+        a.tiles = d_tiles + l.t0;
+        a.order = d_ids;  // position -> caller block id
+        a.blocks = d_sorted;
+        a.rin = d_R;
+        a.wimg = l.path == PATH_F64_STRICT ? (const void*)d_wimg64
+                 : l.path == PATH_F32_COMPLEX ? (const void*)d_wimg32 : (const void*)d_vimg32;
+        a.wimg_stride = static_cast<int64_t>(T) * (l.path == PATH_F64_STRICT ? sr64 : sr32);
+        a.energy0 = d_e0;
+        a.init_energy = d_e0;
+        a.init_max = d_imax;
+        a.conv_out = d_conv;
+        a.flags = d_flags;
+        ck(k2_launch(a, static_cast<int32_t>(l.t1 - l.t0), st), "K2 iterate");
+        ++ctx->launches;
+    }
+
+    // ---- fp32 near-tie guard: re-run flagged blocks in fp64 ----
+    if (fp32 && n > 0) {
+        std::vector<int32_t> flags(static_cast<size_t>(n));
+        ck(cudaMemcpyAsync(flags.data(), d_flags, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st), "D2H flags");
+        ck(cudaStreamSynchronize(st), "sync");
+        std::vector<int32_t> rr;  // caller ids, grouped by class
+        std::vector<BlockDesc> rdesc;
+        for (int64_t i = 0; i < n; ++i) {
+            const int32_t b = ids[static_cast<size_t>(i)];
+            if (flags[static_cast<size_t>(b)]) {
+                rr.push_back(b);
+                rdesc.push_back(job.blocks[static_cast<size_t>(b)]);
+            }
+        }
+        out.reruns = static_cast<int64_t>(rr.size());
+        if (!rr.empty()) {
+            const int64_t m = static_cast<int64_t>(rr.size());
+            BlockDesc* d_rdesc = upload(ctx, "rdesc", rdesc.data(), rdesc.size());
+            int32_t* d_rr = upload(ctx, "rr", rr.data(), rr.size());
+            double2* d_R64 = ctx->buf("R64").as<double2>(static_cast<size_t>(m) * L64.SLOTS);
+            double* d_re0 = ctx->buf("re0").as<double>(static_cast<size_t>(m));
+            double* d_rimax = ctx->buf("rimax").as<double>(static_cast<size_t>(m));
+            K1Args k{};
+            k.T = T;
+            k.Lh = g.Lh;
+            k.Lw = g.Lw;
+            k.n = static_cast<int32_t>(m);
+            k.blocks = d_rdesc;
+            k.fr = fr;
+            k.wcls = d_wcls;
+            k.mode = K1_PACKED;
+            k.path = PATH_F64_STRICT;
+            k.seg = seg64;
+            k.out = d_R64;
+            k.energy = d_re0;
+            k.init_max = d_rimax;
+            k.twid = d_twf;
+            ck(k1_launch(k, st), "K1 rerun spectra");
+            ++ctx->launches;
+            std::vector<Tile> tl = make_tiles(0, m, rdesc, k2_groups_per_cta(T, PATH_F64_STRICT));
+            Tile* d_rt = upload(ctx, "rtiles", tl.data(), tl.size());
+            K2Args a = base_args();
+            a.path = PATH_F64_STRICT;
+            a.seg = seg64;
+            a.tau = 0.0;
+            a.tiles = d_rt;
+            a.order = d_rr;
+            a.blocks = d_rdesc;
+            a.rin = d_R64;
+            a.wimg = d_wimg64;
+            a.wimg_stride = static_cast<int64_t>(T) * sr64;
+            a.energy0 = d_re0;
+            a.init_energy = d_re0;
+            a.init_max = d_rimax;
+            a.conv_out = d_conv;
+            a.flags = nullptr;
+            ck(k2_launch(a, static_cast<int32_t>(tl.size()), st), "K2 rerun");
+            ++ctx->launches;
+        }
+    }
+    ck(cudaEventRecord(ctx->ev[2], st), "event");
+    {
+        std::vector<int32_t> conv(static_cast<size_t>(n));
+        if (n)
+            ck(cudaMemcpyAsync(conv.data(), d_conv, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st), "D2H conv");
+        ck(cudaStreamSynchronize(st), "sync");
+        for (int32_t c : conv) out.converged += c ? 1 : 0;
+    }
+    float ms = 0;
+    ck(cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]), "elapsed");
+    out.init_ms = ms;
+    ck(cudaEventElapsedTime(&ms, ctx->ev[1], ctx->ev[2]), "elapsed");
+    out.iter_ms = ms;
+    out.total_ms = out.init_ms + out.iter_ms;
+    return out;
+}
+
+void fill_report(fofse_report* rep, const RunOut& ro, int64_t n, int64_t ncls, double sq,
+                 int64_t missing, int64_t launches) {
+    if (!rep) return;
+    std::memset(rep, 0, sizeof(*rep));
+    rep->blocks = n;
+    rep->classes = ncls;
+    rep->guard_reruns = ro.reruns;
+    rep->converged_blocks = ro.converged;
+    rep->init_ms = ro.init_ms;
+    rep->iterate_ms = ro.iter_ms;
+    rep->total_ms = ro.total_ms;
+    rep->mean_seconds_per_block = n ? ro.total_ms * 1e-3 / static_cast<double>(n) : 0.0;
+    rep->kernel_launches = launches;
+    // pipeline.cpp:252-260 + grid.cpp:117-120
+    if (n == 0 || sq == 0.0) {
+        rep->psnr_identical = 1;
+        rep->psnr_db = 0.0;
+    } else {
+        const double mse = sq / static_cast<double>(missing);
+        rep->psnr_db = 10.0 * std::log10(255.0 * 255.0 / mse);
+    }
+}
+
+Job make_image_job(const Cfg& cfg, int W, int H, int bh, int bw, const fofse_rect* blocks,
+                   const int64_t* offs, int nframes) {
+    validate_config(cfg);
+    Job job;
+    job.geo = Geometry{cfg.T, bh, bw, cfg.S, bh + 2 * cfg.S, bw + 2 * cfg.S};
+    std::vector<CellGrid> grids(static_cast<size_t>(nframes));
+    // check_pattern_fits (pipeline.cpp:123-132) per frame
+    for (int f = 0; f < nframes; ++f) {
+        const int64_t cnt = offs[f + 1] - offs[f];
+        if (cnt < 0) throw std::invalid_argument("frame_offsets must be non-decreasing");
+        try {
+            validate_pattern(blocks + offs[f], cnt, bh, bw, W, H, grids[static_cast<size_t>(f)]);
+        } catch (const std::invalid_argument& e) {
+            if (nframes == 1) throw;
+            throw std::invalid_argument("frame " + std::to_string(f) + ": " + e.what());
+        }
+    }
+    if (job.geo.Lh > cfg.T || job.geo.Lw > cfg.T)
+        throw std::invalid_argument("conceal: block + support frame exceeds the transform grid");
+    check_gpu_support(cfg);
+    job.wfull = full_weight(job.geo.Lh, job.geo.Lw, cfg.rho);
+    if (offs[nframes] > 0) classify_frames(job, blocks, offs, nframes, W, H, grids);
+    return job;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+int fofse_abi_version(void) { return FOFSE_ABI_VERSION; }
+const char* fofse_last_error(void) { return g_err.c_str(); }
+
+void fofse_params_default(fofse_params* p) {
+    if (!p) return;
+    p->algorithm = FOFSE_ALGO_FOFSE;
+    p->gamma = 0.2;
+    p->iterations = 200;
+    p->transform_size = 64;
+    p->rho_hat = 0.8;
+    p->support_width = 16;
+    p->threads = 1;
+    p->record_traces = 0;
+    p->precision = FOFSE_PREC_FP64;
+    p->guard_tau = -1.0;
+}
+
+int fofse_create(int32_t device, fofse_ctx** out) {
+    return guarded([&] {
+        if (!out) throw std::invalid_argument("out must not be NULL");
+        *out = nullptr;
+        int count = 0;
+        ck(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
+        if (device < 0 || device >= count) throw CudaFailure("no such CUDA device");
+        auto ctx = std::make_unique<fofse_ctx>();
+        ctx->device = device;
+        ctx->activate();
+        ck(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        ctx->own_stream = true;
+        *out = ctx.release();
+    });
+}
+
+void fofse_destroy(fofse_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    for (auto& kv : ctx->bufs) kv.second.release();
+    for (auto& e : ctx->ev)
+        if (e) cudaEventDestroy(e);
+    if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+int fofse_set_stream(fofse_ctx* ctx, void* s) {
+    return guarded([&] {
+        if (!ctx) throw std::invalid_argument("ctx must not be NULL");
+        ctx->activate();
+        if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+        if (s) {
+            ctx->stream = static_cast<cudaStream_t>(s);
+            ctx->own_stream = false;
+        } else {
+            ck(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+            ctx->own_stream = true;
+        }
+    });
+}
+
+int fofse_conceal_f64(fofse_ctx* ctx, const double* image, int32_t width, int32_t height,
+                      const fofse_rect* blocks, int64_t n, int32_t bh, int32_t bw,
+                      const fofse_params* params, double* restored, fofse_record* traces,
+                      int32_t* trace_counts, fofse_report* report) {
+    return guarded([&] {
+        if (!ctx || !image || !restored || (n && !blocks))
+            throw std::invalid_argument("conceal: NULL argument");
+        if (width < 1 || height < 1) throw std::invalid_argument("grid dimensions must be >= 1");
+        const Cfg cfg = to_cfg(params);
+        const int64_t offs[2] = {0, n};
+        Job job = make_image_job(cfg, width, height, bh, bw, blocks, offs, 1);
+        ctx->activate();
+        const size_t npx = static_cast<size_t>(width) * height;
+        double* d_img = ctx->buf("img64").as<double>(npx);
+        ck(cudaMemcpyAsync(d_img, image, npx * sizeof(double), cudaMemcpyHostToDevice, ctx->stream), "H2D image");
+        double* d_sq = ctx->buf("sq").as<double>(static_cast<size_t>(std::max<int64_t>(n, 1)));
+        fofse_record* d_tr = nullptr;
+        int32_t* d_tc = nullptr;
+        if (traces && cfg.iterations > 0) {
+            d_tr = ctx->buf("trace").as<fofse_record>(static_cast<size_t>(n) * cfg.iterations);
+            d_tc = ctx->buf("trace_count").as<int32_t>(static_cast<size_t>(n));
+        }
+        fofse::Frames fr{d_img, d_img, fofse::SRC_F64, width, height, static_cast<int64_t>(npx)};
+        const int64_t l0 = ctx->launches;
+        RunOut ro;
+        if (n > 0) ro = run_job(ctx, job, cfg, fr, fofse::SYN_IMAGE, d_sq, nullptr, d_tr, d_tc);
+        std::vector<double> sq(static_cast<size_t>(n));
+        if (n) ck(cudaMemcpyAsync(sq.data(), d_sq, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream), "D2H sq");
+        ck(cudaMemcpyAsync(restored, d_img, npx * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H image");
+        if (d_tr) {
+            ck(cudaMemcpyAsync(traces, d_tr, sizeof(fofse_record) * n * cfg.iterations, cudaMemcpyDeviceToHost, ctx->stream), "D2H trace");
+            if (trace_counts)
+                ck(cudaMemcpyAsync(trace_counts, d_tc, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, ctx->stream), "D2H trace count");
+        } else if (trace_counts) {
+            std::memset(trace_counts, 0, sizeof(int32_t) * n);
+        }
+        ck(cudaStreamSynchronize(ctx->stream), "sync");
+        double tot = 0.0;
+        for (double v : sq) tot += v;
+        fill_report(report, ro, n, static_cast<int64_t>(job.cls_labels.size()), tot,
+                    n * static_cast<int64_t>(bh) * bw, ctx->launches - l0);
+    });
+}
+
+struct fofse_plan {
+    fofse_ctx* ctx;
+    Cfg cfg;
+    Job job;
+    int32_t n_frames, width, height;
+};
+
+static std::unique_ptr<fofse_plan> make_plan(fofse_ctx* ctx, int32_t n_frames, int32_t width,
+                                             int32_t height, const fofse_rect* blocks,
+                                             const int64_t* offs, int32_t bh, int32_t bw,
+                                             const fofse_params* params) {
+    if (!offs || n_frames < 1) throw std::invalid_argument("plan: bad argument");
+    if (width < 1 || height < 1) throw std::invalid_argument("grid dimensions must be >= 1");
+    if (offs[0] != 0) throw std::invalid_argument("frame_offsets[0] must be 0");
+    if (offs[n_frames] > 0 && !blocks) throw std::invalid_argument("plan: NULL blocks");
+    auto plan = std::make_unique<fofse_plan>();
+    plan->ctx = ctx;
+    plan->cfg = to_cfg(params);
+    plan->job = make_image_job(plan->cfg, width, height, bh, bw, blocks, offs, n_frames);
+    plan->n_frames = n_frames;
+    plan->width = width;
+    plan->height = height;
+    return plan;
+}
+
+int fofse_plan_frames_u8(fofse_ctx* ctx, int32_t n_frames, int32_t width, int32_t height,
+                         const fofse_rect* blocks, const int64_t* offs, int32_t bh, int32_t bw,
+                         const fofse_params* params, fofse_plan** out) {
+    return guarded([&] {
+        if (!out) throw std::invalid_argument("plan: NULL out");
+        *out = nullptr;
+        *out = make_plan(ctx, n_frames, width, height, blocks, offs, bh, bw, params).release();
+    });
+}
+
+void fofse_plan_destroy(fofse_plan* plan) { delete plan; }
+
+static RunOut plan_run(fofse_plan* plan, uint8_t* d_frames, double* d_sq) {
+    fofse_ctx* ctx = plan->ctx;
+    ctx->activate();
+    const int64_t fs = static_cast<int64_t>(plan->width) * plan->height;
+    fofse::Frames fr{d_frames, d_frames, fofse::SRC_U8, plan->width, plan->height, fs};
+    if (plan->job.blocks.empty()) return RunOut{};
+    return run_job(ctx, plan->job, plan->cfg, fr, fofse::SYN_IMAGE, d_sq, nullptr, nullptr, nullptr);
+}
+
+int fofse_validate_conceal(const fofse_params* params, int32_t width, int32_t height,
+                           const fofse_rect* blocks, int64_t n, int32_t bh, int32_t bw) {
+    return guarded([&] {
+        if (n && !blocks) throw std::invalid_argument("validate: NULL blocks");
+        if (width < 1 || height < 1) throw std::invalid_argument("grid dimensions must be >= 1");
+        const Cfg cfg = to_cfg(params);
+        const int64_t offs[2] = {0, n};
+        validate_config(cfg);
+        CellGrid g;
+        validate_pattern(blocks, n, bh, bw, width, height, g);
+        if (bh + 2 * cfg.S > cfg.T || bw + 2 * cfg.S > cfg.T)
+            throw std::invalid_argument("conceal: block + support frame exceeds the transform grid");
+        (void)offs;
+    });
+}
+
+int fofse_plan_info(const fofse_plan* plan, int64_t* n_blocks, int64_t* n_classes,
+                    int64_t* n_sym) {
+    return guarded([&] {
+        if (!plan) throw std::invalid_argument("plan_info: NULL plan");
+        const Job& j = plan->job;
+        if (n_blocks) *n_blocks = static_cast<int64_t>(j.blocks.size());
+        if (n_classes) *n_classes = static_cast<int64_t>(j.cls_labels.size());
+        if (n_sym) {
+            int64_t s = 0;
+            for (const auto& lab : j.cls_labels) s += point_symmetric(lab, j.geo.Lh, j.geo.Lw) ? 1 : 0;
+            *n_sym = s;
+        }
+    });
+}
+
+int fofse_plan_block_labels(const fofse_plan* plan, int64_t i, uint8_t* labels) {
+    return guarded([&] {
+        if (!plan || !labels) throw std::invalid_argument("plan_block_labels: NULL argument");
+        const Job& j = plan->job;
+        if (i < 0 || i >= static_cast<int64_t>(j.blocks.size()))
+            throw std::invalid_argument("plan_block_labels: block index out of range");
+        const auto& lab = j.cls_labels[static_cast<size_t>(j.blocks[static_cast<size_t>(i)].cls)];
+        std::memcpy(labels, lab.data(), lab.size());
+    });
+}
+
+int fofse_plan_execute_device(fofse_plan* plan, uint8_t* d_frames, double* d_block_sq,
+                              fofse_report* report) {
+    return guarded([&] {
+        if (!plan || !d_frames) throw std::invalid_argument("execute: NULL argument");
+        if (!plan->ctx) throw std::invalid_argument("execute: plan was created without a context");
+        fofse_ctx* ctx = plan->ctx;
+        const int64_t n = static_cast<int64_t>(plan->job.blocks.size());
+        double* d_sq = d_block_sq ? d_block_sq : ctx->buf("sq").as<double>(static_cast<size_t>(std::max<int64_t>(n, 1)));
+        const int64_t l0 = ctx->launches;
+        RunOut ro = plan_run(plan, d_frames, d_sq);
+        double tot = 0.0;
+        if (report && n) {
+            std::vector<double> sq(static_cast<size_t>(n));
+            ck(cudaMemcpyAsync(sq.data(), d_sq, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream), "D2H sq");
+            ck(cudaStreamSynchronize(ctx->stream), "sync");
+            for (double v : sq) tot += v;
+        }
+        fill_report(report, ro, n, static_cast<int64_t>(plan->job.cls_labels.size()), tot,
+                    n * static_cast<int64_t>(plan->job.geo.bh) * plan->job.geo.bw, ctx->launches - l0);
+    });
+}
+
+int fofse_conceal_frames_u8(fofse_ctx* ctx, const uint8_t* frames, int32_t n_frames, int32_t width,
+                            int32_t height, const fofse_rect* blocks, const int64_t* offs,
+                            int32_t bh, int32_t bw, const fofse_params* params, uint8_t* restored,
+                            double* block_sq, fofse_report* report) {
+    return guarded([&] {
+        if (!ctx || !frames || !restored || !offs || n_frames < 1)
+            throw std::invalid_argument("conceal_frames: bad argument");
+        std::unique_ptr<fofse_plan> hold =
+            make_plan(ctx, n_frames, width, height, blocks, offs, bh, bw, params);
+        fofse_plan* plan = hold.get();
+        ctx->activate();
+        const size_t bytes = static_cast<size_t>(n_frames) * width * height;
+        uint8_t* d_fr = ctx->buf("frames_u8").as<uint8_t>(bytes);
+        ck(cudaMemcpyAsync(d_fr, frames, bytes, cudaMemcpyHostToDevice, ctx->stream), "H2D frames");
+        const int64_t n = static_cast<int64_t>(plan->job.blocks.size());
+        double* d_sq = ctx->buf("sq").as<double>(static_cast<size_t>(std::max<int64_t>(n, 1)));
+        const int64_t l0 = ctx->launches;
+        RunOut ro = plan_run(plan, d_fr, d_sq);
+        std::vector<double> sq(static_cast<size_t>(n));
+        if (n) ck(cudaMemcpyAsync(sq.data(), d_sq, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream), "D2H sq");
+        ck(cudaMemcpyAsync(restored, d_fr, bytes, cudaMemcpyDeviceToHost, ctx->stream), "D2H frames");
+        ck(cudaStreamSynchronize(ctx->stream), "sync");
+        double tot = 0.0;
+        for (double v : sq) tot += v;
+        if (block_sq && n) std::memcpy(block_sq, sq.data(), sizeof(double) * n);
+        fill_report(report, ro, n, static_cast<int64_t>(plan->job.cls_labels.size()), tot,
+                    n * static_cast<int64_t>(bh) * bw, ctx->launches - l0);
+    });
+}
+
+int fofse_extrapolate_windows(fofse_ctx* ctx, const double* windows, const uint8_t* labels,
+                              int64_t n, int32_t wh, int32_t ww, const fofse_params* params,
+                              double* models, fofse_record* traces, int32_t* trace_counts) {
+    return guarded([&] {
+        if (!ctx || (n && (!windows || !labels || !models)))
+            throw std::invalid_argument("extrapolate_windows: NULL argument");
+        const Cfg cfg = to_cfg(params);
+        validate_config(cfg);
+        if (wh < 1 || ww < 1) throw std::invalid_argument("window dimensions must be >= 1");
+        // init_spectra (engine_spectral.cpp:153-154)
+        if (wh > cfg.T || ww > cfg.T)
+            throw std::invalid_argument("init_spectra: window exceeds the transform grid");
+        check_gpu_support(cfg);
+        Job job;
+        job.geo = Geometry{cfg.T, 0, 0, 0, wh, ww};
+        job.wfull = full_weight(wh, ww, cfg.rho);
+        classify_windows(job, labels, n);
+        ctx->activate();
+        const size_t L = static_cast<size_t>(wh) * ww;
+        double* d_win = upload(ctx, "windows", windows, static_cast<size_t>(n) * L);
+        double* d_mod = ctx->buf("models").as<double>(std::max<size_t>(static_cast<size_t>(n) * L, 1));
+        fofse_record* d_tr = nullptr;
+        int32_t* d_tc = nullptr;
+        if (traces && cfg.iterations > 0) {
+            d_tr = ctx->buf("trace").as<fofse_record>(static_cast<size_t>(n) * cfg.iterations);
+            d_tc = ctx->buf("trace_count").as<int32_t>(static_cast<size_t>(n));
+        }
+        fofse::Frames fr{d_win, d_win, fofse::SRC_F64, ww, wh, static_cast<int64_t>(L)};
+        if (n > 0) {
+            // models default to zero for windows that never iterate
+            ck(cudaMemsetAsync(d_mod, 0, sizeof(double) * n * L, ctx->stream), "memset");
+            run_job(ctx, job, cfg, fr, fofse::SYN_WINDOW, nullptr, d_mod, d_tr, d_tc);
+            ck(cudaMemcpyAsync(models, d_mod, sizeof(double) * n * L, cudaMemcpyDeviceToHost, ctx->stream), "D2H models");
+        }
+        if (d_tr) {
+            ck(cudaMemcpyAsync(traces, d_tr, sizeof(fofse_record) * n * cfg.iterations, cudaMemcpyDeviceToHost, ctx->stream), "D2H trace");
+            if (trace_counts)
+                ck(cudaMemcpyAsync(trace_counts, d_tc, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, ctx->stream), "D2H tc");
+        } else if (trace_counts && n) {
+            std::memset(trace_counts, 0, sizeof(int32_t) * n);
+        }
+        ck(cudaStreamSynchronize(ctx->stream), "sync");
+    });
+}
+
+// ---------------------------------------------------------------------------
+// engine level
+// ---------------------------------------------------------------------------
+int fofse_spectral_init(fofse_ctx* ctx, const double* f, const uint8_t* labels,
+                        const double* weight, int64_t n, int32_t h, int32_t w, int32_t t,
+                        double* rw, double* wspec, double* w0, double* energy, double* imax) {
+    return guarded([&] {
+        using namespace fofse;
+        if (!ctx || (n && (!f || !labels || !weight || !rw || !wspec || !w0 || !energy || !imax)))
+            throw std::invalid_argument("spectral_init: NULL argument");
+        if (h > t || w > t) throw std::invalid_argument("init_spectra: window exceeds the transform grid");
+        Cfg c{};
+        c.T = t;
+        c.algorithm = FOFSE_ALGO_FOFSE;
+        check_gpu_support(c);
+        ctx->activate();
+        const size_t L = static_cast<size_t>(h) * w;
+        // per-spectrum class = its own weight field masked by SUPPORT
+        // (engine_spectral.cpp:166-170: fw = w f on support, wg = w where w != 0)
+        std::vector<double> wg(weight, weight + static_cast<size_t>(n) * L);
+        // f masked: K1 computes w*f only where the class weight is non-zero;
+        // off-support samples of f are zeroed so w*f matches (support ? f : 0).
+        std::vector<double> fm(static_cast<size_t>(n) * L);
+        for (size_t q = 0; q < fm.size(); ++q) fm[q] = labels[q] == FOFSE_SUPPORT ? f[q] : 0.0;
+        std::vector<BlockDesc> bd(static_cast<size_t>(n));
+        for (int64_t i = 0; i < n; ++i) bd[static_cast<size_t>(i)] = BlockDesc{static_cast<int32_t>(i), 0, 0, static_cast<int32_t>(i)};
+        const auto twf = twiddles(t, -1);
+        double2* d_tw = upload(ctx, "twf", twf.data(), twf.size());
+        double* d_f = upload(ctx, "si_f", fm.data(), fm.size());
+        double* d_wg = upload(ctx, "si_wg", wg.data(), wg.size());
+        BlockDesc* d_bd = upload(ctx, "si_bd", bd.data(), bd.size());
+        const size_t tt = static_cast<size_t>(t) * t;
+        double2* d_rw = ctx->buf("si_rw").as<double2>(std::max<size_t>(static_cast<size_t>(n) * tt, 1));
+        double2* d_ws = ctx->buf("si_ws").as<double2>(std::max<size_t>(static_cast<size_t>(n) * tt, 1));
+        double* d_e = ctx->buf("si_e").as<double>(static_cast<size_t>(std::max<int64_t>(n, 1)));
+        double* d_m = ctx->buf("si_m").as<double>(static_cast<size_t>(std::max<int64_t>(n, 1)));
+        double* d_e2 = ctx->buf("si_e2").as<double>(static_cast<size_t>(std::max<int64_t>(n, 1)));
+        double* d_m2 = ctx->buf("si_m2").as<double>(static_cast<size_t>(std::max<int64_t>(n, 1)));
+        K1Args a{};
+        a.T = t;
+        a.Lh = h;
+        a.Lw = w;
+        a.n = static_cast<int32_t>(n);
+        a.blocks = d_bd;
+        a.fr = Frames{d_f, nullptr, SRC_F64, w, h, static_cast<int64_t>(L)};
+        a.wcls = d_wg;
+        a.mode = K1_FULL;
+        a.out = d_rw;
+        a.energy = d_e;
+        a.init_max = d_m;
+        a.twid = d_tw;
+        ck(k1_launch(a, ctx->stream), "K1 init rw");
+        // W = DFT(w): same kernel with f == 1 on every sample of w
+        std::vector<double> ones(static_cast<size_t>(n) * L, 1.0);
+        double* d_one = upload(ctx, "si_one", ones.data(), ones.size());
+        a.fr.src = d_one;
+        a.out = d_ws;
+        a.energy = d_e2;
+        a.init_max = d_m2;
+        ck(k1_launch(a, ctx->stream), "K1 init W");
+        ck(cudaMemcpyAsync(rw, d_rw, sizeof(double2) * n * tt, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        ck(cudaMemcpyAsync(wspec, d_ws, sizeof(double2) * n * tt, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        ck(cudaMemcpyAsync(energy, d_e, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        ck(cudaMemcpyAsync(imax, d_m, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        ck(cudaStreamSynchronize(ctx->stream), "sync");
+        for (int64_t i = 0; i < n; ++i) w0[i] = wspec[2 * static_cast<size_t>(i) * tt];
+    });
+}
+
+int fofse_spectral_iterate(fofse_ctx* ctx, int32_t t, int64_t n, int32_t wh, int32_t ww,
+                           double* rw, const double* wspec, double* g, const double* w0,
+                           double* energy, const double* e_init, const double* imax, int32_t* nu,
+                           int32_t* conv, double gamma, int32_t iterations, int32_t precision,
+                           fofse_record* traces, int32_t* trace_counts) {
+    return guarded([&] {
+        using namespace fofse;
+        if (!ctx || (n && (!rw || !wspec || !g || !w0 || !energy || !e_init || !imax || !nu || !conv)))
+            throw std::invalid_argument("spectral_iterate: NULL argument");
+        if (iterations < 0) throw std::invalid_argument("fast_iterate: iterations must be >= 0");
+        if (!(gamma > 0.0) || gamma > 1.0) throw std::invalid_argument("fast_iterate: gamma must lie in (0, 1]");
+        Cfg c{};
+        c.T = t;
+        c.algorithm = FOFSE_ALGO_FOFSE;
+        check_gpu_support(c);
+        if (precision != FOFSE_PREC_FP64 && precision != FOFSE_PREC_FP32)
+            throw std::invalid_argument("precision must be FOFSE_PREC_FP64 or FOFSE_PREC_FP32");
+        ctx->activate();
+        cudaStream_t st = ctx->stream;
+        const int path = precision == FOFSE_PREC_FP64 ? PATH_F64_STRICT : PATH_F32_COMPLEX;
+        const int seg = seg_of(t, path);
+        const BinLayout Lb = BinLayout::make(t, seg);
+        const int sr = t + seg + 1;
+        const size_t tt = static_cast<size_t>(t) * t;
+        // pack residuals (canonical half) and W images per spectrum
+        std::vector<double2> R64;
+        std::vector<float2> R32;
+        std::vector<double2> W64;
+        std::vector<float2> W32;
+        if (path == PATH_F64_STRICT) {
+            R64.assign(static_cast<size_t>(n) * Lb.SLOTS, make_double2(0, 0));
+            W64.resize(static_cast<size_t>(n) * t * sr);
+        } else {
+            R32.assign(static_cast<size_t>(n) * Lb.SLOTS, make_float2(0, 0));
+            W32.resize(static_cast<size_t>(n) * t * sr);
+        }
+        for (int64_t i = 0; i < n; ++i) {
+            const double* r = rw + 2 * static_cast<size_t>(i) * tt;
+            const double* wsp = wspec + 2 * static_cast<size_t>(i) * tt;
+            for (int s = 0; s < Lb.SLOTS; ++s) {
+                int k1, k2;
+                if (!Lb.slot_bin(s / Lb.NT, s % Lb.NT, &k1, &k2)) continue;
+                const size_t q = static_cast<size_t>(k1) * t + k2;
+                if (path == PATH_F64_STRICT)
+                    R64[static_cast<size_t>(i) * Lb.SLOTS + s] = make_double2(r[2 * q], r[2 * q + 1]);
+                else
+                    R32[static_cast<size_t>(i) * Lb.SLOTS + s] = make_float2((float)r[2 * q], (float)r[2 * q + 1]);
+            }
+            for (int k1 = 0; k1 < t; ++k1)
+                for (int col = 0; col < sr; ++col) {
+                    const size_t q = static_cast<size_t>(k1) * t + col % t;
+                    const size_t o = static_cast<size_t>(i) * t * sr + static_cast<size_t>(k1) * sr + col;
+                    if (path == PATH_F64_STRICT)
+                        W64[o] = make_double2(wsp[2 * q], wsp[2 * q + 1]);
+                    else
+                        W32[o] = make_float2((float)wsp[2 * q], (float)wsp[2 * q + 1]);
+                }
+        }
+        void* d_R = path == PATH_F64_STRICT ? (void*)upload(ctx, "it_R64", R64.data(), R64.size())
+                                            : (void*)upload(ctx, "it_R32", R32.data(), R32.size());
+        void* d_W = path == PATH_F64_STRICT ? (void*)upload(ctx, "it_W64", W64.data(), W64.size())
+                                            : (void*)upload(ctx, "it_W32", W32.data(), W32.size());
+        double2* d_g = upload(ctx, "it_g", reinterpret_cast<const double2*>(g), static_cast<size_t>(n) * tt);
+        double* d_w0 = upload(ctx, "it_w0", w0, static_cast<size_t>(n));
+        double* d_e = upload(ctx, "it_e", energy, static_cast<size_t>(n));
+        double* d_ei = upload(ctx, "it_ei", e_init, static_cast<size_t>(n));
+        double* d_im = upload(ctx, "it_im", imax, static_cast<size_t>(n));
+        int32_t* d_nu = upload(ctx, "it_nu", nu, static_cast<size_t>(n));
+        int32_t* d_cv = upload(ctx, "it_cv", conv, static_cast<size_t>(n));
+        double* d_eo = ctx->buf("it_eo").as<double>(static_cast<size_t>(std::max<int64_t>(n, 1)));
+        int32_t* d_nuo = ctx->buf("it_nuo").as<int32_t>(static_cast<size_t>(std::max<int64_t>(n, 1)));
+        int32_t* d_cvo = ctx->buf("it_cvo").as<int32_t>(static_cast<size_t>(std::max<int64_t>(n, 1)));
+        const size_t rbytes = (path == PATH_F64_STRICT ? sizeof(double2) : sizeof(float2)) * Lb.SLOTS;
+        char* d_Ro = ctx->buf("it_Ro").as<char>(std::max<size_t>(static_cast<size_t>(n) * rbytes, 1));
+        std::vector<BlockDesc> bd(static_cast<size_t>(n));
+        std::vector<Tile> tiles(static_cast<size_t>(n));
+        std::vector<int32_t> order(static_cast<size_t>(n));
+        for (int64_t i = 0; i < n; ++i) {
+            bd[static_cast<size_t>(i)] = BlockDesc{static_cast<int32_t>(i), 0, 0, static_cast<int32_t>(i)};
+            tiles[static_cast<size_t>(i)] = Tile{static_cast<int32_t>(i), static_cast<int32_t>(i), 1, 0};
+            order[static_cast<size_t>(i)] = static_cast<int32_t>(i);
+        }
+        BlockDesc* d_bd = upload(ctx, "it_bd", bd.data(), bd.size());
+        Tile* d_tl = upload(ctx, "it_tl", tiles.data(), tiles.size());
+        int32_t* d_or = upload(ctx, "it_or", order.data(), order.size());
+        fofse_record* d_tr = nullptr;
+        int32_t* d_tc = nullptr;
+        if (traces && iterations > 0) {
+            d_tr = ctx->buf("trace").as<fofse_record>(static_cast<size_t>(n) * iterations);
+            d_tc = ctx->buf("trace_count").as<int32_t>(static_cast<size_t>(n));
+        }
+        int32_t* d_rec_u = nullptr;
+        double2* d_rec_c = nullptr;
+        if (iterations > k2_smem_rec_cap(t, path)) {
+            d_rec_u = ctx->buf("rec_u").as<int32_t>(static_cast<size_t>(n) * iterations);
+            d_rec_c = ctx->buf("rec_c").as<double2>(static_cast<size_t>(n) * iterations);
+        }
+        const auto twi = twiddles(t, +1);
+        double2* d_twi = upload(ctx, "twi", twi.data(), twi.size());
+        K2Args a{};
+        a.T = t;
+        a.Lh = wh;
+        a.Lw = ww;
+        a.path = path;
+        a.seg = seg;
+        a.iterations = iterations;
+        a.gamma = gamma;
+        a.tau = 0.0;
+        a.tiles = d_tl;
+        a.order = d_or;
+        a.blocks = d_bd;
+        a.rin = d_R;
+        a.rout = d_Ro;
+        a.wimg = d_W;
+        a.wimg_stride = static_cast<int64_t>(t) * sr;
+        a.w0 = d_w0;
+        a.energy0 = d_e;
+        a.init_energy = d_ei;
+        a.init_max = d_im;
+        a.nu0 = d_nu;
+        a.conv0 = d_cv;
+        a.energy_out = d_eo;
+        a.nu_out = d_nuo;
+        a.conv_out = d_cvo;
+        a.trace = d_tr;
+        a.trace_count = d_tc;
+        a.gspec = d_g;
+        a.synth = SYN_NONE;
+        a.twid_inv = d_twi;
+        a.rec_u_g = d_rec_u;
+        a.rec_c_g = d_rec_c;
+        if (n) ck(k2_launch(a, static_cast<int32_t>(n), st), "K2 spectral iterate");
+        std::vector<char> Ro(static_cast<size_t>(n) * rbytes);
+        if (n) {
+            ck(cudaMemcpyAsync(Ro.data(), d_Ro, Ro.size(), cudaMemcpyDeviceToHost, st), "D2H");
+            ck(cudaMemcpyAsync(g, d_g, sizeof(double2) * n * tt, cudaMemcpyDeviceToHost, st), "D2H");
+            ck(cudaMemcpyAsync(energy, d_eo, sizeof(double) * n, cudaMemcpyDeviceToHost, st), "D2H");
+            ck(cudaMemcpyAsync(nu, d_nuo, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st), "D2H");
+            ck(cudaMemcpyAsync(conv, d_cvo, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st), "D2H");
+        }
+        if (d_tr) {
+            ck(cudaMemcpyAsync(traces, d_tr, sizeof(fofse_record) * n * iterations, cudaMemcpyDeviceToHost, st), "D2H");
+            if (trace_counts) ck(cudaMemcpyAsync(trace_counts, d_tc, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st), "D2H");
+        } else if (trace_counts && n) {
+            std::memset(trace_counts, 0, sizeof(int32_t) * n);
+        }
+        ck(cudaStreamSynchronize(st), "sync");
+        // unpack: canonical bins from the registers' final state; the rest are
+        // their conjugate partners (never read by the reference, engine_spectral.cpp:25-28)
+        for (int64_t i = 0; i < n; ++i) {
+            double* r = rw + 2 * static_cast<size_t>(i) * tt;
+            for (int s = 0; s < Lb.SLOTS; ++s) {
+                int k1, k2;
+                if (!Lb.slot_bin(s / Lb.NT, s % Lb.NT, &k1, &k2)) continue;
+                double vr, vi;
+                if (path == PATH_F64_STRICT) {
+                    const double2 v = reinterpret_cast<const double2*>(Ro.data())[static_cast<size_t>(i) * Lb.SLOTS + s];
+                    vr = v.x;
+                    vi = v.y;
+                } else {
+                    const float2 v = reinterpret_cast<const float2*>(Ro.data())[static_cast<size_t>(i) * Lb.SLOTS + s];
+                    vr = v.x;
+                    vi = v.y;
+                }
+                const size_t q = static_cast<size_t>(k1) * t + k2;
+                r[2 * q] = vr;
+                r[2 * q + 1] = vi;
+                const size_t qc = static_cast<size_t>((t - k1) % t) * t + (t - k2) % t;
+                if (qc != q) {
+                    r[2 * qc] = vr;
+                    r[2 * qc + 1] = -vi;
+                }
+            }
+        }
+    });
+}
+
+int fofse_spectral_synthesize(fofse_ctx* ctx, int32_t t, int64_t n, const double* g, int32_t h,
+                              int32_t w, double* models, double* max_imag) {
+    return guarded([&] {
+        using namespace fofse;
+        if (!ctx || (n && (!g || !models))) throw std::invalid_argument("spectral_synthesize: NULL argument");
+        Cfg c{};
+        c.T = t;
+        c.algorithm = FOFSE_ALGO_FOFSE;
+        check_gpu_support(c);
+        if (h > t || w > t) throw std::invalid_argument("synthesize: window exceeds the transform grid");
+        ctx->activate();
+        const size_t tt = static_cast<size_t>(t) * t;
+        double2* d = upload(ctx, "sy_g", reinterpret_cast<const double2*>(g), static_cast<size_t>(n) * tt);
+        const auto twf = twiddles(t, -1);
+        double2* d_tw = upload(ctx, "twf", twf.data(), twf.size());
+        if (n) ck(fft2d_launch(d, n, t, +1, d_tw, ctx->stream), "IFFT");
+        std::vector<double2> full(static_cast<size_t>(n) * tt);
+        if (n) ck(cudaMemcpyAsync(full.data(), d, sizeof(double2) * full.size(), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        ck(cudaStreamSynchronize(ctx->stream), "sync");
+        // basis.cpp:102-109 scale by 1/T^2, report max |Im|; crop (engine_spectral.cpp:204-206)
+        const double scale = 1.0 / (static_cast<double>(t) * t);
+        for (int64_t i = 0; i < n; ++i) {
+            double worst = 0.0;
+            const double2* f = full.data() + static_cast<size_t>(i) * tt;
+            for (size_t q = 0; q < tt; ++q) worst = std::max(worst, std::abs(f[q].y * scale));
+            if (max_imag) max_imag[i] = worst;
+            if (worst > 1e-9)
+                throw std::runtime_error("synthesize_model: conjugate symmetry violated");
+            for (int r = 0; r < h; ++r)
+                for (int cc = 0; cc < w; ++cc)
+                    models[static_cast<size_t>(i) * h * w + static_cast<size_t>(r) * w + cc] =
+                        f[static_cast<size_t>(r) * t + cc].x * scale;
+        }
+    });
+}
+
+}  // extern "C"

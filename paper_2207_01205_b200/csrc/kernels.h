@@ -1,0 +1,125 @@
+// kernels.h — host-visible launch interface of the sm_100a kernels.
+//
+//   K1  fofse_k1_spectra   : window gather (u8/f64 frames or window stacks),
+//                            w*f weighting, batched real-input 2-D FFT (fp64),
+//                            outputs the packed canonical residual spectrum
+//                            for K2, full spectra, or the class W images.
+//   K2  fofse_k2_iterate   : the FOFSE loop — per block-group argmax over the
+//                            register-resident canonical spectrum + frequency
+//                            domain residual update against W in shared
+//                            memory, fused sparse synthesis + clamp + write-back.
+//   KL  fofse_lines_fft    : batched 1-D FFT of strided lines in global memory
+//                            (engine-level synthesize of arbitrary spectra).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/fofse.h"
+
+namespace fofse {
+
+// K2 arithmetic paths.
+enum IterPath : int {
+    PATH_F64_STRICT = 0,  // complex W, reference op order, no FMA
+    PATH_F32_COMPLEX = 1, // complex W (asymmetric window masks)
+    PATH_F32_REAL = 2,    // point-symmetric masks: rotated frame, real V
+};
+
+enum SrcType : int { SRC_U8 = 0, SRC_F64 = 1 };
+
+struct BlockDesc {
+    int32_t frame;       // frame (or window) index into the source
+    int32_t row0, col0;  // window origin in that frame
+    int32_t cls;         // window-mask class
+};
+
+struct Tile {
+    int32_t cls;
+    int32_t begin;  // into the block order array
+    int32_t count;
+    int32_t pad;
+};
+
+struct Frames {
+    const void* src;      // u8 or f64 frames (or window stack)
+    void* dst;            // same type; may alias src
+    int32_t type;         // SrcType
+    int32_t width, height;
+    int64_t frame_stride; // elements
+};
+
+struct K1Args {
+    int32_t T, Lh, Lw;
+    int32_t n;                 // blocks (or classes in class mode)
+    const BlockDesc* blocks;   // block mode; NULL in class mode
+    Frames fr;
+    const double* wcls;        // [ncls][Lh*Lw] class weights (0 off support)
+    int32_t mode;              // K1_PACKED, K1_FULL, K1_CLASS
+    int32_t path;              // IterPath for K1_PACKED (precision + rotation)
+    int32_t seg;               // layout SEG of the K2 path
+    void* out;                 // packed R / full spectrum (double2) / W images
+    double* energy;            // per block sum w f^2 (packed/full modes)
+    double* init_max;          // per block max |R| (packed/full modes)
+    // class mode outputs
+    double2* wimg64;           // [ncls][T*SR64] complex fp64 image (SEG of fp64)
+    float2* wimg32;            // [ncls][T*SR32] complex fp32 image
+    float* vimg32;             // [ncls][T*SR32] rotated real image
+    double* w0;                // [ncls]
+    const double2* twid;       // e^{-j 2 pi k / T}, k < T
+};
+enum { K1_PACKED = 0, K1_FULL = 1, K1_CLASS = 2 };
+
+struct K2Args {
+    int32_t T, Lh, Lw, path, seg;
+    int32_t iterations;
+    double gamma;
+    double tau;                 // guard on |R|^2 relative gap (fp32 paths)
+    // Inputs are indexed by POSITION (tile.begin + i): blocks, rin, rout,
+    // energy0, init_energy, init_max, nu0, conv0. Outputs are indexed by the
+    // block id order[position]: everything else.
+    const Tile* tiles;
+    const int32_t* order;
+    const BlockDesc* blocks;
+    const void* rin;            // packed residual (Real2 per slot)
+    void* rout;                 // optional: packed residual written back
+    const void* wimg;           // W images of the path's precision
+    int64_t wimg_stride;        // elements per class
+    const double* w0;           // per class
+    const double* energy0;      // per block (weighted_energy at entry)
+    const double* init_energy;  // per block
+    const double* init_max;     // per block
+    const int32_t* nu0;         // per block (NULL = 0)
+    const int32_t* conv0;       // per block (NULL = 0)
+    double* energy_out;         // per block (optional)
+    int32_t* nu_out;            // per block (optional)
+    int32_t* conv_out;          // per block (optional)
+    int32_t* flags;             // per block guard flag (fp32 paths, optional)
+    fofse_record* trace;        // [block][iterations] (optional)
+    int32_t* trace_count;       // per block (optional)
+    double2* gspec;             // [block][T*T] model spectrum accumulate (optional)
+    // synthesis
+    int32_t synth;              // SYN_NONE / SYN_IMAGE / SYN_WINDOW
+    Frames fr;                  // SYN_IMAGE: frames (reads original, writes restored)
+    int32_t reg_r0, reg_c0, reg_nr, reg_nc;  // region in window coordinates
+    double* models;             // SYN_WINDOW: [block][Lh*Lw]
+    double* block_sq;           // SYN_IMAGE: per block squared error (optional)
+    const double2* twid_inv;    // e^{+j 2 pi k / T}
+    int32_t* rec_u_g;           // global record scratch [block][iterations] when
+    double2* rec_c_g;           //   iterations exceed the shared-memory capacity
+};
+enum { SYN_NONE = 0, SYN_IMAGE = 1, SYN_WINDOW = 2 };
+
+// Host launchers (return cudaError_t).
+int k1_launch(const K1Args& a, cudaStream_t s);
+int k2_launch(const K2Args& a, int32_t ntiles, cudaStream_t s);
+// Batched in-place complex fp64 2-D transform of n T x T spectra (dir -1/+1).
+int fft2d_launch(double2* data, int64_t n, int32_t T, int32_t dir, const double2* twid_fwd,
+                 cudaStream_t s);
+
+// Row stride of W images and the SEG used by a path (same on host/device).
+int seg_of(int T, int path);
+int k2_groups_per_cta(int T, int path);
+int k2_smem_rec_cap(int T, int path);
+
+}  // namespace fofse

@@ -1,0 +1,299 @@
+"""GPU parity tests: the CUDA path (through the C ABI) vs the oracle.
+
+Bars (BASELINE.json north_star):
+  * fp64: identical selected-basis sequence, pixels within 1e-9 absolute;
+    the iteration kernel fed the oracle's own spectra is bit-exact.
+  * fp32 fast mode: max |pixel error| <= 0.5, PSNR within 0.05 dB.
+"""
+import numpy as np
+import pytest
+
+import paper_2207_01205_b200 as P
+from paper_2207_01205_b200 import workloads as WL
+from helpers import MISSING, OUTSIDE, SUPPORT, block_mask, random_grid, random_mask, smooth_test_image
+
+pytestmark = pytest.mark.gpu
+
+FP64_PX_TOL = 1e-9
+FP32_PX_TOL = 0.5
+FP32_PSNR_TOL = 0.05
+
+
+def _oracle_spectrum(orc, rng, t, h, w, masked=True):
+    f = random_grid(rng, h, w) * 100.0
+    m = random_mask(rng, h, w) if masked else np.zeros((h, w), np.uint8)
+    wt = orc.build_isotropic_weight(m, 0.8)
+    return orc.init_spectra(f, m, wt, t), f, m, wt
+
+
+def _gpu_iterate(spec, gamma, iters, precision="fp64"):
+    s = P.spectral.Spectrum(spec.t, spec.window_width, spec.window_height, spec.rw.copy(),
+                            spec.w.copy(), spec.g.copy(), spec.w0, spec.weighted_energy,
+                            spec.initial_energy, spec.initial_max, spec.nu, spec.converged)
+    tr = P.spectral.fast_iterate(s, gamma, iters, precision)
+    return s, tr
+
+
+def _canonical(t):
+    k1, k2 = np.meshgrid(np.arange(t), np.arange(t), indexing="ij")
+    return (k1 * t + k2) <= (((t - k1) % t) * t + (t - k2) % t)
+
+
+@pytest.mark.parametrize("t,h,w,gamma,iters", [
+    (8, 6, 7, 0.2, 20), (16, 14, 13, 0.5, 40), (32, 24, 24, 0.5, 50),
+    (64, 48, 48, 0.5, 200), (64, 40, 47, 0.2, 120), (128, 64, 64, 0.5, 60),
+])
+def test_iterate_bit_exact_vs_oracle(gpu, orc, t, h, w, gamma, iters):
+    """K2 strict fp64 fed the oracle's init_spectra reproduces fast_iterate bit for bit
+    (engine_spectral.cpp:51-144): u, p, c, energies, G and the canonical R_w."""
+    rng = np.random.default_rng(1000 + t + h)
+    spec, *_ = _oracle_spectrum(orc, rng, t, h, w)
+    ref = spec.copy()
+    rec_ref = orc.fast_iterate(ref, gamma, iters)
+    got, rec = _gpu_iterate(spec, gamma, iters)
+    assert len(rec) == len(rec_ref) > 0
+    for k in ("u1", "u2", "p_re", "p_im", "c_re", "c_im", "weighted_energy"):
+        np.testing.assert_array_equal(rec[k], rec_ref[k], err_msg=k)
+    assert got.nu == ref.nu and got.converged == ref.converged
+    assert got.weighted_energy == ref.weighted_energy
+    np.testing.assert_array_equal(got.g, ref.g)
+    can = _canonical(t)
+    np.testing.assert_array_equal(got.rw[can], ref.rw[can])
+
+
+def test_iterate_resumes_like_reference(gpu, orc):
+    """fast_iterate runs at most `iterations` more selections (engine_spectral.hpp:41-43)."""
+    rng = np.random.default_rng(7)
+    spec, *_ = _oracle_spectrum(orc, rng, 64, 48, 48)
+    ref = spec.copy()
+    orc.fast_iterate(ref, 0.5, 90)
+    s = P.spectral.Spectrum(64, spec.window_width, spec.window_height, spec.rw.copy(), spec.w.copy(),
+                            spec.g.copy(), spec.w0, spec.weighted_energy, spec.initial_energy,
+                            spec.initial_max)
+    P.spectral.fast_iterate(s, 0.5, 40)
+    P.spectral.fast_iterate(s, 0.5, 50)
+    assert s.nu == 90
+    np.testing.assert_array_equal(s.g, ref.g)
+    assert s.weighted_energy == ref.weighted_energy
+
+
+def test_zero_signal_converges_immediately(gpu, orc):
+    """engine_spectral_test.cpp:298-308."""
+    m = np.zeros((8, 8), np.uint8)
+    wt = orc.build_isotropic_weight(m, 0.8)
+    spec = orc.init_spectra(np.zeros((8, 8)), m, wt, 8)
+    s, tr = _gpu_iterate(spec, 0.5, 10)
+    assert s.converged and len(tr) == 0 and s.nu == 0
+
+
+def test_constant_window_collapses_to_dc(gpu, orc):
+    """engine_spectral_test.cpp:98-115: u=(0,0), p=c, model == c."""
+    c = 4.0
+    m = block_mask(6, 6, missing=[(2, 2, 2, 2)])
+    wt = orc.build_isotropic_weight(m, 0.8)
+    spec = orc.init_spectra(np.full((6, 6), c), m, wt, 8)
+    s, tr = _gpu_iterate(spec, 1.0, 1)
+    assert len(tr) == 1 and tr[0]["u1"] == 0 and tr[0]["u2"] == 0
+    assert abs(complex(tr[0]["p_re"], tr[0]["p_im"]) - c) < 1e-9
+    assert np.abs(s.rw).max() < 1e-9 * spec.initial_max
+    model = P.spectral.synthesize_model(s)
+    np.testing.assert_allclose(model, c, rtol=1e-9)
+
+
+@pytest.mark.parametrize("t,h,w", [(8, 6, 7), (16, 16, 16), (64, 48, 48), (128, 64, 64), (32, 24, 17)])
+def test_init_spectra_vs_oracle(gpu, orc, t, h, w):
+    """K1 (batched real-input 2-D FFT, fp64) vs init_spectra (engine_spectral.cpp:148-183)."""
+    rng = np.random.default_rng(t * 31 + w)
+    f = random_grid(rng, h, w) * 50.0
+    m = random_mask(rng, h, w)
+    wt = orc.build_isotropic_weight(m, 0.8)
+    ref = orc.init_spectra(f, m, wt, t)
+    got = P.spectral.init_spectra(f, m, wt, t)
+    scale = np.abs(ref.rw).max()
+    assert np.abs(got.rw - ref.rw).max() <= 1e-13 * scale
+    assert np.abs(got.w - ref.w).max() <= 1e-13 * np.abs(ref.w).max()
+    assert got.w0 == pytest.approx(ref.w0, rel=1e-14)
+    assert got.weighted_energy == pytest.approx(ref.weighted_energy, rel=1e-13)
+    assert got.initial_max == pytest.approx(ref.initial_max, rel=1e-13)
+
+
+def test_synthesize_vs_oracle(gpu, orc):
+    rng = np.random.default_rng(5)
+    spec, *_ = _oracle_spectrum(orc, rng, 64, 48, 48)
+    orc.fast_iterate(spec, 0.5, 150)
+    ref = orc.synthesize_model(spec)
+    got = P.spectral.synthesize_model(P.spectral.Spectrum(64, 48, 48, spec.rw, spec.w, spec.g))
+    assert np.abs(got - ref).max() <= 1e-10
+
+
+def _oracle_conceal(orc, img, pat, cfg, traces=True):
+    return orc.conceal(img.astype(np.float64), [tuple(b) for b in pat.blocks], pat.block_height,
+                       pat.block_width, algorithm=2 if cfg.algorithm == "fofse" else 0,
+                       gamma=cfg.gamma, iterations=cfg.iterations, t=cfg.transform_size,
+                       rho_hat=cfg.rho_hat, support=cfg.support_width, traces=traces)
+
+
+def _assert_same_selections(got_traces, ref_traces):
+    assert len(got_traces) == len(ref_traces)
+    for i, (a, b) in enumerate(zip(got_traces, ref_traces)):
+        assert len(a) == len(b), f"block {i}: {len(a)} vs {len(b)} records"
+        np.testing.assert_array_equal(a["u1"], b["u1"], err_msg=f"block {i}")
+        np.testing.assert_array_equal(a["u2"], b["u2"], err_msg=f"block {i}")
+
+
+def test_conceal_fp64_C1(gpu, orc):
+    """BASELINE C1 (512x512, 10% isolated 16x16 losses, T=64, 100 it, fp64): same
+    selected-basis sequence for every block and pixels within 1e-9."""
+    img, pat = WL.C1.frame(seed=11)
+    cfg = WL.C1.config(record_traces=True)
+    out = P.conceal(img.astype(np.float64), pat, cfg)
+    ref = _oracle_conceal(orc, img, pat, cfg)
+    _assert_same_selections(out.report.traces, ref["traces"])
+    assert np.abs(out.restored - ref["restored"]).max() <= FP64_PX_TOL
+    assert out.report.psnr_db == pytest.approx(ref["psnr_db"], rel=1e-12)
+
+
+def test_conceal_fp64_borders_and_neighbours(gpu, orc):
+    """Border windows + lost neighbours inside windows (OUTSIDE labels,
+    pipeline.cpp:95-110), rectangular blocks, the reference's grid pattern."""
+    rng = np.random.default_rng(409)
+    img = smooth_test_image(rng, 160)
+    blocks = [(0, 0, 12, 16), (0, 24, 12, 16), (20, 10, 12, 16), (148, 144, 12, 16),
+              (70, 70, 12, 16), (82, 90, 12, 16), (40, 140, 12, 16)]
+    pat = P.LossPattern(160, 160, 12, 16, [P.Rect(*b) for b in blocks])
+    cfg = P.ConcealConfig(gamma=0.3, iterations=80, transform_size=64, support_width=14,
+                          record_traces=True)
+    out = P.conceal(img, pat, cfg)
+    ref = _oracle_conceal(orc, img, pat, cfg)
+    _assert_same_selections(out.report.traces, ref["traces"])
+    assert np.abs(out.restored - ref["restored"]).max() <= FP64_PX_TOL
+
+
+def test_conceal_empty_pattern_is_identity(gpu):
+    """pipeline_test.cpp:171-183."""
+    img = smooth_test_image(np.random.default_rng(421), 64)
+    out = P.conceal(img, P.LossPattern(64, 64, 16, 16, []), P.ConcealConfig(algorithm="fse"))
+    np.testing.assert_array_equal(out.restored, img)
+    assert out.report.psnr_identical
+
+
+def test_conceal_rewrites_only_missing_samples(gpu):
+    """pipeline_test.cpp:140-169."""
+    img = smooth_test_image(np.random.default_rng(419), 96)
+    pat = P.LossPattern(96, 96, 16, 16, [P.Rect(16, 16, 16, 16), P.Rect(16, 64, 16, 16),
+                                         P.Rect(64, 16, 16, 16), P.Rect(64, 64, 16, 16)])
+    out = P.conceal(img, pat, P.ConcealConfig(iterations=5))
+    lost = np.zeros_like(img, bool)
+    for b in pat.blocks:
+        lost[b.row:b.row + 16, b.col:b.col + 16] = True
+    np.testing.assert_array_equal(out.restored[~lost], img[~lost])
+    assert (out.restored[lost] >= 0).all() and (out.restored[lost] <= 255).all()
+    assert (out.restored[lost] != img[lost]).any()
+
+
+@pytest.mark.parametrize("algo,gamma", [("fse", 0.0), ("fofse", 1.0), ("fofse", 0.2)])
+def test_conceal_fp64_algorithms(gpu, orc, algo, gamma):
+    rng = np.random.default_rng(433)
+    img = smooth_test_image(rng, 96)
+    pat = P.LossPattern(96, 96, 16, 16, [P.Rect(16, 16, 16, 16), P.Rect(64, 64, 16, 16)])
+    cfg = P.ConcealConfig(algorithm=algo, gamma=gamma, iterations=30, record_traces=True)
+    out = P.conceal(img, pat, cfg)
+    ref = _oracle_conceal(orc, img, pat, cfg)
+    _assert_same_selections(out.report.traces, ref["traces"])
+    assert np.abs(out.restored - ref["restored"]).max() <= FP64_PX_TOL
+
+
+def _fp32_vs_ref(got_img, ref_img, lost):
+    err = np.abs(got_img[lost].astype(np.float64) - ref_img[lost])
+    return err.max()
+
+
+def test_conceal_fp32_C2_vs_oracle(gpu, orc):
+    """BASELINE C2 fp32 fast mode vs the fp64 oracle on a 400-block slice:
+    max pixel error <= 0.5, PSNR within 0.05 dB."""
+    img, pat = WL.C2.frame(seed=21)
+    sub = P.LossPattern(pat.image_width, pat.image_height, 16, 16, pat.blocks[::5])
+    cfg32 = WL.C2.config("fp32")
+    out = P.conceal(img.astype(np.float64), sub, cfg32)
+    ref = _oracle_conceal(orc, img, sub, WL.C2.config("fp64"), traces=False)
+    lost = np.zeros(img.shape, bool)
+    for b in sub.blocks:
+        lost[b.row:b.row + 16, b.col:b.col + 16] = True
+    assert _fp32_vs_ref(out.restored, ref["restored"], lost) <= FP32_PX_TOL
+    assert abs(out.report.psnr_db - ref["psnr_db"]) <= FP32_PSNR_TOL
+
+
+def test_conceal_fp32_vs_fp64_full_C2(gpu):
+    """All 2040 blocks of C2: GPU fp32 vs GPU fp64 (the fp64 path is pinned to the
+    oracle above)."""
+    img, pat = WL.C2.frame(seed=22)
+    o64 = P.conceal(img.astype(np.float64), pat, WL.C2.config("fp64"))
+    o32 = P.conceal(img.astype(np.float64), pat, WL.C2.config("fp32"))
+    lost = np.zeros(img.shape, bool)
+    for b in pat.blocks:
+        lost[b.row:b.row + 16, b.col:b.col + 16] = True
+    assert np.abs(o32.restored[lost] - o64.restored[lost]).max() <= FP32_PX_TOL
+    assert abs(o32.report.psnr_db - o64.report.psnr_db) <= FP32_PSNR_TOL
+
+
+def test_extrapolate_windows_vs_oracle(gpu, orc):
+    """Window level (pipeline.cpp:181-203) with arbitrary per-window masks."""
+    rng = np.random.default_rng(99)
+    n, h, w = 6, 40, 44
+    wins = np.stack([random_grid(rng, h, w) * 80 + 100 for _ in range(n)])
+    masks = np.stack([random_mask(rng, h, w, 0.3) for _ in range(n)])
+    cfg = P.ConcealConfig(gamma=0.4, iterations=60, transform_size=64, rho_hat=0.75)
+    runs = P.extrapolate_windows(wins, masks, cfg)
+    for i in range(n):
+        wt = orc.build_isotropic_weight(masks[i], cfg.rho_hat)
+        s = orc.init_spectra(wins[i], masks[i], wt, 64)
+        rec = orc.fast_iterate(s, cfg.gamma, cfg.iterations)
+        model = orc.synthesize_model(s)
+        np.testing.assert_array_equal(runs[i].trace["u1"], rec["u1"])
+        np.testing.assert_array_equal(runs[i].trace["u2"], rec["u2"])
+        assert np.abs(runs[i].model - model).max() <= 1e-9
+
+
+@pytest.mark.parametrize("name", ["C3", "C5"])
+def test_small_and_large_blocks_fp32(gpu, orc, name):
+    """C3 (8x8, T=32, 50 it) and C5 (32x32, T=128, 300 it) on a cropped image."""
+    wl = WL.ALL[name]
+    size = 512 if name == "C3" else 1024
+    img = P.gen_image_u8(31, size, size)
+    rects = P.gen_losses(31, size // wl.block, size // wl.block, wl.loss_frac, wl.block, wl.block)
+    rects = rects[: 120 if name == "C3" else 40]
+    pat = P.LossPattern(size, size, wl.block, wl.block,
+                        [P.Rect(*map(int, (r["row"], r["col"], r["height"], r["width"]))) for r in rects])
+    out = P.conceal(img.astype(np.float64), pat, wl.config("fp32"))
+    ref = _oracle_conceal(orc, img, pat, wl.config("fp64"), traces=False)
+    lost = np.zeros(img.shape, bool)
+    for b in pat.blocks:
+        lost[b.row:b.row + wl.block, b.col:b.col + wl.block] = True
+    assert _fp32_vs_ref(out.restored, ref["restored"], lost) <= FP32_PX_TOL
+    assert abs(out.report.psnr_db - ref["psnr_db"]) <= FP32_PSNR_TOL
+    o64 = P.conceal(img.astype(np.float64), pat, wl.config("fp64"))
+    assert np.abs(o64.restored - ref["restored"]).max() <= FP64_PX_TOL
+
+
+def test_frames_u8_matches_f64_and_is_deterministic(gpu):
+    """Video entry point: u8 frames give write_pgm-rounded results of the f64 path;
+    repeated runs and frame-order changes are bitwise identical."""
+    wl = WL.C4
+    frames, rects, offs = wl.batch(seed=40, frames=3)
+    pats = []
+    for f in range(3):
+        rr = rects[offs[f]:offs[f + 1]]
+        pats.append(P.LossPattern(wl.width, wl.height, 16, 16,
+                                  [P.Rect(*map(int, (r["row"], r["col"], 16, 16))) for r in rr]))
+    cfg = wl.config("fp32")
+    a, sq_a, rep = P.conceal_frames(frames, pats, cfg)
+    b, sq_b, _ = P.conceal_frames(frames, pats, cfg)
+    np.testing.assert_array_equal(a, b)
+    np.testing.assert_array_equal(sq_a, sq_b)
+    # reversed frame order -> same per-frame results
+    c, _, _ = P.conceal_frames(frames[::-1].copy(), pats[::-1], cfg)
+    np.testing.assert_array_equal(c[::-1], a)
+    # f64 path on frame 1, rounded like write_pgm
+    o = P.conceal(frames[1].astype(np.float64), pats[1], cfg)
+    np.testing.assert_array_equal(np.clip(np.floor(o.restored + 0.5), 0, 255).astype(np.uint8), a[1])
+    assert rep.device["blocks"] == offs[-1]
