@@ -72,9 +72,11 @@ typedef struct {
     int32_t record_traces; /* fill per-block IterationRecord traces */
     int32_t precision;     /* FOFSE_PREC_* */
     double guard_tau;      /* FP32 near-tie guard on |R|^2; < 0 = default, 0 = off */
+    int32_t fp64_head;     /* FP32 mode: first selections run in FP64; < 0 = default */
+    int32_t pad0;
 } fofse_params;
 
-/* fse::IterationRecord (include/fse/trace.hpp:13-21), 64 bytes. */
+/* fse::IterationRecord (include/fse/trace.hpp:13-21), 72 bytes. */
 typedef struct {
     int32_t nu, u1, u2, pad0;
     double p_re, p_im, c_re, c_im;
@@ -96,6 +98,8 @@ typedef struct {
     double iterate_ms;         /* K2 iterate + fused synthesis (incl. guard re-runs) */
     double total_ms;           /* device time of the whole call */
     int64_t kernel_launches;
+    double rerun_ms;           /* FP32 guard re-runs (included in iterate_ms) */
+    int64_t fp64_head;         /* FP32 mode: selections run in FP64 per block */
 } fofse_report;
 
 typedef struct fofse_ctx fofse_ctx;
@@ -199,6 +203,24 @@ int fofse_spectral_synthesize(fofse_ctx* ctx, int32_t t, int64_t n, const double
  * kind 0: shared-memory LDS.64 bandwidth [GB/s]; 1: LDS.32 [GB/s];
  * 2: FP32 FFMA [TFLOP/s]; 3: FP64 DFMA [TFLOP/s]. */
 int fofse_microbench(int32_t device, int32_t kind, double* value);
+
+/* Diagnostics (not a reference interface): fofse_conceal_f64 that also
+ * returns, per block and selection, the fp32 paths' relative gap between the
+ * two largest canonical |R|^2 (what guard_tau thresholds). traces,
+ * trace_counts, gap_trace are required (n_blocks*iterations entries). */
+int fofse_diag_conceal_f64(fofse_ctx* ctx, const double* image, int32_t width, int32_t height,
+                           const fofse_rect* blocks, int64_t n_blocks, int32_t block_height,
+                           int32_t block_width, const fofse_params* params, double* restored,
+                           fofse_record* traces, int32_t* trace_counts, float* gap_trace);
+
+/* Diagnostics: fofse_spectral_iterate + per-selection fp32 top-2 gap. */
+int fofse_diag_spectral_iterate(fofse_ctx* ctx, int32_t t, int64_t n, int32_t win_h,
+                                int32_t win_w, double* rw, const double* wspec, double* g,
+                                const double* w0, double* weighted_energy,
+                                const double* initial_energy, const double* initial_max,
+                                int32_t* nu, int32_t* converged, double gamma, int32_t iterations,
+                                int32_t precision, fofse_record* traces, int32_t* trace_counts,
+                                float* gap_trace);
 
 /* Synthetic inputs (host C++, deterministic, multi-threaded).
  * gen_image: sum of 3 low-frequency cosines (amp 40), 4 piecewise-constant

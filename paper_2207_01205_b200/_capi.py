@@ -26,6 +26,7 @@ EXPORTS = [
     "fofse_extrapolate_windows", "fofse_spectral_init", "fofse_spectral_iterate",
     "fofse_spectral_synthesize", "fofse_gen_image_u8", "fofse_gen_losses",
     "fofse_validate_conceal", "fofse_plan_info", "fofse_plan_block_labels", "fofse_microbench",
+    "fofse_diag_conceal_f64", "fofse_diag_spectral_iterate",
 ]
 
 
@@ -46,7 +47,7 @@ class Params(C.Structure):
         ("algorithm", C.c_int32), ("gamma", C.c_double), ("iterations", C.c_int32),
         ("transform_size", C.c_int32), ("rho_hat", C.c_double), ("support_width", C.c_int32),
         ("threads", C.c_int32), ("record_traces", C.c_int32), ("precision", C.c_int32),
-        ("guard_tau", C.c_double),
+        ("guard_tau", C.c_double), ("fp64_head", C.c_int32), ("pad0", C.c_int32),
     ]
 
 
@@ -56,6 +57,7 @@ class Report(C.Structure):
         ("mean_seconds_per_block", C.c_double), ("blocks", C.c_int64), ("classes", C.c_int64),
         ("guard_reruns", C.c_int64), ("converged_blocks", C.c_int64), ("init_ms", C.c_double),
         ("iterate_ms", C.c_double), ("total_ms", C.c_double), ("kernel_launches", C.c_int64),
+        ("rerun_ms", C.c_double), ("fp64_head", C.c_int64),
     ]
 
     def as_dict(self):

@@ -158,13 +158,14 @@ struct Cfg {
     double rho;
     int S, threads, traces, precision;
     double tau;
+    int head;
 };
 
 Cfg to_cfg(const fofse_params* p) {
     if (!p) throw std::invalid_argument("params must not be NULL");
     Cfg c{p->algorithm,      p->gamma,     p->iterations,    p->transform_size,
           p->rho_hat,        p->support_width, p->threads,   p->record_traces,
-          p->precision,      p->guard_tau};
+          p->precision,      p->guard_tau,     p->fp64_head};
     return c;
 }
 
@@ -192,10 +193,6 @@ void check_gpu_support(const Cfg& c) {
 }
 
 double effective_gamma(const Cfg& c) { return c.algorithm == FOFSE_ALGO_FSE ? 1.0 : c.gamma; }
-double effective_tau(const Cfg& c) {
-    if (c.precision != FOFSE_PREC_FP32) return 0.0;
-    return c.tau < 0.0 ? 5e-5 : c.tau;
-}
 
 // Per-frame occupancy grid: cell (row/bh, col/bw) -> index of the block whose
 // top-left corner lies in it. Non-overlapping equal-size blocks never share a
@@ -448,19 +445,38 @@ std::vector<Tile> make_tiles(int64_t begin, int64_t end, const std::vector<Block
 }
 
 struct RunOut {
-    double init_ms = 0, iter_ms = 0, total_ms = 0;
-    int64_t reruns = 0, converged = 0;
+    double init_ms = 0, iter_ms = 0, total_ms = 0, rerun_ms = 0;
+    int64_t reruns = 0, converged = 0, head = 0;
 };
 
-// Device run of a job. frames_dev: source (and destination) frames on device.
+// fp32 fast mode: the first `head` selections of every block run in fp64
+// (they carry the large coefficients whose fp32 rounding would otherwise
+// dominate the late-iteration residual).
+int resolve_head(const Cfg& c) {
+    if (c.precision != FOFSE_PREC_FP32 || c.iterations <= 0) return 0;
+    const int h = c.head < 0 ? std::max(5, (c.iterations + 19) / 20) : c.head;
+    return std::min(h, c.iterations);
+}
+
+double effective_tau(const Cfg& c, int head) {
+    if (c.precision != FOFSE_PREC_FP32) return 0.0;
+    if (c.tau >= 0.0) return c.tau;
+    return head > 0 ? 1e-5 : 5e-5;
+}
+
+// Device run of a job. fr: source (and destination) frames on device.
 // synth: SYN_IMAGE (write-back into frames + block_sq) or SYN_WINDOW (models).
+// Per-block device outputs (block_sq, models, trace, trace_count) are indexed
+// by the caller's block order.
 RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int synth,
-               double* d_block_sq, double* d_models, fofse_record* d_trace, int32_t* d_trace_count) {
+               double* d_block_sq, double* d_models, fofse_record* d_trace, int32_t* d_trace_count,
+               float* d_gap = nullptr) {
     using namespace fofse;
     const Geometry& g = job.geo;
     const int T = g.T;
     const int64_t n = static_cast<int64_t>(job.blocks.size());
     const int ncls = static_cast<int>(job.cls_labels.size());
+    const int I = cfg.iterations;
     RunOut out;
     cudaStream_t st = ctx->stream;
     for (auto& e : ctx->ev)
@@ -478,18 +494,29 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         sym[static_cast<size_t>(c)] = point_symmetric(lab, g.Lh, g.Lw) ? 1 : 0;
     }
     const bool fp32 = cfg.precision == FOFSE_PREC_FP32;
+    const int head = resolve_head(cfg);
+    out.head = head;
+    const bool v2 = fp32 && v2_supported(T);
     auto path_of = [&](int cls) {
         if (!fp32) return (int)PATH_F64_STRICT;
         return sym[static_cast<size_t>(cls)] ? (int)PATH_F32_REAL : (int)PATH_F32_COMPLEX;
     };
 
     const auto twf = twiddles(T, -1), twi = twiddles(T, +1);
+    std::vector<double2> ptab(2 * static_cast<size_t>(T));
+    for (int m = 0; m < 2 * T; ++m)  // e^{-j pi m / T}
+        ptab[static_cast<size_t>(m)] = make_double2(std::cos(M_PI * m / T), -std::sin(M_PI * m / T));
     double2* d_twf = upload(ctx, "twf", twf.data(), twf.size());
     double2* d_twi = upload(ctx, "twi", twi.data(), twi.size());
+    double2* d_ptab = upload(ctx, "ptab", ptab.data(), ptab.size());
     double* d_wcls = upload(ctx, "wcls", wcls.data(), wcls.size());
 
-    const int seg64 = seg_of(T, PATH_F64_STRICT), seg32 = seg_of(T, PATH_F32_REAL);
+    const int seg64 = seg_of(T, PATH_F64_STRICT);
+    const int seg32 = v2 ? v2_seg(T) : seg_of(T, PATH_F32_REAL);
+    const int spt32 = v2 ? v2_spt(T) : 1;
     const int sr64 = T + seg64 + 1, sr32 = T + seg32 + 1;
+    // W images: fp32 images use the fp32 kernel's SEG (K1 class mode derives it
+    // from seg_for(T, 0); K2v2 uses v2_seg(T) — equal for every T).
     double2* d_wimg64 = ctx->buf("wimg64").as<double2>(static_cast<size_t>(ncls) * T * sr64);
     float2* d_wimg32 = fp32 ? ctx->buf("wimg32").as<float2>(static_cast<size_t>(ncls) * T * sr32) : nullptr;
     float* d_vimg32 = fp32 ? ctx->buf("vimg32").as<float>(static_cast<size_t>(ncls) * T * sr32) : nullptr;
@@ -523,77 +550,55 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
     for (int64_t i = 0; i < n; ++i) sorted[static_cast<size_t>(i)] = job.blocks[ids[static_cast<size_t>(i)]];
     BlockDesc* d_sorted = upload(ctx, "sorted", sorted.data(), sorted.size());
     int32_t* d_ids = upload(ctx, "ids", ids.data(), ids.size());
-
-    // residual buffers per position (size of the widest slot type)
-    const BinLayout L64 = BinLayout::make(T, seg64), L32 = BinLayout::make(T, seg32);
-    const size_t slot_bytes = fp32 ? sizeof(float2) * L32.SLOTS : sizeof(double2) * L64.SLOTS;
-    char* d_R = ctx->buf("R").as<char>(static_cast<size_t>(n) * slot_bytes);
-    double* d_e0 = ctx->buf("e0").as<double>(static_cast<size_t>(n));
-    double* d_imax = ctx->buf("imax").as<double>(static_cast<size_t>(n));
-    int32_t* d_flags = fp32 ? ctx->buf("flags").as<int32_t>(static_cast<size_t>(n)) : nullptr;
-    int32_t* d_conv = ctx->buf("conv").as<int32_t>(static_cast<size_t>(n));
-
-    // path ranges over the sorted positions
-    int64_t p0 = 0;
     struct Range { int path; int64_t begin, end; };
     std::vector<Range> ranges;
-    while (p0 < n) {
+    for (int64_t p0 = 0; p0 < n;) {
         const int p = path_of(sorted[static_cast<size_t>(p0)].cls);
         int64_t p1 = p0;
         while (p1 < n && path_of(sorted[static_cast<size_t>(p1)].cls) == p) ++p1;
         ranges.push_back({p, p0, p1});
         p0 = p1;
     }
-    // K1 per path range (output packed in that path's precision/rotation)
-    for (const Range& r : ranges) {
+
+    const BinLayout L64 = BinLayout::make(T, seg64), L32 = BinLayout::make(T, seg32, spt32);
+    double* d_e0 = ctx->buf("e0").as<double>(static_cast<size_t>(n));      // by position
+    double* d_imax = ctx->buf("imax").as<double>(static_cast<size_t>(n));  // by position
+    int32_t* d_flags = fp32 ? ctx->buf("flags").as<int32_t>(static_cast<size_t>(n)) : nullptr;
+    int32_t* d_conv = ctx->buf("conv").as<int32_t>(static_cast<size_t>(n));  // by caller id
+    const bool rec_glob = fp32 || I > k2_smem_rec_cap(T, 0);
+    int32_t* d_rec_u = nullptr;
+    double2* d_rec_c = nullptr;
+    if (rec_glob && I > 0) {
+        d_rec_u = ctx->buf("rec_u").as<int32_t>(static_cast<size_t>(n) * I);
+        d_rec_c = ctx->buf("rec_c").as<double2>(static_cast<size_t>(n) * I);
+    }
+    auto k1_packed = [&](const BlockDesc* descs, int64_t cnt, int path, int seg, int spt, void* outp,
+                         double* e, double* m) {
         K1Args a{};
         a.T = T;
         a.Lh = g.Lh;
         a.Lw = g.Lw;
-        a.n = static_cast<int32_t>(r.end - r.begin);
-        a.blocks = d_sorted + r.begin;
+        a.n = static_cast<int32_t>(cnt);
+        a.blocks = descs;
         a.fr = fr;
         a.wcls = d_wcls;
         a.mode = K1_PACKED;
-        a.path = r.path;
-        a.seg = seg_of(T, r.path);
-        a.out = d_R + static_cast<size_t>(r.begin) * slot_bytes;
-        // K1 indexes its outputs from 0: shift the packed base per range
-        a.energy = d_e0 + r.begin;
-        a.init_max = d_imax + r.begin;
+        a.path = path;
+        a.seg = seg;
+        a.spt = spt;
+        a.out = outp;
+        a.energy = e;
+        a.init_max = m;
         a.twid = d_twf;
-        // packed output stride equals the path's slot size; fp32 ranges use
-        // float2 slots, fp64 double2 — both fit in slot_bytes.
-        if (r.path != PATH_F64_STRICT && slot_bytes != sizeof(float2) * L32.SLOTS)
-            throw std::logic_error("slot size mismatch");
         ck(k1_launch(a, st), "K1 residual spectra");
         ++ctx->launches;
-    }
-    ck(cudaEventRecord(ctx->ev[1], st), "event");
-
-    // ---- K2 per path range ----
-    std::vector<Tile> all_tiles;
-    struct Launch { int path; int64_t t0, t1; };
-    std::vector<Launch> launches;
-    for (const Range& r : ranges) {
-        std::vector<Tile> tl = make_tiles(r.begin, r.end, sorted, k2_groups_per_cta(T, r.path));
-        const int64_t t0 = static_cast<int64_t>(all_tiles.size());
-        all_tiles.insert(all_tiles.end(), tl.begin(), tl.end());
-        launches.push_back({r.path, t0, static_cast<int64_t>(all_tiles.size())});
-    }
-    Tile* d_tiles = upload(ctx, "tiles", all_tiles.data(), all_tiles.size());
-    int32_t* d_rec_u = nullptr;
-    double2* d_rec_c = nullptr;
-    if (cfg.iterations > k2_smem_rec_cap(T, 0)) {
-        d_rec_u = ctx->buf("rec_u").as<int32_t>(static_cast<size_t>(n) * cfg.iterations);
-        d_rec_c = ctx->buf("rec_c").as<double2>(static_cast<size_t>(n) * cfg.iterations);
-    }
+    };
     auto base_args = [&]() {
         K2Args a{};
         a.T = T;
         a.Lh = g.Lh;
         a.Lw = g.Lw;
-        a.iterations = cfg.iterations;
+        a.iterations = I;
         a.gamma = effective_gamma(cfg);
         a.w0 = d_w0;
         a.synth = synth;
@@ -605,34 +610,121 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         a.models = d_models;
         a.block_sq = d_block_sq;
         a.twid_inv = d_twi;
+        a.ptab = d_ptab;
         a.rec_u_g = d_rec_u;
         a.rec_c_g = d_rec_c;
+        a.rec_stride = I;
         a.trace = d_trace;
         a.trace_count = d_trace_count;
-        return a;
-    };
-    for (const Launch& l : launches) {
-        K2Args a = base_args();
-        a.path = l.path;
-        a.seg = seg_of(T, l.path);
-        a.tau = l.path == PATH_F64_STRICT ? 0.0 : effective_tau(cfg);
-        a.tiles = d_tiles + l.t0;
-        a.order = d_ids;  // position -> caller block id
+        a.trace_stride = I;
+        a.gap_trace = d_gap;
+        a.order = d_ids;
         a.blocks = d_sorted;
-        a.rin = d_R;
-        a.wimg = l.path == PATH_F64_STRICT ? (const void*)d_wimg64
-                 : l.path == PATH_F32_COMPLEX ? (const void*)d_wimg32 : (const void*)d_vimg32;
-        a.wimg_stride = static_cast<int64_t>(T) * (l.path == PATH_F64_STRICT ? sr64 : sr32);
         a.energy0 = d_e0;
         a.init_energy = d_e0;
         a.init_max = d_imax;
         a.conv_out = d_conv;
-        a.flags = d_flags;
-        ck(k2_launch(a, static_cast<int32_t>(l.t1 - l.t0), st), "K2 iterate");
+        return a;
+    };
+    auto tiles_for = [&](int64_t b0, int64_t b1, int ng) {
+        return make_tiles(b0, b1, sorted, ng);
+    };
+
+    // ---- phase A: residual spectra ----
+    char* d_R64 = nullptr;
+    char* d_R32 = nullptr;
+    if (!fp32 || head > 0) {
+        d_R64 = ctx->buf("R64").as<char>(static_cast<size_t>(n) * sizeof(double2) * L64.SLOTS);
+        k1_packed(d_sorted, n, PATH_F64_STRICT, seg64, 1, d_R64, d_e0, d_imax);
+    }
+    if (fp32) d_R32 = ctx->buf("R32").as<char>(static_cast<size_t>(n) * sizeof(float2) * L32.SLOTS);
+    if (fp32 && head == 0)
+        for (const Range& r : ranges)
+            k1_packed(d_sorted + r.begin, r.end - r.begin, r.path, seg32, spt32,
+                      d_R32 + static_cast<size_t>(r.begin) * sizeof(float2) * L32.SLOTS, d_e0 + r.begin,
+                      d_imax + r.begin);
+    ck(cudaEventRecord(ctx->ev[1], st), "event");
+
+    // ---- phase B: fp64 (strict reference op order) ----
+    double* d_en = nullptr;
+    int32_t* d_nu = nullptr;
+    int32_t* d_cvh = nullptr;
+    if (!fp32 || head > 0) {
+        std::vector<Tile> tl = tiles_for(0, n, k2_groups_per_cta(T, PATH_F64_STRICT));
+        Tile* d_tl = upload(ctx, "tiles64", tl.data(), tl.size());
+        K2Args a = base_args();
+        a.path = PATH_F64_STRICT;
+        a.seg = seg64;
+        a.tau = 0.0;
+        a.tiles = d_tl;
+        a.rin = d_R64;
+        a.wimg = d_wimg64;
+        a.wimg_stride = static_cast<int64_t>(T) * sr64;
+        a.rec_global = fp32 ? 1 : 0;
+        if (fp32) {
+            // head: `head` selections, state handed to the fp32 phase by position
+            d_en = ctx->buf("en").as<double>(static_cast<size_t>(n));
+            d_nu = ctx->buf("nu").as<int32_t>(static_cast<size_t>(n));
+            d_cvh = ctx->buf("cvh").as<int32_t>(static_cast<size_t>(n));
+            a.iterations = head;
+            a.synth = SYN_NONE;
+            a.rout = d_R64;
+            a.state_by_pos = 1;
+            a.energy_out = d_en;
+            a.nu_out = d_nu;
+            a.conv_out = d_cvh;
+            a.trace_count = nullptr;
+            a.gap_trace = nullptr;
+        }
+        ck(k2_launch(a, static_cast<int32_t>(tl.size()), st), "K2 fp64");
         ++ctx->launches;
     }
+    // ---- phase C: fp32 fast mode ----
+    if (fp32) {
+        for (const Range& r : ranges) {
+            if (head > 0) {
+                CvtArgs c{};
+                c.T = T;
+                c.Lh = g.Lh;
+                c.Lw = g.Lw;
+                c.n = static_cast<int32_t>(r.end - r.begin);
+                c.in = reinterpret_cast<const double2*>(d_R64) + static_cast<size_t>(r.begin) * L64.SLOTS;
+                c.out = reinterpret_cast<float2*>(d_R32) + static_cast<size_t>(r.begin) * L32.SLOTS;
+                c.out_seg = seg32;
+                c.out_spt = spt32;
+                c.rotate = r.path == PATH_F32_REAL;
+                ck(cvt_launch(c, st), "convert head state");
+                ++ctx->launches;
+            }
+            const int ng = v2 ? k2v2_warps_per_cta() : k2_groups_per_cta(T, r.path);
+            std::vector<Tile> tl = tiles_for(r.begin, r.end, ng);
+            Tile* d_tl = upload(ctx, r.path == PATH_F32_REAL ? "tilesR" : "tilesC", tl.data(), tl.size());
+            K2Args a = base_args();
+            a.path = r.path;
+            a.seg = seg32;
+            a.tau = effective_tau(cfg, head);
+            a.tiles = d_tl;
+            a.rin = d_R32;
+            a.wimg = r.path == PATH_F32_REAL ? (const void*)d_vimg32 : (const void*)d_wimg32;
+            a.wimg_stride = static_cast<int64_t>(T) * sr32;
+            a.flags = d_flags;
+            a.rec_global = 1;
+            a.iterations = I - head;
+            a.trace_from_nu0 = 1;
+            if (head > 0) {
+                a.energy0 = d_en;
+                a.nu0 = d_nu;
+                a.conv0 = d_cvh;
+            }
+            ck(v2 ? k2v2_launch(a, static_cast<int32_t>(tl.size()), st)
+                  : k2_launch(a, static_cast<int32_t>(tl.size()), st),
+               "K2 fp32");
+            ++ctx->launches;
+        }
+    }
+    ck(cudaEventRecord(ctx->ev[2], st), "event");
 
-    // ---- fp32 near-tie guard: re-run flagged blocks in fp64 ----
+    // ---- fp32 near-tie guard: re-run flagged blocks in fp64 from scratch ----
     if (fp32 && n > 0) {
         std::vector<int32_t> flags(static_cast<size_t>(n));
         ck(cudaMemcpyAsync(flags.data(), d_flags, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st), "D2H flags");
@@ -651,26 +743,10 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             const int64_t m = static_cast<int64_t>(rr.size());
             BlockDesc* d_rdesc = upload(ctx, "rdesc", rdesc.data(), rdesc.size());
             int32_t* d_rr = upload(ctx, "rr", rr.data(), rr.size());
-            double2* d_R64 = ctx->buf("R64").as<double2>(static_cast<size_t>(m) * L64.SLOTS);
+            double2* d_Rr = ctx->buf("Rr").as<double2>(static_cast<size_t>(m) * L64.SLOTS);
             double* d_re0 = ctx->buf("re0").as<double>(static_cast<size_t>(m));
             double* d_rimax = ctx->buf("rimax").as<double>(static_cast<size_t>(m));
-            K1Args k{};
-            k.T = T;
-            k.Lh = g.Lh;
-            k.Lw = g.Lw;
-            k.n = static_cast<int32_t>(m);
-            k.blocks = d_rdesc;
-            k.fr = fr;
-            k.wcls = d_wcls;
-            k.mode = K1_PACKED;
-            k.path = PATH_F64_STRICT;
-            k.seg = seg64;
-            k.out = d_R64;
-            k.energy = d_re0;
-            k.init_max = d_rimax;
-            k.twid = d_twf;
-            ck(k1_launch(k, st), "K1 rerun spectra");
-            ++ctx->launches;
+            k1_packed(d_rdesc, m, PATH_F64_STRICT, seg64, 1, d_Rr, d_re0, d_rimax);
             std::vector<Tile> tl = make_tiles(0, m, rdesc, k2_groups_per_cta(T, PATH_F64_STRICT));
             Tile* d_rt = upload(ctx, "rtiles", tl.data(), tl.size());
             K2Args a = base_args();
@@ -680,19 +756,18 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             a.tiles = d_rt;
             a.order = d_rr;
             a.blocks = d_rdesc;
-            a.rin = d_R64;
+            a.rin = d_Rr;
             a.wimg = d_wimg64;
             a.wimg_stride = static_cast<int64_t>(T) * sr64;
             a.energy0 = d_re0;
             a.init_energy = d_re0;
             a.init_max = d_rimax;
-            a.conv_out = d_conv;
-            a.flags = nullptr;
+            a.rec_global = 0;  // smem records (or the per-block global scratch when I > cap)
             ck(k2_launch(a, static_cast<int32_t>(tl.size()), st), "K2 rerun");
             ++ctx->launches;
         }
     }
-    ck(cudaEventRecord(ctx->ev[2], st), "event");
+    ck(cudaEventRecord(ctx->ev[3], st), "event");
     {
         std::vector<int32_t> conv(static_cast<size_t>(n));
         if (n)
@@ -705,6 +780,9 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
     out.init_ms = ms;
     ck(cudaEventElapsedTime(&ms, ctx->ev[1], ctx->ev[2]), "elapsed");
     out.iter_ms = ms;
+    ck(cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]), "elapsed");
+    out.rerun_ms = ms;
+    out.iter_ms += out.rerun_ms;
     out.total_ms = out.init_ms + out.iter_ms;
     return out;
 }
@@ -720,6 +798,8 @@ void fill_report(fofse_report* rep, const RunOut& ro, int64_t n, int64_t ncls, d
     rep->init_ms = ro.init_ms;
     rep->iterate_ms = ro.iter_ms;
     rep->total_ms = ro.total_ms;
+    rep->rerun_ms = ro.rerun_ms;
+    rep->fp64_head = ro.head;
     rep->mean_seconds_per_block = n ? ro.total_ms * 1e-3 / static_cast<double>(n) : 0.0;
     rep->kernel_launches = launches;
     // pipeline.cpp:252-260 + grid.cpp:117-120
@@ -779,6 +859,7 @@ void fofse_params_default(fofse_params* p) {
     p->record_traces = 0;
     p->precision = FOFSE_PREC_FP64;
     p->guard_tau = -1.0;
+    p->fp64_head = -1;
 }
 
 int fofse_create(int32_t device, fofse_ctx** out) {
@@ -864,6 +945,41 @@ int fofse_conceal_f64(fofse_ctx* ctx, const double* image, int32_t width, int32_
         for (double v : sq) tot += v;
         fill_report(report, ro, n, static_cast<int64_t>(job.cls_labels.size()), tot,
                     n * static_cast<int64_t>(bh) * bw, ctx->launches - l0);
+    });
+}
+
+// Diagnostics: fofse_conceal_f64 plus, per block and selection, the relative
+// gap between the two largest canonical |R|^2 seen by the fp32 paths (the
+// quantity the near-tie guard thresholds). Not part of the reference API.
+int fofse_diag_conceal_f64(fofse_ctx* ctx, const double* image, int32_t width, int32_t height,
+                           const fofse_rect* blocks, int64_t n, int32_t bh, int32_t bw,
+                           const fofse_params* params, double* restored, fofse_record* traces,
+                           int32_t* trace_counts, float* gap_trace) {
+    return guarded([&] {
+        if (!ctx || !image || !restored || (n && !blocks) || !traces || !trace_counts || !gap_trace)
+            throw std::invalid_argument("diag_conceal: NULL argument");
+        const Cfg cfg = to_cfg(params);
+        const int64_t offs[2] = {0, n};
+        Job job = make_image_job(cfg, width, height, bh, bw, blocks, offs, 1);
+        ctx->activate();
+        const size_t npx = static_cast<size_t>(width) * height;
+        double* d_img = ctx->buf("img64").as<double>(npx);
+        ck(cudaMemcpyAsync(d_img, image, npx * sizeof(double), cudaMemcpyHostToDevice, ctx->stream), "H2D");
+        double* d_sq = ctx->buf("sq").as<double>(static_cast<size_t>(std::max<int64_t>(n, 1)));
+        const size_t nr = static_cast<size_t>(n) * std::max(cfg.iterations, 1);
+        fofse_record* d_tr = ctx->buf("trace").as<fofse_record>(nr);
+        int32_t* d_tc = ctx->buf("trace_count").as<int32_t>(static_cast<size_t>(std::max<int64_t>(n, 1)));
+        float* d_gap = ctx->buf("gap").as<float>(nr);
+        ck(cudaMemsetAsync(d_gap, 0, nr * sizeof(float), ctx->stream), "memset");
+        fofse::Frames fr{d_img, d_img, fofse::SRC_F64, width, height, static_cast<int64_t>(npx)};
+        if (n > 0) run_job(ctx, job, cfg, fr, fofse::SYN_IMAGE, d_sq, nullptr, d_tr, d_tc, d_gap);
+        ck(cudaMemcpyAsync(restored, d_img, npx * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        if (n) {
+            ck(cudaMemcpyAsync(traces, d_tr, sizeof(fofse_record) * nr, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+            ck(cudaMemcpyAsync(trace_counts, d_tc, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+            ck(cudaMemcpyAsync(gap_trace, d_gap, sizeof(float) * nr, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        }
+        ck(cudaStreamSynchronize(ctx->stream), "sync");
     });
 }
 
@@ -1121,11 +1237,11 @@ int fofse_spectral_init(fofse_ctx* ctx, const double* f, const uint8_t* labels,
     });
 }
 
-int fofse_spectral_iterate(fofse_ctx* ctx, int32_t t, int64_t n, int32_t wh, int32_t ww,
+static int spectral_iterate_impl(fofse_ctx* ctx, int32_t t, int64_t n, int32_t wh, int32_t ww,
                            double* rw, const double* wspec, double* g, const double* w0,
                            double* energy, const double* e_init, const double* imax, int32_t* nu,
                            int32_t* conv, double gamma, int32_t iterations, int32_t precision,
-                           fofse_record* traces, int32_t* trace_counts) {
+                           fofse_record* traces, int32_t* trace_counts, float* gap_trace) {
     return guarded([&] {
         using namespace fofse;
         if (!ctx || (n && (!rw || !wspec || !g || !w0 || !energy || !e_init || !imax || !nu || !conv)))
@@ -1252,7 +1368,15 @@ int fofse_spectral_iterate(fofse_ctx* ctx, int32_t t, int64_t n, int32_t wh, int
         a.twid_inv = d_twi;
         a.rec_u_g = d_rec_u;
         a.rec_c_g = d_rec_c;
+        float* d_gap = nullptr;
+        if (gap_trace && iterations > 0) {
+            d_gap = ctx->buf("gap").as<float>(static_cast<size_t>(n) * iterations);
+            ck(cudaMemsetAsync(d_gap, 0, sizeof(float) * n * iterations, st), "memset");
+        }
+        a.gap_trace = d_gap;
         if (n) ck(k2_launch(a, static_cast<int32_t>(n), st), "K2 spectral iterate");
+        if (d_gap)
+            ck(cudaMemcpyAsync(gap_trace, d_gap, sizeof(float) * n * iterations, cudaMemcpyDeviceToHost, st), "D2H");
         std::vector<char> Ro(static_cast<size_t>(n) * rbytes);
         if (n) {
             ck(cudaMemcpyAsync(Ro.data(), d_Ro, Ro.size(), cudaMemcpyDeviceToHost, st), "D2H");
@@ -1296,6 +1420,25 @@ int fofse_spectral_iterate(fofse_ctx* ctx, int32_t t, int64_t n, int32_t wh, int
             }
         }
     });
+}
+
+int fofse_spectral_iterate(fofse_ctx* ctx, int32_t t, int64_t n, int32_t wh, int32_t ww,
+                           double* rw, const double* wspec, double* g, const double* w0,
+                           double* energy, const double* e_init, const double* imax, int32_t* nu,
+                           int32_t* conv, double gamma, int32_t iterations, int32_t precision,
+                           fofse_record* traces, int32_t* trace_counts) {
+    return spectral_iterate_impl(ctx, t, n, wh, ww, rw, wspec, g, w0, energy, e_init, imax, nu, conv,
+                                 gamma, iterations, precision, traces, trace_counts, nullptr);
+}
+
+int fofse_diag_spectral_iterate(fofse_ctx* ctx, int32_t t, int64_t n, int32_t wh, int32_t ww,
+                                double* rw, const double* wspec, double* g, const double* w0,
+                                double* energy, const double* e_init, const double* imax,
+                                int32_t* nu, int32_t* conv, double gamma, int32_t iterations,
+                                int32_t precision, fofse_record* traces, int32_t* trace_counts,
+                                float* gap_trace) {
+    return spectral_iterate_impl(ctx, t, n, wh, ww, rw, wspec, g, w0, energy, e_init, imax, nu, conv,
+                                 gamma, iterations, precision, traces, trace_counts, gap_trace);
 }
 
 int fofse_spectral_synthesize(fofse_ctx* ctx, int32_t t, int64_t n, const double* g, int32_t h,

@@ -1,0 +1,126 @@
+// kcommon.cuh — device helpers shared by the FOFSE kernels (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "kernels.h"
+#include "layout.h"
+
+namespace fofse {
+
+// ----------------------------------------------------------------------------
+// small helpers
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(int id, int count) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+// TMA bulk copy global -> shared, completion on an mbarrier (SASS: UBLKCP).
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(phase)
+            : "memory");
+    }
+}
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 conjd(double2 a) { return make_double2(a.x, -a.y); }
+
+template <int T>
+struct Log2 {
+    static constexpr int v = T <= 1 ? 0 : 1 + Log2<T / 2>::v;
+};
+template <>
+struct Log2<1> {
+    static constexpr int v = 0;
+};
+
+template <int T>
+__device__ __forceinline__ int bitrev(int x) {
+    return static_cast<int>(__brev(static_cast<unsigned>(x)) >> (32 - Log2<T>::v));
+}
+
+// e^{+j pi x / T} for the rotation phase phi(k) = pi (k1 (Lh-1) + k2 (Lw-1)) / T.
+template <int T>
+__device__ __forceinline__ double2 phase_pos(long long num) {
+    const long long m = ((num % (2 * T)) + 2 * T) % (2 * T);
+    double s, c;
+    sincospi(static_cast<double>(m) / T, &s, &c);
+    return make_double2(c, s);
+}
+
+// In-place radix-2 DIT over `nvec` length-T vectors (input bit-reversed,
+// output natural order). Vector v starts at buf + v*vstride, elements at
+// stride estride. tw[k] = e^{-j 2 pi k / T}; dir = +1 conjugates it.
+template <int T>
+__device__ void fft_inplace(double2* buf, int nvec, int vstride, int estride, const double2* tw,
+                            int dir) {
+    constexpr int HALFT = T / 2;
+    const int nb = nvec * HALFT;
+    for (int len = 2; len <= T; len <<= 1) {
+        const int half = len >> 1;
+        const int twstep = T / len;
+        for (int t = threadIdx.x; t < nb; t += blockDim.x) {
+            const int v = t / HALFT, b = t % HALFT;
+            const int grp = b / half, k = b % half;
+            const int i = grp * len + k, j = i + half;
+            double2 w = tw[k * twstep];
+            if (dir > 0) w.y = -w.y;
+            double2* x = buf + (size_t)v * vstride;
+            const double2 xi = x[i * estride], xj = x[j * estride];
+            const double2 wx = cmul(w, xj);
+            x[i * estride] = cadd(xi, wx);
+            x[j * estride] = csub(xi, wx);
+        }
+        __syncthreads();
+    }
+}
+
+template <class V>
+__device__ __forceinline__ V block_reduce(V v, V* red, bool is_max) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const V u = __shfl_xor_sync(0xffffffffu, v, o);
+        v = is_max ? (u > v ? u : v) : v + u;
+    }
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    V r = red[0];
+    for (int w = 1; w < nw; ++w) r = is_max ? (red[w] > r ? red[w] : r) : r + red[w];
+    return r;
+}
+
+}  // namespace fofse

@@ -14,125 +14,11 @@
 
 #include <climits>
 
+#include "kcommon.cuh"
 #include "kernels.h"
 #include "layout.h"
 
 namespace fofse {
-
-// ----------------------------------------------------------------------------
-// small helpers
-// ----------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void named_bar_sync(int id, int count) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
-__device__ __forceinline__ void named_bar_arrive(int id, int count) {
-    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
-
-// TMA bulk copy global -> shared, completion on an mbarrier (SASS: UBLKCP).
-__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-    uint32_t done = 0;
-    while (!done) {
-        asm volatile(
-            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-            : "=r"(done)
-            : "r"(smem_u32(bar)), "r"(phase)
-            : "memory");
-    }
-}
-
-__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
-__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
-    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
-}
-__device__ __forceinline__ double2 conjd(double2 a) { return make_double2(a.x, -a.y); }
-
-template <int T>
-struct Log2 {
-    static constexpr int v = T <= 1 ? 0 : 1 + Log2<T / 2>::v;
-};
-template <>
-struct Log2<1> {
-    static constexpr int v = 0;
-};
-
-template <int T>
-__device__ __forceinline__ int bitrev(int x) {
-    return static_cast<int>(__brev(static_cast<unsigned>(x)) >> (32 - Log2<T>::v));
-}
-
-// e^{+j pi x / T} for the rotation phase phi(k) = pi (k1 (Lh-1) + k2 (Lw-1)) / T.
-template <int T>
-__device__ __forceinline__ double2 phase_pos(long long num) {
-    const long long m = ((num % (2 * T)) + 2 * T) % (2 * T);
-    double s, c;
-    sincospi(static_cast<double>(m) / T, &s, &c);
-    return make_double2(c, s);
-}
-
-// In-place radix-2 DIT over `nvec` length-T vectors (input bit-reversed,
-// output natural order). Vector v starts at buf + v*vstride, elements at
-// stride estride. tw[k] = e^{-j 2 pi k / T}; dir = +1 conjugates it.
-template <int T>
-__device__ void fft_inplace(double2* buf, int nvec, int vstride, int estride, const double2* tw,
-                            int dir) {
-    constexpr int HALFT = T / 2;
-    const int nb = nvec * HALFT;
-    for (int len = 2; len <= T; len <<= 1) {
-        const int half = len >> 1;
-        const int twstep = T / len;
-        for (int t = threadIdx.x; t < nb; t += blockDim.x) {
-            const int v = t / HALFT, b = t % HALFT;
-            const int grp = b / half, k = b % half;
-            const int i = grp * len + k, j = i + half;
-            double2 w = tw[k * twstep];
-            if (dir > 0) w.y = -w.y;
-            double2* x = buf + (size_t)v * vstride;
-            const double2 xi = x[i * estride], xj = x[j * estride];
-            const double2 wx = cmul(w, xj);
-            x[i * estride] = cadd(xi, wx);
-            x[j * estride] = csub(xi, wx);
-        }
-        __syncthreads();
-    }
-}
-
-template <class V>
-__device__ __forceinline__ V block_reduce(V v, V* red, bool is_max) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        const V u = __shfl_xor_sync(0xffffffffu, v, o);
-        v = is_max ? (u > v ? u : v) : v + u;
-    }
-    __syncthreads();
-    if (lane == 0) red[warp] = v;
-    __syncthreads();
-    V r = red[0];
-    for (int w = 1; w < nw; ++w) r = is_max ? (red[w] > r ? red[w] : r) : r + red[w];
-    return r;
-}
 
 // ----------------------------------------------------------------------------
 // K1 — window gather + w*f + batched real-input 2-D FFT (fp64)
@@ -278,7 +164,7 @@ __global__ void __launch_bounds__(256) k1_kernel(K1Args a) {
             vmax = fmax(vmax, hypot(v.x, v.y));
         }
     } else {
-        const BinLayout L = BinLayout::make(T, a.seg);
+        const BinLayout L = BinLayout::make(T, a.seg, a.spt > 0 ? a.spt : 1);
         const bool rotate = a.path == PATH_F32_REAL;
         for (int s = threadIdx.x; s < L.SLOTS; s += blockDim.x) {
             const int j = s / L.NT, tid = s % L.NT;
@@ -468,10 +354,12 @@ __global__ void __launch_bounds__(K2Cfg<T, PATH>::THREADS) k2_kernel(K2Args a) {
 
         int* rec_u = rec_u_s;
         double2* rec_c = rec_c_s;
-        if (a.iterations > Cf::REC_CAP) {
-            rec_u = a.rec_u_g + (size_t)b * a.iterations;
-            rec_c = a.rec_c_g + (size_t)b * a.iterations;
+        const int rstride = a.rec_stride > 0 ? a.rec_stride : a.iterations;
+        if (a.rec_global || a.iterations > Cf::REC_CAP) {
+            rec_u = a.rec_u_g + (size_t)b * rstride;
+            rec_c = a.rec_c_g + (size_t)b * rstride;
         }
+        const int tstride = a.trace_stride > 0 ? a.trace_stride : a.iterations;
 
         // controller state (meaningful in warp 0)
         double energy = a.energy0[pos];
@@ -479,7 +367,9 @@ __global__ void __launch_bounds__(K2Cfg<T, PATH>::THREADS) k2_kernel(K2Args a) {
         const double imax = a.init_max[pos];
         int nu = a.nu0 ? a.nu0[pos] : 0;
         int conv = a.conv0 ? a.conv0[pos] : 0;
-        int nrec = 0, flagged = 0, ntrace = 0;
+        // records: global phases index them by the selection count nu
+        int nrec = a.rec_global ? nu : 0, flagged = 0;
+        int ntrace = a.trace_from_nu0 ? nu : 0;
 
         for (int it = 0; it < a.iterations && !conv; ++it) {
             // ---- local argmax over owned canonical bins (strict '>' in index order) ----
@@ -644,7 +534,7 @@ __global__ void __launch_bounds__(K2Cfg<T, PATH>::THREADS) k2_kernel(K2Args a) {
                     p.c_im = upd_im;
                     if (lane == 0) {
                         // synthesis record: pair factor folded in (2 Re(c phi) / Re(c phi))
-                        if (nrec < a.iterations) {
+                        if (nrec < (a.rec_global ? rstride : a.iterations)) {
                             rec_u[nrec] = (u1 << 16) | u2;
                             rec_c[nrec] = self ? make_double2(c_re, 0.0) : make_double2(2.0 * c_re, 2.0 * c_im);
                         }
@@ -662,8 +552,11 @@ __global__ void __launch_bounds__(K2Cfg<T, PATH>::THREADS) k2_kernel(K2Args a) {
                             r.weighted_energy = energy;
                             r.degenerate = 0;
                             r.pad1 = 0;
-                            a.trace[(size_t)b * a.iterations + ntrace] = r;
+                            a.trace[(size_t)b * tstride + ntrace] = r;
                         }
+                        if (a.gap_trace)
+                            a.gap_trace[(size_t)b * tstride + ntrace] =
+                                (float)(M2 > 0.0 ? (M - M2) / M : 1.0);
                         if (a.gspec) {
                             // engine_spectral.cpp:127-129: G[u] += T^2 c; G[v] += T^2 conj(c)
                             const double scale = (double)T * T;
@@ -782,11 +675,12 @@ __global__ void __launch_bounds__(K2Cfg<T, PATH>::THREADS) k2_kernel(K2Args a) {
             gs->prm.nrec = nrec;
             gs->prm.flagged = flagged;
             gs->prm.conv = conv;
-            if (a.energy_out) a.energy_out[b] = energy;
-            if (a.nu_out) a.nu_out[b] = nu;
-            if (a.conv_out) a.conv_out[b] = conv;
+            const int sb = a.state_by_pos ? pos : b;
+            if (a.energy_out) a.energy_out[sb] = energy;
+            if (a.nu_out) a.nu_out[sb] = nu;
+            if (a.conv_out) a.conv_out[sb] = conv;
             if (a.flags) a.flags[b] = flagged;
-            if (a.trace_count) a.trace_count[b] = ntrace;
+            if (a.trace_count) a.trace_count[b] = ntrace;  // == nu when trace_from_nu0
         }
         if constexpr (NW == 1)
             __syncwarp();

@@ -58,6 +58,7 @@ struct K1Args {
     int32_t mode;              // K1_PACKED, K1_FULL, K1_CLASS
     int32_t path;              // IterPath for K1_PACKED (precision + rotation)
     int32_t seg;               // layout SEG of the K2 path
+    int32_t spt;               // layout segments per thread (0 = 1)
     void* out;                 // packed R / full spectrum (double2) / W images
     double* energy;            // per block sum w f^2 (packed/full modes)
     double* init_max;          // per block max |R| (packed/full modes)
@@ -107,6 +108,21 @@ struct K2Args {
     const double2* twid_inv;    // e^{+j 2 pi k / T}
     int32_t* rec_u_g;           // global record scratch [block][iterations] when
     double2* rec_c_g;           //   iterations exceed the shared-memory capacity
+    float* gap_trace;           // diagnostics: [block][iterations] top-2 relative gap
+    const double2* ptab;        // e^{-j pi m / T}, m < 2T (rotated-frame phase P[u])
+    int32_t rec_global;         // records in rec_*_g at index nu-1 (resumable phases)
+    int32_t rec_stride;         // record slots per block in rec_*_g (0 = iterations)
+    int32_t trace_from_nu0;     // trace index continues from nu0 (multi-phase calls)
+    int32_t trace_stride;       // trace records per block (0 = iterations)
+    int32_t state_by_pos;       // energy_out / nu_out / conv_out indexed by position
+};
+
+struct CvtArgs {
+    int32_t T, Lh, Lw, n;
+    const double2* in;          // packed fp64 residuals (strict layout: seg_of(T, F64), SPT 1)
+    float2* out;                // packed fp32 residuals (K2v2 layout)
+    int32_t out_seg, out_spt;
+    int32_t rotate;             // apply the rotated-frame phase e^{+j phi(k)} (PATH_F32_REAL)
 };
 enum { SYN_NONE = 0, SYN_IMAGE = 1, SYN_WINDOW = 2 };
 
@@ -116,6 +132,11 @@ int k2_launch(const K2Args& a, int32_t ntiles, cudaStream_t s);
 // Batched in-place complex fp64 2-D transform of n T x T spectra (dir -1/+1).
 int fft2d_launch(double2* data, int64_t n, int32_t T, int32_t dir, const double2* twid_fwd,
                  cudaStream_t s);
+
+// K2v2: single-warp fp32 iteration kernel (T <= 64); convert fp64 head state.
+int k2v2_launch(const K2Args& a, int32_t ntiles, cudaStream_t s);
+int k2v2_warps_per_cta();
+int cvt_launch(const CvtArgs& a, cudaStream_t s);
 
 // Row stride of W images and the SEG used by a path (same on host/device).
 int seg_of(int T, int path);

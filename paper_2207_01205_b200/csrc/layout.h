@@ -35,21 +35,24 @@ FOFSE_HDC int seg_for(int t, int fp64) {
 }
 
 struct BinLayout {
-    int T, SEG, HT, QN, NT, SR, SLOTS;
-    FOFSE_HD static BinLayout make(int t, int seg) {
+    // T: transform size; SEG: bins per segment; SPT: segments per thread;
+    // NT: threads per block-group; SLOTS: packed slots per block.
+    int T, SEG, SPT, HT, QN, NT, SR, SLOTS;
+    FOFSE_HD static BinLayout make(int t, int seg, int spt = 1) {
         BinLayout l;
         l.T = t;
         l.SEG = seg;
+        l.SPT = spt;
         l.HT = t / 2;
         l.QN = t / seg;
-        l.NT = l.HT * l.QN;
+        l.NT = l.HT * l.QN / spt;
         l.SR = t + seg + 1;
-        l.SLOTS = (seg + 1) * l.NT;
+        l.SLOTS = spt * (seg + 1) * l.NT;
         return l;
     }
-    // Segment of thread `tid` (< NT): row k1, first column c0, extra bin flag.
-    FOFSE_HD void segment(int tid, int* k1, int* c0, int* extra) const {
-        const int q = tid / HT, vr = tid % HT;
+    // Segment q (0 <= q < QN) of virtual row vr: row k1, first column c0,
+    // extra-bin flag (the self-conjugate bin (k1, T/2) follows the segment).
+    FOFSE_HD void segment_q(int q, int vr, int* k1, int* c0, int* extra) const {
         if (vr == 0) {
             const int half = QN / 2;
             if (q < half) {
@@ -67,16 +70,54 @@ struct BinLayout {
             *extra = 0;
         }
     }
-    // Bin (k1, k2) held in slot (j, tid); returns 0 for an unused extra slot.
-    FOFSE_HD int slot_bin(int j, int tid, int* k1, int* k2) const {
+    // Segment s (< SPT) of thread tid (< NT).
+    FOFSE_HD void thread_segment(int tid, int s, int* k1, int* c0, int* extra) const {
+        segment_q((tid / HT) * SPT + s, tid % HT, k1, c0, extra);
+    }
+    // SPT == 1 form used by the multi-warp kernel.
+    FOFSE_HD void segment(int tid, int* k1, int* c0, int* extra) const {
+        thread_segment(tid, 0, k1, c0, extra);
+    }
+    // Bin held in slot i (< SPT*(SEG+1)) of thread tid; packed address i*NT + tid.
+    // Returns 0 for an unused extra slot.
+    FOFSE_HD int slot_bin(int i, int tid, int* k1, int* k2) const {
+        const int s = i / (SEG + 1), j = i % (SEG + 1);
         int r, c, ex;
-        segment(tid, &r, &c, &ex);
+        thread_segment(tid, s, &r, &c, &ex);
         if (j == SEG && !ex) return 0;
         *k1 = r;
         *k2 = c + j;
         return 1;
     }
 };
+
+// Inverse of slot_bin for a canonical bin: slot i and thread tid.
+FOFSE_HD void bin_slot(const BinLayout& L, int k1, int k2, int* i, int* tid) {
+    int q, j, vr;
+    if (k1 > 0 && k1 < L.HT) {
+        vr = k1;
+        q = k2 / L.SEG;
+        j = k2 % L.SEG;
+    } else {
+        vr = 0;
+        const int half = L.QN / 2;
+        if (k2 < L.HT) {
+            q = (k1 == 0 ? 0 : half) + k2 / L.SEG;
+            j = k2 % L.SEG;
+        } else {  // the self-conjugate bin (k1, T/2): extra slot of the row's last segment
+            q = (k1 == 0 ? half : L.QN) - 1;
+            j = L.SEG;
+        }
+    }
+    *tid = (q / L.SPT) * L.HT + vr;
+    *i = (q % L.SPT) * (L.SEG + 1) + j;
+}
+
+// Layout of the single-warp fp32 iteration kernel (K2v2): one warp owns a
+// whole lost block for T <= 64 (T = 64: 32 lanes x 2 segments x 32 bins).
+FOFSE_HDC int v2_seg(int t) { return t <= 8 ? 4 : (t <= 16 ? 8 : (t <= 32 ? 16 : 32)); }
+FOFSE_HDC int v2_spt(int t) { return t == 64 ? 2 : 1; }
+FOFSE_HDC bool v2_supported(int t) { return t >= 8 && t <= 64; }
 
 // Canonical representative test (basis.cpp:44-47).
 FOFSE_HD bool is_canonical(int t, int k1, int k2) {

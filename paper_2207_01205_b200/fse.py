@@ -73,6 +73,7 @@ class ConcealConfig:
     record_traces: bool = False
     precision: str = "fp64"
     guard_tau: float = -1.0
+    fp64_head: int = -1
 
     def validate(self):
         """pipeline.cpp:34-38 + engine_spatial.cpp:8-15 (same messages)."""
@@ -104,6 +105,7 @@ class ConcealConfig:
             raise ValueError("config: precision must be 'fp64' or 'fp32'")
         p.precision = _PRECS[self.precision]
         p.guard_tau = self.guard_tau
+        p.fp64_head = self.fp64_head
         return p
 
 
