@@ -134,9 +134,10 @@ struct DevBuf {
 struct fofse_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t side = nullptr;  // concurrent small launches (asymmetric-mask blocks)
     bool own_stream = false;
     std::map<std::string, DevBuf> bufs;
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     int64_t launches = 0;
 
     DevBuf& buf(const std::string& name) { return bufs[name]; }
@@ -422,10 +423,11 @@ std::vector<double2> twiddles(int T, int sign) {
 }
 
 template <class T>
-T* upload(fofse_ctx* ctx, const std::string& name, const T* host, size_t count) {
+T* upload(fofse_ctx* ctx, const std::string& name, const T* host, size_t count,
+          cudaStream_t s = nullptr) {
     T* d = ctx->buf(name).as<T>(count);
     if (count)
-        ck(cudaMemcpyAsync(d, host, count * sizeof(T), cudaMemcpyHostToDevice, ctx->stream), "H2D");
+        ck(cudaMemcpyAsync(d, host, count * sizeof(T), cudaMemcpyHostToDevice, s ? s : ctx->stream), "H2D");
     return d;
 }
 
@@ -519,7 +521,8 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
     // from seg_for(T, 0); K2v2 uses v2_seg(T) — equal for every T).
     double2* d_wimg64 = ctx->buf("wimg64").as<double2>(static_cast<size_t>(ncls) * T * sr64);
     float2* d_wimg32 = fp32 ? ctx->buf("wimg32").as<float2>(static_cast<size_t>(ncls) * T * sr32) : nullptr;
-    float* d_vimg32 = fp32 ? ctx->buf("vimg32").as<float>(static_cast<size_t>(ncls) * T * sr32) : nullptr;
+    const size_t vimg_elems = v2 ? 2 * static_cast<size_t>(T) * v2_srv(T) : static_cast<size_t>(T) * sr32;
+    float* d_vimg32 = fp32 ? ctx->buf("vimg32").as<float>(static_cast<size_t>(ncls) * vimg_elems) : nullptr;
     double* d_w0 = ctx->buf("w0").as<double>(static_cast<size_t>(ncls));
     {
         K1Args a{};
@@ -532,6 +535,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         a.wimg64 = d_wimg64;
         a.wimg32 = d_wimg32;
         a.vimg32 = d_vimg32;
+        a.vpairs = v2 ? 1 : 0;
         a.w0 = d_w0;
         a.twid = d_twf;
         ck(k1_launch(a, st), "K1 class spectra");
@@ -573,7 +577,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         d_rec_c = ctx->buf("rec_c").as<double2>(static_cast<size_t>(n) * I);
     }
     auto k1_packed = [&](const BlockDesc* descs, int64_t cnt, int path, int seg, int spt, void* outp,
-                         double* e, double* m) {
+                         double* e, double* m, int soa = 0, int64_t stride = 0) {
         K1Args a{};
         a.T = T;
         a.Lh = g.Lh;
@@ -586,6 +590,8 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         a.path = path;
         a.seg = seg;
         a.spt = spt;
+        a.soa = soa;
+        a.out_stride = stride;
         a.out = outp;
         a.energy = e;
         a.init_max = m;
@@ -637,12 +643,18 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         d_R64 = ctx->buf("R64").as<char>(static_cast<size_t>(n) * sizeof(double2) * L64.SLOTS);
         k1_packed(d_sorted, n, PATH_F64_STRICT, seg64, 1, d_R64, d_e0, d_imax);
     }
-    if (fp32) d_R32 = ctx->buf("R32").as<char>(static_cast<size_t>(n) * sizeof(float2) * L32.SLOTS);
+    // fp32 residuals: AoS float2 slots (complex path, T = 128) or, for the K2v2
+    // real path, SoA bin pairs; one common per-block stride (floats)
+    auto soa_of = [&](int path) { return (v2 && path == PATH_F32_REAL) ? 1 : 0; };
+    auto spt_of = [&](int path) { return (v2 && path == PATH_F32_REAL) ? v2_real_spt(T) : spt32; };
+    const BinLayout L32r = BinLayout::make(T, seg32, spt_of(PATH_F32_REAL));
+    const int64_t s32 = static_cast<int64_t>(std::max(packed32_floats(L32, 0), packed32_floats(L32r, soa_of(PATH_F32_REAL))));
+    if (fp32) d_R32 = ctx->buf("R32").as<char>(static_cast<size_t>(n) * sizeof(float) * s32);
     if (fp32 && head == 0)
         for (const Range& r : ranges)
-            k1_packed(d_sorted + r.begin, r.end - r.begin, r.path, seg32, spt32,
-                      d_R32 + static_cast<size_t>(r.begin) * sizeof(float2) * L32.SLOTS, d_e0 + r.begin,
-                      d_imax + r.begin);
+            k1_packed(d_sorted + r.begin, r.end - r.begin, r.path, seg32, spt_of(r.path),
+                      d_R32 + static_cast<size_t>(r.begin) * sizeof(float) * s32, d_e0 + r.begin,
+                      d_imax + r.begin, soa_of(r.path), s32);
     ck(cudaEventRecord(ctx->ev[1], st), "event");
 
     // ---- phase B: fp64 (strict reference op order) ----
@@ -680,8 +692,16 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         ++ctx->launches;
     }
     // ---- phase C: fp32 fast mode ----
+    // Asymmetric-mask blocks (few, image borders) run on the side stream,
+    // concurrently with the symmetric bulk on the main stream.
     if (fp32) {
+        ck(cudaEventRecord(ctx->ev[4], st), "event");
+        ck(cudaStreamWaitEvent(ctx->side, ctx->ev[4], 0), "wait");
+        bool used_side = false;
         for (const Range& r : ranges) {
+            const bool on_side = r.path == PATH_F32_COMPLEX && ranges.size() > 1;
+            cudaStream_t rs = on_side ? ctx->side : st;
+            used_side |= on_side;
             if (head > 0) {
                 CvtArgs c{};
                 c.T = T;
@@ -689,24 +709,27 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
                 c.Lw = g.Lw;
                 c.n = static_cast<int32_t>(r.end - r.begin);
                 c.in = reinterpret_cast<const double2*>(d_R64) + static_cast<size_t>(r.begin) * L64.SLOTS;
-                c.out = reinterpret_cast<float2*>(d_R32) + static_cast<size_t>(r.begin) * L32.SLOTS;
+                c.out = reinterpret_cast<float2*>(d_R32 + static_cast<size_t>(r.begin) * sizeof(float) * s32);
                 c.out_seg = seg32;
-                c.out_spt = spt32;
+                c.out_spt = spt_of(r.path);
                 c.rotate = r.path == PATH_F32_REAL;
-                ck(cvt_launch(c, st), "convert head state");
+                c.soa = soa_of(r.path);
+                c.out_stride = s32;
+                ck(cvt_launch(c, rs), "convert head state");
                 ++ctx->launches;
             }
             const int ng = v2 ? k2v2_warps_per_cta() : k2_groups_per_cta(T, r.path);
             std::vector<Tile> tl = tiles_for(r.begin, r.end, ng);
-            Tile* d_tl = upload(ctx, r.path == PATH_F32_REAL ? "tilesR" : "tilesC", tl.data(), tl.size());
+            Tile* d_tl = upload(ctx, r.path == PATH_F32_REAL ? "tilesR" : "tilesC", tl.data(), tl.size(), rs);
             K2Args a = base_args();
             a.path = r.path;
             a.seg = seg32;
             a.tau = effective_tau(cfg, head);
             a.tiles = d_tl;
             a.rin = d_R32;
+            a.rin_stride = v2 ? s32 : 0;
             a.wimg = r.path == PATH_F32_REAL ? (const void*)d_vimg32 : (const void*)d_wimg32;
-            a.wimg_stride = static_cast<int64_t>(T) * sr32;
+            a.wimg_stride = r.path == PATH_F32_REAL ? static_cast<int64_t>(vimg_elems) : static_cast<int64_t>(T) * sr32;
             a.flags = d_flags;
             a.rec_global = 1;
             a.iterations = I - head;
@@ -716,10 +739,14 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
                 a.nu0 = d_nu;
                 a.conv0 = d_cvh;
             }
-            ck(v2 ? k2v2_launch(a, static_cast<int32_t>(tl.size()), st)
-                  : k2_launch(a, static_cast<int32_t>(tl.size()), st),
+            ck(v2 ? k2v2_launch(a, static_cast<int32_t>(tl.size()), rs)
+                  : k2_launch(a, static_cast<int32_t>(tl.size()), rs),
                "K2 fp32");
             ++ctx->launches;
+        }
+        if (used_side) {
+            ck(cudaEventRecord(ctx->ev[5], ctx->side), "event");
+            ck(cudaStreamWaitEvent(st, ctx->ev[5], 0), "wait");
         }
     }
     ck(cudaEventRecord(ctx->ev[2], st), "event");
@@ -873,6 +900,7 @@ int fofse_create(int32_t device, fofse_ctx** out) {
         ctx->device = device;
         ctx->activate();
         ck(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        ck(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking), "cudaStreamCreate");
         ctx->own_stream = true;
         *out = ctx.release();
     });
@@ -885,7 +913,9 @@ void fofse_destroy(fofse_ctx* ctx) {
     for (auto& kv : ctx->bufs) kv.second.release();
     for (auto& e : ctx->ev)
         if (e) cudaEventDestroy(e);
+    if (ctx->side) cudaStreamSynchronize(ctx->side);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+    if (ctx->side) cudaStreamDestroy(ctx->side);
     delete ctx;
 }
 

@@ -123,4 +123,27 @@ __device__ __forceinline__ V block_reduce(V v, V* red, bool is_max) {
     return r;
 }
 
+// Store bin slot i of `lane` into a packed fp32 residual. AoS: float2 at
+// i*NT + lane. SoA (K2v2 real path): bins (2p, 2p+1) of a segment share the
+// float4 (re_a, re_b, im_a, im_b) at q*NT + lane, q = seg*SEG/2 + p; the
+// segment's extra bin has its own float4 (re, 0, im, 0) at q = SPT*SEG/2 + seg.
+__device__ __forceinline__ void put_packed32(float* out, const BinLayout& L, int soa, int i, int lane,
+                                             float re, float im) {
+    if (!soa) {
+        reinterpret_cast<float2*>(out)[(size_t)i * L.NT + lane] = make_float2(re, im);
+        return;
+    }
+    const int s = i / (L.SEG + 1), j = i % (L.SEG + 1);
+    if (j < L.SEG) {
+        float* f = out + ((size_t)(s * (L.SEG / 2) + j / 2) * L.NT + lane) * 4;
+        f[j & 1] = re;
+        f[2 + (j & 1)] = im;
+    } else {
+        float* f = out + ((size_t)(L.SPT * L.SEG / 2 + s) * L.NT + lane) * 4;
+        f[0] = re;
+        f[1] = 0.f;
+        f[2] = im;
+        f[3] = 0.f;
+    }
+}
 }  // namespace fofse

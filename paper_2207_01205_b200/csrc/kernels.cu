@@ -140,9 +140,16 @@ __global__ void __launch_bounds__(256) k1_kernel(K1Args a) {
             }
         }
         if (a.vimg32) {
-            float* o = a.vimg32 + (size_t)b * T * sr32;
-            for (int i = threadIdx.x; i < T * sr32; i += blockDim.x) {
-                const int r = i / sr32, col = i % sr32, k2 = col % T;
+            // rotated real V with its anti-periodic extension (col >= T: sc V[col-T]).
+            // vpairs (K2v2): two copies, E[c] = V[c] and O[c] = V[c+1], row stride
+            // v2_srv(T), so every pair of adjacent columns is one aligned 8-byte load.
+            const int srv = a.vpairs ? v2_srv(T) : sr32;
+            const int ncopy = a.vpairs ? 2 : 1;
+            float* o = a.vimg32 + (size_t)b * ncopy * T * srv;
+            for (int i = threadIdx.x; i < ncopy * T * srv; i += blockDim.x) {
+                const int cp = i / (T * srv), rem = i % (T * srv);
+                const int r = rem / srv, col = rem % srv + cp;
+                const int k2 = col % T;
                 const double2 w = k1_spec<T>(cbuf, r, k2);
                 const double2 ph = phase_pos<T>((long long)r * (a.Lh - 1) + (long long)k2 * (a.Lw - 1));
                 double v = w.x * ph.x - w.y * ph.y;  // Re(W e^{j phi})
@@ -166,6 +173,7 @@ __global__ void __launch_bounds__(256) k1_kernel(K1Args a) {
     } else {
         const BinLayout L = BinLayout::make(T, a.seg, a.spt > 0 ? a.spt : 1);
         const bool rotate = a.path == PATH_F32_REAL;
+        const size_t per = a.out_stride > 0 ? (size_t)a.out_stride : packed32_floats(L, a.soa);
         for (int s = threadIdx.x; s < L.SLOTS; s += blockDim.x) {
             const int j = s / L.NT, tid = s % L.NT;
             int k1 = 0, k2 = 0;
@@ -181,8 +189,8 @@ __global__ void __launch_bounds__(256) k1_kernel(K1Args a) {
             if (a.path == PATH_F64_STRICT)
                 static_cast<double2*>(a.out)[(size_t)b * L.SLOTS + s] = v;
             else
-                static_cast<float2*>(a.out)[(size_t)b * L.SLOTS + s] =
-                    make_float2(static_cast<float>(v.x), static_cast<float>(v.y));
+                put_packed32(static_cast<float*>(a.out) + (size_t)b * per, L, a.soa, j, tid,
+                             static_cast<float>(v.x), static_cast<float>(v.y));
         }
     }
     vmax = block_reduce<double>(vmax, red, true);

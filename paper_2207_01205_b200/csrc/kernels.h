@@ -59,13 +59,16 @@ struct K1Args {
     int32_t path;              // IterPath for K1_PACKED (precision + rotation)
     int32_t seg;               // layout SEG of the K2 path
     int32_t spt;               // layout segments per thread (0 = 1)
+    int32_t soa;               // fp32 packed output in the K2v2 SoA pair layout
+    int64_t out_stride;        // fp32 packed output: floats per block (0 = packed size)
     void* out;                 // packed R / full spectrum (double2) / W images
     double* energy;            // per block sum w f^2 (packed/full modes)
     double* init_max;          // per block max |R| (packed/full modes)
     // class mode outputs
     double2* wimg64;           // [ncls][T*SR64] complex fp64 image (SEG of fp64)
     float2* wimg32;            // [ncls][T*SR32] complex fp32 image
-    float* vimg32;             // [ncls][T*SR32] rotated real image
+    float* vimg32;             // [ncls][T*SR32] rotated real image ([ncls][2][T*SRV] with vpairs)
+    int32_t vpairs;            // write the K2v2 even/odd paired V layout
     double* w0;                // [ncls]
     const double2* twid;       // e^{-j 2 pi k / T}, k < T
 };
@@ -83,6 +86,7 @@ struct K2Args {
     const int32_t* order;
     const BlockDesc* blocks;
     const void* rin;            // packed residual (Real2 per slot)
+    int64_t rin_stride;         // K2v2: floats per block in rin/rout (0 = packed size)
     void* rout;                 // optional: packed residual written back
     const void* wimg;           // W images of the path's precision
     int64_t wimg_stride;        // elements per class
@@ -123,6 +127,8 @@ struct CvtArgs {
     float2* out;                // packed fp32 residuals (K2v2 layout)
     int32_t out_seg, out_spt;
     int32_t rotate;             // apply the rotated-frame phase e^{+j phi(k)} (PATH_F32_REAL)
+    int32_t soa;                // SoA pair layout (K2v2 real path)
+    int64_t out_stride;         // floats per block (0 = packed size)
 };
 enum { SYN_NONE = 0, SYN_IMAGE = 1, SYN_WINDOW = 2 };
 

@@ -18,6 +18,7 @@
 #include <stdint.h>
 
 #include <climits>
+#include <cstdlib>
 #include <type_traits>
 
 #include "kcommon.cuh"
@@ -33,56 +34,269 @@ struct V2Cfg {
     static constexpr int HT = T / 2;
     static constexpr int QN = T / SEG;
     static constexpr int NT = HT * QN / SPT;
-    static constexpr int NB = SPT * (SEG + 1);
-    static constexpr int SR = T + SEG + 1;
+    static constexpr int NB = SPT * (SEG + 1);  // slots per lane (AoS layout)
+    static constexpr int NP = SPT * SEG / 2;    // bin pairs per lane (SoA real path)
+    static constexpr int SR = T + SEG + 1;      // complex image row stride
+    static constexpr int SRV = v2_srv(T);       // paired real image row stride
     static constexpr int SLOTS = NB * NT;
     static constexpr int WARPS = 4;
-    using WT = typename std::conditional<PATH == PATH_F32_REAL, float, float2>::type;
-    static constexpr size_t WBYTES = ((sizeof(WT) * T * SR + 15) / 16) * 16;
-    static constexpr size_t OFF_P = WBYTES;                       // 2T double2
+    static constexpr bool REAL = PATH == PATH_F32_REAL;
+    // REAL: two float copies (even / odd aligned) of the rotated V; else complex W
+    static constexpr size_t WELEMS = REAL ? (size_t)2 * T * SRV : (size_t)T * SR;
+    static constexpr size_t WBYTES = ((WELEMS * (REAL ? 4 : 8) + 15) / 16) * 16;
+    static constexpr size_t OFF_P = WBYTES;                            // 2T double2
     static constexpr size_t OFF_TW = OFF_P + sizeof(double2) * 2 * T;  // T float2
-    static constexpr size_t OFF_SP = OFF_TW + sizeof(float2) * T;      // spill WARPS x NB float2
-    static constexpr size_t OFF_BAR = OFF_SP + sizeof(float2) * WARPS * NB;
+    static constexpr size_t OFF_SP = OFF_TW + sizeof(float2) * T;      // spill: WARPS x (NP+SPT) float4
+    static constexpr size_t OFF_ST = OFF_SP + sizeof(float4) * WARPS * (NP + SPT + 1);  // WARPS x V2State
+    static constexpr size_t OFF_BAR = OFF_ST + 64 * WARPS;
     static constexpr size_t SMEM = OFF_BAR + 16;
     static_assert(NT <= 32, "K2v2 needs one warp per block");
+    static_assert(SEG % 2 == 0, "bin pairs");
 };
 
+template <class Cf>
+__device__ __forceinline__ constexpr int T_of() { return Cf::HT * 2; }
+
+// Per-warp scalar state of the block being iterated, kept in shared memory to
+// leave the register file to the 132 registers of the residual spectrum.
+struct V2State {
+    double energy;  // weighted residual energy (engine_spectral.cpp:100-110)
+    double thr_e;   // 1e-12 * initial_energy        (stop test, :60)
+    double thr_m;   // (1e-12 * initial_max)^2 on |R|^2 (stop test, :61)
+    double w0, gw;  // W[0] and gamma / W[0]
+    int nu, ntrace, pad0, pad1;
+};
+static_assert(sizeof(V2State) <= 64, "state slot");
+
 __device__ __forceinline__ unsigned fbits(float x) { return __float_as_uint(x); }
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+    float r;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));  // FMNMX3
+    return r;
+}
 
-template <int T, int PATH>
-__global__ void __launch_bounds__(128, 3) k2v2_kernel(K2Args a) {
-    using Cf = V2Cfg<T, PATH>;
-    using WT = typename Cf::WT;
-    constexpr int SEG = Cf::SEG, SPT = Cf::SPT, NT = Cf::NT, NB = Cf::NB, SR = Cf::SR;
-    constexpr bool REAL = PATH == PATH_F32_REAL;
-
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const Tile tile = a.tiles[blockIdx.x];
-    const WT* wimg = reinterpret_cast<const WT*>(smem_raw);
-    const double2* ptab = reinterpret_cast<const double2*>(smem_raw + Cf::OFF_P);
-    const float2* twi = reinterpret_cast<const float2*>(smem_raw + Cf::OFF_TW);
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + Cf::OFF_BAR);
-
+// Stage the class image (TMA bulk copy), the rotated-frame phase table and the
+// synthesis twiddles; returns once everything is resident.
+template <class Cf>
+__device__ __forceinline__ void v2_stage(const K2Args& a, const Tile& tile, unsigned char* smem) {
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Cf::OFF_BAR);
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
-        const char* src = static_cast<const char*>(a.wimg) + (size_t)tile.cls * a.wimg_stride * sizeof(WT);
-        const uint32_t bytes = static_cast<uint32_t>(sizeof(WT) * T * SR);
+        const uint32_t bytes = static_cast<uint32_t>(Cf::WELEMS * (Cf::REAL ? 4 : 8));
+        const char* src = static_cast<const char*>(a.wimg) + (size_t)tile.cls * bytes;
         mbar_expect_tx(bar, bytes);
         for (uint32_t off = 0; off < bytes; off += 32768)
-            bulk_g2s(smem_raw + off, src + off, bytes - off < 32768u ? bytes - off : 32768u, bar);
+            bulk_g2s(smem + off, src + off, bytes - off < 32768u ? bytes - off : 32768u, bar);
     }
-    for (int i = threadIdx.x; i < 2 * T; i += blockDim.x)
-        reinterpret_cast<double2*>(smem_raw + Cf::OFF_P)[i] = a.ptab ? a.ptab[i] : make_double2(1.0, 0.0);
-    for (int i = threadIdx.x; i < T; i += blockDim.x) {
+    for (int i = threadIdx.x; i < 2 * T_of<Cf>(); i += blockDim.x)
+        reinterpret_cast<double2*>(smem + Cf::OFF_P)[i] = a.ptab ? a.ptab[i] : make_double2(1.0, 0.0);
+    for (int i = threadIdx.x; i < T_of<Cf>(); i += blockDim.x) {
         const double2 t = a.twid_inv[i];
-        reinterpret_cast<float2*>(smem_raw + Cf::OFF_TW)[i] = make_float2((float)t.x, (float)t.y);
+        reinterpret_cast<float2*>(smem + Cf::OFF_TW)[i] = make_float2((float)t.x, (float)t.y);
     }
     __syncthreads();
     mbar_wait(bar, 0);
+}
+
+// Lane 0 records a selection: synthesis record (pair factor folded in), the
+// IterationRecord trace (trace.hpp:13-21) and the guard diagnostics.
+__device__ __forceinline__ void v2_record(const K2Args& a, int b, int nu, int ntrace, int rstride,
+                                          int tstride, int* rec_u, double2* rec_c, int u1, int u2,
+                                          int self, double p_re, double p_im, double c_re,
+                                          double c_im, double energy, double Mf, double Sf) {
+    if (rec_u && nu - 1 < rstride) {
+        rec_u[nu - 1] = (u1 << 16) | u2;
+        rec_c[nu - 1] = self ? make_double2(c_re, 0.0) : make_double2(2.0 * c_re, 2.0 * c_im);
+    }
+    if (a.trace && ntrace < tstride) {
+        fofse_record rr;
+        rr.nu = nu;
+        rr.u1 = u1;
+        rr.u2 = u2;
+        rr.pad0 = 0;
+        rr.p_re = p_re;
+        rr.p_im = p_im;
+        rr.c_re = c_re;
+        rr.c_im = c_im;
+        rr.gamma_effective = a.gamma;
+        rr.weighted_energy = energy;
+        rr.degenerate = 0;
+        rr.pad1 = 0;
+        a.trace[(size_t)b * tstride + ntrace] = rr;
+    }
+    if (a.gap_trace && ntrace < tstride)
+        a.gap_trace[(size_t)b * tstride + ntrace] = (float)(Sf > 0.0 ? (Mf - Sf) / Mf : 1.0);
+}
+
+// Block outputs + fused sparse synthesis (synthesize_model, engine_spectral.cpp:
+// 195-208) over the MISSING region, clamp + write-back (pipeline.cpp:226-232).
+// A team of NTH threads (t = 0..NTH-1, whole warps) shares the pixels; for
+// NTH > 32 the teams' partial squared errors meet in red[] behind named barrier bar.
+template <int T, int NTH>
+__device__ __forceinline__ void v2_finish(const K2Args& a, const BlockDesc& desc, int pos, int b,
+                                          int t, double energy, int nu, int conv, int flagged,
+                                          int ntrace, const int* rec_u, const double2* rec_c,
+                                          int rstride, const float2* twi, double* red = nullptr,
+                                          int bar = 0) {
+    const int lane = t & 31;
+    if (t == 0) {
+        const int sb = a.state_by_pos ? pos : b;
+        if (a.energy_out) a.energy_out[sb] = energy;
+        if (a.nu_out) a.nu_out[sb] = nu;
+        if (a.conv_out) a.conv_out[sb] = conv;
+        if (a.flags) a.flags[b] = flagged;
+        if (a.trace_count) a.trace_count[b] = ntrace;
+    }
+    __syncwarp();
+    if (a.synth == SYN_NONE || flagged) return;
+    const int nr = nu < rstride ? nu : rstride;
+    const int npx = a.reg_nr * a.reg_nc;
+    double sq = 0.0;
+    for (int p0 = 0; p0 < npx; p0 += NTH * 8) {
+        float acc[8];
+        int mm[8], nn[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            acc[k] = 0.f;
+            const int px = p0 + k * NTH + t;
+            mm[k] = a.reg_r0 + (px < npx ? px / a.reg_nc : 0);
+            nn[k] = a.reg_c0 + (px < npx ? px % a.reg_nc : 0);
+        }
+        for (int q = 0; q < nr; ++q) {
+            const int u = rec_u[q];
+            const double2 cd = rec_c[q];
+            const float cx = (float)cd.x, cy = (float)cd.y;
+            const int uu1 = u >> 16, uu2 = u & 0xffff;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const float2 tw = twi[(uu1 * mm[k] + uu2 * nn[k]) & (T - 1)];
+                acc[k] = fmaf(cx, tw.x, fmaf(-cy, tw.y, acc[k]));
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int px = p0 + k * NTH + t;
+            if (px >= npx) continue;
+            const int m = mm[k], n = nn[k];
+            if (a.synth == SYN_WINDOW) {
+                a.models[(size_t)b * a.Lh * a.Lw + m * a.Lw + n] = acc[k];
+            } else {
+                const double v0 = acc[k];
+                const double v = v0 < 0.0 ? 0.0 : (v0 > 255.0 ? 255.0 : v0);
+                const int64_t gi = (int64_t)desc.frame * a.fr.frame_stride +
+                                   (int64_t)(desc.row0 + m) * a.fr.width + (desc.col0 + n);
+                double orig;
+                if (a.fr.type == SRC_U8) {
+                    orig = (double)static_cast<const uint8_t*>(a.fr.src)[gi];
+                    static_cast<uint8_t*>(a.fr.dst)[gi] = static_cast<uint8_t>(round(v));
+                } else {
+                    orig = static_cast<const double*>(a.fr.src)[gi];
+                    static_cast<double*>(a.fr.dst)[gi] = v;
+                }
+                sq += (orig - v) * (orig - v);
+            }
+        }
+    }
+    if (a.block_sq && a.synth == SYN_IMAGE) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+        if constexpr (NTH == 32) {
+            if (lane == 0) a.block_sq[b] = sq;
+        } else {
+            if (lane == 0) red[t >> 5] = sq;
+            named_bar_sync(bar, NTH);
+            if (t == 0) {
+                double tot = 0.0;
+                for (int w = 0; w < NTH / 32; ++w) tot += red[w];
+                a.block_sq[b] = tot;
+            }
+        }
+    }
+}
+
+// fp32 argmax on packed keys: |R|^2 with its 6 low mantissa bits replaced by
+// (63 - pair index). Truncation merges values within 2^-17 relative into ties;
+// every tie leaves the runner-up equal to the maximum, which the near-tie guard
+// (tau >= 1e-5 > 2^-17) flags for an fp64 re-run, so the key order never
+// decides an unflagged selection.
+struct KAcc {
+    float m1, m2;  // best key, runner-up
+};
+__device__ __forceinline__ unsigned key_mask() {
+    unsigned m;  // kept in a register so the key is one LOP3: (bits & mask) | imm
+    asm volatile("mov.b32 %0, 0xffffffc0;" : "=r"(m));
+    return m;
+}
+__device__ __forceinline__ float pkey(float m, int p, unsigned mask) {
+    return __uint_as_float((__float_as_uint(m) & mask) | static_cast<unsigned>(63 - p));
+}
+__device__ __forceinline__ void kacc_pair(KAcc& A, float2 mp, int p, unsigned mask) {
+    const float hi = fmaxf(mp.x, mp.y), lo = fminf(mp.x, mp.y);
+    const float k = pkey(hi, p, mask);
+    A.m2 = fmax3(A.m2, lo, fminf(k, A.m1));
+    A.m1 = fmaxf(A.m1, k);
+}
+__device__ __forceinline__ void kacc_one(KAcc& A, float m, int p, unsigned mask) {
+    const float k = pkey(m, p, mask);
+    A.m2 = fmaxf(A.m2, fminf(k, A.m1));
+    A.m1 = fmaxf(A.m1, k);
+}
+
+// The winning bin pair of a lane, selected by a warp-uniform index: an
+// unrolled switch (jump table) instead of dynamic register indexing, so the
+// winner lane stores one float4 instead of its whole segment.
+template <int NP, int SPT>
+__device__ __forceinline__ float4 pick_pair(int pw, const float2* rp, const float2* ip, const float* xr,
+                                            const float* xi) {
+    float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+    switch (pw) {
+#define PICK_CASE(P) \
+    case P:          \
+        if (P < NP) q = make_float4(rp[P < NP ? P : 0].x, rp[P < NP ? P : 0].y, ip[P < NP ? P : 0].x, ip[P < NP ? P : 0].y); \
+        else q = make_float4(xr[P - NP < SPT && P >= NP ? P - NP : 0], 0.f, xi[P - NP < SPT && P >= NP ? P - NP : 0], 0.f); \
+        break;
+        PICK_CASE(0) PICK_CASE(1) PICK_CASE(2) PICK_CASE(3) PICK_CASE(4) PICK_CASE(5) PICK_CASE(6)
+        PICK_CASE(7) PICK_CASE(8) PICK_CASE(9) PICK_CASE(10) PICK_CASE(11) PICK_CASE(12) PICK_CASE(13)
+        PICK_CASE(14) PICK_CASE(15) PICK_CASE(16) PICK_CASE(17) PICK_CASE(18) PICK_CASE(19) PICK_CASE(20)
+        PICK_CASE(21) PICK_CASE(22) PICK_CASE(23) PICK_CASE(24) PICK_CASE(25) PICK_CASE(26) PICK_CASE(27)
+        PICK_CASE(28) PICK_CASE(29) PICK_CASE(30) PICK_CASE(31) PICK_CASE(32) PICK_CASE(33)
+#undef PICK_CASE
+        default: break;
+    }
+    return q;
+}
+
+// (value, index) argmax merge: larger value wins, ties to the lower index.
+__device__ __forceinline__ void am_merge(float& m1, int& i1, float& m2, float om1, int oi1, float om2) {
+    const bool take = om1 > m1 || (om1 == m1 && oi1 < i1);
+    m2 = fmax3(m2, om2, take ? m1 : om1);
+    m1 = take ? om1 : m1;
+    i1 = take ? oi1 : i1;
+}
+
+// ============================================================================
+// Real (rotated-frame) path: point-symmetric window masks, W = P V, V real.
+// Bins are held as SoA pairs (re_a, re_b), (im_a, im_b) of adjacent columns,
+// so one LDS.64 from the even/odd-aligned V copy feeds two bins and every
+// update / magnitude is an FFMA2 / FMUL2 on a pair.
+// ============================================================================
+template <int T>
+__global__ void __launch_bounds__(128, 3) k2v2r_kernel(K2Args a) {
+    using Cf = V2Cfg<T, PATH_F32_REAL>;
+    constexpr int SEG = Cf::SEG, SPT = Cf::SPT, NT = Cf::NT, NP = Cf::NP, SRV = Cf::SRV;
+    constexpr int PPS = SEG / 2;  // pairs per segment
+    constexpr int ACC = 2;        // independent argmax chains
+
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const Tile tile = a.tiles[blockIdx.x];
+    v2_stage<Cf>(a, tile, smem_raw);
+    const float* vE = reinterpret_cast<const float*>(smem_raw);
+    const double2* ptab = reinterpret_cast<const double2*>(smem_raw + Cf::OFF_P);
+    const float2* twi = reinterpret_cast<const float2*>(smem_raw + Cf::OFF_TW);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool active = lane < NT;
-    float2* spill = reinterpret_cast<float2*>(smem_raw + Cf::OFF_SP) + warp * NB;
+    float4* spill = reinterpret_cast<float4*>(smem_raw + Cf::OFF_SP) + warp * (NP + SPT + 1);
 
     const BinLayout L = BinLayout::make(T, SEG, SPT);
     int k1s[SPT], c0s[SPT], exs[SPT];
@@ -93,8 +307,488 @@ __global__ void __launch_bounds__(128, 3) k2v2_kernel(K2Args a) {
     }
     const int gb0 = k1s[0] * T + c0s[0];
     const int gb1 = k1s[SPT - 1] * T + c0s[SPT - 1];
+    static_assert(NP + SPT <= 64, "pair index must fit the 6 key bits");
     const float sgn_r = ((a.Lh - 1) & 1) ? -1.f : 1.f;
     const float sgn_c = ((a.Lw - 1) & 1) ? -1.f : 1.f;
+    const unsigned kmask = key_mask();
+    V2State* st = reinterpret_cast<V2State*>(smem_raw + Cf::OFF_ST + 64 * warp);
+
+    for (int bi = warp; bi < tile.count; bi += Cf::WARPS) {
+        const int pos = tile.begin + bi;
+        const int b = a.order[pos];
+        float2 rp[NP], ip[NP];   // (re, re), (im, im) of bins 2p, 2p+1
+        float xr[SPT], xi[SPT];  // the self-conjugate extra bin (k1, T/2) of a segment
+        {
+            // SoA pair layout (put_packed32): one 16-byte load per bin pair
+            const size_t rs = a.rin_stride > 0 ? (size_t)a.rin_stride : (size_t)(NP + SPT) * NT * 4;
+            const float4* R = reinterpret_cast<const float4*>(static_cast<const float*>(a.rin) + (size_t)pos * rs);
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+                const float4 u = active ? R[p * NT + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+                rp[p] = make_float2(u.x, u.y);
+                ip[p] = make_float2(u.z, u.w);
+            }
+#pragma unroll
+            for (int s = 0; s < SPT; ++s) {
+                const float4 u = active ? R[(NP + s) * NT + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+                xr[s] = u.x;
+                xi[s] = u.z;
+            }
+        }
+        const double e_init = a.init_energy[pos];
+        if (lane == 0) {
+            const double im = 1e-12 * a.init_max[pos];
+            st->energy = a.energy0[pos];
+            st->thr_e = 1e-12 * e_init;
+            st->thr_m = im * im;
+            st->w0 = a.w0[tile.cls];
+            st->gw = a.gamma / st->w0;
+            st->nu = a.nu0 ? a.nu0[pos] : 0;
+            st->ntrace = a.trace_from_nu0 ? st->nu : 0;
+        }
+        int conv = (a.conv0 ? a.conv0[pos] : 0) | (e_init <= 0.0);
+        int flagged = 0;
+        __syncwarp();
+
+        // argmax chains on packed keys (|R|^2 bits, low 6 bits = 63 - pair);
+        // the scan of iteration k+1 is fused into the update of iteration k
+        KAcc A[ACC + 1];
+#pragma unroll
+        for (int k = 0; k <= ACC; ++k) A[k] = KAcc{0.f, 0.f};
+#pragma unroll
+        for (int p = 0; p < NP; ++p) kacc_pair(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+#pragma unroll
+        for (int s = 0; s < SPT; ++s)
+            if (exs[s]) kacc_one(A[ACC], fmaf(xi[s], xi[s], xr[s] * xr[s]), NP + s, kmask);
+
+        for (int it = 0; it < a.iterations && !conv; ++it) {
+            float bm1 = A[0].m1, bm2 = A[0].m2;
+#pragma unroll
+            for (int k = 1; k <= ACC; ++k) {
+                bm2 = fmax3(bm2, A[k].m2, fminf(bm1, A[k].m1));
+                bm1 = fmaxf(bm1, A[k].m1);
+            }
+            // ---- warp argmax + runner-up (near-tie guard) ----
+            const unsigned M = __reduce_max_sync(0xffffffffu, fbits(bm1));
+            const bool cand = fbits(bm1) == M;
+            const int wl = __ffs(__ballot_sync(0xffffffffu, cand)) - 1;
+            const unsigned S = __reduce_max_sync(0xffffffffu, fbits(lane == wl ? bm2 : bm1));
+            const int pw = 63 - static_cast<int>(M & 63u);  // winning pair (or NP + segment)
+            __syncwarp();
+            if (lane == wl) spill[0] = pick_pair<NP, SPT>(pw, rp, ip, xr, xi);  // uniform jump table
+            __syncwarp();
+            float2 pre;
+            int jw, sw;
+            {
+                const float4 q = spill[0];
+                if (pw < NP) {
+                    const float ma = fmaf(q.z, q.z, q.x * q.x), mb = fmaf(q.w, q.w, q.y * q.y);
+                    const int half = mb > ma ? 1 : 0;  // ties to the lower column
+                    pre = half ? make_float2(q.y, q.w) : make_float2(q.x, q.z);
+                    sw = pw / PPS;
+                    jw = 2 * (pw % PPS) + half;
+                } else {
+                    pre = make_float2(q.x, q.z);
+                    sw = pw - NP;
+                    jw = SEG;
+                }
+            }
+            const int G = __shfl_sync(0xffffffffu, (SPT == 2 && sw == 1) ? gb1 : gb0, wl) + jw;
+
+            // ---- scalar part of iterate (engine_spectral.cpp:58-110), fp64 ----
+            const double Mf = (double)__uint_as_float(M), Sf = (double)__uint_as_float(S);
+            const double energy = st->energy, w0 = st->w0, gw = st->gw;
+            if (energy < st->thr_e || !(Mf > 0.0) || Mf < st->thr_m) {
+                conv = 1;
+                break;
+            }
+            if (Sf > Mf * (1.0 - a.tau)) {  // tau == 0 disables (Sf <= Mf)
+                flagged = 1;  // near-tie: the host re-runs this block in fp64
+                break;
+            }
+            const int u1 = G / T, u2 = G % T;
+            const int self = ((T - u1) % T == u1) && ((T - u2) % T == u2);
+            const double pr = pre.x, pi = pre.y;
+            const double2 P = ptab[(u1 * (a.Lh - 1) + u2 * (a.Lw - 1)) & (2 * T - 1)];  // e^{-j phi(u)}
+            const double ar = pr * gw, ai = pi * gw;  // a = gamma R'[u] / w0
+            double c_re = ar * P.x - ai * P.y, c_im = ar * P.y + ai * P.x;  // c = P a
+            double a_re = ar, a_im = ai, delta;
+            if (self) {
+                c_im = 0.0;
+                a_re = c_re * P.x;
+                a_im = -c_re * P.y;
+                delta = -2.0 * c_re * (pr * P.x - pi * P.y) + c_re * c_re * w0;
+            } else {
+                const int mi1 = 2 * u1, mi2 = 2 * u2;
+                const float v2 = vE[(mi1 & (T - 1)) * SRV + (mi2 & (T - 1))];
+                const double sig = ((mi1 >= T) ? (double)sgn_r : 1.0) * ((mi2 >= T) ? (double)sgn_c : 1.0);
+                delta = -4.0 * (a_re * pr + a_im * pi) + 2.0 * (a_re * a_re + a_im * a_im) * w0 +
+                        2.0 * sig * (double)v2 * (a_re * a_re - a_im * a_im);
+            }
+            const double e = energy + delta;
+            const double en = 0.0 < e ? e : 0.0;
+            const int nu = st->nu + 1;
+            __syncwarp();
+            if (lane == 0) {
+                const int rs = a.rec_stride > 0 ? a.rec_stride : a.iterations;
+                if (nu - 1 < rs) {
+                    a.rec_u_g[(size_t)b * rs + nu - 1] = (u1 << 16) | u2;
+                    a.rec_c_g[(size_t)b * rs + nu - 1] =
+                        self ? make_double2(c_re, 0.0) : make_double2(2.0 * c_re, 2.0 * c_im);
+                }
+                st->energy = en;
+                st->nu = nu;
+            }
+            if (a.trace || a.gap_trace) {  // diagnostics only
+                if (lane == 0) {
+                    const int tstride = a.trace_stride > 0 ? a.trace_stride : a.iterations;
+                    const double iw = 1.0 / w0;
+                    v2_record(a, b, nu, st->ntrace, 0, tstride, nullptr, nullptr, u1, u2, self,
+                              (pr * P.x - pi * P.y) * iw, (pr * P.y + pi * P.x) * iw, c_re, c_im, en, Mf, Sf);
+                    st->ntrace += 1;
+                }
+            } else if (lane == 0) {
+                st->ntrace += 1;
+            }
+
+            // ---- residual update: R' -= s1 a V[k-u] + s2 conj(a) V[k+u] (+ next scan) ----
+            const float fr = (float)a_re, fi = (float)a_im;
+            const int par = u2 & 1;
+            const float* vimg = vE + par * (T * SRV);  // O copy holds V[c+1]
+#pragma unroll
+            for (int k = 0; k <= ACC; ++k) A[k] = KAcc{0.f, 0.f};
+#pragma unroll
+            for (int s = 0; s < SPT; ++s) {
+                const int k1 = k1s[s], c0 = c0s[s];
+                const int rA = (k1 - u1) & (T - 1), rB = (k1 + u1) & (T - 1);
+                const int cA = (c0 - u2) & (T - 1), cB = (c0 + u2) & (T - 1);
+                const float s1 = ((k1 < u1) ? sgn_r : 1.f) * ((c0 < u2) ? sgn_c : 1.f);
+                const float s2 = ((k1 + u1 >= T) ? sgn_r : 1.f) * ((c0 + u2 >= T) ? sgn_c : 1.f);
+                const float2* va = reinterpret_cast<const float2*>(vimg + rA * SRV + (cA - par));
+                const float2* vb = reinterpret_cast<const float2*>(vimg + rB * SRV + (cB - par));
+                const float2 n1r = make_float2(-s1 * fr, -s1 * fr), n1i = make_float2(-s1 * fi, -s1 * fi);
+                const float2 n2r = make_float2(-s2 * fr, -s2 * fr), n2i = make_float2(s2 * fi, s2 * fi);
+                if (self) {
+#pragma unroll
+                    for (int q = 0; q < PPS; ++q) {
+                        const int p = s * PPS + q;
+                        const float2 x = va[q];
+                        rp[p] = __ffma2_rn(n1r, x, rp[p]);
+                        ip[p] = __ffma2_rn(n1i, x, ip[p]);
+                        kacc_pair(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < PPS; ++q) {
+                        const int p = s * PPS + q;
+                        const float2 x = va[q], y = vb[q];
+                        rp[p] = __ffma2_rn(n2r, y, __ffma2_rn(n1r, x, rp[p]));
+                        ip[p] = __ffma2_rn(n2i, y, __ffma2_rn(n1i, x, ip[p]));
+                        kacc_pair(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+                    }
+                }
+                if (exs[s]) {
+                    const float x = vE[rA * SRV + cA + SEG];
+                    xr[s] = fmaf(-s1 * fr, x, xr[s]);
+                    xi[s] = fmaf(-s1 * fi, x, xi[s]);
+                    if (!self) {
+                        const float y = vE[rB * SRV + cB + SEG];
+                        xr[s] = fmaf(-s2 * fr, y, xr[s]);
+                        xi[s] = fmaf(s2 * fi, y, xi[s]);
+                    }
+                    kacc_one(A[ACC], fmaf(xi[s], xi[s], xr[s] * xr[s]), NP + s, kmask);
+                }
+            }
+        }
+
+        if (a.rout && active) {
+            const size_t rs = a.rin_stride > 0 ? (size_t)a.rin_stride : (size_t)(NP + SPT) * NT * 4;
+            float4* R = reinterpret_cast<float4*>(static_cast<float*>(a.rout) + (size_t)pos * rs);
+#pragma unroll
+            for (int p = 0; p < NP; ++p) R[p * NT + lane] = make_float4(rp[p].x, rp[p].y, ip[p].x, ip[p].y);
+#pragma unroll
+            for (int s = 0; s < SPT; ++s) R[(NP + s) * NT + lane] = make_float4(xr[s], 0.f, xi[s], 0.f);
+        }
+        __syncwarp();
+        {
+            const int rstride = a.rec_stride > 0 ? a.rec_stride : a.iterations;
+            v2_finish<T, 32>(a, a.blocks[pos], pos, b, lane, st->energy, st->nu, conv, flagged, st->ntrace,
+                         a.rec_u_g + (size_t)b * rstride, a.rec_c_g + (size_t)b * rstride, rstride, twi);
+        }
+        __syncwarp();
+    }
+}
+
+// ============================================================================
+// Real path, TWO WARPS PER LOST BLOCK (T = 64): each warp owns one 32-column
+// segment of every canonical row (16 bin pairs + the self-conjugate extra for
+// lane 0) — half the registers of the one-warp form, so twice the warps per SM
+// and room for instruction-level parallelism. The two warps meet once per
+// selection at a 64-thread named barrier: each warp publishes its best key,
+// runner-up and its winner lane's bins (double-buffered by iteration parity),
+// then both warps resolve the same global argmax and run the scalar update.
+// ============================================================================
+template <int T>
+struct V2R2Cfg {
+    static constexpr int SEG = 32, SPT = 1, HT = T / 2, QN = T / SEG;
+    static constexpr int NT = HT * QN;  // 64 threads = 2 warps
+    static constexpr int NP = SEG / 2, PPS = SEG / 2;
+    static constexpr int SRV = T + SEG + 2;
+    static constexpr int GROUPS = 4;     // lost blocks per CTA (256 threads)
+    static constexpr bool REAL = true;
+    static constexpr size_t WELEMS = (size_t)2 * T * SRV;
+    static constexpr size_t WBYTES = ((WELEMS * 4 + 15) / 16) * 16;
+    static constexpr size_t OFF_P = WBYTES;
+    static constexpr size_t OFF_TW = OFF_P + sizeof(double2) * 2 * T;
+    // per group: slots [2 parity][2 warps] x 16 B, spill [2][2][NP+1] float4, red 2 doubles
+    static constexpr size_t GRP = 2 * 2 * 16 + 2 * 2 * (NP + 1) * 16 + 16;
+    static constexpr size_t OFF_G = OFF_TW + sizeof(float2) * T;
+    static constexpr size_t OFF_BAR = OFF_G + GRP * GROUPS;
+    static constexpr size_t SMEM = OFF_BAR + 16;
+    static_assert(NT == 64, "two warps per block");
+};
+
+struct R2Slot {
+    unsigned key;
+    float second;
+    int gbase, lane;
+};
+
+template <int T>
+__global__ void __launch_bounds__(256, 2) k2v2r2_kernel(K2Args a) {
+    using Cf = V2R2Cfg<T>;
+    constexpr int SEG = Cf::SEG, NT = Cf::NT, NP = Cf::NP, PPS = Cf::PPS, SRV = Cf::SRV;
+    constexpr int ACC = 2;
+
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const Tile tile = a.tiles[blockIdx.x];
+    v2_stage<Cf>(a, tile, smem_raw);
+    const float* vE = reinterpret_cast<const float*>(smem_raw);
+    const double2* ptab = reinterpret_cast<const double2*>(smem_raw + Cf::OFF_P);
+    const float2* twi = reinterpret_cast<const float2*>(smem_raw + Cf::OFF_TW);
+
+    const int grp = threadIdx.x / NT, tid = threadIdx.x % NT;
+    const int w = tid >> 5, lane = tid & 31;
+    unsigned char* gsm = smem_raw + Cf::OFF_G + Cf::GRP * grp;
+    R2Slot* slots = reinterpret_cast<R2Slot*>(gsm);                       // [2][2]
+    float4* spills = reinterpret_cast<float4*>(gsm + 2 * 2 * 16);          // [2][2][NP+1]
+    double* red = reinterpret_cast<double*>(gsm + 2 * 2 * 16 + 2 * 2 * (NP + 1) * 16);
+    const int bar = 1 + grp;
+
+    const BinLayout L = BinLayout::make(T, SEG, 1);
+    int k1, c0, ex;
+    L.thread_segment(tid, 0, &k1, &c0, &ex);
+    const int gb = k1 * T + c0;
+    const float sgn_r = ((a.Lh - 1) & 1) ? -1.f : 1.f;
+    const float sgn_c = ((a.Lw - 1) & 1) ? -1.f : 1.f;
+    const unsigned kmask = key_mask();
+    const int rstride = a.rec_stride > 0 ? a.rec_stride : a.iterations;
+    const int tstride = a.trace_stride > 0 ? a.trace_stride : a.iterations;
+
+    for (int bi = grp; bi < tile.count; bi += Cf::GROUPS) {
+        const int pos = tile.begin + bi;
+        const int b = a.order[pos];
+        float2 rp[NP], ip[NP];
+        float xr, xi;
+        {
+            const size_t rs = a.rin_stride > 0 ? (size_t)a.rin_stride : (size_t)(NP + 1) * NT * 4;
+            const float4* R = reinterpret_cast<const float4*>(static_cast<const float*>(a.rin) + (size_t)pos * rs);
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+                const float4 u = R[p * NT + tid];
+                rp[p] = make_float2(u.x, u.y);
+                ip[p] = make_float2(u.z, u.w);
+            }
+            const float4 u = R[NP * NT + tid];
+            xr = u.x;
+            xi = u.z;
+        }
+        double energy = a.energy0[pos];
+        const double e_init = a.init_energy[pos];
+        const double thr_e = 1e-12 * e_init;
+        const double thr_m = (1e-12 * a.init_max[pos]) * (1e-12 * a.init_max[pos]);
+        const double w0 = a.w0[tile.cls], gw = a.gamma / w0;
+        int nu = a.nu0 ? a.nu0[pos] : 0;
+        int ntrace = a.trace_from_nu0 ? nu : 0;
+        int conv = (a.conv0 ? a.conv0[pos] : 0) | (e_init <= 0.0);
+        int flagged = 0;
+
+        KAcc A[ACC + 1];
+#pragma unroll
+        for (int k = 0; k <= ACC; ++k) A[k] = KAcc{0.f, 0.f};
+#pragma unroll
+        for (int p = 0; p < NP; ++p) kacc_pair(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+        if (ex) kacc_one(A[ACC], fmaf(xi, xi, xr * xr), NP, kmask);
+
+        for (int it = 0; it < a.iterations && !conv; ++it) {
+            const int par = it & 1;
+            float bm1 = A[0].m1, bm2 = A[0].m2;
+#pragma unroll
+            for (int k = 1; k <= ACC; ++k) {
+                bm2 = fmax3(bm2, A[k].m2, fminf(bm1, A[k].m1));
+                bm1 = fmaxf(bm1, A[k].m1);
+            }
+            // ---- per-warp argmax, published with the winner lane's bins ----
+            const unsigned Mw = __reduce_max_sync(0xffffffffu, fbits(bm1));
+            const int wl = __ffs(__ballot_sync(0xffffffffu, fbits(bm1) == Mw)) - 1;
+            const unsigned Sw = __reduce_max_sync(0xffffffffu, fbits(lane == wl ? bm2 : bm1));
+            if (lane == wl) {
+                float4* sp = spills + (par * 2 + w) * (NP + 1);
+#pragma unroll
+                for (int p = 0; p < NP; ++p) sp[p] = make_float4(rp[p].x, rp[p].y, ip[p].x, ip[p].y);
+                sp[NP] = make_float4(xr, 0.f, xi, 0.f);
+                slots[par * 2 + w] = R2Slot{Mw, __uint_as_float(Sw), gb, wl};
+            }
+            named_bar_sync(bar, NT);
+            const R2Slot s0 = slots[par * 2], s1 = slots[par * 2 + 1];
+            const int ww = s1.key > s0.key ? 1 : 0;
+            const unsigned M = ww ? s1.key : s0.key;
+            const float S = fmaxf(ww ? s1.second : s0.second, __uint_as_float(ww ? s0.key : s1.key));
+            const int pw = 63 - static_cast<int>(M & 63u);
+            float2 pre;
+            int jw;
+            {
+                const float4 q = spills[(par * 2 + ww) * (NP + 1) + pw];
+                if (pw < NP) {
+                    const float ma = fmaf(q.z, q.z, q.x * q.x), mb = fmaf(q.w, q.w, q.y * q.y);
+                    const int half = mb > ma ? 1 : 0;
+                    pre = half ? make_float2(q.y, q.w) : make_float2(q.x, q.z);
+                    jw = 2 * pw + half;
+                } else {
+                    pre = make_float2(q.x, q.z);
+                    jw = SEG;
+                }
+            }
+            const int G = (ww ? s1.gbase : s0.gbase) + jw;
+
+            // ---- scalar part of iterate (engine_spectral.cpp:58-110), fp64, both warps ----
+            const double Mf = (double)__uint_as_float(M), Sf = (double)S;
+            if (energy < thr_e || !(Mf > 0.0) || Mf < thr_m) {
+                conv = 1;
+                break;
+            }
+            if (Sf > Mf * (1.0 - a.tau)) {
+                flagged = 1;
+                break;
+            }
+            const int u1 = G / T, u2 = G % T;
+            const int self = ((T - u1) % T == u1) && ((T - u2) % T == u2);
+            const double pr = pre.x, pi = pre.y;
+            const double2 P = ptab[(u1 * (a.Lh - 1) + u2 * (a.Lw - 1)) & (2 * T - 1)];
+            const double ar = pr * gw, ai = pi * gw;
+            double c_re = ar * P.x - ai * P.y, c_im = ar * P.y + ai * P.x;
+            double a_re = ar, a_im = ai, delta;
+            if (self) {
+                c_im = 0.0;
+                a_re = c_re * P.x;
+                a_im = -c_re * P.y;
+                delta = -2.0 * c_re * (pr * P.x - pi * P.y) + c_re * c_re * w0;
+            } else {
+                const int mi1 = 2 * u1, mi2 = 2 * u2;
+                const float v2 = vE[(mi1 & (T - 1)) * SRV + (mi2 & (T - 1))];
+                const double sig = ((mi1 >= T) ? (double)sgn_r : 1.0) * ((mi2 >= T) ? (double)sgn_c : 1.0);
+                delta = -4.0 * (a_re * pr + a_im * pi) + 2.0 * (a_re * a_re + a_im * a_im) * w0 +
+                        2.0 * sig * (double)v2 * (a_re * a_re - a_im * a_im);
+            }
+            const double e = energy + delta;
+            energy = 0.0 < e ? e : 0.0;
+            nu += 1;
+            if (tid == 0) {
+                const double iw = gw / a.gamma;
+                v2_record(a, b, nu, ntrace, rstride, tstride, a.rec_u_g + (size_t)b * rstride,
+                          a.rec_c_g + (size_t)b * rstride, u1, u2, self, (pr * P.x - pi * P.y) * iw,
+                          (pr * P.y + pi * P.x) * iw, c_re, c_im, energy, Mf, Sf);
+            }
+            ntrace += 1;
+
+            // ---- residual update of this warp's segment (+ fused next scan) ----
+            const float fr = (float)a_re, fi = (float)a_im;
+            const int pr2 = u2 & 1;
+            const float* vimg = vE + pr2 * (T * SRV);
+            const int rA = (k1 - u1) & (T - 1), rB = (k1 + u1) & (T - 1);
+            const int cA = (c0 - u2) & (T - 1), cB = (c0 + u2) & (T - 1);
+            const float s1f = ((k1 < u1) ? sgn_r : 1.f) * ((c0 < u2) ? sgn_c : 1.f);
+            const float s2f = ((k1 + u1 >= T) ? sgn_r : 1.f) * ((c0 + u2 >= T) ? sgn_c : 1.f);
+            const float2* va = reinterpret_cast<const float2*>(vimg + rA * SRV + (cA - pr2));
+            const float2* vb = reinterpret_cast<const float2*>(vimg + rB * SRV + (cB - pr2));
+            const float2 n1r = make_float2(-s1f * fr, -s1f * fr), n1i = make_float2(-s1f * fi, -s1f * fi);
+            const float2 n2r = make_float2(-s2f * fr, -s2f * fr), n2i = make_float2(s2f * fi, s2f * fi);
+#pragma unroll
+            for (int k = 0; k <= ACC; ++k) A[k] = KAcc{0.f, 0.f};
+            if (self) {
+#pragma unroll
+                for (int q = 0; q < PPS; ++q) {
+                    const float2 x = va[q];
+                    rp[q] = __ffma2_rn(n1r, x, rp[q]);
+                    ip[q] = __ffma2_rn(n1i, x, ip[q]);
+                    kacc_pair(A[q % ACC], __ffma2_rn(ip[q], ip[q], __fmul2_rn(rp[q], rp[q])), q, kmask);
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < PPS; ++q) {
+                    const float2 x = va[q], y = vb[q];
+                    rp[q] = __ffma2_rn(n2r, y, __ffma2_rn(n1r, x, rp[q]));
+                    ip[q] = __ffma2_rn(n2i, y, __ffma2_rn(n1i, x, ip[q]));
+                    kacc_pair(A[q % ACC], __ffma2_rn(ip[q], ip[q], __fmul2_rn(rp[q], rp[q])), q, kmask);
+                }
+            }
+            if (ex) {
+                const float x = vE[rA * SRV + cA + SEG];
+                xr = fmaf(-s1f * fr, x, xr);
+                xi = fmaf(-s1f * fi, x, xi);
+                if (!self) {
+                    const float y = vE[rB * SRV + cB + SEG];
+                    xr = fmaf(-s2f * fr, y, xr);
+                    xi = fmaf(s2f * fi, y, xi);
+                }
+                kacc_one(A[ACC], fmaf(xi, xi, xr * xr), NP, kmask);
+            }
+        }
+
+        if (a.rout) {
+            const size_t rs = a.rin_stride > 0 ? (size_t)a.rin_stride : (size_t)(NP + 1) * NT * 4;
+            float4* R = reinterpret_cast<float4*>(static_cast<float*>(a.rout) + (size_t)pos * rs);
+#pragma unroll
+            for (int p = 0; p < NP; ++p) R[p * NT + tid] = make_float4(rp[p].x, rp[p].y, ip[p].x, ip[p].y);
+            R[NP * NT + tid] = make_float4(xr, 0.f, xi, 0.f);
+        }
+        // both warps see the records written by tid 0 before synthesising
+        named_bar_sync(bar, NT);
+        v2_finish<T, NT>(a, a.blocks[pos], pos, b, tid, energy, nu, conv, flagged, ntrace,
+                         a.rec_u_g + (size_t)b * rstride, a.rec_c_g + (size_t)b * rstride, rstride, twi,
+                         red, bar);
+        named_bar_sync(bar, NT);
+    }
+}
+
+// ============================================================================
+// Complex path: asymmetric window masks (image borders, neighbouring losses).
+// ============================================================================
+template <int T>
+__global__ void __launch_bounds__(128, 3) k2v2c_kernel(K2Args a) {
+    using Cf = V2Cfg<T, PATH_F32_COMPLEX>;
+    constexpr int SEG = Cf::SEG, SPT = Cf::SPT, NT = Cf::NT, NB = Cf::NB, SR = Cf::SR;
+
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const Tile tile = a.tiles[blockIdx.x];
+    v2_stage<Cf>(a, tile, smem_raw);
+    const float2* wimg = reinterpret_cast<const float2*>(smem_raw);
+    const float2* twi = reinterpret_cast<const float2*>(smem_raw + Cf::OFF_TW);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool active = lane < NT;
+    float2* spill = reinterpret_cast<float2*>(reinterpret_cast<float4*>(smem_raw + Cf::OFF_SP) +
+                                              warp * (Cf::NP + SPT + 1));
+
+    const BinLayout L = BinLayout::make(T, SEG, SPT);
+    int k1s[SPT], c0s[SPT], exs[SPT];
+#pragma unroll
+    for (int s = 0; s < SPT; ++s) {
+        k1s[s] = c0s[s] = exs[s] = 0;
+        if (active) L.thread_segment(lane, s, &k1s[s], &c0s[s], &exs[s]);
+    }
+    const int gb0 = k1s[0] * T + c0s[0];
+    const int gb1 = k1s[SPT - 1] * T + c0s[SPT - 1];
     const double w0 = a.w0[tile.cls];
     const double inv_w0 = 1.0 / w0;
     const int rstride = a.rec_stride > 0 ? a.rec_stride : a.iterations;
@@ -107,7 +801,8 @@ __global__ void __launch_bounds__(128, 3) k2v2_kernel(K2Args a) {
 
         float2 r[NB];
         {
-            const float2* R = static_cast<const float2*>(a.rin) + (size_t)pos * Cf::SLOTS;
+            const size_t rs = a.rin_stride > 0 ? (size_t)a.rin_stride : (size_t)Cf::SLOTS * 2;
+            const float2* R = reinterpret_cast<const float2*>(static_cast<const float*>(a.rin) + (size_t)pos * rs);
 #pragma unroll
             for (int i = 0; i < NB; ++i) {
                 const int s = i / (SEG + 1), j = i % (SEG + 1);
@@ -127,7 +822,6 @@ __global__ void __launch_bounds__(128, 3) k2v2_kernel(K2Args a) {
         int ntrace = a.trace_from_nu0 ? nu : 0;
 
         for (int it = 0; it < a.iterations && !conv; ++it) {
-            // ---- local argmax (strict '>' in index order) + runner-up ----
             float m1 = 0.f, m2 = 0.f;
             int i1 = 0;
 #pragma unroll
@@ -140,7 +834,6 @@ __global__ void __launch_bounds__(128, 3) k2v2_kernel(K2Args a) {
                 m1 = fmaxf(m1, m);
                 i1 = gt ? i : i1;
             }
-            // ---- warp argmax: max |R|^2, then the lowest row-major index ----
             const unsigned M = __reduce_max_sync(0xffffffffu, fbits(m1));
             const int s1 = i1 / (SEG + 1), j1 = i1 % (SEG + 1);
             int g = INT_MAX;
@@ -148,8 +841,7 @@ __global__ void __launch_bounds__(128, 3) k2v2_kernel(K2Args a) {
             const unsigned G = __reduce_min_sync(0xffffffffu, static_cast<unsigned>(g));
             const bool win = static_cast<unsigned>(g) == G;
             const unsigned S = __reduce_max_sync(0xffffffffu, fbits(win ? m2 : m1));
-            const unsigned wmask = __ballot_sync(0xffffffffu, win);
-            const int wl = __ffs(wmask) - 1;
+            const int wl = __ffs(__ballot_sync(0xffffffffu, win)) - 1;
             const int iw = __shfl_sync(0xffffffffu, i1, wl);
             __syncwarp();
             if (lane == wl) {
@@ -159,211 +851,71 @@ __global__ void __launch_bounds__(128, 3) k2v2_kernel(K2Args a) {
             __syncwarp();
             const float2 pre = spill[iw];
 
-            // ---- scalar part of iterate (engine_spectral.cpp:58-110), fp64 ----
             const double Mf = (double)__uint_as_float(M), Sf = (double)__uint_as_float(S);
             if (e_init <= 0.0 || energy < 1e-12 * e_init || !(Mf > 0.0) || sqrt(Mf) < 1e-12 * imax) {
                 conv = 1;
                 break;
             }
             if (a.tau > 0.0 && Sf > Mf * (1.0 - a.tau)) {
-                flagged = 1;  // near-tie: re-run this block in fp64 (host)
+                flagged = 1;
                 break;
             }
             const int u1 = static_cast<int>(G) / T, u2 = static_cast<int>(G) % T;
             const int self = ((T - u1) % T == u1) && ((T - u2) % T == u2);
-            double c_re, c_im, p_re, p_im, upd_re, upd_im, delta;
             const double pr = pre.x, pi = pre.y;
-            if constexpr (REAL) {
-                const int m = (u1 * (a.Lh - 1) + u2 * (a.Lw - 1)) & (2 * T - 1);
-                const double2 P = ptab[m];  // e^{-j phi(u)}
-                const double ar = pr * inv_w0 * a.gamma, ai = pi * inv_w0 * a.gamma;
-                p_re = (pr * P.x - pi * P.y) * inv_w0;
-                p_im = (pr * P.y + pi * P.x) * inv_w0;
-                c_re = ar * P.x - ai * P.y;
-                c_im = ar * P.y + ai * P.x;
-                double a_re = ar, a_im = ai;
-                if (self) {
-                    c_im = 0.0;
-                    a_re = c_re * P.x;
-                    a_im = -c_re * P.y;
-                    delta = -2.0 * c_re * (pr * P.x - pi * P.y) + c_re * c_re * w0;
-                } else {
-                    const int mi1 = 2 * u1, mi2 = 2 * u2;
-                    const float v2 = wimg[(mi1 & (T - 1)) * SR + (mi2 & (T - 1))];
-                    const double sig = ((mi1 >= T) ? (double)sgn_r : 1.0) * ((mi2 >= T) ? (double)sgn_c : 1.0);
-                    delta = -4.0 * (a_re * pr + a_im * pi) + 2.0 * (a_re * a_re + a_im * a_im) * w0 +
-                            2.0 * sig * (double)v2 * (a_re * a_re - a_im * a_im);
-                }
-                upd_re = a_re;
-                upd_im = a_im;
+            const double p_re = pr * inv_w0, p_im = pi * inv_w0;
+            const double c_re = p_re * a.gamma, c_im = self ? 0.0 : p_im * a.gamma;
+            double delta;
+            if (self) {
+                delta = -2.0 * c_re * pr + c_re * c_re * w0;
             } else {
-                p_re = pr * inv_w0;
-                p_im = pi * inv_w0;
-                c_re = p_re * a.gamma;
-                c_im = self ? 0.0 : p_im * a.gamma;
-                if (self) {
-                    delta = -2.0 * c_re * pr + c_re * c_re * w0;
-                } else {
-                    const float2 w2 = wimg[((2 * u1) & (T - 1)) * SR + ((2 * u2) & (T - 1))];
-                    const double w2r = w2.x, w2i = -(double)w2.y;
-                    const double cc_r = c_re * c_re - c_im * c_im, cc_i = 2.0 * c_re * c_im;
-                    delta = -4.0 * (c_re * pr + c_im * pi) + 2.0 * (c_re * c_re + c_im * c_im) * w0 +
-                            2.0 * (cc_r * w2r - cc_i * w2i);
-                }
-                upd_re = c_re;
-                upd_im = c_im;
+                const float2 w2 = wimg[((2 * u1) & (T - 1)) * SR + ((2 * u2) & (T - 1))];
+                const double w2r = w2.x, w2i = -(double)w2.y;
+                const double cc_r = c_re * c_re - c_im * c_im, cc_i = 2.0 * c_re * c_im;
+                delta = -4.0 * (c_re * pr + c_im * pi) + 2.0 * (c_re * c_re + c_im * c_im) * w0 +
+                        2.0 * (cc_r * w2r - cc_i * w2i);
             }
             const double e = energy + delta;
             energy = 0.0 < e ? e : 0.0;
             nu += 1;
-            if (lane == 0) {
-                if (nu - 1 < rstride) {
-                    rec_u[nu - 1] = (u1 << 16) | u2;
-                    rec_c[nu - 1] = self ? make_double2(c_re, 0.0) : make_double2(2.0 * c_re, 2.0 * c_im);
-                }
-                if (a.trace && ntrace < tstride) {
-                    fofse_record rr;
-                    rr.nu = nu;
-                    rr.u1 = u1;
-                    rr.u2 = u2;
-                    rr.pad0 = 0;
-                    rr.p_re = p_re;
-                    rr.p_im = p_im;
-                    rr.c_re = c_re;
-                    rr.c_im = c_im;
-                    rr.gamma_effective = a.gamma;
-                    rr.weighted_energy = energy;
-                    rr.degenerate = 0;
-                    rr.pad1 = 0;
-                    a.trace[(size_t)b * tstride + ntrace] = rr;
-                }
-                if (a.gap_trace && ntrace < tstride)
-                    a.gap_trace[(size_t)b * tstride + ntrace] = (float)(Sf > 0.0 ? (Mf - Sf) / Mf : 1.0);
-            }
+            if (lane == 0)
+                v2_record(a, b, nu, ntrace, rstride, tstride, rec_u, rec_c, u1, u2, self, p_re, p_im,
+                          c_re, c_im, energy, Mf, Sf);
             ntrace += 1;
 
-            // ---- residual update over the owned bins (engine_spectral.cpp:112-125) ----
+            const float cr = (float)c_re, ci = (float)c_im;
 #pragma unroll
             for (int s = 0; s < SPT; ++s) {
                 const int k1 = k1s[s], c0 = c0s[s];
-                const int rA = (k1 - u1) & (T - 1), rB = (k1 + u1) & (T - 1);
-                const int cA = (c0 - u2) & (T - 1), cB = (c0 + u2) & (T - 1);
-                const WT* wa = wimg + rA * SR + cA;
-                const WT* wb = wimg + rB * SR + cB;
-                if constexpr (REAL) {
-                    const float s1 = ((k1 < u1) ? sgn_r : 1.f) * ((c0 < u2) ? sgn_c : 1.f);
-                    const float s2 = ((k1 + u1 >= T) ? sgn_r : 1.f) * ((c0 + u2 >= T) ? sgn_c : 1.f);
-                    const float ar = (float)upd_re, ai = (float)upd_im;
-                    const float2 na1 = make_float2(-s1 * ar, -s1 * ai);
-                    const float2 na2 = make_float2(-s2 * ar, s2 * ai);  // -(s2 conj(a))
-                    if (self) {
+                const float2* wa = wimg + ((k1 - u1) & (T - 1)) * SR + ((c0 - u2) & (T - 1));
+                const float2* wb = wimg + ((k1 + u1) & (T - 1)) * SR + ((c0 + u2) & (T - 1));
 #pragma unroll
-                        for (int j = 0; j <= SEG; ++j) {
-                            if (j == SEG && !exs[s]) break;
-                            const float x = wa[j];
-                            r[s * (SEG + 1) + j] = __ffma2_rn(na1, make_float2(x, x), r[s * (SEG + 1) + j]);
-                        }
-                    } else {
-#pragma unroll
-                        for (int j = 0; j <= SEG; ++j) {
-                            if (j == SEG && !exs[s]) break;
-                            const float x = wa[j], y = wb[j];
-                            float2 v = __ffma2_rn(na1, make_float2(x, x), r[s * (SEG + 1) + j]);
-                            r[s * (SEG + 1) + j] = __ffma2_rn(na2, make_float2(y, y), v);
-                        }
+                for (int j = 0; j <= SEG; ++j) {
+                    if (j == SEG && !exs[s]) break;
+                    float2 v = r[s * (SEG + 1) + j];
+                    const float2 x = wa[j];
+                    v.x = fmaf(-cr, x.x, fmaf(ci, x.y, v.x));
+                    v.y = fmaf(-cr, x.y, fmaf(-ci, x.x, v.y));
+                    if (!self) {
+                        const float2 y = wb[j];
+                        v.x = fmaf(-cr, y.x, fmaf(-ci, y.y, v.x));
+                        v.y = fmaf(-cr, y.y, fmaf(ci, y.x, v.y));
                     }
-                } else {
-                    const float cr = (float)upd_re, ci = (float)upd_im;
-#pragma unroll
-                    for (int j = 0; j <= SEG; ++j) {
-                        if (j == SEG && !exs[s]) break;
-                        float2 v = r[s * (SEG + 1) + j];
-                        const float2 x = wa[j];
-                        v.x = fmaf(-cr, x.x, fmaf(ci, x.y, v.x));
-                        v.y = fmaf(-cr, x.y, fmaf(-ci, x.x, v.y));
-                        if (!self) {
-                            const float2 y = wb[j];
-                            v.x = fmaf(-cr, y.x, fmaf(-ci, y.y, v.x));
-                            v.y = fmaf(-cr, y.y, fmaf(ci, y.x, v.y));
-                        }
-                        r[s * (SEG + 1) + j] = v;
-                    }
+                    r[s * (SEG + 1) + j] = v;
                 }
             }
         }
 
-        // ---- epilogue ----
-        if (lane == 0) {
-            const int sb = a.state_by_pos ? pos : b;
-            if (a.energy_out) a.energy_out[sb] = energy;
-            if (a.nu_out) a.nu_out[sb] = nu;
-            if (a.conv_out) a.conv_out[sb] = conv;
-            if (a.flags) a.flags[b] = flagged;
-            if (a.trace_count) a.trace_count[b] = ntrace;
-        }
         if (a.rout) {
-            float2* R = static_cast<float2*>(a.rout) + (size_t)pos * Cf::SLOTS;
+            const size_t rs = a.rin_stride > 0 ? (size_t)a.rin_stride : (size_t)Cf::SLOTS * 2;
+            float2* R = reinterpret_cast<float2*>(static_cast<float*>(a.rout) + (size_t)pos * rs);
 #pragma unroll
             for (int i = 0; i < NB; ++i) {
                 const int s = i / (SEG + 1), j = i % (SEG + 1);
                 if (active && (j < SEG || exs[s])) R[i * NT + lane] = r[i];
             }
         }
-        __syncwarp();
-        if (a.synth == SYN_NONE || flagged) continue;
-        const int nr = nu < rstride ? nu : rstride;
-        const int npx = a.reg_nr * a.reg_nc;
-        double sq = 0.0;
-        for (int p0 = 0; p0 < npx; p0 += 32 * 8) {
-            float acc[8];
-            int mm[8], nn[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                acc[k] = 0.f;
-                const int px = p0 + k * 32 + lane;
-                mm[k] = a.reg_r0 + (px < npx ? px / a.reg_nc : 0);
-                nn[k] = a.reg_c0 + (px < npx ? px % a.reg_nc : 0);
-            }
-            for (int q = 0; q < nr; ++q) {
-                const int u = rec_u[q];
-                const double2 cd = rec_c[q];
-                const float cx = (float)cd.x, cy = (float)cd.y;
-                const int uu1 = u >> 16, uu2 = u & 0xffff;
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const float2 t = twi[(uu1 * mm[k] + uu2 * nn[k]) & (T - 1)];
-                    acc[k] = fmaf(cx, t.x, fmaf(-cy, t.y, acc[k]));
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const int px = p0 + k * 32 + lane;
-                if (px >= npx) continue;
-                const int m = mm[k], n = nn[k];
-                if (a.synth == SYN_WINDOW) {
-                    a.models[(size_t)b * a.Lh * a.Lw + m * a.Lw + n] = acc[k];
-                } else {
-                    const double v0 = acc[k];
-                    const double v = v0 < 0.0 ? 0.0 : (v0 > 255.0 ? 255.0 : v0);
-                    const int64_t gi = (int64_t)desc.frame * a.fr.frame_stride +
-                                       (int64_t)(desc.row0 + m) * a.fr.width + (desc.col0 + n);
-                    double orig;
-                    if (a.fr.type == SRC_U8) {
-                        orig = (double)static_cast<const uint8_t*>(a.fr.src)[gi];
-                        static_cast<uint8_t*>(a.fr.dst)[gi] = static_cast<uint8_t>(round(v));
-                    } else {
-                        orig = static_cast<const double*>(a.fr.src)[gi];
-                        static_cast<double*>(a.fr.dst)[gi] = v;
-                    }
-                    sq += (orig - v) * (orig - v);
-                }
-            }
-        }
-        if (a.block_sq && a.synth == SYN_IMAGE) {
-#pragma unroll
-            for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-            if (lane == 0) a.block_sq[b] = sq;
-        }
+        v2_finish<T, 32>(a, desc, pos, b, lane, energy, nu, conv, flagged, ntrace, rec_u, rec_c, rstride, twi);
     }
 }
 
@@ -373,7 +925,8 @@ __global__ void __launch_bounds__(256) cvt_kernel(CvtArgs a) {
     const BinLayout Li = BinLayout::make(T, seg_for(T, 1), 1);
     const BinLayout Lo = BinLayout::make(T, a.out_seg, a.out_spt);
     const double2* in = a.in + (size_t)blockIdx.x * Li.SLOTS;
-    float2* out = a.out + (size_t)blockIdx.x * Lo.SLOTS;
+    float* out = reinterpret_cast<float*>(a.out) +
+                 (size_t)blockIdx.x * (a.out_stride > 0 ? (size_t)a.out_stride : packed32_floats(Lo, a.soa));
     for (int s = threadIdx.x; s < Lo.SLOTS; s += blockDim.x) {
         const int i = s / Lo.NT, tid = s % Lo.NT;
         int k1 = 0, k2 = 0;
@@ -385,23 +938,34 @@ __global__ void __launch_bounds__(256) cvt_kernel(CvtArgs a) {
             if (a.rotate) x = cmul(x, phase_pos<T>((long long)k1 * (a.Lh - 1) + (long long)k2 * (a.Lw - 1)));
             v = make_float2((float)x.x, (float)x.y);
         }
-        out[s] = v;
+        put_packed32(out, Lo, a.soa, i, tid, v.x, v.y);
     }
 }
 
 template <int T, int PATH>
 static int k2v2_launch_t(const K2Args& a, int32_t ntiles, cudaStream_t s) {
     using Cf = V2Cfg<T, PATH>;
-    cudaError_t e = cudaFuncSetAttribute(k2v2_kernel<T, PATH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)Cf::SMEM);
+    auto* fn = PATH == PATH_F32_REAL ? k2v2r_kernel<T> : k2v2c_kernel<T>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
     if (e != cudaSuccess) return e;
     if (ntiles <= 0) return cudaSuccess;
-    k2v2_kernel<T, PATH><<<ntiles, 32 * Cf::WARPS, Cf::SMEM, s>>>(a);
+    fn<<<ntiles, 32 * Cf::WARPS, Cf::SMEM, s>>>(a);
+    return cudaGetLastError();
+}
+
+template <int T>
+static int k2v2r2_launch(const K2Args& a, int32_t ntiles, cudaStream_t s) {
+    using Cf = V2R2Cfg<T>;
+    cudaError_t e = cudaFuncSetAttribute(k2v2r2_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
+    if (e != cudaSuccess) return e;
+    if (ntiles <= 0) return cudaSuccess;
+    k2v2r2_kernel<T><<<ntiles, Cf::NT * Cf::GROUPS, Cf::SMEM, s>>>(a);
     return cudaGetLastError();
 }
 
 template <int T>
 static int k2v2_T(const K2Args& a, int32_t ntiles, cudaStream_t s) {
+    if (a.path == PATH_F32_REAL && v2_real_gw(T) == 2) return k2v2r2_launch<T == 64 ? 64 : 64>(a, ntiles, s);
     if (a.path == PATH_F32_REAL) return k2v2_launch_t<T, PATH_F32_REAL>(a, ntiles, s);
     if (a.path == PATH_F32_COMPLEX) return k2v2_launch_t<T, PATH_F32_COMPLEX>(a, ntiles, s);
     return cudaErrorInvalidValue;
@@ -417,7 +981,16 @@ int k2v2_launch(const K2Args& a, int32_t ntiles, cudaStream_t s) {
     return cudaErrorInvalidValue;
 }
 
-int k2v2_warps_per_cta() { return 4; }
+int k2v2_warps_per_cta() { return 4; }  // lost blocks per CTA (both forms)
+
+static int g_real_gw = -1;
+int v2_real_gw(int t) {
+    if (g_real_gw < 0) {
+        const char* e = getenv("FOFSE_V2_REAL_GW");
+        g_real_gw = e ? atoi(e) : 1;
+    }
+    return (t == 64 && g_real_gw == 2) ? 2 : 1;
+}
 
 template <int T>
 static int cvt_t(const CvtArgs& a, cudaStream_t s) {

@@ -18,6 +18,8 @@
 // j in [0, SEG] (j == SEG is the extra slot), so every load is coalesced.
 #pragma once
 
+#include <stddef.h>
+
 #ifdef __CUDACC__
 #define FOFSE_HD __host__ __device__ __forceinline__
 #define FOFSE_HDC __host__ __device__ constexpr
@@ -118,6 +120,20 @@ FOFSE_HD void bin_slot(const BinLayout& L, int k1, int k2, int* i, int* tid) {
 FOFSE_HDC int v2_seg(int t) { return t <= 8 ? 4 : (t <= 16 ? 8 : (t <= 32 ? 16 : 32)); }
 FOFSE_HDC int v2_spt(int t) { return t == 64 ? 2 : 1; }
 FOFSE_HDC bool v2_supported(int t) { return t >= 8 && t <= 64; }
+// Row stride of K2v2's paired V images: T + SEG + 2 == 2 (mod 4), so 16 lanes on
+// consecutive rows hit distinct 8-byte bank pairs.
+FOFSE_HDC int v2_srv(int t) { return t + v2_seg(t) + 2; }
+// Warps per lost block of the K2v2 real path: T = 64 splits the block over two
+// warps (one 32-column segment each), smaller T keep one warp.
+// (host override for experiments: v2_set_real_gw)
+int v2_real_gw(int t);
+inline int v2_real_spt(int t) { return v2_real_gw(t) == 2 ? 1 : v2_spt(t); }
+
+// Floats per block of a packed fp32 residual: AoS float2 slots, or the K2v2
+// SoA pair layout (float4 per bin pair + one float4 per segment extra bin).
+FOFSE_HD size_t packed32_floats(const BinLayout& L, int soa) {
+    return soa ? (size_t)(L.SPT * L.SEG / 2 + L.SPT) * L.NT * 4 : (size_t)L.SLOTS * 2;
+}
 
 // Canonical representative test (basis.cpp:44-47).
 FOFSE_HD bool is_canonical(int t, int k1, int k2) {
