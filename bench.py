@@ -133,7 +133,7 @@ def cpu_reference_rate(wl, seed, budget_s, threads):
     cfg = wl.config("fp64")
     blocks_done, secs, frames = 0, 0.0, 0
     f = 0
-    while secs < budget_s and f < max(wl.frames, 1) * 4:
+    while (frames == 0 or secs < budget_s) and f < max(wl.frames, 1) * 4:
         img, pat = wl.frame(seed + 100000, f)
         t0 = time.perf_counter()
         impl.conceal(img.astype(np.float64), [tuple(b) for b in pat.blocks], wl.block, wl.block,

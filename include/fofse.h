@@ -124,6 +124,14 @@ int fofse_conceal_f64(fofse_ctx* ctx, const double* image, int32_t width, int32_
                       int32_t block_width, const fofse_params* params, double* restored,
                       fofse_record* traces, int32_t* trace_counts, fofse_report* report);
 
+/* Shard of fofse_conceal_f64 for multi-GPU runs: all n_blocks are lost (and
+ * validated), only blocks[first .. first+count) are concealed and written back
+ * (restored = image elsewhere); report covers the shard. */
+int fofse_conceal_shard_f64(fofse_ctx* ctx, const double* image, int32_t width, int32_t height,
+                            const fofse_rect* blocks, int64_t n_blocks, int64_t first,
+                            int64_t count, int32_t block_height, int32_t block_width,
+                            const fofse_params* params, double* restored, fofse_report* report);
+
 /* Batched uint8 frames (the video workload): frames n_frames*height*width,
  * frame f owns blocks[frame_offsets[f] .. frame_offsets[f+1]). restored is
  * written like the reference's write_pgm (std::round + clamp,

@@ -934,17 +934,21 @@ int fofse_set_stream(fofse_ctx* ctx, void* s) {
     });
 }
 
-int fofse_conceal_f64(fofse_ctx* ctx, const double* image, int32_t width, int32_t height,
-                      const fofse_rect* blocks, int64_t n, int32_t bh, int32_t bw,
-                      const fofse_params* params, double* restored, fofse_record* traces,
-                      int32_t* trace_counts, fofse_report* report) {
-    return guarded([&] {
-        if (!ctx || !image || !restored || (n && !blocks))
+static void conceal_f64_impl(fofse_ctx* ctx, const double* image, int32_t width, int32_t height,
+                             const fofse_rect* blocks, int64_t n_all, int64_t first, int64_t count,
+                             int32_t bh, int32_t bw, const fofse_params* params, double* restored,
+                             fofse_record* traces, int32_t* trace_counts, fofse_report* report) {
+        if (!ctx || !image || !restored || (n_all && !blocks))
             throw std::invalid_argument("conceal: NULL argument");
         if (width < 1 || height < 1) throw std::invalid_argument("grid dimensions must be >= 1");
+        if (first < 0 || count < 0 || first + count > n_all)
+            throw std::invalid_argument("conceal: shard out of range");
         const Cfg cfg = to_cfg(params);
-        const int64_t offs[2] = {0, n};
+        const int64_t offs[2] = {0, n_all};
         Job job = make_image_job(cfg, width, height, bh, bw, blocks, offs, 1);
+        if (first != 0 || count != n_all)  // shard: every block stays lost, only these are concealed
+            job.blocks = std::vector<BlockDesc>(job.blocks.begin() + first, job.blocks.begin() + first + count);
+        const int64_t n = count;
         ctx->activate();
         const size_t npx = static_cast<size_t>(width) * height;
         double* d_img = ctx->buf("img64").as<double>(npx);
@@ -975,6 +979,25 @@ int fofse_conceal_f64(fofse_ctx* ctx, const double* image, int32_t width, int32_
         for (double v : sq) tot += v;
         fill_report(report, ro, n, static_cast<int64_t>(job.cls_labels.size()), tot,
                     n * static_cast<int64_t>(bh) * bw, ctx->launches - l0);
+}
+
+int fofse_conceal_f64(fofse_ctx* ctx, const double* image, int32_t width, int32_t height,
+                      const fofse_rect* blocks, int64_t n, int32_t bh, int32_t bw,
+                      const fofse_params* params, double* restored, fofse_record* traces,
+                      int32_t* trace_counts, fofse_report* report) {
+    return guarded([&] {
+        conceal_f64_impl(ctx, image, width, height, blocks, n, 0, n, bh, bw, params, restored, traces,
+                         trace_counts, report);
+    });
+}
+
+int fofse_conceal_shard_f64(fofse_ctx* ctx, const double* image, int32_t width, int32_t height,
+                            const fofse_rect* blocks, int64_t n_blocks, int64_t first, int64_t count,
+                            int32_t bh, int32_t bw, const fofse_params* params, double* restored,
+                            fofse_report* report) {
+    return guarded([&] {
+        conceal_f64_impl(ctx, image, width, height, blocks, n_blocks, first, count, bh, bw, params,
+                         restored, nullptr, nullptr, report);
     });
 }
 

@@ -177,6 +177,24 @@ def conceal(image: np.ndarray, pattern: LossPattern, config: ConcealConfig | Non
     return ConcealOutput(restored, _report(config, rep, tr))
 
 
+def conceal_shard(image: np.ndarray, pattern: LossPattern, first: int, count: int,
+                  config: ConcealConfig | None = None, device: int = 0):
+    """Conceal blocks[first:first+count] only; every block of the pattern stays
+    lost (OUTSIDE in the others' windows). Returns (restored, report)."""
+    config = config or ConcealConfig()
+    image = np.ascontiguousarray(image, np.float64)
+    h, w = image.shape
+    rects = capi.rects_array(pattern.blocks)
+    restored = np.empty_like(image)
+    rep = capi.Report()
+    ctx = capi.context(device)
+    capi.check(capi.lib().fofse_conceal_shard_f64(
+        ctx.handle, capi.ptr(image), w, h, rects.ctypes.data_as(C.POINTER(capi.Rect_)), len(rects),
+        int(first), int(count), pattern.block_height, pattern.block_width, C.byref(config.params()),
+        capi.ptr(restored), C.byref(rep)))
+    return restored, _report(config, rep)
+
+
 def conceal_frames(frames: np.ndarray, patterns: list, config: ConcealConfig | None = None,
                    device: int = 0, inplace: bool = False):
     """Batched uint8 frames (video). Returns (restored u8 frames, per-block sq errors, report)."""

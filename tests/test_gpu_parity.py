@@ -297,3 +297,19 @@ def test_frames_u8_matches_f64_and_is_deterministic(gpu):
     o = P.conceal(frames[1].astype(np.float64), pats[1], cfg)
     np.testing.assert_array_equal(np.clip(np.floor(o.restored + 0.5), 0, 255).astype(np.uint8), a[1])
     assert rep.device["blocks"] == offs[-1]
+
+
+def test_shards_reassemble_the_full_run(gpu):
+    """fofse_conceal_shard_f64: disjoint shards (every block still lost) reproduce
+    the single-call result bit for bit — the multi-GPU decomposition."""
+    img, pat = WL.C1.frame(seed=12)
+    cfg = WL.C1.config()
+    full = P.conceal(img.astype(np.float64), pat, cfg).restored
+    out = img.astype(np.float64).copy()
+    n = len(pat.blocks)
+    for first in range(0, n, 37):
+        cnt = min(37, n - first)
+        r, _ = P.conceal_shard(img.astype(np.float64), pat, first, cnt, cfg)
+        for b in pat.blocks[first:first + cnt]:
+            out[b.row:b.row + 16, b.col:b.col + 16] = r[b.row:b.row + 16, b.col:b.col + 16]
+    np.testing.assert_array_equal(out, full)
