@@ -165,7 +165,7 @@ def conceal(image: np.ndarray, pattern: LossPattern, config: ConcealConfig | Non
     rep = capi.Report()
     ctx = capi.context(device)
     capi.check(capi.lib().fofse_conceal_f64(
-        ctx.handle, capi.ptr(image), w, h, rects.ctypes.data_as(C.POINTER(capi.Rect_)), n,
+        ctx.handle, capi.ptr(image), w, h, rects.ctypes.data_as(C.POINTER(capi.Rect_)), C.c_int64(n),
         pattern.block_height, pattern.block_width, C.byref(config.params()), capi.ptr(restored),
         capi.vptr(traces), capi.ptr(counts, C.c_int32), C.byref(rep)))
     tr = None
@@ -189,8 +189,8 @@ def conceal_shard(image: np.ndarray, pattern: LossPattern, first: int, count: in
     rep = capi.Report()
     ctx = capi.context(device)
     capi.check(capi.lib().fofse_conceal_shard_f64(
-        ctx.handle, capi.ptr(image), w, h, rects.ctypes.data_as(C.POINTER(capi.Rect_)), len(rects),
-        int(first), int(count), pattern.block_height, pattern.block_width, C.byref(config.params()),
+        ctx.handle, capi.ptr(image), w, h, rects.ctypes.data_as(C.POINTER(capi.Rect_)),
+        C.c_int64(len(rects)), C.c_int64(int(first)), C.c_int64(int(count)), pattern.block_height, pattern.block_width, C.byref(config.params()),
         capi.ptr(restored), C.byref(rep)))
     return restored, _report(config, rep)
 
@@ -244,7 +244,7 @@ def extrapolate_windows(windows: np.ndarray, masks: np.ndarray, config: ConcealC
         counts = np.zeros(n, np.int32)
     ctx = capi.context(device)
     capi.check(capi.lib().fofse_extrapolate_windows(
-        ctx.handle, capi.ptr(windows), capi.ptr(masks, C.c_uint8), n, wh, ww,
+        ctx.handle, capi.ptr(windows), capi.ptr(masks, C.c_uint8), C.c_int64(n), wh, ww,
         C.byref(config.params()), capi.ptr(models), capi.vptr(traces), capi.ptr(counts, C.c_int32)))
     it = config.iterations
     runs = []
@@ -320,7 +320,7 @@ class spectral:
         m = np.zeros(1)
         ctx = capi.context(device)
         capi.check(capi.lib().fofse_spectral_init(
-            ctx.handle, capi.ptr(f), capi.ptr(mask, C.c_uint8), capi.ptr(weight), 1, h, w, t,
+            ctx.handle, capi.ptr(f), capi.ptr(mask, C.c_uint8), capi.ptr(weight), C.c_int64(1), h, w, t,
             capi.ptr(rw.view(np.float64)), capi.ptr(ws.view(np.float64)), capi.ptr(w0), capi.ptr(e),
             capi.ptr(m)))
         return spectral.Spectrum(t, w, h, rw, ws, np.zeros((t, t), np.complex128), float(w0[0]),
@@ -344,7 +344,7 @@ class spectral:
         tc = np.zeros(1, np.int32)
         ctx = capi.context(device)
         capi.check(capi.lib().fofse_spectral_iterate(
-            ctx.handle, t, 1, spec.window_height, spec.window_width, capi.ptr(rw.view(np.float64)),
+            ctx.handle, t, C.c_int64(1), spec.window_height, spec.window_width, capi.ptr(rw.view(np.float64)),
             capi.ptr(ws.view(np.float64)), capi.ptr(g.view(np.float64)), capi.ptr(w0), capi.ptr(e),
             capi.ptr(ei), capi.ptr(im), capi.ptr(nu, C.c_int32), capi.ptr(cv, C.c_int32),
             C.c_double(gamma), int(iterations), _PRECS[precision], capi.vptr(tr),
@@ -364,6 +364,6 @@ class spectral:
         mi = np.zeros(1)
         ctx = capi.context(device)
         capi.check(capi.lib().fofse_spectral_synthesize(
-            ctx.handle, t, 1, capi.ptr(g.view(np.float64)), spec.window_height, spec.window_width,
+            ctx.handle, t, C.c_int64(1), capi.ptr(g.view(np.float64)), spec.window_height, spec.window_width,
             capi.ptr(out), capi.ptr(mi)))
         return out

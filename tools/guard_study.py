@@ -29,7 +29,7 @@ def diag(img, pat, cfg):
     gap = np.zeros(n * it, np.float32)
     capi.check(capi.lib().fofse_diag_conceal_f64(
         capi.context(0).handle, capi.ptr(img), img.shape[1], img.shape[0],
-        rects.ctypes.data_as(C.POINTER(capi.Rect_)), n, pat.block_height, pat.block_width,
+        rects.ctypes.data_as(C.POINTER(capi.Rect_)), C.c_int64(n), pat.block_height, pat.block_width,
         C.byref(cfg.params()), capi.ptr(restored), capi.vptr(tr), capi.ptr(tc, C.c_int32),
         capi.ptr(gap, C.c_float)))
     return restored, tr.reshape(n, it), tc, gap.reshape(n, it)

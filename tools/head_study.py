@@ -45,7 +45,7 @@ def init(t, ws, ls, wt):
     rw = np.zeros((n, t, t), np.complex128)
     W = np.zeros((n, t, t), np.complex128)
     w0, e, m = np.zeros(n), np.zeros(n), np.zeros(n)
-    capi.check(L.fofse_spectral_init(ctx.handle, capi.ptr(ws), capi.ptr(ls, C.c_uint8), capi.ptr(wt), n, h, w, t,
+    capi.check(L.fofse_spectral_init(ctx.handle, capi.ptr(ws), capi.ptr(ls, C.c_uint8), capi.ptr(wt), C.c_int64(n), h, w, t,
                                      capi.ptr(rw.view(np.float64)), capi.ptr(W.view(np.float64)), capi.ptr(w0),
                                      capi.ptr(e), capi.ptr(m)))
     return dict(rw=rw, W=W, w0=w0, e=e, e0=e.copy(), m=m, g=np.zeros_like(rw), nu=np.zeros(n, np.int32),
@@ -58,7 +58,7 @@ def iterate(st, t, h, w, gamma, its, prec):
     tc = np.zeros(n, np.int32)
     gap = np.zeros(n * max(its, 1), np.float32)
     capi.check(L.fofse_diag_spectral_iterate(
-        ctx.handle, t, n, h, w, capi.ptr(st["rw"].view(np.float64)), capi.ptr(st["W"].view(np.float64)),
+        ctx.handle, t, C.c_int64(n), h, w, capi.ptr(st["rw"].view(np.float64)), capi.ptr(st["W"].view(np.float64)),
         capi.ptr(st["g"].view(np.float64)), capi.ptr(st["w0"]), capi.ptr(st["e"]), capi.ptr(st["e0"]),
         capi.ptr(st["m"]), capi.ptr(st["nu"], C.c_int32), capi.ptr(st["cv"], C.c_int32), C.c_double(gamma), its,
         prec, capi.vptr(tr), capi.ptr(tc, C.c_int32), capi.ptr(gap, C.c_float)))
@@ -69,7 +69,7 @@ def synth(st, t, h, w):
     n = st["g"].shape[0]
     out = np.zeros((n, h, w))
     mi = np.zeros(n)
-    capi.check(L.fofse_spectral_synthesize(ctx.handle, t, n, capi.ptr(st["g"].view(np.float64)), h, w,
+    capi.check(L.fofse_spectral_synthesize(ctx.handle, t, C.c_int64(n), capi.ptr(st["g"].view(np.float64)), h, w,
                                            capi.ptr(out), capi.ptr(mi)))
     return out
 
