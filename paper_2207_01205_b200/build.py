@@ -19,8 +19,8 @@ OBJ = os.path.join(PKG, "_build")
 LIB_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIB_DIR, "libfofse.so")
 
-SOURCES = ["kernels.cu", "kernels_v2.cu", "engine.cpp", "gen.cpp", "microbench.cu"]
-HEADERS = ["kernels.h", "layout.h", "kcommon.cuh"]
+SOURCES = ["kernels.cu", "kernels_v2.cu", "kernels_f64.cu", "engine.cpp", "gen.cpp", "microbench.cu"]
+HEADERS = ["kernels.h", "layout.h", "kcommon.cuh", "v2common.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "nvcc")
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-Wall", "-I" + os.path.join(ROOT, "include")]

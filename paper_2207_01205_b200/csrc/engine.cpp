@@ -451,6 +451,13 @@ struct RunOut {
     int64_t reruns = 0, converged = 0, head = 0;
 };
 
+// FOFSE_F64_KERNEL=strict routes every fp64 iteration through the strict
+// (reference operation order) kernel instead of K2d (diagnostics).
+bool f64_strict_forced() {
+    const char* e = std::getenv("FOFSE_F64_KERNEL");
+    return e && std::string(e) == "strict";
+}
+
 // fp32 fast mode: the first `head` selections of every block run in fp64
 // (they carry the large coefficients whose fp32 rounding would otherwise
 // dominate the late-iteration residual).
@@ -499,9 +506,15 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
     const int head = resolve_head(cfg);
     out.head = head;
     const bool v2 = fp32 && v2_supported(T);
+    const bool use_d = d_supported(T) && !f64_strict_forced();  // K2d for symmetric masks
     auto path_of = [&](int cls) {
-        if (!fp32) return (int)PATH_F64_STRICT;
-        return sym[static_cast<size_t>(cls)] ? (int)PATH_F32_REAL : (int)PATH_F32_COMPLEX;
+        const bool sy = sym[static_cast<size_t>(cls)] != 0;
+        if (!fp32) return (sy && use_d) ? (int)PATH_F64_REAL : (int)PATH_F64_STRICT;
+        return sy ? (int)PATH_F32_REAL : (int)PATH_F32_COMPLEX;
+    };
+    // the fp64 kernel serving a range (fp64 mode, the fp32 mode's head and re-runs)
+    auto hi_path = [&](int p) {
+        return (use_d && (p == PATH_F32_REAL || p == PATH_F64_REAL)) ? (int)PATH_F64_REAL : (int)PATH_F64_STRICT;
     };
 
     const auto twf = twiddles(T, -1), twi = twiddles(T, +1);
@@ -524,6 +537,8 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
     const size_t vimg_elems = v2 ? 2 * static_cast<size_t>(T) * v2_srv(T) : static_cast<size_t>(T) * sr32;
     float* d_vimg32 = fp32 ? ctx->buf("vimg32").as<float>(static_cast<size_t>(ncls) * vimg_elems) : nullptr;
     double* d_w0 = ctx->buf("w0").as<double>(static_cast<size_t>(ncls));
+    const size_t vimg64_elems = 2 * static_cast<size_t>(T) * d_srv(T);
+    double* d_vimg64 = use_d ? ctx->buf("vimg64").as<double>(static_cast<size_t>(ncls) * vimg64_elems) : nullptr;
     {
         K1Args a{};
         a.T = T;
@@ -536,6 +551,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         a.wimg32 = d_wimg32;
         a.vimg32 = d_vimg32;
         a.vpairs = v2 ? 1 : 0;
+        a.vimg64 = d_vimg64;
         a.w0 = d_w0;
         a.twid = d_twf;
         ck(k1_launch(a, st), "K1 class spectra");
@@ -569,7 +585,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
     double* d_imax = ctx->buf("imax").as<double>(static_cast<size_t>(n));  // by position
     int32_t* d_flags = fp32 ? ctx->buf("flags").as<int32_t>(static_cast<size_t>(n)) : nullptr;
     int32_t* d_conv = ctx->buf("conv").as<int32_t>(static_cast<size_t>(n));  // by caller id
-    const bool rec_glob = fp32 || I > k2_smem_rec_cap(T, 0);
+    const bool rec_glob = fp32 || use_d || I > k2_smem_rec_cap(T, 0);
     int32_t* d_rec_u = nullptr;
     double2* d_rec_c = nullptr;
     if (rec_glob && I > 0) {
@@ -577,7 +593,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         d_rec_c = ctx->buf("rec_c").as<double2>(static_cast<size_t>(n) * I);
     }
     auto k1_packed = [&](const BlockDesc* descs, int64_t cnt, int path, int seg, int spt, void* outp,
-                         double* e, double* m, int soa = 0, int64_t stride = 0) {
+                         double* e, double* m, int soa = 0, int64_t stride = 0, cudaStream_t ks = nullptr) {
         K1Args a{};
         a.T = T;
         a.Lh = g.Lh;
@@ -596,7 +612,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         a.energy = e;
         a.init_max = m;
         a.twid = d_twf;
-        ck(k1_launch(a, st), "K1 residual spectra");
+        ck(k1_launch(a, ks ? ks : st), "K1 residual spectra");
         ++ctx->launches;
     };
     auto base_args = [&]() {
@@ -639,10 +655,31 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
     // ---- phase A: residual spectra ----
     char* d_R64 = nullptr;
     char* d_R32 = nullptr;
+    const size_t r64_bytes = sizeof(double2) * L64.SLOTS;  // per block
     if (!fp32 || head > 0) {
-        d_R64 = ctx->buf("R64").as<char>(static_cast<size_t>(n) * sizeof(double2) * L64.SLOTS);
-        k1_packed(d_sorted, n, PATH_F64_STRICT, seg64, 1, d_R64, d_e0, d_imax);
+        d_R64 = ctx->buf("R64").as<char>(static_cast<size_t>(n) * r64_bytes);
+        for (const Range& r : ranges)
+            k1_packed(d_sorted + r.begin, r.end - r.begin, hi_path(r.path), seg64, 1,
+                      d_R64 + static_cast<size_t>(r.begin) * r64_bytes, d_e0 + r.begin, d_imax + r.begin);
     }
+    // one fp64 iteration launch over positions [b0, b1) of `descs` (K2d or strict)
+    auto k2_f64 = [&](K2Args a, int hp, int64_t b0, int64_t b1, const std::vector<BlockDesc>& descs,
+                      const std::string& tag, cudaStream_t s) {
+        const int ng = hp == PATH_F64_REAL ? k2d_blocks_per_cta(T) : k2_groups_per_cta(T, PATH_F64_STRICT);
+        std::vector<Tile> tl = make_tiles(b0, b1, descs, ng);
+        Tile* d_tl = upload(ctx, "tiles64" + tag, tl.data(), tl.size(), s);
+        a.path = hp;
+        a.seg = seg64;
+        a.tau = 0.0;
+        a.tiles = d_tl;
+        a.wimg = hp == PATH_F64_REAL ? (const void*)d_vimg64 : (const void*)d_wimg64;
+        a.wimg_stride = hp == PATH_F64_REAL ? static_cast<int64_t>(vimg64_elems) : static_cast<int64_t>(T) * sr64;
+        if (hp == PATH_F64_REAL)
+            ck(k2d_launch(a, static_cast<int32_t>(tl.size()), s), "K2d fp64");
+        else
+            ck(k2_launch(a, static_cast<int32_t>(tl.size()), s), "K2 fp64");
+        ++ctx->launches;
+    };
     // fp32 residuals: AoS float2 slots (complex path, T = 128) or, for the K2v2
     // real path, SoA bin pairs; one common per-block stride (floats)
     auto soa_of = [&](int path) { return (v2 && path == PATH_F32_REAL) ? 1 : 0; };
@@ -662,16 +699,8 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
     int32_t* d_nu = nullptr;
     int32_t* d_cvh = nullptr;
     if (!fp32 || head > 0) {
-        std::vector<Tile> tl = tiles_for(0, n, k2_groups_per_cta(T, PATH_F64_STRICT));
-        Tile* d_tl = upload(ctx, "tiles64", tl.data(), tl.size());
         K2Args a = base_args();
-        a.path = PATH_F64_STRICT;
-        a.seg = seg64;
-        a.tau = 0.0;
-        a.tiles = d_tl;
         a.rin = d_R64;
-        a.wimg = d_wimg64;
-        a.wimg_stride = static_cast<int64_t>(T) * sr64;
         a.rec_global = fp32 ? 1 : 0;
         if (fp32) {
             // head: `head` selections, state handed to the fp32 phase by position
@@ -688,8 +717,8 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             a.trace_count = nullptr;
             a.gap_trace = nullptr;
         }
-        ck(k2_launch(a, static_cast<int32_t>(tl.size()), st), "K2 fp64");
-        ++ctx->launches;
+        for (size_t i = 0; i < ranges.size(); ++i)
+            k2_f64(a, hi_path(ranges[i].path), ranges[i].begin, ranges[i].end, sorted, std::to_string(i), st);
     }
     // ---- phase C: fp32 fast mode ----
     // Asymmetric-mask blocks (few, image borders) run on the side stream,
@@ -708,11 +737,11 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
                 c.Lh = g.Lh;
                 c.Lw = g.Lw;
                 c.n = static_cast<int32_t>(r.end - r.begin);
-                c.in = reinterpret_cast<const double2*>(d_R64) + static_cast<size_t>(r.begin) * L64.SLOTS;
+                c.in = reinterpret_cast<const double2*>(d_R64 + static_cast<size_t>(r.begin) * r64_bytes);
                 c.out = reinterpret_cast<float2*>(d_R32 + static_cast<size_t>(r.begin) * sizeof(float) * s32);
                 c.out_seg = seg32;
                 c.out_spt = spt_of(r.path);
-                c.rotate = r.path == PATH_F32_REAL;
+                c.rotate = r.path == PATH_F32_REAL && hi_path(r.path) != PATH_F64_REAL;  // K2d head is rotated
                 c.soa = soa_of(r.path);
                 c.out_stride = s32;
                 ck(cvt_launch(c, rs), "convert head state");
@@ -770,28 +799,41 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             const int64_t m = static_cast<int64_t>(rr.size());
             BlockDesc* d_rdesc = upload(ctx, "rdesc", rdesc.data(), rdesc.size());
             int32_t* d_rr = upload(ctx, "rr", rr.data(), rr.size());
-            double2* d_Rr = ctx->buf("Rr").as<double2>(static_cast<size_t>(m) * L64.SLOTS);
+            char* d_Rr = ctx->buf("Rr").as<char>(static_cast<size_t>(m) * r64_bytes);
             double* d_re0 = ctx->buf("re0").as<double>(static_cast<size_t>(m));
             double* d_rimax = ctx->buf("rimax").as<double>(static_cast<size_t>(m));
-            k1_packed(d_rdesc, m, PATH_F64_STRICT, seg64, 1, d_Rr, d_re0, d_rimax);
-            std::vector<Tile> tl = make_tiles(0, m, rdesc, k2_groups_per_cta(T, PATH_F64_STRICT));
-            Tile* d_rt = upload(ctx, "rtiles", tl.data(), tl.size());
             K2Args a = base_args();
-            a.path = PATH_F64_STRICT;
-            a.seg = seg64;
-            a.tau = 0.0;
-            a.tiles = d_rt;
             a.order = d_rr;
             a.blocks = d_rdesc;
             a.rin = d_Rr;
-            a.wimg = d_wimg64;
-            a.wimg_stride = static_cast<int64_t>(T) * sr64;
             a.energy0 = d_re0;
             a.init_energy = d_re0;
             a.init_max = d_rimax;
-            a.rec_global = 0;  // smem records (or the per-block global scratch when I > cap)
-            ck(k2_launch(a, static_cast<int32_t>(tl.size()), st), "K2 rerun");
-            ++ctx->launches;
+            a.rec_global = 0;  // strict: smem records (or the per-block global scratch when I > cap)
+            // re-run blocks arrive grouped by path (ids order): one K1 + K2 per fp64
+            // path; the (few, latency-bound) strict blocks run on the side stream
+            // concurrently with the K2d blocks
+            ck(cudaEventRecord(ctx->ev[4], st), "event");
+            bool side_used = false;
+            for (int64_t q0 = 0, k = 0; q0 < m; ++k) {
+                const int hp = hi_path(path_of(rdesc[static_cast<size_t>(q0)].cls));
+                int64_t q1 = q0;
+                while (q1 < m && hi_path(path_of(rdesc[static_cast<size_t>(q1)].cls)) == hp) ++q1;
+                cudaStream_t rs = st;
+                if (hp == PATH_F64_STRICT && use_d) {
+                    if (!side_used) ck(cudaStreamWaitEvent(ctx->side, ctx->ev[4], 0), "wait");
+                    side_used = true;
+                    rs = ctx->side;
+                }
+                k1_packed(d_rdesc + q0, q1 - q0, hp, seg64, 1, d_Rr + static_cast<size_t>(q0) * r64_bytes,
+                          d_re0 + q0, d_rimax + q0, 0, 0, rs);
+                k2_f64(a, hp, q0, q1, rdesc, "r" + std::to_string(k), rs);
+                q0 = q1;
+            }
+            if (side_used) {
+                ck(cudaEventRecord(ctx->ev[5], ctx->side), "event");
+                ck(cudaStreamWaitEvent(st, ctx->ev[5], 0), "wait");
+            }
         }
     }
     ck(cudaEventRecord(ctx->ev[3], st), "event");

@@ -157,6 +157,21 @@ __global__ void __launch_bounds__(256) k1_kernel(K1Args a) {
                 o[i] = static_cast<float>(v);
             }
         }
+        if (a.vimg64) {
+            // fp64 rotated real V, even / odd copies (K2d): E[c] = V[c], O[c] = V[c+1]
+            const int srv = d_srv(T);
+            double* o = a.vimg64 + (size_t)b * 2 * T * srv;
+            for (int i = threadIdx.x; i < 2 * T * srv; i += blockDim.x) {
+                const int cp = i / (T * srv), rem = i % (T * srv);
+                const int r = rem / srv, col = rem % srv + cp;
+                const int k2 = col % T;
+                const double2 w = k1_spec<T>(cbuf, r, k2);
+                const double2 ph = phase_pos<T>((long long)r * (a.Lh - 1) + (long long)k2 * (a.Lw - 1));
+                double v = w.x * ph.x - w.y * ph.y;
+                if (col >= T) v *= sc;
+                o[i] = v;
+            }
+        }
         if (threadIdx.x == 0 && a.w0) a.w0[b] = cbuf[0].x;
         return;
     }
@@ -172,7 +187,7 @@ __global__ void __launch_bounds__(256) k1_kernel(K1Args a) {
         }
     } else {
         const BinLayout L = BinLayout::make(T, a.seg, a.spt > 0 ? a.spt : 1);
-        const bool rotate = a.path == PATH_F32_REAL;
+        const bool rotate = path_is_rotated(a.path);
         const size_t per = a.out_stride > 0 ? (size_t)a.out_stride : packed32_floats(L, a.soa);
         for (int s = threadIdx.x; s < L.SLOTS; s += blockDim.x) {
             const int j = s / L.NT, tid = s % L.NT;
@@ -186,7 +201,7 @@ __global__ void __launch_bounds__(256) k1_kernel(K1Args a) {
                     v = cmul(v, phase_pos<T>((long long)k1 * (a.Lh - 1) + (long long)k2 * (a.Lw - 1)));
                 }
             }
-            if (a.path == PATH_F64_STRICT)
+            if (path_is_f64(a.path))
                 static_cast<double2*>(a.out)[(size_t)b * L.SLOTS + s] = v;
             else
                 put_packed32(static_cast<float*>(a.out) + (size_t)b * per, L, a.soa, j, tid,
@@ -799,7 +814,7 @@ __global__ void __launch_bounds__(256) kl_lines(double2* data, int64_t n, int co
 // ----------------------------------------------------------------------------
 // launchers
 // ----------------------------------------------------------------------------
-int seg_of(int T, int path) { return seg_for(T, path == PATH_F64_STRICT); }
+int seg_of(int T, int path) { return seg_for(T, path_is_f64(path)); }
 
 template <int T>
 static int k1_launch_t(const K1Args& a, cudaStream_t s) {

@@ -24,7 +24,10 @@ enum IterPath : int {
     PATH_F64_STRICT = 0,  // complex W, reference op order, no FMA
     PATH_F32_COMPLEX = 1, // complex W (asymmetric window masks)
     PATH_F32_REAL = 2,    // point-symmetric masks: rotated frame, real V
+    PATH_F64_REAL = 3,    // fp64 rotated frame, real V (K2d; T <= 64)
 };
+__host__ __device__ inline bool path_is_f64(int p) { return p == PATH_F64_STRICT || p == PATH_F64_REAL; }
+__host__ __device__ inline bool path_is_rotated(int p) { return p == PATH_F32_REAL || p == PATH_F64_REAL; }
 
 enum SrcType : int { SRC_U8 = 0, SRC_F64 = 1 };
 
@@ -68,6 +71,7 @@ struct K1Args {
     double2* wimg64;           // [ncls][T*SR64] complex fp64 image (SEG of fp64)
     float2* wimg32;            // [ncls][T*SR32] complex fp32 image
     float* vimg32;             // [ncls][T*SR32] rotated real image ([ncls][2][T*SRV] with vpairs)
+    double* vimg64;            // [ncls][2][T*d_srv(T)] fp64 rotated real image, even/odd pairs (K2d)
     int32_t vpairs;            // write the K2v2 even/odd paired V layout
     double* w0;                // [ncls]
     const double2* twid;       // e^{-j 2 pi k / T}, k < T
@@ -141,6 +145,9 @@ int fft2d_launch(double2* data, int64_t n, int32_t T, int32_t dir, const double2
 
 // K2v2: single-warp fp32 iteration kernel (T <= 64); convert fp64 head state.
 int k2v2_launch(const K2Args& a, int32_t ntiles, cudaStream_t s);
+// K2d: fp64 rotated-frame iteration (PATH_F64_REAL), groups of d_group_threads(T).
+int k2d_launch(const K2Args& a, int32_t ntiles, cudaStream_t s);
+int k2d_blocks_per_cta(int T);
 int k2v2_warps_per_cta();
 int cvt_launch(const CvtArgs& a, cudaStream_t s);
 

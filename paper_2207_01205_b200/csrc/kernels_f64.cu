@@ -1,0 +1,311 @@
+// kernels_f64.cu — K2d: the FOFSE iteration in fp64 for point-symmetric window
+// masks (the rotated frame of DESIGN.md §4), T <= 64.
+//
+// Reference loop: engine_spectral.cpp:20-33 (find_peak), :51-144 (iterate),
+// :195-208 (synthesize_model), pipeline.cpp:226-232 (write-back). K2d keeps
+// the fp64 precision of the reference but not its operation order:
+//  * R' = conj(P) R and W = P V with V real: the update of a bin is four DFMA
+//    against two real V gathers (the strict kernel: 8 DMUL/DADD against two
+//    complex W gathers); V is held twice in shared memory (even / odd aligned)
+//    so every bin pair is one 16-byte LDS;
+//  * the argmax runs on 64-bit keys: |R'|^2 (== |R|^2) with its 12 low mantissa
+//    bits replaced by 4095 - G (G = row-major bin index). One u64 max gives the
+//    largest value and, among values equal to 2^-40 relative, the lowest index —
+//    the reference's strict '>' scan in row-major order;
+//  * a block-group (4 warps at T = 64) owns one lost block; per iteration each
+//    warp reduces its key with REDUX.SYNC (hi word, then lo word), the winner
+//    lane publishes (key, G, R'[G]) to a parity-double-buffered slot, ONE named
+//    barrier, then every thread resolves the same group winner and runs the
+//    scalar part of iterate redundantly (no controller hand-off);
+//  * the next scan is fused into the update (one pass over the registers).
+// Used for fp64 concealment, the fp32 mode's fp64 head and its guard re-runs.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "kcommon.cuh"
+#include "kernels.h"
+#include "layout.h"
+#include "v2common.cuh"
+
+namespace fofse {
+
+template <int T>
+struct DCfg {
+    static constexpr int SEG = seg_for(T, 1);
+    static constexpr int HT = T / 2;
+    static constexpr int QN = T / SEG;
+    static constexpr int NT = HT * QN;             // threads holding bins
+    static constexpr int GT = NT < 32 ? 32 : NT;  // threads per block-group
+    static constexpr int NW = GT / 32;
+    static constexpr int PPS = SEG / 2;
+    static constexpr int SRV = d_srv(T);
+    static constexpr int GROUPS = 256 / GT;  // lost blocks per CTA
+    static constexpr bool REAL = true;
+    static constexpr size_t IMG_BYTES = (size_t)2 * T * SRV * sizeof(double);
+    static constexpr bool TW64 = true;
+    static constexpr size_t WBYTES = ((IMG_BYTES + 15) / 16) * 16;
+    static constexpr size_t OFF_P = WBYTES;                            // 2T double2
+    static constexpr size_t OFF_TW = OFF_P + sizeof(double2) * 2 * T;  // T double2
+    static constexpr size_t GRP = ((2 * NW * 32 + 8 * NW + 15) / 16) * 16;  // slots[2][NW] + red[NW]
+    static constexpr size_t OFF_G = OFF_TW + sizeof(double2) * T;
+    static constexpr size_t OFF_BAR = OFF_G + GRP * GROUPS;
+    static constexpr size_t SMEM = OFF_BAR + 16;
+    static_assert(T * T <= 4096, "key index bits");
+    static_assert(SEG % 2 == 0 && SEG <= 16, "bin pairs");
+};
+
+struct DSlot {
+    unsigned hi, lo;  // the warp's best key
+    int g, pad;
+    double pre_re, pre_im;  // R'[g]
+};
+static_assert(sizeof(DSlot) == 32, "slot");
+
+constexpr unsigned long long DKEY_MASK = 0xFFFFFFFFFFFFF000ull;
+constexpr int DKEY_TOP = 4095;
+
+__device__ __forceinline__ void dscan(unsigned long long& K, double re, double im, unsigned kidx) {
+    const double m = fma(im, im, re * re);
+    const unsigned long long key = (static_cast<unsigned long long>(__double_as_longlong(m)) & DKEY_MASK) | kidx;
+    K = key > K ? key : K;
+}
+
+// R'[j] of the winner lane by a (lane-local) jump on j.
+template <int NB>
+__device__ __forceinline__ double2 dpick(int j, const double* re, const double* im) {
+    double2 q = make_double2(0.0, 0.0);
+    switch (j) {
+#define DPICK(J) \
+    case J:      \
+        if (J < NB) q = make_double2(re[J < NB ? J : 0], im[J < NB ? J : 0]); \
+        break;
+        DPICK(0) DPICK(1) DPICK(2) DPICK(3) DPICK(4) DPICK(5) DPICK(6) DPICK(7) DPICK(8)
+        DPICK(9) DPICK(10) DPICK(11) DPICK(12) DPICK(13) DPICK(14) DPICK(15) DPICK(16)
+#undef DPICK
+        default: break;
+    }
+    return q;
+}
+
+template <int T>
+__global__ void __launch_bounds__(256, 2) k2d_kernel(K2Args a) {
+    using Cf = DCfg<T>;
+    constexpr int SEG = Cf::SEG, NT = Cf::NT, GT = Cf::GT, NW = Cf::NW, PPS = Cf::PPS, SRV = Cf::SRV;
+    constexpr int NB = SEG + 1;
+
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const Tile tile = a.tiles[blockIdx.x];
+    v2_stage<Cf>(a, tile, smem_raw);
+    const double* vE = reinterpret_cast<const double*>(smem_raw);
+    const double2* ptab = reinterpret_cast<const double2*>(smem_raw + Cf::OFF_P);
+    const double2* twi = reinterpret_cast<const double2*>(smem_raw + Cf::OFF_TW);
+
+    const int grp = threadIdx.x / GT, ltid = threadIdx.x % GT;
+    const int w = ltid >> 5;
+    const bool active = ltid < NT;
+    unsigned char* gsm = smem_raw + Cf::OFF_G + Cf::GRP * grp;
+    DSlot* slots = reinterpret_cast<DSlot*>(gsm);  // [2][NW]
+    double* red = reinterpret_cast<double*>(gsm + 2 * NW * 32);
+    const int bar = 1 + grp;
+
+    const BinLayout L = BinLayout::make(T, SEG, 1);
+    int k1 = 0, c0 = 0, ex = 0;
+    if (active) L.segment(ltid, &k1, &c0, &ex);
+    const int gbase = k1 * T + c0;
+    const unsigned kbase = static_cast<unsigned>(DKEY_TOP - gbase);
+    const double sgn_r = ((a.Lh - 1) & 1) ? -1.0 : 1.0;
+    const double sgn_c = ((a.Lw - 1) & 1) ? -1.0 : 1.0;
+    const int rstride = a.rec_stride > 0 ? a.rec_stride : a.iterations;
+    const int tstride = a.trace_stride > 0 ? a.trace_stride : a.iterations;
+    const double w0 = a.w0[tile.cls], gw = a.gamma / w0, iw = 1.0 / w0;
+
+    for (int bi = grp; bi < tile.count; bi += Cf::GROUPS) {
+        const int pos = tile.begin + bi;
+        const int b = a.order[pos];
+        double re[NB], im[NB];
+        {
+            const double2* R = static_cast<const double2*>(a.rin) + (size_t)pos * L.SLOTS;
+#pragma unroll
+            for (int j = 0; j < SEG; ++j) {
+                const double2 v = active ? R[j * NT + ltid] : make_double2(0.0, 0.0);
+                re[j] = v.x;
+                im[j] = v.y;
+            }
+            const double2 v = (active && ex) ? R[SEG * NT + ltid] : make_double2(0.0, 0.0);
+            re[SEG] = v.x;
+            im[SEG] = v.y;
+        }
+        int* rec_u = a.rec_u_g + (size_t)b * rstride;
+        double2* rec_c = a.rec_c_g + (size_t)b * rstride;
+        double energy = a.energy0[pos];
+        const double e_init = a.init_energy[pos];
+        const double thr_e = 1e-12 * e_init;
+        const double thr_m = (1e-12 * a.init_max[pos]) * (1e-12 * a.init_max[pos]);
+        int nu = a.nu0 ? a.nu0[pos] : 0;
+        int ntrace = a.trace_from_nu0 ? nu : 0;
+        int conv = (a.conv0 ? a.conv0[pos] : 0) | (e_init <= 0.0);
+
+        unsigned long long KA = 0, KB = 0;  // two independent max chains
+#pragma unroll
+        for (int j = 0; j < SEG; ++j) dscan((j & 1) ? KB : KA, re[j], im[j], kbase - j);
+        if (ex) dscan(KA, re[SEG], im[SEG], kbase - SEG);
+
+        for (int it = 0; it < a.iterations && !conv; ++it) {
+            const int par = it & 1;
+            unsigned long long K = KA > KB ? KA : KB;
+            if (!active) K = 0;
+            // ---- warp argmax on the 64-bit key (unique: the index is in it) ----
+            const unsigned hi = static_cast<unsigned>(K >> 32), lo = static_cast<unsigned>(K);
+            const unsigned Mhi = __reduce_max_sync(0xffffffffu, hi);
+            const unsigned Mlo = __reduce_max_sync(0xffffffffu, hi == Mhi ? lo : 0u);
+            if (hi == Mhi && lo == Mlo) {
+                const int g = DKEY_TOP - static_cast<int>(Mlo & 0xFFFu);
+                const double2 pre = dpick<NB>(g - gbase, re, im);
+                slots[par * NW + w] = DSlot{Mhi, Mlo, g, 0, pre.x, pre.y};
+            }
+            if constexpr (NW == 1)
+                __syncwarp();
+            else
+                named_bar_sync(bar, GT);
+            DSlot s = slots[par * NW];
+#pragma unroll
+            for (int k = 1; k < NW; ++k) {
+                const DSlot o = slots[par * NW + k];
+                if (o.hi > s.hi || (o.hi == s.hi && o.lo > s.lo)) s = o;
+            }
+
+            // ---- scalar part of iterate (engine_spectral.cpp:58-110), every thread ----
+            const double pr = s.pre_re, pi = s.pre_im;
+            const double M = fma(pi, pi, pr * pr);
+            if (energy < thr_e || !(M > 0.0) || M < thr_m) {
+                conv = 1;
+                break;
+            }
+            const int G = s.g;
+            const int u1 = G / T, u2 = G % T;
+            const int self = ((T - u1) % T == u1) && ((T - u2) % T == u2);
+            const double2 P = ptab[(u1 * (a.Lh - 1) + u2 * (a.Lw - 1)) & (2 * T - 1)];  // e^{-j phi(u)}
+            const double ar = pr * gw, ai = pi * gw;  // a = gamma R'[u] / w0
+            double c_re = ar * P.x - ai * P.y, c_im = ar * P.y + ai * P.x;  // c = P a
+            double a_re = ar, a_im = ai, delta;
+            if (self) {
+                c_im = 0.0;
+                a_re = c_re * P.x;
+                a_im = -c_re * P.y;
+                delta = -2.0 * c_re * (pr * P.x - pi * P.y) + c_re * c_re * w0;
+            } else {
+                const int mi1 = 2 * u1, mi2 = 2 * u2;
+                const double v2 = vE[(mi1 & (T - 1)) * SRV + (mi2 & (T - 1))];
+                const double sig = ((mi1 >= T) ? sgn_r : 1.0) * ((mi2 >= T) ? sgn_c : 1.0);
+                delta = -4.0 * (a_re * pr + a_im * pi) + 2.0 * (a_re * a_re + a_im * a_im) * w0 +
+                        2.0 * sig * v2 * (a_re * a_re - a_im * a_im);
+            }
+            const double e = energy + delta;
+            energy = 0.0 < e ? e : 0.0;
+            nu += 1;
+            if (ltid == 0) {
+                v2_record(a, b, nu, ntrace, rstride, tstride, rec_u, rec_c, u1, u2, self,
+                          (pr * P.x - pi * P.y) * iw, (pr * P.y + pi * P.x) * iw, c_re, c_im, energy, M, 0.0);
+            }
+            ntrace += 1;
+
+            // ---- residual update R' -= s1 a V[k-u] + s2 conj(a) V[k+u], fused next scan ----
+            const int p2 = u2 & 1;
+            const double* vimg = vE + p2 * (T * SRV);  // odd copy holds V[c+1]
+            const int rA = (k1 - u1) & (T - 1), rB = (k1 + u1) & (T - 1);
+            const int cA = (c0 - u2) & (T - 1), cB = (c0 + u2) & (T - 1);
+            const double s1 = ((k1 < u1) ? sgn_r : 1.0) * ((c0 < u2) ? sgn_c : 1.0);
+            const double s2 = ((k1 + u1 >= T) ? sgn_r : 1.0) * ((c0 + u2 >= T) ? sgn_c : 1.0);
+            const double2* va = reinterpret_cast<const double2*>(vimg + rA * SRV + (cA - p2));
+            const double2* vb = reinterpret_cast<const double2*>(vimg + rB * SRV + (cB - p2));
+            const double n1r = -s1 * a_re, n1i = -s1 * a_im;
+            const double n2r = -s2 * a_re, n2i = s2 * a_im;
+            KA = 0;
+            KB = 0;
+            if (self) {
+#pragma unroll
+                for (int q = 0; q < PPS; ++q) {
+                    const double2 x = va[q];
+                    re[2 * q] = fma(n1r, x.x, re[2 * q]);
+                    im[2 * q] = fma(n1i, x.x, im[2 * q]);
+                    re[2 * q + 1] = fma(n1r, x.y, re[2 * q + 1]);
+                    im[2 * q + 1] = fma(n1i, x.y, im[2 * q + 1]);
+                    dscan(KA, re[2 * q], im[2 * q], kbase - 2 * q);
+                    dscan(KB, re[2 * q + 1], im[2 * q + 1], kbase - 2 * q - 1);
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < PPS; ++q) {
+                    const double2 x = va[q], y = vb[q];
+                    re[2 * q] = fma(n2r, y.x, fma(n1r, x.x, re[2 * q]));
+                    im[2 * q] = fma(n2i, y.x, fma(n1i, x.x, im[2 * q]));
+                    re[2 * q + 1] = fma(n2r, y.y, fma(n1r, x.y, re[2 * q + 1]));
+                    im[2 * q + 1] = fma(n2i, y.y, fma(n1i, x.y, im[2 * q + 1]));
+                    dscan(KA, re[2 * q], im[2 * q], kbase - 2 * q);
+                    dscan(KB, re[2 * q + 1], im[2 * q + 1], kbase - 2 * q - 1);
+                }
+            }
+            if (ex) {
+                const double x = vE[rA * SRV + cA + SEG];
+                re[SEG] = fma(n1r, x, re[SEG]);
+                im[SEG] = fma(n1i, x, im[SEG]);
+                if (!self) {
+                    const double y = vE[rB * SRV + cB + SEG];
+                    re[SEG] = fma(n2r, y, re[SEG]);
+                    im[SEG] = fma(n2i, y, im[SEG]);
+                }
+                dscan(KA, re[SEG], im[SEG], kbase - SEG);
+            }
+        }
+
+        if (a.rout && active) {
+            double2* R = static_cast<double2*>(a.rout) + (size_t)pos * L.SLOTS;
+#pragma unroll
+            for (int j = 0; j < SEG; ++j) R[j * NT + ltid] = make_double2(re[j], im[j]);
+            if (ex) R[SEG * NT + ltid] = make_double2(re[SEG], im[SEG]);
+        }
+        // thread 0's records visible to the group before the synthesis
+        if constexpr (NW == 1)
+            __syncwarp();
+        else
+            named_bar_sync(bar, GT);
+        v2_finish<T, GT, double2>(a, a.blocks[pos], pos, b, ltid, energy, nu, conv, 0, ntrace, rec_u, rec_c,
+                                  rstride, twi, red, bar);
+        if constexpr (NW == 1)
+            __syncwarp();
+        else
+            named_bar_sync(bar, GT);
+    }
+}
+
+template <int T>
+static int k2d_t(const K2Args& a, int32_t ntiles, cudaStream_t s) {
+    using Cf = DCfg<T>;
+    cudaError_t e = cudaFuncSetAttribute(k2d_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
+    if (e != cudaSuccess) return e;
+    if (ntiles <= 0) return cudaSuccess;
+    k2d_kernel<T><<<ntiles, Cf::GT * Cf::GROUPS, Cf::SMEM, s>>>(a);
+    return cudaGetLastError();
+}
+
+int k2d_launch(const K2Args& a, int32_t ntiles, cudaStream_t s) {
+    switch (a.T) {
+        case 8: return k2d_t<8>(a, ntiles, s);
+        case 16: return k2d_t<16>(a, ntiles, s);
+        case 32: return k2d_t<32>(a, ntiles, s);
+        case 64: return k2d_t<64>(a, ntiles, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+int k2d_blocks_per_cta(int T) {
+    switch (T) {
+        case 8: return DCfg<8>::GROUPS;
+        case 16: return DCfg<16>::GROUPS;
+        case 32: return DCfg<32>::GROUPS;
+        case 64: return DCfg<64>::GROUPS;
+    }
+    return 1;
+}
+
+}  // namespace fofse

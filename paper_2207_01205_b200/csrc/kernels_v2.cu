@@ -24,6 +24,7 @@
 #include "kcommon.cuh"
 #include "kernels.h"
 #include "layout.h"
+#include "v2common.cuh"
 
 namespace fofse {
 
@@ -43,7 +44,9 @@ struct V2Cfg {
     static constexpr bool REAL = PATH == PATH_F32_REAL;
     // REAL: two float copies (even / odd aligned) of the rotated V; else complex W
     static constexpr size_t WELEMS = REAL ? (size_t)2 * T * SRV : (size_t)T * SR;
-    static constexpr size_t WBYTES = ((WELEMS * (REAL ? 4 : 8) + 15) / 16) * 16;
+    static constexpr size_t IMG_BYTES = WELEMS * (REAL ? 4 : 8);
+    static constexpr bool TW64 = false;
+    static constexpr size_t WBYTES = ((IMG_BYTES + 15) / 16) * 16;
     static constexpr size_t OFF_P = WBYTES;                            // 2T double2
     static constexpr size_t OFF_TW = OFF_P + sizeof(double2) * 2 * T;  // T float2
     static constexpr size_t OFF_SP = OFF_TW + sizeof(float2) * T;      // spill: WARPS x (NP+SPT) float4
@@ -53,166 +56,6 @@ struct V2Cfg {
     static_assert(NT <= 32, "K2v2 needs one warp per block");
     static_assert(SEG % 2 == 0, "bin pairs");
 };
-
-template <class Cf>
-__device__ __forceinline__ constexpr int T_of() { return Cf::HT * 2; }
-
-// Per-warp scalar state of the block being iterated, kept in shared memory to
-// leave the register file to the 132 registers of the residual spectrum.
-struct V2State {
-    double energy;  // weighted residual energy (engine_spectral.cpp:100-110)
-    double thr_e;   // 1e-12 * initial_energy        (stop test, :60)
-    double thr_m;   // (1e-12 * initial_max)^2 on |R|^2 (stop test, :61)
-    double w0, gw;  // W[0] and gamma / W[0]
-    int nu, ntrace, pad0, pad1;
-};
-static_assert(sizeof(V2State) <= 64, "state slot");
-
-__device__ __forceinline__ unsigned fbits(float x) { return __float_as_uint(x); }
-__device__ __forceinline__ float fmax3(float a, float b, float c) {
-    float r;
-    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));  // FMNMX3
-    return r;
-}
-
-// Stage the class image (TMA bulk copy), the rotated-frame phase table and the
-// synthesis twiddles; returns once everything is resident.
-template <class Cf>
-__device__ __forceinline__ void v2_stage(const K2Args& a, const Tile& tile, unsigned char* smem) {
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Cf::OFF_BAR);
-    if (threadIdx.x == 0) {
-        mbar_init(bar, 1);
-        const uint32_t bytes = static_cast<uint32_t>(Cf::WELEMS * (Cf::REAL ? 4 : 8));
-        const char* src = static_cast<const char*>(a.wimg) + (size_t)tile.cls * bytes;
-        mbar_expect_tx(bar, bytes);
-        for (uint32_t off = 0; off < bytes; off += 32768)
-            bulk_g2s(smem + off, src + off, bytes - off < 32768u ? bytes - off : 32768u, bar);
-    }
-    for (int i = threadIdx.x; i < 2 * T_of<Cf>(); i += blockDim.x)
-        reinterpret_cast<double2*>(smem + Cf::OFF_P)[i] = a.ptab ? a.ptab[i] : make_double2(1.0, 0.0);
-    for (int i = threadIdx.x; i < T_of<Cf>(); i += blockDim.x) {
-        const double2 t = a.twid_inv[i];
-        reinterpret_cast<float2*>(smem + Cf::OFF_TW)[i] = make_float2((float)t.x, (float)t.y);
-    }
-    __syncthreads();
-    mbar_wait(bar, 0);
-}
-
-// Lane 0 records a selection: synthesis record (pair factor folded in), the
-// IterationRecord trace (trace.hpp:13-21) and the guard diagnostics.
-__device__ __forceinline__ void v2_record(const K2Args& a, int b, int nu, int ntrace, int rstride,
-                                          int tstride, int* rec_u, double2* rec_c, int u1, int u2,
-                                          int self, double p_re, double p_im, double c_re,
-                                          double c_im, double energy, double Mf, double Sf) {
-    if (rec_u && nu - 1 < rstride) {
-        rec_u[nu - 1] = (u1 << 16) | u2;
-        rec_c[nu - 1] = self ? make_double2(c_re, 0.0) : make_double2(2.0 * c_re, 2.0 * c_im);
-    }
-    if (a.trace && ntrace < tstride) {
-        fofse_record rr;
-        rr.nu = nu;
-        rr.u1 = u1;
-        rr.u2 = u2;
-        rr.pad0 = 0;
-        rr.p_re = p_re;
-        rr.p_im = p_im;
-        rr.c_re = c_re;
-        rr.c_im = c_im;
-        rr.gamma_effective = a.gamma;
-        rr.weighted_energy = energy;
-        rr.degenerate = 0;
-        rr.pad1 = 0;
-        a.trace[(size_t)b * tstride + ntrace] = rr;
-    }
-    if (a.gap_trace && ntrace < tstride)
-        a.gap_trace[(size_t)b * tstride + ntrace] = (float)(Sf > 0.0 ? (Mf - Sf) / Mf : 1.0);
-}
-
-// Block outputs + fused sparse synthesis (synthesize_model, engine_spectral.cpp:
-// 195-208) over the MISSING region, clamp + write-back (pipeline.cpp:226-232).
-// A team of NTH threads (t = 0..NTH-1, whole warps) shares the pixels; for
-// NTH > 32 the teams' partial squared errors meet in red[] behind named barrier bar.
-template <int T, int NTH>
-__device__ __forceinline__ void v2_finish(const K2Args& a, const BlockDesc& desc, int pos, int b,
-                                          int t, double energy, int nu, int conv, int flagged,
-                                          int ntrace, const int* rec_u, const double2* rec_c,
-                                          int rstride, const float2* twi, double* red = nullptr,
-                                          int bar = 0) {
-    const int lane = t & 31;
-    if (t == 0) {
-        const int sb = a.state_by_pos ? pos : b;
-        if (a.energy_out) a.energy_out[sb] = energy;
-        if (a.nu_out) a.nu_out[sb] = nu;
-        if (a.conv_out) a.conv_out[sb] = conv;
-        if (a.flags) a.flags[b] = flagged;
-        if (a.trace_count) a.trace_count[b] = ntrace;
-    }
-    __syncwarp();
-    if (a.synth == SYN_NONE || flagged) return;
-    const int nr = nu < rstride ? nu : rstride;
-    const int npx = a.reg_nr * a.reg_nc;
-    double sq = 0.0;
-    for (int p0 = 0; p0 < npx; p0 += NTH * 8) {
-        float acc[8];
-        int mm[8], nn[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            acc[k] = 0.f;
-            const int px = p0 + k * NTH + t;
-            mm[k] = a.reg_r0 + (px < npx ? px / a.reg_nc : 0);
-            nn[k] = a.reg_c0 + (px < npx ? px % a.reg_nc : 0);
-        }
-        for (int q = 0; q < nr; ++q) {
-            const int u = rec_u[q];
-            const double2 cd = rec_c[q];
-            const float cx = (float)cd.x, cy = (float)cd.y;
-            const int uu1 = u >> 16, uu2 = u & 0xffff;
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const float2 tw = twi[(uu1 * mm[k] + uu2 * nn[k]) & (T - 1)];
-                acc[k] = fmaf(cx, tw.x, fmaf(-cy, tw.y, acc[k]));
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const int px = p0 + k * NTH + t;
-            if (px >= npx) continue;
-            const int m = mm[k], n = nn[k];
-            if (a.synth == SYN_WINDOW) {
-                a.models[(size_t)b * a.Lh * a.Lw + m * a.Lw + n] = acc[k];
-            } else {
-                const double v0 = acc[k];
-                const double v = v0 < 0.0 ? 0.0 : (v0 > 255.0 ? 255.0 : v0);
-                const int64_t gi = (int64_t)desc.frame * a.fr.frame_stride +
-                                   (int64_t)(desc.row0 + m) * a.fr.width + (desc.col0 + n);
-                double orig;
-                if (a.fr.type == SRC_U8) {
-                    orig = (double)static_cast<const uint8_t*>(a.fr.src)[gi];
-                    static_cast<uint8_t*>(a.fr.dst)[gi] = static_cast<uint8_t>(round(v));
-                } else {
-                    orig = static_cast<const double*>(a.fr.src)[gi];
-                    static_cast<double*>(a.fr.dst)[gi] = v;
-                }
-                sq += (orig - v) * (orig - v);
-            }
-        }
-    }
-    if (a.block_sq && a.synth == SYN_IMAGE) {
-#pragma unroll
-        for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-        if constexpr (NTH == 32) {
-            if (lane == 0) a.block_sq[b] = sq;
-        } else {
-            if (lane == 0) red[t >> 5] = sq;
-            named_bar_sync(bar, NTH);
-            if (t == 0) {
-                double tot = 0.0;
-                for (int w = 0; w < NTH / 32; ++w) tot += red[w];
-                a.block_sq[b] = tot;
-            }
-        }
-    }
-}
 
 // fp32 argmax on packed keys: |R|^2 with its 6 low mantissa bits replaced by
 // (63 - pair index). Truncation merges values within 2^-17 relative into ties;
@@ -537,7 +380,9 @@ struct V2R2Cfg {
     static constexpr int GROUPS = 4;     // lost blocks per CTA (256 threads)
     static constexpr bool REAL = true;
     static constexpr size_t WELEMS = (size_t)2 * T * SRV;
-    static constexpr size_t WBYTES = ((WELEMS * 4 + 15) / 16) * 16;
+    static constexpr size_t IMG_BYTES = WELEMS * 4;
+    static constexpr bool TW64 = false;
+    static constexpr size_t WBYTES = ((IMG_BYTES + 15) / 16) * 16;
     static constexpr size_t OFF_P = WBYTES;
     static constexpr size_t OFF_TW = OFF_P + sizeof(double2) * 2 * T;
     // per group: slots [2 parity][2 warps] x 16 B, spill [2][2][NP+1] float4, red 2 doubles

@@ -129,6 +129,12 @@ FOFSE_HDC int v2_srv(int t) { return t + v2_seg(t) + 2; }
 int v2_real_gw(int t);
 inline int v2_real_spt(int t) { return v2_real_gw(t) == 2 ? 1 : v2_spt(t); }
 
+// K2d (fp64 rotated frame): the fp64 strict bin layout (SEG = seg_for(T, 1),
+// one segment per thread), V as two fp64 copies (even / odd aligned) with row
+// stride T + SEG + 2 so every bin pair is one aligned 16-byte load.
+FOFSE_HDC bool d_supported(int t) { return t >= 8 && t <= 64; }
+FOFSE_HDC int d_srv(int t) { return t + seg_for(t, 1) + 2; }
+
 // Floats per block of a packed fp32 residual: AoS float2 slots, or the K2v2
 // SoA pair layout (float4 per bin pair + one float4 per segment extra bin).
 FOFSE_HD size_t packed32_floats(const BinLayout& L, int soa) {

@@ -169,6 +169,45 @@ def test_conceal_fp64_borders_and_neighbours(gpu, orc):
     assert np.abs(out.restored - ref["restored"]).max() <= FP64_PX_TOL
 
 
+def test_conceal_fp64_k2d_vs_oracle_C2_slice(gpu, orc):
+    """K2d (fp64 rotated frame, symmetric masks) on 400 C2 blocks at 200
+    iterations: the oracle's selected-basis sequence for every block, pixels
+    within 1e-9."""
+    img, pat = WL.C2.frame(seed=23)
+    sub = P.LossPattern(pat.image_width, pat.image_height, 16, 16, pat.blocks[::5])
+    cfg = WL.C2.config("fp64", record_traces=True)
+    out = P.conceal(img.astype(np.float64), sub, cfg)
+    ref = _oracle_conceal(orc, img, sub, cfg)
+    _assert_same_selections(out.report.traces, ref["traces"])
+    assert np.abs(out.restored - ref["restored"]).max() <= FP64_PX_TOL
+
+
+def test_conceal_fp64_k2d_matches_strict_full_C2(gpu, monkeypatch):
+    """All 2040 C2 blocks: K2d vs the strict (reference operation order) kernel —
+    identical selections, pixels within 1e-9."""
+    img, pat = WL.C2.frame(seed=24)
+    cfg = WL.C2.config("fp64", record_traces=True)
+    fast = P.conceal(img.astype(np.float64), pat, cfg)
+    monkeypatch.setenv("FOFSE_F64_KERNEL", "strict")
+    strict = P.conceal(img.astype(np.float64), pat, cfg)
+    _assert_same_selections(fast.report.traces, strict.report.traces)
+    assert np.abs(fast.restored - strict.restored).max() <= FP64_PX_TOL
+
+
+@pytest.mark.parametrize("t,b,sw", [(8, 4, 2), (16, 8, 4), (32, 8, 8), (32, 16, 8)])
+def test_conceal_fp64_small_transforms(gpu, orc, t, b, sw):
+    """K2d at T = 8/16/32 (one warp per block, idle lanes for T < 32) vs the oracle."""
+    rng = np.random.default_rng(449 + t + b)
+    img = smooth_test_image(rng, 96)
+    cells = [(r, c) for r in range(b, 96 - 2 * b, 3 * b) for c in range(b, 96 - 2 * b, 3 * b)]
+    pat = P.LossPattern(96, 96, b, b, [P.Rect(r, c, b, b) for r, c in cells])
+    cfg = P.ConcealConfig(gamma=0.5, iterations=40, transform_size=t, support_width=sw, record_traces=True)
+    out = P.conceal(img, pat, cfg)
+    ref = _oracle_conceal(orc, img, pat, cfg)
+    _assert_same_selections(out.report.traces, ref["traces"])
+    assert np.abs(out.restored - ref["restored"]).max() <= FP64_PX_TOL
+
+
 def test_conceal_empty_pattern_is_identity(gpu):
     """pipeline_test.cpp:171-183."""
     img = smooth_test_image(np.random.default_rng(421), 64)
