@@ -612,6 +612,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         a.energy = e;
         a.init_max = m;
         a.twid = d_twf;
+        a.ptab = d_ptab;
         ck(k1_launch(a, ks ? ks : st), "K1 residual spectra");
         ++ctx->launches;
     };

@@ -13,6 +13,7 @@
 #include <stdint.h>
 
 #include <climits>
+#include <cstdlib>
 
 #include "kcommon.cuh"
 #include "kernels.h"
@@ -816,6 +817,12 @@ __global__ void __launch_bounds__(256) kl_lines(double2* data, int64_t n, int co
 // ----------------------------------------------------------------------------
 int seg_of(int T, int path) { return seg_for(T, path_is_f64(path)); }
 
+// FOFSE_K1=slow keeps the shared-memory radix-2 K1 for every T (diagnostics).
+static bool k1_slow_forced() {
+    const char* e = getenv("FOFSE_K1");
+    return e && e[0] == 's';
+}
+
 template <int T>
 static int k1_launch_t(const K1Args& a, cudaStream_t s) {
     const size_t smem = K1Cfg<T>::smem;
@@ -828,6 +835,7 @@ static int k1_launch_t(const K1Args& a, cudaStream_t s) {
 }
 
 int k1_launch(const K1Args& a, cudaStream_t s) {
+    if (k1f_supported(a) && !k1_slow_forced()) return k1f_launch(a, s);
     switch (a.T) {
         case 8: return k1_launch_t<8>(a, s);
         case 16: return k1_launch_t<16>(a, s);

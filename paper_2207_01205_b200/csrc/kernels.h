@@ -75,6 +75,7 @@ struct K1Args {
     int32_t vpairs;            // write the K2v2 even/odd paired V layout
     double* w0;                // [ncls]
     const double2* twid;       // e^{-j 2 pi k / T}, k < T
+    const double2* ptab;       // e^{-j pi m / T}, m < 2T (rotation phases; NULL = computed)
 };
 enum { K1_PACKED = 0, K1_FULL = 1, K1_CLASS = 2 };
 
@@ -138,6 +139,9 @@ enum { SYN_NONE = 0, SYN_IMAGE = 1, SYN_WINDOW = 2 };
 
 // Host launchers (return cudaError_t).
 int k1_launch(const K1Args& a, cudaStream_t s);
+// K1 fast path (T = 64, packed mode): register radix-8x8 FFT (kernels_k1.cu).
+bool k1f_supported(const K1Args& a);
+int k1f_launch(const K1Args& a, cudaStream_t s);
 int k2_launch(const K2Args& a, int32_t ntiles, cudaStream_t s);
 // Batched in-place complex fp64 2-D transform of n T x T spectra (dir -1/+1).
 int fft2d_launch(double2* data, int64_t n, int32_t T, int32_t dir, const double2* twid_fwd,

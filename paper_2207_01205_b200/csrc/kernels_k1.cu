@@ -1,0 +1,258 @@
+// kernels_k1.cu — K1 fast path: window gather + w*f + real-input 2-D FFT (fp64)
+// for T = 64, packed canonical output for the iteration kernels.
+//
+// Reference: engine_spectral.cpp:161-181 (fw = w f on SUPPORT, energy =
+// sum w f^2, R_w = DFT(fw)), basis.cpp:57-70 (embed at (0,0), zero pad,
+// forward unnormalised DFT), transform.cpp:48-80.
+//
+// Register FFT: a 64-point transform is 8 x 8 (Cooley-Tukey): eight threads
+// each hold 8 elements, run a radix-8 butterfly in registers, multiply the
+// inter-stage twiddles, transpose through a padded shared-memory tile (the 8
+// threads are lanes of one warp: __syncwarp only) and run the second radix-8.
+//  * rows: the Lh window rows are paired into complex rows z = x_a + j x_b
+//    (ceil(Lh/2) <= 32 transforms), unpacked into the T/2+1 non-redundant
+//    columns of a column-major spectrum tile in shared memory;
+//  * columns: columns 1..T/2-1 are complex transforms; columns 0 and T/2 are
+//    real (DFTs of real rows at k = 0, T/2) and share one complex transform —
+//    exactly 32 column transforms = 256 threads;
+//  * the canonical half is packed from the tile (conjugate symmetry for the
+//    columns > T/2) with the rotated-frame phase from a table.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "kcommon.cuh"
+#include "kernels.h"
+#include "layout.h"
+
+namespace fofse {
+
+namespace {
+
+constexpr int FT = 64;         // transform size of this kernel
+constexpr int FNC = FT / 2 + 1;  // non-redundant columns
+constexpr int FCS = FT + 1;    // column stride of the spectrum tile (double2), conflict-free row-pass stores
+constexpr int FSS = 9;         // transpose tile row stride (double2)
+
+struct K1fSmem {
+    static constexpr size_t tw = 0;                                   // W64^e, e < 64
+    static constexpr size_t ph = tw + sizeof(double2) * FT;           // e^{+j pi m / T}, m < 2T
+    static constexpr size_t cb = ph + sizeof(double2) * 2 * FT;       // [FNC][FCS] spectrum tile
+    static constexpr size_t sc = cb + sizeof(double2) * FNC * FCS;    // [32 groups][8][FSS] transpose tiles
+    static constexpr size_t red = sc + sizeof(double2) * 32 * 8 * FSS;
+    static constexpr size_t total = red + 16 * sizeof(double);
+};
+
+__device__ __forceinline__ double2 c_add(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 c_sub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 c_mul(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 c_mj(double2 a) { return make_double2(a.y, -a.x); }  // -j a
+
+// Forward 8-point DFT in registers, natural order in and out.
+__device__ __forceinline__ void fft8(double2 (&x)[8]) {
+    constexpr double H = 0.70710678118654752440;
+    // radix-2 split: even / odd 4-point DFTs
+    const double2 a0 = c_add(x[0], x[4]), a1 = c_sub(x[0], x[4]);
+    const double2 a2 = c_add(x[2], x[6]), a3 = c_sub(x[2], x[6]);
+    const double2 b0 = c_add(x[1], x[5]), b1 = c_sub(x[1], x[5]);
+    const double2 b2 = c_add(x[3], x[7]), b3 = c_sub(x[3], x[7]);
+    const double2 E0 = c_add(a0, a2), E2 = c_sub(a0, a2);
+    const double2 E1 = c_add(a1, c_mj(a3)), E3 = c_sub(a1, c_mj(a3));
+    const double2 O0 = c_add(b0, b2), O2 = c_sub(b0, b2);
+    const double2 O1 = c_add(b1, c_mj(b3)), O3 = c_sub(b1, c_mj(b3));
+    // W8^1 = H(1 - j), W8^2 = -j, W8^3 = -H(1 + j)
+    const double2 t1 = make_double2(H * (O1.x + O1.y), H * (O1.y - O1.x));
+    const double2 t2 = c_mj(O2);
+    const double2 t3 = make_double2(H * (O3.y - O3.x), -H * (O3.x + O3.y));
+    x[0] = c_add(E0, O0);
+    x[4] = c_sub(E0, O0);
+    x[1] = c_add(E1, t1);
+    x[5] = c_sub(E1, t1);
+    x[2] = c_add(E2, t2);
+    x[6] = c_sub(E2, t2);
+    x[3] = c_add(E3, t3);
+    x[7] = c_sub(E3, t3);
+}
+
+// 64-point forward DFT of the vector v[n] = x_t[m], n = t + 8m, held by the 8
+// lanes t of a group. On return lane t holds X[t + 8 k2] in x[k2].
+__device__ __forceinline__ void fft64_group(double2 (&x)[8], int t, const double2* tw, double2* tile,
+                                            unsigned gmask) {
+    fft8(x);  // Y[t][k1] = sum_m x[t + 8m] W8^{m k1}
+#pragma unroll
+    for (int k1 = 1; k1 < 8; ++k1) x[k1] = c_mul(x[k1], tw[t * k1]);  // * W64^{t k1}
+#pragma unroll
+    for (int k1 = 0; k1 < 8; ++k1) tile[k1 * FSS + t] = x[k1];
+    __syncwarp(gmask);
+#pragma unroll
+    for (int s = 0; s < 8; ++s) x[s] = tile[t * FSS + s];  // lane t = k1 now holds Y[s][k1]
+    __syncwarp(gmask);
+    fft8(x);  // X[k1 + 8 k2] = sum_s Y[s][k1] W8^{s k2}
+}
+
+__device__ __forceinline__ double k1f_pixel(const K1Args& a, const BlockDesc& d, int r, int c) {
+    const int gr = d.row0 + r, gc = d.col0 + c;
+    if (gr < 0 || gc < 0 || gr >= a.fr.height || gc >= a.fr.width) return 0.0;
+    const int64_t idx = (int64_t)d.frame * a.fr.frame_stride + (int64_t)gr * a.fr.width + gc;
+    if (a.fr.type == SRC_U8) return static_cast<double>(static_cast<const uint8_t*>(a.fr.src)[idx]);
+    return static_cast<const double*>(a.fr.src)[idx];
+}
+
+__global__ void __launch_bounds__(256, 3) k1f_kernel(K1Args a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double2* tw = reinterpret_cast<double2*>(smem_raw + K1fSmem::tw);
+    double2* ph = reinterpret_cast<double2*>(smem_raw + K1fSmem::ph);
+    double2* cb = reinterpret_cast<double2*>(smem_raw + K1fSmem::cb);
+    double* red = reinterpret_cast<double*>(smem_raw + K1fSmem::red);
+    const int g = threadIdx.x >> 3, t = threadIdx.x & 7;
+    const unsigned gmask = 0xFFu << (8 * (g & 3));  // the group's 8 lanes (groups may diverge)
+    double2* tile = reinterpret_cast<double2*>(smem_raw + K1fSmem::sc) + g * 8 * FSS;
+
+    const int b = blockIdx.x;
+    const BlockDesc d = a.blocks[b];
+    const double* wc = a.wcls + (size_t)d.cls * a.Lh * a.Lw;
+    for (int i = threadIdx.x; i < FT; i += blockDim.x) tw[i] = a.twid[i];
+    for (int i = threadIdx.x; i < 2 * FT; i += blockDim.x) {
+        if (a.ptab) {
+            const double2 p = a.ptab[i];  // e^{-j pi m / T}
+            ph[i] = make_double2(p.x, -p.y);
+        } else {
+            ph[i] = phase_pos<FT>(i);
+        }
+    }
+    __syncthreads();
+
+    // ---- row pass: row pair g (rows 2g, 2g+1) ----
+    double energy = 0.0;
+    const int npairs = (a.Lh + 1) / 2;
+    if (g < npairs) {
+        const int ra = 2 * g, rb = ra + 1;
+        double2 x[8];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            const int n = t + 8 * m;
+            double va = 0.0, vb = 0.0;
+            if (n < a.Lw) {
+                const double wa = wc[ra * a.Lw + n];
+                if (wa != 0.0) {
+                    const double f = k1f_pixel(a, d, ra, n);
+                    va = wa * f;
+                    energy += wa * f * f;
+                }
+                if (rb < a.Lh) {
+                    const double wb = wc[rb * a.Lw + n];
+                    if (wb != 0.0) {
+                        const double f = k1f_pixel(a, d, rb, n);
+                        vb = wb * f;
+                        energy += wb * f * f;
+                    }
+                }
+            }
+            x[m] = make_double2(va, vb);
+        }
+        fft64_group(x, t, tw, tile, gmask);
+        // lane t holds Z[k], k = t + 8 k2; unpack needs Z[-k] (lane (8 - t) & 7)
+#pragma unroll
+        for (int k2 = 0; k2 < 8; ++k2) tile[k2 * FSS + t] = x[k2];
+        __syncwarp(gmask);
+#pragma unroll
+        for (int k2 = 0; k2 < 8; ++k2) {
+            const int k = t + 8 * k2;
+            if (k > FT / 2) continue;
+            const int nk = (FT - k) & (FT - 1);
+            const double2 zc = tile[(nk >> 3) * FSS + (nk & 7)];
+            const double2 z = x[k2];
+            // Xa = (Z + conj Z-)/2, Xb = -j (Z - conj Z-)/2
+            cb[k * FCS + ra] = make_double2(0.5 * (z.x + zc.x), 0.5 * (z.y - zc.y));
+            if (rb < FT) cb[k * FCS + rb] = make_double2(0.5 * (z.y + zc.y), -0.5 * (z.x - zc.x));
+        }
+        __syncwarp(gmask);
+    }
+    // rows >= Lh stay zero
+    for (int i = threadIdx.x; i < FNC * FT; i += blockDim.x) {
+        const int k = i / FT, r = i % FT;
+        if (r >= 2 * npairs) cb[k * FCS + r] = make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+
+    // ---- column pass: group g < 31 -> column g + 1; group 31 -> columns 0 and T/2 packed ----
+    {
+        const int col = g < 31 ? g + 1 : 0;
+        double2 x[8];
+        if (g < 31) {
+#pragma unroll
+            for (int m = 0; m < 8; ++m) x[m] = cb[col * FCS + t + 8 * m];
+        } else {
+            // both columns hold DFTs of real rows at k = 0 and k = T/2: real values
+#pragma unroll
+            for (int m = 0; m < 8; ++m)
+                x[m] = make_double2(cb[t + 8 * m].x, cb[(FT / 2) * FCS + t + 8 * m].x);
+        }
+        fft64_group(x, t, tw, tile, gmask);
+        if (g < 31) {
+#pragma unroll
+            for (int k2 = 0; k2 < 8; ++k2) cb[col * FCS + t + 8 * k2] = x[k2];
+        } else {
+#pragma unroll
+            for (int k2 = 0; k2 < 8; ++k2) tile[k2 * FSS + t] = x[k2];
+            __syncwarp(gmask);
+#pragma unroll
+            for (int k2 = 0; k2 < 8; ++k2) {
+                const int k = t + 8 * k2;
+                const int nk = (FT - k) & (FT - 1);
+                const double2 zc = tile[(nk >> 3) * FSS + (nk & 7)];
+                const double2 z = x[k2];
+                cb[k] = make_double2(0.5 * (z.x + zc.x), 0.5 * (z.y - zc.y));
+                cb[(FT / 2) * FCS + k] = make_double2(0.5 * (z.y + zc.y), -0.5 * (z.x - zc.x));
+            }
+        }
+    }
+    energy = block_reduce<double>(energy, red, false);  // (its __syncthreads orders the tile)
+
+    // ---- pack the canonical half ----
+    double vmax2 = 0.0;
+    const BinLayout L = BinLayout::make(FT, a.seg, a.spt > 0 ? a.spt : 1);
+    const bool rotate = path_is_rotated(a.path);
+    const size_t per = a.out_stride > 0 ? (size_t)a.out_stride : packed32_floats(L, a.soa);
+    for (int s = threadIdx.x; s < L.SLOTS; s += blockDim.x) {
+        const int j = s / L.NT, tid = s % L.NT;
+        int k1 = 0, k2 = 0;
+        double2 v = make_double2(0.0, 0.0);
+        if (L.slot_bin(j, tid, &k1, &k2)) {
+            if (k2 <= FT / 2) {
+                v = cb[k2 * FCS + k1];
+            } else {
+                const double2 u = cb[(FT - k2) * FCS + ((FT - k1) & (FT - 1))];
+                v = make_double2(u.x, -u.y);
+            }
+            vmax2 = fmax(vmax2, fma(v.x, v.x, v.y * v.y));
+            if (rotate) v = c_mul(v, ph[(k1 * (a.Lh - 1) + k2 * (a.Lw - 1)) & (2 * FT - 1)]);
+        }
+        if (path_is_f64(a.path))
+            static_cast<double2*>(a.out)[(size_t)b * L.SLOTS + s] = v;
+        else
+            put_packed32(static_cast<float*>(a.out) + (size_t)b * per, L, a.soa, j, tid,
+                         static_cast<float>(v.x), static_cast<float>(v.y));
+    }
+    vmax2 = block_reduce<double>(vmax2, red, true);
+    if (threadIdx.x == 0) {
+        a.energy[b] = energy;
+        a.init_max[b] = sqrt(vmax2);
+    }
+}
+
+}  // namespace
+
+bool k1f_supported(const K1Args& a) { return a.T == FT && a.mode == K1_PACKED && a.Lh <= FT && a.Lw <= FT; }
+
+int k1f_launch(const K1Args& a, cudaStream_t s) {
+    cudaError_t e = cudaFuncSetAttribute(k1f_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)K1fSmem::total);
+    if (e != cudaSuccess) return e;
+    if (a.n <= 0) return cudaSuccess;
+    k1f_kernel<<<a.n, 256, K1fSmem::total, s>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace fofse

@@ -194,6 +194,19 @@ def test_conceal_fp64_k2d_matches_strict_full_C2(gpu, monkeypatch):
     assert np.abs(fast.restored - strict.restored).max() <= FP64_PX_TOL
 
 
+def test_k1_register_fft_matches_radix2(gpu, monkeypatch):
+    """The T = 64 register radix-8x8 K1 vs the shared-memory radix-2 K1 (both fp64):
+    identical selections on 600 C2 blocks (borders included), pixels within 1e-9."""
+    img, pat = WL.C2.frame(seed=25)
+    sub = P.LossPattern(pat.image_width, pat.image_height, 16, 16, pat.blocks[::3])
+    cfg = WL.C2.config("fp64", record_traces=True)
+    fast = P.conceal(img.astype(np.float64), sub, cfg)
+    monkeypatch.setenv("FOFSE_K1", "slow")
+    slow = P.conceal(img.astype(np.float64), sub, cfg)
+    _assert_same_selections(fast.report.traces, slow.report.traces)
+    assert np.abs(fast.restored - slow.restored).max() <= FP64_PX_TOL
+
+
 @pytest.mark.parametrize("t,b,sw", [(8, 4, 2), (16, 8, 4), (32, 8, 8), (32, 16, 8)])
 def test_conceal_fp64_small_transforms(gpu, orc, t, b, sw):
     """K2d at T = 8/16/32 (one warp per block, idle lanes for T < 32) vs the oracle."""
