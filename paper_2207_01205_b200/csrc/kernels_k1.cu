@@ -91,14 +91,17 @@ __device__ __forceinline__ void fft64_group(double2 (&x)[8], int t, const double
     fft8(x);  // X[k1 + 8 k2] = sum_s Y[s][k1] W8^{s k2}
 }
 
-__device__ __forceinline__ double k1f_pixel(const K1Args& a, const BlockDesc& d, int r, int c) {
-    const int gr = d.row0 + r, gc = d.col0 + c;
-    if (gr < 0 || gc < 0 || gr >= a.fr.height || gc >= a.fr.width) return 0.0;
-    const int64_t idx = (int64_t)d.frame * a.fr.frame_stride + (int64_t)gr * a.fr.width + gc;
-    if (a.fr.type == SRC_U8) return static_cast<double>(static_cast<const uint8_t*>(a.fr.src)[idx]);
-    return static_cast<const double*>(a.fr.src)[idx];
+// Window row r of block d: pointer to its column 0 (NULL when the row is
+// outside the frame) — samples are then read with a column bound check only.
+template <class SRC>
+__device__ __forceinline__ const SRC* k1f_row(const K1Args& a, const BlockDesc& d, int r) {
+    const int gr = d.row0 + r;
+    if (gr < 0 || gr >= a.fr.height) return nullptr;
+    return static_cast<const SRC*>(a.fr.src) + (int64_t)d.frame * a.fr.frame_stride + (int64_t)gr * a.fr.width +
+           d.col0;
 }
 
+template <class SRC>
 __global__ void __launch_bounds__(256, 3) k1f_kernel(K1Args a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double2* tw = reinterpret_cast<double2*>(smem_raw + K1fSmem::tw);
@@ -129,26 +132,30 @@ __global__ void __launch_bounds__(256, 3) k1f_kernel(K1Args a) {
     if (g < npairs) {
         const int ra = 2 * g, rb = ra + 1;
         double2 x[8];
+        // branch-free gather (w = 0 off SUPPORT; window samples outside the frame
+        // read as 0 and always carry w = 0): all loads of a lane are independent
+        const bool hasb = rb < a.Lh;
+        const SRC* pa = k1f_row<SRC>(a, d, ra);
+        const SRC* pb = hasb ? k1f_row<SRC>(a, d, rb) : nullptr;
+        const double* wra = wc + ra * a.Lw;
+        const double* wrb = wc + (hasb ? rb : ra) * a.Lw;
+        const int c_lo = -d.col0, c_hi = a.fr.width - d.col0;  // in-frame window columns [c_lo, c_hi)
+        double wa[8], wb[8], fa[8], fb[8];
 #pragma unroll
         for (int m = 0; m < 8; ++m) {
             const int n = t + 8 * m;
-            double va = 0.0, vb = 0.0;
-            if (n < a.Lw) {
-                const double wa = wc[ra * a.Lw + n];
-                if (wa != 0.0) {
-                    const double f = k1f_pixel(a, d, ra, n);
-                    va = wa * f;
-                    energy += wa * f * f;
-                }
-                if (rb < a.Lh) {
-                    const double wb = wc[rb * a.Lw + n];
-                    if (wb != 0.0) {
-                        const double f = k1f_pixel(a, d, rb, n);
-                        vb = wb * f;
-                        energy += wb * f * f;
-                    }
-                }
-            }
+            const bool in = n < a.Lw;
+            const bool inf = in && n >= c_lo && n < c_hi;
+            wa[m] = in ? wra[n] : 0.0;
+            wb[m] = (in && hasb) ? wrb[n] : 0.0;
+            fa[m] = (inf && pa) ? static_cast<double>(pa[n]) : 0.0;
+            fb[m] = (inf && pb) ? static_cast<double>(pb[n]) : 0.0;
+        }
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            const double va = wa[m] * fa[m], vb = wb[m] * fb[m];
+            energy += va * fa[m];
+            energy += vb * fb[m];
             x[m] = make_double2(va, vb);
         }
         fft64_group(x, t, tw, tile, gmask);
@@ -169,12 +176,8 @@ __global__ void __launch_bounds__(256, 3) k1f_kernel(K1Args a) {
         }
         __syncwarp(gmask);
     }
-    // rows >= Lh stay zero
-    for (int i = threadIdx.x; i < FNC * FT; i += blockDim.x) {
-        const int k = i / FT, r = i % FT;
-        if (r >= 2 * npairs) cb[k * FCS + r] = make_double2(0.0, 0.0);
-    }
     __syncthreads();
+    const int nrows = 2 * npairs;  // rows >= nrows are zero (never stored)
 
     // ---- column pass: group g < 31 -> column g + 1; group 31 -> columns 0 and T/2 packed ----
     {
@@ -182,12 +185,14 @@ __global__ void __launch_bounds__(256, 3) k1f_kernel(K1Args a) {
         double2 x[8];
         if (g < 31) {
 #pragma unroll
-            for (int m = 0; m < 8; ++m) x[m] = cb[col * FCS + t + 8 * m];
+            for (int m = 0; m < 8; ++m)
+                x[m] = (t + 8 * m < nrows) ? cb[col * FCS + t + 8 * m] : make_double2(0.0, 0.0);
         } else {
             // both columns hold DFTs of real rows at k = 0 and k = T/2: real values
 #pragma unroll
             for (int m = 0; m < 8; ++m)
-                x[m] = make_double2(cb[t + 8 * m].x, cb[(FT / 2) * FCS + t + 8 * m].x);
+                x[m] = (t + 8 * m < nrows) ? make_double2(cb[t + 8 * m].x, cb[(FT / 2) * FCS + t + 8 * m].x)
+                                           : make_double2(0.0, 0.0);
         }
         fft64_group(x, t, tw, tile, gmask);
         if (g < 31) {
@@ -215,25 +220,45 @@ __global__ void __launch_bounds__(256, 3) k1f_kernel(K1Args a) {
     const BinLayout L = BinLayout::make(FT, a.seg, a.spt > 0 ? a.spt : 1);
     const bool rotate = path_is_rotated(a.path);
     const size_t per = a.out_stride > 0 ? (size_t)a.out_stride : packed32_floats(L, a.soa);
-    for (int s = threadIdx.x; s < L.SLOTS; s += blockDim.x) {
-        const int j = s / L.NT, tid = s % L.NT;
-        int k1 = 0, k2 = 0;
-        double2 v = make_double2(0.0, 0.0);
-        if (L.slot_bin(j, tid, &k1, &k2)) {
-            if (k2 <= FT / 2) {
-                v = cb[k2 * FCS + k1];
-            } else {
-                const double2 u = cb[(FT - k2) * FCS + ((FT - k1) & (FT - 1))];
-                v = make_double2(u.x, -u.y);
-            }
-            vmax2 = fmax(vmax2, fma(v.x, v.x, v.y * v.y));
-            if (rotate) v = c_mul(v, ph[(k1 * (a.Lh - 1) + k2 * (a.Lw - 1)) & (2 * FT - 1)]);
+    // thread -> (tid, first slot): the segment(s) of tid are fixed, no divisions
+    const int NT = L.NT, tid = threadIdx.x % NT, step = blockDim.x / NT;
+    auto spec = [&](int k1, int k2) {
+        double2 v;
+        if (k2 <= FT / 2) {
+            v = cb[k2 * FCS + k1];
+        } else {
+            const double2 u = cb[(FT - k2) * FCS + ((FT - k1) & (FT - 1))];
+            v = make_double2(u.x, -u.y);
         }
-        if (path_is_f64(a.path))
-            static_cast<double2*>(a.out)[(size_t)b * L.SLOTS + s] = v;
-        else
-            put_packed32(static_cast<float*>(a.out) + (size_t)b * per, L, a.soa, j, tid,
-                         static_cast<float>(v.x), static_cast<float>(v.y));
+        vmax2 = fmax(vmax2, fma(v.x, v.x, v.y * v.y));
+        if (rotate) v = c_mul(v, ph[(k1 * (a.Lh - 1) + k2 * (a.Lw - 1)) & (2 * FT - 1)]);
+        return v;
+    };
+    if (L.SPT == 1 && path_is_f64(a.path)) {
+        // fp64 AoS (K2d / strict input): slot j of tid at j * NT + tid
+        int k1, c0, ex;
+        L.thread_segment(tid, 0, &k1, &c0, &ex);
+        double2* o = static_cast<double2*>(a.out) + (size_t)b * L.SLOTS + tid;
+        for (int j = threadIdx.x / NT; j <= L.SEG; j += step) {
+            const double2 v = (j < L.SEG || ex) ? spec(k1, c0 + j) : make_double2(0.0, 0.0);
+            o[(size_t)j * NT] = v;
+        }
+    } else {
+        int k1a, c0a, exa, k1b = 0, c0b = 0, exb = 0;
+        L.thread_segment(tid, 0, &k1a, &c0a, &exa);
+        if (L.SPT > 1) L.thread_segment(tid, 1, &k1b, &c0b, &exb);
+        const int nslot = L.SPT * (L.SEG + 1);
+        for (int j = threadIdx.x / NT; j < nslot; j += step) {
+            const bool q = j > L.SEG;
+            const int jj = q ? j - (L.SEG + 1) : j;
+            const int k1 = q ? k1b : k1a, k2 = (q ? c0b : c0a) + jj;
+            const double2 v = (jj < L.SEG || (q ? exb : exa)) ? spec(k1, k2) : make_double2(0.0, 0.0);
+            if (path_is_f64(a.path))
+                static_cast<double2*>(a.out)[(size_t)b * L.SLOTS + j * NT + tid] = v;
+            else
+                put_packed32(static_cast<float*>(a.out) + (size_t)b * per, L, a.soa, j, tid,
+                             static_cast<float>(v.x), static_cast<float>(v.y));
+        }
     }
     vmax2 = block_reduce<double>(vmax2, red, true);
     if (threadIdx.x == 0) {
@@ -244,14 +269,24 @@ __global__ void __launch_bounds__(256, 3) k1f_kernel(K1Args a) {
 
 }  // namespace
 
-bool k1f_supported(const K1Args& a) { return a.T == FT && a.mode == K1_PACKED && a.Lh <= FT && a.Lw <= FT; }
+bool k1f_supported(const K1Args& a) {
+    if (a.T != FT || a.mode != K1_PACKED || a.Lh > FT || a.Lw > FT) return false;
+    const BinLayout L = BinLayout::make(FT, a.seg, a.spt > 0 ? a.spt : 1);
+    return L.SPT <= 2 && L.NT <= 256 && 256 % L.NT == 0;
+}
 
 int k1f_launch(const K1Args& a, cudaStream_t s) {
-    cudaError_t e = cudaFuncSetAttribute(k1f_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k1f_kernel<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)K1fSmem::total);
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k1f_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)K1fSmem::total);
+    if (e != cudaSuccess) return e;
     if (a.n <= 0) return cudaSuccess;
-    k1f_kernel<<<a.n, 256, K1fSmem::total, s>>>(a);
+    if (a.fr.type == SRC_U8)
+        k1f_kernel<uint8_t><<<a.n, 256, K1fSmem::total, s>>>(a);
+    else
+        k1f_kernel<double><<<a.n, 256, K1fSmem::total, s>>>(a);
     return cudaGetLastError();
 }
 
