@@ -43,6 +43,7 @@ struct DCfg {
     static constexpr bool REAL = true;
     static constexpr size_t IMG_BYTES = (size_t)2 * T * SRV * sizeof(double);
     static constexpr bool TW64 = true;
+    static constexpr bool P32 = false;
     static constexpr size_t WBYTES = ((IMG_BYTES + 15) / 16) * 16;
     static constexpr size_t OFF_P = WBYTES;                            // 2T double2
     static constexpr size_t OFF_TW = OFF_P + sizeof(double2) * 2 * T;  // T double2

@@ -46,6 +46,7 @@ struct V2Cfg {
     static constexpr size_t WELEMS = REAL ? (size_t)2 * T * SRV : (size_t)T * SR;
     static constexpr size_t IMG_BYTES = WELEMS * (REAL ? 4 : 8);
     static constexpr bool TW64 = false;
+    static constexpr bool P32 = true;  // fp32 rotated-frame phase table
     static constexpr size_t WBYTES = ((IMG_BYTES + 15) / 16) * 16;
     static constexpr size_t OFF_P = WBYTES;                            // 2T double2
     static constexpr size_t OFF_TW = OFF_P + sizeof(double2) * 2 * T;  // T float2
@@ -123,18 +124,21 @@ __device__ __forceinline__ void am_merge(float& m1, int& i1, float& m2, float om
 // so one LDS.64 from the even/odd-aligned V copy feeds two bins and every
 // update / magnitude is an FFMA2 / FMUL2 on a pair.
 // ============================================================================
-template <int T>
-__global__ void __launch_bounds__(128, 3) k2v2r_kernel(K2Args a) {
+template <int T, int VAR>
+__global__ void __launch_bounds__(128, VAR == 0 ? 3 : 2) k2v2r_kernel(K2Args a) {
     using Cf = V2Cfg<T, PATH_F32_REAL>;
     constexpr int SEG = Cf::SEG, SPT = Cf::SPT, NT = Cf::NT, NP = Cf::NP, SRV = Cf::SRV;
     constexpr int PPS = SEG / 2;  // pairs per segment
-    constexpr int ACC = 2;        // independent argmax chains
+    // VAR 0: scan fused into the update (2 argmax chains); VAR 1: the scan runs as
+    // its own pass over the updated registers with 4 independent chains (ILP)
+    constexpr bool FUSED = VAR != 1;
+    constexpr int ACC = FUSED ? 2 : 4;  // independent argmax chains
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const Tile tile = a.tiles[blockIdx.x];
     v2_stage<Cf>(a, tile, smem_raw);
     const float* vE = reinterpret_cast<const float*>(smem_raw);
-    const double2* ptab = reinterpret_cast<const double2*>(smem_raw + Cf::OFF_P);
+    const float2* ptab = reinterpret_cast<const float2*>(smem_raw + Cf::OFF_P);
     const float2* twi = reinterpret_cast<const float2*>(smem_raw + Cf::OFF_TW);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -181,11 +185,12 @@ __global__ void __launch_bounds__(128, 3) k2v2r_kernel(K2Args a) {
         const double e_init = a.init_energy[pos];
         if (lane == 0) {
             const double im = 1e-12 * a.init_max[pos];
+            const double w0 = a.w0[tile.cls];
             st->energy = a.energy0[pos];
             st->thr_e = 1e-12 * e_init;
-            st->thr_m = im * im;
-            st->w0 = a.w0[tile.cls];
-            st->gw = a.gamma / st->w0;
+            st->thr_m = (float)(im * im);
+            st->w0 = (float)w0;
+            st->gw = (float)(a.gamma / w0);
             st->nu = a.nu0 ? a.nu0[pos] : 0;
             st->ntrace = a.trace_from_nu0 ? st->nu : 0;
         }
@@ -238,37 +243,39 @@ __global__ void __launch_bounds__(128, 3) k2v2r_kernel(K2Args a) {
             }
             const int G = __shfl_sync(0xffffffffu, (SPT == 2 && sw == 1) ? gb1 : gb0, wl) + jw;
 
-            // ---- scalar part of iterate (engine_spectral.cpp:58-110), fp64 ----
-            const double Mf = (double)__uint_as_float(M), Sf = (double)__uint_as_float(S);
-            const double energy = st->energy, w0 = st->w0, gw = st->gw;
-            if (energy < st->thr_e || !(Mf > 0.0) || Mf < st->thr_m) {
+            // ---- scalar part of iterate (engine_spectral.cpp:58-110), fp32 (the
+            // update it feeds is fp32); the energy bookkeeping accumulates in fp64 ----
+            const float Mf = __uint_as_float(M), Sf = __uint_as_float(S);
+            const double energy = st->energy;
+            const float w0 = st->w0, gw = st->gw;
+            if (energy < st->thr_e || !(Mf > 0.f) || Mf < st->thr_m) {
                 conv = 1;
                 break;
             }
-            if (Sf > Mf * (1.0 - a.tau)) {  // tau == 0 disables (Sf <= Mf)
+            if (Sf > Mf * (float)(1.0 - a.tau)) {  // tau == 0 disables (Sf <= Mf)
                 flagged = 1;  // near-tie: the host re-runs this block in fp64
                 break;
             }
             const int u1 = G / T, u2 = G % T;
-            const int self = ((T - u1) % T == u1) && ((T - u2) % T == u2);
-            const double pr = pre.x, pi = pre.y;
-            const double2 P = ptab[(u1 * (a.Lh - 1) + u2 * (a.Lw - 1)) & (2 * T - 1)];  // e^{-j phi(u)}
-            const double ar = pr * gw, ai = pi * gw;  // a = gamma R'[u] / w0
-            double c_re = ar * P.x - ai * P.y, c_im = ar * P.y + ai * P.x;  // c = P a
-            double a_re = ar, a_im = ai, delta;
+            const int self = ((u1 & (T / 2 - 1)) == 0) && ((u2 & (T / 2 - 1)) == 0);
+            const float pr = pre.x, pi = pre.y;
+            const float2 P = ptab[(u1 * (a.Lh - 1) + u2 * (a.Lw - 1)) & (2 * T - 1)];  // e^{-j phi(u)}
+            const float ar = pr * gw, ai = pi * gw;  // a = gamma R'[u] / w0
+            float c_re = ar * P.x - ai * P.y, c_im = ar * P.y + ai * P.x;  // c = P a
+            float a_re = ar, a_im = ai, delta;
             if (self) {
-                c_im = 0.0;
+                c_im = 0.f;
                 a_re = c_re * P.x;
                 a_im = -c_re * P.y;
-                delta = -2.0 * c_re * (pr * P.x - pi * P.y) + c_re * c_re * w0;
+                delta = c_re * (c_re * w0 - 2.f * (pr * P.x - pi * P.y));
             } else {
                 const int mi1 = 2 * u1, mi2 = 2 * u2;
                 const float v2 = vE[(mi1 & (T - 1)) * SRV + (mi2 & (T - 1))];
-                const double sig = ((mi1 >= T) ? (double)sgn_r : 1.0) * ((mi2 >= T) ? (double)sgn_c : 1.0);
-                delta = -4.0 * (a_re * pr + a_im * pi) + 2.0 * (a_re * a_re + a_im * a_im) * w0 +
-                        2.0 * sig * (double)v2 * (a_re * a_re - a_im * a_im);
+                const float sig = ((mi1 >= T) ? sgn_r : 1.f) * ((mi2 >= T) ? sgn_c : 1.f);
+                delta = -4.f * (a_re * pr + a_im * pi) + 2.f * (a_re * a_re + a_im * a_im) * w0 +
+                        2.f * sig * v2 * (a_re * a_re - a_im * a_im);
             }
-            const double e = energy + delta;
+            const double e = energy + (double)delta;
             const double en = 0.0 < e ? e : 0.0;
             const int nu = st->nu + 1;
             __syncwarp();
@@ -281,17 +288,13 @@ __global__ void __launch_bounds__(128, 3) k2v2r_kernel(K2Args a) {
                 }
                 st->energy = en;
                 st->nu = nu;
-            }
-            if (a.trace || a.gap_trace) {  // diagnostics only
-                if (lane == 0) {
-                    const int tstride = a.trace_stride > 0 ? a.trace_stride : a.iterations;
-                    const double iw = 1.0 / w0;
-                    v2_record(a, b, nu, st->ntrace, 0, tstride, nullptr, nullptr, u1, u2, self,
-                              (pr * P.x - pi * P.y) * iw, (pr * P.y + pi * P.x) * iw, c_re, c_im, en, Mf, Sf);
-                    st->ntrace += 1;
-                }
-            } else if (lane == 0) {
                 st->ntrace += 1;
+                if (a.trace || a.gap_trace) {  // diagnostics only
+                    const int tstride = a.trace_stride > 0 ? a.trace_stride : a.iterations;
+                    const float iw = 1.f / w0;
+                    v2_record(a, b, nu, st->ntrace - 1, 0, tstride, nullptr, nullptr, u1, u2, self,
+                              (pr * P.x - pi * P.y) * iw, (pr * P.y + pi * P.x) * iw, c_re, c_im, en, Mf, Sf);
+                }
             }
 
             // ---- residual update: R' -= s1 a V[k-u] + s2 conj(a) V[k+u] (+ next scan) ----
@@ -318,7 +321,8 @@ __global__ void __launch_bounds__(128, 3) k2v2r_kernel(K2Args a) {
                         const float2 x = va[q];
                         rp[p] = __ffma2_rn(n1r, x, rp[p]);
                         ip[p] = __ffma2_rn(n1i, x, ip[p]);
-                        kacc_pair(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+                        if constexpr (FUSED)
+                            kacc_pair(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
                     }
                 } else {
 #pragma unroll
@@ -327,7 +331,8 @@ __global__ void __launch_bounds__(128, 3) k2v2r_kernel(K2Args a) {
                         const float2 x = va[q], y = vb[q];
                         rp[p] = __ffma2_rn(n2r, y, __ffma2_rn(n1r, x, rp[p]));
                         ip[p] = __ffma2_rn(n2i, y, __ffma2_rn(n1i, x, ip[p]));
-                        kacc_pair(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+                        if constexpr (FUSED)
+                            kacc_pair(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
                     }
                 }
                 if (exs[s]) {
@@ -339,8 +344,16 @@ __global__ void __launch_bounds__(128, 3) k2v2r_kernel(K2Args a) {
                         xr[s] = fmaf(-s2 * fr, y, xr[s]);
                         xi[s] = fmaf(s2 * fi, y, xi[s]);
                     }
-                    kacc_one(A[ACC], fmaf(xi[s], xi[s], xr[s] * xr[s]), NP + s, kmask);
+                    if constexpr (FUSED) kacc_one(A[ACC], fmaf(xi[s], xi[s], xr[s] * xr[s]), NP + s, kmask);
                 }
+            }
+            if constexpr (!FUSED) {
+#pragma unroll
+                for (int p = 0; p < NP; ++p)
+                    kacc_pair(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+#pragma unroll
+                for (int s = 0; s < SPT; ++s)
+                    if (exs[s]) kacc_one(A[ACC], fmaf(xi[s], xi[s], xr[s] * xr[s]), NP + s, kmask);
             }
         }
 
@@ -382,6 +395,7 @@ struct V2R2Cfg {
     static constexpr size_t WELEMS = (size_t)2 * T * SRV;
     static constexpr size_t IMG_BYTES = WELEMS * 4;
     static constexpr bool TW64 = false;
+    static constexpr bool P32 = false;
     static constexpr size_t WBYTES = ((IMG_BYTES + 15) / 16) * 16;
     static constexpr size_t OFF_P = WBYTES;
     static constexpr size_t OFF_TW = OFF_P + sizeof(double2) * 2 * T;
@@ -787,10 +801,22 @@ __global__ void __launch_bounds__(256) cvt_kernel(CvtArgs a) {
     }
 }
 
+static int g_v2r_var = -1;
+static int v2r_variant() {
+    if (g_v2r_var < 0) {
+        const char* e = getenv("FOFSE_V2R_VAR");
+        g_v2r_var = e ? atoi(e) : 0;
+    }
+    return g_v2r_var;
+}
+
 template <int T, int PATH>
 static int k2v2_launch_t(const K2Args& a, int32_t ntiles, cudaStream_t s) {
     using Cf = V2Cfg<T, PATH>;
-    auto* fn = PATH == PATH_F32_REAL ? k2v2r_kernel<T> : k2v2c_kernel<T>;
+    auto* fn = PATH == PATH_F32_REAL ? (v2r_variant() == 1   ? k2v2r_kernel<T, 1>
+                                        : v2r_variant() == 2 ? k2v2r_kernel<T, 2>
+                                                             : k2v2r_kernel<T, 0>)
+                                     : k2v2c_kernel<T>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
     if (e != cudaSuccess) return e;
     if (ntiles <= 0) return cudaSuccess;

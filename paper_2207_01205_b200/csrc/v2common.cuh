@@ -19,9 +19,9 @@ __device__ __forceinline__ constexpr int T_of() { return Cf::HT * 2; }
 struct V2State {
     double energy;  // weighted residual energy (engine_spectral.cpp:100-110)
     double thr_e;   // 1e-12 * initial_energy        (stop test, :60)
-    double thr_m;   // (1e-12 * initial_max)^2 on |R|^2 (stop test, :61)
-    double w0, gw;  // W[0] and gamma / W[0]
-    int nu, ntrace, pad0, pad1;
+    float thr_m;    // (1e-12 * initial_max)^2 on |R|^2 (stop test, :61)
+    float w0, gw;   // W[0] and gamma / W[0]
+    int nu, ntrace, pad0;
 };
 static_assert(sizeof(V2State) <= 64, "state slot");
 
@@ -45,8 +45,13 @@ __device__ __forceinline__ void v2_stage(const K2Args& a, const Tile& tile, unsi
         for (uint32_t off = 0; off < bytes; off += 32768)
             bulk_g2s(smem + off, src + off, bytes - off < 32768u ? bytes - off : 32768u, bar);
     }
-    for (int i = threadIdx.x; i < 2 * T_of<Cf>(); i += blockDim.x)
-        reinterpret_cast<double2*>(smem + Cf::OFF_P)[i] = a.ptab ? a.ptab[i] : make_double2(1.0, 0.0);
+    for (int i = threadIdx.x; i < 2 * T_of<Cf>(); i += blockDim.x) {
+        const double2 p = a.ptab ? a.ptab[i] : make_double2(1.0, 0.0);
+        if constexpr (Cf::P32)
+            reinterpret_cast<float2*>(smem + Cf::OFF_P)[i] = make_float2((float)p.x, (float)p.y);
+        else
+            reinterpret_cast<double2*>(smem + Cf::OFF_P)[i] = p;
+    }
     for (int i = threadIdx.x; i < T_of<Cf>(); i += blockDim.x) {
         const double2 t = a.twid_inv[i];
         if constexpr (Cf::TW64)
@@ -124,15 +129,27 @@ __device__ __forceinline__ void v2_finish(const K2Args& a, const BlockDesc& desc
             mm[k] = a.reg_r0 + (px < npx ? px / a.reg_nc : 0);
             nn[k] = a.reg_c0 + (px < npx ? px % a.reg_nc : 0);
         }
-        for (int q = 0; q < nr; ++q) {
-            const int u = rec_u[q];
-            const double2 cd = rec_c[q];
-            const Acc cx = (Acc)cd.x, cy = (Acc)cd.y;
-            const int uu1 = u >> 16, uu2 = u & 0xffff;
+        // records are staged 32 at a time in the lanes' registers (one coalesced
+        // load each) and broadcast with shuffles
+        for (int q0 = 0; q0 < nr; q0 += 32) {
+            int uq = 0;
+            Acc cxq = 0, cyq = 0;
+            if (q0 + lane < nr) {
+                uq = rec_u[q0 + lane];
+                const double2 cd = rec_c[q0 + lane];
+                cxq = (Acc)cd.x;
+                cyq = (Acc)cd.y;
+            }
+            const int nq = nr - q0 < 32 ? nr - q0 : 32;
+            for (int q = 0; q < nq; ++q) {
+                const int u = __shfl_sync(0xffffffffu, uq, q);
+                const Acc cx = __shfl_sync(0xffffffffu, cxq, q), cy = __shfl_sync(0xffffffffu, cyq, q);
+                const int uu1 = u >> 16, uu2 = u & 0xffff;
 #pragma unroll
-            for (int k = 0; k < PX; ++k) {
-                const TW tw = twi[(uu1 * mm[k] + uu2 * nn[k]) & (T - 1)];
-                acc[k] = fma(cx, tw.x, fma(-cy, tw.y, acc[k]));
+                for (int k = 0; k < PX; ++k) {
+                    const TW tw = twi[(uu1 * mm[k] + uu2 * nn[k]) & (T - 1)];
+                    acc[k] = fma(cx, tw.x, fma(-cy, tw.y, acc[k]));
+                }
             }
         }
 #pragma unroll
