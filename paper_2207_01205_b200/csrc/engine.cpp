@@ -534,7 +534,10 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
     // from seg_for(T, 0); K2v2 uses v2_seg(T) — equal for every T).
     double2* d_wimg64 = ctx->buf("wimg64").as<double2>(static_cast<size_t>(ncls) * T * sr64);
     float2* d_wimg32 = fp32 ? ctx->buf("wimg32").as<float2>(static_cast<size_t>(ncls) * T * sr32) : nullptr;
-    const size_t vimg_elems = v2 ? 2 * static_cast<size_t>(T) * v2_srv(T) : static_cast<size_t>(T) * sr32;
+    const int vcopies = v2 ? v2_real_copies(T) : 1;
+    const size_t vimg_elems = !v2 ? static_cast<size_t>(T) * sr32
+                              : vcopies == 4 ? 4 * static_cast<size_t>(T) * v2_srv4(T)
+                                             : 2 * static_cast<size_t>(T) * v2_srv(T);
     float* d_vimg32 = fp32 ? ctx->buf("vimg32").as<float>(static_cast<size_t>(ncls) * vimg_elems) : nullptr;
     double* d_w0 = ctx->buf("w0").as<double>(static_cast<size_t>(ncls));
     const size_t vimg64_elems = 2 * static_cast<size_t>(T) * d_srv(T);
@@ -550,7 +553,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         a.wimg64 = d_wimg64;
         a.wimg32 = d_wimg32;
         a.vimg32 = d_vimg32;
-        a.vpairs = v2 ? 1 : 0;
+        a.vpairs = v2 ? (vcopies == 4 ? 4 : 1) : 0;
         a.vimg64 = d_vimg64;
         a.w0 = d_w0;
         a.twid = d_twf;
@@ -647,6 +650,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         a.init_energy = d_e0;
         a.init_max = d_imax;
         a.conv_out = d_conv;
+        a.kmask = 0xffffffc0u;
         return a;
     };
     auto tiles_for = [&](int64_t b0, int64_t b1, int ng) {

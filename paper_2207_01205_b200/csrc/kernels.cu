@@ -144,8 +144,8 @@ __global__ void __launch_bounds__(256) k1_kernel(K1Args a) {
             // rotated real V with its anti-periodic extension (col >= T: sc V[col-T]).
             // vpairs (K2v2): two copies, E[c] = V[c] and O[c] = V[c+1], row stride
             // v2_srv(T), so every pair of adjacent columns is one aligned 8-byte load.
-            const int srv = a.vpairs ? v2_srv(T) : sr32;
-            const int ncopy = a.vpairs ? 2 : 1;
+            const int srv = a.vpairs == 4 ? v2_srv4(T) : (a.vpairs ? v2_srv(T) : sr32);
+            const int ncopy = a.vpairs == 4 ? 4 : (a.vpairs ? 2 : 1);
             float* o = a.vimg32 + (size_t)b * ncopy * T * srv;
             for (int i = threadIdx.x; i < ncopy * T * srv; i += blockDim.x) {
                 const int cp = i / (T * srv), rem = i % (T * srv);
@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(256) k1_kernel(K1Args a) {
                 const double2 w = k1_spec<T>(cbuf, r, k2);
                 const double2 ph = phase_pos<T>((long long)r * (a.Lh - 1) + (long long)k2 * (a.Lw - 1));
                 double v = w.x * ph.x - w.y * ph.y;  // Re(W e^{j phi})
-                if (col >= T) v *= sc;              // anti-periodic extension
+                if ((col / T) & 1) v *= sc;         // anti-periodic extension
                 o[i] = static_cast<float>(v);
             }
         }

@@ -72,7 +72,7 @@ struct K1Args {
     float2* wimg32;            // [ncls][T*SR32] complex fp32 image
     float* vimg32;             // [ncls][T*SR32] rotated real image ([ncls][2][T*SRV] with vpairs)
     double* vimg64;            // [ncls][2][T*d_srv(T)] fp64 rotated real image, even/odd pairs (K2d)
-    int32_t vpairs;            // write the K2v2 even/odd paired V layout
+    int32_t vpairs;            // K2v2 real V layout: 0 single, 1 even/odd pairs, 4 quads
     double* w0;                // [ncls]
     const double2* twid;       // e^{-j 2 pi k / T}, k < T
     const double2* ptab;       // e^{-j pi m / T}, m < 2T (rotation phases; NULL = computed)
@@ -124,6 +124,8 @@ struct K2Args {
     int32_t trace_from_nu0;     // trace index continues from nu0 (multi-phase calls)
     int32_t trace_stride;       // trace records per block (0 = iterations)
     int32_t state_by_pos;       // energy_out / nu_out / conv_out indexed by position
+    uint32_t kmask;             // K2v2 packed-key mantissa mask (0xffffffc0), a runtime value so
+                                // the key is one LOP3 (mask in a register, index immediate)
 };
 
 struct CvtArgs {

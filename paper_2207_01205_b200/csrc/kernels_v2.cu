@@ -28,7 +28,7 @@
 
 namespace fofse {
 
-template <int T, int PATH>
+template <int T, int PATH, bool Q4 = false>
 struct V2Cfg {
     static constexpr int SEG = v2_seg(T);
     static constexpr int SPT = v2_spt(T);
@@ -38,12 +38,13 @@ struct V2Cfg {
     static constexpr int NB = SPT * (SEG + 1);  // slots per lane (AoS layout)
     static constexpr int NP = SPT * SEG / 2;    // bin pairs per lane (SoA real path)
     static constexpr int SR = T + SEG + 1;      // complex image row stride
-    static constexpr int SRV = v2_srv(T);       // paired real image row stride
+    static constexpr int SRV = Q4 ? v2_srv4(T) : v2_srv(T);  // real image row stride
+    static constexpr int NCOPY = Q4 ? 4 : 2;                   // copies of V (shifted by 0..NCOPY-1)
     static constexpr int SLOTS = NB * NT;
     static constexpr int WARPS = 4;
     static constexpr bool REAL = PATH == PATH_F32_REAL;
     // REAL: two float copies (even / odd aligned) of the rotated V; else complex W
-    static constexpr size_t WELEMS = REAL ? (size_t)2 * T * SRV : (size_t)T * SR;
+    static constexpr size_t WELEMS = REAL ? (size_t)NCOPY * T * SRV : (size_t)T * SR;
     static constexpr size_t IMG_BYTES = WELEMS * (REAL ? 4 : 8);
     static constexpr bool TW64 = false;
     static constexpr bool P32 = true;  // fp32 rotated-frame phase table
@@ -66,10 +67,10 @@ struct V2Cfg {
 struct KAcc {
     float m1, m2;  // best key, runner-up
 };
-__device__ __forceinline__ unsigned key_mask() {
-    unsigned m;  // kept in a register so the key is one LOP3: (bits & mask) | imm
-    asm volatile("mov.b32 %0, 0xffffffc0;" : "=r"(m));
-    return m;
+template <bool RUNTIME = true>
+__device__ __forceinline__ unsigned key_mask(const K2Args& a) {
+    if constexpr (RUNTIME) return a.kmask ? a.kmask : 0xffffffc0u;  // runtime value: kept in a register
+    return 0xffffffc0u;
 }
 __device__ __forceinline__ float pkey(float m, int p, unsigned mask) {
     return __uint_as_float((__float_as_uint(m) & mask) | static_cast<unsigned>(63 - p));
@@ -126,13 +127,16 @@ __device__ __forceinline__ void am_merge(float& m1, int& i1, float& m2, float om
 // ============================================================================
 template <int T, int VAR>
 __global__ void __launch_bounds__(128, VAR == 0 ? 3 : 2) k2v2r_kernel(K2Args a) {
-    using Cf = V2Cfg<T, PATH_F32_REAL>;
+    // VAR 3: quad V layout, one LDS.128 per two bin pairs
+    constexpr bool Q4 = VAR == 3 || VAR == 9;
+    using Cf = V2Cfg<T, PATH_F32_REAL, Q4>;
     constexpr int SEG = Cf::SEG, SPT = Cf::SPT, NT = Cf::NT, NP = Cf::NP, SRV = Cf::SRV;
     constexpr int PPS = SEG / 2;  // pairs per segment
     // VAR 0: scan fused into the update (2 argmax chains); VAR 1: the scan runs as
     // its own pass over the updated registers with 4 independent chains (ILP)
     constexpr bool FUSED = VAR != 1;
-    constexpr int ACC = FUSED ? 2 : 4;  // independent argmax chains
+    static_assert(!Q4 || FUSED, "quad layout uses the fused scan");
+    constexpr int ACC = (VAR == 0 || VAR == 2) ? 2 : 4;  // independent argmax chains
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const Tile tile = a.tiles[blockIdx.x];
@@ -157,7 +161,7 @@ __global__ void __launch_bounds__(128, VAR == 0 ? 3 : 2) k2v2r_kernel(K2Args a) 
     static_assert(NP + SPT <= 64, "pair index must fit the 6 key bits");
     const float sgn_r = ((a.Lh - 1) & 1) ? -1.f : 1.f;
     const float sgn_c = ((a.Lw - 1) & 1) ? -1.f : 1.f;
-    const unsigned kmask = key_mask();
+    const unsigned kmask = key_mask<VAR != 0>(a);
     V2State* st = reinterpret_cast<V2State*>(smem_raw + Cf::OFF_ST + 64 * warp);
 
     for (int bi = warp; bi < tile.count; bi += Cf::WARPS) {
@@ -210,6 +214,20 @@ __global__ void __launch_bounds__(128, VAR == 0 ? 3 : 2) k2v2r_kernel(K2Args a) 
             if (exs[s]) kacc_one(A[ACC], fmaf(xi[s], xi[s], xr[s] * xr[s]), NP + s, kmask);
 
         for (int it = 0; it < a.iterations && !conv; ++it) {
+            int u1, u2, self;
+            float a_re, a_im;
+            if constexpr (VAR == 9) {
+                // diagnostic: the update + scan alone (one REDUX, synthetic selections)
+                float bm1 = A[ACC].m1;
+#pragma unroll
+                for (int k = 0; k < ACC; ++k) bm1 = fmaxf(bm1, A[k].m1);
+                const unsigned M = __reduce_max_sync(0xffffffffu, fbits(bm1));
+                u1 = (it * 7 + static_cast<int>(M & 1u)) & (T / 2 - 1);
+                u2 = (it * 13 + 1) & (T - 1);
+                self = 0;
+                a_re = 1e-4f;
+                a_im = 1e-4f;
+            } else {
             float bm1 = A[0].m1, bm2 = A[0].m2;
 #pragma unroll
             for (int k = 1; k <= ACC; ++k) {
@@ -256,13 +274,16 @@ __global__ void __launch_bounds__(128, VAR == 0 ? 3 : 2) k2v2r_kernel(K2Args a) 
                 flagged = 1;  // near-tie: the host re-runs this block in fp64
                 break;
             }
-            const int u1 = G / T, u2 = G % T;
-            const int self = ((u1 & (T / 2 - 1)) == 0) && ((u2 & (T / 2 - 1)) == 0);
+            u1 = G / T;
+            u2 = G % T;
+            self = ((u1 & (T / 2 - 1)) == 0) && ((u2 & (T / 2 - 1)) == 0);
             const float pr = pre.x, pi = pre.y;
             const float2 P = ptab[(u1 * (a.Lh - 1) + u2 * (a.Lw - 1)) & (2 * T - 1)];  // e^{-j phi(u)}
             const float ar = pr * gw, ai = pi * gw;  // a = gamma R'[u] / w0
             float c_re = ar * P.x - ai * P.y, c_im = ar * P.y + ai * P.x;  // c = P a
-            float a_re = ar, a_im = ai, delta;
+            float delta;
+            a_re = ar;
+            a_im = ai;
             if (self) {
                 c_im = 0.f;
                 a_re = c_re * P.x;
@@ -297,6 +318,7 @@ __global__ void __launch_bounds__(128, VAR == 0 ? 3 : 2) k2v2r_kernel(K2Args a) 
                 }
             }
 
+            }
             // ---- residual update: R' -= s1 a V[k-u] + s2 conj(a) V[k+u] (+ next scan) ----
             const float fr = (float)a_re, fi = (float)a_im;
             const int par = u2 & 1;
@@ -314,7 +336,39 @@ __global__ void __launch_bounds__(128, VAR == 0 ? 3 : 2) k2v2r_kernel(K2Args a) 
                 const float2* vb = reinterpret_cast<const float2*>(vimg + rB * SRV + (cB - par));
                 const float2 n1r = make_float2(-s1 * fr, -s1 * fr), n1i = make_float2(-s1 * fi, -s1 * fi);
                 const float2 n2r = make_float2(-s2 * fr, -s2 * fr), n2i = make_float2(s2 * fi, s2 * fi);
-                if (self) {
+                if constexpr (Q4) {
+                    // copy k holds V[c + k]: columns cA.. are 16-byte aligned in copy cA & 3
+                    const int shA = cA & 3, shB = cB & 3;
+                    const float4* qa = reinterpret_cast<const float4*>(vE + shA * (T * SRV) + rA * SRV + (cA - shA));
+                    const float4* qb = reinterpret_cast<const float4*>(vE + shB * (T * SRV) + rB * SRV + (cB - shB));
+                    if (self) {
+#pragma unroll
+                        for (int q = 0; q < PPS / 2; ++q) {
+                            const int p = s * PPS + 2 * q;
+                            const float4 x = qa[q];
+                            rp[p] = __ffma2_rn(n1r, make_float2(x.x, x.y), rp[p]);
+                            ip[p] = __ffma2_rn(n1i, make_float2(x.x, x.y), ip[p]);
+                            rp[p + 1] = __ffma2_rn(n1r, make_float2(x.z, x.w), rp[p + 1]);
+                            ip[p + 1] = __ffma2_rn(n1i, make_float2(x.z, x.w), ip[p + 1]);
+                            kacc_pair(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+                            kacc_pair(A[(p + 1) % ACC], __ffma2_rn(ip[p + 1], ip[p + 1], __fmul2_rn(rp[p + 1], rp[p + 1])),
+                                      p + 1, kmask);
+                        }
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < PPS / 2; ++q) {
+                            const int p = s * PPS + 2 * q;
+                            const float4 x = qa[q], y = qb[q];
+                            rp[p] = __ffma2_rn(n2r, make_float2(y.x, y.y), __ffma2_rn(n1r, make_float2(x.x, x.y), rp[p]));
+                            ip[p] = __ffma2_rn(n2i, make_float2(y.x, y.y), __ffma2_rn(n1i, make_float2(x.x, x.y), ip[p]));
+                            rp[p + 1] = __ffma2_rn(n2r, make_float2(y.z, y.w), __ffma2_rn(n1r, make_float2(x.z, x.w), rp[p + 1]));
+                            ip[p + 1] = __ffma2_rn(n2i, make_float2(y.z, y.w), __ffma2_rn(n1i, make_float2(x.z, x.w), ip[p + 1]));
+                            kacc_pair(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+                            kacc_pair(A[(p + 1) % ACC], __ffma2_rn(ip[p + 1], ip[p + 1], __fmul2_rn(rp[p + 1], rp[p + 1])),
+                                      p + 1, kmask);
+                        }
+                    }
+                } else if (self) {
 #pragma unroll
                     for (int q = 0; q < PPS; ++q) {
                         const int p = s * PPS + q;
@@ -379,43 +433,47 @@ __global__ void __launch_bounds__(128, VAR == 0 ? 3 : 2) k2v2r_kernel(K2Args a) 
 // Real path, TWO WARPS PER LOST BLOCK (T = 64): each warp owns one 32-column
 // segment of every canonical row (16 bin pairs + the self-conjugate extra for
 // lane 0) — half the registers of the one-warp form, so twice the warps per SM
-// and room for instruction-level parallelism. The two warps meet once per
-// selection at a 64-thread named barrier: each warp publishes its best key,
-// runner-up and its winner lane's bins (double-buffered by iteration parity),
-// then both warps resolve the same global argmax and run the scalar update.
+// to hide the latency of the per-selection control chain. Once per selection
+// each warp publishes (best key, runner-up, winner pair, segment base) to a
+// parity-double-buffered slot; ONE 64-thread named barrier; both warps resolve
+// the same winner and run the (fp32) scalar part redundantly. V is held as four
+// shifted copies (quad layout) so every two bin pairs are one LDS.128.
 // ============================================================================
 template <int T>
-struct V2R2Cfg {
-    static constexpr int SEG = 32, SPT = 1, HT = T / 2, QN = T / SEG;
+struct V2HCfg {
+    static constexpr int SEG = 32, HT = T / 2, QN = T / SEG;
     static constexpr int NT = HT * QN;  // 64 threads = 2 warps
     static constexpr int NP = SEG / 2, PPS = SEG / 2;
-    static constexpr int SRV = T + SEG + 2;
-    static constexpr int GROUPS = 4;     // lost blocks per CTA (256 threads)
+    static constexpr int SRV = v2_srv4(T);
+    static constexpr int GROUPS = 4;  // lost blocks per CTA (256 threads)
     static constexpr bool REAL = true;
-    static constexpr size_t WELEMS = (size_t)2 * T * SRV;
+    static constexpr size_t WELEMS = (size_t)4 * T * SRV;
     static constexpr size_t IMG_BYTES = WELEMS * 4;
     static constexpr bool TW64 = false;
-    static constexpr bool P32 = false;
+    static constexpr bool P32 = true;
     static constexpr size_t WBYTES = ((IMG_BYTES + 15) / 16) * 16;
     static constexpr size_t OFF_P = WBYTES;
     static constexpr size_t OFF_TW = OFF_P + sizeof(double2) * 2 * T;
-    // per group: slots [2 parity][2 warps] x 16 B, spill [2][2][NP+1] float4, red 2 doubles
-    static constexpr size_t GRP = 2 * 2 * 16 + 2 * 2 * (NP + 1) * 16 + 16;
+    // per group: slots [2 parity][2 warps] x 32 B, red 2 doubles
+    static constexpr size_t GRP = 2 * 2 * 32 + 16;
     static constexpr size_t OFF_G = OFF_TW + sizeof(float2) * T;
     static constexpr size_t OFF_BAR = OFF_G + GRP * GROUPS;
     static constexpr size_t SMEM = OFF_BAR + 16;
     static_assert(NT == 64, "two warps per block");
 };
 
-struct R2Slot {
-    unsigned key;
-    float second;
-    int gbase, lane;
+struct HSlot {
+    unsigned key;   // the warp's best packed key
+    float second;   // its runner-up
+    int gbase;      // row-major index of the winner lane's segment start
+    int pad;
+    float4 pair;    // the winning bin pair (re_a, re_b, im_a, im_b) or the extra bin
 };
+static_assert(sizeof(HSlot) == 32, "slot");
 
 template <int T>
-__global__ void __launch_bounds__(256, 2) k2v2r2_kernel(K2Args a) {
-    using Cf = V2R2Cfg<T>;
+__global__ void __launch_bounds__(256, 2) k2v2h_kernel(K2Args a) {
+    using Cf = V2HCfg<T>;
     constexpr int SEG = Cf::SEG, NT = Cf::NT, NP = Cf::NP, PPS = Cf::PPS, SRV = Cf::SRV;
     constexpr int ACC = 2;
 
@@ -423,15 +481,14 @@ __global__ void __launch_bounds__(256, 2) k2v2r2_kernel(K2Args a) {
     const Tile tile = a.tiles[blockIdx.x];
     v2_stage<Cf>(a, tile, smem_raw);
     const float* vE = reinterpret_cast<const float*>(smem_raw);
-    const double2* ptab = reinterpret_cast<const double2*>(smem_raw + Cf::OFF_P);
+    const float2* ptab = reinterpret_cast<const float2*>(smem_raw + Cf::OFF_P);
     const float2* twi = reinterpret_cast<const float2*>(smem_raw + Cf::OFF_TW);
 
     const int grp = threadIdx.x / NT, tid = threadIdx.x % NT;
     const int w = tid >> 5, lane = tid & 31;
     unsigned char* gsm = smem_raw + Cf::OFF_G + Cf::GRP * grp;
-    R2Slot* slots = reinterpret_cast<R2Slot*>(gsm);                       // [2][2]
-    float4* spills = reinterpret_cast<float4*>(gsm + 2 * 2 * 16);          // [2][2][NP+1]
-    double* red = reinterpret_cast<double*>(gsm + 2 * 2 * 16 + 2 * 2 * (NP + 1) * 16);
+    HSlot* slots = reinterpret_cast<HSlot*>(gsm);  // [2][2]
+    double* red = reinterpret_cast<double*>(gsm + 2 * 2 * 32);
     const int bar = 1 + grp;
 
     const BinLayout L = BinLayout::make(T, SEG, 1);
@@ -440,9 +497,12 @@ __global__ void __launch_bounds__(256, 2) k2v2r2_kernel(K2Args a) {
     const int gb = k1 * T + c0;
     const float sgn_r = ((a.Lh - 1) & 1) ? -1.f : 1.f;
     const float sgn_c = ((a.Lw - 1) & 1) ? -1.f : 1.f;
-    const unsigned kmask = key_mask();
+    const unsigned kmask = key_mask(a);
     const int rstride = a.rec_stride > 0 ? a.rec_stride : a.iterations;
     const int tstride = a.trace_stride > 0 ? a.trace_stride : a.iterations;
+    const float w0 = (float)a.w0[tile.cls], gw = (float)(a.gamma / a.w0[tile.cls]);
+    const float tau1 = (float)(1.0 - a.tau);
+    const float iw = 1.f / w0;
 
     for (int bi = grp; bi < tile.count; bi += Cf::GROUPS) {
         const int pos = tile.begin + bi;
@@ -465,12 +525,13 @@ __global__ void __launch_bounds__(256, 2) k2v2r2_kernel(K2Args a) {
         double energy = a.energy0[pos];
         const double e_init = a.init_energy[pos];
         const double thr_e = 1e-12 * e_init;
-        const double thr_m = (1e-12 * a.init_max[pos]) * (1e-12 * a.init_max[pos]);
-        const double w0 = a.w0[tile.cls], gw = a.gamma / w0;
+        const float thr_m = (float)((1e-12 * a.init_max[pos]) * (1e-12 * a.init_max[pos]));
         int nu = a.nu0 ? a.nu0[pos] : 0;
         int ntrace = a.trace_from_nu0 ? nu : 0;
         int conv = (a.conv0 ? a.conv0[pos] : 0) | (e_init <= 0.0);
         int flagged = 0;
+        int* rec_u = a.rec_u_g + (size_t)b * rstride;
+        double2* rec_c = a.rec_c_g + (size_t)b * rstride;
 
         KAcc A[ACC + 1];
 #pragma unroll
@@ -487,108 +548,109 @@ __global__ void __launch_bounds__(256, 2) k2v2r2_kernel(K2Args a) {
                 bm2 = fmax3(bm2, A[k].m2, fminf(bm1, A[k].m1));
                 bm1 = fmaxf(bm1, A[k].m1);
             }
-            // ---- per-warp argmax, published with the winner lane's bins ----
+            // ---- per-warp argmax (+ runner-up), published with the winner pair ----
             const unsigned Mw = __reduce_max_sync(0xffffffffu, fbits(bm1));
             const int wl = __ffs(__ballot_sync(0xffffffffu, fbits(bm1) == Mw)) - 1;
             const unsigned Sw = __reduce_max_sync(0xffffffffu, fbits(lane == wl ? bm2 : bm1));
             if (lane == wl) {
-                float4* sp = spills + (par * 2 + w) * (NP + 1);
-#pragma unroll
-                for (int p = 0; p < NP; ++p) sp[p] = make_float4(rp[p].x, rp[p].y, ip[p].x, ip[p].y);
-                sp[NP] = make_float4(xr, 0.f, xi, 0.f);
-                slots[par * 2 + w] = R2Slot{Mw, __uint_as_float(Sw), gb, wl};
+                const int pw = 63 - static_cast<int>(Mw & 63u);
+                float xra[1] = {xr}, xia[1] = {xi};
+                slots[par * 2 + w] = HSlot{Mw, __uint_as_float(Sw), gb, 0, pick_pair<NP, 1>(pw, rp, ip, xra, xia)};
             }
             named_bar_sync(bar, NT);
-            const R2Slot s0 = slots[par * 2], s1 = slots[par * 2 + 1];
-            const int ww = s1.key > s0.key ? 1 : 0;
-            const unsigned M = ww ? s1.key : s0.key;
-            const float S = fmaxf(ww ? s1.second : s0.second, __uint_as_float(ww ? s0.key : s1.key));
+            const HSlot s0 = slots[par * 2], s1 = slots[par * 2 + 1];
+            const bool w1 = s1.key > s0.key;  // keys are unique within a warp; ties across warps -> warp 0 (lower index)
+            const HSlot& sw = w1 ? s1 : s0;
+            const unsigned M = sw.key;
+            const float Mf = __uint_as_float(M);
+            const float Sf = fmaxf(sw.second, __uint_as_float(w1 ? s0.key : s1.key));
             const int pw = 63 - static_cast<int>(M & 63u);
             float2 pre;
             int jw;
-            {
-                const float4 q = spills[(par * 2 + ww) * (NP + 1) + pw];
-                if (pw < NP) {
-                    const float ma = fmaf(q.z, q.z, q.x * q.x), mb = fmaf(q.w, q.w, q.y * q.y);
-                    const int half = mb > ma ? 1 : 0;
-                    pre = half ? make_float2(q.y, q.w) : make_float2(q.x, q.z);
-                    jw = 2 * pw + half;
-                } else {
-                    pre = make_float2(q.x, q.z);
-                    jw = SEG;
-                }
+            if (pw < NP) {
+                const float4 q = sw.pair;
+                const float ma = fmaf(q.z, q.z, q.x * q.x), mb = fmaf(q.w, q.w, q.y * q.y);
+                const int half = mb > ma ? 1 : 0;  // ties to the lower column
+                pre = half ? make_float2(q.y, q.w) : make_float2(q.x, q.z);
+                jw = 2 * pw + half;
+            } else {
+                pre = make_float2(sw.pair.x, sw.pair.z);
+                jw = SEG;
             }
-            const int G = (ww ? s1.gbase : s0.gbase) + jw;
+            const int G = sw.gbase + jw;
 
-            // ---- scalar part of iterate (engine_spectral.cpp:58-110), fp64, both warps ----
-            const double Mf = (double)__uint_as_float(M), Sf = (double)S;
-            if (energy < thr_e || !(Mf > 0.0) || Mf < thr_m) {
+            // ---- scalar part of iterate (engine_spectral.cpp:58-110), fp32, both warps ----
+            if (energy < thr_e || !(Mf > 0.f) || Mf < thr_m) {
                 conv = 1;
                 break;
             }
-            if (Sf > Mf * (1.0 - a.tau)) {
-                flagged = 1;
+            if (Sf > Mf * tau1) {
+                flagged = 1;  // near-tie: the host re-runs this block in fp64
                 break;
             }
             const int u1 = G / T, u2 = G % T;
-            const int self = ((T - u1) % T == u1) && ((T - u2) % T == u2);
-            const double pr = pre.x, pi = pre.y;
-            const double2 P = ptab[(u1 * (a.Lh - 1) + u2 * (a.Lw - 1)) & (2 * T - 1)];
-            const double ar = pr * gw, ai = pi * gw;
-            double c_re = ar * P.x - ai * P.y, c_im = ar * P.y + ai * P.x;
-            double a_re = ar, a_im = ai, delta;
+            const int self = ((u1 & (T / 2 - 1)) == 0) && ((u2 & (T / 2 - 1)) == 0);
+            const float pr = pre.x, pi = pre.y;
+            const float2 P = ptab[(u1 * (a.Lh - 1) + u2 * (a.Lw - 1)) & (2 * T - 1)];
+            const float ar = pr * gw, ai = pi * gw;
+            float c_re = ar * P.x - ai * P.y, c_im = ar * P.y + ai * P.x;
+            float a_re = ar, a_im = ai, delta;
             if (self) {
-                c_im = 0.0;
+                c_im = 0.f;
                 a_re = c_re * P.x;
                 a_im = -c_re * P.y;
-                delta = -2.0 * c_re * (pr * P.x - pi * P.y) + c_re * c_re * w0;
+                delta = c_re * (c_re * w0 - 2.f * (pr * P.x - pi * P.y));
             } else {
                 const int mi1 = 2 * u1, mi2 = 2 * u2;
                 const float v2 = vE[(mi1 & (T - 1)) * SRV + (mi2 & (T - 1))];
-                const double sig = ((mi1 >= T) ? (double)sgn_r : 1.0) * ((mi2 >= T) ? (double)sgn_c : 1.0);
-                delta = -4.0 * (a_re * pr + a_im * pi) + 2.0 * (a_re * a_re + a_im * a_im) * w0 +
-                        2.0 * sig * (double)v2 * (a_re * a_re - a_im * a_im);
+                const float sig = ((mi1 >= T) ? sgn_r : 1.f) * ((mi2 >= T) ? sgn_c : 1.f);
+                delta = -4.f * (a_re * pr + a_im * pi) + 2.f * (a_re * a_re + a_im * a_im) * w0 +
+                        2.f * sig * v2 * (a_re * a_re - a_im * a_im);
             }
-            const double e = energy + delta;
+            const double e = energy + (double)delta;
             energy = 0.0 < e ? e : 0.0;
             nu += 1;
-            if (tid == 0) {
-                const double iw = gw / a.gamma;
-                v2_record(a, b, nu, ntrace, rstride, tstride, a.rec_u_g + (size_t)b * rstride,
-                          a.rec_c_g + (size_t)b * rstride, u1, u2, self, (pr * P.x - pi * P.y) * iw,
-                          (pr * P.y + pi * P.x) * iw, c_re, c_im, energy, Mf, Sf);
-            }
+            if (tid == 0)
+                v2_record(a, b, nu, ntrace, rstride, tstride, rec_u, rec_c, u1, u2, self,
+                          (pr * P.x - pi * P.y) * iw, (pr * P.y + pi * P.x) * iw, c_re, c_im, energy, Mf, Sf);
             ntrace += 1;
 
             // ---- residual update of this warp's segment (+ fused next scan) ----
-            const float fr = (float)a_re, fi = (float)a_im;
-            const int pr2 = u2 & 1;
-            const float* vimg = vE + pr2 * (T * SRV);
+            const float fr = a_re, fi = a_im;
             const int rA = (k1 - u1) & (T - 1), rB = (k1 + u1) & (T - 1);
             const int cA = (c0 - u2) & (T - 1), cB = (c0 + u2) & (T - 1);
             const float s1f = ((k1 < u1) ? sgn_r : 1.f) * ((c0 < u2) ? sgn_c : 1.f);
             const float s2f = ((k1 + u1 >= T) ? sgn_r : 1.f) * ((c0 + u2 >= T) ? sgn_c : 1.f);
-            const float2* va = reinterpret_cast<const float2*>(vimg + rA * SRV + (cA - pr2));
-            const float2* vb = reinterpret_cast<const float2*>(vimg + rB * SRV + (cB - pr2));
+            const int shA = cA & 3, shB = cB & 3;
+            const float4* qa = reinterpret_cast<const float4*>(vE + shA * (T * SRV) + rA * SRV + (cA - shA));
+            const float4* qb = reinterpret_cast<const float4*>(vE + shB * (T * SRV) + rB * SRV + (cB - shB));
             const float2 n1r = make_float2(-s1f * fr, -s1f * fr), n1i = make_float2(-s1f * fi, -s1f * fi);
             const float2 n2r = make_float2(-s2f * fr, -s2f * fr), n2i = make_float2(s2f * fi, s2f * fi);
 #pragma unroll
             for (int k = 0; k <= ACC; ++k) A[k] = KAcc{0.f, 0.f};
             if (self) {
 #pragma unroll
-                for (int q = 0; q < PPS; ++q) {
-                    const float2 x = va[q];
-                    rp[q] = __ffma2_rn(n1r, x, rp[q]);
-                    ip[q] = __ffma2_rn(n1i, x, ip[q]);
-                    kacc_pair(A[q % ACC], __ffma2_rn(ip[q], ip[q], __fmul2_rn(rp[q], rp[q])), q, kmask);
+                for (int q = 0; q < PPS / 2; ++q) {
+                    const int p = 2 * q;
+                    const float4 x = qa[q];
+                    rp[p] = __ffma2_rn(n1r, make_float2(x.x, x.y), rp[p]);
+                    ip[p] = __ffma2_rn(n1i, make_float2(x.x, x.y), ip[p]);
+                    rp[p + 1] = __ffma2_rn(n1r, make_float2(x.z, x.w), rp[p + 1]);
+                    ip[p + 1] = __ffma2_rn(n1i, make_float2(x.z, x.w), ip[p + 1]);
+                    kacc_pair(A[0], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+                    kacc_pair(A[1], __ffma2_rn(ip[p + 1], ip[p + 1], __fmul2_rn(rp[p + 1], rp[p + 1])), p + 1, kmask);
                 }
             } else {
 #pragma unroll
-                for (int q = 0; q < PPS; ++q) {
-                    const float2 x = va[q], y = vb[q];
-                    rp[q] = __ffma2_rn(n2r, y, __ffma2_rn(n1r, x, rp[q]));
-                    ip[q] = __ffma2_rn(n2i, y, __ffma2_rn(n1i, x, ip[q]));
-                    kacc_pair(A[q % ACC], __ffma2_rn(ip[q], ip[q], __fmul2_rn(rp[q], rp[q])), q, kmask);
+                for (int q = 0; q < PPS / 2; ++q) {
+                    const int p = 2 * q;
+                    const float4 x = qa[q], y = qb[q];
+                    rp[p] = __ffma2_rn(n2r, make_float2(y.x, y.y), __ffma2_rn(n1r, make_float2(x.x, x.y), rp[p]));
+                    ip[p] = __ffma2_rn(n2i, make_float2(y.x, y.y), __ffma2_rn(n1i, make_float2(x.x, x.y), ip[p]));
+                    rp[p + 1] = __ffma2_rn(n2r, make_float2(y.z, y.w), __ffma2_rn(n1r, make_float2(x.z, x.w), rp[p + 1]));
+                    ip[p + 1] = __ffma2_rn(n2i, make_float2(y.z, y.w), __ffma2_rn(n1i, make_float2(x.z, x.w), ip[p + 1]));
+                    kacc_pair(A[0], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+                    kacc_pair(A[1], __ffma2_rn(ip[p + 1], ip[p + 1], __fmul2_rn(rp[p + 1], rp[p + 1])), p + 1, kmask);
                 }
             }
             if (ex) {
@@ -613,9 +675,8 @@ __global__ void __launch_bounds__(256, 2) k2v2r2_kernel(K2Args a) {
         }
         // both warps see the records written by tid 0 before synthesising
         named_bar_sync(bar, NT);
-        v2_finish<T, NT>(a, a.blocks[pos], pos, b, tid, energy, nu, conv, flagged, ntrace,
-                         a.rec_u_g + (size_t)b * rstride, a.rec_c_g + (size_t)b * rstride, rstride, twi,
-                         red, bar);
+        v2_finish<T, NT>(a, a.blocks[pos], pos, b, tid, energy, nu, conv, flagged, ntrace, rec_u, rec_c, rstride,
+                         twi, red, bar);
         named_bar_sync(bar, NT);
     }
 }
@@ -815,28 +876,32 @@ static int k2v2_launch_t(const K2Args& a, int32_t ntiles, cudaStream_t s) {
     using Cf = V2Cfg<T, PATH>;
     auto* fn = PATH == PATH_F32_REAL ? (v2r_variant() == 1   ? k2v2r_kernel<T, 1>
                                         : v2r_variant() == 2 ? k2v2r_kernel<T, 2>
+                                        : v2r_variant() == 3 ? k2v2r_kernel<T, 3>
+                                        : v2r_variant() == 9 ? k2v2r_kernel<T, 9>
                                                              : k2v2r_kernel<T, 0>)
                                      : k2v2c_kernel<T>;
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
+    const size_t smem = PATH == PATH_F32_REAL && (v2r_variant() == 3 || v2r_variant() == 9)
+                            ? V2Cfg<T, PATH, true>::SMEM : Cf::SMEM;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     if (ntiles <= 0) return cudaSuccess;
-    fn<<<ntiles, 32 * Cf::WARPS, Cf::SMEM, s>>>(a);
+    fn<<<ntiles, 32 * Cf::WARPS, smem, s>>>(a);
     return cudaGetLastError();
 }
 
 template <int T>
-static int k2v2r2_launch(const K2Args& a, int32_t ntiles, cudaStream_t s) {
-    using Cf = V2R2Cfg<T>;
-    cudaError_t e = cudaFuncSetAttribute(k2v2r2_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
+static int k2v2h_launch(const K2Args& a, int32_t ntiles, cudaStream_t s) {
+    using Cf = V2HCfg<T>;
+    cudaError_t e = cudaFuncSetAttribute(k2v2h_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
     if (e != cudaSuccess) return e;
     if (ntiles <= 0) return cudaSuccess;
-    k2v2r2_kernel<T><<<ntiles, Cf::NT * Cf::GROUPS, Cf::SMEM, s>>>(a);
+    k2v2h_kernel<T><<<ntiles, Cf::NT * Cf::GROUPS, Cf::SMEM, s>>>(a);
     return cudaGetLastError();
 }
 
 template <int T>
 static int k2v2_T(const K2Args& a, int32_t ntiles, cudaStream_t s) {
-    if (a.path == PATH_F32_REAL && v2_real_gw(T) == 2) return k2v2r2_launch<T == 64 ? 64 : 64>(a, ntiles, s);
+    if (a.path == PATH_F32_REAL && v2_real_gw(T) == 2) return k2v2h_launch<64>(a, ntiles, s);
     if (a.path == PATH_F32_REAL) return k2v2_launch_t<T, PATH_F32_REAL>(a, ntiles, s);
     if (a.path == PATH_F32_COMPLEX) return k2v2_launch_t<T, PATH_F32_COMPLEX>(a, ntiles, s);
     return cudaErrorInvalidValue;
@@ -853,6 +918,11 @@ int k2v2_launch(const K2Args& a, int32_t ntiles, cudaStream_t s) {
 }
 
 int k2v2_warps_per_cta() { return 4; }  // lost blocks per CTA (both forms)
+
+int v2_real_copies(int t) {
+    if (v2_real_gw(t) == 2) return 4;  // K2v2h: quad layout
+    return (v2r_variant() == 3 || v2r_variant() == 9) ? 4 : 2;
+}
 
 static int g_real_gw = -1;
 int v2_real_gw(int t) {

@@ -123,11 +123,16 @@ FOFSE_HDC bool v2_supported(int t) { return t >= 8 && t <= 64; }
 // Row stride of K2v2's paired V images: T + SEG + 2 == 2 (mod 4), so 16 lanes on
 // consecutive rows hit distinct 8-byte bank pairs.
 FOFSE_HDC int v2_srv(int t) { return t + v2_seg(t) + 2; }
+// Quad layout: four copies C_k[c] = V[c + k] with a row stride that is a
+// multiple of 4, so any 4 consecutive columns are one aligned 16-byte load.
+FOFSE_HDC int v2_srv4(int t) { return ((t + v2_seg(t) + 4 + 3) / 4) * 4; }
 // Warps per lost block of the K2v2 real path: T = 64 splits the block over two
 // warps (one 32-column segment each), smaller T keep one warp.
 // (host override for experiments: v2_set_real_gw)
 int v2_real_gw(int t);
 inline int v2_real_spt(int t) { return v2_real_gw(t) == 2 ? 1 : v2_spt(t); }
+// Copies of V in the K2v2 real path's class image (2: even/odd pairs, 4: quads).
+int v2_real_copies(int t);
 
 // K2d (fp64 rotated frame): the fp64 strict bin layout (SEG = seg_for(T, 1),
 // one segment per thread), V as two fp64 copies (even / odd aligned) with row
