@@ -143,6 +143,30 @@ struct fofse_ctx {
     std::vector<cudaEvent_t> evpool;  // per-chunk events of the fp32 pipeline
     int64_t launches = 0;
 
+    // pinned staging for host -> device uploads (truly asynchronous copies);
+    // reset when an API call starts (every call ends with its streams idle)
+    char* pin = nullptr;
+    size_t pin_cap = 0, pin_used = 0;
+    void* stage(const void* src, size_t bytes) {
+        const size_t need = (bytes + 255) & ~size_t(255);
+        if (pin_used + need > pin_cap) {
+            // earlier staged copies of this call must land before the arena moves
+            for (cudaStream_t x : {stream, side, aux, cpy})
+                if (x) ck(cudaStreamSynchronize(x), "sync");
+            const size_t cap = std::max<size_t>({need, 2 * pin_cap, size_t(8) << 20});
+            if (pin) cudaFreeHost(pin);
+            pin = nullptr;
+            pin_cap = 0;
+            ck(cudaHostAlloc(reinterpret_cast<void**>(&pin), cap, cudaHostAllocDefault), "cudaHostAlloc");
+            pin_cap = cap;
+            pin_used = 0;
+        }
+        char* d = pin + pin_used;
+        pin_used += need;
+        std::memcpy(d, src, bytes);
+        return d;
+    }
+
     DevBuf& buf(const std::string& name) { return bufs[name]; }
     cudaEvent_t event(size_t i) {
         while (evpool.size() <= i) {
@@ -152,7 +176,10 @@ struct fofse_ctx {
         }
         return evpool[i];
     }
-    void activate() { ck(cudaSetDevice(device), "cudaSetDevice"); }
+    void activate() {
+        ck(cudaSetDevice(device), "cudaSetDevice");
+        pin_used = 0;
+    }
 };
 
 namespace {
@@ -337,6 +364,10 @@ struct Job {
     std::vector<BlockDesc> blocks;          // caller order
     std::vector<std::vector<uint8_t>> cls_labels;
     std::vector<double> wfull;
+    // cached execution order (run_job): caller ids by position and their descs
+    int order_key = -1;
+    std::vector<int32_t> ids;
+    std::vector<BlockDesc> sorted;
 };
 
 // Image-mode classes: key = (clip top/bottom/left/right, other lost blocks
@@ -433,12 +464,16 @@ std::vector<double2> twiddles(int T, int sign) {
     return tw;
 }
 
+// Host -> device copy through the context's pinned staging arena: the call
+// returns at once and the copy is ordered on stream s (default: ctx->stream).
 template <class T>
 T* upload(fofse_ctx* ctx, const std::string& name, const T* host, size_t count,
           cudaStream_t s = nullptr) {
     T* d = ctx->buf(name).as<T>(count);
     if (count)
-        ck(cudaMemcpyAsync(d, host, count * sizeof(T), cudaMemcpyHostToDevice, s ? s : ctx->stream), "H2D");
+        ck(cudaMemcpyAsync(d, ctx->stage(host, count * sizeof(T)), count * sizeof(T), cudaMemcpyHostToDevice,
+                           s ? s : ctx->stream),
+           "H2D");
     return d;
 }
 
@@ -461,6 +496,18 @@ struct RunOut {
     double init_ms = 0, iter_ms = 0, total_ms = 0, rerun_ms = 0;
     double chunk_pre_ms = 0, chunk_iter_ms = 0, rerun_tail_ms = 0;  // fp32 pipeline
     int64_t reruns = 0, converged = 0, head = 0;
+};
+
+// FOFSE_HOST_PROF=1 prints host-side checkpoints of run_job to stderr.
+struct HostProf {
+    bool on;
+    std::chrono::steady_clock::time_point t0;
+    HostProf() : on(std::getenv("FOFSE_HOST_PROF") != nullptr), t0(std::chrono::steady_clock::now()) {}
+    void mark(const char* what) const {
+        if (!on) return;
+        const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        std::fprintf(stderr, "[fofse host] %8.2f ms  %s\n", ms, what);
+    }
 };
 
 // FOFSE_F64_KERNEL=strict routes every fp64 iteration through the strict
@@ -499,6 +546,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
     const int ncls = static_cast<int>(job.cls_labels.size());
     const int I = cfg.iterations;
     RunOut out;
+    const HostProf hp_;
     cudaStream_t st = ctx->stream;
     for (auto& e : ctx->ev)
         if (!e) ck(cudaEventCreate(&e), "cudaEventCreate");
@@ -572,19 +620,36 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         ck(k1_launch(a, st), "K1 class spectra");
         ++ctx->launches;
     }
+    hp_.mark("class tables + K1 class");
 
-    // ---- blocks grouped by (path, class); stable within a class ----
-    std::vector<int32_t> ids(static_cast<size_t>(n));
-    std::iota(ids.begin(), ids.end(), 0);
-    std::stable_sort(ids.begin(), ids.end(), [&](int32_t x, int32_t y) {
-        const int px = path_of(job.blocks[x].cls), py = path_of(job.blocks[y].cls);
-        if (px != py) return px < py;
-        return job.blocks[x].cls < job.blocks[y].cls;
-    });
-    std::vector<BlockDesc> sorted(static_cast<size_t>(n));
-    for (int64_t i = 0; i < n; ++i) sorted[static_cast<size_t>(i)] = job.blocks[ids[static_cast<size_t>(i)]];
+    // ---- blocks grouped by (path, class); stable within a class (counting sort,
+    // cached in the job: plans reuse it across executions) ----
+    const int sort_key = (fp32 ? 1 : 0) | (use_d ? 2 : 0);
+    if (job.order_key != sort_key || job.ids.size() != static_cast<size_t>(n)) {
+        std::vector<int> cls_path(static_cast<size_t>(ncls));
+        for (int c = 0; c < ncls; ++c) cls_path[static_cast<size_t>(c)] = path_of(c);
+        const int nkeys = 4 * ncls;  // path (< 4) major, class minor
+        std::vector<int64_t> cnt(static_cast<size_t>(nkeys) + 1, 0);
+        auto key_of = [&](int32_t b) {
+            const int c = job.blocks[static_cast<size_t>(b)].cls;
+            return cls_path[static_cast<size_t>(c)] * ncls + c;
+        };
+        for (int64_t i = 0; i < n; ++i) ++cnt[static_cast<size_t>(key_of(static_cast<int32_t>(i))) + 1];
+        for (int k = 0; k < nkeys; ++k) cnt[static_cast<size_t>(k) + 1] += cnt[static_cast<size_t>(k)];
+        job.ids.assign(static_cast<size_t>(n), 0);
+        for (int64_t i = 0; i < n; ++i)
+            job.ids[static_cast<size_t>(cnt[static_cast<size_t>(key_of(static_cast<int32_t>(i)))]++)] =
+                static_cast<int32_t>(i);
+        job.sorted.resize(static_cast<size_t>(n));
+        for (int64_t i = 0; i < n; ++i) job.sorted[static_cast<size_t>(i)] = job.blocks[job.ids[static_cast<size_t>(i)]];
+        job.order_key = sort_key;
+    }
+    const std::vector<int32_t>& ids = job.ids;
+    const std::vector<BlockDesc>& sorted = job.sorted;
+    hp_.mark("sort");
     BlockDesc* d_sorted = upload(ctx, "sorted", sorted.data(), sorted.size());
     int32_t* d_ids = upload(ctx, "ids", ids.data(), ids.size());
+    hp_.mark("upload order");
     struct Range { int path; int64_t begin, end; };
     std::vector<Range> ranges;
     for (int64_t p0 = 0; p0 < n;) {
@@ -817,6 +882,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             ck(cudaEventRecord(ctx->event(3 * ci + 2), ch.s), "event");
         }
         ck(cudaEventRecord(ctx->ev[1], st), "event");  // all fp32 work enqueued
+        hp_.mark("fp32 chunks enqueued");
 
         // ---- near-tie guard: re-run flagged blocks in fp64 from scratch, per chunk ----
         int64_t max_chunk = 0;
@@ -847,8 +913,12 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             char* d_Rr = ctx->buf("Rr").as<char>(static_cast<size_t>(max_chunk) * r64_bytes);
             double* d_re0 = ctx->buf("re0").as<double>(static_cast<size_t>(max_chunk));
             double* d_rimax = ctx->buf("rimax").as<double>(static_cast<size_t>(max_chunk));
-            ck(cudaMemcpyAsync(d_rdesc, rdesc.data(), sizeof(BlockDesc) * m, cudaMemcpyHostToDevice, ctx->aux), "H2D");
-            ck(cudaMemcpyAsync(d_rr, rr.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, ctx->aux), "H2D");
+            ck(cudaMemcpyAsync(d_rdesc, ctx->stage(rdesc.data(), sizeof(BlockDesc) * m), sizeof(BlockDesc) * m,
+                               cudaMemcpyHostToDevice, ctx->aux),
+               "H2D");
+            ck(cudaMemcpyAsync(d_rr, ctx->stage(rr.data(), sizeof(int32_t) * m), sizeof(int32_t) * m,
+                               cudaMemcpyHostToDevice, ctx->aux),
+               "H2D");
             K2Args a = base_args();
             a.order = d_rr;
             a.blocks = d_rdesc;
@@ -860,9 +930,8 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             const int hp = hi_path(ch.path);
             k1_packed(d_rdesc, m, hp, seg64, 1, d_Rr, d_re0, d_rimax, 0, 0, ctx->aux);
             k2_f64(a, hp, 0, m, rdesc, tag, ctx->aux);
-            // the host vectors must outlive the (pageable) copies
-            ck(cudaStreamSynchronize(ctx->aux), "sync");
         }
+        hp_.mark("re-runs enqueued");
         ck(cudaEventRecord(ctx->ev[5], ctx->side), "event");
         ck(cudaStreamWaitEvent(st, ctx->ev[5], 0), "wait");
         ck(cudaEventRecord(ctx->ev[5], ctx->aux), "event");
@@ -892,6 +961,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         ck(cudaStreamSynchronize(st), "sync");
         for (int32_t c : conv) out.converged += c ? 1 : 0;
     }
+    hp_.mark("done");
     float ms = 0;
     ck(cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[3]), "elapsed");
     out.total_ms = ms;
@@ -1010,6 +1080,7 @@ void fofse_destroy(fofse_ctx* ctx) {
     for (auto& e : ctx->ev)
         if (e) cudaEventDestroy(e);
     for (auto e : ctx->evpool) cudaEventDestroy(e);
+    if (ctx->pin) cudaFreeHost(ctx->pin);
     for (cudaStream_t x : {ctx->side, ctx->aux, ctx->cpy})
         if (x) {
             cudaStreamSynchronize(x);
@@ -1253,13 +1324,21 @@ int fofse_conceal_frames_u8(fofse_ctx* ctx, const uint8_t* frames, int32_t n_fra
     return guarded([&] {
         if (!ctx || !frames || !restored || !offs || n_frames < 1)
             throw std::invalid_argument("conceal_frames: bad argument");
-        std::unique_ptr<fofse_plan> hold =
-            make_plan(ctx, n_frames, width, height, blocks, offs, bh, bw, params);
-        fofse_plan* plan = hold.get();
+        if (width < 1 || height < 1) throw std::invalid_argument("grid dimensions must be >= 1");
         ctx->activate();
+        // the frame upload (asynchronous from pinned memory) overlaps the host-side
+        // validation + window-mask classification of make_plan
         const size_t bytes = static_cast<size_t>(n_frames) * width * height;
         uint8_t* d_fr = ctx->buf("frames_u8").as<uint8_t>(bytes);
         ck(cudaMemcpyAsync(d_fr, frames, bytes, cudaMemcpyHostToDevice, ctx->stream), "H2D frames");
+        std::unique_ptr<fofse_plan> hold;
+        try {
+            hold = make_plan(ctx, n_frames, width, height, blocks, offs, bh, bw, params);
+        } catch (...) {
+            cudaStreamSynchronize(ctx->stream);  // the caller's buffer is being read
+            throw;
+        }
+        fofse_plan* plan = hold.get();
         const int64_t n = static_cast<int64_t>(plan->job.blocks.size());
         double* d_sq = ctx->buf("sq").as<double>(static_cast<size_t>(std::max<int64_t>(n, 1)));
         const int64_t l0 = ctx->launches;
