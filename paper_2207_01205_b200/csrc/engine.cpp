@@ -137,6 +137,7 @@ struct fofse_ctx {
     cudaStream_t side = nullptr;  // concurrent small launches (asymmetric-mask blocks)
     cudaStream_t aux = nullptr;   // fp32 guard re-runs, overlapping the later chunks
     cudaStream_t cpy = nullptr;   // guard-flag read-back
+    cudaStream_t io = nullptr;    // frame uploads / downloads of the pipelined host API
     bool own_stream = false;
     std::map<std::string, DevBuf> bufs;
     cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -151,7 +152,7 @@ struct fofse_ctx {
         const size_t need = (bytes + 255) & ~size_t(255);
         if (pin_used + need > pin_cap) {
             // earlier staged copies of this call must land before the arena moves
-            for (cudaStream_t x : {stream, side, aux, cpy})
+            for (cudaStream_t x : {stream, side, aux, cpy, io})
                 if (x) ck(cudaStreamSynchronize(x), "sync");
             const size_t cap = std::max<size_t>({need, 2 * pin_cap, size_t(8) << 20});
             if (pin) cudaFreeHost(pin);
@@ -364,6 +365,12 @@ struct Job {
     std::vector<BlockDesc> blocks;          // caller order
     std::vector<std::vector<uint8_t>> cls_labels;
     std::vector<double> wfull;
+    // frame groups of the pipelined frames API (group-major execution order)
+    int groups = 1;
+    int32_t nframes = 1;
+    int group_of(const BlockDesc& d) const {
+        return groups > 1 ? static_cast<int>(static_cast<int64_t>(d.frame) * groups / nframes) : 0;
+    }
     // cached execution order (run_job): caller ids by position and their descs
     int order_key = -1;
     std::vector<int32_t> ids;
@@ -532,13 +539,21 @@ double effective_tau(const Cfg& c, int head) {
     return head > 0 ? 1e-5 : 5e-5;
 }
 
+// Frame-group I/O hooks of the pipelined frames API: group g's first kernel
+// waits for h2d_done[g]; once all of group g's work (iteration, re-runs) is
+// enqueued, on_done(g, s) enqueues its download on stream s after it.
+struct GroupIO {
+    std::vector<cudaEvent_t> h2d_done;
+    std::function<void(int, cudaStream_t)> on_done;
+};
+
 // Device run of a job. fr: source (and destination) frames on device.
 // synth: SYN_IMAGE (write-back into frames + block_sq) or SYN_WINDOW (models).
 // Per-block device outputs (block_sq, models, trace, trace_count) are indexed
 // by the caller's block order.
 RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int synth,
                double* d_block_sq, double* d_models, fofse_record* d_trace, int32_t* d_trace_count,
-               float* d_gap = nullptr) {
+               float* d_gap = nullptr, const GroupIO* gio = nullptr) {
     using namespace fofse;
     const Geometry& g = job.geo;
     const int T = g.T;
@@ -624,15 +639,15 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
 
     // ---- blocks grouped by (path, class); stable within a class (counting sort,
     // cached in the job: plans reuse it across executions) ----
-    const int sort_key = (fp32 ? 1 : 0) | (use_d ? 2 : 0);
+    const int sort_key = (fp32 ? 1 : 0) | (use_d ? 2 : 0) | (job.groups << 2);
     if (job.order_key != sort_key || job.ids.size() != static_cast<size_t>(n)) {
         std::vector<int> cls_path(static_cast<size_t>(ncls));
         for (int c = 0; c < ncls; ++c) cls_path[static_cast<size_t>(c)] = path_of(c);
-        const int nkeys = 4 * ncls;  // path (< 4) major, class minor
+        const int nkeys = job.groups * 4 * ncls;  // frame group, then path (< 4), then class
         std::vector<int64_t> cnt(static_cast<size_t>(nkeys) + 1, 0);
         auto key_of = [&](int32_t b) {
-            const int c = job.blocks[static_cast<size_t>(b)].cls;
-            return cls_path[static_cast<size_t>(c)] * ncls + c;
+            const BlockDesc& d = job.blocks[static_cast<size_t>(b)];
+            return (job.group_of(d) * 4 + cls_path[static_cast<size_t>(d.cls)]) * ncls + d.cls;
         };
         for (int64_t i = 0; i < n; ++i) ++cnt[static_cast<size_t>(key_of(static_cast<int32_t>(i))) + 1];
         for (int k = 0; k < nkeys; ++k) cnt[static_cast<size_t>(k) + 1] += cnt[static_cast<size_t>(k)];
@@ -650,15 +665,22 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
     BlockDesc* d_sorted = upload(ctx, "sorted", sorted.data(), sorted.size());
     int32_t* d_ids = upload(ctx, "ids", ids.data(), ids.size());
     hp_.mark("upload order");
-    struct Range { int path; int64_t begin, end; };
+    struct Range { int path; int64_t begin, end; int grp; };
     std::vector<Range> ranges;
     for (int64_t p0 = 0; p0 < n;) {
         const int p = path_of(sorted[static_cast<size_t>(p0)].cls);
+        const int gq = job.group_of(sorted[static_cast<size_t>(p0)]);
         int64_t p1 = p0;
-        while (p1 < n && path_of(sorted[static_cast<size_t>(p1)].cls) == p) ++p1;
-        ranges.push_back({p, p0, p1});
+        while (p1 < n && path_of(sorted[static_cast<size_t>(p1)].cls) == p &&
+               job.group_of(sorted[static_cast<size_t>(p1)]) == gq)
+            ++p1;
+        ranges.push_back({p, p0, p1, gq});
         p0 = p1;
     }
+    const int ngroups = job.groups;
+    if (gio && !fp32)
+        for (int gq = 0; gq < ngroups; ++gq)
+            ck(cudaStreamWaitEvent(st, gio->h2d_done[static_cast<size_t>(gq)], 0), "wait");
 
     const BinLayout L64 = BinLayout::make(T, seg64), L32 = BinLayout::make(T, seg32, spt32);
     double* d_e0 = ctx->buf("e0").as<double>(static_cast<size_t>(n));      // by position
@@ -780,6 +802,8 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             k2_f64(a, hi_path(ranges[i].path), ranges[i].begin, ranges[i].end, sorted, std::to_string(i), st);
         ck(cudaEventRecord(ctx->ev[2], st), "event");
         ck(cudaEventRecord(ctx->ev[3], st), "event");
+        if (gio)
+            for (int gq = 0; gq < ngroups; ++gq) gio->on_done(gq, st);
     } else {
         // ---- fp32 fast mode: a pipeline over chunks of blocks ----
         // chunk = K1 (+ fp64 head + convert) + the fp32 iteration; once a chunk
@@ -798,6 +822,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             int path;
             int64_t b0, b1;
             cudaStream_t s;
+            int grp;
         };
         std::vector<Chunk> chunks;
         const int64_t chunk_min = 24576;  // blocks: keeps every chunk several waves deep
@@ -806,16 +831,23 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             const int64_t len = r.end - r.begin;
             const int nc = r.path == PATH_F32_REAL ? static_cast<int>(std::clamp<int64_t>(len / chunk_min, 1, 8)) : 1;
             for (int c = 0; c < nc; ++c)
-                chunks.push_back({r.path, r.begin + len * c / nc, r.begin + len * (c + 1) / nc, on_side ? ctx->side : st});
+                chunks.push_back({r.path, r.begin + len * c / nc, r.begin + len * (c + 1) / nc, on_side ? ctx->side : st,
+                                  r.grp});
         }
         ck(cudaEventRecord(ctx->ev[4], st), "event");
         ck(cudaStreamWaitEvent(ctx->side, ctx->ev[4], 0), "wait");
         ck(cudaStreamWaitEvent(ctx->aux, ctx->ev[4], 0), "wait");
+        std::vector<char> waited(static_cast<size_t>(2 * ngroups), 0);  // [group][main/side] upload waits
         // per chunk: events [3i] after K1, [3i+1] before the fp32 iteration, [3i+2] done
         for (size_t ci = 0; ci < chunks.size(); ++ci) {
             const Chunk& ch = chunks[ci];
             const int64_t cn = ch.b1 - ch.b0;
             const std::string tag = std::to_string(ci);
+            if (gio) {
+                char& wt = waited[static_cast<size_t>(2 * ch.grp + (ch.s == st ? 0 : 1))];
+                if (!wt) ck(cudaStreamWaitEvent(ch.s, gio->h2d_done[static_cast<size_t>(ch.grp)], 0), "wait");
+                wt = 1;
+            }
             ck(cudaEventRecord(ctx->event(3 * ci + 0), ch.s), "event");
             if (head > 0) {
                 k1_packed(d_sorted + ch.b0, cn, hi_path(ch.path), seg64, 1,
@@ -904,7 +936,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
                 }
             }
             out.reruns += static_cast<int64_t>(rr.size());
-            if (rr.empty()) continue;
+            if (!rr.empty()) {
             // re-run buffers are sized for the largest chunk and reused in stream order
             const int64_t m = static_cast<int64_t>(rr.size());
             const std::string tag = "r" + std::to_string(ci);
@@ -930,6 +962,16 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             const int hp = hi_path(ch.path);
             k1_packed(d_rdesc, m, hp, seg64, 1, d_Rr, d_re0, d_rimax, 0, 0, ctx->aux);
             k2_f64(a, hp, 0, m, rdesc, tag, ctx->aux);
+            }
+            // a frame group is complete once its last chunk and its re-runs are done
+            const bool last_of_group = ci + 1 == chunks.size() || chunks[ci + 1].grp != ch.grp;
+            if (gio && last_of_group) {
+                ck(cudaEventRecord(ctx->ev[5], ctx->aux), "event");
+                ck(cudaStreamWaitEvent(ctx->io, ctx->ev[5], 0), "wait");
+                for (size_t cj = 0; cj <= ci; ++cj)
+                    if (chunks[cj].grp == ch.grp) ck(cudaStreamWaitEvent(ctx->io, ctx->event(3 * cj + 2), 0), "wait");
+                gio->on_done(ch.grp, ctx->io);
+            }
         }
         hp_.mark("re-runs enqueued");
         ck(cudaEventRecord(ctx->ev[5], ctx->side), "event");
@@ -1067,6 +1109,7 @@ int fofse_create(int32_t device, fofse_ctx** out) {
         ck(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking), "cudaStreamCreate");
         ck(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking), "cudaStreamCreate");
         ck(cudaStreamCreateWithFlags(&ctx->cpy, cudaStreamNonBlocking), "cudaStreamCreate");
+        ck(cudaStreamCreateWithFlags(&ctx->io, cudaStreamNonBlocking), "cudaStreamCreate");
         ctx->own_stream = true;
         *out = ctx.release();
     });
@@ -1081,7 +1124,7 @@ void fofse_destroy(fofse_ctx* ctx) {
         if (e) cudaEventDestroy(e);
     for (auto e : ctx->evpool) cudaEventDestroy(e);
     if (ctx->pin) cudaFreeHost(ctx->pin);
-    for (cudaStream_t x : {ctx->side, ctx->aux, ctx->cpy})
+    for (cudaStream_t x : {ctx->side, ctx->aux, ctx->cpy, ctx->io})
         if (x) {
             cudaStreamSynchronize(x);
             cudaStreamDestroy(x);
@@ -1326,27 +1369,65 @@ int fofse_conceal_frames_u8(fofse_ctx* ctx, const uint8_t* frames, int32_t n_fra
             throw std::invalid_argument("conceal_frames: bad argument");
         if (width < 1 || height < 1) throw std::invalid_argument("grid dimensions must be >= 1");
         ctx->activate();
-        // the frame upload (asynchronous from pinned memory) overlaps the host-side
-        // validation + window-mask classification of make_plan
-        const size_t bytes = static_cast<size_t>(n_frames) * width * height;
+        // Frames are processed as G groups: group uploads are queued up front on
+        // the io stream (overlapping the host-side validation + classification of
+        // make_plan), each group starts iterating once its frames have landed, and
+        // a group's download is queued as soon as its iteration and guard re-runs
+        // are done — transfers overlap the iteration of the other groups.
+        const size_t fs = static_cast<size_t>(width) * height;
+        const size_t bytes = static_cast<size_t>(n_frames) * fs;
+        const int G = (params && params->precision == FOFSE_PREC_FP32)
+                          ? static_cast<int>(std::clamp<int32_t>(n_frames / 16, 1, 8)) : 1;
+        auto f0 = [&](int gq) { return static_cast<size_t>((static_cast<int64_t>(gq) * n_frames + G - 1) / G); };
         uint8_t* d_fr = ctx->buf("frames_u8").as<uint8_t>(bytes);
-        ck(cudaMemcpyAsync(d_fr, frames, bytes, cudaMemcpyHostToDevice, ctx->stream), "H2D frames");
+        std::vector<cudaEvent_t> h2d(static_cast<size_t>(G), nullptr);
+        struct EvHold {
+            std::vector<cudaEvent_t>& v;
+            ~EvHold() {
+                for (auto e : v)
+                    if (e) cudaEventDestroy(e);
+            }
+        } ev_hold{h2d};
+        for (int gq = 0; gq < G; ++gq) {
+            ck(cudaEventCreateWithFlags(&h2d[static_cast<size_t>(gq)], cudaEventDisableTiming), "cudaEventCreate");
+            const size_t a0 = f0(gq) * fs, a1 = f0(gq + 1) * fs;
+            if (a1 > a0)
+                ck(cudaMemcpyAsync(d_fr + a0, frames + a0, a1 - a0, cudaMemcpyHostToDevice, ctx->io), "H2D frames");
+            ck(cudaEventRecord(h2d[static_cast<size_t>(gq)], ctx->io), "event");
+        }
+        const HostProf hp_;
         std::unique_ptr<fofse_plan> hold;
         try {
             hold = make_plan(ctx, n_frames, width, height, blocks, offs, bh, bw, params);
         } catch (...) {
-            cudaStreamSynchronize(ctx->stream);  // the caller's buffer is being read
+            cudaStreamSynchronize(ctx->io);  // the caller's buffer is being read
             throw;
         }
+        hp_.mark("conceal_frames: plan (validate + classify)");
         fofse_plan* plan = hold.get();
+        plan->job.groups = G;
+        plan->job.nframes = n_frames;
         const int64_t n = static_cast<int64_t>(plan->job.blocks.size());
         double* d_sq = ctx->buf("sq").as<double>(static_cast<size_t>(std::max<int64_t>(n, 1)));
         const int64_t l0 = ctx->launches;
-        RunOut ro = plan_run(plan, d_fr, d_sq);
+        GroupIO gio;
+        gio.h2d_done = h2d;
+        std::vector<char> down(static_cast<size_t>(G), 0);
+        gio.on_done = [&](int gq, cudaStream_t s) {
+            const size_t a0 = f0(gq) * fs, a1 = f0(gq + 1) * fs;
+            if (a1 > a0) ck(cudaMemcpyAsync(restored + a0, d_fr + a0, a1 - a0, cudaMemcpyDeviceToHost, s), "D2H frames");
+            down[static_cast<size_t>(gq)] = 1;
+        };
+        RunOut ro;
+        fofse::Frames fr{d_fr, d_fr, fofse::SRC_U8, width, height, static_cast<int64_t>(fs)};
+        if (n > 0)
+            ro = run_job(ctx, plan->job, plan->cfg, fr, fofse::SYN_IMAGE, d_sq, nullptr, nullptr, nullptr, nullptr, &gio);
+        for (int gq = 0; gq < G; ++gq)  // groups without lost blocks come back unchanged
+            if (!down[static_cast<size_t>(gq)]) gio.on_done(gq, ctx->io);
         std::vector<double> sq(static_cast<size_t>(n));
         if (n) ck(cudaMemcpyAsync(sq.data(), d_sq, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream), "D2H sq");
-        ck(cudaMemcpyAsync(restored, d_fr, bytes, cudaMemcpyDeviceToHost, ctx->stream), "D2H frames");
         ck(cudaStreamSynchronize(ctx->stream), "sync");
+        ck(cudaStreamSynchronize(ctx->io), "sync");
         double tot = 0.0;
         for (double v : sq) tot += v;
         if (block_sq && n) std::memcpy(block_sq, sq.data(), sizeof(double) * n);
