@@ -532,6 +532,9 @@ __global__ void __launch_bounds__(256, 2) k2v2h_kernel(K2Args a) {
         int flagged = 0;
         int* rec_u = a.rec_u_g + (size_t)b * rstride;
         double2* rec_c = a.rec_c_g + (size_t)b * rstride;
+        int bu = 0;  // record batch (warp 0): selection nu-1 in lane (nu-1) & 31
+        float bcx = 0.f, bcy = 0.f;
+        const int nstart = nu;  // earlier records belong to the fp64 head
 
         KAcc A[ACC + 1];
 #pragma unroll
@@ -550,20 +553,26 @@ __global__ void __launch_bounds__(256, 2) k2v2h_kernel(K2Args a) {
             }
             // ---- per-warp argmax (+ runner-up), published with the winner pair ----
             const unsigned Mw = __reduce_max_sync(0xffffffffu, fbits(bm1));
-            const int wl = __ffs(__ballot_sync(0xffffffffu, fbits(bm1) == Mw)) - 1;
-            const unsigned Sw = __reduce_max_sync(0xffffffffu, fbits(lane == wl ? bm2 : bm1));
+            const bool top = fbits(bm1) == Mw;
+            const unsigned tb = __ballot_sync(0xffffffffu, top);
+            // runner-up: every lane holding the maximum contributes its own
+            // runner-up; two such lanes (an exact key tie) make it the maximum
+            const unsigned Sr = __reduce_max_sync(0xffffffffu, fbits(top ? bm2 : bm1));
+            const unsigned Sw = (tb & (tb - 1)) ? Mw : Sr;
+            const int wl = __ffs(tb) - 1;
             if (lane == wl) {
                 const int pw = 63 - static_cast<int>(Mw & 63u);
                 float xra[1] = {xr}, xia[1] = {xi};
                 slots[par * 2 + w] = HSlot{Mw, __uint_as_float(Sw), gb, 0, pick_pair<NP, 1>(pw, rp, ip, xra, xia)};
             }
             named_bar_sync(bar, NT);
-            const HSlot s0 = slots[par * 2], s1 = slots[par * 2 + 1];
-            const bool w1 = s1.key > s0.key;  // keys are unique within a warp; ties across warps -> warp 0 (lower index)
-            const HSlot& sw = w1 ? s1 : s0;
-            const unsigned M = sw.key;
+            const uint2 k0 = *reinterpret_cast<const uint2*>(&slots[par * 2]);
+            const uint2 k1v = *reinterpret_cast<const uint2*>(&slots[par * 2 + 1]);
+            const bool w1 = k1v.x > k0.x;  // ties across warps -> the guard (S == M) flags them
+            const HSlot& sw = slots[par * 2 + (w1 ? 1 : 0)];
+            const unsigned M = w1 ? k1v.x : k0.x;
             const float Mf = __uint_as_float(M);
-            const float Sf = fmaxf(sw.second, __uint_as_float(w1 ? s0.key : s1.key));
+            const float Sf = fmaxf(__uint_as_float(w1 ? k1v.y : k0.y), __uint_as_float(w1 ? k0.x : k1v.x));
             const int pw = 63 - static_cast<int>(M & 63u);
             float2 pre;
             int jw;
@@ -610,9 +619,23 @@ __global__ void __launch_bounds__(256, 2) k2v2h_kernel(K2Args a) {
             const double e = energy + (double)delta;
             energy = 0.0 < e ? e : 0.0;
             nu += 1;
-            if (tid == 0)
-                v2_record(a, b, nu, ntrace, rstride, tstride, rec_u, rec_c, u1, u2, self,
-                          (pr * P.x - pi * P.y) * iw, (pr * P.y + pi * P.x) * iw, c_re, c_im, energy, Mf, Sf);
+            // record nu-1 lives in lane (nu-1) & 31 of warp 0 until the batch is flushed
+            if (w == 0) {
+                if (lane == ((nu - 1) & 31)) {
+                    bu = (u1 << 16) | u2;
+                    bcx = self ? c_re : 2.f * c_re;
+                    bcy = self ? 0.f : 2.f * c_im;
+                }
+                if (((nu & 31) == 0) && nu - 32 + lane >= nstart && nu - 32 + lane < rstride) {
+                    rec_u[nu - 32 + lane] = bu;
+                    rec_c[nu - 32 + lane] = make_double2(bcx, bcy);
+                }
+            }
+            if (a.trace || a.gap_trace) {  // diagnostics only
+                if (tid == 0)
+                    v2_record(a, b, nu, ntrace, 0, tstride, nullptr, nullptr, u1, u2, self,
+                              (pr * P.x - pi * P.y) * iw, (pr * P.y + pi * P.x) * iw, c_re, c_im, energy, Mf, Sf);
+            }
             ntrace += 1;
 
             // ---- residual update of this warp's segment (+ fused next scan) ----
@@ -666,6 +689,13 @@ __global__ void __launch_bounds__(256, 2) k2v2h_kernel(K2Args a) {
             }
         }
 
+        if (w == 0) {  // flush the partial record batch: selections (nu & ~31) .. nu-1
+            const int q = (nu & ~31) + lane;
+            if (lane < (nu & 31) && q >= nstart && q < rstride) {
+                rec_u[q] = bu;
+                rec_c[q] = make_double2(bcx, bcy);
+            }
+        }
         if (a.rout) {
             const size_t rs = a.rin_stride > 0 ? (size_t)a.rin_stride : (size_t)(NP + 1) * NT * 4;
             float4* R = reinterpret_cast<float4*>(static_cast<float*>(a.rout) + (size_t)pos * rs);
