@@ -865,7 +865,17 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
                 a.conv_out = d_cvh;
                 a.trace_count = nullptr;
                 a.gap_trace = nullptr;
+                // K2d hands its state straight to the fp32 real path (no convert pass)
+                const bool direct = hi_path(ch.path) == PATH_F64_REAL && soa_of(ch.path);
+                if (direct) {
+                    a.rout = d_R32;
+                    a.rout_f32 = 1;
+                    a.rout_seg = seg32;
+                    a.rout_spt = spt_of(ch.path);
+                    a.rout_stride = s32;
+                }
                 k2_f64(a, hi_path(ch.path), ch.b0, ch.b1, sorted, "h" + tag, ch.s);
+                if (!direct) {
                 CvtArgs c{};
                 c.T = T;
                 c.Lh = g.Lh;
@@ -880,6 +890,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
                 c.out_stride = s32;
                 ck(cvt_launch(c, ch.s), "convert head state");
                 ++ctx->launches;
+                }
             } else {
                 k1_packed(d_sorted + ch.b0, cn, ch.path, seg32, spt_of(ch.path),
                           d_R32 + static_cast<size_t>(ch.b0) * sizeof(float) * s32, d_e0 + ch.b0, d_imax + ch.b0,
@@ -1051,17 +1062,23 @@ Job make_image_job(const Cfg& cfg, int W, int H, int bh, int bw, const fofse_rec
     Job job;
     job.geo = Geometry{cfg.T, bh, bw, cfg.S, bh + 2 * cfg.S, bw + 2 * cfg.S};
     std::vector<CellGrid> grids(static_cast<size_t>(nframes));
-    // check_pattern_fits (pipeline.cpp:123-132) per frame
-    for (int f = 0; f < nframes; ++f) {
-        const int64_t cnt = offs[f + 1] - offs[f];
-        if (cnt < 0) throw std::invalid_argument("frame_offsets must be non-decreasing");
+    // check_pattern_fits (pipeline.cpp:123-132) per frame, frames in parallel;
+    // the first failing frame (in frame order) is reported
+    for (int f = 0; f < nframes; ++f)
+        if (offs[f + 1] - offs[f] < 0) throw std::invalid_argument("frame_offsets must be non-decreasing");
+    std::vector<std::string> errs(static_cast<size_t>(nframes));
+    parallel_for(nframes, [&](int64_t f) {
         try {
-            validate_pattern(blocks + offs[f], cnt, bh, bw, W, H, grids[static_cast<size_t>(f)]);
+            validate_pattern(blocks + offs[f], offs[f + 1] - offs[f], bh, bw, W, H, grids[static_cast<size_t>(f)]);
         } catch (const std::invalid_argument& e) {
-            if (nframes == 1) throw;
-            throw std::invalid_argument("frame " + std::to_string(f) + ": " + e.what());
+            errs[static_cast<size_t>(f)] = e.what();
         }
-    }
+    });
+    for (int f = 0; f < nframes; ++f)
+        if (!errs[static_cast<size_t>(f)].empty()) {
+            if (nframes == 1) throw std::invalid_argument(errs[0]);
+            throw std::invalid_argument("frame " + std::to_string(f) + ": " + errs[static_cast<size_t>(f)]);
+        }
     if (job.geo.Lh > cfg.T || job.geo.Lw > cfg.T)
         throw std::invalid_argument("conceal: block + support frame exceeds the transform grid");
     check_gpu_support(cfg);

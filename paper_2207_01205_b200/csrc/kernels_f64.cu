@@ -260,10 +260,31 @@ __global__ void __launch_bounds__(256, 2) k2d_kernel(K2Args a) {
         }
 
         if (a.rout && active) {
-            double2* R = static_cast<double2*>(a.rout) + (size_t)pos * L.SLOTS;
+            if (a.rout_f32) {
+                // hand-off to the fp32 real path: SoA bin pairs (re_a, re_b, im_a, im_b)
+                const BinLayout Lo = BinLayout::make(T, a.rout_seg, a.rout_spt);
+                float* o = static_cast<float*>(a.rout) + (size_t)pos * a.rout_stride;
 #pragma unroll
-            for (int j = 0; j < SEG; ++j) R[j * NT + ltid] = make_double2(re[j], im[j]);
-            if (ex) R[SEG * NT + ltid] = make_double2(re[SEG], im[SEG]);
+                for (int q = 0; q < PPS; ++q) {
+                    int i, t;
+                    bin_slot(Lo, k1, c0 + 2 * q, &i, &t);
+                    const int s = i / (Lo.SEG + 1), j = i - s * (Lo.SEG + 1);
+                    reinterpret_cast<float4*>(o)[(size_t)(s * (Lo.SEG / 2) + j / 2) * Lo.NT + t] =
+                        make_float4((float)re[2 * q], (float)re[2 * q + 1], (float)im[2 * q], (float)im[2 * q + 1]);
+                }
+                if (ex) {
+                    int i, t;
+                    bin_slot(Lo, k1, T / 2, &i, &t);
+                    const int s = i / (Lo.SEG + 1);
+                    reinterpret_cast<float4*>(o)[(size_t)(Lo.SPT * Lo.SEG / 2 + s) * Lo.NT + t] =
+                        make_float4((float)re[SEG], 0.f, (float)im[SEG], 0.f);
+                }
+            } else {
+                double2* R = static_cast<double2*>(a.rout) + (size_t)pos * L.SLOTS;
+#pragma unroll
+                for (int j = 0; j < SEG; ++j) R[j * NT + ltid] = make_double2(re[j], im[j]);
+                if (ex) R[SEG * NT + ltid] = make_double2(re[SEG], im[SEG]);
+            }
         }
         // thread 0's records visible to the group before the synthesis
         if constexpr (NW == 1)
