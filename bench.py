@@ -148,6 +148,25 @@ def cpu_reference_rate(wl, seed, budget_s, threads):
                       f"{threads} threads, {secs:.1f} s"}
 
 
+def cpu_reference_1thread(wl, seed, nblocks=160):
+    """One host thread, the first `nblocks` lost blocks of one frame (SURVEY §8d
+    asks for a 1-thread figure beside the all-core baseline)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle  # checker / CPU baseline only
+
+    impl = oracle.Reference() if oracle.have_reference() else oracle.Oracle()
+    cfg = wl.config("fp64")
+    img, pat = wl.frame(seed + 100000, 0)
+    blocks = [tuple(b) for b in pat.blocks[:nblocks]]
+    t0 = time.perf_counter()
+    impl.conceal(img.astype(np.float64), blocks, wl.block, wl.block, gamma=cfg.gamma,
+                 iterations=cfg.iterations, t=cfg.transform_size, rho_hat=cfg.rho_hat,
+                 support=cfg.support_width, threads=1)
+    secs = time.perf_counter() - t0
+    return {"value": len(blocks) / secs, "unit": UNIT, "cores": 1,
+            "sample": f"{len(blocks)} blocks of one {wl.name} frame, 1 thread, {secs:.1f} s"}
+
+
 def run_reference_arm(args, wl):
     world, rank, _ = dist_env()
     if rank != 0:
@@ -251,7 +270,7 @@ def main():
         torch.cuda.synchronize()
 
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    k2_ms, init_ms, launches, reruns = [], [], 0, 0
+    k2_ms, init_ms, launches, reruns, real_ms, real_blocks, head = [], [], 0, 0, [], 0, 0
     barrier()
     with ClockSampler(local) as clk:
         ev0.record(stream)
@@ -259,6 +278,8 @@ def main():
             r = execute()
             k2_ms.append(r.iterate_ms)
             init_ms.append(r.init_ms)
+            real_ms.append(r.real_iterate_ms)
+            real_blocks, head = r.real_blocks, r.fp64_head
             launches += r.kernel_launches
             reruns += r.guard_reruns
         ev1.record(stream)
@@ -290,7 +311,8 @@ def main():
     e2e_ms = ev0.elapsed_time(ev1) / args.steps
 
     # ---- max over ranks ----
-    t = torch.tensor([ms, e2e_ms, statistics.mean(k2_ms)], dtype=torch.float64, device=dev)
+    t = torch.tensor([ms, e2e_ms, statistics.mean(k2_ms), statistics.mean(real_ms)], dtype=torch.float64,
+                     device=dev)
     if world > 1:
         import torch.distributed as dist
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -299,14 +321,21 @@ def main():
         total_blocks = int(nb.item())
     else:
         total_blocks = n_blocks
-    ms, e2e_ms, k2_avg = (float(x) for x in t.tolist())
+    ms, e2e_ms, k2_avg, real_avg = (float(x) for x in t.tolist())
 
     if rank == 0:
-        # roofline of the dominant kernel K2 (SMEM bytes = 4 s H per block-iteration)
+        # roofline of the dominant kernel, the real-path iteration K2v2 (SMEM
+        # bytes = 4 s H per block-iteration): its algorithmic bytes over the summed
+        # durations of its launches (CUDA events on the launching stream, in the library)
         H = wl.transform_size ** 2 // 2 + 2
         s = 4 if prec == "fp32" else 8
-        alg_bytes = 4 * s * H * wl.iterations * n_blocks  # per K2 pass over this rank's blocks
-        achieved = alg_bytes / (k2_avg * 1e-3) / 1e9
+        its = wl.iterations - (head if prec == "fp32" else 0)
+        if prec == "fp32" and real_avg > 0:
+            alg_bytes = 4 * s * H * its * real_blocks
+            achieved = alg_bytes / (real_avg * 1e-3) / 1e9
+        else:
+            alg_bytes = 4 * s * H * wl.iterations * n_blocks
+            achieved = alg_bytes / (k2_avg * 1e-3) / 1e9
         peaks = load_peaks()
         try:  # live, same box: LDS.64 bandwidth (the W gathers of K2 are LDS.64 / LDS.32)
             peaks["smem_gbs"] = capi.microbench(local, 0)
@@ -314,15 +343,19 @@ def main():
         except Exception:
             pass
         peak = peaks.get("smem_gbs")
-        roof = {"bound": "smem", "kernel": "fofse::k2_kernel (iterate + fused synthesis)",
+        kname = ("fofse::k2v2r_kernel<64> (fp32 rotated-frame iterate + fused synthesis)" if prec == "fp32"
+                 else "fofse::k2d_kernel<64> / k2_kernel (fp64 iterate + fused synthesis)")
+        roof = {"bound": "smem", "kernel": kname,
                 "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if peak else None, "traffic": peaks.get("k2_dram_bytes"),
-                "per_unit": f"4*s*H = {4 * s * H} B per block-iteration (s={s}, H={H})",
+                "per_unit": f"4*s*H = {4 * s * H} B per block-iteration (s={s}, H={H}); "
+                            f"{its} fp32 iterations x {real_blocks if prec == 'fp32' else n_blocks} blocks per step",
                 "peak_source": peaks.get("smem_source")}
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             try:
                 cpu = cpu_reference_rate(wl, args.seed, args.cpu_seconds, os.cpu_count() or 1)
+                cpu["one_thread"] = cpu_reference_1thread(wl, args.seed)
             except Exception as e:  # baseline is reported, never required
                 cpu = {"error": str(e)}
         line = {
@@ -345,7 +378,8 @@ def main():
             "gpu_launches": launches,
             "detail": {"k2_ms": k2_avg, "init_ms": statistics.mean(init_ms), "guard_reruns_per_step": reruns / args.steps,
                        "psnr_db": first.psnr_db if first else None, "e2e_psnr_db": e2e_psnr,
-                       "classes": first.classes if first else None, "input_gen_s": gen_s},
+                       "classes": first.classes if first else None, "input_gen_s": gen_s,
+                       "real_blocks": real_blocks, "real_iterate_ms": real_avg, "fp64_head": head},
         }
         print(json.dumps(line), flush=True)
     L.fofse_plan_destroy(plan)

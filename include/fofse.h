@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define FOFSE_ABI_VERSION 1
+#define FOFSE_ABI_VERSION 2
 
 enum {
     FOFSE_OK = 0,
@@ -94,12 +94,14 @@ typedef struct {
     int64_t classes;           /* distinct window masks (weight spectra) */
     int64_t guard_reruns;      /* FP32 blocks re-run in FP64 */
     int64_t converged_blocks;  /* early-stopped blocks (engine_spectral.cpp:60-65) */
-    double init_ms;            /* K0 class spectra + K1 residual spectra */
-    double iterate_ms;         /* K2 iterate + fused synthesis (incl. guard re-runs) */
+    double init_ms;            /* K0 class spectra + K1 residual spectra (+ FP32 mode: FP64 head) */
+    double iterate_ms;         /* total_ms - init_ms: iteration, synthesis, guard re-runs */
     double total_ms;           /* device time of the whole call */
     int64_t kernel_launches;
-    double rerun_ms;           /* FP32 guard re-runs (included in iterate_ms) */
+    double rerun_ms;           /* FP32 guard re-runs not overlapped by other work */
     int64_t fp64_head;         /* FP32 mode: selections run in FP64 per block */
+    int64_t real_blocks;       /* blocks on the rotated-frame real path (point-symmetric masks) */
+    double real_iterate_ms;    /* FP32 mode: summed durations of the real-path iteration launches */
 } fofse_report;
 
 typedef struct fofse_ctx fofse_ctx;

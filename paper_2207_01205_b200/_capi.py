@@ -58,7 +58,8 @@ class Report(C.Structure):
         ("mean_seconds_per_block", C.c_double), ("blocks", C.c_int64), ("classes", C.c_int64),
         ("guard_reruns", C.c_int64), ("converged_blocks", C.c_int64), ("init_ms", C.c_double),
         ("iterate_ms", C.c_double), ("total_ms", C.c_double), ("kernel_launches", C.c_int64),
-        ("rerun_ms", C.c_double), ("fp64_head", C.c_int64),
+        ("rerun_ms", C.c_double), ("fp64_head", C.c_int64), ("real_blocks", C.c_int64),
+        ("real_iterate_ms", C.c_double),
     ]
 
     def as_dict(self):

@@ -502,6 +502,8 @@ std::vector<Tile> make_tiles(int64_t begin, int64_t end, const std::vector<Block
 struct RunOut {
     double init_ms = 0, iter_ms = 0, total_ms = 0, rerun_ms = 0;
     double chunk_pre_ms = 0, chunk_iter_ms = 0, rerun_tail_ms = 0;  // fp32 pipeline
+    double real_iter_ms = 0;                                         // fp32 real-path launches
+    int64_t real_blocks = 0;
     int64_t reruns = 0, converged = 0, head = 0;
 };
 
@@ -678,6 +680,8 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         p0 = p1;
     }
     const int ngroups = job.groups;
+    for (const Range& r : ranges)
+        if (r.path == PATH_F32_REAL || r.path == PATH_F64_REAL) out.real_blocks += r.end - r.begin;
     if (gio && !fp32)
         for (int gq = 0; gq < ngroups; ++gq)
             ck(cudaStreamWaitEvent(st, gio->h2d_done[static_cast<size_t>(gq)], 0), "wait");
@@ -1004,6 +1008,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             out.chunk_pre_ms += ms;
             ck(cudaEventElapsedTime(&ms, ctx->event(3 * ci + 1), ctx->event(3 * ci + 2)), "elapsed");
             out.chunk_iter_ms += ms;
+            if (chunks[ci].path == PATH_F32_REAL) out.real_iter_ms += ms;
         }
     }
     ck(cudaEventRecord(ctx->ev[3], st), "event");
@@ -1044,6 +1049,8 @@ void fill_report(fofse_report* rep, const RunOut& ro, int64_t n, int64_t ncls, d
     rep->total_ms = ro.total_ms;
     rep->rerun_ms = ro.rerun_ms;
     rep->fp64_head = ro.head;
+    rep->real_blocks = ro.real_blocks;
+    rep->real_iterate_ms = ro.real_iter_ms;
     rep->mean_seconds_per_block = n ? ro.total_ms * 1e-3 / static_cast<double>(n) : 0.0;
     rep->kernel_launches = launches;
     // pipeline.cpp:252-260 + grid.cpp:117-120

@@ -22,7 +22,7 @@ def test_library_exports_every_declared_symbol(lib):
     assert declared == set(capi.EXPORTS)
     for name in declared:
         assert hasattr(lib, name), name
-    assert lib.fofse_abi_version() == 1
+    assert lib.fofse_abi_version() == 2
 
 
 def test_params_default_match_conceal_config(lib):
@@ -36,7 +36,7 @@ def test_params_default_match_conceal_config(lib):
 def test_struct_layouts_match_header(lib):
     assert C.sizeof(capi.Params) == 64
     assert capi.RECORD_DTYPE.itemsize == 72
-    assert C.sizeof(capi.Report) == 104
+    assert C.sizeof(capi.Report) == 120
 
 
 def test_generators_deterministic(lib):
