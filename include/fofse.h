@@ -204,6 +204,13 @@ int fofse_spectral_iterate(fofse_ctx* ctx, int32_t t, int64_t n, int32_t win_h, 
                            const double* initial_max, int32_t* nu, int32_t* converged,
                            double gamma, int32_t iterations, int32_t precision,
                            fofse_record* traces, int32_t* trace_counts);
+/* fse::spectral::fast_iterate_full_od (engine_spectral.hpp:47-48, .cpp:191-193):
+ * OFSE, gamma_eff = min(|p w0^2 / d|, 1) with d = sum_l R_w[l] W[u-l]; fp64. */
+int fofse_spectral_iterate_full_od(fofse_ctx* ctx, int32_t t, int64_t n, int32_t win_h, int32_t win_w,
+                                   double* rw, const double* wspec, double* g, const double* w0,
+                                   double* weighted_energy, const double* initial_energy,
+                                   const double* initial_max, int32_t* nu, int32_t* converged,
+                                   int32_t iterations, fofse_record* traces, int32_t* trace_counts);
 /* synthesize: models n*h*w = Re(IDFT(g))/T^2 cropped; max_imag n values.
  * Fails with FOFSE_ERUNTIME like synthesize_model if any |Im| > 1e-9. */
 int fofse_spectral_synthesize(fofse_ctx* ctx, int32_t t, int64_t n, const double* g, int32_t h,

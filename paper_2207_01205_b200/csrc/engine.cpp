@@ -226,13 +226,14 @@ void validate_config(const Cfg& c) {
 }
 
 void check_gpu_support(const Cfg& c) {
-    if (c.algorithm == FOFSE_ALGO_OFSE)
-        throw Unsupported("ofse (full-OD compensation) is not part of this build's GPU path");
     if (!(c.T == 8 || c.T == 16 || c.T == 32 || c.T == 64 || c.T == 128))
         throw Unsupported("transform_size must be a power of two in [8, 128] on the GPU path");
 }
 
 double effective_gamma(const Cfg& c) { return c.algorithm == FOFSE_ALGO_FSE ? 1.0 : c.gamma; }
+// OFSE (full-OD compensation, engine_spectral.cpp:79-97) is an fp64 algorithm:
+// an fp32 request runs the fp64 kernels.
+bool full_od(const Cfg& c) { return c.algorithm == FOFSE_ALGO_OFSE; }
 
 // Per-frame occupancy grid: cell (row/bh, col/bw) -> index of the block whose
 // top-left corner lies in it. Non-overlapping equal-size blocks never share a
@@ -579,8 +580,8 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             if (lab[i] == FOFSE_SUPPORT) wcls[static_cast<size_t>(c) * L + i] = job.wfull[i];
         sym[static_cast<size_t>(c)] = point_symmetric(lab, g.Lh, g.Lw) ? 1 : 0;
     }
-    const bool fp32 = cfg.precision == FOFSE_PREC_FP32;
-    const int head = resolve_head(cfg);
+    const bool fp32 = cfg.precision == FOFSE_PREC_FP32 && !full_od(cfg);
+    const int head = fp32 ? resolve_head(cfg) : 0;
     out.head = head;
     const bool v2 = fp32 && v2_supported(T);
     const bool use_d = d_supported(T) && !f64_strict_forced();  // K2d for symmetric masks
@@ -729,6 +730,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         a.Lw = g.Lw;
         a.iterations = I;
         a.gamma = effective_gamma(cfg);
+        a.full_od = full_od(cfg) ? 1 : 0;
         a.w0 = d_w0;
         a.synth = synth;
         a.fr = fr;
@@ -1578,13 +1580,16 @@ static int spectral_iterate_impl(fofse_ctx* ctx, int32_t t, int64_t n, int32_t w
                            double* rw, const double* wspec, double* g, const double* w0,
                            double* energy, const double* e_init, const double* imax, int32_t* nu,
                            int32_t* conv, double gamma, int32_t iterations, int32_t precision,
-                           fofse_record* traces, int32_t* trace_counts, float* gap_trace) {
+                           fofse_record* traces, int32_t* trace_counts, float* gap_trace,
+                           int fod = 0) {
     return guarded([&] {
         using namespace fofse;
         if (!ctx || (n && (!rw || !wspec || !g || !w0 || !energy || !e_init || !imax || !nu || !conv)))
             throw std::invalid_argument("spectral_iterate: NULL argument");
         if (iterations < 0) throw std::invalid_argument("fast_iterate: iterations must be >= 0");
-        if (!(gamma > 0.0) || gamma > 1.0) throw std::invalid_argument("fast_iterate: gamma must lie in (0, 1]");
+        if (!fod && (!(gamma > 0.0) || gamma > 1.0))
+            throw std::invalid_argument("fast_iterate: gamma must lie in (0, 1]");
+        if (fod) precision = FOFSE_PREC_FP64;  // OFSE: fp64 only
         Cfg c{};
         c.T = t;
         c.algorithm = FOFSE_ALGO_FOFSE;
@@ -1674,6 +1679,7 @@ static int spectral_iterate_impl(fofse_ctx* ctx, int32_t t, int64_t n, int32_t w
         const auto twi = twiddles(t, +1);
         double2* d_twi = upload(ctx, "twi", twi.data(), twi.size());
         K2Args a{};
+        a.full_od = fod;
         a.T = t;
         a.Lh = wh;
         a.Lw = ww;
@@ -1766,6 +1772,15 @@ int fofse_spectral_iterate(fofse_ctx* ctx, int32_t t, int64_t n, int32_t wh, int
                            fofse_record* traces, int32_t* trace_counts) {
     return spectral_iterate_impl(ctx, t, n, wh, ww, rw, wspec, g, w0, energy, e_init, imax, nu, conv,
                                  gamma, iterations, precision, traces, trace_counts, nullptr);
+}
+
+int fofse_spectral_iterate_full_od(fofse_ctx* ctx, int32_t t, int64_t n, int32_t wh, int32_t ww,
+                                   double* rw, const double* wspec, double* g, const double* w0,
+                                   double* energy, const double* e_init, const double* imax, int32_t* nu,
+                                   int32_t* conv, int32_t iterations, fofse_record* traces,
+                                   int32_t* trace_counts) {
+    return spectral_iterate_impl(ctx, t, n, wh, ww, rw, wspec, g, w0, energy, e_init, imax, nu, conv, 1.0,
+                                 iterations, FOFSE_PREC_FP64, traces, trace_counts, nullptr, 1);
 }
 
 int fofse_diag_spectral_iterate(fofse_ctx* ctx, int32_t t, int64_t n, int32_t wh, int32_t ww,

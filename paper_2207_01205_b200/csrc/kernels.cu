@@ -265,14 +265,16 @@ struct Slot {
 };
 struct Params {
     double c_re, c_im;  // update coefficient (c, or a in the rotated frame)
+    double pre_re, pre_im;  // R_w[u] (full-OD second phase)
     int u1, u2, self, stop;
-    int nrec, flagged, conv, pad;
+    int nrec, flagged, conv, need_d;  // need_d: OFSE reduction pending for u
 };
 template <int NW>
 struct GroupSmem {
     Slot slot[NW];
     Params prm;
     double red[NW];
+    double2 dpart[NW];  // OFSE: per-warp partial sums of d = sum_l R[l] W[u-l]
 };
 
 template <int T, int PATH>
@@ -461,6 +463,14 @@ __global__ void __launch_bounds__(K2Cfg<T, PATH>::THREADS) k2_kernel(K2Args a) {
                 else
                     named_bar_arrive(barA, GT);
             }
+            // OFSE (full-OD) runs the controller twice: phase 0 publishes u, every
+            // thread adds its bins to d = sum_l R[l] W[u-l], phase 1 finishes with
+            // gamma_eff = min(|p w0^2 / d|, 1) (engine_spectral.cpp:79-97).
+            double d_re = 0.0, d_im = 0.0;
+            bool stop_it = false;
+            Params p;
+            for (int phase = 0;; ++phase) {
+            const bool want_d = PATH == PATH_F64_STRICT && a.full_od && phase == 0;
             if (warp == 0) {
                 // ===== controller: find_peak result + scalar part of iterate =====
                 double M = -1.0, M2 = -1.0, pr = 0.0, pi = 0.0;
@@ -477,9 +487,9 @@ __global__ void __launch_bounds__(K2Cfg<T, PATH>::THREADS) k2_kernel(K2Args a) {
                         pi = s.pre_im;
                     }
                 }
-                Params p;
                 p.stop = 0;
                 p.self = 0;
+                p.need_d = 0;
                 p.u1 = p.u2 = 0;
                 p.c_re = p.c_im = 0.0;
                 const double mag = sqrt(M);
@@ -497,12 +507,32 @@ __global__ void __launch_bounds__(K2Cfg<T, PATH>::THREADS) k2_kernel(K2Args a) {
                     const int v1 = (T - u1) % T, v2 = (T - u2) % T;
                     const int self = (u1 == v1 && u2 == v2);
                     double c_re, c_im, p_re, p_im, upd_re, upd_im, delta;
+                    double geff = a.gamma;
+                    int degen = 0;
+                    if (want_d) {
+                        p.u1 = u1;
+                        p.u2 = u2;
+                        p.self = self;
+                        p.need_d = 1;
+                    } else {
                     if constexpr (PATH == PATH_F64_STRICT || PATH == PATH_F32_COMPLEX) {
                         // engine_spectral.cpp:70-78, 98: p = pre / w0, c = gamma p
                         p_re = __ddiv_rn(pr, w0);
                         p_im = __ddiv_rn(pi, w0);
-                        c_re = __dmul_rn(p_re, a.gamma);
-                        c_im = __dmul_rn(p_im, a.gamma);
+                        if (PATH == PATH_F64_STRICT && a.full_od) {
+                            // engine_spectral.cpp:87-95
+                            const double pw2 = hypot(p_re, p_im) * w0 * w0;
+                            const double dm = hypot(d_re, d_im);
+                            if (dm < 1e-12 * pw2) {
+                                geff = 1.0;
+                                degen = 1;
+                            } else {
+                                // |p w0^2 / d| = |p| w0^2 / |d|
+                                geff = fmin(pw2 / dm, 1.0);
+                            }
+                        }
+                        c_re = __dmul_rn(p_re, geff);
+                        c_im = __dmul_rn(p_im, geff);
                         if (self) c_im = 0.0;
                         // engine_spectral.cpp:100-110 energy bookkeeping
                         if (self) {
@@ -572,9 +602,9 @@ __global__ void __launch_bounds__(K2Cfg<T, PATH>::THREADS) k2_kernel(K2Args a) {
                             r.p_im = p_im;
                             r.c_re = c_re;
                             r.c_im = c_im;
-                            r.gamma_effective = a.gamma;
+                            r.gamma_effective = geff;
                             r.weighted_energy = energy;
-                            r.degenerate = 0;
+                            r.degenerate = degen;
                             r.pad1 = 0;
                             a.trace[(size_t)b * tstride + ntrace] = r;
                         }
@@ -599,6 +629,7 @@ __global__ void __launch_bounds__(K2Cfg<T, PATH>::THREADS) k2_kernel(K2Args a) {
                     }
                     nrec += 1;
                     ntrace += 1;
+                    }  // !want_d
                 }
                 p.nrec = nrec;
                 p.flagged = flagged;
@@ -613,12 +644,58 @@ __global__ void __launch_bounds__(K2Cfg<T, PATH>::THREADS) k2_kernel(K2Args a) {
                 else
                     named_bar_sync(barB, GT);
             }
-            const Params p = gs->prm;
+            p = gs->prm;
             if (p.stop) {
                 conv = p.conv;
                 flagged = p.flagged;
+                stop_it = true;
                 break;
             }
+            if (!p.need_d) break;
+            if constexpr (PATH == PATH_F64_STRICT) {
+                // partial d over the owned canonical bins: R[k] W[u-k] = R conj(W[k-u]);
+                // the partner -k adds conj(R[k]) W[u+k] unless k is self-conjugate
+                double pr_ = 0.0, pi_ = 0.0;
+                if (active) {
+                    const int rA = (k1 - p.u1) & (T - 1), rB = (k1 + p.u1) & (T - 1);
+                    const int cA = (c0 - p.u2) & (T - 1), cB = (c0 + p.u2) & (T - 1);
+                    const WT* wa = wimg + rA * SR + cA;
+                    const WT* wb = wimg + rB * SR + cB;
+#pragma unroll
+                    for (int j = 0; j < NB; ++j) {
+                        if (j == SEG && !ex) break;
+                        const double2 x = wa[j], y = wb[j];
+                        pr_ = fma(re[j], x.x, fma(im[j], x.y, pr_));
+                        pi_ = fma(im[j], x.x, fma(-re[j], x.y, pi_));
+                        const bool selfk = (j == SEG) || (j == 0 && c0 == 0 && (k1 == 0 || k1 == T / 2));
+                        if (!selfk) {
+                            pr_ = fma(re[j], y.x, fma(im[j], y.y, pr_));
+                            pi_ = fma(re[j], y.y, fma(-im[j], y.x, pi_));
+                        }
+                    }
+                }
+#pragma unroll
+                for (int o = 16; o; o >>= 1) {
+                    pr_ += __shfl_xor_sync(0xffffffffu, pr_, o);
+                    pi_ += __shfl_xor_sync(0xffffffffu, pi_, o);
+                }
+                if (lane == 0) gs->dpart[warp] = make_double2(pr_, pi_);
+                if constexpr (NW == 1)
+                    __syncwarp();
+                else
+                    named_bar_sync(barA, GT);
+                if (warp == 0) {
+                    d_re = 0.0;
+                    d_im = 0.0;
+#pragma unroll
+                    for (int w = 0; w < NW; ++w) {
+                        d_re += gs->dpart[w].x;
+                        d_im += gs->dpart[w].y;
+                    }
+                }
+            }
+            }  // phase
+            if (stop_it) break;
 
             // ---- residual update over owned bins (engine_spectral.cpp:112-125) ----
             const int u1 = p.u1, u2 = p.u2;

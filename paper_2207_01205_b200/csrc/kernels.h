@@ -126,6 +126,7 @@ struct K2Args {
     int32_t state_by_pos;       // energy_out / nu_out / conv_out indexed by position
     uint32_t kmask;             // K2v2 packed-key mantissa mask (0xffffffc0), a runtime value so
                                 // the key is one LOP3 (mask in a register, index immediate)
+    int32_t full_od;            // OFSE: full orthogonality-deficiency compensation (engine_spectral.cpp:79-97)
     int32_t rout_f32;           // K2d: write rout as the fp32 SoA pair layout of the K2v2 real
     int32_t rout_seg, rout_spt; //   path (segment / segments per lane), rout_stride floats per
     int64_t rout_stride;        //   block — the fp32 phase reads it directly (no convert pass)

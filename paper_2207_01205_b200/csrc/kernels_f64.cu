@@ -47,7 +47,8 @@ struct DCfg {
     static constexpr size_t WBYTES = ((IMG_BYTES + 15) / 16) * 16;
     static constexpr size_t OFF_P = WBYTES;                            // 2T double2
     static constexpr size_t OFF_TW = OFF_P + sizeof(double2) * 2 * T;  // T double2
-    static constexpr size_t GRP = ((2 * NW * 32 + 8 * NW + 15) / 16) * 16;  // slots[2][NW] + red[NW]
+    // per group: slots[2][NW] (32 B) + full-OD partials dred[2][NW] (16 B) + red[NW] (8 B)
+    static constexpr size_t GRP = ((2 * NW * 32 + 2 * NW * 16 + 8 * NW + 15) / 16) * 16;
     static constexpr size_t OFF_G = OFF_TW + sizeof(double2) * T;
     static constexpr size_t OFF_BAR = OFF_G + GRP * GROUPS;
     static constexpr size_t SMEM = OFF_BAR + 16;
@@ -88,7 +89,7 @@ __device__ __forceinline__ double2 dpick(int j, const double* re, const double* 
     return q;
 }
 
-template <int T>
+template <int T, bool FOD>
 __global__ void __launch_bounds__(256, 2) k2d_kernel(K2Args a) {
     using Cf = DCfg<T>;
     constexpr int SEG = Cf::SEG, NT = Cf::NT, GT = Cf::GT, NW = Cf::NW, PPS = Cf::PPS, SRV = Cf::SRV;
@@ -106,13 +107,17 @@ __global__ void __launch_bounds__(256, 2) k2d_kernel(K2Args a) {
     const bool active = ltid < NT;
     unsigned char* gsm = smem_raw + Cf::OFF_G + Cf::GRP * grp;
     DSlot* slots = reinterpret_cast<DSlot*>(gsm);  // [2][NW]
-    double* red = reinterpret_cast<double*>(gsm + 2 * NW * 32);
+    double2* dred = reinterpret_cast<double2*>(gsm + 2 * NW * 32);  // [2][NW]
+    double* red = reinterpret_cast<double*>(gsm + 2 * NW * 32 + 2 * NW * 16);
     const int bar = 1 + grp;
 
     const BinLayout L = BinLayout::make(T, SEG, 1);
     int k1 = 0, c0 = 0, ex = 0;
     if (active) L.segment(ltid, &k1, &c0, &ex);
     const int gbase = k1 * T + c0;
+    // self-conjugate canonical bins (0,0), (T/2,0) at slot 0 and the extra bins
+    // (0,T/2), (T/2,T/2) have no partner in the full spectrum (OFSE reduction)
+    const bool selfbin0 = active && c0 == 0 && (k1 == 0 || k1 == T / 2);
     const unsigned kbase = static_cast<unsigned>(DKEY_TOP - gbase);
     const double sgn_r = ((a.Lh - 1) & 1) ? -1.0 : 1.0;
     const double sgn_c = ((a.Lw - 1) & 1) ? -1.0 : 1.0;
@@ -186,7 +191,71 @@ __global__ void __launch_bounds__(256, 2) k2d_kernel(K2Args a) {
             const int u1 = G / T, u2 = G % T;
             const int self = ((T - u1) % T == u1) && ((T - u2) % T == u2);
             const double2 P = ptab[(u1 * (a.Lh - 1) + u2 * (a.Lw - 1)) & (2 * T - 1)];  // e^{-j phi(u)}
-            const double ar = pr * gw, ai = pi * gw;  // a = gamma R'[u] / w0
+            // gathers of this selection: V[k-u] (sign s1) and V[k+u] (sign s2) per owned bin
+            const int p2 = u2 & 1;
+            const double* vimg = vE + p2 * (T * SRV);  // odd copy holds V[c+1]
+            const int rA = (k1 - u1) & (T - 1), rB = (k1 + u1) & (T - 1);
+            const int cA = (c0 - u2) & (T - 1), cB = (c0 + u2) & (T - 1);
+            const double s1 = ((k1 < u1) ? sgn_r : 1.0) * ((c0 < u2) ? sgn_c : 1.0);
+            const double s2 = ((k1 + u1 >= T) ? sgn_r : 1.0) * ((c0 + u2 >= T) ? sgn_c : 1.0);
+            const double2* va = reinterpret_cast<const double2*>(vimg + rA * SRV + (cA - p2));
+            const double2* vb = reinterpret_cast<const double2*>(vimg + rB * SRV + (cB - p2));
+            double gfac = gw, geff = a.gamma;
+            int degen = 0;
+            if constexpr (FOD) {
+                // OFSE (engine_spectral.cpp:79-97): d = sum_l R[l] W[u-l] over the FULL
+                // spectrum = P[u] sum_canonical (R'[l] V[l-u] + conj(R'[l]) V[l+u]), the
+                // second term only for l with a distinct partner -l
+                double d1r = 0.0, d1i = 0.0, d2r = 0.0, d2i = 0.0;
+                if (active) {
+#pragma unroll
+                    for (int q = 0; q < PPS; ++q) {
+                        const double2 x = va[q], y = vb[q];
+                        d1r = fma(x.x, re[2 * q], fma(x.y, re[2 * q + 1], d1r));
+                        d1i = fma(x.x, im[2 * q], fma(x.y, im[2 * q + 1], d1i));
+                        d2r = fma(y.x, re[2 * q], fma(y.y, re[2 * q + 1], d2r));
+                        d2i = fma(-y.x, im[2 * q], fma(-y.y, im[2 * q + 1], d2i));
+                    }
+                    if (selfbin0) {
+                        const double y0 = vb[0].x;
+                        d2r = fma(-y0, re[0], d2r);
+                        d2i = fma(y0, im[0], d2i);
+                    }
+                    if (ex) {
+                        const double x = vE[rA * SRV + cA + SEG];
+                        d1r = fma(x, re[SEG], d1r);
+                        d1i = fma(x, im[SEG], d1i);
+                    }
+                }
+                double dr = s1 * d1r + s2 * d2r, di = s1 * d1i + s2 * d2i;
+#pragma unroll
+                for (int o = 16; o; o >>= 1) {
+                    dr += __shfl_xor_sync(0xffffffffu, dr, o);
+                    di += __shfl_xor_sync(0xffffffffu, di, o);
+                }
+                if (NW > 1) {
+                    if ((ltid & 31) == 0) dred[par * NW + w] = make_double2(dr, di);
+                    named_bar_sync(bar, GT);
+                    dr = 0.0;
+                    di = 0.0;
+#pragma unroll
+                    for (int k = 0; k < NW; ++k) {
+                        const double2 v = dred[par * NW + k];
+                        dr += v.x;
+                        di += v.y;
+                    }
+                }
+                const double ru = sqrt(M);           // |R'[u]| = |R[u]|
+                const double dm = sqrt(fma(di, di, dr * dr));  // |d|
+                if (dm < 1e-12 * (ru * w0)) {        // |d| < 1e-12 |p| w0^2
+                    geff = 1.0;
+                    degen = 1;
+                } else {
+                    geff = fmin(ru * w0 / dm, 1.0);  // |p w0^2 / d|
+                }
+                gfac = geff / w0;
+            }
+            const double ar = pr * gfac, ai = pi * gfac;  // a = gamma_eff R'[u] / w0
             double c_re = ar * P.x - ai * P.y, c_im = ar * P.y + ai * P.x;  // c = P a
             double a_re = ar, a_im = ai, delta;
             if (self) {
@@ -206,19 +275,12 @@ __global__ void __launch_bounds__(256, 2) k2d_kernel(K2Args a) {
             nu += 1;
             if (ltid == 0) {
                 v2_record(a, b, nu, ntrace, rstride, tstride, rec_u, rec_c, u1, u2, self,
-                          (pr * P.x - pi * P.y) * iw, (pr * P.y + pi * P.x) * iw, c_re, c_im, energy, M, 0.0);
+                          (pr * P.x - pi * P.y) * iw, (pr * P.y + pi * P.x) * iw, c_re, c_im, energy, M, 0.0, geff,
+                          degen);
             }
             ntrace += 1;
 
             // ---- residual update R' -= s1 a V[k-u] + s2 conj(a) V[k+u], fused next scan ----
-            const int p2 = u2 & 1;
-            const double* vimg = vE + p2 * (T * SRV);  // odd copy holds V[c+1]
-            const int rA = (k1 - u1) & (T - 1), rB = (k1 + u1) & (T - 1);
-            const int cA = (c0 - u2) & (T - 1), cB = (c0 + u2) & (T - 1);
-            const double s1 = ((k1 < u1) ? sgn_r : 1.0) * ((c0 < u2) ? sgn_c : 1.0);
-            const double s2 = ((k1 + u1 >= T) ? sgn_r : 1.0) * ((c0 + u2 >= T) ? sgn_c : 1.0);
-            const double2* va = reinterpret_cast<const double2*>(vimg + rA * SRV + (cA - p2));
-            const double2* vb = reinterpret_cast<const double2*>(vimg + rB * SRV + (cB - p2));
             const double n1r = -s1 * a_re, n1i = -s1 * a_im;
             const double n2r = -s2 * a_re, n2i = s2 * a_im;
             KA = 0;
@@ -303,10 +365,11 @@ __global__ void __launch_bounds__(256, 2) k2d_kernel(K2Args a) {
 template <int T>
 static int k2d_t(const K2Args& a, int32_t ntiles, cudaStream_t s) {
     using Cf = DCfg<T>;
-    cudaError_t e = cudaFuncSetAttribute(k2d_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
+    auto* fn = a.full_od ? k2d_kernel<T, true> : k2d_kernel<T, false>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
     if (e != cudaSuccess) return e;
     if (ntiles <= 0) return cudaSuccess;
-    k2d_kernel<T><<<ntiles, Cf::GT * Cf::GROUPS, Cf::SMEM, s>>>(a);
+    fn<<<ntiles, Cf::GT * Cf::GROUPS, Cf::SMEM, s>>>(a);
     return cudaGetLastError();
 }
 

@@ -68,7 +68,8 @@ __device__ __forceinline__ void v2_stage(const K2Args& a, const Tile& tile, unsi
 __device__ __forceinline__ void v2_record(const K2Args& a, int b, int nu, int ntrace, int rstride,
                                           int tstride, int* rec_u, double2* rec_c, int u1, int u2,
                                           int self, double p_re, double p_im, double c_re,
-                                          double c_im, double energy, double Mf, double Sf) {
+                                          double c_im, double energy, double Mf, double Sf,
+                                          double gamma_eff = -1.0, int degenerate = 0) {
     if (rec_u && nu - 1 < rstride) {
         rec_u[nu - 1] = (u1 << 16) | u2;
         rec_c[nu - 1] = self ? make_double2(c_re, 0.0) : make_double2(2.0 * c_re, 2.0 * c_im);
@@ -83,9 +84,9 @@ __device__ __forceinline__ void v2_record(const K2Args& a, int b, int nu, int nt
         rr.p_im = p_im;
         rr.c_re = c_re;
         rr.c_im = c_im;
-        rr.gamma_effective = a.gamma;
+        rr.gamma_effective = gamma_eff >= 0.0 ? gamma_eff : a.gamma;
         rr.weighted_energy = energy;
-        rr.degenerate = 0;
+        rr.degenerate = degenerate;
         rr.pad1 = 0;
         a.trace[(size_t)b * tstride + ntrace] = rr;
     }

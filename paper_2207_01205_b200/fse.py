@@ -327,8 +327,18 @@ class spectral:
                                  float(e[0]), float(e[0]), float(m[0]))
 
     @staticmethod
+    def fast_iterate_full_od(spec, iterations: int, device: int = 0):
+        """OFSE (engine_spectral.cpp:191-193): full orthogonality-deficiency
+        compensation, gamma_eff = min(|p w0^2 / d|, 1); fp64. Resumable."""
+        return spectral._iterate(spec, 1.0, iterations, "fp64", device, full_od=True)
+
+    @staticmethod
     def fast_iterate(spec, gamma: float, iterations: int, precision: str = "fp64", device: int = 0):
         """Resumable like the reference: runs at most `iterations` more selections."""
+        return spectral._iterate(spec, gamma, iterations, precision, device)
+
+    @staticmethod
+    def _iterate(spec, gamma, iterations, precision, device, full_od=False):
         t = spec.t
         rw = np.ascontiguousarray(spec.rw, np.complex128)
         g = np.ascontiguousarray(spec.g, np.complex128)
@@ -343,12 +353,19 @@ class spectral:
         tr = np.zeros(max(its, 1), capi.RECORD_DTYPE)
         tc = np.zeros(1, np.int32)
         ctx = capi.context(device)
-        capi.check(capi.lib().fofse_spectral_iterate(
-            ctx.handle, t, C.c_int64(1), spec.window_height, spec.window_width, capi.ptr(rw.view(np.float64)),
-            capi.ptr(ws.view(np.float64)), capi.ptr(g.view(np.float64)), capi.ptr(w0), capi.ptr(e),
-            capi.ptr(ei), capi.ptr(im), capi.ptr(nu, C.c_int32), capi.ptr(cv, C.c_int32),
-            C.c_double(gamma), int(iterations), _PRECS[precision], capi.vptr(tr),
-            capi.ptr(tc, C.c_int32)))
+        if full_od:
+            capi.check(capi.lib().fofse_spectral_iterate_full_od(
+                ctx.handle, t, C.c_int64(1), spec.window_height, spec.window_width,
+                capi.ptr(rw.view(np.float64)), capi.ptr(ws.view(np.float64)), capi.ptr(g.view(np.float64)),
+                capi.ptr(w0), capi.ptr(e), capi.ptr(ei), capi.ptr(im), capi.ptr(nu, C.c_int32),
+                capi.ptr(cv, C.c_int32), int(iterations), capi.vptr(tr), capi.ptr(tc, C.c_int32)))
+        else:
+            capi.check(capi.lib().fofse_spectral_iterate(
+                ctx.handle, t, C.c_int64(1), spec.window_height, spec.window_width, capi.ptr(rw.view(np.float64)),
+                capi.ptr(ws.view(np.float64)), capi.ptr(g.view(np.float64)), capi.ptr(w0), capi.ptr(e),
+                capi.ptr(ei), capi.ptr(im), capi.ptr(nu, C.c_int32), capi.ptr(cv, C.c_int32),
+                C.c_double(gamma), int(iterations), _PRECS[precision], capi.vptr(tr),
+                capi.ptr(tc, C.c_int32)))
         spec.rw, spec.g = rw, g
         spec.weighted_energy = float(e[0])
         spec.nu = int(nu[0])

@@ -61,6 +61,32 @@ def test_iterate_bit_exact_vs_oracle(gpu, orc, t, h, w, gamma, iters):
     np.testing.assert_array_equal(got.rw[can], ref.rw[can])
 
 
+@pytest.mark.parametrize("t,h,w,iters", [(8, 6, 7, 20), (32, 24, 24, 50), (64, 48, 48, 120), (64, 40, 47, 80),
+                                          (128, 64, 64, 40)])
+def test_iterate_full_od_vs_oracle(gpu, orc, t, h, w, iters):
+    """OFSE (fast_iterate_full_od, engine_spectral.cpp:79-97): the strict kernel with
+    the block-wide d = sum_l R_w[l] W[u-l] reduction gives the oracle's selections;
+    gamma_eff / p / c / energies agree to rounding (the reduction order differs)."""
+    rng = np.random.default_rng(2000 + t + h)
+    spec, *_ = _oracle_spectrum(orc, rng, t, h, w)
+    ref = spec.copy()
+    rec_ref = orc.fast_iterate_full_od(ref, iters)
+    got = P.spectral.Spectrum(spec.t, spec.window_width, spec.window_height, spec.rw.copy(), spec.w.copy(),
+                              spec.g.copy(), spec.w0, spec.weighted_energy, spec.initial_energy,
+                              spec.initial_max, spec.nu, spec.converged)
+    rec = P.spectral.fast_iterate_full_od(got, iters)
+    assert len(rec) == len(rec_ref) > 0
+    for k in ("u1", "u2", "degenerate"):
+        np.testing.assert_array_equal(rec[k], rec_ref[k], err_msg=k)
+    for k in ("p_re", "p_im", "c_re", "c_im", "gamma_effective"):
+        np.testing.assert_allclose(rec[k], rec_ref[k], rtol=1e-9, atol=1e-12 * np.abs(rec_ref["p_re"]).max(),
+                                   err_msg=k)
+    assert (rec["gamma_effective"] < 1.0).any()  # the compensation is active
+    np.testing.assert_allclose(rec["weighted_energy"], rec_ref["weighted_energy"], rtol=1e-9,
+                               atol=1e-9 * spec.initial_energy)
+    assert np.abs(got.g - ref.g).max() <= 1e-9 * np.abs(ref.g).max()
+
+
 def test_iterate_resumes_like_reference(gpu, orc):
     """fast_iterate runs at most `iterations` more selections (engine_spectral.hpp:41-43)."""
     rng = np.random.default_rng(7)
@@ -128,7 +154,7 @@ def test_synthesize_vs_oracle(gpu, orc):
 
 def _oracle_conceal(orc, img, pat, cfg, traces=True):
     return orc.conceal(img.astype(np.float64), [tuple(b) for b in pat.blocks], pat.block_height,
-                       pat.block_width, algorithm=2 if cfg.algorithm == "fofse" else 0,
+                       pat.block_width, algorithm={"fse": 0, "ofse": 1, "fofse": 2}[cfg.algorithm],
                        gamma=cfg.gamma, iterations=cfg.iterations, t=cfg.transform_size,
                        rho_hat=cfg.rho_hat, support=cfg.support_width, traces=traces)
 
@@ -216,6 +242,38 @@ def test_conceal_fp64_small_transforms(gpu, orc, t, b, sw):
     pat = P.LossPattern(96, 96, b, b, [P.Rect(r, c, b, b) for r, c in cells])
     cfg = P.ConcealConfig(gamma=0.5, iterations=40, transform_size=t, support_width=sw, record_traces=True)
     out = P.conceal(img, pat, cfg)
+    ref = _oracle_conceal(orc, img, pat, cfg)
+    _assert_same_selections(out.report.traces, ref["traces"])
+    assert np.abs(out.restored - ref["restored"]).max() <= FP64_PX_TOL
+
+
+def test_conceal_ofse_vs_oracle(gpu, orc):
+    """pipeline ofse (fast_iterate_full_od per window, pipeline.cpp:194-196): K2d with
+    the rotated-frame d reduction (interior masks) and the strict kernel (border and
+    neighbour masks) give the oracle's selections; pixels within 1e-9."""
+    rng = np.random.default_rng(457)
+    img = smooth_test_image(rng, 160)
+    blocks = [(0, 0, 16, 16), (0, 48, 16, 16), (48, 48, 16, 16), (48, 80, 16, 16), (96, 16, 16, 16),
+              (112, 128, 16, 16), (144, 144, 16, 16)]
+    pat = P.LossPattern(160, 160, 16, 16, [P.Rect(*b) for b in blocks])
+    cfg = P.ConcealConfig(algorithm="ofse", iterations=60, transform_size=64, support_width=16,
+                          record_traces=True)
+    out = P.conceal(img, pat, cfg)
+    ref = _oracle_conceal(orc, img, pat, cfg)
+    _assert_same_selections(out.report.traces, ref["traces"])
+    assert np.abs(out.restored - ref["restored"]).max() <= FP64_PX_TOL
+    # an fp32 request runs the same fp64 OFSE kernels
+    out32 = P.conceal(img, pat, P.ConcealConfig(algorithm="ofse", iterations=60, transform_size=64,
+                                                support_width=16, precision="fp32"))
+    np.testing.assert_array_equal(out32.restored, out.restored)
+
+
+def test_conceal_ofse_C1(gpu, orc):
+    """BASELINE C1 frame with algorithm = ofse (100 iterations): oracle selections, pixels <= 1e-9."""
+    img, pat = WL.C1.frame(seed=12)
+    cfg = WL.C1.config(record_traces=True)
+    cfg.algorithm = "ofse"
+    out = P.conceal(img.astype(np.float64), pat, cfg)
     ref = _oracle_conceal(orc, img, pat, cfg)
     _assert_same_selections(out.report.traces, ref["traces"])
     assert np.abs(out.restored - ref["restored"]).max() <= FP64_PX_TOL
