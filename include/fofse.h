@@ -204,6 +204,16 @@ int fofse_spectral_iterate(fofse_ctx* ctx, int32_t t, int64_t n, int32_t win_h, 
                            const double* initial_max, int32_t* nu, int32_t* converged,
                            double gamma, int32_t iterations, int32_t precision,
                            fofse_record* traces, int32_t* trace_counts);
+/* fse::psnr_vs_iterations (pipeline.hpp:86-100, pipeline.cpp:264-369): for each of
+ * n_series configs, the PSNR over all MISSING samples after stride, 2*stride, ...
+ * <= max_iterations selections (resumable fp64 phases on the GPU). checkpoints
+ * (optional, max_iterations/stride entries) receives the iteration counts;
+ * psnr_db is [n_series][max_iterations/stride] (+inf for an exact model). */
+int fofse_psnr_curves(fofse_ctx* ctx, const double* image, int32_t width, int32_t height,
+                      const fofse_rect* blocks, int64_t n, int32_t bh, int32_t bw, const fofse_params* series,
+                      int32_t n_series, int32_t max_iterations, int32_t stride, int32_t* checkpoints,
+                      double* psnr_db);
+
 /* fse::spectral::fast_iterate_full_od (engine_spectral.hpp:47-48, .cpp:191-193):
  * OFSE, gamma_eff = min(|p w0^2 / d|, 1) with d = sum_l R_w[l] W[u-l]; fp64. */
 int fofse_spectral_iterate_full_od(fofse_ctx* ctx, int32_t t, int64_t n, int32_t win_h, int32_t win_w,

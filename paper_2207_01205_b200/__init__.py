@@ -8,13 +8,13 @@ Python mirror over it (see fse.py).
 from . import _capi
 from ._capi import (FofseCudaError, FofseError, Context, context, gen_image_u8, gen_losses,
                     LIB_PATH)
-from .fse import (ConcealConfig, ConcealmentReport, ConcealOutput, LossPattern, Rect, Region,
+from .fse import (ConcealConfig, ConcealmentReport, ConcealOutput, CurveSeries, LossPattern, Rect, Region,
                   WindowRun, build_isotropic_weight, conceal, conceal_frames, conceal_shard, extrapolate_window,
-                  extrapolate_windows, parse_algorithm, psnr, series_label, spectral)
+                  extrapolate_windows, parse_algorithm, psnr, psnr_vs_iterations, series_label, spectral)
 
 __all__ = [
-    "ConcealConfig", "ConcealmentReport", "ConcealOutput", "LossPattern", "Rect", "Region",
+    "ConcealConfig", "ConcealmentReport", "ConcealOutput", "CurveSeries", "LossPattern", "Rect", "Region",
     "WindowRun", "build_isotropic_weight", "conceal", "conceal_frames", "conceal_shard", "extrapolate_window",
-    "extrapolate_windows", "parse_algorithm", "psnr", "series_label", "spectral",
+    "extrapolate_windows", "parse_algorithm", "psnr", "psnr_vs_iterations", "series_label", "spectral",
     "FofseCudaError", "FofseError", "Context", "context", "gen_image_u8", "gen_losses", "LIB_PATH",
 ]

@@ -24,6 +24,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <limits>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -556,7 +557,8 @@ struct GroupIO {
 // by the caller's block order.
 RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int synth,
                double* d_block_sq, double* d_models, fofse_record* d_trace, int32_t* d_trace_count,
-               float* d_gap = nullptr, const GroupIO* gio = nullptr) {
+               float* d_gap = nullptr, const GroupIO* gio = nullptr,
+               const std::vector<int>* ckpts = nullptr) {
     using namespace fofse;
     const Geometry& g = job.geo;
     const int T = g.T;
@@ -580,7 +582,8 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             if (lab[i] == FOFSE_SUPPORT) wcls[static_cast<size_t>(c) * L + i] = job.wfull[i];
         sym[static_cast<size_t>(c)] = point_symmetric(lab, g.Lh, g.Lw) ? 1 : 0;
     }
-    const bool fp32 = cfg.precision == FOFSE_PREC_FP32 && !full_od(cfg);
+    // fp64 only: OFSE and the checkpointed curves (resumable fp64 phases)
+    const bool fp32 = cfg.precision == FOFSE_PREC_FP32 && !full_od(cfg) && !ckpts;
     const int head = fp32 ? resolve_head(cfg) : 0;
     out.head = head;
     const bool v2 = fp32 && v2_supported(T);
@@ -734,10 +737,11 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         a.w0 = d_w0;
         a.synth = synth;
         a.fr = fr;
-        a.reg_r0 = synth == SYN_IMAGE ? g.S : 0;
-        a.reg_c0 = synth == SYN_IMAGE ? g.S : 0;
-        a.reg_nr = synth == SYN_IMAGE ? g.bh : g.Lh;
-        a.reg_nc = synth == SYN_IMAGE ? g.bw : g.Lw;
+        const bool img_region = synth == SYN_IMAGE || synth == SYN_ERR;  // the block, not the window
+        a.reg_r0 = img_region ? g.S : 0;
+        a.reg_c0 = img_region ? g.S : 0;
+        a.reg_nr = img_region ? g.bh : g.Lh;
+        a.reg_nc = img_region ? g.bw : g.Lw;
         a.models = d_models;
         a.block_sq = d_block_sq;
         a.twid_inv = d_twi;
@@ -804,8 +808,42 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         K2Args a = base_args();
         a.rin = d_R64;
         a.rec_global = 0;
-        for (size_t i = 0; i < ranges.size(); ++i)
-            k2_f64(a, hi_path(ranges[i].path), ranges[i].begin, ranges[i].end, sorted, std::to_string(i), st);
+        if (!ckpts) {
+            for (size_t i = 0; i < ranges.size(); ++i)
+                k2_f64(a, hi_path(ranges[i].path), ranges[i].begin, ranges[i].end, sorted, std::to_string(i), st);
+        } else {
+            // checkpointed curves (pipeline.cpp:264-369): resumable phases up to each
+            // checkpoint, state carried by position in place, records at nu-1, then
+            // the squared error of the clamped model (no write-back): d_block_sq
+            // holds [checkpoint][block]
+            double* d_en = ctx->buf("en").as<double>(static_cast<size_t>(n));
+            int32_t* d_nu = ctx->buf("nu").as<int32_t>(static_cast<size_t>(n));
+            int32_t* d_cv = ctx->buf("cvh").as<int32_t>(static_cast<size_t>(n));
+            ck(cudaMemcpyAsync(d_en, d_e0, sizeof(double) * n, cudaMemcpyDeviceToDevice, st), "D2D");
+            ck(cudaMemsetAsync(d_nu, 0, sizeof(int32_t) * n, st), "memset");
+            ck(cudaMemsetAsync(d_cv, 0, sizeof(int32_t) * n, st), "memset");
+            ck(cudaMemsetAsync(d_conv, 0, sizeof(int32_t) * n, st), "memset");
+            a.rout = d_R64;
+            a.state_by_pos = 1;
+            a.energy0 = d_en;
+            a.energy_out = d_en;
+            a.nu0 = d_nu;
+            a.nu_out = d_nu;
+            a.conv0 = d_cv;
+            a.conv_out = d_cv;
+            a.rec_global = 1;
+            a.trace_from_nu0 = 1;
+            a.synth = SYN_ERR;
+            int done = 0;
+            for (size_t c = 0; c < ckpts->size(); ++c) {
+                a.iterations = (*ckpts)[c] - done;
+                a.block_sq = d_block_sq + c * static_cast<size_t>(n);
+                for (size_t i = 0; i < ranges.size(); ++i)
+                    k2_f64(a, hi_path(ranges[i].path), ranges[i].begin, ranges[i].end, sorted,
+                           std::to_string(i), st);
+                done = (*ckpts)[c];
+            }
+        }
         ck(cudaEventRecord(ctx->ev[2], st), "event");
         ck(cudaEventRecord(ctx->ev[3], st), "event");
         if (gio)
@@ -1219,6 +1257,53 @@ static void conceal_f64_impl(fofse_ctx* ctx, const double* image, int32_t width,
         for (double v : sq) tot += v;
         fill_report(report, ro, n, static_cast<int64_t>(job.cls_labels.size()), tot,
                     n * static_cast<int64_t>(bh) * bw, ctx->launches - l0);
+}
+
+int fofse_psnr_curves(fofse_ctx* ctx, const double* image, int32_t width, int32_t height,
+                      const fofse_rect* blocks, int64_t n, int32_t bh, int32_t bw, const fofse_params* series,
+                      int32_t n_series, int32_t max_iterations, int32_t stride, int32_t* checkpoints,
+                      double* psnr_db) {
+    return guarded([&] {
+        // pipeline.cpp:264-279
+        if (stride < 1) throw std::invalid_argument("psnr_vs_iterations: stride must be >= 1");
+        if (max_iterations < 0) throw std::invalid_argument("psnr_vs_iterations: iterations must be >= 0");
+        if (!ctx || !image || (n && !blocks) || (n_series && !series))
+            throw std::invalid_argument("psnr_curves: NULL argument");
+        if (width < 1 || height < 1) throw std::invalid_argument("grid dimensions must be >= 1");
+        std::vector<int> cks;
+        for (int it = stride; it <= max_iterations; it += stride) cks.push_back(it);
+        if (checkpoints)
+            for (size_t c = 0; c < cks.size(); ++c) checkpoints[c] = cks[c];
+        if (cks.empty()) return;
+        const int64_t missing = n * static_cast<int64_t>(bh) * bw;  // disjoint blocks
+        const size_t npx = static_cast<size_t>(width) * height;
+        for (int si = 0; si < n_series; ++si) {
+            Cfg cfg = to_cfg(series + si);
+            const int64_t offs[2] = {0, n};
+            Job job = make_image_job(cfg, width, height, bh, bw, blocks, offs, 1);  // validate + fits
+            cfg.iterations = cks.back();
+            cfg.precision = FOFSE_PREC_FP64;
+            ctx->activate();
+            double* d_img = ctx->buf("img64").as<double>(npx);
+            ck(cudaMemcpyAsync(d_img, image, npx * sizeof(double), cudaMemcpyHostToDevice, ctx->stream), "H2D image");
+            double* d_sq = ctx->buf("cksq").as<double>(std::max<size_t>(cks.size() * static_cast<size_t>(n), 1));
+            fofse::Frames fr{d_img, d_img, fofse::SRC_F64, width, height, static_cast<int64_t>(npx)};
+            std::vector<double> sq(cks.size() * static_cast<size_t>(n), 0.0);
+            if (n > 0) {
+                run_job(ctx, job, cfg, fr, fofse::SYN_ERR, d_sq, nullptr, nullptr, nullptr, nullptr, nullptr, &cks);
+                ck(cudaMemcpyAsync(sq.data(), d_sq, sizeof(double) * sq.size(), cudaMemcpyDeviceToHost, ctx->stream),
+                    "D2H sq");
+                ck(cudaStreamSynchronize(ctx->stream), "sync");
+            }
+            for (size_t c = 0; c < cks.size(); ++c) {
+                double total = 0.0;  // block order, for determinism (pipeline.cpp:356-358)
+                for (int64_t b = 0; b < n; ++b) total += sq[c * static_cast<size_t>(n) + static_cast<size_t>(b)];
+                const double mse = missing ? total / static_cast<double>(missing) : 0.0;
+                psnr_db[static_cast<size_t>(si) * cks.size() + c] =
+                    mse > 0.0 ? 10.0 * std::log10(255.0 * 255.0 / mse) : std::numeric_limits<double>::infinity();
+            }
+        }
+    });
 }
 
 int fofse_conceal_f64(fofse_ctx* ctx, const double* image, int32_t width, int32_t height,

@@ -824,17 +824,17 @@ __global__ void __launch_bounds__(K2Cfg<T, PATH>::THREADS) k2_kernel(K2Args a) {
                     if (a.fr.type == SRC_U8) {
                         orig = (double)static_cast<const uint8_t*>(a.fr.src)[gi];
                         // write_pgm rounding (image_io.cpp:73-77): std::round = half away from 0
-                        static_cast<uint8_t*>(a.fr.dst)[gi] = static_cast<uint8_t>(round(v));
+                        if (a.synth == SYN_IMAGE) static_cast<uint8_t*>(a.fr.dst)[gi] = static_cast<uint8_t>(round(v));
                     } else {
                         orig = static_cast<const double*>(a.fr.src)[gi];
-                        static_cast<double*>(a.fr.dst)[gi] = v;
+                        if (a.synth == SYN_IMAGE) static_cast<double*>(a.fr.dst)[gi] = v;
                     }
                     const double e = orig - v;
                     sq += e * e;
                 }
             }
         }
-        if (a.block_sq && a.synth == SYN_IMAGE) {
+        if (a.block_sq && (a.synth == SYN_IMAGE || a.synth == SYN_ERR)) {
 #pragma unroll
             for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
             if (lane == 0) gs->red[warp] = sq;

@@ -109,7 +109,7 @@ struct K2Args {
     int32_t* trace_count;       // per block (optional)
     double2* gspec;             // [block][T*T] model spectrum accumulate (optional)
     // synthesis
-    int32_t synth;              // SYN_NONE / SYN_IMAGE / SYN_WINDOW
+    int32_t synth;              // SYN_NONE / SYN_IMAGE / SYN_WINDOW / SYN_ERR
     Frames fr;                  // SYN_IMAGE: frames (reads original, writes restored)
     int32_t reg_r0, reg_c0, reg_nr, reg_nc;  // region in window coordinates
     double* models;             // SYN_WINDOW: [block][Lh*Lw]
@@ -141,7 +141,9 @@ struct CvtArgs {
     int32_t soa;                // SoA pair layout (K2v2 real path)
     int64_t out_stride;         // floats per block (0 = packed size)
 };
-enum { SYN_NONE = 0, SYN_IMAGE = 1, SYN_WINDOW = 2 };
+// SYN_ERR: squared error of the clamped model vs the source over the region, no
+// write-back (checkpointed PSNR curves, pipeline.cpp:264-369)
+enum { SYN_NONE = 0, SYN_IMAGE = 1, SYN_WINDOW = 2, SYN_ERR = 3 };
 
 // Host launchers (return cudaError_t).
 int k1_launch(const K1Args& a, cudaStream_t s);

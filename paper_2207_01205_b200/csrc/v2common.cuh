@@ -168,16 +168,16 @@ __device__ __forceinline__ void v2_finish(const K2Args& a, const BlockDesc& desc
                 double orig;
                 if (a.fr.type == SRC_U8) {
                     orig = (double)static_cast<const uint8_t*>(a.fr.src)[gi];
-                    static_cast<uint8_t*>(a.fr.dst)[gi] = static_cast<uint8_t>(round(v));
+                    if (a.synth == SYN_IMAGE) static_cast<uint8_t*>(a.fr.dst)[gi] = static_cast<uint8_t>(round(v));
                 } else {
                     orig = static_cast<const double*>(a.fr.src)[gi];
-                    static_cast<double*>(a.fr.dst)[gi] = v;
+                    if (a.synth == SYN_IMAGE) static_cast<double*>(a.fr.dst)[gi] = v;
                 }
                 sq += (orig - v) * (orig - v);
             }
         }
     }
-    if (a.block_sq && a.synth == SYN_IMAGE) {
+    if (a.block_sq && (a.synth == SYN_IMAGE || a.synth == SYN_ERR)) {
 #pragma unroll
         for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
         if constexpr (NTH == 32) {

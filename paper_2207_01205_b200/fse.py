@@ -143,6 +143,41 @@ def _report(config, rep: capi.Report, traces=None) -> ConcealmentReport:
         mean_seconds_per_block=rep.mean_seconds_per_block, traces=traces, device=rep.as_dict())
 
 
+@dataclass
+class CurveSeries:
+    """fse::CurveSeries (pipeline.hpp:86-96): label + (iterations, psnr_db) points."""
+    label: str
+    points: list
+
+
+def psnr_vs_iterations(image: np.ndarray, pattern: LossPattern, algorithms, max_iterations: int,
+                       stride: int, device: int = 0) -> list:
+    """fse::psnr_vs_iterations (pipeline.cpp:264-369): the PSNR over all MISSING
+    samples after stride, 2 stride, ... <= max_iterations selections, per config
+    (the paper's Fig. 4/5 gamma sweep). Resumable fp64 phases on the GPU."""
+    if stride < 1:
+        raise ValueError("psnr_vs_iterations: stride must be >= 1")
+    if max_iterations < 0:
+        raise ValueError("psnr_vs_iterations: iterations must be >= 0")
+    algorithms = list(algorithms)
+    image = np.ascontiguousarray(image, np.float64)
+    h, w = image.shape
+    nck = max_iterations // stride
+    if nck == 0:
+        return [CurveSeries(series_label(c), []) for c in algorithms]
+    rects = capi.rects_array(pattern.blocks)
+    params = (capi.Params * max(len(algorithms), 1))(*[c.params() for c in algorithms])
+    cks = np.zeros(nck, np.int32)
+    db = np.zeros((len(algorithms), nck), np.float64)
+    ctx = capi.context(device)
+    capi.check(capi.lib().fofse_psnr_curves(
+        ctx.handle, capi.ptr(image), w, h, rects.ctypes.data_as(C.POINTER(capi.Rect_)), C.c_int64(len(rects)),
+        pattern.block_height, pattern.block_width, params, len(algorithms), int(max_iterations), int(stride),
+        capi.ptr(cks, C.c_int32), capi.ptr(db)))
+    return [CurveSeries(series_label(c), [(int(cks[k]), float(db[i, k])) for k in range(nck)])
+            for i, c in enumerate(algorithms)]
+
+
 def conceal(image: np.ndarray, pattern: LossPattern, config: ConcealConfig | None = None,
             device: int = 0) -> ConcealOutput:
     """fse::conceal: restored image (MISSING samples replaced, clamped, unrounded) + report."""

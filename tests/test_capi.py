@@ -208,3 +208,13 @@ def test_python_config_validation_messages():
         P.parse_algorithm("bogus")
     assert P.series_label(P.ConcealConfig(gamma=0.35)) == "fofse_g0.35"
     assert P.series_label(P.ConcealConfig(algorithm="fse")) == "fse"
+
+
+def test_psnr_curves_validation_without_gpu():
+    """pipeline.cpp:267-270: stride and iteration bounds are checked first."""
+    pat = P.LossPattern(64, 64, 16, 16, [])
+    with pytest.raises(ValueError, match="stride must be >= 1"):
+        P.psnr_vs_iterations(np.zeros((64, 64)), pat, [P.ConcealConfig()], 10, 0)
+    with pytest.raises(ValueError, match="iterations must be >= 0"):
+        P.psnr_vs_iterations(np.zeros((64, 64)), pat, [P.ConcealConfig()], -1, 5)
+    assert P.psnr_vs_iterations(np.zeros((64, 64)), pat, [P.ConcealConfig(gamma=0.5)], 3, 5)[0].label == "fofse_g0.5"

@@ -279,6 +279,27 @@ def test_conceal_ofse_C1(gpu, orc):
     assert np.abs(out.restored - ref["restored"]).max() <= FP64_PX_TOL
 
 
+def test_psnr_curves_vs_oracle(gpu, orc):
+    """psnr_vs_iterations (pipeline.cpp:264-369): checkpointed PSNR after every
+    `stride` selections for a gamma sweep + fse + ofse equals, point by point, the
+    PSNR of a plain conceal run with that many iterations (oracle)."""
+    rng = np.random.default_rng(461)
+    img = smooth_test_image(rng, 128)
+    blocks = [(16, 16, 16, 16), (16, 80, 16, 16), (64, 48, 16, 16), (96, 96, 16, 16), (0, 112, 16, 16)]
+    pat = P.LossPattern(128, 128, 16, 16, [P.Rect(*b) for b in blocks])
+    algos = [P.ConcealConfig(gamma=g) for g in (0.2, 0.5, 1.0)] + [P.ConcealConfig(algorithm="fse"),
+                                                                   P.ConcealConfig(algorithm="ofse")]
+    curves = P.psnr_vs_iterations(img, pat, algos, max_iterations=45, stride=15)
+    assert [c.label for c in curves] == ["fofse_g0.2", "fofse_g0.5", "fofse_g1", "fse", "ofse"]
+    for cfg, cur in zip(algos, curves):
+        assert [it for it, _ in cur.points] == [15, 30, 45]
+        for it, db in cur.points:
+            c2 = P.ConcealConfig(algorithm=cfg.algorithm, gamma=cfg.gamma, iterations=it)
+            ref = _oracle_conceal(orc, img, pat, c2, traces=False)
+            assert db == pytest.approx(ref["psnr_db"], rel=1e-9), (cur.label, it)
+    assert P.psnr_vs_iterations(img, pat, algos[:1], max_iterations=5, stride=10)[0].points == []
+
+
 def test_conceal_empty_pattern_is_identity(gpu):
     """pipeline_test.cpp:171-183."""
     img = smooth_test_image(np.random.default_rng(421), 64)
