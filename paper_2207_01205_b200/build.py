@@ -53,9 +53,24 @@ def build(verbose: bool = False) -> str:
     if _newer(LIB, objs):
         cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs, "-lpthread", "-ldl", "-lrt"]
         subprocess.run(cmd, check=True)
+    build_cli()
     if verbose:
         print(LIB)
     return LIB
+
+
+CLI_SRC = os.path.join(PKG, "cli", "fofse_cli.cpp")
+CLI = os.path.join(LIB_DIR, "fofse")
+
+
+def build_cli() -> str:
+    """The reference-CLI front-end (cli/fofse_cli.cpp) linked against libfofse.so."""
+    deps = [CLI_SRC, LIB, os.path.join(ROOT, "include", "fofse.h"), os.path.join(ROOT, "include", "fofse_fse.hpp")]
+    if _newer(CLI, deps):
+        cmd = [os.environ.get("CXX", "g++"), "-O2", "-std=c++17", "-Wall", "-I" + os.path.join(ROOT, "include"),
+               CLI_SRC, "-o", CLI, "-L" + LIB_DIR, "-lfofse", "-Wl,-rpath,$ORIGIN"]
+        subprocess.run(cmd, check=True)
+    return CLI
 
 
 if __name__ == "__main__":
