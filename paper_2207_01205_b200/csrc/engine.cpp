@@ -401,7 +401,9 @@ void classify_frames(Job& job, const fofse_rect* blocks, const int64_t* offs, in
             job.blocks[static_cast<size_t>(i)] = d;
             const int top = std::max(0, -r0), left = std::max(0, -c0);
             const int bottom = std::max(0, r0 + g.Lh - H), right = std::max(0, c0 + g.Lw - W);
-            std::vector<int32_t> nb;
+            std::array<int32_t, 4> nbuf[64];  // neighbour rects inside the window (no heap for the common case)
+            int nnb = 0;
+            std::vector<std::array<int32_t, 4>> nbig;
             const int cr0 = std::max(0, (std::max(r0, 0)) / g.bh - 1);
             const int cr1 = std::min(cg.gh - 1, (std::min(r0 + g.Lh, H) - 1) / g.bh);
             const int cc0 = std::max(0, (std::max(c0, 0)) / g.bw - 1);
@@ -414,15 +416,18 @@ void classify_frames(Job& job, const fofse_rect* blocks, const int64_t* offs, in
                     const int a0 = std::max(o.row - r0, 0), a1 = std::min(o.row + o.height - r0, g.Lh);
                     const int b0 = std::max(o.col - c0, 0), b1 = std::min(o.col + o.width - c0, g.Lw);
                     if (a0 >= a1 || b0 >= b1) continue;
-                    nb.insert(nb.end(), {a0, b0, a1, b1});
+                    if (nnb < 64)
+                        nbuf[nnb++] = {a0, b0, a1, b1};
+                    else
+                        nbig.push_back({a0, b0, a1, b1});
                 }
-            if (!top && !left && !bottom && !right && nb.empty()) {
+            if (!top && !left && !bottom && !right && nnb == 0) {
                 interior[static_cast<size_t>(i)] = 1;
                 continue;
             }
             // canonical order of the neighbour rects
-            std::vector<std::array<int32_t, 4>> rects;
-            for (size_t k = 0; k < nb.size(); k += 4) rects.push_back({nb[k], nb[k + 1], nb[k + 2], nb[k + 3]});
+            std::vector<std::array<int32_t, 4>> rects(nbuf, nbuf + nnb);
+            rects.insert(rects.end(), nbig.begin(), nbig.end());
             std::sort(rects.begin(), rects.end());
             std::vector<int32_t> key = {top, bottom, left, right, static_cast<int32_t>(rects.size())};
             for (auto& r : rects) key.insert(key.end(), r.begin(), r.end());
@@ -433,12 +438,14 @@ void classify_frames(Job& job, const fofse_rect* blocks, const int64_t* offs, in
     const std::vector<int32_t> interior_key = {0, 0, 0, 0, 0};
     int32_t interior_id = -1;
     for (int64_t i = 0; i < n; ++i) {
+        if (interior[static_cast<size_t>(i)] && interior_id >= 0) {  // the common case: no key at all
+            job.blocks[static_cast<size_t>(i)].cls = interior_id;
+            continue;
+        }
         std::vector<int32_t> key = interior[static_cast<size_t>(i)] ? interior_key
                                                                     : std::move(keys[static_cast<size_t>(i)]);
         int32_t id;
-        if (interior[static_cast<size_t>(i)] && interior_id >= 0) {
-            id = interior_id;
-        } else {
+        {
             const std::vector<int32_t> kcopy = key;
             id = tab.intern(std::move(key), [&] { return labels_from_key(g, kcopy); });
             if (interior[static_cast<size_t>(i)]) interior_id = id;
@@ -1106,6 +1113,7 @@ void fill_report(fofse_report* rep, const RunOut& ro, int64_t n, int64_t ncls, d
 Job make_image_job(const Cfg& cfg, int W, int H, int bh, int bw, const fofse_rect* blocks,
                    const int64_t* offs, int nframes) {
     validate_config(cfg);
+    const HostProf hp_;
     Job job;
     job.geo = Geometry{cfg.T, bh, bw, cfg.S, bh + 2 * cfg.S, bw + 2 * cfg.S};
     std::vector<CellGrid> grids(static_cast<size_t>(nframes));
@@ -1129,8 +1137,10 @@ Job make_image_job(const Cfg& cfg, int W, int H, int bh, int bw, const fofse_rec
     if (job.geo.Lh > cfg.T || job.geo.Lw > cfg.T)
         throw std::invalid_argument("conceal: block + support frame exceeds the transform grid");
     check_gpu_support(cfg);
+    hp_.mark("make_image_job: validate");
     job.wfull = full_weight(job.geo.Lh, job.geo.Lw, cfg.rho);
     if (offs[nframes] > 0) classify_frames(job, blocks, offs, nframes, W, H, grids);
+    hp_.mark("make_image_job: classify");
     return job;
 }
 
