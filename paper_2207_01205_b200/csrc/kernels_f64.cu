@@ -326,14 +326,16 @@ __global__ void __launch_bounds__(256, 2) k2d_kernel(K2Args a) {
                 // hand-off to the fp32 real path: SoA bin pairs (re_a, re_b, im_a, im_b)
                 const BinLayout Lo = BinLayout::make(T, a.rout_seg, a.rout_spt);
                 float* o = static_cast<float*>(a.rout) + (size_t)pos * a.rout_stride;
+                // this thread's bins are consecutive columns of one destination segment:
+                // locate pair 0 once, the others follow (pair slot p0 + q, same lane)
+                int i0, t;
+                bin_slot(Lo, k1, c0, &i0, &t);
+                const int s0 = i0 / (Lo.SEG + 1), j0 = i0 - s0 * (Lo.SEG + 1);
+                float4* o4 = reinterpret_cast<float4*>(o) + (size_t)(s0 * (Lo.SEG / 2) + j0 / 2) * Lo.NT + t;
 #pragma unroll
-                for (int q = 0; q < PPS; ++q) {
-                    int i, t;
-                    bin_slot(Lo, k1, c0 + 2 * q, &i, &t);
-                    const int s = i / (Lo.SEG + 1), j = i - s * (Lo.SEG + 1);
-                    reinterpret_cast<float4*>(o)[(size_t)(s * (Lo.SEG / 2) + j / 2) * Lo.NT + t] =
+                for (int q = 0; q < PPS; ++q)
+                    o4[(size_t)q * Lo.NT] =
                         make_float4((float)re[2 * q], (float)re[2 * q + 1], (float)im[2 * q], (float)im[2 * q + 1]);
-                }
                 if (ex) {
                     int i, t;
                     bin_slot(Lo, k1, T / 2, &i, &t);
