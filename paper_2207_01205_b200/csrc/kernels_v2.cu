@@ -132,11 +132,11 @@ __global__ void __launch_bounds__(128, VAR == 0 ? 3 : 2) k2v2r_kernel(K2Args a) 
     using Cf = V2Cfg<T, PATH_F32_REAL, Q4>;
     constexpr int SEG = Cf::SEG, SPT = Cf::SPT, NT = Cf::NT, NP = Cf::NP, SRV = Cf::SRV;
     constexpr int PPS = SEG / 2;  // pairs per segment
-    // VAR 0: scan fused into the update (2 argmax chains); VAR 1: the scan runs as
-    // its own pass over the updated registers with 4 independent chains (ILP)
-    constexpr bool FUSED = VAR != 1;
-    static_assert(!Q4 || FUSED, "quad layout uses the fused scan");
-    constexpr int ACC = (VAR == 0 || VAR == 2) ? 2 : 4;  // independent argmax chains
+    // VAR 0 (production): even/odd V pairs, 168 registers, 3 CTAs/SM;
+    // VAR 3: quad V layout (LDS.128 per two pairs), 2 CTAs/SM — measured ~2 % slower;
+    // VAR 9: diagnostic — the update + scan alone (one REDUX, synthetic selections).
+    // The next scan is fused into the update in every variant.
+    constexpr int ACC = VAR == 0 ? 2 : 4;  // independent argmax chains
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const Tile tile = a.tiles[blockIdx.x];
@@ -375,8 +375,7 @@ __global__ void __launch_bounds__(128, VAR == 0 ? 3 : 2) k2v2r_kernel(K2Args a) 
                         const float2 x = va[q];
                         rp[p] = __ffma2_rn(n1r, x, rp[p]);
                         ip[p] = __ffma2_rn(n1i, x, ip[p]);
-                        if constexpr (FUSED)
-                            kacc_pair(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+                        kacc_pair(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
                     }
                 } else {
 #pragma unroll
@@ -385,8 +384,7 @@ __global__ void __launch_bounds__(128, VAR == 0 ? 3 : 2) k2v2r_kernel(K2Args a) 
                         const float2 x = va[q], y = vb[q];
                         rp[p] = __ffma2_rn(n2r, y, __ffma2_rn(n1r, x, rp[p]));
                         ip[p] = __ffma2_rn(n2i, y, __ffma2_rn(n1i, x, ip[p]));
-                        if constexpr (FUSED)
-                            kacc_pair(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+                        kacc_pair(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
                     }
                 }
                 if (exs[s]) {
@@ -398,16 +396,8 @@ __global__ void __launch_bounds__(128, VAR == 0 ? 3 : 2) k2v2r_kernel(K2Args a) 
                         xr[s] = fmaf(-s2 * fr, y, xr[s]);
                         xi[s] = fmaf(s2 * fi, y, xi[s]);
                     }
-                    if constexpr (FUSED) kacc_one(A[ACC], fmaf(xi[s], xi[s], xr[s] * xr[s]), NP + s, kmask);
+                    kacc_one(A[ACC], fmaf(xi[s], xi[s], xr[s] * xr[s]), NP + s, kmask);
                 }
-            }
-            if constexpr (!FUSED) {
-#pragma unroll
-                for (int p = 0; p < NP; ++p)
-                    kacc_pair(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
-#pragma unroll
-                for (int s = 0; s < SPT; ++s)
-                    if (exs[s]) kacc_one(A[ACC], fmaf(xi[s], xi[s], xr[s] * xr[s]), NP + s, kmask);
             }
         }
 
@@ -904,9 +894,7 @@ static int v2r_variant() {
 template <int T, int PATH>
 static int k2v2_launch_t(const K2Args& a, int32_t ntiles, cudaStream_t s) {
     using Cf = V2Cfg<T, PATH>;
-    auto* fn = PATH == PATH_F32_REAL ? (v2r_variant() == 1   ? k2v2r_kernel<T, 1>
-                                        : v2r_variant() == 2 ? k2v2r_kernel<T, 2>
-                                        : v2r_variant() == 3 ? k2v2r_kernel<T, 3>
+    auto* fn = PATH == PATH_F32_REAL ? (v2r_variant() == 3   ? k2v2r_kernel<T, 3>
                                         : v2r_variant() == 9 ? k2v2r_kernel<T, 9>
                                                              : k2v2r_kernel<T, 0>)
                                      : k2v2c_kernel<T>;
