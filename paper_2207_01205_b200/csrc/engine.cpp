@@ -597,12 +597,15 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
     const bool use_d = d_supported(T) && !f64_strict_forced();  // K2d for symmetric masks
     auto path_of = [&](int cls) {
         const bool sy = sym[static_cast<size_t>(cls)] != 0;
-        if (!fp32) return (sy && use_d) ? (int)PATH_F64_REAL : (int)PATH_F64_STRICT;
+        if (!fp32) return !use_d ? (int)PATH_F64_STRICT : sy ? (int)PATH_F64_REAL : (int)PATH_F64_CPLX;
         return sy ? (int)PATH_F32_REAL : (int)PATH_F32_COMPLEX;
     };
-    // the fp64 kernel serving a range (fp64 mode, the fp32 mode's head and re-runs)
+    // the fp64 kernel serving a range (fp64 mode, the fp32 mode's head and re-runs):
+    // K2d (symmetric masks) / K2dc (asymmetric) for T <= 64, else the strict kernel
     auto hi_path = [&](int p) {
-        return (use_d && (p == PATH_F32_REAL || p == PATH_F64_REAL)) ? (int)PATH_F64_REAL : (int)PATH_F64_STRICT;
+        if (!use_d) return (int)PATH_F64_STRICT;
+        if (p == PATH_F32_REAL || p == PATH_F64_REAL) return (int)PATH_F64_REAL;
+        return (int)PATH_F64_CPLX;
     };
 
     const auto twf = twiddles(T, -1), twi = twiddles(T, +1);
@@ -656,11 +659,13 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
     if (job.order_key != sort_key || job.ids.size() != static_cast<size_t>(n)) {
         std::vector<int> cls_path(static_cast<size_t>(ncls));
         for (int c = 0; c < ncls; ++c) cls_path[static_cast<size_t>(c)] = path_of(c);
-        const int nkeys = job.groups * 4 * ncls;  // frame group, then path (< 4), then class
+        constexpr int NPATH = 8;  // IterPath values (< NPATH)
+        static_assert(PATH_F64_CPLX < NPATH, "path key space");
+        const int nkeys = job.groups * NPATH * ncls;  // frame group, then path, then class
         std::vector<int64_t> cnt(static_cast<size_t>(nkeys) + 1, 0);
         auto key_of = [&](int32_t b) {
             const BlockDesc& d = job.blocks[static_cast<size_t>(b)];
-            return (job.group_of(d) * 4 + cls_path[static_cast<size_t>(d.cls)]) * ncls + d.cls;
+            return (job.group_of(d) * NPATH + cls_path[static_cast<size_t>(d.cls)]) * ncls + d.cls;
         };
         for (int64_t i = 0; i < n; ++i) ++cnt[static_cast<size_t>(key_of(static_cast<int32_t>(i))) + 1];
         for (int k = 0; k < nkeys; ++k) cnt[static_cast<size_t>(k) + 1] += cnt[static_cast<size_t>(k)];
@@ -786,7 +791,8 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
     // one fp64 iteration launch over positions [b0, b1) of `descs` (K2d or strict)
     auto k2_f64 = [&](K2Args a, int hp, int64_t b0, int64_t b1, const std::vector<BlockDesc>& descs,
                       const std::string& tag, cudaStream_t s) {
-        const int ng = hp == PATH_F64_REAL ? k2d_blocks_per_cta(T) : k2_groups_per_cta(T, PATH_F64_STRICT);
+        const bool fast = hp == PATH_F64_REAL || hp == PATH_F64_CPLX;
+        const int ng = fast ? k2d_blocks_per_cta(T) : k2_groups_per_cta(T, PATH_F64_STRICT);
         std::vector<Tile> tl = make_tiles(b0, b1, descs, ng);
         Tile* d_tl = upload(ctx, "tiles64" + tag, tl.data(), tl.size(), s);
         a.path = hp;
@@ -795,7 +801,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         a.tiles = d_tl;
         a.wimg = hp == PATH_F64_REAL ? (const void*)d_vimg64 : (const void*)d_wimg64;
         a.wimg_stride = hp == PATH_F64_REAL ? static_cast<int64_t>(vimg64_elems) : static_cast<int64_t>(T) * sr64;
-        if (hp == PATH_F64_REAL)
+        if (fast)
             ck(k2d_launch(a, static_cast<int32_t>(tl.size()), s), "K2d fp64");
         else
             ck(k2_launch(a, static_cast<int32_t>(tl.size()), s), "K2 fp64");

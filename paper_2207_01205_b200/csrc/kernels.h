@@ -25,8 +25,11 @@ enum IterPath : int {
     PATH_F32_COMPLEX = 1, // complex W (asymmetric window masks)
     PATH_F32_REAL = 2,    // point-symmetric masks: rotated frame, real V
     PATH_F64_REAL = 3,    // fp64 rotated frame, real V (K2d; T <= 64)
+    PATH_F64_CPLX = 4,    // fp64 complex W, block-group kernel (K2dc; T <= 64)
 };
-__host__ __device__ inline bool path_is_f64(int p) { return p == PATH_F64_STRICT || p == PATH_F64_REAL; }
+__host__ __device__ inline bool path_is_f64(int p) {
+    return p == PATH_F64_STRICT || p == PATH_F64_REAL || p == PATH_F64_CPLX;
+}
 __host__ __device__ inline bool path_is_rotated(int p) { return p == PATH_F32_REAL || p == PATH_F64_REAL; }
 
 enum SrcType : int { SRC_U8 = 0, SRC_F64 = 1 };

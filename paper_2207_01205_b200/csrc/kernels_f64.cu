@@ -364,6 +364,251 @@ __global__ void __launch_bounds__(256, 2) k2d_kernel(K2Args a) {
     }
 }
 
+// ============================================================================
+// K2dc: the same fp64 block-group kernel for ASYMMETRIC window masks (image
+// borders, lost neighbours): no rotated frame, complex W gathers (one 16-byte
+// LDS per bin and term, 8 DFMA per bin), the reference's update
+// R[k] -= c W[k-u] + conj(c) W[k+u] and energy bookkeeping with W[2u]
+// (engine_spectral.cpp:98-125). Replaces the strict kernel for the fp32 mode's
+// border heads / re-runs and fp64 border blocks (the strict kernel stays the
+// bit-exact engine-level path).
+// ============================================================================
+template <int T>
+struct DCCfg {
+    static constexpr int SEG = seg_for(T, 1);
+    static constexpr int HT = T / 2;
+    static constexpr int QN = T / SEG;
+    static constexpr int NT = HT * QN;
+    static constexpr int GT = NT < 32 ? 32 : NT;
+    static constexpr int NW = GT / 32;
+    static constexpr int SR = T + SEG + 1;  // complex W row stride (the class-image layout of K1)
+    static constexpr int GROUPS = 256 / GT;
+    static constexpr bool REAL = false;
+    static constexpr size_t IMG_BYTES = (size_t)T * SR * sizeof(double2);
+    static constexpr bool TW64 = true;
+    static constexpr bool P32 = false;
+    static constexpr size_t WBYTES = ((IMG_BYTES + 15) / 16) * 16;
+    static constexpr size_t OFF_P = WBYTES;
+    static constexpr size_t OFF_TW = OFF_P + sizeof(double2) * 2 * T;
+    static constexpr size_t GRP = ((2 * NW * 32 + 2 * NW * 16 + 8 * NW + 15) / 16) * 16;
+    static constexpr size_t OFF_G = OFF_TW + sizeof(double2) * T;
+    static constexpr size_t OFF_BAR = OFF_G + GRP * GROUPS;
+    static constexpr size_t SMEM = OFF_BAR + 16;
+    static_assert(T * T <= 4096, "key index bits");
+};
+
+template <int T, bool FOD>
+__global__ void __launch_bounds__(256, 2) k2dc_kernel(K2Args a) {
+    using Cf = DCCfg<T>;
+    constexpr int SEG = Cf::SEG, NT = Cf::NT, GT = Cf::GT, NW = Cf::NW, SR = Cf::SR;
+    constexpr int NB = SEG + 1;
+
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const Tile tile = a.tiles[blockIdx.x];
+    v2_stage<Cf>(a, tile, smem_raw);
+    const double2* wimg = reinterpret_cast<const double2*>(smem_raw);
+    const double2* twi = reinterpret_cast<const double2*>(smem_raw + Cf::OFF_TW);
+
+    const int grp = threadIdx.x / GT, ltid = threadIdx.x % GT;
+    const int w = ltid >> 5;
+    const bool active = ltid < NT;
+    unsigned char* gsm = smem_raw + Cf::OFF_G + Cf::GRP * grp;
+    DSlot* slots = reinterpret_cast<DSlot*>(gsm);
+    double2* dred = reinterpret_cast<double2*>(gsm + 2 * NW * 32);
+    double* red = reinterpret_cast<double*>(gsm + 2 * NW * 32 + 2 * NW * 16);
+    const int bar = 1 + grp;
+
+    const BinLayout L = BinLayout::make(T, SEG, 1);
+    int k1 = 0, c0 = 0, ex = 0;
+    if (active) L.segment(ltid, &k1, &c0, &ex);
+    const int gbase = k1 * T + c0;
+    const bool selfbin0 = active && c0 == 0 && (k1 == 0 || k1 == T / 2);
+    const unsigned kbase = static_cast<unsigned>(DKEY_TOP - gbase);
+    const int rstride = a.rec_stride > 0 ? a.rec_stride : a.iterations;
+    const int tstride = a.trace_stride > 0 ? a.trace_stride : a.iterations;
+    const double w0 = a.w0[tile.cls], iw = 1.0 / w0;
+
+    for (int bi = grp; bi < tile.count; bi += Cf::GROUPS) {
+        const int pos = tile.begin + bi;
+        const int b = a.order[pos];
+        double re[NB], im[NB];
+        {
+            const double2* R = static_cast<const double2*>(a.rin) + (size_t)pos * L.SLOTS;
+#pragma unroll
+            for (int j = 0; j < SEG; ++j) {
+                const double2 v = active ? R[j * NT + ltid] : make_double2(0.0, 0.0);
+                re[j] = v.x;
+                im[j] = v.y;
+            }
+            const double2 v = (active && ex) ? R[SEG * NT + ltid] : make_double2(0.0, 0.0);
+            re[SEG] = v.x;
+            im[SEG] = v.y;
+        }
+        int* rec_u = a.rec_u_g + (size_t)b * rstride;
+        double2* rec_c = a.rec_c_g + (size_t)b * rstride;
+        double energy = a.energy0[pos];
+        const double e_init = a.init_energy[pos];
+        const double thr_e = 1e-12 * e_init;
+        const double thr_m = (1e-12 * a.init_max[pos]) * (1e-12 * a.init_max[pos]);
+        int nu = a.nu0 ? a.nu0[pos] : 0;
+        int ntrace = a.trace_from_nu0 ? nu : 0;
+        int conv = (a.conv0 ? a.conv0[pos] : 0) | (e_init <= 0.0);
+
+        unsigned long long KA = 0, KB = 0;
+#pragma unroll
+        for (int j = 0; j < SEG; ++j) dscan((j & 1) ? KB : KA, re[j], im[j], kbase - j);
+        if (ex) dscan(KA, re[SEG], im[SEG], kbase - SEG);
+
+        for (int it = 0; it < a.iterations && !conv; ++it) {
+            const int par = it & 1;
+            unsigned long long K = KA > KB ? KA : KB;
+            if (!active) K = 0;
+            const unsigned hi = static_cast<unsigned>(K >> 32), lo = static_cast<unsigned>(K);
+            const unsigned Mhi = __reduce_max_sync(0xffffffffu, hi);
+            const unsigned Mlo = __reduce_max_sync(0xffffffffu, hi == Mhi ? lo : 0u);
+            if (hi == Mhi && lo == Mlo) {
+                const int g = DKEY_TOP - static_cast<int>(Mlo & 0xFFFu);
+                const double2 pre = dpick<NB>(g - gbase, re, im);
+                slots[par * NW + w] = DSlot{Mhi, Mlo, g, 0, pre.x, pre.y};
+            }
+            if constexpr (NW == 1)
+                __syncwarp();
+            else
+                named_bar_sync(bar, GT);
+            DSlot s = slots[par * NW];
+#pragma unroll
+            for (int k = 1; k < NW; ++k) {
+                const DSlot o = slots[par * NW + k];
+                if (o.hi > s.hi || (o.hi == s.hi && o.lo > s.lo)) s = o;
+            }
+            const double pr = s.pre_re, pi = s.pre_im;
+            const double M = fma(pi, pi, pr * pr);
+            if (energy < thr_e || !(M > 0.0) || M < thr_m) {
+                conv = 1;
+                break;
+            }
+            const int G = s.g;
+            const int u1 = G / T, u2 = G % T;
+            const int self = ((T - u1) % T == u1) && ((T - u2) % T == u2);
+            const double2* wa = wimg + ((k1 - u1) & (T - 1)) * SR + ((c0 - u2) & (T - 1));  // W[k-u]
+            const double2* wb = wimg + ((k1 + u1) & (T - 1)) * SR + ((c0 + u2) & (T - 1));  // W[k+u]
+            double geff = a.gamma;
+            int degen = 0;
+            if constexpr (FOD) {
+                // d = sum_l R[l] W[u-l] = sum_canonical R conj(W[l-u]) + conj(R) W[l+u]
+                double dr = 0.0, di = 0.0;
+                if (active) {
+#pragma unroll
+                    for (int j = 0; j < NB; ++j) {
+                        if (j == SEG && !ex) break;
+                        const double2 x = wa[j];
+                        dr = fma(re[j], x.x, fma(im[j], x.y, dr));
+                        di = fma(im[j], x.x, fma(-re[j], x.y, di));
+                        if (!(j == SEG || (j == 0 && selfbin0))) {
+                            const double2 y = wb[j];
+                            dr = fma(re[j], y.x, fma(im[j], y.y, dr));
+                            di = fma(re[j], y.y, fma(-im[j], y.x, di));
+                        }
+                    }
+                }
+#pragma unroll
+                for (int o = 16; o; o >>= 1) {
+                    dr += __shfl_xor_sync(0xffffffffu, dr, o);
+                    di += __shfl_xor_sync(0xffffffffu, di, o);
+                }
+                if (NW > 1) {
+                    if ((ltid & 31) == 0) dred[par * NW + w] = make_double2(dr, di);
+                    named_bar_sync(bar, GT);
+                    dr = 0.0;
+                    di = 0.0;
+#pragma unroll
+                    for (int k = 0; k < NW; ++k) {
+                        const double2 v = dred[par * NW + k];
+                        dr += v.x;
+                        di += v.y;
+                    }
+                }
+                const double ru = sqrt(M), dm = sqrt(fma(di, di, dr * dr));
+                if (dm < 1e-12 * (ru * w0)) {
+                    geff = 1.0;
+                    degen = 1;
+                } else {
+                    geff = fmin(ru * w0 / dm, 1.0);
+                }
+            }
+            // p = pre / w0, c = gamma_eff p (self: real), energy bookkeeping with W[2u]
+            const double p_re = pr * iw, p_im = pi * iw;
+            const double c_re = p_re * geff, c_im = self ? 0.0 : p_im * geff;
+            double delta;
+            if (self) {
+                delta = -2.0 * c_re * pr + c_re * c_re * w0;
+            } else {
+                const double2 w2 = wimg[((2 * u1) & (T - 1)) * SR + ((2 * u2) & (T - 1))];
+                const double cc_r = c_re * c_re - c_im * c_im, cc_i = 2.0 * c_re * c_im;
+                delta = -4.0 * (c_re * pr + c_im * pi) + 2.0 * (c_re * c_re + c_im * c_im) * w0 +
+                        2.0 * (cc_r * w2.x + cc_i * w2.y);  // Re(c^2 conj(W[2u]))
+            }
+            const double e = energy + delta;
+            energy = 0.0 < e ? e : 0.0;
+            nu += 1;
+            if (ltid == 0)
+                v2_record(a, b, nu, ntrace, rstride, tstride, rec_u, rec_c, u1, u2, self, p_re, p_im, c_re, c_im,
+                          energy, M, 0.0, geff, degen);
+            ntrace += 1;
+
+            // ---- R[k] -= c W[k-u] + conj(c) W[k+u] (engine_spectral.cpp:112-125), next scan ----
+            KA = 0;
+            KB = 0;
+#pragma unroll
+            for (int j = 0; j < NB; ++j) {
+                if (j == SEG && !ex) break;
+                const double2 x = wa[j];
+                double r = fma(-c_re, x.x, fma(c_im, x.y, re[j]));
+                double m = fma(-c_re, x.y, fma(-c_im, x.x, im[j]));
+                if (!self) {
+                    const double2 y = wb[j];
+                    r = fma(-c_re, y.x, fma(-c_im, y.y, r));
+                    m = fma(-c_re, y.y, fma(c_im, y.x, m));
+                }
+                re[j] = r;
+                im[j] = m;
+                if (j < SEG)
+                    dscan((j & 1) ? KB : KA, r, m, kbase - j);
+                else
+                    dscan(KA, r, m, kbase - SEG);
+            }
+        }
+
+        if (a.rout && active) {
+            double2* R = static_cast<double2*>(a.rout) + (size_t)pos * L.SLOTS;
+#pragma unroll
+            for (int j = 0; j < SEG; ++j) R[j * NT + ltid] = make_double2(re[j], im[j]);
+            if (ex) R[SEG * NT + ltid] = make_double2(re[SEG], im[SEG]);
+        }
+        if constexpr (NW == 1)
+            __syncwarp();
+        else
+            named_bar_sync(bar, GT);
+        v2_finish<T, GT, double2>(a, a.blocks[pos], pos, b, ltid, energy, nu, conv, 0, ntrace, rec_u, rec_c,
+                                  rstride, twi, red, bar);
+        if constexpr (NW == 1)
+            __syncwarp();
+        else
+            named_bar_sync(bar, GT);
+    }
+}
+
+template <int T>
+static int k2dc_t(const K2Args& a, int32_t ntiles, cudaStream_t s) {
+    using Cf = DCCfg<T>;
+    auto* fn = a.full_od ? k2dc_kernel<T, true> : k2dc_kernel<T, false>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
+    if (e != cudaSuccess) return e;
+    if (ntiles <= 0) return cudaSuccess;
+    fn<<<ntiles, Cf::GT * Cf::GROUPS, Cf::SMEM, s>>>(a);
+    return cudaGetLastError();
+}
+
 template <int T>
 static int k2d_t(const K2Args& a, int32_t ntiles, cudaStream_t s) {
     using Cf = DCfg<T>;
@@ -376,6 +621,15 @@ static int k2d_t(const K2Args& a, int32_t ntiles, cudaStream_t s) {
 }
 
 int k2d_launch(const K2Args& a, int32_t ntiles, cudaStream_t s) {
+    if (a.path == PATH_F64_CPLX) {
+        switch (a.T) {
+            case 8: return k2dc_t<8>(a, ntiles, s);
+            case 16: return k2dc_t<16>(a, ntiles, s);
+            case 32: return k2dc_t<32>(a, ntiles, s);
+            case 64: return k2dc_t<64>(a, ntiles, s);
+        }
+        return cudaErrorInvalidValue;
+    }
     switch (a.T) {
         case 8: return k2d_t<8>(a, ntiles, s);
         case 16: return k2d_t<16>(a, ntiles, s);
