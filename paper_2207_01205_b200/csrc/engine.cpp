@@ -632,6 +632,8 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
     float* d_vimg32 = fp32 ? ctx->buf("vimg32").as<float>(static_cast<size_t>(ncls) * vimg_elems) : nullptr;
     double* d_w0 = ctx->buf("w0").as<double>(static_cast<size_t>(ncls));
     const size_t vimg64_elems = 2 * static_cast<size_t>(T) * d_srv(T);
+    const size_t wpl_elems = 4 * static_cast<size_t>(T) * v2_srv(T);  // K2v2 complex planes
+    float* d_wpl32 = v2 ? ctx->buf("wpl32").as<float>(static_cast<size_t>(ncls) * wpl_elems) : nullptr;
     double* d_vimg64 = use_d ? ctx->buf("vimg64").as<double>(static_cast<size_t>(ncls) * vimg64_elems) : nullptr;
     {
         K1Args a{};
@@ -646,6 +648,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         a.vimg32 = d_vimg32;
         a.vpairs = v2 ? (vcopies == 4 ? 4 : 1) : 0;
         a.vimg64 = d_vimg64;
+        a.wplanar32 = d_wpl32;
         a.w0 = d_w0;
         a.twid = d_twf;
         ck(k1_launch(a, st), "K1 class spectra");
@@ -809,7 +812,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
     };
     // fp32 residuals: AoS float2 slots (complex path, T = 128) or, for the K2v2
     // real path, SoA bin pairs; one common per-block stride (floats)
-    auto soa_of = [&](int path) { return (v2 && path == PATH_F32_REAL) ? 1 : 0; };
+    auto soa_of = [&](int path) { return (v2 && (path == PATH_F32_REAL || path == PATH_F32_COMPLEX)) ? 1 : 0; };
     auto spt_of = [&](int path) { return (v2 && path == PATH_F32_REAL) ? v2_real_spt(T) : spt32; };
     const BinLayout L32r = BinLayout::make(T, seg32, spt_of(PATH_F32_REAL));
     const int64_t s32 = static_cast<int64_t>(std::max(packed32_floats(L32, 0), packed32_floats(L32r, soa_of(PATH_F32_REAL))));
@@ -964,8 +967,10 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             a.tiles = d_tl;
             a.rin = d_R32;
             a.rin_stride = v2 ? s32 : 0;
-            a.wimg = ch.path == PATH_F32_REAL ? (const void*)d_vimg32 : (const void*)d_wimg32;
-            a.wimg_stride = ch.path == PATH_F32_REAL ? static_cast<int64_t>(vimg_elems) : static_cast<int64_t>(T) * sr32;
+            a.wimg = ch.path == PATH_F32_REAL ? (const void*)d_vimg32 : v2 ? (const void*)d_wpl32 : (const void*)d_wimg32;
+            a.wimg_stride = ch.path == PATH_F32_REAL ? static_cast<int64_t>(vimg_elems)
+                            : v2                    ? static_cast<int64_t>(wpl_elems)
+                                                    : static_cast<int64_t>(T) * sr32;
             a.flags = d_flags;
             a.rec_global = 1;
             a.iterations = I - head;

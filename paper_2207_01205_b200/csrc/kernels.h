@@ -75,6 +75,7 @@ struct K1Args {
     float2* wimg32;            // [ncls][T*SR32] complex fp32 image
     float* vimg32;             // [ncls][T*SR32] rotated real image ([ncls][2][T*SRV] with vpairs)
     double* vimg64;            // [ncls][2][T*d_srv(T)] fp64 rotated real image, even/odd pairs (K2d)
+    float* wplanar32;          // [ncls][Re,Im][even,odd][T][v2_srv(T)] fp32 complex W planes (K2v2 complex)
     int32_t vpairs;            // K2v2 real V layout: 0 single, 1 even/odd pairs, 4 quads
     double* w0;                // [ncls]
     const double2* twid;       // e^{-j 2 pi k / T}, k < T

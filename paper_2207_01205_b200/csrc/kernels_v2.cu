@@ -703,22 +703,56 @@ __global__ void __launch_bounds__(256, 2) k2v2h_kernel(K2Args a) {
 
 // ============================================================================
 // Complex path: asymmetric window masks (image borders, neighbouring losses).
+// Same structure as the real path (one warp per block, SoA bin pairs, packed
+// keys fused into the update), but W is complex: held as four planes
+// (Re/Im x even/odd aligned copies) so every bin pair of each plane is one
+// LDS.64 and the complex multiply-subtracts are FFMA2 on pairs:
+// R[k] -= c W[k-u] + conj(c) W[k+u] (engine_spectral.cpp:112-125), 8 FFMA2
+// and 4 LDS.64 per bin pair.
 // ============================================================================
 template <int T>
+struct V2PCfg {
+    static constexpr int SEG = v2_seg(T);
+    static constexpr int SPT = v2_spt(T);
+    static constexpr int HT = T / 2;
+    static constexpr int QN = T / SEG;
+    static constexpr int NT = HT * QN / SPT;
+    static constexpr int NP = SPT * SEG / 2;
+    static constexpr int SRV = v2_srv(T);
+    static constexpr int WARPS = 4;
+    static constexpr bool REAL = false;
+    static constexpr size_t PLANE = (size_t)T * SRV;  // floats per plane
+    static constexpr size_t IMG_BYTES = 4 * PLANE * 4;
+    static constexpr bool TW64 = false;
+    static constexpr bool P32 = true;
+    static constexpr size_t WBYTES = ((IMG_BYTES + 15) / 16) * 16;
+    static constexpr size_t OFF_P = WBYTES;
+    static constexpr size_t OFF_TW = OFF_P + sizeof(double2) * 2 * T;
+    static constexpr size_t OFF_SP = OFF_TW + sizeof(float2) * T;
+    static constexpr size_t OFF_ST = OFF_SP + sizeof(float4) * WARPS * (NP + SPT + 1);
+    static constexpr size_t OFF_BAR = OFF_ST + 64 * WARPS;
+    static constexpr size_t SMEM = OFF_BAR + 16;
+    static_assert(NT <= 32, "one warp per block");
+};
+
+template <int T>
 __global__ void __launch_bounds__(128, 3) k2v2c_kernel(K2Args a) {
-    using Cf = V2Cfg<T, PATH_F32_COMPLEX>;
-    constexpr int SEG = Cf::SEG, SPT = Cf::SPT, NT = Cf::NT, NB = Cf::NB, SR = Cf::SR;
+    using Cf = V2PCfg<T>;
+    constexpr int SEG = Cf::SEG, SPT = Cf::SPT, NT = Cf::NT, NP = Cf::NP, SRV = Cf::SRV;
+    constexpr int PPS = SEG / 2;
+    constexpr size_t PL = Cf::PLANE;
+    constexpr int ACC = 2;
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const Tile tile = a.tiles[blockIdx.x];
     v2_stage<Cf>(a, tile, smem_raw);
-    const float2* wimg = reinterpret_cast<const float2*>(smem_raw);
+    const float* wre = reinterpret_cast<const float*>(smem_raw);  // [copy][T][SRV], copy c holds W[col + c]
+    const float* wim = wre + 2 * PL;
     const float2* twi = reinterpret_cast<const float2*>(smem_raw + Cf::OFF_TW);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool active = lane < NT;
-    float2* spill = reinterpret_cast<float2*>(reinterpret_cast<float4*>(smem_raw + Cf::OFF_SP) +
-                                              warp * (Cf::NP + SPT + 1));
+    float4* spill = reinterpret_cast<float4*>(smem_raw + Cf::OFF_SP) + warp * (NP + SPT + 1);
 
     const BinLayout L = BinLayout::make(T, SEG, SPT);
     int k1s[SPT], c0s[SPT], exs[SPT];
@@ -729,133 +763,200 @@ __global__ void __launch_bounds__(128, 3) k2v2c_kernel(K2Args a) {
     }
     const int gb0 = k1s[0] * T + c0s[0];
     const int gb1 = k1s[SPT - 1] * T + c0s[SPT - 1];
-    const double w0 = a.w0[tile.cls];
-    const double inv_w0 = 1.0 / w0;
+    const unsigned kmask = key_mask<false>(a);
+    V2State* st = reinterpret_cast<V2State*>(smem_raw + Cf::OFF_ST + 64 * warp);
     const int rstride = a.rec_stride > 0 ? a.rec_stride : a.iterations;
     const int tstride = a.trace_stride > 0 ? a.trace_stride : a.iterations;
 
     for (int bi = warp; bi < tile.count; bi += Cf::WARPS) {
         const int pos = tile.begin + bi;
         const int b = a.order[pos];
-        const BlockDesc desc = a.blocks[pos];
-
-        float2 r[NB];
+        float2 rp[NP], ip[NP];
+        float xr[SPT], xi[SPT];
         {
-            const size_t rs = a.rin_stride > 0 ? (size_t)a.rin_stride : (size_t)Cf::SLOTS * 2;
-            const float2* R = reinterpret_cast<const float2*>(static_cast<const float*>(a.rin) + (size_t)pos * rs);
+            const size_t rs = a.rin_stride > 0 ? (size_t)a.rin_stride : (size_t)(NP + SPT) * NT * 4;
+            const float4* R = reinterpret_cast<const float4*>(static_cast<const float*>(a.rin) + (size_t)pos * rs);
 #pragma unroll
-            for (int i = 0; i < NB; ++i) {
-                const int s = i / (SEG + 1), j = i % (SEG + 1);
-                const bool ok = active && (j < SEG || exs[s]);
-                r[i] = ok ? R[i * NT + lane] : make_float2(0.f, 0.f);
+            for (int p = 0; p < NP; ++p) {
+                const float4 u = active ? R[p * NT + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+                rp[p] = make_float2(u.x, u.y);
+                ip[p] = make_float2(u.z, u.w);
+            }
+#pragma unroll
+            for (int s = 0; s < SPT; ++s) {
+                const float4 u = active ? R[(NP + s) * NT + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+                xr[s] = u.x;
+                xi[s] = u.z;
             }
         }
-        int* rec_u = a.rec_u_g + (size_t)b * rstride;
-        double2* rec_c = a.rec_c_g + (size_t)b * rstride;
-
-        double energy = a.energy0[pos];
         const double e_init = a.init_energy[pos];
-        const double imax = a.init_max[pos];
-        int nu = a.nu0 ? a.nu0[pos] : 0;
-        int conv = a.conv0 ? a.conv0[pos] : 0;
+        if (lane == 0) {
+            const double im = 1e-12 * a.init_max[pos];
+            const double w0 = a.w0[tile.cls];
+            st->energy = a.energy0[pos];
+            st->thr_e = 1e-12 * e_init;
+            st->thr_m = (float)(im * im);
+            st->w0 = (float)w0;
+            st->gw = (float)(a.gamma / w0);
+            st->nu = a.nu0 ? a.nu0[pos] : 0;
+            st->ntrace = a.trace_from_nu0 ? st->nu : 0;
+        }
+        int conv = (a.conv0 ? a.conv0[pos] : 0) | (e_init <= 0.0);
         int flagged = 0;
-        int ntrace = a.trace_from_nu0 ? nu : 0;
+        __syncwarp();
+
+        KAcc A[ACC + 1];
+#pragma unroll
+        for (int k = 0; k <= ACC; ++k) A[k] = KAcc{0.f, 0.f};
+#pragma unroll
+        for (int p = 0; p < NP; ++p) kacc_pair(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+#pragma unroll
+        for (int s = 0; s < SPT; ++s)
+            if (exs[s]) kacc_one(A[ACC], fmaf(xi[s], xi[s], xr[s] * xr[s]), NP + s, kmask);
 
         for (int it = 0; it < a.iterations && !conv; ++it) {
-            float m1 = 0.f, m2 = 0.f;
-            int i1 = 0;
+            float bm1 = A[0].m1, bm2 = A[0].m2;
 #pragma unroll
-            for (int i = 0; i < NB; ++i) {
-                const int j = i % (SEG + 1);
-                if (j == SEG && !exs[i / (SEG + 1)]) continue;
-                const float m = fmaf(r[i].y, r[i].y, r[i].x * r[i].x);
-                m2 = fmaxf(m2, fminf(m, m1));
-                const bool gt = m > m1;
-                m1 = fmaxf(m1, m);
-                i1 = gt ? i : i1;
+            for (int k = 1; k <= ACC; ++k) {
+                bm2 = fmax3(bm2, A[k].m2, fminf(bm1, A[k].m1));
+                bm1 = fmaxf(bm1, A[k].m1);
             }
-            const unsigned M = __reduce_max_sync(0xffffffffu, fbits(m1));
-            const int s1 = i1 / (SEG + 1), j1 = i1 % (SEG + 1);
-            int g = INT_MAX;
-            if (active && fbits(m1) == M) g = ((SPT == 2 && s1 == 1) ? gb1 : gb0) + j1;
-            const unsigned G = __reduce_min_sync(0xffffffffu, static_cast<unsigned>(g));
-            const bool win = static_cast<unsigned>(g) == G;
-            const unsigned S = __reduce_max_sync(0xffffffffu, fbits(win ? m2 : m1));
-            const int wl = __ffs(__ballot_sync(0xffffffffu, win)) - 1;
-            const int iw = __shfl_sync(0xffffffffu, i1, wl);
+            const unsigned M = __reduce_max_sync(0xffffffffu, fbits(bm1));
+            const bool cand = fbits(bm1) == M;
+            const int wl = __ffs(__ballot_sync(0xffffffffu, cand)) - 1;
+            const unsigned S = __reduce_max_sync(0xffffffffu, fbits(lane == wl ? bm2 : bm1));
+            const int pw = 63 - static_cast<int>(M & 63u);
             __syncwarp();
-            if (lane == wl) {
-#pragma unroll
-                for (int i = 0; i < NB; ++i) spill[i] = r[i];
+            if (lane == wl) spill[0] = pick_pair<NP, SPT>(pw, rp, ip, xr, xi);
+            __syncwarp();
+            float2 pre;
+            int jw, sw;
+            {
+                const float4 q = spill[0];
+                if (pw < NP) {
+                    const float ma = fmaf(q.z, q.z, q.x * q.x), mb = fmaf(q.w, q.w, q.y * q.y);
+                    const int half = mb > ma ? 1 : 0;
+                    pre = half ? make_float2(q.y, q.w) : make_float2(q.x, q.z);
+                    sw = pw / PPS;
+                    jw = 2 * (pw % PPS) + half;
+                } else {
+                    pre = make_float2(q.x, q.z);
+                    sw = pw - NP;
+                    jw = SEG;
+                }
             }
-            __syncwarp();
-            const float2 pre = spill[iw];
+            const int G = __shfl_sync(0xffffffffu, (SPT == 2 && sw == 1) ? gb1 : gb0, wl) + jw;
 
-            const double Mf = (double)__uint_as_float(M), Sf = (double)__uint_as_float(S);
-            if (e_init <= 0.0 || energy < 1e-12 * e_init || !(Mf > 0.0) || sqrt(Mf) < 1e-12 * imax) {
+            // ---- scalar part of iterate (engine_spectral.cpp:58-110), fp32; energy in fp64 ----
+            const float Mf = __uint_as_float(M), Sf = __uint_as_float(S);
+            const double energy = st->energy;
+            const float w0 = st->w0, gw = st->gw;
+            if (energy < st->thr_e || !(Mf > 0.f) || Mf < st->thr_m) {
                 conv = 1;
                 break;
             }
-            if (a.tau > 0.0 && Sf > Mf * (1.0 - a.tau)) {
+            if (Sf > Mf * (float)(1.0 - a.tau)) {
                 flagged = 1;
                 break;
             }
-            const int u1 = static_cast<int>(G) / T, u2 = static_cast<int>(G) % T;
-            const int self = ((T - u1) % T == u1) && ((T - u2) % T == u2);
-            const double pr = pre.x, pi = pre.y;
-            const double p_re = pr * inv_w0, p_im = pi * inv_w0;
-            const double c_re = p_re * a.gamma, c_im = self ? 0.0 : p_im * a.gamma;
-            double delta;
+            const int u1 = G / T, u2 = G % T;
+            const int self = ((u1 & (T / 2 - 1)) == 0) && ((u2 & (T / 2 - 1)) == 0);
+            const float pr = pre.x, pi = pre.y;
+            const float c_re = pr * gw, c_im = self ? 0.f : pi * gw;  // c = gamma R[u] / w0
+            float delta;
             if (self) {
-                delta = -2.0 * c_re * pr + c_re * c_re * w0;
+                delta = c_re * (c_re * w0 - 2.f * pr);
             } else {
-                const float2 w2 = wimg[((2 * u1) & (T - 1)) * SR + ((2 * u2) & (T - 1))];
-                const double w2r = w2.x, w2i = -(double)w2.y;
-                const double cc_r = c_re * c_re - c_im * c_im, cc_i = 2.0 * c_re * c_im;
-                delta = -4.0 * (c_re * pr + c_im * pi) + 2.0 * (c_re * c_re + c_im * c_im) * w0 +
-                        2.0 * (cc_r * w2r - cc_i * w2i);
+                const int wi = ((2 * u1) & (T - 1)) * SRV + ((2 * u2) & (T - 1));
+                const float w2r = wre[wi], w2i = wim[wi];
+                const float cc_r = c_re * c_re - c_im * c_im, cc_i = 2.f * c_re * c_im;
+                delta = -4.f * (c_re * pr + c_im * pi) + 2.f * (c_re * c_re + c_im * c_im) * w0 +
+                        2.f * (cc_r * w2r + cc_i * w2i);
             }
-            const double e = energy + delta;
-            energy = 0.0 < e ? e : 0.0;
-            nu += 1;
-            if (lane == 0)
-                v2_record(a, b, nu, ntrace, rstride, tstride, rec_u, rec_c, u1, u2, self, p_re, p_im,
-                          c_re, c_im, energy, Mf, Sf);
-            ntrace += 1;
+            const double e = energy + (double)delta;
+            const double en = 0.0 < e ? e : 0.0;
+            const int nu = st->nu + 1;
+            __syncwarp();
+            if (lane == 0) {
+                if (nu - 1 < rstride) {
+                    a.rec_u_g[(size_t)b * rstride + nu - 1] = (u1 << 16) | u2;
+                    a.rec_c_g[(size_t)b * rstride + nu - 1] =
+                        self ? make_double2(c_re, 0.0) : make_double2(2.0 * c_re, 2.0 * c_im);
+                }
+                st->energy = en;
+                st->nu = nu;
+                st->ntrace += 1;
+                if (a.trace || a.gap_trace) {
+                    const float iw = 1.f / w0;
+                    v2_record(a, b, nu, st->ntrace - 1, 0, tstride, nullptr, nullptr, u1, u2, self, pr * iw, pi * iw,
+                              c_re, c_im, en, Mf, Sf);
+                }
+            }
 
-            const float cr = (float)c_re, ci = (float)c_im;
+            // ---- R[k] -= c W[k-u] + conj(c) W[k+u] on bin pairs (+ next scan) ----
+            const int par = u2 & 1;
+            const float* pre_re = wre + par * PL;  // odd copy holds W[c+1]
+            const float* pre_im = wim + par * PL;
+            const float2 ncr = make_float2(-c_re, -c_re), pci = make_float2(c_im, c_im), nci = make_float2(-c_im, -c_im);
+#pragma unroll
+            for (int k = 0; k <= ACC; ++k) A[k] = KAcc{0.f, 0.f};
 #pragma unroll
             for (int s = 0; s < SPT; ++s) {
                 const int k1 = k1s[s], c0 = c0s[s];
-                const float2* wa = wimg + ((k1 - u1) & (T - 1)) * SR + ((c0 - u2) & (T - 1));
-                const float2* wb = wimg + ((k1 + u1) & (T - 1)) * SR + ((c0 + u2) & (T - 1));
+                const int rA = (k1 - u1) & (T - 1), rB = (k1 + u1) & (T - 1);
+                const int cA = (c0 - u2) & (T - 1), cB = (c0 + u2) & (T - 1);
+                const float2* ar = reinterpret_cast<const float2*>(pre_re + rA * SRV + (cA - par));
+                const float2* ai = reinterpret_cast<const float2*>(pre_im + rA * SRV + (cA - par));
+                const float2* br = reinterpret_cast<const float2*>(pre_re + rB * SRV + (cB - par));
+                const float2* bi = reinterpret_cast<const float2*>(pre_im + rB * SRV + (cB - par));
+                if (self) {
 #pragma unroll
-                for (int j = 0; j <= SEG; ++j) {
-                    if (j == SEG && !exs[s]) break;
-                    float2 v = r[s * (SEG + 1) + j];
-                    const float2 x = wa[j];
-                    v.x = fmaf(-cr, x.x, fmaf(ci, x.y, v.x));
-                    v.y = fmaf(-cr, x.y, fmaf(-ci, x.x, v.y));
-                    if (!self) {
-                        const float2 y = wb[j];
-                        v.x = fmaf(-cr, y.x, fmaf(-ci, y.y, v.x));
-                        v.y = fmaf(-cr, y.y, fmaf(ci, y.x, v.y));
+                    for (int q = 0; q < PPS; ++q) {
+                        const int p = s * PPS + q;
+                        const float2 xr2 = ar[q], xi2 = ai[q];
+                        rp[p] = __ffma2_rn(ncr, xr2, __ffma2_rn(pci, xi2, rp[p]));
+                        ip[p] = __ffma2_rn(ncr, xi2, __ffma2_rn(nci, xr2, ip[p]));
+                        kacc_pair(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
                     }
-                    r[s * (SEG + 1) + j] = v;
+                } else {
+#pragma unroll
+                    for (int q = 0; q < PPS; ++q) {
+                        const int p = s * PPS + q;
+                        const float2 xr2 = ar[q], xi2 = ai[q], yr2 = br[q], yi2 = bi[q];
+                        rp[p] = __ffma2_rn(nci, yi2, __ffma2_rn(ncr, yr2, __ffma2_rn(pci, xi2, __ffma2_rn(ncr, xr2, rp[p]))));
+                        ip[p] = __ffma2_rn(pci, yr2, __ffma2_rn(ncr, yi2, __ffma2_rn(nci, xr2, __ffma2_rn(ncr, xi2, ip[p]))));
+                        kacc_pair(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+                    }
+                }
+                if (exs[s]) {
+                    const int ia = rA * SRV + cA + SEG, ib = rB * SRV + cB + SEG;
+                    const float x_r = wre[ia], x_i = wim[ia];
+                    float r = fmaf(-c_re, x_r, fmaf(c_im, x_i, xr[s]));
+                    float m = fmaf(-c_re, x_i, fmaf(-c_im, x_r, xi[s]));
+                    if (!self) {
+                        const float y_r = wre[ib], y_i = wim[ib];
+                        r = fmaf(-c_re, y_r, fmaf(-c_im, y_i, r));
+                        m = fmaf(-c_re, y_i, fmaf(c_im, y_r, m));
+                    }
+                    xr[s] = r;
+                    xi[s] = m;
+                    kacc_one(A[ACC], fmaf(m, m, r * r), NP + s, kmask);
                 }
             }
         }
 
-        if (a.rout) {
-            const size_t rs = a.rin_stride > 0 ? (size_t)a.rin_stride : (size_t)Cf::SLOTS * 2;
-            float2* R = reinterpret_cast<float2*>(static_cast<float*>(a.rout) + (size_t)pos * rs);
+        if (a.rout && active) {
+            const size_t rs = a.rin_stride > 0 ? (size_t)a.rin_stride : (size_t)(NP + SPT) * NT * 4;
+            float4* R = reinterpret_cast<float4*>(static_cast<float*>(a.rout) + (size_t)pos * rs);
 #pragma unroll
-            for (int i = 0; i < NB; ++i) {
-                const int s = i / (SEG + 1), j = i % (SEG + 1);
-                if (active && (j < SEG || exs[s])) R[i * NT + lane] = r[i];
-            }
+            for (int p = 0; p < NP; ++p) R[p * NT + lane] = make_float4(rp[p].x, rp[p].y, ip[p].x, ip[p].y);
+#pragma unroll
+            for (int s = 0; s < SPT; ++s) R[(NP + s) * NT + lane] = make_float4(xr[s], 0.f, xi[s], 0.f);
         }
-        v2_finish<T, 32>(a, desc, pos, b, lane, energy, nu, conv, flagged, ntrace, rec_u, rec_c, rstride, twi);
+        __syncwarp();
+        v2_finish<T, 32>(a, a.blocks[pos], pos, b, lane, st->energy, st->nu, conv, flagged, st->ntrace,
+                         a.rec_u_g + (size_t)b * rstride, a.rec_c_g + (size_t)b * rstride, rstride, twi);
+        __syncwarp();
     }
 }
 
@@ -893,18 +994,25 @@ static int v2r_variant() {
 
 template <int T, int PATH>
 static int k2v2_launch_t(const K2Args& a, int32_t ntiles, cudaStream_t s) {
-    using Cf = V2Cfg<T, PATH>;
-    auto* fn = PATH == PATH_F32_REAL ? (v2r_variant() == 3   ? k2v2r_kernel<T, 3>
-                                        : v2r_variant() == 9 ? k2v2r_kernel<T, 9>
-                                                             : k2v2r_kernel<T, 0>)
-                                     : k2v2c_kernel<T>;
-    const size_t smem = PATH == PATH_F32_REAL && (v2r_variant() == 3 || v2r_variant() == 9)
-                            ? V2Cfg<T, PATH, true>::SMEM : Cf::SMEM;
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    if (ntiles <= 0) return cudaSuccess;
-    fn<<<ntiles, 32 * Cf::WARPS, smem, s>>>(a);
-    return cudaGetLastError();
+    if constexpr (PATH == PATH_F32_COMPLEX) {
+        using Cf = V2PCfg<T>;
+        cudaError_t e = cudaFuncSetAttribute(k2v2c_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
+        if (e != cudaSuccess) return e;
+        if (ntiles <= 0) return cudaSuccess;
+        k2v2c_kernel<T><<<ntiles, 32 * Cf::WARPS, Cf::SMEM, s>>>(a);
+        return cudaGetLastError();
+    } else {
+        using Cf = V2Cfg<T, PATH>;
+        auto* fn = v2r_variant() == 3   ? k2v2r_kernel<T, 3>
+                   : v2r_variant() == 9 ? k2v2r_kernel<T, 9>
+                                        : k2v2r_kernel<T, 0>;
+        const size_t smem = (v2r_variant() == 3 || v2r_variant() == 9) ? V2Cfg<T, PATH, true>::SMEM : Cf::SMEM;
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        if (ntiles <= 0) return cudaSuccess;
+        fn<<<ntiles, 32 * Cf::WARPS, smem, s>>>(a);
+        return cudaGetLastError();
+    }
 }
 
 template <int T>
