@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--seed", type=int, default=2207)
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    # diagnostics only (not the BASELINE configuration): guard threshold / fp64 head overrides
+    ap.add_argument("--guard-tau", type=float, default=None)
+    ap.add_argument("--fp64-head", type=int, default=None)
     return ap.parse_args()
 
 
@@ -226,6 +229,10 @@ def main():
     L = capi.lib()
     prec = args.precision or wl.precision
     cfg = wl.config(prec)
+    if args.guard_tau is not None:
+        cfg.guard_tau = args.guard_tau
+    if args.fp64_head is not None:
+        cfg.fp64_head = args.fp64_head
     params = cfg.params()
 
     # ---- inputs for this rank (weak scaling: own frames per rank) ----

@@ -77,9 +77,20 @@ int guarded(F&& f) {
     }
 }
 
+// Host worker threads: the cores of the node shared among the local ranks
+// (torchrun sets LOCAL_WORLD_SIZE), or FOFSE_HOST_THREADS.
 unsigned host_threads() {
-    const unsigned n = std::thread::hardware_concurrency();
-    return n ? n : 1;
+    static const unsigned n = [] {
+        if (const char* e = std::getenv("FOFSE_HOST_THREADS")) return static_cast<unsigned>(std::max(1, std::atoi(e)));
+        unsigned hw = std::thread::hardware_concurrency();
+        hw = hw ? hw : 1;
+        if (const char* e = std::getenv("LOCAL_WORLD_SIZE")) {
+            const int lw = std::atoi(e);
+            if (lw > 1) hw = std::max(1u, hw / static_cast<unsigned>(lw));
+        }
+        return hw;
+    }();
+    return n;
 }
 
 template <class F>

@@ -14,7 +14,7 @@ import paper_2207_01205_b200 as P  # noqa: E402
 from paper_2207_01205_b200 import workloads as WL  # noqa: E402
 
 
-def main(frames=64, seed=9100, taus=(1e-5, 5e-6, 3e-6, 2e-6)):
+def main(frames=64, seed=9100, taus=(1e-5, 5e-6, 3e-6, 2e-6), head=-1):
     wl = WL.C4
     stats = {t: dict(reruns=0, maxerr=0.0, bad=0, dpsnr=0.0) for t in taus}
     nblocks = 0
@@ -30,6 +30,7 @@ def main(frames=64, seed=9100, taus=(1e-5, 5e-6, 3e-6, 2e-6)):
         for t in taus:
             cfg = wl.config("fp32")
             cfg.guard_tau = t
+            cfg.fp64_head = head
             o32 = P.conceal(img, pat, cfg)
             d = np.abs(o32.restored - o64.restored)
             s = stats[t]
@@ -41,10 +42,13 @@ def main(frames=64, seed=9100, taus=(1e-5, 5e-6, 3e-6, 2e-6)):
             s["dpsnr"] = max(s["dpsnr"], abs(o32.report.psnr_db - o64.report.psnr_db))
     for t in taus:
         s = stats[t]
-        print(f"tau={t:g}: blocks={nblocks} reruns={s['reruns']} ({100 * s['reruns'] / nblocks:.2f}%) "
+        print(f"head={head} tau={t:g}: blocks={nblocks} reruns={s['reruns']} ({100 * s['reruns'] / nblocks:.2f}%) "
               f"maxerr={s['maxerr']:.4f} blocks>0.5px={s['bad']} max|dPSNR|={s['dpsnr']:.5f} dB", flush=True)
     print(f"done {time.time() - t0:.1f}s")
 
 
 if __name__ == "__main__":
-    main(int(sys.argv[1]) if len(sys.argv) > 1 else 64)
+    frames = int(sys.argv[1]) if len(sys.argv) > 1 else 64
+    head = int(sys.argv[2]) if len(sys.argv) > 2 else -1
+    taus = tuple(float(x) for x in sys.argv[3].split(",")) if len(sys.argv) > 3 else (1e-5, 5e-6, 3e-6, 2e-6)
+    main(frames, head=head, taus=taus)
