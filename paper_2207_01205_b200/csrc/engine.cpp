@@ -605,18 +605,23 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
     const int head = fp32 ? resolve_head(cfg) : 0;
     out.head = head;
     const bool v2 = fp32 && v2_supported(T);
+    // the fp32 real path: K2v2 (T <= 64) or its multi-warp form K2v2h (T = 128)
+    const bool v2r = v2 || (fp32 && T == 128 && v2h128_enabled());
     const bool use_d = d_supported(T) && !f64_strict_forced();  // K2d for symmetric masks
     auto path_of = [&](int cls) {
         const bool sy = sym[static_cast<size_t>(cls)] != 0;
-        if (!fp32) return !use_d ? (int)PATH_F64_STRICT : sy ? (int)PATH_F64_REAL : (int)PATH_F64_CPLX;
+        if (!fp32)
+            return !use_d ? (int)PATH_F64_STRICT
+                   : sy   ? (int)PATH_F64_REAL
+                          : (dc_supported(T) ? (int)PATH_F64_CPLX : (int)PATH_F64_STRICT);
         return sy ? (int)PATH_F32_REAL : (int)PATH_F32_COMPLEX;
     };
     // the fp64 kernel serving a range (fp64 mode, the fp32 mode's head and re-runs):
-    // K2d (symmetric masks) / K2dc (asymmetric) for T <= 64, else the strict kernel
+    // K2d (symmetric masks, T <= 128) / K2dc (asymmetric, T <= 64), else the strict kernel
     auto hi_path = [&](int p) {
         if (!use_d) return (int)PATH_F64_STRICT;
         if (p == PATH_F32_REAL || p == PATH_F64_REAL) return (int)PATH_F64_REAL;
-        return (int)PATH_F64_CPLX;
+        return dc_supported(T) ? (int)PATH_F64_CPLX : (int)PATH_F64_STRICT;
     };
 
     const auto twf = twiddles(T, -1), twi = twiddles(T, +1);
@@ -636,13 +641,13 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
     // from seg_for(T, 0); K2v2 uses v2_seg(T) — equal for every T).
     double2* d_wimg64 = ctx->buf("wimg64").as<double2>(static_cast<size_t>(ncls) * T * sr64);
     float2* d_wimg32 = fp32 ? ctx->buf("wimg32").as<float2>(static_cast<size_t>(ncls) * T * sr32) : nullptr;
-    const int vcopies = v2 ? v2_real_copies(T) : 1;
-    const size_t vimg_elems = !v2 ? static_cast<size_t>(T) * sr32
+    const int vcopies = v2r ? v2_real_copies(T) : 1;
+    const size_t vimg_elems = !v2r ? static_cast<size_t>(T) * sr32
                               : vcopies == 4 ? 4 * static_cast<size_t>(T) * v2_srv4(T)
                                              : 2 * static_cast<size_t>(T) * v2_srv(T);
     float* d_vimg32 = fp32 ? ctx->buf("vimg32").as<float>(static_cast<size_t>(ncls) * vimg_elems) : nullptr;
     double* d_w0 = ctx->buf("w0").as<double>(static_cast<size_t>(ncls));
-    const size_t vimg64_elems = 2 * static_cast<size_t>(T) * d_srv(T);
+    const size_t vimg64_elems = static_cast<size_t>(d_ncopy(T)) * T * d_srv(T);
     const size_t wpl_elems = 4 * static_cast<size_t>(T) * v2_srv(T);  // K2v2 complex planes
     float* d_wpl32 = v2 ? ctx->buf("wpl32").as<float>(static_cast<size_t>(ncls) * wpl_elems) : nullptr;
     double* d_vimg64 = use_d ? ctx->buf("vimg64").as<double>(static_cast<size_t>(ncls) * vimg64_elems) : nullptr;
@@ -657,7 +662,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         a.wimg64 = d_wimg64;
         a.wimg32 = d_wimg32;
         a.vimg32 = d_vimg32;
-        a.vpairs = v2 ? (vcopies == 4 ? 4 : 1) : 0;
+        a.vpairs = v2r ? (vcopies == 4 ? 4 : 1) : 0;
         a.vimg64 = d_vimg64;
         a.wplanar32 = d_wpl32;
         a.w0 = d_w0;
@@ -823,8 +828,10 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
     };
     // fp32 residuals: AoS float2 slots (complex path, T = 128) or, for the K2v2
     // real path, SoA bin pairs; one common per-block stride (floats)
-    auto soa_of = [&](int path) { return (v2 && (path == PATH_F32_REAL || path == PATH_F32_COMPLEX)) ? 1 : 0; };
-    auto spt_of = [&](int path) { return (v2 && path == PATH_F32_REAL) ? v2_real_spt(T) : spt32; };
+    auto soa_of = [&](int path) {
+        return ((v2r && path == PATH_F32_REAL) || (v2 && path == PATH_F32_COMPLEX)) ? 1 : 0;
+    };
+    auto spt_of = [&](int path) { return (v2r && path == PATH_F32_REAL) ? v2_real_spt(T) : spt32; };
     const BinLayout L32r = BinLayout::make(T, seg32, spt_of(PATH_F32_REAL));
     const int64_t s32 = static_cast<int64_t>(std::max(packed32_floats(L32, 0), packed32_floats(L32r, soa_of(PATH_F32_REAL))));
     if (fp32) d_R32 = ctx->buf("R32").as<char>(static_cast<size_t>(n) * sizeof(float) * s32);
@@ -968,7 +975,8 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
                           soa_of(ch.path), s32, ch.s);
             }
             ck(cudaEventRecord(ctx->event(3 * ci + 1), ch.s), "event");
-            const int ng = v2 ? k2v2_warps_per_cta() : k2_groups_per_cta(T, ch.path);
+            const bool kv2 = ch.path == PATH_F32_REAL ? v2r : v2;  // K2v2 family, else K2
+            const int ng = kv2 ? k2v2_warps_per_cta(T) : k2_groups_per_cta(T, ch.path);
             std::vector<Tile> tl = tiles_for(ch.b0, ch.b1, ng);
             Tile* d_tl = upload(ctx, "tilesF" + tag, tl.data(), tl.size(), ch.s);
             K2Args a = base_args();
@@ -977,7 +985,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             a.tau = effective_tau(cfg, head);
             a.tiles = d_tl;
             a.rin = d_R32;
-            a.rin_stride = v2 ? s32 : 0;
+            a.rin_stride = s32;
             a.wimg = ch.path == PATH_F32_REAL ? (const void*)d_vimg32 : v2 ? (const void*)d_wpl32 : (const void*)d_wimg32;
             a.wimg_stride = ch.path == PATH_F32_REAL ? static_cast<int64_t>(vimg_elems)
                             : v2                    ? static_cast<int64_t>(wpl_elems)
@@ -991,7 +999,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
                 a.nu0 = d_nu;
                 a.conv0 = d_cvh;
             }
-            ck(v2 ? k2v2_launch(a, static_cast<int32_t>(tl.size()), ch.s)
+            ck(kv2 ? k2v2_launch(a, static_cast<int32_t>(tl.size()), ch.s)
                   : k2_launch(a, static_cast<int32_t>(tl.size()), ch.s),
                "K2 fp32");
             ++ctx->launches;

@@ -159,10 +159,11 @@ __global__ void __launch_bounds__(256) k1_kernel(K1Args a) {
             }
         }
         if (a.vimg64) {
-            // fp64 rotated real V, even / odd copies (K2d): E[c] = V[c], O[c] = V[c+1]
-            const int srv = d_srv(T);
-            double* o = a.vimg64 + (size_t)b * 2 * T * srv;
-            for (int i = threadIdx.x; i < 2 * T * srv; i += blockDim.x) {
+            // fp64 rotated real V (K2d): even / odd copies E[c] = V[c], O[c] = V[c+1]
+            // (T <= 64), one copy at T = 128
+            const int srv = d_srv(T), ncopy = d_ncopy(T);
+            double* o = a.vimg64 + (size_t)b * ncopy * T * srv;
+            for (int i = threadIdx.x; i < ncopy * T * srv; i += blockDim.x) {
                 const int cp = i / (T * srv), rem = i % (T * srv);
                 const int r = rem / srv, col = rem % srv + cp;
                 const int k2 = col % T;
@@ -375,7 +376,9 @@ __global__ void __launch_bounds__(K2Cfg<T, PATH>::THREADS) k2_kernel(K2Args a) {
         // ---- residual spectrum -> registers ----
         Real re[NB], im[NB];
         {
-            const R2* R = static_cast<const R2*>(a.rin) + (size_t)pos * Cf::SLOTS;
+            // rin_stride (floats, fp32 only): the fp32 buffer is shared with the K2v2 layout
+            const size_t rs = a.rin_stride > 0 ? (size_t)a.rin_stride * sizeof(float) / sizeof(R2) : (size_t)Cf::SLOTS;
+            const R2* R = static_cast<const R2*>(a.rin) + (size_t)pos * rs;
 #pragma unroll
             for (int j = 0; j < SEG; ++j) {
                 R2 v = {0, 0};

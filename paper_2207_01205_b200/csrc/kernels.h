@@ -74,7 +74,7 @@ struct K1Args {
     double2* wimg64;           // [ncls][T*SR64] complex fp64 image (SEG of fp64)
     float2* wimg32;            // [ncls][T*SR32] complex fp32 image
     float* vimg32;             // [ncls][T*SR32] rotated real image ([ncls][2][T*SRV] with vpairs)
-    double* vimg64;            // [ncls][2][T*d_srv(T)] fp64 rotated real image, even/odd pairs (K2d)
+    double* vimg64;            // [ncls][d_ncopy(T)][T*d_srv(T)] fp64 rotated real image (K2d)
     float* wplanar32;          // [ncls][Re,Im][even,odd][T][v2_srv(T)] fp32 complex W planes (K2v2 complex)
     int32_t vpairs;            // K2v2 real V layout: 0 single, 1 even/odd pairs, 4 quads
     double* w0;                // [ncls]
@@ -95,7 +95,7 @@ struct K2Args {
     const int32_t* order;
     const BlockDesc* blocks;
     const void* rin;            // packed residual (Real2 per slot)
-    int64_t rin_stride;         // K2v2: floats per block in rin/rout (0 = packed size)
+    int64_t rin_stride;         // fp32: floats per block in rin/rout (0 = packed size)
     void* rout;                 // optional: packed residual written back
     const void* wimg;           // W images of the path's precision
     int64_t wimg_stride;        // elements per class
@@ -164,7 +164,7 @@ int k2v2_launch(const K2Args& a, int32_t ntiles, cudaStream_t s);
 // K2d: fp64 rotated-frame iteration (PATH_F64_REAL), groups of d_group_threads(T).
 int k2d_launch(const K2Args& a, int32_t ntiles, cudaStream_t s);
 int k2d_blocks_per_cta(int T);
-int k2v2_warps_per_cta();
+int k2v2_warps_per_cta(int t);
 int cvt_launch(const CvtArgs& a, cudaStream_t s);
 
 // Row stride of W images and the SEG used by a path (same on host/device).

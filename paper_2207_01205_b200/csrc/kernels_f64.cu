@@ -39,9 +39,16 @@ struct DCfg {
     static constexpr int NW = GT / 32;
     static constexpr int PPS = SEG / 2;
     static constexpr int SRV = d_srv(T);
-    static constexpr int GROUPS = 256 / GT;  // lost blocks per CTA
+    static constexpr int NCOPY = d_ncopy(T);  // 2: even/odd pairs (T <= 64), 1: one copy (T = 128)
+    static constexpr int GROUPS = GT >= 256 ? 1 : 256 / GT;  // lost blocks per CTA
+    static constexpr int THREADS = GT * GROUPS;
+    static constexpr int MINB = THREADS >= 512 ? 1 : 2;     // CTAs per SM (launch bounds)
+    // argmax key: the low KBITS of |R'|^2 hold KTOP - G (G < T^2)
+    static constexpr int KBITS = T * T <= 4096 ? 12 : 14;
+    static constexpr unsigned KTOP = (1u << KBITS) - 1u;
+    static constexpr unsigned long long KMASK = ~0ull << KBITS;
     static constexpr bool REAL = true;
-    static constexpr size_t IMG_BYTES = (size_t)2 * T * SRV * sizeof(double);
+    static constexpr size_t IMG_BYTES = (size_t)NCOPY * T * SRV * sizeof(double);
     static constexpr bool TW64 = true;
     static constexpr bool P32 = false;
     static constexpr size_t WBYTES = ((IMG_BYTES + 15) / 16) * 16;
@@ -52,8 +59,9 @@ struct DCfg {
     static constexpr size_t OFF_G = OFF_TW + sizeof(double2) * T;
     static constexpr size_t OFF_BAR = OFF_G + GRP * GROUPS;
     static constexpr size_t SMEM = OFF_BAR + 16;
-    static_assert(T * T <= 4096, "key index bits");
+    static_assert(T * T <= (1 << KBITS), "key index bits");
     static_assert(SEG % 2 == 0 && SEG <= 16, "bin pairs");
+    static_assert(SMEM <= 227 * 1024, "shared memory");
 };
 
 struct DSlot {
@@ -66,9 +74,10 @@ static_assert(sizeof(DSlot) == 32, "slot");
 constexpr unsigned long long DKEY_MASK = 0xFFFFFFFFFFFFF000ull;
 constexpr int DKEY_TOP = 4095;
 
+template <unsigned long long MASK = DKEY_MASK>
 __device__ __forceinline__ void dscan(unsigned long long& K, double re, double im, unsigned kidx) {
     const double m = fma(im, im, re * re);
-    const unsigned long long key = (static_cast<unsigned long long>(__double_as_longlong(m)) & DKEY_MASK) | kidx;
+    const unsigned long long key = (static_cast<unsigned long long>(__double_as_longlong(m)) & MASK) | kidx;
     K = key > K ? key : K;
 }
 
@@ -90,10 +99,12 @@ __device__ __forceinline__ double2 dpick(int j, const double* re, const double* 
 }
 
 template <int T, bool FOD>
-__global__ void __launch_bounds__(256, 2) k2d_kernel(K2Args a) {
+__global__ void __launch_bounds__(DCfg<T>::THREADS, DCfg<T>::MINB) k2d_kernel(K2Args a) {
     using Cf = DCfg<T>;
     constexpr int SEG = Cf::SEG, NT = Cf::NT, GT = Cf::GT, NW = Cf::NW, PPS = Cf::PPS, SRV = Cf::SRV;
     constexpr int NB = SEG + 1;
+    constexpr unsigned long long KM = Cf::KMASK;
+    constexpr int KTOP = static_cast<int>(Cf::KTOP);
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const Tile tile = a.tiles[blockIdx.x];
@@ -118,7 +129,7 @@ __global__ void __launch_bounds__(256, 2) k2d_kernel(K2Args a) {
     // self-conjugate canonical bins (0,0), (T/2,0) at slot 0 and the extra bins
     // (0,T/2), (T/2,T/2) have no partner in the full spectrum (OFSE reduction)
     const bool selfbin0 = active && c0 == 0 && (k1 == 0 || k1 == T / 2);
-    const unsigned kbase = static_cast<unsigned>(DKEY_TOP - gbase);
+    const unsigned kbase = static_cast<unsigned>(KTOP - gbase);
     const double sgn_r = ((a.Lh - 1) & 1) ? -1.0 : 1.0;
     const double sgn_c = ((a.Lw - 1) & 1) ? -1.0 : 1.0;
     const int rstride = a.rec_stride > 0 ? a.rec_stride : a.iterations;
@@ -153,8 +164,8 @@ __global__ void __launch_bounds__(256, 2) k2d_kernel(K2Args a) {
 
         unsigned long long KA = 0, KB = 0;  // two independent max chains
 #pragma unroll
-        for (int j = 0; j < SEG; ++j) dscan((j & 1) ? KB : KA, re[j], im[j], kbase - j);
-        if (ex) dscan(KA, re[SEG], im[SEG], kbase - SEG);
+        for (int j = 0; j < SEG; ++j) dscan<KM>((j & 1) ? KB : KA, re[j], im[j], kbase - j);
+        if (ex) dscan<KM>(KA, re[SEG], im[SEG], kbase - SEG);
 
         for (int it = 0; it < a.iterations && !conv; ++it) {
             const int par = it & 1;
@@ -165,7 +176,7 @@ __global__ void __launch_bounds__(256, 2) k2d_kernel(K2Args a) {
             const unsigned Mhi = __reduce_max_sync(0xffffffffu, hi);
             const unsigned Mlo = __reduce_max_sync(0xffffffffu, hi == Mhi ? lo : 0u);
             if (hi == Mhi && lo == Mlo) {
-                const int g = DKEY_TOP - static_cast<int>(Mlo & 0xFFFu);
+                const int g = KTOP - static_cast<int>(Mlo & Cf::KTOP);
                 const double2 pre = dpick<NB>(g - gbase, re, im);
                 slots[par * NW + w] = DSlot{Mhi, Mlo, g, 0, pre.x, pre.y};
             }
@@ -173,12 +184,19 @@ __global__ void __launch_bounds__(256, 2) k2d_kernel(K2Args a) {
                 __syncwarp();
             else
                 named_bar_sync(bar, GT);
-            DSlot s = slots[par * NW];
+            // group winner: compare the warps' keys (8-byte loads), then read its slot
+            int wb = 0;
+            {
+                uint2 kb = *reinterpret_cast<const uint2*>(&slots[par * NW]);
 #pragma unroll
-            for (int k = 1; k < NW; ++k) {
-                const DSlot o = slots[par * NW + k];
-                if (o.hi > s.hi || (o.hi == s.hi && o.lo > s.lo)) s = o;
+                for (int k = 1; k < NW; ++k) {
+                    const uint2 o = *reinterpret_cast<const uint2*>(&slots[par * NW + k]);
+                    const bool gt = o.x > kb.x || (o.x == kb.x && o.y > kb.y);
+                    kb = gt ? o : kb;
+                    wb = gt ? k : wb;
+                }
             }
+            const DSlot s = slots[par * NW + wb];
 
             // ---- scalar part of iterate (engine_spectral.cpp:58-110), every thread ----
             const double pr = s.pre_re, pi = s.pre_im;
@@ -192,14 +210,20 @@ __global__ void __launch_bounds__(256, 2) k2d_kernel(K2Args a) {
             const int self = ((T - u1) % T == u1) && ((T - u2) % T == u2);
             const double2 P = ptab[(u1 * (a.Lh - 1) + u2 * (a.Lw - 1)) & (2 * T - 1)];  // e^{-j phi(u)}
             // gathers of this selection: V[k-u] (sign s1) and V[k+u] (sign s2) per owned bin
-            const int p2 = u2 & 1;
-            const double* vimg = vE + p2 * (T * SRV);  // odd copy holds V[c+1]
+            // two copies: the odd copy holds V[c+1], so columns cA, cA+1 are one
+            // aligned 16-byte load; one copy (T = 128): two 8-byte loads
+            const int p2 = Cf::NCOPY == 2 ? (u2 & 1) : 0;
+            const double* vimg = vE + p2 * (T * SRV);
             const int rA = (k1 - u1) & (T - 1), rB = (k1 + u1) & (T - 1);
             const int cA = (c0 - u2) & (T - 1), cB = (c0 + u2) & (T - 1);
             const double s1 = ((k1 < u1) ? sgn_r : 1.0) * ((c0 < u2) ? sgn_c : 1.0);
             const double s2 = ((k1 + u1 >= T) ? sgn_r : 1.0) * ((c0 + u2 >= T) ? sgn_c : 1.0);
-            const double2* va = reinterpret_cast<const double2*>(vimg + rA * SRV + (cA - p2));
-            const double2* vb = reinterpret_cast<const double2*>(vimg + rB * SRV + (cB - p2));
+            const double* va = vimg + rA * SRV + (cA - p2);
+            const double* vb = vimg + rB * SRV + (cB - p2);
+            auto ld2 = [](const double* v, int q) {  // columns 2q, 2q+1 of the segment
+                if constexpr (Cf::NCOPY == 2) return reinterpret_cast<const double2*>(v)[q];
+                return make_double2(v[2 * q], v[2 * q + 1]);
+            };
             double gfac = gw, geff = a.gamma;
             int degen = 0;
             if constexpr (FOD) {
@@ -210,14 +234,14 @@ __global__ void __launch_bounds__(256, 2) k2d_kernel(K2Args a) {
                 if (active) {
 #pragma unroll
                     for (int q = 0; q < PPS; ++q) {
-                        const double2 x = va[q], y = vb[q];
+                        const double2 x = ld2(va, q), y = ld2(vb, q);
                         d1r = fma(x.x, re[2 * q], fma(x.y, re[2 * q + 1], d1r));
                         d1i = fma(x.x, im[2 * q], fma(x.y, im[2 * q + 1], d1i));
                         d2r = fma(y.x, re[2 * q], fma(y.y, re[2 * q + 1], d2r));
                         d2i = fma(-y.x, im[2 * q], fma(-y.y, im[2 * q + 1], d2i));
                     }
                     if (selfbin0) {
-                        const double y0 = vb[0].x;
+                        const double y0 = vb[0];
                         d2r = fma(-y0, re[0], d2r);
                         d2i = fma(y0, im[0], d2i);
                     }
@@ -288,24 +312,24 @@ __global__ void __launch_bounds__(256, 2) k2d_kernel(K2Args a) {
             if (self) {
 #pragma unroll
                 for (int q = 0; q < PPS; ++q) {
-                    const double2 x = va[q];
+                    const double2 x = ld2(va, q);
                     re[2 * q] = fma(n1r, x.x, re[2 * q]);
                     im[2 * q] = fma(n1i, x.x, im[2 * q]);
                     re[2 * q + 1] = fma(n1r, x.y, re[2 * q + 1]);
                     im[2 * q + 1] = fma(n1i, x.y, im[2 * q + 1]);
-                    dscan(KA, re[2 * q], im[2 * q], kbase - 2 * q);
-                    dscan(KB, re[2 * q + 1], im[2 * q + 1], kbase - 2 * q - 1);
+                    dscan<KM>(KA, re[2 * q], im[2 * q], kbase - 2 * q);
+                    dscan<KM>(KB, re[2 * q + 1], im[2 * q + 1], kbase - 2 * q - 1);
                 }
             } else {
 #pragma unroll
                 for (int q = 0; q < PPS; ++q) {
-                    const double2 x = va[q], y = vb[q];
+                    const double2 x = ld2(va, q), y = ld2(vb, q);
                     re[2 * q] = fma(n2r, y.x, fma(n1r, x.x, re[2 * q]));
                     im[2 * q] = fma(n2i, y.x, fma(n1i, x.x, im[2 * q]));
                     re[2 * q + 1] = fma(n2r, y.y, fma(n1r, x.y, re[2 * q + 1]));
                     im[2 * q + 1] = fma(n2i, y.y, fma(n1i, x.y, im[2 * q + 1]));
-                    dscan(KA, re[2 * q], im[2 * q], kbase - 2 * q);
-                    dscan(KB, re[2 * q + 1], im[2 * q + 1], kbase - 2 * q - 1);
+                    dscan<KM>(KA, re[2 * q], im[2 * q], kbase - 2 * q);
+                    dscan<KM>(KB, re[2 * q + 1], im[2 * q + 1], kbase - 2 * q - 1);
                 }
             }
             if (ex) {
@@ -317,7 +341,7 @@ __global__ void __launch_bounds__(256, 2) k2d_kernel(K2Args a) {
                     re[SEG] = fma(n2r, y, re[SEG]);
                     im[SEG] = fma(n2i, y, im[SEG]);
                 }
-                dscan(KA, re[SEG], im[SEG], kbase - SEG);
+                dscan<KM>(KA, re[SEG], im[SEG], kbase - SEG);
             }
         }
 
@@ -616,7 +640,7 @@ static int k2d_t(const K2Args& a, int32_t ntiles, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
     if (e != cudaSuccess) return e;
     if (ntiles <= 0) return cudaSuccess;
-    fn<<<ntiles, Cf::GT * Cf::GROUPS, Cf::SMEM, s>>>(a);
+    fn<<<ntiles, Cf::THREADS, Cf::SMEM, s>>>(a);
     return cudaGetLastError();
 }
 
@@ -635,6 +659,7 @@ int k2d_launch(const K2Args& a, int32_t ntiles, cudaStream_t s) {
         case 16: return k2d_t<16>(a, ntiles, s);
         case 32: return k2d_t<32>(a, ntiles, s);
         case 64: return k2d_t<64>(a, ntiles, s);
+        case 128: return k2d_t<128>(a, ntiles, s);
     }
     return cudaErrorInvalidValue;
 }
@@ -645,6 +670,7 @@ int k2d_blocks_per_cta(int T) {
         case 16: return DCfg<16>::GROUPS;
         case 32: return DCfg<32>::GROUPS;
         case 64: return DCfg<64>::GROUPS;
+        case 128: return DCfg<128>::GROUPS;
     }
     return 1;
 }

@@ -432,24 +432,31 @@ __global__ void __launch_bounds__(128, VAR == 0 ? 3 : 2) k2v2r_kernel(K2Args a) 
 template <int T>
 struct V2HCfg {
     static constexpr int SEG = 32, HT = T / 2, QN = T / SEG;
-    static constexpr int NT = HT * QN;  // 64 threads = 2 warps
+    static constexpr int NT = HT * QN;  // threads per lost block: 64 (T = 64) or 256 (T = 128)
+    static constexpr int GW = NT / 32;  // warps per lost block
     static constexpr int NP = SEG / 2, PPS = SEG / 2;
-    static constexpr int SRV = v2_srv4(T);
-    static constexpr int GROUPS = 4;  // lost blocks per CTA (256 threads)
+    // T = 64: quad V layout (one LDS.128 per two bin pairs), 4 blocks per CTA;
+    // T = 128: even/odd pairs (the quad image would not fit), 2 blocks per CTA
+    static constexpr int NCOPY = T == 64 ? 4 : 2;
+    static constexpr int SRV = NCOPY == 4 ? v2_srv4(T) : v2_srv(T);
+    static constexpr int GROUPS = T == 64 ? 4 : 2;  // lost blocks per CTA
+    static constexpr int THREADS = NT * GROUPS;
+    static constexpr int MINB = T == 64 ? 2 : 1;  // CTAs per SM (launch bounds)
     static constexpr bool REAL = true;
-    static constexpr size_t WELEMS = (size_t)4 * T * SRV;
+    static constexpr size_t WELEMS = (size_t)NCOPY * T * SRV;
     static constexpr size_t IMG_BYTES = WELEMS * 4;
     static constexpr bool TW64 = false;
     static constexpr bool P32 = true;
     static constexpr size_t WBYTES = ((IMG_BYTES + 15) / 16) * 16;
     static constexpr size_t OFF_P = WBYTES;
     static constexpr size_t OFF_TW = OFF_P + sizeof(double2) * 2 * T;
-    // per group: slots [2 parity][2 warps] x 32 B, red 2 doubles
-    static constexpr size_t GRP = 2 * 2 * 32 + 16;
+    // per group: slots [2 parity][GW warps] x 32 B, red GW doubles
+    static constexpr size_t GRP = 2 * GW * 32 + 8 * GW;
     static constexpr size_t OFF_G = OFF_TW + sizeof(float2) * T;
     static constexpr size_t OFF_BAR = OFF_G + GRP * GROUPS;
     static constexpr size_t SMEM = OFF_BAR + 16;
-    static_assert(NT == 64, "two warps per block");
+    static_assert(NT % 32 == 0 && GW >= 2 && GW <= 8, "whole warps per block");
+    static_assert(SMEM <= 227 * 1024, "shared memory");
 };
 
 struct HSlot {
@@ -462,9 +469,9 @@ struct HSlot {
 static_assert(sizeof(HSlot) == 32, "slot");
 
 template <int T>
-__global__ void __launch_bounds__(256, 2) k2v2h_kernel(K2Args a) {
+__global__ void __launch_bounds__(V2HCfg<T>::THREADS, V2HCfg<T>::MINB) k2v2h_kernel(K2Args a) {
     using Cf = V2HCfg<T>;
-    constexpr int SEG = Cf::SEG, NT = Cf::NT, NP = Cf::NP, PPS = Cf::PPS, SRV = Cf::SRV;
+    constexpr int SEG = Cf::SEG, NT = Cf::NT, NP = Cf::NP, PPS = Cf::PPS, SRV = Cf::SRV, GW = Cf::GW;
     constexpr int ACC = 2;
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -477,8 +484,8 @@ __global__ void __launch_bounds__(256, 2) k2v2h_kernel(K2Args a) {
     const int grp = threadIdx.x / NT, tid = threadIdx.x % NT;
     const int w = tid >> 5, lane = tid & 31;
     unsigned char* gsm = smem_raw + Cf::OFF_G + Cf::GRP * grp;
-    HSlot* slots = reinterpret_cast<HSlot*>(gsm);  // [2][2]
-    double* red = reinterpret_cast<double*>(gsm + 2 * 2 * 32);
+    HSlot* slots = reinterpret_cast<HSlot*>(gsm);  // [2 parity][GW]
+    double* red = reinterpret_cast<double*>(gsm + 2 * GW * 32);
     const int bar = 1 + grp;
 
     const BinLayout L = BinLayout::make(T, SEG, 1);
@@ -553,16 +560,25 @@ __global__ void __launch_bounds__(256, 2) k2v2h_kernel(K2Args a) {
             if (lane == wl) {
                 const int pw = 63 - static_cast<int>(Mw & 63u);
                 float xra[1] = {xr}, xia[1] = {xi};
-                slots[par * 2 + w] = HSlot{Mw, __uint_as_float(Sw), gb, 0, pick_pair<NP, 1>(pw, rp, ip, xra, xia)};
+                slots[par * GW + w] = HSlot{Mw, __uint_as_float(Sw), gb, 0, pick_pair<NP, 1>(pw, rp, ip, xra, xia)};
             }
             named_bar_sync(bar, NT);
-            const uint2 k0 = *reinterpret_cast<const uint2*>(&slots[par * 2]);
-            const uint2 k1v = *reinterpret_cast<const uint2*>(&slots[par * 2 + 1]);
-            const bool w1 = k1v.x > k0.x;  // ties across warps -> the guard (S == M) flags them
-            const HSlot& sw = slots[par * 2 + (w1 ? 1 : 0)];
-            const unsigned M = w1 ? k1v.x : k0.x;
+            // merge the GW warps: the winner is the largest key (keys are distinct
+            // unless tied, and a tie across warps leaves the runner-up equal to
+            // the maximum, which the guard flags); the runner-up is the larger of
+            // the winner's own runner-up and the other warps' best keys
+            unsigned M = 0u, S2 = 0u;
+            int wsel = 0;
+#pragma unroll
+            for (int v = 0; v < GW; ++v) {
+                const unsigned kv = reinterpret_cast<const uint2*>(&slots[par * GW + v])->x;
+                S2 = max(S2, min(kv, M));
+                wsel = kv > M ? v : wsel;
+                M = max(M, kv);
+            }
+            const HSlot& sw = slots[par * GW + wsel];
             const float Mf = __uint_as_float(M);
-            const float Sf = fmaxf(__uint_as_float(w1 ? k1v.y : k0.y), __uint_as_float(w1 ? k0.x : k1v.x));
+            const float Sf = fmaxf(sw.second, __uint_as_float(S2));
             const int pw = 63 - static_cast<int>(M & 63u);
             float2 pre;
             int jw;
@@ -634,9 +650,17 @@ __global__ void __launch_bounds__(256, 2) k2v2h_kernel(K2Args a) {
             const int cA = (c0 - u2) & (T - 1), cB = (c0 + u2) & (T - 1);
             const float s1f = ((k1 < u1) ? sgn_r : 1.f) * ((c0 < u2) ? sgn_c : 1.f);
             const float s2f = ((k1 + u1 >= T) ? sgn_r : 1.f) * ((c0 + u2 >= T) ? sgn_c : 1.f);
-            const int shA = cA & 3, shB = cB & 3;
-            const float4* qa = reinterpret_cast<const float4*>(vE + shA * (T * SRV) + rA * SRV + (cA - shA));
-            const float4* qb = reinterpret_cast<const float4*>(vE + shB * (T * SRV) + rB * SRV + (cB - shB));
+            // copy k of V holds V[c + k]: the segment starting at column cA is
+            // 16-byte (quad) / 8-byte (pair) aligned in copy cA mod NCOPY
+            constexpr int NC = Cf::NCOPY;
+            const int shA = cA & (NC - 1), shB = cB & (NC - 1);
+            const float* va = vE + shA * (T * SRV) + rA * SRV + (cA - shA);
+            const float* vb = vE + shB * (T * SRV) + rB * SRV + (cB - shB);
+            auto ld4 = [](const float* v, int q) {  // bins 4q .. 4q+3 of the segment
+                if constexpr (NC == 4) return reinterpret_cast<const float4*>(v)[q];
+                const float2 lo = reinterpret_cast<const float2*>(v)[2 * q], hi = reinterpret_cast<const float2*>(v)[2 * q + 1];
+                return make_float4(lo.x, lo.y, hi.x, hi.y);
+            };
             const float2 n1r = make_float2(-s1f * fr, -s1f * fr), n1i = make_float2(-s1f * fi, -s1f * fi);
             const float2 n2r = make_float2(-s2f * fr, -s2f * fr), n2i = make_float2(s2f * fi, s2f * fi);
 #pragma unroll
@@ -645,7 +669,7 @@ __global__ void __launch_bounds__(256, 2) k2v2h_kernel(K2Args a) {
 #pragma unroll
                 for (int q = 0; q < PPS / 2; ++q) {
                     const int p = 2 * q;
-                    const float4 x = qa[q];
+                    const float4 x = ld4(va, q);
                     rp[p] = __ffma2_rn(n1r, make_float2(x.x, x.y), rp[p]);
                     ip[p] = __ffma2_rn(n1i, make_float2(x.x, x.y), ip[p]);
                     rp[p + 1] = __ffma2_rn(n1r, make_float2(x.z, x.w), rp[p + 1]);
@@ -657,7 +681,7 @@ __global__ void __launch_bounds__(256, 2) k2v2h_kernel(K2Args a) {
 #pragma unroll
                 for (int q = 0; q < PPS / 2; ++q) {
                     const int p = 2 * q;
-                    const float4 x = qa[q], y = qb[q];
+                    const float4 x = ld4(va, q), y = ld4(vb, q);
                     rp[p] = __ffma2_rn(n2r, make_float2(y.x, y.y), __ffma2_rn(n1r, make_float2(x.x, x.y), rp[p]));
                     ip[p] = __ffma2_rn(n2i, make_float2(y.x, y.y), __ffma2_rn(n1i, make_float2(x.x, x.y), ip[p]));
                     rp[p + 1] = __ffma2_rn(n2r, make_float2(y.z, y.w), __ffma2_rn(n1r, make_float2(x.z, x.w), rp[p + 1]));
@@ -1027,7 +1051,8 @@ static int k2v2h_launch(const K2Args& a, int32_t ntiles, cudaStream_t s) {
 
 template <int T>
 static int k2v2_T(const K2Args& a, int32_t ntiles, cudaStream_t s) {
-    if (a.path == PATH_F32_REAL && v2_real_gw(T) == 2) return k2v2h_launch<64>(a, ntiles, s);
+    if constexpr (T == 64)
+        if (a.path == PATH_F32_REAL && v2_real_gw(T) == 2) return k2v2h_launch<64>(a, ntiles, s);
     if (a.path == PATH_F32_REAL) return k2v2_launch_t<T, PATH_F32_REAL>(a, ntiles, s);
     if (a.path == PATH_F32_COMPLEX) return k2v2_launch_t<T, PATH_F32_COMPLEX>(a, ntiles, s);
     return cudaErrorInvalidValue;
@@ -1039,15 +1064,27 @@ int k2v2_launch(const K2Args& a, int32_t ntiles, cudaStream_t s) {
         case 16: return k2v2_T<16>(a, ntiles, s);
         case 32: return k2v2_T<32>(a, ntiles, s);
         case 64: return k2v2_T<64>(a, ntiles, s);
+        case 128:  // the multi-warp real form only (complex W at T = 128 stays on K2)
+            return a.path == PATH_F32_REAL ? k2v2h_launch<128>(a, ntiles, s) : cudaErrorInvalidValue;
     }
     return cudaErrorInvalidValue;
 }
 
-int k2v2_warps_per_cta() { return 4; }  // lost blocks per CTA (both forms)
+int k2v2_warps_per_cta(int t) { return t == 128 ? V2HCfg<128>::GROUPS : 4; }  // lost blocks per CTA
 
 int v2_real_copies(int t) {
+    if (t == 128) return V2HCfg<128>::NCOPY;
     if (v2_real_gw(t) == 2) return 4;  // K2v2h: quad layout
     return (v2r_variant() == 3 || v2r_variant() == 9) ? 4 : 2;
+}
+
+bool v2h128_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = getenv("FOFSE_K2_128");
+        on = (e && e[0] == 'v' && e[1] == '1') ? 0 : 1;
+    }
+    return on != 0;
 }
 
 static int g_real_gw = -1;

@@ -133,12 +133,21 @@ int v2_real_gw(int t);
 inline int v2_real_spt(int t) { return v2_real_gw(t) == 2 ? 1 : v2_spt(t); }
 // Copies of V in the K2v2 real path's class image (2: even/odd pairs, 4: quads).
 int v2_real_copies(int t);
+// T = 128 fp32 real path on K2v2h (8 warps per lost block); FOFSE_K2_128=v1
+// keeps the older K2 kernel (experiments).
+bool v2h128_enabled();
 
 // K2d (fp64 rotated frame): the fp64 strict bin layout (SEG = seg_for(T, 1),
-// one segment per thread), V as two fp64 copies (even / odd aligned) with row
-// stride T + SEG + 2 so every bin pair is one aligned 16-byte load.
-FOFSE_HDC bool d_supported(int t) { return t >= 8 && t <= 64; }
-FOFSE_HDC int d_srv(int t) { return t + seg_for(t, 1) + 2; }
+// one segment per thread). T <= 64: V as two fp64 copies (even / odd aligned)
+// with row stride T + SEG + 2 so every bin pair is one aligned 16-byte load;
+// T = 128: one copy (two would not fit in shared memory) with an odd row stride
+// T + SEG + 1, so the 8-byte gathers of a warp's consecutive rows are
+// conflict free. K2dc (complex W, asymmetric masks) stops at T = 64: the fp64
+// complex image of T = 128 exceeds shared memory (the strict kernel serves it).
+FOFSE_HDC bool d_supported(int t) { return t >= 8 && t <= 128; }
+FOFSE_HDC bool dc_supported(int t) { return t >= 8 && t <= 64; }
+FOFSE_HDC int d_ncopy(int t) { return t <= 64 ? 2 : 1; }
+FOFSE_HDC int d_srv(int t) { return t <= 64 ? t + seg_for(t, 1) + 2 : t + seg_for(t, 1) + 1; }
 
 // Floats per block of a packed fp32 residual: AoS float2 slots, or the K2v2
 // SoA pair layout (float4 per bin pair + one float4 per segment extra bin).

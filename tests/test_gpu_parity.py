@@ -220,6 +220,41 @@ def test_conceal_fp64_k2d_matches_strict_full_C2(gpu, monkeypatch):
     assert np.abs(fast.restored - strict.restored).max() <= FP64_PX_TOL
 
 
+def _c5_crop(seed, size, nblocks, border=True):
+    wl = WL.C5
+    img = P.gen_image_u8(seed, size, size)
+    rects = P.gen_losses(seed, size // wl.block, size // wl.block, wl.loss_frac, wl.block, wl.block)
+    blocks = [tuple(map(int, (r["row"], r["col"], r["height"], r["width"]))) for r in rects][:nblocks]
+    if border:  # windows clipped by the image edge (asymmetric masks: the strict kernel at T = 128)
+        blocks += [(0, 0, 32, 32), (size - 32, 96, 32, 32)]
+    return img, P.LossPattern(size, size, wl.block, wl.block, [P.Rect(*b) for b in blocks])
+
+
+def test_conceal_fp64_T128_vs_oracle(gpu, orc):
+    """C5 blocks (32x32, T = 128, 300 iterations) in fp64: K2d at T = 128 (one
+    fp64 V copy, 16 warps per block, 14-bit key index) for interior windows and
+    the strict kernel for border windows give the oracle's selected-basis
+    sequence for every block, pixels within 1e-9."""
+    img, pat = _c5_crop(57, 768, 14)
+    cfg = WL.C5.config("fp64", record_traces=True)
+    out = P.conceal(img.astype(np.float64), pat, cfg)
+    ref = _oracle_conceal(orc, img, pat, cfg)
+    _assert_same_selections(out.report.traces, ref["traces"])
+    assert np.abs(out.restored - ref["restored"]).max() <= FP64_PX_TOL
+
+
+def test_conceal_fp64_T128_k2d_matches_strict(gpu, monkeypatch):
+    """160 C5 blocks: K2d (T = 128) vs the strict kernel — identical selections,
+    pixels within 1e-9."""
+    img, pat = _c5_crop(58, 2048, 160, border=False)
+    cfg = WL.C5.config("fp64", record_traces=True)
+    fast = P.conceal(img.astype(np.float64), pat, cfg)
+    monkeypatch.setenv("FOFSE_F64_KERNEL", "strict")
+    strict = P.conceal(img.astype(np.float64), pat, cfg)
+    _assert_same_selections(fast.report.traces, strict.report.traces)
+    assert np.abs(fast.restored - strict.restored).max() <= FP64_PX_TOL
+
+
 def test_k1_register_fft_matches_radix2(gpu, monkeypatch):
     """The T = 64 register radix-8x8 K1 vs the shared-memory radix-2 K1 (both fp64):
     identical selections on 600 C2 blocks (borders included), pixels within 1e-9."""
