@@ -278,6 +278,7 @@ def main():
 
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     k2_ms, init_ms, launches, reruns, real_ms, real_blocks, head = [], [], 0, 0, [], 0, 0
+    dev_total, e2e_total, e2e_wall = [], [], []
     barrier()
     with ClockSampler(local) as clk:
         ev0.record(stream)
@@ -285,6 +286,7 @@ def main():
             r = execute()
             k2_ms.append(r.iterate_ms)
             init_ms.append(r.init_ms)
+            dev_total.append(r.total_ms)
             real_ms.append(r.real_iterate_ms)
             real_blocks, head = r.real_blocks, r.fp64_head
             launches += r.kernel_launches
@@ -312,7 +314,10 @@ def main():
     barrier()
     ev0.record(stream)
     for _ in range(args.steps):
+        t0 = time.perf_counter()
         e2e_call()
+        e2e_wall.append((time.perf_counter() - t0) * 1e3)
+        e2e_total.append(rep.total_ms)
     ev1.record(stream)
     barrier()
     e2e_ms = ev0.elapsed_time(ev1) / args.steps
@@ -350,8 +355,10 @@ def main():
         except Exception:
             pass
         peak = peaks.get("smem_gbs")
-        kname = ("fofse::k2v2r_kernel<64> (fp32 rotated-frame iterate + fused synthesis)" if prec == "fp32"
-                 else "fofse::k2d_kernel<64> / k2_kernel (fp64 iterate + fused synthesis)")
+        T = wl.transform_size
+        k32 = f"fofse::k2v2h_kernel<{T}>" if T == 128 else f"fofse::k2v2r_kernel<{T}>"
+        kname = (f"{k32} (fp32 rotated-frame iterate + fused synthesis)" if prec == "fp32"
+                 else f"fofse::k2d_kernel<{T}> / k2_kernel (fp64 iterate + fused synthesis)")
         roof = {"bound": "smem", "kernel": kname,
                 "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if peak else None, "traffic": peaks.get("k2_dram_bytes"),
@@ -386,7 +393,11 @@ def main():
             "detail": {"k2_ms": k2_avg, "init_ms": statistics.mean(init_ms), "guard_reruns_per_step": reruns / args.steps,
                        "psnr_db": first.psnr_db if first else None, "e2e_psnr_db": e2e_psnr,
                        "classes": first.classes if first else None, "input_gen_s": gen_s,
-                       "real_blocks": real_blocks, "real_iterate_ms": real_avg, "fp64_head": head},
+                       "real_blocks": real_blocks, "real_iterate_ms": real_avg, "fp64_head": head,
+                       # library-side device span (first to last event of run_job) and host wall
+                       # time per e2e call: the gap is host preparation + transfers
+                       "device_total_ms": statistics.mean(dev_total), "e2e_device_total_ms": statistics.mean(e2e_total),
+                       "e2e_wall_ms": statistics.mean(e2e_wall)},
         }
         print(json.dumps(line), flush=True)
     L.fofse_plan_destroy(plan)

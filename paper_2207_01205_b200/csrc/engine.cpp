@@ -21,6 +21,7 @@
 #include <functional>
 #include <atomic>
 #include <chrono>
+#include <condition_variable>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -93,24 +94,92 @@ unsigned host_threads() {
     return n;
 }
 
+// Persistent host worker pool (created on first use, host_threads() - 1
+// workers): the plan-building passes (pattern validation, classification, the
+// block sort) run several short parallel loops per call, and spawning threads
+// for each would cost more than the loops themselves. One job at a time (a
+// mutex serialises concurrent callers); the calling thread works too.
+class HostPool {
+  public:
+    static HostPool& get() {
+        static HostPool pool(host_threads() > 1 ? host_threads() - 1 : 0);
+        return pool;
+    }
+    // fn(i) for i < n on up to `nt` threads (the caller included)
+    void run(int64_t n, int64_t nt, const std::function<void(int64_t)>& fn) {
+        std::lock_guard<std::mutex> serial(run_mu_);
+        const int64_t helpers = std::min<int64_t>(nt - 1, static_cast<int64_t>(workers_.size()));
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            fn_ = &fn;
+            n_ = n;
+            next_.store(0);
+            want_ = helpers;
+            active_ = helpers;
+            ++gen_;
+        }
+        cv_.notify_all();
+        work();
+        std::unique_lock<std::mutex> lk(mu_);
+        done_cv_.wait(lk, [&] { return active_ == 0; });
+        fn_ = nullptr;
+    }
+    ~HostPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+            ++gen_;
+        }
+        cv_.notify_all();
+        for (auto& t : workers_) t.join();
+    }
+
+  private:
+    explicit HostPool(unsigned nworkers) {
+        for (unsigned w = 0; w < nworkers; ++w) workers_.emplace_back([this, w] { loop(w); });
+    }
+    void work() {
+        for (;;) {
+            const int64_t i = next_.fetch_add(1);
+            if (i >= n_) return;
+            (*fn_)(i);
+        }
+    }
+    void loop(unsigned w) {
+        uint64_t seen = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return gen_ != seen; });
+                seen = gen_;
+                if (stop_) return;
+                if (static_cast<int64_t>(w) >= want_) continue;  // not needed for this job
+            }
+            work();
+            std::lock_guard<std::mutex> lk(mu_);
+            if (--active_ == 0) done_cv_.notify_one();
+        }
+    }
+    std::vector<std::thread> workers_;
+    std::mutex run_mu_, mu_;
+    std::condition_variable cv_, done_cv_;
+    const std::function<void(int64_t)>* fn_ = nullptr;
+    int64_t n_ = 0, want_ = 0, active_ = 0;
+    std::atomic<int64_t> next_{0};
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+};
+
+// fn(i) for i < n on up to host_threads() threads, at least `grain` items per thread
 template <class F>
-void parallel_for(int64_t n, F&& fn) {
-    const int64_t nt = std::min<int64_t>(host_threads(), std::max<int64_t>(1, n / 4));
+void parallel_for(int64_t n, F&& fn, int64_t grain = 4) {
+    const int64_t nt = std::min<int64_t>(host_threads(), std::max<int64_t>(1, n / std::max<int64_t>(grain, 1)));
     if (nt <= 1) {
         for (int64_t i = 0; i < n; ++i) fn(i);
         return;
     }
-    std::atomic<int64_t> next{0};
-    std::vector<std::thread> pool;
-    for (int64_t t = 0; t < nt; ++t)
-        pool.emplace_back([&] {
-            for (;;) {
-                const int64_t i = next.fetch_add(1);
-                if (i >= n) return;
-                fn(i);
-            }
-        });
-    for (auto& th : pool) th.join();
+    const std::function<void(int64_t)> f = [&](int64_t i) { fn(i); };
+    HostPool::get().run(n, nt, f);
 }
 
 // ---------------------------------------------------------------------------
@@ -154,6 +223,8 @@ struct fofse_ctx {
     std::map<std::string, DevBuf> bufs;
     cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     std::vector<cudaEvent_t> evpool;  // per-chunk events of the fp32 pipeline
+    // job storage of fofse_conceal_frames_u8, reused from call to call
+    std::unique_ptr<fofse_plan, void (*)(fofse_plan*)> frames_plan{nullptr, fofse_plan_destroy};
     int64_t launches = 0;
 
     // pinned staging for host -> device uploads (truly asynchronous copies);
@@ -176,7 +247,16 @@ struct fofse_ctx {
         }
         char* d = pin + pin_used;
         pin_used += need;
-        std::memcpy(d, src, bytes);
+        if (src) {  // (src == NULL: the caller fills the slot)
+            constexpr size_t piece = size_t(256) << 10;  // large uploads: memcpy in parallel pieces
+            if (bytes >= 4 * piece)
+                parallel_for(static_cast<int64_t>((bytes + piece - 1) / piece), [&](int64_t i) {
+                    const size_t o = static_cast<size_t>(i) * piece;
+                    std::memcpy(d + o, static_cast<const char*>(src) + o, std::min(piece, bytes - o));
+                }, 1);
+            else
+                std::memcpy(d, src, bytes);
+        }
         return d;
     }
 
@@ -380,12 +460,18 @@ struct Job {
     std::vector<double> wfull;
     // frame groups of the pipelined frames API (group-major execution order)
     int groups = 1;
-    int32_t nframes = 1;
+    std::vector<int32_t> frame_group;  // group of each frame (groups > 1)
     int group_of(const BlockDesc& d) const {
-        return groups > 1 ? static_cast<int>(static_cast<int64_t>(d.frame) * groups / nframes) : 0;
+        return groups > 1 ? frame_group[static_cast<size_t>(d.frame)] : 0;
     }
-    // cached execution order (run_job): caller ids by position and their descs
+    // cached execution order (run_job): caller ids by position and their descs,
+    // start positions of the (group, path, class) key runs
     int order_key = -1;
+    std::vector<int64_t> runs;
+    // plan-building scratch kept with the job (the frames API reuses its job
+    // across calls: no fresh allocations / page faults per call)
+    std::vector<CellGrid> grids;
+    std::vector<uint16_t> lid;
     std::vector<int32_t> ids;
     std::vector<BlockDesc> sorted;
 };
@@ -397,11 +483,30 @@ void classify_frames(Job& job, const fofse_rect* blocks, const int64_t* offs, in
     const Geometry& g = job.geo;
     const int64_t n = offs[nframes];
     job.blocks.resize(static_cast<size_t>(n));
-    std::vector<std::vector<int32_t>> keys(static_cast<size_t>(n));
-    std::vector<uint8_t> interior(static_cast<size_t>(n), 0);
-    parallel_for(nframes, [&](int64_t f) {
-        CellGrid& cg = grids[static_cast<size_t>(f)];
-        for (int64_t i = offs[f]; i < offs[f + 1]; ++i) {
+    // Work pieces of <= 2048 blocks of one frame. Each piece dedupes its class
+    // keys locally (first-appearance order; a window has few distinct keys), the
+    // serial pass interns only those, piece by piece — the same first-appearance
+    // class numbering as one scan in block order.
+    struct Piece {
+        int f;
+        int64_t i0, i1;
+        std::vector<std::vector<int32_t>> uniq;  // distinct keys of the piece, in order
+        std::vector<int32_t> gid;                // their global class ids
+    };
+    std::vector<Piece> pieces;
+    for (int f = 0; f < nframes; ++f)
+        for (int64_t i0 = offs[f]; i0 < offs[f + 1]; i0 += 2048)
+            pieces.push_back({f, i0, std::min<int64_t>(i0 + 2048, offs[f + 1]), {}, {}});
+    std::vector<uint16_t>& lid = job.lid;  // piece-local key index per block (< 2048)
+    lid.resize(static_cast<size_t>(n));
+    parallel_for(static_cast<int64_t>(pieces.size()), [&](int64_t pi) {
+        Piece& pc = pieces[static_cast<size_t>(pi)];
+        const int f = pc.f;
+        CellGrid& cg = grids[static_cast<size_t>(f)];  // read only (at() is not const)
+        int interior_lid = -1;
+        std::vector<std::array<int32_t, 4>> rects;
+        std::vector<int32_t> key;
+        for (int64_t i = pc.i0; i < pc.i1; ++i) {
             const fofse_rect& b = blocks[i];
             const int r0 = b.row - g.S, c0 = b.col - g.S;
             BlockDesc d;
@@ -412,9 +517,7 @@ void classify_frames(Job& job, const fofse_rect* blocks, const int64_t* offs, in
             job.blocks[static_cast<size_t>(i)] = d;
             const int top = std::max(0, -r0), left = std::max(0, -c0);
             const int bottom = std::max(0, r0 + g.Lh - H), right = std::max(0, c0 + g.Lw - W);
-            std::array<int32_t, 4> nbuf[64];  // neighbour rects inside the window (no heap for the common case)
-            int nnb = 0;
-            std::vector<std::array<int32_t, 4>> nbig;
+            rects.clear();
             const int cr0 = std::max(0, (std::max(r0, 0)) / g.bh - 1);
             const int cr1 = std::min(cg.gh - 1, (std::min(r0 + g.Lh, H) - 1) / g.bh);
             const int cc0 = std::max(0, (std::max(c0, 0)) / g.bw - 1);
@@ -427,42 +530,37 @@ void classify_frames(Job& job, const fofse_rect* blocks, const int64_t* offs, in
                     const int a0 = std::max(o.row - r0, 0), a1 = std::min(o.row + o.height - r0, g.Lh);
                     const int b0 = std::max(o.col - c0, 0), b1 = std::min(o.col + o.width - c0, g.Lw);
                     if (a0 >= a1 || b0 >= b1) continue;
-                    if (nnb < 64)
-                        nbuf[nnb++] = {a0, b0, a1, b1};
-                    else
-                        nbig.push_back({a0, b0, a1, b1});
+                    rects.push_back({a0, b0, a1, b1});
                 }
-            if (!top && !left && !bottom && !right && nnb == 0) {
-                interior[static_cast<size_t>(i)] = 1;
+            const bool interior = !top && !left && !bottom && !right && rects.empty();
+            if (interior && interior_lid >= 0) {  // the common case
+                lid[static_cast<size_t>(i)] = static_cast<uint16_t>(interior_lid);
                 continue;
             }
             // canonical order of the neighbour rects
-            std::vector<std::array<int32_t, 4>> rects(nbuf, nbuf + nnb);
-            rects.insert(rects.end(), nbig.begin(), nbig.end());
             std::sort(rects.begin(), rects.end());
-            std::vector<int32_t> key = {top, bottom, left, right, static_cast<int32_t>(rects.size())};
+            key.assign({top, bottom, left, right, static_cast<int32_t>(rects.size())});
             for (auto& r : rects) key.insert(key.end(), r.begin(), r.end());
-            keys[static_cast<size_t>(i)] = std::move(key);
+            size_t u = 0;
+            while (u < pc.uniq.size() && pc.uniq[u] != key) ++u;
+            if (u == pc.uniq.size()) pc.uniq.push_back(key);
+            if (interior) interior_lid = static_cast<int>(u);
+            lid[static_cast<size_t>(i)] = static_cast<uint16_t>(u);
         }
-    });
+    }, 1);
     ClassTable tab;
-    const std::vector<int32_t> interior_key = {0, 0, 0, 0, 0};
-    int32_t interior_id = -1;
-    for (int64_t i = 0; i < n; ++i) {
-        if (interior[static_cast<size_t>(i)] && interior_id >= 0) {  // the common case: no key at all
-            job.blocks[static_cast<size_t>(i)].cls = interior_id;
-            continue;
+    for (Piece& pc : pieces) {
+        pc.gid.resize(pc.uniq.size());
+        for (size_t u = 0; u < pc.uniq.size(); ++u) {
+            const std::vector<int32_t>& k = pc.uniq[u];
+            pc.gid[u] = tab.intern(std::vector<int32_t>(k), [&] { return labels_from_key(g, k); });
         }
-        std::vector<int32_t> key = interior[static_cast<size_t>(i)] ? interior_key
-                                                                    : std::move(keys[static_cast<size_t>(i)]);
-        int32_t id;
-        {
-            const std::vector<int32_t> kcopy = key;
-            id = tab.intern(std::move(key), [&] { return labels_from_key(g, kcopy); });
-            if (interior[static_cast<size_t>(i)]) interior_id = id;
-        }
-        job.blocks[static_cast<size_t>(i)].cls = id;
     }
+    parallel_for(static_cast<int64_t>(pieces.size()), [&](int64_t pi) {
+        const Piece& pc = pieces[static_cast<size_t>(pi)];
+        for (int64_t i = pc.i0; i < pc.i1; ++i)
+            job.blocks[static_cast<size_t>(i)].cls = pc.gid[lid[static_cast<size_t>(i)]];
+    }, 1);
     job.cls_labels = std::move(tab.labels);
 }
 
@@ -519,6 +617,7 @@ std::vector<Tile> make_tiles(int64_t begin, int64_t end, const std::vector<Block
     return tiles;
 }
 
+
 struct RunOut {
     double init_ms = 0, iter_ms = 0, total_ms = 0, rerun_ms = 0;
     double chunk_pre_ms = 0, chunk_iter_ms = 0, rerun_tail_ms = 0;  // fp32 pipeline
@@ -566,6 +665,11 @@ double effective_tau(const Cfg& c, int head) {
 // enqueued, on_done(g, s) enqueues its download on stream s after it.
 struct GroupIO {
     std::vector<cudaEvent_t> h2d_done;
+    // enqueue the uploads of groups <= g (once) and record their h2d_done events:
+    // called right before the first wait on h2d_done[g], so the small metadata
+    // copies of earlier groups are not queued behind the later groups' frames
+    // on the copy engine
+    std::function<void(int)> ensure_h2d;
     std::function<void(int, cudaStream_t)> on_done;
 };
 
@@ -681,19 +785,41 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         constexpr int NPATH = 8;  // IterPath values (< NPATH)
         static_assert(PATH_F64_CPLX < NPATH, "path key space");
         const int nkeys = job.groups * NPATH * ncls;  // frame group, then path, then class
-        std::vector<int64_t> cnt(static_cast<size_t>(nkeys) + 1, 0);
         auto key_of = [&](int32_t b) {
             const BlockDesc& d = job.blocks[static_cast<size_t>(b)];
             return (job.group_of(d) * NPATH + cls_path[static_cast<size_t>(d.cls)]) * ncls + d.cls;
         };
-        for (int64_t i = 0; i < n; ++i) ++cnt[static_cast<size_t>(key_of(static_cast<int32_t>(i))) + 1];
-        for (int k = 0; k < nkeys; ++k) cnt[static_cast<size_t>(k) + 1] += cnt[static_cast<size_t>(k)];
-        job.ids.assign(static_cast<size_t>(n), 0);
-        for (int64_t i = 0; i < n; ++i)
-            job.ids[static_cast<size_t>(cnt[static_cast<size_t>(key_of(static_cast<int32_t>(i)))]++)] =
-                static_cast<int32_t>(i);
+        // stable counting sort in P contiguous slices: per-slice histograms, a
+        // (key, slice)-major prefix, per-slice scatter (same order as one pass)
+        const int64_t P = std::clamp<int64_t>(n / 8192, 1, static_cast<int64_t>(host_threads()));
+        std::vector<int64_t> hist(static_cast<size_t>(P * nkeys), 0);
+        auto slice = [&](int64_t q) { return n * q / P; };
+        parallel_for(P, [&](int64_t q) {
+            int64_t* h = hist.data() + q * nkeys;
+            for (int64_t i = slice(q); i < slice(q + 1); ++i) ++h[key_of(static_cast<int32_t>(i))];
+        }, 1);
+        int64_t run = 0;
+        job.runs.clear();
+        for (int k = 0; k < nkeys; ++k) {
+            const int64_t k0 = run;
+            for (int64_t q = 0; q < P; ++q) {
+                int64_t& h = hist[static_cast<size_t>(q * nkeys + k)];
+                const int64_t c = h;
+                h = run;
+                run += c;
+            }
+            if (run > k0) job.runs.push_back(k0);
+        }
+        job.ids.resize(static_cast<size_t>(n));
         job.sorted.resize(static_cast<size_t>(n));
-        for (int64_t i = 0; i < n; ++i) job.sorted[static_cast<size_t>(i)] = job.blocks[job.ids[static_cast<size_t>(i)]];
+        parallel_for(P, [&](int64_t q) {
+            int64_t* h = hist.data() + q * nkeys;
+            for (int64_t i = slice(q); i < slice(q + 1); ++i) {
+                const int64_t pos = h[key_of(static_cast<int32_t>(i))]++;
+                job.ids[static_cast<size_t>(pos)] = static_cast<int32_t>(i);
+                job.sorted[static_cast<size_t>(pos)] = job.blocks[static_cast<size_t>(i)];
+            }
+        }, 1);
         job.order_key = sort_key;
     }
     const std::vector<int32_t>& ids = job.ids;
@@ -719,7 +845,10 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         if (r.path == PATH_F32_REAL || r.path == PATH_F64_REAL) out.real_blocks += r.end - r.begin;
     if (gio && !fp32)
         for (int gq = 0; gq < ngroups; ++gq)
+        {
+            gio->ensure_h2d(gq);
             ck(cudaStreamWaitEvent(st, gio->h2d_done[static_cast<size_t>(gq)], 0), "wait");
+        }
 
     const BinLayout L64 = BinLayout::make(T, seg64), L32 = BinLayout::make(T, seg32, spt32);
     double* d_e0 = ctx->buf("e0").as<double>(static_cast<size_t>(n));      // by position
@@ -793,9 +922,6 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         a.kmask = 0xffffffc0u;
         return a;
     };
-    auto tiles_for = [&](int64_t b0, int64_t b1, int ng) {
-        return make_tiles(b0, b1, sorted, ng);
-    };
 
     // ---- phase A: residual spectra ----
     char* d_R64 = nullptr;
@@ -808,12 +934,21 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
                       d_R64 + static_cast<size_t>(r.begin) * r64_bytes, d_e0 + r.begin, d_imax + r.begin);
     }
     // one fp64 iteration launch over positions [b0, b1) of `descs` (K2d or strict)
+    auto ng_f64 = [&](int hp) {
+        return (hp == PATH_F64_REAL || hp == PATH_F64_CPLX) ? k2d_blocks_per_cta(T) : k2_groups_per_cta(T, PATH_F64_STRICT);
+    };
+    // pre: tiles already on the device (the chunk pipeline uploads all of its tile
+    // lists in one copy up front)
     auto k2_f64 = [&](K2Args a, int hp, int64_t b0, int64_t b1, const std::vector<BlockDesc>& descs,
-                      const std::string& tag, cudaStream_t s) {
+                      const std::string& tag, cudaStream_t s, const Tile* pre = nullptr, size_t npre = 0) {
         const bool fast = hp == PATH_F64_REAL || hp == PATH_F64_CPLX;
-        const int ng = fast ? k2d_blocks_per_cta(T) : k2_groups_per_cta(T, PATH_F64_STRICT);
-        std::vector<Tile> tl = make_tiles(b0, b1, descs, ng);
-        Tile* d_tl = upload(ctx, "tiles64" + tag, tl.data(), tl.size(), s);
+        std::vector<Tile> tl;
+        const Tile* d_tl = pre;
+        if (!pre) {
+            tl = make_tiles(b0, b1, descs, ng_f64(hp));
+            d_tl = upload(ctx, "tiles64" + tag, tl.data(), tl.size(), s);
+            npre = tl.size();
+        }
         a.path = hp;
         a.seg = seg64;
         a.tau = 0.0;
@@ -821,9 +956,9 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         a.wimg = hp == PATH_F64_REAL ? (const void*)d_vimg64 : (const void*)d_wimg64;
         a.wimg_stride = hp == PATH_F64_REAL ? static_cast<int64_t>(vimg64_elems) : static_cast<int64_t>(T) * sr64;
         if (fast)
-            ck(k2d_launch(a, static_cast<int32_t>(tl.size()), s), "K2d fp64");
+            ck(k2d_launch(a, static_cast<int32_t>(npre), s), "K2d fp64");
         else
-            ck(k2_launch(a, static_cast<int32_t>(tl.size()), s), "K2 fp64");
+            ck(k2_launch(a, static_cast<int32_t>(npre), s), "K2 fp64");
         ++ctx->launches;
     };
     // fp32 residuals: AoS float2 slots (complex path, T = 128) or, for the K2v2
@@ -912,6 +1047,52 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
                 chunks.push_back({r.path, r.begin + len * c / nc, r.begin + len * (c + 1) / nc, on_side ? ctx->side : st,
                                   r.grp});
         }
+        // every tile list of the pipeline (heads, fp32 iterations) in one upload,
+        // queued ahead of the later frame groups' uploads on the copy engine
+        // tile lists [chunk][head, fp32 iteration] as class-run tables (one small
+        // upload, queued ahead of the later frame groups' uploads); the tiles
+        // themselves are cut on the device right before each launch
+        struct TList {
+            size_t r0 = 0, nr = 0, t0 = 0, nt = 0;
+            int ng = 1;
+        };
+        std::vector<TileRun> all_runs;
+        std::vector<TList> tls(2 * chunks.size());
+        size_t ntiles_all = 0;
+        for (size_t ci = 0; ci < chunks.size(); ++ci) {
+            const Chunk& ch = chunks[ci];
+            for (int k = 0; k < 2; ++k) {
+                if (k == 0 && head == 0) continue;
+                const bool kv2 = ch.path == PATH_F32_REAL ? v2r : v2;
+                const int ng = k == 0 ? ng_f64(hi_path(ch.path)) : kv2 ? k2v2_warps_per_cta(T) : k2_groups_per_cta(T, ch.path);
+                TList& tl = tls[2 * ci + static_cast<size_t>(k)];
+                tl.ng = ng;
+                tl.r0 = all_runs.size();
+                tl.t0 = ntiles_all;
+                size_t r = static_cast<size_t>(std::upper_bound(job.runs.begin(), job.runs.end(), ch.b0) - job.runs.begin());
+                int32_t nt = 0;
+                for (int64_t i = ch.b0; i < ch.b1; ++r) {
+                    const int64_t stop = std::min<int64_t>(ch.b1, r < job.runs.size() ? job.runs[r] : ch.b1);
+                    all_runs.push_back(TileRun{static_cast<int32_t>(i), static_cast<int32_t>(stop),
+                                               sorted[static_cast<size_t>(i)].cls, nt});
+                    nt += static_cast<int32_t>((stop - i + ng - 1) / ng);
+                    i = stop;
+                }
+                tl.nr = all_runs.size() - tl.r0;
+                tl.nt = static_cast<size_t>(nt);
+                ntiles_all += tl.nt;
+            }
+        }
+        const TileRun* d_runs = upload(ctx, "tile_runs", all_runs.data(), all_runs.size(), st);
+        Tile* d_all_tiles = ctx->buf("tiles_all").as<Tile>(std::max<size_t>(ntiles_all, 1));
+        auto cut_tiles = [&](size_t li, cudaStream_t s) {
+            const TList& tl = tls[li];
+            ck(tiles_launch(d_runs + tl.r0, static_cast<int32_t>(tl.nr), static_cast<int32_t>(tl.nt), tl.ng,
+                            d_all_tiles + tl.t0, s), "tiles");
+            ++ctx->launches;
+            return static_cast<const Tile*>(d_all_tiles + tl.t0);
+        };
+        hp_.mark("tile runs uploaded");
         ck(cudaEventRecord(ctx->ev[4], st), "event");
         ck(cudaStreamWaitEvent(ctx->side, ctx->ev[4], 0), "wait");
         ck(cudaStreamWaitEvent(ctx->aux, ctx->ev[4], 0), "wait");
@@ -923,7 +1104,10 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             const std::string tag = std::to_string(ci);
             if (gio) {
                 char& wt = waited[static_cast<size_t>(2 * ch.grp + (ch.s == st ? 0 : 1))];
-                if (!wt) ck(cudaStreamWaitEvent(ch.s, gio->h2d_done[static_cast<size_t>(ch.grp)], 0), "wait");
+                if (!wt) {
+                    gio->ensure_h2d(ch.grp);
+                    ck(cudaStreamWaitEvent(ch.s, gio->h2d_done[static_cast<size_t>(ch.grp)], 0), "wait");
+                }
                 wt = 1;
             }
             ck(cudaEventRecord(ctx->event(3 * ci + 0), ch.s), "event");
@@ -952,7 +1136,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
                     a.rout_spt = spt_of(ch.path);
                     a.rout_stride = s32;
                 }
-                k2_f64(a, hi_path(ch.path), ch.b0, ch.b1, sorted, "h" + tag, ch.s);
+                k2_f64(a, hi_path(ch.path), ch.b0, ch.b1, sorted, "h" + tag, ch.s, cut_tiles(2 * ci, ch.s), tls[2 * ci].nt);
                 if (!direct) {
                 CvtArgs c{};
                 c.T = T;
@@ -976,9 +1160,8 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             }
             ck(cudaEventRecord(ctx->event(3 * ci + 1), ch.s), "event");
             const bool kv2 = ch.path == PATH_F32_REAL ? v2r : v2;  // K2v2 family, else K2
-            const int ng = kv2 ? k2v2_warps_per_cta(T) : k2_groups_per_cta(T, ch.path);
-            std::vector<Tile> tl = tiles_for(ch.b0, ch.b1, ng);
-            Tile* d_tl = upload(ctx, "tilesF" + tag, tl.data(), tl.size(), ch.s);
+            const Tile* d_tl = cut_tiles(2 * ci + 1, ch.s);
+            const size_t ntl = tls[2 * ci + 1].nt;
             K2Args a = base_args();
             a.path = ch.path;
             a.seg = seg32;
@@ -999,8 +1182,8 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
                 a.nu0 = d_nu;
                 a.conv0 = d_cvh;
             }
-            ck(kv2 ? k2v2_launch(a, static_cast<int32_t>(tl.size()), ch.s)
-                  : k2_launch(a, static_cast<int32_t>(tl.size()), ch.s),
+            ck(kv2 ? k2v2_launch(a, static_cast<int32_t>(ntl), ch.s)
+                  : k2_launch(a, static_cast<int32_t>(ntl), ch.s),
                "K2 fp32");
             ++ctx->launches;
             ck(cudaEventRecord(ctx->event(3 * ci + 2), ch.s), "event");
@@ -1087,6 +1270,17 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             out.chunk_iter_ms += ms;
             if (chunks[ci].path == PATH_F32_REAL) out.real_iter_ms += ms;
         }
+        if (hp_.on) {  // chunk timeline (FOFSE_HOST_PROF): start / iterate / done vs the job start
+            for (size_t ci = 0; ci < chunks.size(); ++ci) {
+                float t0 = 0, t1 = 0, t2 = 0;
+                ck(cudaEventElapsedTime(&t0, ctx->ev[0], ctx->event(3 * ci + 0)), "elapsed");
+                ck(cudaEventElapsedTime(&t1, ctx->ev[0], ctx->event(3 * ci + 1)), "elapsed");
+                ck(cudaEventElapsedTime(&t2, ctx->ev[0], ctx->event(3 * ci + 2)), "elapsed");
+                std::fprintf(stderr, "[fofse chunk] %2zu grp %d path %d blocks %7lld  %8.2f %8.2f %8.2f ms\n", ci,
+                             chunks[ci].grp, chunks[ci].path, static_cast<long long>(chunks[ci].b1 - chunks[ci].b0),
+                             t0, t1, t2);
+            }
+        }
     }
     ck(cudaEventRecord(ctx->ev[3], st), "event");
     {
@@ -1140,13 +1334,18 @@ void fill_report(fofse_report* rep, const RunOut& ro, int64_t n, int64_t ncls, d
     }
 }
 
-Job make_image_job(const Cfg& cfg, int W, int H, int bh, int bw, const fofse_rect* blocks,
-                   const int64_t* offs, int nframes) {
+// (Re)fill `job` for an image / frames request, reusing its vectors' storage.
+void fill_image_job(Job& job, const Cfg& cfg, int W, int H, int bh, int bw, const fofse_rect* blocks,
+                    const int64_t* offs, int nframes) {
     validate_config(cfg);
     const HostProf hp_;
-    Job job;
+    job.order_key = -1;
+    job.groups = 1;
+    job.frame_group.clear();
+    job.cls_labels.clear();
     job.geo = Geometry{cfg.T, bh, bw, cfg.S, bh + 2 * cfg.S, bw + 2 * cfg.S};
-    std::vector<CellGrid> grids(static_cast<size_t>(nframes));
+    std::vector<CellGrid>& grids = job.grids;
+    grids.resize(static_cast<size_t>(nframes));
     // check_pattern_fits (pipeline.cpp:123-132) per frame, frames in parallel;
     // the first failing frame (in frame order) is reported
     for (int f = 0; f < nframes; ++f)
@@ -1158,7 +1357,7 @@ Job make_image_job(const Cfg& cfg, int W, int H, int bh, int bw, const fofse_rec
         } catch (const std::invalid_argument& e) {
             errs[static_cast<size_t>(f)] = e.what();
         }
-    });
+    }, 1);
     for (int f = 0; f < nframes; ++f)
         if (!errs[static_cast<size_t>(f)].empty()) {
             if (nframes == 1) throw std::invalid_argument(errs[0]);
@@ -1169,8 +1368,17 @@ Job make_image_job(const Cfg& cfg, int W, int H, int bh, int bw, const fofse_rec
     check_gpu_support(cfg);
     hp_.mark("make_image_job: validate");
     job.wfull = full_weight(job.geo.Lh, job.geo.Lw, cfg.rho);
+    job.blocks.clear();
     if (offs[nframes] > 0) classify_frames(job, blocks, offs, nframes, W, H, grids);
     hp_.mark("make_image_job: classify");
+}
+
+Job make_image_job(const Cfg& cfg, int W, int H, int bh, int bw, const fofse_rect* blocks,
+                   const int64_t* offs, int nframes) {
+    Job job;
+    fill_image_job(job, cfg, W, H, bh, bw, blocks, offs, nframes);
+    job.grids = {};
+    job.lid = {};
     return job;
 }
 
@@ -1408,21 +1616,27 @@ struct fofse_plan {
     int32_t n_frames, width, height;
 };
 
-static std::unique_ptr<fofse_plan> make_plan(fofse_ctx* ctx, int32_t n_frames, int32_t width,
-                                             int32_t height, const fofse_rect* blocks,
-                                             const int64_t* offs, int32_t bh, int32_t bw,
-                                             const fofse_params* params) {
+static void fill_plan(fofse_plan* plan, fofse_ctx* ctx, int32_t n_frames, int32_t width, int32_t height,
+                      const fofse_rect* blocks, const int64_t* offs, int32_t bh, int32_t bw,
+                      const fofse_params* params) {
     if (!offs || n_frames < 1) throw std::invalid_argument("plan: bad argument");
     if (width < 1 || height < 1) throw std::invalid_argument("grid dimensions must be >= 1");
     if (offs[0] != 0) throw std::invalid_argument("frame_offsets[0] must be 0");
     if (offs[n_frames] > 0 && !blocks) throw std::invalid_argument("plan: NULL blocks");
-    auto plan = std::make_unique<fofse_plan>();
     plan->ctx = ctx;
     plan->cfg = to_cfg(params);
-    plan->job = make_image_job(plan->cfg, width, height, bh, bw, blocks, offs, n_frames);
+    fill_image_job(plan->job, plan->cfg, width, height, bh, bw, blocks, offs, n_frames);
     plan->n_frames = n_frames;
     plan->width = width;
     plan->height = height;
+}
+
+static std::unique_ptr<fofse_plan> make_plan(fofse_ctx* ctx, int32_t n_frames, int32_t width,
+                                             int32_t height, const fofse_rect* blocks,
+                                             const int64_t* offs, int32_t bh, int32_t bw,
+                                             const fofse_params* params) {
+    auto plan = std::make_unique<fofse_plan>();
+    fill_plan(plan.get(), ctx, n_frames, width, height, blocks, offs, bh, bw, params);
     return plan;
 }
 
@@ -1529,7 +1743,20 @@ int fofse_conceal_frames_u8(fofse_ctx* ctx, const uint8_t* frames, int32_t n_fra
         const size_t bytes = static_cast<size_t>(n_frames) * fs;
         const int G = (params && params->precision == FOFSE_PREC_FP32)
                           ? static_cast<int>(std::clamp<int32_t>(n_frames / 16, 1, 8)) : 1;
-        auto f0 = [&](int gq) { return static_cast<size_t>((static_cast<int64_t>(gq) * n_frames + G - 1) / G); };
+        // group boundaries: the first and last groups are a quarter of the others —
+        // the first upload and the last download are the only transfers that
+        // nothing overlaps
+        std::vector<size_t> gb(static_cast<size_t>(G) + 1, 0);
+        {
+            const int units = G <= 2 ? G : 4 * (G - 2) + 2;
+            int u = 0;
+            for (int gq = 0; gq < G; ++gq) {
+                u += (G <= 2 || gq == 0 || gq == G - 1) ? 1 : 4;
+                gb[static_cast<size_t>(gq) + 1] = static_cast<size_t>((static_cast<int64_t>(u) * n_frames + units - 1) / units);
+            }
+            gb[static_cast<size_t>(G)] = static_cast<size_t>(n_frames);
+        }
+        auto f0 = [&](int gq) { return gb[static_cast<size_t>(gq)]; };
         uint8_t* d_fr = ctx->buf("frames_u8").as<uint8_t>(bytes);
         std::vector<cudaEvent_t> h2d(static_cast<size_t>(G), nullptr);
         struct EvHold {
@@ -1539,30 +1766,44 @@ int fofse_conceal_frames_u8(fofse_ctx* ctx, const uint8_t* frames, int32_t n_fra
                     if (e) cudaEventDestroy(e);
             }
         } ev_hold{h2d};
-        for (int gq = 0; gq < G; ++gq) {
-            ck(cudaEventCreateWithFlags(&h2d[static_cast<size_t>(gq)], cudaEventDisableTiming), "cudaEventCreate");
-            const size_t a0 = f0(gq) * fs, a1 = f0(gq + 1) * fs;
-            if (a1 > a0)
-                ck(cudaMemcpyAsync(d_fr + a0, frames + a0, a1 - a0, cudaMemcpyHostToDevice, ctx->io), "H2D frames");
-            ck(cudaEventRecord(h2d[static_cast<size_t>(gq)], ctx->io), "event");
-        }
+        int h2d_next = 0;  // groups [0, h2d_next) have their upload enqueued
+        auto ensure_h2d = [&](int g) {
+            for (; h2d_next <= g && h2d_next < G; ++h2d_next) {
+                const int gq = h2d_next;
+                ck(cudaEventCreateWithFlags(&h2d[static_cast<size_t>(gq)], cudaEventDisableTiming), "cudaEventCreate");
+                const size_t a0 = f0(gq) * fs, a1 = f0(gq + 1) * fs;
+                if (a1 > a0)
+                    ck(cudaMemcpyAsync(d_fr + a0, frames + a0, a1 - a0, cudaMemcpyHostToDevice, ctx->io), "H2D frames");
+                ck(cudaEventRecord(h2d[static_cast<size_t>(gq)], ctx->io), "event");
+            }
+        };
+        // the first group's upload overlaps the host-side plan; the others are
+        // enqueued as run_job reaches them
+        ensure_h2d(0);
         const HostProf hp_;
-        std::unique_ptr<fofse_plan> hold;
+        // the context's reusable frames plan (its job storage survives the call)
+        if (!ctx->frames_plan) ctx->frames_plan.reset(new fofse_plan{});
+        fofse_plan* plan = ctx->frames_plan.get();
         try {
-            hold = make_plan(ctx, n_frames, width, height, blocks, offs, bh, bw, params);
+            fill_plan(plan, ctx, n_frames, width, height, blocks, offs, bh, bw, params);
         } catch (...) {
             cudaStreamSynchronize(ctx->io);  // the caller's buffer is being read
             throw;
         }
         hp_.mark("conceal_frames: plan (validate + classify)");
-        fofse_plan* plan = hold.get();
         plan->job.groups = G;
-        plan->job.nframes = n_frames;
+        plan->job.frame_group.assign(static_cast<size_t>(n_frames), 0);
+        for (int gq = 0; gq < G; ++gq)
+            for (size_t f = f0(gq); f < f0(gq + 1); ++f) plan->job.frame_group[f] = gq;
         const int64_t n = static_cast<int64_t>(plan->job.blocks.size());
         double* d_sq = ctx->buf("sq").as<double>(static_cast<size_t>(std::max<int64_t>(n, 1)));
         const int64_t l0 = ctx->launches;
         GroupIO gio;
         gio.h2d_done = h2d;
+        gio.ensure_h2d = [&](int g) {
+            ensure_h2d(g);
+            gio.h2d_done = h2d;
+        };
         std::vector<char> down(static_cast<size_t>(G), 0);
         gio.on_done = [&](int gq, cudaStream_t s) {
             const size_t a0 = f0(gq) * fs, a1 = f0(gq + 1) * fs;
@@ -1573,6 +1814,7 @@ int fofse_conceal_frames_u8(fofse_ctx* ctx, const uint8_t* frames, int32_t n_fra
         fofse::Frames fr{d_fr, d_fr, fofse::SRC_U8, width, height, static_cast<int64_t>(fs)};
         if (n > 0)
             ro = run_job(ctx, plan->job, plan->cfg, fr, fofse::SYN_IMAGE, d_sq, nullptr, nullptr, nullptr, nullptr, &gio);
+        ensure_h2d(G - 1);
         for (int gq = 0; gq < G; ++gq)  // groups without lost blocks come back unchanged
             if (!down[static_cast<size_t>(gq)]) gio.on_done(gq, ctx->io);
         std::vector<double> sq(static_cast<size_t>(n));

@@ -959,6 +959,24 @@ static int k2_launch_T(const K2Args& a, int32_t ntiles, cudaStream_t s) {
     return cudaErrorInvalidValue;
 }
 
+// One thread per tile: find its run (a list has a handful), cut the tile.
+__global__ void __launch_bounds__(256) tiles_kernel(const TileRun* runs, int32_t nruns, int32_t ntiles, int32_t ng,
+                                                    Tile* out) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ntiles) return;
+    int r = 0;
+    while (r + 1 < nruns && runs[r + 1].t0 <= t) ++r;
+    const TileRun q = runs[r];
+    const int b = q.begin + (t - q.t0) * ng;
+    out[t] = Tile{q.cls, b, min(ng, q.end - b), 0};
+}
+
+int tiles_launch(const TileRun* runs, int32_t nruns, int32_t ntiles, int32_t ng, Tile* out, cudaStream_t s) {
+    if (ntiles <= 0) return cudaSuccess;
+    tiles_kernel<<<(ntiles + 255) / 256, 256, 0, s>>>(runs, nruns, ntiles, ng, out);
+    return cudaGetLastError();
+}
+
 int k2_launch(const K2Args& a, int32_t ntiles, cudaStream_t s) {
     switch (a.T) {
         case 8: return k2_launch_T<8>(a, ntiles, s);

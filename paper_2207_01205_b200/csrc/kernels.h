@@ -167,6 +167,14 @@ int k2d_blocks_per_cta(int T);
 int k2v2_warps_per_cta(int t);
 int cvt_launch(const CvtArgs& a, cudaStream_t s);
 
+// Tile lists on the device: `runs` = nruns (begin, end, cls, first tile) rows of
+// one list (class runs of the execution order, ascending), tiles of at most ng
+// blocks cut from each run; writes ntiles tiles to out.
+struct TileRun {
+    int32_t begin, end, cls, t0;
+};
+int tiles_launch(const TileRun* runs, int32_t nruns, int32_t ntiles, int32_t ng, Tile* out, cudaStream_t s);
+
 // Row stride of W images and the SEG used by a path (same on host/device).
 int seg_of(int T, int path);
 int k2_groups_per_cta(int T, int path);
