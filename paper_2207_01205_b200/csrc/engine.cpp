@@ -215,7 +215,8 @@ struct DevBuf {
 struct fofse_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
-    cudaStream_t side = nullptr;  // concurrent small launches (asymmetric-mask blocks)
+    cudaStream_t side = nullptr;     // concurrent launches (asymmetric-mask blocks)
+    cudaStream_t side_hi = nullptr;  // the same at high priority (a border range under one wave)
     cudaStream_t aux = nullptr;   // fp32 guard re-runs, overlapping the later chunks
     cudaStream_t cpy = nullptr;   // guard-flag read-back
     cudaStream_t io = nullptr;    // frame uploads / downloads of the pipelined host API
@@ -236,7 +237,7 @@ struct fofse_ctx {
         const size_t need = (bytes + 255) & ~size_t(255);
         if (pin_used + need > pin_cap) {
             // earlier staged copies of this call must land before the arena moves
-            for (cudaStream_t x : {stream, side, aux, cpy, io})
+            for (cudaStream_t x : {stream, side, side_hi, aux, cpy, io, pre})
                 if (x) ck(cudaStreamSynchronize(x), "sync");
             const size_t cap = std::max<size_t>({need, 2 * pin_cap, size_t(8) << 20});
             if (pin) cudaFreeHost(pin);
@@ -1040,12 +1041,16 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         };
         std::vector<Chunk> chunks;
         const int64_t chunk_min = 24576;  // blocks: keeps every chunk several waves deep
+        int nsm = 148;
+        ck(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device), "SM count");
+        const int64_t one_wave = 2LL * nsm;  // a border range this small goes on the high-priority stream
         for (const Range& r : ranges) {
             const bool on_side = r.path == PATH_F32_COMPLEX && ranges.size() > 1;
             const int64_t len = r.end - r.begin;
             const int nc = r.path == PATH_F32_REAL ? static_cast<int>(std::clamp<int64_t>(len / chunk_min, 1, 8)) : 1;
             for (int c = 0; c < nc; ++c)
-                chunks.push_back({r.path, r.begin + len * c / nc, r.begin + len * (c + 1) / nc, on_side ? ctx->side : st,
+                chunks.push_back({r.path, r.begin + len * c / nc, r.begin + len * (c + 1) / nc,
+                                  on_side ? (len <= one_wave ? ctx->side_hi : ctx->side) : st,
                                   r.grp});
         }
         // every tile list of the pipeline (heads, fp32 iterations) in one upload,
@@ -1096,6 +1101,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         hp_.mark("tile runs uploaded");
         ck(cudaEventRecord(ctx->ev[4], st), "event");
         ck(cudaStreamWaitEvent(ctx->side, ctx->ev[4], 0), "wait");
+        ck(cudaStreamWaitEvent(ctx->side_hi, ctx->ev[4], 0), "wait");
         ck(cudaStreamWaitEvent(ctx->pre, ctx->ev[4], 0), "wait");
         // FOFSE_PRE_STREAM=1: main-stream chunks run spectra + head on the pre
         // stream, so chunk k+1's preparation overlaps chunk k's iteration. Measured
@@ -1262,6 +1268,8 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         }
         hp_.mark("re-runs enqueued");
         ck(cudaEventRecord(ctx->ev[5], ctx->side), "event");
+        ck(cudaStreamWaitEvent(st, ctx->ev[5], 0), "wait");
+        ck(cudaEventRecord(ctx->ev[5], ctx->side_hi), "event");
         ck(cudaStreamWaitEvent(st, ctx->ev[5], 0), "wait");
         ck(cudaEventRecord(ctx->ev[5], ctx->aux), "event");
         ck(cudaStreamWaitEvent(st, ctx->ev[5], 0), "wait");
@@ -1430,9 +1438,24 @@ int fofse_create(int32_t device, fofse_ctx** out) {
         ctx->device = device;
         ctx->activate();
         ck(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        // the side (border blocks) and aux (guard re-runs) streams carry short
+        // launches whose completion gates later work (re-runs, frame-group
+        // downloads): higher priority, so their CTAs take SMs as the main
+        // stream's CTAs retire instead of queueing behind a whole chunk
+        // (FOFSE_STREAM_PRIO=0 disables)
+        int prio_lo = 0, prio_hi = 0;
+        ck(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi), "priority range");
+        // Measured (C4 / C5): the high-priority aux stream +1 % e2e on C4; a
+        // high-priority border stream +20 % on C5 (42 border blocks finish early,
+        // their re-runs overlap) but -1 % on C4 (9.6k border blocks then displace
+        // the main chunks) — run_job picks side_hi only for a border range under
+        // one wave. FOFSE_STREAM_PRIO=0 disables both (experiments).
+        const char* pe = std::getenv("FOFSE_STREAM_PRIO");
+        const bool prio = !(pe && pe[0] == '0');
         ck(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking), "cudaStreamCreate");
+        ck(cudaStreamCreateWithPriority(&ctx->side_hi, cudaStreamNonBlocking, prio ? prio_hi : prio_lo), "cudaStreamCreate");
         ck(cudaStreamCreateWithFlags(&ctx->pre, cudaStreamNonBlocking), "cudaStreamCreate");
-        ck(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking), "cudaStreamCreate");
+        ck(cudaStreamCreateWithPriority(&ctx->aux, cudaStreamNonBlocking, prio ? prio_hi : prio_lo), "cudaStreamCreate");
         ck(cudaStreamCreateWithFlags(&ctx->cpy, cudaStreamNonBlocking), "cudaStreamCreate");
         ck(cudaStreamCreateWithFlags(&ctx->io, cudaStreamNonBlocking), "cudaStreamCreate");
         ctx->own_stream = true;
@@ -1449,7 +1472,7 @@ void fofse_destroy(fofse_ctx* ctx) {
         if (e) cudaEventDestroy(e);
     for (auto e : ctx->evpool) cudaEventDestroy(e);
     if (ctx->pin) cudaFreeHost(ctx->pin);
-    for (cudaStream_t x : {ctx->side, ctx->aux, ctx->cpy, ctx->io, ctx->pre})
+    for (cudaStream_t x : {ctx->side, ctx->side_hi, ctx->aux, ctx->cpy, ctx->io, ctx->pre})
         if (x) {
             cudaStreamSynchronize(x);
             cudaStreamDestroy(x);
