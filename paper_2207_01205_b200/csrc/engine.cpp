@@ -107,7 +107,12 @@ class HostPool {
     }
     // fn(i) for i < n on up to `nt` threads (the caller included)
     void run(int64_t n, int64_t nt, const std::function<void(int64_t)>& fn) {
+        if (in_job()) {  // nested parallel_for (from inside a pool job): run inline
+            for (int64_t i = 0; i < n; ++i) fn(i);
+            return;
+        }
         std::lock_guard<std::mutex> serial(run_mu_);
+        in_job() = true;
         const int64_t helpers = std::min<int64_t>(nt - 1, static_cast<int64_t>(workers_.size()));
         {
             std::lock_guard<std::mutex> lk(mu_);
@@ -123,6 +128,7 @@ class HostPool {
         std::unique_lock<std::mutex> lk(mu_);
         done_cv_.wait(lk, [&] { return active_ == 0; });
         fn_ = nullptr;
+        in_job() = false;
     }
     ~HostPool() {
         {
@@ -135,6 +141,10 @@ class HostPool {
     }
 
   private:
+    static bool& in_job() {
+        thread_local bool flag = false;
+        return flag;
+    }
     explicit HostPool(unsigned nworkers) {
         for (unsigned w = 0; w < nworkers; ++w) workers_.emplace_back([this, w] { loop(w); });
     }
@@ -146,6 +156,7 @@ class HostPool {
         }
     }
     void loop(unsigned w) {
+        in_job() = true;  // workers never start nested pool jobs
         uint64_t seen = 0;
         for (;;) {
             {
@@ -352,8 +363,8 @@ bool overlap(const fofse_rect& a, const fofse_rect& b) {
 
 // pattern.cpp:55-69 validate_pattern (first failing block, lowest partner j),
 // leaving `g` filled with the (valid) pattern.
-void validate_pattern(const fofse_rect* blocks, int64_t n, int bh, int bw, int W, int H,
-                      CellGrid& g) {
+void validate_pattern_seq(const fofse_rect* blocks, int64_t n, int bh, int bw, int W, int H,
+                          CellGrid& g) {
     g.reset(W, H, std::max(bh, 1), std::max(bw, 1));
     for (int64_t i = 0; i < n; ++i) {
         const fofse_rect& b = blocks[i];
@@ -375,6 +386,60 @@ void validate_pattern(const fofse_rect* blocks, int64_t n, int bh, int bw, int W
                                         std::to_string(i) + " overlap");
         g.at(cr, cc) = static_cast<int32_t>(i);
     }
+}
+
+// pattern.cpp:55-69 checks in block order; the first failing block (size /
+// bounds, or an overlap with the lowest earlier block) is reported. Large
+// patterns run the same checks in parallel: the first size/bounds failure, then
+// the anchor grid of the blocks before it (one block per cell unless two
+// overlap — then the sequential scan names the pair), then per block its
+// earlier overlapping neighbours; the lowest failing block wins, as in order.
+void validate_pattern(const fofse_rect* blocks, int64_t n, int bh, int bw, int W, int H, CellGrid& g,
+                      bool parallel = true) {
+    if (!parallel || n < 16384) return validate_pattern_seq(blocks, n, bh, bw, W, H, g);
+    constexpr int64_t PIECE = 4096;
+    const int64_t np = (n + PIECE - 1) / PIECE;
+    std::vector<int64_t> bad(static_cast<size_t>(np), n);
+    parallel_for(np, [&](int64_t p) {
+        for (int64_t i = p * PIECE; i < std::min(n, (p + 1) * PIECE); ++i) {
+            const fofse_rect& b = blocks[i];
+            if (b.height != bh || b.width != bw || b.row < 0 || b.col < 0 || b.row + b.height > H ||
+                b.col + b.width > W) {
+                bad[static_cast<size_t>(p)] = i;
+                return;
+            }
+        }
+    }, 1);
+    const int64_t first_bad = *std::min_element(bad.begin(), bad.end());
+    g.reset(W, H, std::max(bh, 1), std::max(bw, 1));
+    std::atomic<bool> shared_cell{false};
+    parallel_for(np, [&](int64_t p) {
+        for (int64_t i = p * PIECE; i < std::min(first_bad, (p + 1) * PIECE); ++i) {
+            const fofse_rect& b = blocks[i];
+            auto* cell = reinterpret_cast<std::atomic<int32_t>*>(&g.at(b.row / bh, b.col / bw));
+            int32_t expect = -1;
+            if (!cell->compare_exchange_strong(expect, static_cast<int32_t>(i))) shared_cell = true;
+        }
+    }, 1);
+    if (shared_cell) return validate_pattern_seq(blocks, n, bh, bw, W, H, g);
+    std::vector<int64_t> ovl(static_cast<size_t>(np), n);
+    parallel_for(np, [&](int64_t p) {
+        for (int64_t i = p * PIECE; i < std::min(first_bad, (p + 1) * PIECE); ++i) {
+            const fofse_rect& b = blocks[i];
+            const int cr = b.row / bh, cc = b.col / bw;
+            for (int r = std::max(0, cr - 1); r <= std::min(g.gh - 1, cr + 1); ++r)
+                for (int c = std::max(0, cc - 1); c <= std::min(g.gw - 1, cc + 1); ++c) {
+                    const int32_t j = g.at(r, c);
+                    if (j >= 0 && j < i && overlap(b, blocks[j])) {
+                        ovl[static_cast<size_t>(p)] = i;
+                        return;
+                    }
+                }
+        }
+    }, 1);
+    const int64_t first_ovl = *std::min_element(ovl.begin(), ovl.end());
+    if (first_ovl < n || first_bad < n)  // the sequential scan produces the exact message
+        return validate_pattern_seq(blocks, n, bh, bw, W, H, g);
 }
 
 // ---------------------------------------------------------------------------
@@ -1371,9 +1436,11 @@ void fill_image_job(Job& job, const Cfg& cfg, int W, int H, int bh, int bw, cons
     for (int f = 0; f < nframes; ++f)
         if (offs[f + 1] - offs[f] < 0) throw std::invalid_argument("frame_offsets must be non-decreasing");
     std::vector<std::string> errs(static_cast<size_t>(nframes));
+    // frames in parallel; a single frame parallelises inside
     parallel_for(nframes, [&](int64_t f) {
         try {
-            validate_pattern(blocks + offs[f], offs[f + 1] - offs[f], bh, bw, W, H, grids[static_cast<size_t>(f)]);
+            validate_pattern(blocks + offs[f], offs[f + 1] - offs[f], bh, bw, W, H, grids[static_cast<size_t>(f)],
+                             nframes == 1);
         } catch (const std::invalid_argument& e) {
             errs[static_cast<size_t>(f)] = e.what();
         }

@@ -127,6 +127,30 @@ def test_pattern_validation_matches_reference(lib, ref):
         assert rc == 1 and msg == str(ei.value)
 
 
+def test_large_pattern_validation_matches_reference(lib, ref):
+    """Patterns of >= 16384 blocks are validated in parallel (engine.cpp
+    validate_pattern): same first failing block and message as the reference's
+    in-order scan (pattern.cpp:55-69)."""
+    img = np.zeros((1200, 1200))
+    grid = [(r * 9, c * 9, 8, 8) for r in range(133) for c in range(133)]
+    assert len(grid) >= 16384
+    p = _params(iterations=1, transform_size=32, support_width=8)
+    assert _validate(lib, p, 1200, 1200, grid, 8, 8) == (0, "")
+    mid = len(grid) // 2
+    cases = [
+        grid + [(4, 4, 8, 8)],                                       # late overlap with block 0
+        grid[:mid] + [(grid[5][0] + 3, grid[5][1] + 2, 8, 8)] + grid[mid:] + [(1195, 0, 8, 8)],
+        grid[:mid] + [(1195, 0, 8, 8)] + grid[mid:] + [(4, 4, 8, 8)],  # bounds before overlap
+        grid[:mid] + [(grid[mid][0] + 1, grid[mid][1] + 1, 8, 8)] + grid[mid:],  # same anchor cell
+        grid[:100] + [(0, 0, 8, 4)] + grid[100:],                    # size mismatch
+    ]
+    for blocks in cases:
+        rc, msg = _validate(lib, p, 1200, 1200, blocks, 8, 8)
+        with pytest.raises(ValueError) as ei:
+            ref.conceal(img, blocks, 8, 8, iterations=1, t=32, support=8)
+        assert rc == 1 and msg == str(ei.value)
+
+
 def _host_plan(lib, blocks_per_frame, w, h, bh, bw, **kw):
     allb = [b for fr in blocks_per_frame for b in fr]
     offs = np.cumsum([0] + [len(f) for f in blocks_per_frame]).astype(np.int64)
