@@ -1,20 +1,21 @@
 // kernels_k1.cu — K1 fast path: window gather + w*f + real-input 2-D FFT (fp64)
-// for T = 64, packed canonical output for the iteration kernels.
+// for T = 32 and 64, packed canonical output for the iteration kernels.
 //
 // Reference: engine_spectral.cpp:161-181 (fw = w f on SUPPORT, energy =
 // sum w f^2, R_w = DFT(fw)), basis.cpp:57-70 (embed at (0,0), zero pad,
 // forward unnormalised DFT), transform.cpp:48-80.
 //
-// Register FFT: a 64-point transform is 8 x 8 (Cooley-Tukey): eight threads
-// each hold 8 elements, run a radix-8 butterfly in registers, multiply the
-// inter-stage twiddles, transpose through a padded shared-memory tile (the 8
-// threads are lanes of one warp: __syncwarp only) and run the second radix-8.
+// Register FFT: a T-point transform is 8 x LG (Cooley-Tukey, LG = T/8 lanes of
+// one warp each holding 8 elements): a radix-8 butterfly in registers, the
+// inter-stage twiddles, a transpose through a padded shared-memory tile
+// (__syncwarp only) and the second stage — one radix-8 (T = 64) or two radix-4
+// (T = 32) per lane. Lane t ends with X[t + LG j], j = 0..7.
 //  * rows: the Lh window rows are paired into complex rows z = x_a + j x_b
 //    (ceil(Lh/2) <= 32 transforms), unpacked into the T/2+1 non-redundant
 //    columns of a column-major spectrum tile in shared memory;
 //  * columns: columns 1..T/2-1 are complex transforms; columns 0 and T/2 are
 //    real (DFTs of real rows at k = 0, T/2) and share one complex transform —
-//    exactly 32 column transforms = 256 threads;
+//    exactly T/2 column transforms = T^2/16 threads (256 at T = 64, 64 at 32);
 //  * the canonical half is packed from the tile (conjugate symmetry for the
 //    columns > T/2) with the rotated-frame phase from a table.
 #include <cuda_runtime.h>
@@ -28,18 +29,20 @@ namespace fofse {
 
 namespace {
 
-constexpr int FT = 64;         // transform size of this kernel
-constexpr int FNC = FT / 2 + 1;  // non-redundant columns
-constexpr int FCS = FT + 1;    // column stride of the spectrum tile (double2), conflict-free row-pass stores
-constexpr int FSS = 9;         // transpose tile row stride (double2)
-
-struct K1fSmem {
-    static constexpr size_t tw = 0;                                   // W64^e, e < 64
+template <int FT>
+struct K1fCfg {
+    static constexpr int LG = FT / 8;                 // lanes per transform
+    static constexpr int THREADS = FT * FT / 16;      // FT/2 transforms x LG lanes
+    static constexpr int NC = FT / 2 + 1;             // non-redundant columns
+    static constexpr int CS = FT + 1;                 // column stride of the spectrum tile (double2)
+    static constexpr int SS = LG + 1;                 // transpose tile row stride (double2)
+    static constexpr size_t tw = 0;                                   // W_T^e, e < T
     static constexpr size_t ph = tw + sizeof(double2) * FT;           // e^{+j pi m / T}, m < 2T
-    static constexpr size_t cb = ph + sizeof(double2) * 2 * FT;       // [FNC][FCS] spectrum tile
-    static constexpr size_t sc = cb + sizeof(double2) * FNC * FCS;    // [32 groups][8][FSS] transpose tiles
-    static constexpr size_t red = sc + sizeof(double2) * 32 * 8 * FSS;
+    static constexpr size_t cb = ph + sizeof(double2) * 2 * FT;       // [NC][CS] spectrum tile
+    static constexpr size_t sc = cb + sizeof(double2) * NC * CS;      // [T/2 groups][8][SS] transpose tiles
+    static constexpr size_t red = sc + sizeof(double2) * (FT / 2) * 8 * SS;
     static constexpr size_t total = red + 16 * sizeof(double);
+    static_assert(LG == 4 || LG == 8, "T = 32 or 64");
 };
 
 __device__ __forceinline__ double2 c_add(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
@@ -75,20 +78,50 @@ __device__ __forceinline__ void fft8(double2 (&x)[8]) {
     x[7] = c_sub(E3, t3);
 }
 
-// 64-point forward DFT of the vector v[n] = x_t[m], n = t + 8m, held by the 8
-// lanes t of a group. On return lane t holds X[t + 8 k2] in x[k2].
-__device__ __forceinline__ void fft64_group(double2 (&x)[8], int t, const double2* tw, double2* tile,
-                                            unsigned gmask) {
-    fft8(x);  // Y[t][k1] = sum_m x[t + 8m] W8^{m k1}
+// Forward 4-point DFT of y[0..3] (natural order in and out).
+__device__ __forceinline__ void fft4(double2& y0, double2& y1, double2& y2, double2& y3) {
+    const double2 a0 = c_add(y0, y2), a1 = c_sub(y0, y2);
+    const double2 b0 = c_add(y1, y3), b1 = c_mj(c_sub(y1, y3));
+    y0 = c_add(a0, b0);
+    y2 = c_sub(a0, b0);
+    y1 = c_add(a1, b1);
+    y3 = c_sub(a1, b1);
+}
+
+// T-point forward DFT of v[n] = x_t[m], n = t + LG m, held by the LG lanes t of
+// a group. On return lane t holds X[t + LG j] in x[j].
+template <int FT>
+__device__ __forceinline__ void fft_group(double2 (&x)[8], int t, const double2* tw, double2* tile,
+                                          unsigned gmask) {
+    constexpr int LG = K1fCfg<FT>::LG, SS = K1fCfg<FT>::SS;
+    fft8(x);  // Y[t][k1] = sum_m x[t + LG m] W8^{m k1}
 #pragma unroll
-    for (int k1 = 1; k1 < 8; ++k1) x[k1] = c_mul(x[k1], tw[t * k1]);  // * W64^{t k1}
+    for (int k1 = 1; k1 < 8; ++k1) x[k1] = c_mul(x[k1], tw[t * k1]);  // * W_T^{t k1}
 #pragma unroll
-    for (int k1 = 0; k1 < 8; ++k1) tile[k1 * FSS + t] = x[k1];
+    for (int k1 = 0; k1 < 8; ++k1) tile[k1 * SS + t] = x[k1];
     __syncwarp(gmask);
+    if constexpr (LG == 8) {
 #pragma unroll
-    for (int s = 0; s < 8; ++s) x[s] = tile[t * FSS + s];  // lane t = k1 now holds Y[s][k1]
-    __syncwarp(gmask);
-    fft8(x);  // X[k1 + 8 k2] = sum_s Y[s][k1] W8^{s k2}
+        for (int s = 0; s < 8; ++s) x[s] = tile[t * SS + s];  // lane t = k1 now holds Y[s][k1]
+        __syncwarp(gmask);
+        fft8(x);  // X[k1 + 8 k2] = sum_s Y[s][k1] W8^{s k2}
+    } else {
+        // lane t takes k1 = t and t + 4: X[k1 + 8 k2] = sum_s Y[s][k1] W4^{s k2}
+        double2 a[4], b[4];
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+            a[s] = tile[t * SS + s];
+            b[s] = tile[(t + 4) * SS + s];
+        }
+        __syncwarp(gmask);
+        fft4(a[0], a[1], a[2], a[3]);
+        fft4(b[0], b[1], b[2], b[3]);
+#pragma unroll
+        for (int k2 = 0; k2 < 4; ++k2) {  // X[t + 4 j]: j = 2 k2 (k1 = t), 2 k2 + 1 (k1 = t + 4)
+            x[2 * k2] = a[k2];
+            x[2 * k2 + 1] = b[k2];
+        }
+    }
 }
 
 // Window row r of block d: pointer to its column 0 (NULL when the row is
@@ -101,16 +134,19 @@ __device__ __forceinline__ const SRC* k1f_row(const K1Args& a, const BlockDesc& 
            d.col0;
 }
 
-template <class SRC>
-__global__ void __launch_bounds__(256, 3) k1f_kernel(K1Args a) {
+template <int FT, class SRC>
+__global__ void __launch_bounds__(K1fCfg<FT>::THREADS, FT == 64 ? 3 : 8) k1f_kernel(K1Args a) {
+    using C = K1fCfg<FT>;
+    constexpr int LG = C::LG, SS = C::SS, CS = C::CS;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    double2* tw = reinterpret_cast<double2*>(smem_raw + K1fSmem::tw);
-    double2* ph = reinterpret_cast<double2*>(smem_raw + K1fSmem::ph);
-    double2* cb = reinterpret_cast<double2*>(smem_raw + K1fSmem::cb);
-    double* red = reinterpret_cast<double*>(smem_raw + K1fSmem::red);
-    const int g = threadIdx.x >> 3, t = threadIdx.x & 7;
-    const unsigned gmask = 0xFFu << (8 * (g & 3));  // the group's 8 lanes (groups may diverge)
-    double2* tile = reinterpret_cast<double2*>(smem_raw + K1fSmem::sc) + g * 8 * FSS;
+    double2* tw = reinterpret_cast<double2*>(smem_raw + C::tw);
+    double2* ph = reinterpret_cast<double2*>(smem_raw + C::ph);
+    double2* cb = reinterpret_cast<double2*>(smem_raw + C::cb);
+    double* red = reinterpret_cast<double*>(smem_raw + C::red);
+    const int g = threadIdx.x / LG, t = threadIdx.x % LG;
+    // the group's LG lanes (groups may diverge)
+    const unsigned gmask = ((1u << LG) - 1u) << (LG * (g % (32 / LG)));
+    double2* tile = reinterpret_cast<double2*>(smem_raw + C::sc) + g * 8 * SS;
 
     const int b = blockIdx.x;
     const BlockDesc d = a.blocks[b];
@@ -143,7 +179,7 @@ __global__ void __launch_bounds__(256, 3) k1f_kernel(K1Args a) {
         double wa[8], wb[8], fa[8], fb[8];
 #pragma unroll
         for (int m = 0; m < 8; ++m) {
-            const int n = t + 8 * m;
+            const int n = t + LG * m;
             const bool in = n < a.Lw;
             const bool inf = in && n >= c_lo && n < c_hi;
             wa[m] = in ? wra[n] : 0.0;
@@ -158,58 +194,59 @@ __global__ void __launch_bounds__(256, 3) k1f_kernel(K1Args a) {
             energy += vb * fb[m];
             x[m] = make_double2(va, vb);
         }
-        fft64_group(x, t, tw, tile, gmask);
-        // lane t holds Z[k], k = t + 8 k2; unpack needs Z[-k] (lane (8 - t) & 7)
+        fft_group<FT>(x, t, tw, tile, gmask);
+        // lane t holds Z[k], k = t + LG j; unpack needs Z[-k]
 #pragma unroll
-        for (int k2 = 0; k2 < 8; ++k2) tile[k2 * FSS + t] = x[k2];
+        for (int j = 0; j < 8; ++j) tile[j * SS + t] = x[j];
         __syncwarp(gmask);
 #pragma unroll
-        for (int k2 = 0; k2 < 8; ++k2) {
-            const int k = t + 8 * k2;
+        for (int j = 0; j < 8; ++j) {
+            const int k = t + LG * j;
             if (k > FT / 2) continue;
             const int nk = (FT - k) & (FT - 1);
-            const double2 zc = tile[(nk >> 3) * FSS + (nk & 7)];
-            const double2 z = x[k2];
+            const double2 zc = tile[(nk / LG) * SS + (nk % LG)];
+            const double2 z = x[j];
             // Xa = (Z + conj Z-)/2, Xb = -j (Z - conj Z-)/2
-            cb[k * FCS + ra] = make_double2(0.5 * (z.x + zc.x), 0.5 * (z.y - zc.y));
-            if (rb < FT) cb[k * FCS + rb] = make_double2(0.5 * (z.y + zc.y), -0.5 * (z.x - zc.x));
+            cb[k * CS + ra] = make_double2(0.5 * (z.x + zc.x), 0.5 * (z.y - zc.y));
+            if (rb < FT) cb[k * CS + rb] = make_double2(0.5 * (z.y + zc.y), -0.5 * (z.x - zc.x));
         }
         __syncwarp(gmask);
     }
     __syncthreads();
     const int nrows = 2 * npairs;  // rows >= nrows are zero (never stored)
 
-    // ---- column pass: group g < 31 -> column g + 1; group 31 -> columns 0 and T/2 packed ----
+    // ---- column pass: group g < T/2-1 -> column g + 1; the last group -> columns 0 and T/2 packed ----
     {
-        const int col = g < 31 ? g + 1 : 0;
+        constexpr int GL = FT / 2 - 1;  // the packed group
+        const int col = g < GL ? g + 1 : 0;
         double2 x[8];
-        if (g < 31) {
+        if (g < GL) {
 #pragma unroll
             for (int m = 0; m < 8; ++m)
-                x[m] = (t + 8 * m < nrows) ? cb[col * FCS + t + 8 * m] : make_double2(0.0, 0.0);
+                x[m] = (t + LG * m < nrows) ? cb[col * CS + t + LG * m] : make_double2(0.0, 0.0);
         } else {
             // both columns hold DFTs of real rows at k = 0 and k = T/2: real values
 #pragma unroll
             for (int m = 0; m < 8; ++m)
-                x[m] = (t + 8 * m < nrows) ? make_double2(cb[t + 8 * m].x, cb[(FT / 2) * FCS + t + 8 * m].x)
-                                           : make_double2(0.0, 0.0);
+                x[m] = (t + LG * m < nrows) ? make_double2(cb[t + LG * m].x, cb[(FT / 2) * CS + t + LG * m].x)
+                                            : make_double2(0.0, 0.0);
         }
-        fft64_group(x, t, tw, tile, gmask);
-        if (g < 31) {
+        fft_group<FT>(x, t, tw, tile, gmask);
+        if (g < GL) {
 #pragma unroll
-            for (int k2 = 0; k2 < 8; ++k2) cb[col * FCS + t + 8 * k2] = x[k2];
+            for (int j = 0; j < 8; ++j) cb[col * CS + t + LG * j] = x[j];
         } else {
 #pragma unroll
-            for (int k2 = 0; k2 < 8; ++k2) tile[k2 * FSS + t] = x[k2];
+            for (int j = 0; j < 8; ++j) tile[j * SS + t] = x[j];
             __syncwarp(gmask);
 #pragma unroll
-            for (int k2 = 0; k2 < 8; ++k2) {
-                const int k = t + 8 * k2;
+            for (int j = 0; j < 8; ++j) {
+                const int k = t + LG * j;
                 const int nk = (FT - k) & (FT - 1);
-                const double2 zc = tile[(nk >> 3) * FSS + (nk & 7)];
-                const double2 z = x[k2];
+                const double2 zc = tile[(nk / LG) * SS + (nk % LG)];
+                const double2 z = x[j];
                 cb[k] = make_double2(0.5 * (z.x + zc.x), 0.5 * (z.y - zc.y));
-                cb[(FT / 2) * FCS + k] = make_double2(0.5 * (z.y + zc.y), -0.5 * (z.x - zc.x));
+                cb[(FT / 2) * CS + k] = make_double2(0.5 * (z.y + zc.y), -0.5 * (z.x - zc.x));
             }
         }
     }
@@ -225,9 +262,9 @@ __global__ void __launch_bounds__(256, 3) k1f_kernel(K1Args a) {
     auto spec = [&](int k1, int k2) {
         double2 v;
         if (k2 <= FT / 2) {
-            v = cb[k2 * FCS + k1];
+            v = cb[k2 * CS + k1];
         } else {
-            const double2 u = cb[(FT - k2) * FCS + ((FT - k1) & (FT - 1))];
+            const double2 u = cb[(FT - k2) * CS + ((FT - k1) & (FT - 1))];
             v = make_double2(u.x, -u.y);
         }
         vmax2 = fmax(vmax2, fma(v.x, v.x, v.y * v.y));
@@ -270,24 +307,30 @@ __global__ void __launch_bounds__(256, 3) k1f_kernel(K1Args a) {
 }  // namespace
 
 bool k1f_supported(const K1Args& a) {
-    if (a.T != FT || a.mode != K1_PACKED || a.Lh > FT || a.Lw > FT) return false;
-    const BinLayout L = BinLayout::make(FT, a.seg, a.spt > 0 ? a.spt : 1);
-    return L.SPT <= 2 && L.NT <= 256 && 256 % L.NT == 0;
+    if ((a.T != 32 && a.T != 64) || a.mode != K1_PACKED || a.Lh > a.T || a.Lw > a.T) return false;
+    const int threads = a.T * a.T / 16;
+    const BinLayout L = BinLayout::make(a.T, a.seg, a.spt > 0 ? a.spt : 1);
+    return L.SPT <= 2 && L.NT <= threads && threads % L.NT == 0;
 }
 
-int k1f_launch(const K1Args& a, cudaStream_t s) {
-    cudaError_t e = cudaFuncSetAttribute(k1f_kernel<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)K1fSmem::total);
+template <int FT>
+static int k1f_launch_t(const K1Args& a, cudaStream_t s) {
+    using C = K1fCfg<FT>;
+    cudaError_t e = cudaFuncSetAttribute(k1f_kernel<FT, uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)C::total);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k1f_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)K1fSmem::total);
+    e = cudaFuncSetAttribute(k1f_kernel<FT, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::total);
     if (e != cudaSuccess) return e;
     if (a.n <= 0) return cudaSuccess;
     if (a.fr.type == SRC_U8)
-        k1f_kernel<uint8_t><<<a.n, 256, K1fSmem::total, s>>>(a);
+        k1f_kernel<FT, uint8_t><<<a.n, C::THREADS, C::total, s>>>(a);
     else
-        k1f_kernel<double><<<a.n, 256, K1fSmem::total, s>>>(a);
+        k1f_kernel<FT, double><<<a.n, C::THREADS, C::total, s>>>(a);
     return cudaGetLastError();
+}
+
+int k1f_launch(const K1Args& a, cudaStream_t s) {
+    return a.T == 32 ? k1f_launch_t<32>(a, s) : k1f_launch_t<64>(a, s);
 }
 
 }  // namespace fofse

@@ -255,12 +255,16 @@ def test_conceal_fp64_T128_k2d_matches_strict(gpu, monkeypatch):
     assert np.abs(fast.restored - strict.restored).max() <= FP64_PX_TOL
 
 
-def test_k1_register_fft_matches_radix2(gpu, monkeypatch):
-    """The T = 64 register radix-8x8 K1 vs the shared-memory radix-2 K1 (both fp64):
-    identical selections on 600 C2 blocks (borders included), pixels within 1e-9."""
-    img, pat = WL.C2.frame(seed=25)
-    sub = P.LossPattern(pat.image_width, pat.image_height, 16, 16, pat.blocks[::3])
-    cfg = WL.C2.config("fp64", record_traces=True)
+@pytest.mark.parametrize("name", ["C2", "C3"])
+def test_k1_register_fft_matches_radix2(gpu, monkeypatch, name):
+    """The register K1 (T = 64: radix-8x8; T = 32: radix-8 then two radix-4 per
+    lane) vs the shared-memory radix-2 K1 (both fp64): identical selections on
+    C2 / C3 blocks (borders included), pixels within 1e-9."""
+    wl = WL.ALL[name]
+    img, pat = wl.frame(seed=25)
+    step = 3 if name == "C2" else 40
+    sub = P.LossPattern(pat.image_width, pat.image_height, wl.block, wl.block, pat.blocks[::step])
+    cfg = wl.config("fp64", record_traces=True)
     fast = P.conceal(img.astype(np.float64), sub, cfg)
     monkeypatch.setenv("FOFSE_K1", "slow")
     slow = P.conceal(img.astype(np.float64), sub, cfg)
