@@ -6,7 +6,7 @@ import subprocess
 import sys
 
 KEYS = {
-    "gpu__time_duration.sum": "time_ns",
+    "gpu__time_duration.sum": "time",
     "launch__registers_per_thread": "regs",
     "launch__grid_size": "grid",
     "launch__block_size": "block",
@@ -29,7 +29,7 @@ KEYS = {
 def main(path, kfilter=""):
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    hdr = rows[0]
+    hdr, units = rows[0], rows[1]
     idx = {h: i for i, h in enumerate(hdr)}
     stall_cols = [h for h in hdr if h.startswith("smsp__average_warps_issue_stalled_") and h.endswith("_per_issue_active.ratio")]
     for r in rows[2:]:
@@ -40,7 +40,9 @@ def main(path, kfilter=""):
         vals = []
         for k, short in KEYS.items():
             if k in idx and idx[k] < len(r):
-                vals.append(f"{short}={r[idx[k]]}")
+                u = units[idx[k]] if idx[k] < len(units) else ""
+                u = "" if u in ("", "%", "register/thread", "inst/cycle") else " " + u
+                vals.append(f"{short}={r[idx[k]]}{u}")
         print("   " + "  ".join(vals))
         st = []
         for c in stall_cols:
