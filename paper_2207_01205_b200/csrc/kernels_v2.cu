@@ -163,6 +163,11 @@ __global__ void __launch_bounds__(128, VAR == 0 ? 3 : 2) k2v2r_kernel(K2Args a) 
     const float sgn_c = ((a.Lw - 1) & 1) ? -1.f : 1.f;
     const unsigned kmask = key_mask<VAR != 0>(a);
     V2State* st = reinterpret_cast<V2State*>(smem_raw + Cf::OFF_ST + 64 * warp);
+    // loop invariants of the controller (kept out of the per-selection path)
+    const float tau1 = (float)(1.0 - a.tau);  // tau == 0 disables the guard (S <= M)
+    const int rstride = a.rec_stride > 0 ? a.rec_stride : a.iterations;
+    const int lh1 = a.Lh - 1, lw1 = a.Lw - 1;
+    const bool diag = a.trace != nullptr || a.gap_trace != nullptr;
 
     for (int bi = warp; bi < tile.count; bi += Cf::WARPS) {
         const int pos = tile.begin + bi;
@@ -200,6 +205,8 @@ __global__ void __launch_bounds__(128, VAR == 0 ? 3 : 2) k2v2r_kernel(K2Args a) 
         }
         int conv = (a.conv0 ? a.conv0[pos] : 0) | (e_init <= 0.0);
         int flagged = 0;
+        int* rec_u = a.rec_u_g + (size_t)b * rstride;
+        double2* rec_c = a.rec_c_g + (size_t)b * rstride;
         __syncwarp();
 
         // argmax chains on packed keys (|R|^2 bits, low 6 bits = 63 - pair);
@@ -270,7 +277,7 @@ __global__ void __launch_bounds__(128, VAR == 0 ? 3 : 2) k2v2r_kernel(K2Args a) 
                 conv = 1;
                 break;
             }
-            if (Sf > Mf * (float)(1.0 - a.tau)) {  // tau == 0 disables (Sf <= Mf)
+            if (Sf > Mf * tau1) {
                 flagged = 1;  // near-tie: the host re-runs this block in fp64
                 break;
             }
@@ -278,7 +285,7 @@ __global__ void __launch_bounds__(128, VAR == 0 ? 3 : 2) k2v2r_kernel(K2Args a) 
             u2 = G % T;
             self = ((u1 & (T / 2 - 1)) == 0) && ((u2 & (T / 2 - 1)) == 0);
             const float pr = pre.x, pi = pre.y;
-            const float2 P = ptab[(u1 * (a.Lh - 1) + u2 * (a.Lw - 1)) & (2 * T - 1)];  // e^{-j phi(u)}
+            const float2 P = ptab[(u1 * lh1 + u2 * lw1) & (2 * T - 1)];  // e^{-j phi(u)}
             const float ar = pr * gw, ai = pi * gw;  // a = gamma R'[u] / w0
             float c_re = ar * P.x - ai * P.y, c_im = ar * P.y + ai * P.x;  // c = P a
             float delta;
@@ -301,16 +308,14 @@ __global__ void __launch_bounds__(128, VAR == 0 ? 3 : 2) k2v2r_kernel(K2Args a) 
             const int nu = st->nu + 1;
             __syncwarp();
             if (lane == 0) {
-                const int rs = a.rec_stride > 0 ? a.rec_stride : a.iterations;
-                if (nu - 1 < rs) {
-                    a.rec_u_g[(size_t)b * rs + nu - 1] = (u1 << 16) | u2;
-                    a.rec_c_g[(size_t)b * rs + nu - 1] =
-                        self ? make_double2(c_re, 0.0) : make_double2(2.0 * c_re, 2.0 * c_im);
+                if (nu - 1 < rstride) {
+                    rec_u[nu - 1] = (u1 << 16) | u2;
+                    rec_c[nu - 1] = self ? make_double2(c_re, 0.0) : make_double2(2.0 * c_re, 2.0 * c_im);
                 }
                 st->energy = en;
                 st->nu = nu;
                 st->ntrace += 1;
-                if (a.trace || a.gap_trace) {  // diagnostics only
+                if (diag) {  // diagnostics only
                     const int tstride = a.trace_stride > 0 ? a.trace_stride : a.iterations;
                     const float iw = 1.f / w0;
                     v2_record(a, b, nu, st->ntrace - 1, 0, tstride, nullptr, nullptr, u1, u2, self,
@@ -410,11 +415,8 @@ __global__ void __launch_bounds__(128, VAR == 0 ? 3 : 2) k2v2r_kernel(K2Args a) 
             for (int s = 0; s < SPT; ++s) R[(NP + s) * NT + lane] = make_float4(xr[s], 0.f, xi[s], 0.f);
         }
         __syncwarp();
-        {
-            const int rstride = a.rec_stride > 0 ? a.rec_stride : a.iterations;
-            v2_finish<T, 32>(a, a.blocks[pos], pos, b, lane, st->energy, st->nu, conv, flagged, st->ntrace,
-                         a.rec_u_g + (size_t)b * rstride, a.rec_c_g + (size_t)b * rstride, rstride, twi);
-        }
+        v2_finish<T, 32>(a, a.blocks[pos], pos, b, lane, st->energy, st->nu, conv, flagged, st->ntrace, rec_u, rec_c,
+                         rstride, twi);
         __syncwarp();
     }
 }
