@@ -669,6 +669,14 @@ T* upload(fofse_ctx* ctx, const std::string& name, const T* host, size_t count,
     return d;
 }
 
+// Host -> device copy into an existing device buffer through the pinned arena.
+template <class T>
+void upload_to(fofse_ctx* ctx, T* d, const T* host, size_t count, cudaStream_t s) {
+    if (count)
+        ck(cudaMemcpyAsync(d, ctx->stage(host, count * sizeof(T)), count * sizeof(T), cudaMemcpyHostToDevice, s),
+           "H2D");
+}
+
 // Positions [begin, end) (grouped by class) cut into tiles of NG blocks,
 // one lost block per block-group per tile.
 std::vector<Tile> make_tiles(int64_t begin, int64_t end, const std::vector<BlockDesc>& by_pos, int ng) {
@@ -690,7 +698,7 @@ struct RunOut {
     double chunk_pre_ms = 0, chunk_iter_ms = 0, rerun_tail_ms = 0;  // fp32 pipeline
     double real_iter_ms = 0;                                         // fp32 real-path launches
     int64_t real_blocks = 0;
-    int64_t reruns = 0, converged = 0, head = 0;
+    int64_t reruns = 0, converged = 0, head = 0, resumed = 0;
 };
 
 // FOFSE_HOST_PROF=1 prints host-side checkpoints of run_job to stderr.
@@ -1176,6 +1184,12 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             const char* e = std::getenv("FOFSE_PRE_STREAM");
             return e && e[0] == '1';
         }();
+        // guard re-runs resume at the near-tie (k2d_replay + K2d); FOFSE_RESUME=0
+        // re-runs them from scratch (diagnostics)
+        const bool resume_on = [] {
+            const char* e = std::getenv("FOFSE_RESUME");
+            return !(e && e[0] == '0');
+        }();
         ck(cudaStreamWaitEvent(ctx->aux, ctx->ev[4], 0), "wait");
         std::vector<char> waited(static_cast<size_t>(2 * ngroups), 0);  // [group][main/side] upload waits
         // per chunk: events [3i] after K1, [3i+1] before the fp32 iteration, [3i+2] done
@@ -1284,42 +1298,82 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             ck(cudaEventSynchronize(ctx->event(3 * ci + 2)), "sync chunk");
             ck(cudaMemcpyAsync(h_flags, d_flags, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, ctx->cpy), "D2H flags");
             ck(cudaStreamSynchronize(ctx->cpy), "sync");
-            std::vector<int32_t> rr;  // caller ids, grouped by class
-            std::vector<BlockDesc> rdesc;
+            std::vector<int32_t> rr, rs;  // caller ids (from scratch / resumed), grouped by class
+            std::vector<BlockDesc> rdesc, sdesc;
+            std::vector<int32_t> spos, snuf;  // resumed: position of the K1 spectrum, selections made
+            // resume at the near-tie when the fp64 K1 spectrum is still in place (direct
+            // head hand-off) and the fp32 phase had made selections beyond the head
+            const bool can_resume = resume_on && head > 0 && hi_path(ch.path) == PATH_F64_REAL && soa_of(ch.path) &&
+                                    k2d_replay_fits(T, I);
             for (int64_t i = ch.b0; i < ch.b1; ++i) {
                 const int32_t b = ids[static_cast<size_t>(i)];
-                if (h_flags[b]) {
+                const int32_t f = h_flags[b];
+                if (!f) continue;
+                if (can_resume && f - 1 > head) {
+                    rs.push_back(b);
+                    sdesc.push_back(job.blocks[static_cast<size_t>(b)]);
+                    spos.push_back(static_cast<int32_t>(i));
+                    snuf.push_back(f - 1);
+                } else {
                     rr.push_back(b);
                     rdesc.push_back(job.blocks[static_cast<size_t>(b)]);
                 }
             }
-            out.reruns += static_cast<int64_t>(rr.size());
-            if (!rr.empty()) {
-            // re-run buffers are sized for the largest chunk and reused in stream order
-            const int64_t m = static_cast<int64_t>(rr.size());
-            const std::string tag = "r" + std::to_string(ci);
+            out.reruns += static_cast<int64_t>(rr.size() + rs.size());
+            out.resumed += static_cast<int64_t>(rs.size());
+            if (hp_.on && !(rr.empty() && rs.empty())) {  // where the near-ties stop the fp32 iteration
+                int hist[10] = {0};
+                for (int32_t b : rr) hist[std::min(9, (std::max(h_flags[b], 1) - 1) * 10 / std::max(1, I))]++;
+                for (int32_t b : rs) hist[std::min(9, (h_flags[b] - 1) * 10 / std::max(1, I))]++;
+                std::fprintf(stderr, "[fofse guard] chunk %zu: %zu flagged (%zu resumed); by tenth of I:", ci,
+                             rr.size() + rs.size(), rs.size());
+                for (int q = 0; q < 10; ++q) std::fprintf(stderr, " %d", hist[q]);
+                std::fprintf(stderr, "\n");
+            }
+            // re-run buffers are sized for the largest chunk and reused in stream order (aux)
             BlockDesc* d_rdesc = ctx->buf("rdesc").as<BlockDesc>(static_cast<size_t>(max_chunk));
             int32_t* d_rr = ctx->buf("rr").as<int32_t>(static_cast<size_t>(max_chunk));
             char* d_Rr = ctx->buf("Rr").as<char>(static_cast<size_t>(max_chunk) * r64_bytes);
             double* d_re0 = ctx->buf("re0").as<double>(static_cast<size_t>(max_chunk));
             double* d_rimax = ctx->buf("rimax").as<double>(static_cast<size_t>(max_chunk));
-            ck(cudaMemcpyAsync(d_rdesc, ctx->stage(rdesc.data(), sizeof(BlockDesc) * m), sizeof(BlockDesc) * m,
-                               cudaMemcpyHostToDevice, ctx->aux),
-               "H2D");
-            ck(cudaMemcpyAsync(d_rr, ctx->stage(rr.data(), sizeof(int32_t) * m), sizeof(int32_t) * m,
-                               cudaMemcpyHostToDevice, ctx->aux),
-               "H2D");
-            K2Args a = base_args();
-            a.order = d_rr;
-            a.blocks = d_rdesc;
-            a.rin = d_Rr;
-            a.energy0 = d_re0;
-            a.init_energy = d_re0;
-            a.init_max = d_rimax;
-            a.rec_global = 0;  // strict: smem records (or the per-block global scratch when I > cap)
-            const int hp = hi_path(ch.path);
-            k1_packed(d_rdesc, m, hp, seg64, 1, d_Rr, d_re0, d_rimax, 0, 0, ctx->aux);
-            k2_f64(a, hp, 0, m, rdesc, tag, ctx->aux);
+            if (!rr.empty()) {  // from scratch: K1 + all I selections in fp64
+                const int64_t m = static_cast<int64_t>(rr.size());
+                const std::string tag = "r" + std::to_string(ci);
+                upload_to(ctx, d_rdesc, rdesc.data(), rdesc.size(), ctx->aux);
+                upload_to(ctx, d_rr, rr.data(), rr.size(), ctx->aux);
+                K2Args a = base_args();
+                a.order = d_rr;
+                a.blocks = d_rdesc;
+                a.rin = d_Rr;
+                a.energy0 = d_re0;
+                a.init_energy = d_re0;
+                a.init_max = d_rimax;
+                a.rec_global = 0;  // strict: smem records (or the per-block global scratch when I > cap)
+                const int hp = hi_path(ch.path);
+                k1_packed(d_rdesc, m, hp, seg64, 1, d_Rr, d_re0, d_rimax, 0, 0, ctx->aux);
+                k2_f64(a, hp, 0, m, rdesc, tag, ctx->aux);
+            }
+            if (!rs.empty()) {  // resumed: K2d REPLAY rebuilds the fp64 state at the near-tie and goes on
+                const int64_t m = static_cast<int64_t>(rs.size());
+                const std::string tag = "s" + std::to_string(ci);
+                int32_t* d_rpos = ctx->buf("rpos").as<int32_t>(static_cast<size_t>(max_chunk));
+                int32_t* d_rnuf = ctx->buf("rnuf").as<int32_t>(static_cast<size_t>(max_chunk));
+                upload_to(ctx, d_rdesc, sdesc.data(), sdesc.size(), ctx->aux);
+                upload_to(ctx, d_rr, rs.data(), rs.size(), ctx->aux);
+                upload_to(ctx, d_rpos, spos.data(), spos.size(), ctx->aux);
+                upload_to(ctx, d_rnuf, snuf.data(), snuf.size(), ctx->aux);
+                K2Args a = base_args();
+                a.order = d_rr;
+                a.blocks = d_rdesc;
+                a.rin = d_R64;  // K1 spectra, initial energy / max: by position (src_pos)
+                a.src_pos = d_rpos;
+                a.nu_flag = d_rnuf;
+                a.init_energy = d_e0;
+                a.init_max = d_imax;
+                a.nu_limit = I;
+                a.rec_global = 1;
+                a.trace_from_nu0 = 1;
+                k2_f64(a, PATH_F64_REAL, 0, m, sdesc, tag, ctx->aux);
             }
             // a frame group is complete once its last chunk and its re-runs are done
             const bool last_of_group = ci + 1 == chunks.size() || chunks[ci + 1].grp != ch.grp;

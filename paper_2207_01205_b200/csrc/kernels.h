@@ -134,6 +134,10 @@ struct K2Args {
     int32_t rout_f32;           // K2d: write rout as the fp32 SoA pair layout of the K2v2 real
     int32_t rout_seg, rout_spt; //   path (segment / segments per lane), rout_stride floats per
     int64_t rout_stride;        //   block — the fp32 phase reads it directly (no convert pass)
+    // guard re-runs resumed at the near-tie (K2d REPLAY mode):
+    int32_t nu_limit;           // K2d: iterate until nu == nu_limit (per-block resume points; 0 = off)
+    const int32_t* src_pos;     // K2d REPLAY: position of the block's K1 spectrum in rin / init_*
+    const int32_t* nu_flag;     // K2d REPLAY: selections to replay (made in fp32 before the near-tie)
 };
 
 struct CvtArgs {
@@ -164,6 +168,9 @@ int k2v2_launch(const K2Args& a, int32_t ntiles, cudaStream_t s);
 // K2d: fp64 rotated-frame iteration (PATH_F64_REAL), groups of d_group_threads(T).
 int k2d_launch(const K2Args& a, int32_t ntiles, cudaStream_t s);
 int k2d_blocks_per_cta(int T);
+// K2d REPLAY mode (a.src_pos set): rebuilds a near-tie block's fp64 state after
+// its first nu_flag[pos] recorded selections, then iterates on to nu_limit.
+bool k2d_replay_fits(int T, int rstride);
 int k2v2_warps_per_cta(int t);
 int cvt_launch(const CvtArgs& a, cudaStream_t s);
 

@@ -98,7 +98,184 @@ __device__ __forceinline__ double2 dpick(int j, const double* re, const double* 
     return q;
 }
 
-template <int T, bool FOD>
+// ============================================================================
+// Guard re-runs resumed at the near-tie (K2d REPLAY mode). A block flagged by
+// the fp32 guard at selection nf made its first nf selections unambiguously
+// (runner-up more than tau below the maximum), so the fp64 path takes the same
+// ones. Instead of re-running all I selections in fp64, the block's fp64 state
+// at selection nf is rebuilt from its K1 spectrum R'_0 and the recorded u_i:
+//  1. one warp, right-looking: lane l keeps R'[u_q] for q = l (mod 32) and folds
+//     each new a_i into its later entries (the K2d update at those bins), so
+//     selection q needs no reduction; every lane runs the scalar part of
+//     iterate on R'[u_q] exactly as K2d (a_q, c_q, energy; the fp64 c_q
+//     overwrite the fp32 records);
+//  2. every owned bin in parallel: R'_nf[k] = R'_0[k] - sum_{i<nf} (a_i s1
+//     V[k-u_i] + conj(a_i) s2 V[k+u_i]) — the K2d update without argmax or
+//     barriers;
+// and the same kernel continues with the ordinary K2d loop up to I selections.
+// ============================================================================
+struct RSel {
+    double ar, ai;  // the update factor a (after the self-conjugate adjustment)
+    int u1, u2, self, pad;
+};
+static_assert(sizeof(RSel) == 32, "RSel");
+
+template <class Cf>
+__device__ __forceinline__ void d_replay(const K2Args& a, const double* vE, const double2* ptab, RSel* sel,
+                                         double2* pend, double* bcast, int bar, int w, int lane, int ltid,
+                                         bool active, int k1, int c0, int ex, const BinLayout& L, int pos, int b,
+                                         int src, double sgn_r, double sgn_c, double w0, double gw, int rstride,
+                                         double (&re)[Cf::SEG + 1], double (&im)[Cf::SEG + 1], double& energy_out,
+                                         int& nf_out, int& conv_out) {
+    constexpr int T = Cf::HT * 2, SEG = Cf::SEG, NT = Cf::NT, PPS = Cf::PPS, SRV = Cf::SRV, GT = Cf::GT;
+    const double2* R0 = static_cast<const double2*>(a.rin) + (size_t)src * L.SLOTS;
+    const int* rec_u = a.rec_u_g + (size_t)b * rstride;
+    double2* rec_c = a.rec_c_g + (size_t)b * rstride;
+    const double e_init = a.init_energy[src], imax = a.init_max[src];
+    auto vdiff = [&](int p1, int p2, int q1, int q2) {  // V[p - q], anti-periodic extension
+        const double s = ((p1 < q1) ? sgn_r : 1.0) * ((p2 < q2) ? sgn_c : 1.0);
+        return s * vE[((p1 - q1) & (T - 1)) * SRV + ((p2 - q2) & (T - 1))];
+    };
+    auto vsum = [&](int p1, int p2, int q1, int q2) {  // V[p + q]
+        const double s = ((p1 + q1 >= T) ? sgn_r : 1.0) * ((p2 + q2 >= T) ? sgn_c : 1.0);
+        return s * vE[((p1 + q1) & (T - 1)) * SRV + ((p2 + q2) & (T - 1))];
+    };
+    if (w == 0) {
+        double energy = e_init;
+        const double thr_e = 1e-12 * e_init, thr_m = (1e-12 * imax) * (1e-12 * imax);
+        int nf = min(a.nu_flag[pos], rstride), conv = e_init <= 0.0;
+        for (int q = lane; q < nf; q += 32) {  // R'_0 at every selected bin, in parallel
+            const int u = rec_u[q], u1 = u >> 16, u2 = u & 0xffff;
+            int slot, tid;
+            bin_slot(L, u1, u2, &slot, &tid);
+            pend[q] = R0[slot * NT + tid];
+            sel[q].u1 = u1;
+            sel[q].u2 = u2;
+        }
+        __syncwarp();
+        for (int q = 0; q < nf && !conv; ++q) {
+            const int u1 = sel[q].u1, u2 = sel[q].u2;
+            const double pr = pend[q].x, pi = pend[q].y;
+            // ---- scalar part of iterate (engine_spectral.cpp:58-110), as K2d ----
+            const double M = fma(pi, pi, pr * pr);
+            if (energy < thr_e || !(M > 0.0) || M < thr_m) {
+                conv = 1;
+                nf = q;
+                break;
+            }
+            const int self = ((T - u1) % T == u1) && ((T - u2) % T == u2);
+            const double2 P = ptab[(u1 * (a.Lh - 1) + u2 * (a.Lw - 1)) & (2 * T - 1)];
+            const double ar = pr * gw, ai = pi * gw;
+            double c_re = ar * P.x - ai * P.y, c_im = ar * P.y + ai * P.x;
+            double a_re = ar, a_im = ai, delta;
+            if (self) {
+                c_im = 0.0;
+                a_re = c_re * P.x;
+                a_im = -c_re * P.y;
+                delta = -2.0 * c_re * (pr * P.x - pi * P.y) + c_re * c_re * w0;
+            } else {
+                const int mi1 = 2 * u1, mi2 = 2 * u2;
+                const double v2 = vE[(mi1 & (T - 1)) * SRV + (mi2 & (T - 1))];
+                const double sig = ((mi1 >= T) ? sgn_r : 1.0) * ((mi2 >= T) ? sgn_c : 1.0);
+                delta = -4.0 * (a_re * pr + a_im * pi) + 2.0 * (a_re * a_re + a_im * a_im) * w0 +
+                        2.0 * sig * v2 * (a_re * a_re - a_im * a_im);
+            }
+            const double e = energy + delta;
+            energy = 0.0 < e ? e : 0.0;
+            if (lane == 0) {
+                sel[q].ar = a_re;
+                sel[q].ai = a_im;
+                sel[q].self = self;
+                rec_c[q] = self ? make_double2(c_re, 0.0) : make_double2(2.0 * c_re, 2.0 * c_im);
+            }
+            // fold a_q into this lane's later selections (the K2d update at bin u_t)
+            for (int t = q + 1 + ((lane - q - 1) & 31); t < nf; t += 32) {
+                const int t1 = sel[t].u1, t2 = sel[t].u2;
+                const double v1 = vdiff(t1, t2, u1, u2);
+                double dr = a_re * v1, di = a_im * v1;
+                if (!self) {
+                    const double v2 = vsum(t1, t2, u1, u2);
+                    dr = fma(a_re, v2, dr);
+                    di = fma(-a_im, v2, di);
+                }
+                pend[t] = make_double2(pend[t].x - dr, pend[t].y - di);
+            }
+            __syncwarp();
+        }
+        if (lane == 0) {
+            bcast[0] = energy;
+            bcast[1] = (double)nf;
+            bcast[2] = (double)conv;
+        }
+    }
+    named_bar_sync(bar, GT);
+    energy_out = bcast[0];
+    nf_out = (int)bcast[1];
+    conv_out = (int)bcast[2];
+    const int nf = nf_out;
+#pragma unroll
+    for (int q = 0; q < SEG; ++q) {
+        const double2 v = active ? R0[q * NT + ltid] : make_double2(0.0, 0.0);
+        re[q] = v.x;
+        im[q] = v.y;
+    }
+    {
+        const double2 v = (active && ex) ? R0[SEG * NT + ltid] : make_double2(0.0, 0.0);
+        re[SEG] = v.x;
+        im[SEG] = v.y;
+    }
+    if (active) {
+        for (int i = 0; i < nf; ++i) {
+            const RSel s = sel[i];
+            const int u1 = s.u1, u2 = s.u2;
+            const int p2 = Cf::NCOPY == 2 ? (u2 & 1) : 0;
+            const double* vimg = vE + p2 * (T * SRV);
+            const int rA = (k1 - u1) & (T - 1), rB = (k1 + u1) & (T - 1);
+            const int cA = (c0 - u2) & (T - 1), cB = (c0 + u2) & (T - 1);
+            const double s1 = ((k1 < u1) ? sgn_r : 1.0) * ((c0 < u2) ? sgn_c : 1.0);
+            const double s2 = ((k1 + u1 >= T) ? sgn_r : 1.0) * ((c0 + u2 >= T) ? sgn_c : 1.0);
+            const double* va = vimg + rA * SRV + (cA - p2);
+            const double* vb = vimg + rB * SRV + (cB - p2);
+            auto ld2 = [](const double* v, int q) {
+                if constexpr (Cf::NCOPY == 2) return reinterpret_cast<const double2*>(v)[q];
+                return make_double2(v[2 * q], v[2 * q + 1]);
+            };
+            const double n1r = -s1 * s.ar, n1i = -s1 * s.ai;
+            const double n2r = -s2 * s.ar, n2i = s2 * s.ai;
+            if (s.self) {
+#pragma unroll
+                for (int q = 0; q < PPS; ++q) {
+                    const double2 x = ld2(va, q);
+                    re[2 * q] = fma(n1r, x.x, re[2 * q]);
+                    im[2 * q] = fma(n1i, x.x, im[2 * q]);
+                    re[2 * q + 1] = fma(n1r, x.y, re[2 * q + 1]);
+                    im[2 * q + 1] = fma(n1i, x.y, im[2 * q + 1]);
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < PPS; ++q) {
+                    const double2 x = ld2(va, q), y = ld2(vb, q);
+                    re[2 * q] = fma(n2r, y.x, fma(n1r, x.x, re[2 * q]));
+                    im[2 * q] = fma(n2i, y.x, fma(n1i, x.x, im[2 * q]));
+                    re[2 * q + 1] = fma(n2r, y.y, fma(n1r, x.y, re[2 * q + 1]));
+                    im[2 * q + 1] = fma(n2i, y.y, fma(n1i, x.y, im[2 * q + 1]));
+                }
+            }
+            if (ex) {
+                const double x = vE[rA * SRV + cA + SEG];
+                re[SEG] = fma(n1r, x, re[SEG]);
+                im[SEG] = fma(n1i, x, im[SEG]);
+                if (!s.self) {
+                    const double y = vE[rB * SRV + cB + SEG];
+                    re[SEG] = fma(n2r, y, re[SEG]);
+                    im[SEG] = fma(n2i, y, im[SEG]);
+                }
+            }
+        }
+    }
+}
+
+template <int T, bool FOD, bool REPLAY = false>
 __global__ void __launch_bounds__(DCfg<T>::THREADS, DCfg<T>::MINB) k2d_kernel(K2Args a) {
     using Cf = DCfg<T>;
     constexpr int SEG = Cf::SEG, NT = Cf::NT, GT = Cf::GT, NW = Cf::NW, PPS = Cf::PPS, SRV = Cf::SRV;
@@ -140,7 +317,24 @@ __global__ void __launch_bounds__(DCfg<T>::THREADS, DCfg<T>::MINB) k2d_kernel(K2
         const int pos = tile.begin + bi;
         const int b = a.order[pos];
         double re[NB], im[NB];
-        {
+        int* rec_u = a.rec_u_g + (size_t)b * rstride;
+        double2* rec_c = a.rec_c_g + (size_t)b * rstride;
+        double energy;
+        int nu, conv;
+        const int src = REPLAY ? a.src_pos[pos] : pos;  // REPLAY: inputs by the spectrum's position
+        const double e_init = a.init_energy[src];
+        const double thr_e = 1e-12 * e_init;
+        const double thr_m = (1e-12 * a.init_max[src]) * (1e-12 * a.init_max[src]);
+        if constexpr (REPLAY) {
+            unsigned char* rbase = smem_raw + ((Cf::SMEM + 31) & ~size_t(31));
+            RSel* sel = reinterpret_cast<RSel*>(rbase) + (size_t)grp * rstride;
+            double2* pend = reinterpret_cast<double2*>(reinterpret_cast<RSel*>(rbase) + (size_t)Cf::GROUPS * rstride) +
+                            (size_t)grp * rstride;
+            d_replay<Cf>(a, vE, ptab, sel, pend, reinterpret_cast<double*>(dred), bar, w, ltid & 31, ltid, active, k1,
+                         c0, ex, L, pos, b, src, sgn_r, sgn_c, w0, gw, rstride, re, im, energy, nu, conv);
+            conv |= (e_init <= 0.0);
+            named_bar_sync(bar, GT);  // sel / pend / dred are reused below and by the next block
+        } else {
             const double2* R = static_cast<const double2*>(a.rin) + (size_t)pos * L.SLOTS;
 #pragma unroll
             for (int j = 0; j < SEG; ++j) {
@@ -151,23 +345,19 @@ __global__ void __launch_bounds__(DCfg<T>::THREADS, DCfg<T>::MINB) k2d_kernel(K2
             const double2 v = (active && ex) ? R[SEG * NT + ltid] : make_double2(0.0, 0.0);
             re[SEG] = v.x;
             im[SEG] = v.y;
+            energy = a.energy0[pos];
+            nu = a.nu0 ? a.nu0[pos] : 0;
+            conv = (a.conv0 ? a.conv0[pos] : 0) | (e_init <= 0.0);
         }
-        int* rec_u = a.rec_u_g + (size_t)b * rstride;
-        double2* rec_c = a.rec_c_g + (size_t)b * rstride;
-        double energy = a.energy0[pos];
-        const double e_init = a.init_energy[pos];
-        const double thr_e = 1e-12 * e_init;
-        const double thr_m = (1e-12 * a.init_max[pos]) * (1e-12 * a.init_max[pos]);
-        int nu = a.nu0 ? a.nu0[pos] : 0;
         int ntrace = a.trace_from_nu0 ? nu : 0;
-        int conv = (a.conv0 ? a.conv0[pos] : 0) | (e_init <= 0.0);
 
         unsigned long long KA = 0, KB = 0;  // two independent max chains
 #pragma unroll
         for (int j = 0; j < SEG; ++j) dscan<KM>((j & 1) ? KB : KA, re[j], im[j], kbase - j);
         if (ex) dscan<KM>(KA, re[SEG], im[SEG], kbase - SEG);
 
-        for (int it = 0; it < a.iterations && !conv; ++it) {
+        const int nu_end = a.nu_limit > 0 ? a.nu_limit : nu + a.iterations;  // per-block resume points
+        for (int it = 0; nu < nu_end && !conv; ++it) {
             const int par = it & 1;
             unsigned long long K = KA > KB ? KA : KB;
             if (!active) K = 0;
@@ -483,7 +673,8 @@ __global__ void __launch_bounds__(256, 2) k2dc_kernel(K2Args a) {
         for (int j = 0; j < SEG; ++j) dscan((j & 1) ? KB : KA, re[j], im[j], kbase - j);
         if (ex) dscan(KA, re[SEG], im[SEG], kbase - SEG);
 
-        for (int it = 0; it < a.iterations && !conv; ++it) {
+        const int nu_end = a.nu_limit > 0 ? a.nu_limit : nu + a.iterations;  // per-block resume points
+        for (int it = 0; nu < nu_end && !conv; ++it) {
             const int par = it & 1;
             unsigned long long K = KA > KB ? KA : KB;
             if (!active) K = 0;
@@ -636,12 +827,32 @@ static int k2dc_t(const K2Args& a, int32_t ntiles, cudaStream_t s) {
 template <int T>
 static int k2d_t(const K2Args& a, int32_t ntiles, cudaStream_t s) {
     using Cf = DCfg<T>;
-    auto* fn = a.full_od ? k2d_kernel<T, true> : k2d_kernel<T, false>;
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
+    const bool replay = a.src_pos != nullptr;
+    auto* fn = replay ? k2d_kernel<T, false, true> : a.full_od ? k2d_kernel<T, true> : k2d_kernel<T, false>;
+    const int rstride = a.rec_stride > 0 ? a.rec_stride : a.iterations;
+    const size_t smem = replay ? ((Cf::SMEM + 31) & ~size_t(31)) +
+                                     (sizeof(RSel) + sizeof(double2)) * (size_t)Cf::GROUPS * rstride
+                               : Cf::SMEM;
+    if (smem > 227 * 1024) return cudaErrorInvalidValue;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     if (ntiles <= 0) return cudaSuccess;
-    fn<<<ntiles, Cf::THREADS, Cf::SMEM, s>>>(a);
+    fn<<<ntiles, Cf::THREADS, smem, s>>>(a);
     return cudaGetLastError();
+}
+
+bool k2d_replay_fits(int T, int rstride) {
+    auto need = [&](size_t smem, int groups) {
+        return ((smem + 31) & ~size_t(31)) + (sizeof(RSel) + sizeof(double2)) * (size_t)groups * rstride <= 227 * 1024;
+    };
+    switch (T) {
+        case 8: return need(DCfg<8>::SMEM, DCfg<8>::GROUPS);
+        case 16: return need(DCfg<16>::SMEM, DCfg<16>::GROUPS);
+        case 32: return need(DCfg<32>::SMEM, DCfg<32>::GROUPS);
+        case 64: return need(DCfg<64>::SMEM, DCfg<64>::GROUPS);
+        case 128: return need(DCfg<128>::SMEM, DCfg<128>::GROUPS);
+    }
+    return false;
 }
 
 int k2d_launch(const K2Args& a, int32_t ntiles, cudaStream_t s) {

@@ -278,7 +278,9 @@ __global__ void __launch_bounds__(128, VAR == 0 ? 3 : 2) k2v2r_kernel(K2Args a) 
                 break;
             }
             if (Sf > Mf * tau1) {
-                flagged = 1;  // near-tie: the host re-runs this block in fp64
+                // near-tie: the host re-runs this block in fp64; flag = 1 + the
+                // selections already made
+                flagged = 1 + st->nu;
                 break;
             }
             u1 = G / T;
@@ -602,7 +604,7 @@ __global__ void __launch_bounds__(V2HCfg<T>::THREADS, V2HCfg<T>::MINB) k2v2h_ker
                 break;
             }
             if (Sf > Mf * tau1) {
-                flagged = 1;  // near-tie: the host re-runs this block in fp64
+                flagged = 1 + nu;  // near-tie: the host re-runs this block in fp64
                 break;
             }
             const int u1 = G / T, u2 = G % T;
@@ -882,7 +884,7 @@ __global__ void __launch_bounds__(128, 3) k2v2c_kernel(K2Args a) {
                 break;
             }
             if (Sf > Mf * (float)(1.0 - a.tau)) {
-                flagged = 1;
+                flagged = 1 + st->nu;
                 break;
             }
             const int u1 = G / T, u2 = G % T;

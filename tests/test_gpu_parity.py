@@ -445,6 +445,37 @@ def test_small_and_large_blocks_fp32(gpu, orc, name):
     assert np.abs(o64.restored - ref["restored"]).max() <= FP64_PX_TOL
 
 
+@pytest.mark.parametrize("name", ["C2", "C5"])
+def test_guard_resume_matches_rerun_from_scratch(gpu, monkeypatch, name):
+    """fp32 mode: near-tie blocks resumed at the flagged selection (k2d_replay
+    rebuilds the fp64 state from the K1 spectrum and the recorded selections,
+    K2d continues) give the pixels of re-running them from scratch in fp64 —
+    the selections made before the near-tie are the fp64 path's own — within
+    fp64 rounding, and within the fp32 bar of the fp64 path."""
+    wl = WL.ALL[name]
+    if name == "C2":
+        img, pat = wl.frame(seed=27)
+    else:
+        size = 1024
+        img = P.gen_image_u8(33, size, size)
+        rects = P.gen_losses(33, size // wl.block, size // wl.block, wl.loss_frac, wl.block, wl.block)
+        pat = P.LossPattern(size, size, wl.block, wl.block,
+                            [P.Rect(*map(int, (r["row"], r["col"], r["height"], r["width"]))) for r in rects])
+    cfg = wl.config("fp32")
+    resumed = P.conceal(img.astype(np.float64), pat, cfg)
+    assert resumed.report.device["guard_reruns"] > 0
+    monkeypatch.setenv("FOFSE_RESUME", "0")
+    scratch = P.conceal(img.astype(np.float64), pat, cfg)
+    assert resumed.report.device["guard_reruns"] == scratch.report.device["guard_reruns"]
+    assert np.abs(resumed.restored - scratch.restored).max() <= 1e-6
+    o64 = P.conceal(img.astype(np.float64), pat, wl.config("fp64"))
+    lost = np.zeros(img.shape, bool)
+    for b in pat.blocks:
+        lost[b.row:b.row + wl.block, b.col:b.col + wl.block] = True
+    assert _fp32_vs_ref(resumed.restored, o64.restored, lost) <= FP32_PX_TOL
+    assert abs(resumed.report.psnr_db - o64.report.psnr_db) <= FP32_PSNR_TOL
+
+
 def test_frames_u8_matches_f64_and_is_deterministic(gpu):
     """Video entry point: u8 frames give write_pgm-rounded results of the f64 path;
     repeated runs and frame-order changes are bitwise identical."""
