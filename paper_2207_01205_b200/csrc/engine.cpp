@@ -1117,14 +1117,27 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         int nsm = 148;
         ck(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device), "SM count");
         const int64_t one_wave = 2LL * nsm;  // a border range this small goes on the high-priority stream
+        // real ranges: chunks of a whole number of the fp32 kernel's waves (the
+        // last takes the remainder), at least chunk_min blocks, at most 8 per range
+        const int64_t wave = v2r ? k2v2_real_wave(T, ctx->device) : 0;
         for (const Range& r : ranges) {
             const bool on_side = r.path == PATH_F32_COMPLEX && ranges.size() > 1;
             const int64_t len = r.end - r.begin;
-            const int nc = r.path == PATH_F32_REAL ? static_cast<int>(std::clamp<int64_t>(len / chunk_min, 1, 8)) : 1;
-            for (int c = 0; c < nc; ++c)
-                chunks.push_back({r.path, r.begin + len * c / nc, r.begin + len * (c + 1) / nc,
-                                  on_side ? (len <= one_wave ? ctx->side_hi : ctx->side) : st,
-                                  r.grp});
+            const cudaStream_t cs = on_side ? (len <= one_wave ? ctx->side_hi : ctx->side) : st;
+            if (r.path != PATH_F32_REAL) {
+                chunks.push_back({r.path, r.begin, r.end, cs, r.grp});
+                continue;
+            }
+            const int nc = static_cast<int>(std::clamp<int64_t>(len / chunk_min, 1, 8));
+            if (wave <= 0 || nc == 1) {
+                for (int c = 0; c < nc; ++c)
+                    chunks.push_back({r.path, r.begin + len * c / nc, r.begin + len * (c + 1) / nc, cs, r.grp});
+                continue;
+            }
+            const int64_t cw = std::max<int64_t>(1, (len / nc) / wave) * wave;  // whole waves
+            int64_t b0 = r.begin;
+            for (int c = 0; c + 1 < nc; ++c, b0 += cw) chunks.push_back({r.path, b0, b0 + cw, cs, r.grp});
+            chunks.push_back({r.path, b0, r.end, cs, r.grp});
         }
         // every tile list of the pipeline (heads, fp32 iterations) in one upload,
         // queued ahead of the later frame groups' uploads on the copy engine

@@ -172,6 +172,8 @@ int k2d_blocks_per_cta(int T);
 // its first nu_flag[pos] recorded selections, then iterates on to nu_limit.
 bool k2d_replay_fits(int T, int rstride);
 int k2v2_warps_per_cta(int t);
+// Lost blocks per full wave of the fp32 real-path kernel on device dev (0 = unknown).
+int64_t k2v2_real_wave(int t, int dev);
 int cvt_launch(const CvtArgs& a, cudaStream_t s);
 
 // Tile lists on the device: `runs` = nruns (begin, end, cls, first tile) rows of

@@ -1076,6 +1076,39 @@ int k2v2_launch(const K2Args& a, int32_t ntiles, cudaStream_t s) {
 
 int k2v2_warps_per_cta(int t) { return t == 128 ? V2HCfg<128>::GROUPS : 4; }  // lost blocks per CTA
 
+// Lost blocks resident at once on the device for the fp32 real-path kernel
+// (SMs x CTAs per SM x blocks per CTA): chunk sizes are multiples of it, so no
+// chunk ends in a nearly empty wave.
+template <int T>
+static int64_t wave_t(int dev) {
+    int nsm = 0, per_sm = 0;
+    if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+    cudaError_t e;
+    if constexpr (T == 128) {
+        using Cf = V2HCfg<128>;
+        cudaFuncSetAttribute(k2v2h_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2v2h_kernel<128>, Cf::THREADS, Cf::SMEM);
+        return e == cudaSuccess ? (int64_t)nsm * per_sm * Cf::GROUPS : 0;
+    } else {
+        using Cf = V2Cfg<T, PATH_F32_REAL>;
+        cudaFuncSetAttribute(k2v2r_kernel<T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2v2r_kernel<T, 0>, 32 * Cf::WARPS, Cf::SMEM);
+        return e == cudaSuccess ? (int64_t)nsm * per_sm * Cf::WARPS : 0;
+    }
+}
+
+int64_t k2v2_real_wave(int t, int dev) {
+    if (v2_real_gw(t) == 2 || v2r_variant() != 0) return 0;  // experiments: no alignment
+    switch (t) {
+        case 8: return wave_t<8>(dev);
+        case 16: return wave_t<16>(dev);
+        case 32: return wave_t<32>(dev);
+        case 64: return wave_t<64>(dev);
+        case 128: return wave_t<128>(dev);
+    }
+    return 0;
+}
+
 int v2_real_copies(int t) {
     if (t == 128) return V2HCfg<128>::NCOPY;
     if (v2_real_gw(t) == 2) return 4;  // K2v2h: quad layout
