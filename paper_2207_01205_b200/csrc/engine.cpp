@@ -1982,11 +1982,19 @@ int fofse_conceal_frames_u8(fofse_ctx* ctx, const uint8_t* frames, int32_t n_fra
         };
         RunOut ro;
         fofse::Frames fr{d_fr, d_fr, fofse::SRC_U8, width, height, static_cast<int64_t>(fs)};
-        if (n > 0)
-            ro = run_job(ctx, plan->job, plan->cfg, fr, fofse::SYN_IMAGE, d_sq, nullptr, nullptr, nullptr, nullptr, &gio);
-        ensure_h2d(G - 1);
-        for (int gq = 0; gq < G; ++gq)  // groups without lost blocks come back unchanged
-            if (!down[static_cast<size_t>(gq)]) gio.on_done(gq, ctx->io);
+        try {
+            if (n > 0)
+                ro = run_job(ctx, plan->job, plan->cfg, fr, fofse::SYN_IMAGE, d_sq, nullptr, nullptr, nullptr, nullptr,
+                             &gio);
+            ensure_h2d(G - 1);
+            for (int gq = 0; gq < G; ++gq)  // groups without lost blocks come back unchanged
+                if (!down[static_cast<size_t>(gq)]) gio.on_done(gq, ctx->io);
+        } catch (...) {
+            // the caller's host buffers may still be in flight on the copy streams
+            cudaStreamSynchronize(ctx->io);
+            cudaStreamSynchronize(ctx->stream);
+            throw;
+        }
         std::vector<double> sq(static_cast<size_t>(n));
         if (n) ck(cudaMemcpyAsync(sq.data(), d_sq, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream), "D2H sq");
         ck(cudaStreamSynchronize(ctx->stream), "sync");
