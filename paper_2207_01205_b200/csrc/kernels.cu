@@ -175,14 +175,14 @@ __global__ void __launch_bounds__(256) k1_kernel(K1Args a) {
             }
         }
         if (a.wplanar32) {
-            // complex W as four fp32 planes: (Re, Im) x (even: W[c], odd: W[c+1]), periodic
+            // complex W as four fp32 planes [copy][Re, Im] (copy 0: W[c], copy 1: W[c+1]), periodic
             const int srv = v2_srv(T);
             float* o = a.wplanar32 + (size_t)b * 4 * T * srv;
             for (int i = threadIdx.x; i < 4 * T * srv; i += blockDim.x) {
                 const int pl = i / (T * srv), rem = i % (T * srv);
-                const int r = rem / srv, col = rem % srv + (pl & 1);
+                const int r = rem / srv, col = rem % srv + (pl >> 1);
                 const double2 w = k1_spec<T>(cbuf, r, col % T);
-                o[i] = static_cast<float>((pl >> 1) ? w.y : w.x);
+                o[i] = static_cast<float>((pl & 1) ? w.y : w.x);
             }
         }
         if (threadIdx.x == 0 && a.w0) a.w0[b] = cbuf[0].x;

@@ -49,6 +49,7 @@ struct DCfg {
     static constexpr unsigned long long KMASK = ~0ull << KBITS;
     static constexpr bool REAL = true;
     static constexpr size_t IMG_BYTES = (size_t)NCOPY * T * SRV * sizeof(double);
+    static constexpr size_t CLASS_BYTES = IMG_BYTES;  // class stride of the image array
     static constexpr bool TW64 = true;
     static constexpr bool P32 = false;
     static constexpr size_t WBYTES = ((IMG_BYTES + 15) / 16) * 16;
@@ -599,6 +600,7 @@ struct DCCfg {
     static constexpr int GROUPS = 256 / GT;
     static constexpr bool REAL = false;
     static constexpr size_t IMG_BYTES = (size_t)T * SR * sizeof(double2);
+    static constexpr size_t CLASS_BYTES = IMG_BYTES;  // class stride of the image array
     static constexpr bool TW64 = true;
     static constexpr bool P32 = false;
     static constexpr size_t WBYTES = ((IMG_BYTES + 15) / 16) * 16;

@@ -46,6 +46,7 @@ struct V2Cfg {
     // REAL: two float copies (even / odd aligned) of the rotated V; else complex W
     static constexpr size_t WELEMS = REAL ? (size_t)NCOPY * T * SRV : (size_t)T * SR;
     static constexpr size_t IMG_BYTES = WELEMS * (REAL ? 4 : 8);
+    static constexpr size_t CLASS_BYTES = IMG_BYTES;  // class stride of the image array
     static constexpr bool TW64 = false;
     static constexpr bool P32 = true;  // fp32 rotated-frame phase table
     static constexpr size_t WBYTES = ((IMG_BYTES + 15) / 16) * 16;
@@ -449,6 +450,7 @@ struct V2HCfg {
     static constexpr bool REAL = true;
     static constexpr size_t WELEMS = (size_t)NCOPY * T * SRV;
     static constexpr size_t IMG_BYTES = WELEMS * 4;
+    static constexpr size_t CLASS_BYTES = IMG_BYTES;  // class stride of the image array
     static constexpr bool TW64 = false;
     static constexpr bool P32 = true;
     static constexpr size_t WBYTES = ((IMG_BYTES + 15) / 16) * 16;
@@ -738,7 +740,7 @@ __global__ void __launch_bounds__(V2HCfg<T>::THREADS, V2HCfg<T>::MINB) k2v2h_ker
 // R[k] -= c W[k-u] + conj(c) W[k+u] (engine_spectral.cpp:112-125), 8 FFMA2
 // and 4 LDS.64 per bin pair.
 // ============================================================================
-template <int T>
+template <int T, int NC = 2>
 struct V2PCfg {
     static constexpr int SEG = v2_seg(T);
     static constexpr int SPT = v2_spt(T);
@@ -750,7 +752,11 @@ struct V2PCfg {
     static constexpr int WARPS = 4;
     static constexpr bool REAL = false;
     static constexpr size_t PLANE = (size_t)T * SRV;  // floats per plane
-    static constexpr size_t IMG_BYTES = 4 * PLANE * 4;
+    // class image: planes [copy][Re, Im], copy c holds W[col + c]; NC = 1 stages
+    // only copy 0 (half the shared memory: 3 CTAs / SM instead of 2) and reads
+    // the odd-aligned bin pairs as two 4-byte loads
+    static constexpr size_t IMG_BYTES = 2 * NC * PLANE * 4;
+    static constexpr size_t CLASS_BYTES = 4 * PLANE * 4;
     static constexpr bool TW64 = false;
     static constexpr bool P32 = true;
     static constexpr size_t WBYTES = ((IMG_BYTES + 15) / 16) * 16;
@@ -763,9 +769,9 @@ struct V2PCfg {
     static_assert(NT <= 32, "one warp per block");
 };
 
-template <int T>
+template <int T, int NC>
 __global__ void __launch_bounds__(128, 3) k2v2c_kernel(K2Args a) {
-    using Cf = V2PCfg<T>;
+    using Cf = V2PCfg<T, NC>;
     constexpr int SEG = Cf::SEG, SPT = Cf::SPT, NT = Cf::NT, NP = Cf::NP, SRV = Cf::SRV;
     constexpr int PPS = SEG / 2;
     constexpr size_t PL = Cf::PLANE;
@@ -774,8 +780,8 @@ __global__ void __launch_bounds__(128, 3) k2v2c_kernel(K2Args a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const Tile tile = a.tiles[blockIdx.x];
     v2_stage<Cf>(a, tile, smem_raw);
-    const float* wre = reinterpret_cast<const float*>(smem_raw);  // [copy][T][SRV], copy c holds W[col + c]
-    const float* wim = wre + 2 * PL;
+    const float* wre = reinterpret_cast<const float*>(smem_raw);  // copy 0: Re plane, Im plane
+    const float* wim = wre + PL;
     const float2* twi = reinterpret_cast<const float2*>(smem_raw + Cf::OFF_TW);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -922,9 +928,10 @@ __global__ void __launch_bounds__(128, 3) k2v2c_kernel(K2Args a) {
             }
 
             // ---- R[k] -= c W[k-u] + conj(c) W[k+u] on bin pairs (+ next scan) ----
-            const int par = u2 & 1;
-            const float* pre_re = wre + par * PL;  // odd copy holds W[c+1]
-            const float* pre_im = wim + par * PL;
+            const int par = NC == 2 ? (u2 & 1) : 0;
+            const float* pre_re = wre + par * 2 * PL;  // odd copy holds W[c+1]
+            const float* pre_im = wim + par * 2 * PL;
+            const bool odd = NC == 1 && (u2 & 1);  // unaligned pairs (single copy)
             const float2 ncr = make_float2(-c_re, -c_re), pci = make_float2(c_im, c_im), nci = make_float2(-c_im, -c_im);
 #pragma unroll
             for (int k = 0; k <= ACC; ++k) A[k] = KAcc{0.f, 0.f};
@@ -933,11 +940,37 @@ __global__ void __launch_bounds__(128, 3) k2v2c_kernel(K2Args a) {
                 const int k1 = k1s[s], c0 = c0s[s];
                 const int rA = (k1 - u1) & (T - 1), rB = (k1 + u1) & (T - 1);
                 const int cA = (c0 - u2) & (T - 1), cB = (c0 + u2) & (T - 1);
-                const float2* ar = reinterpret_cast<const float2*>(pre_re + rA * SRV + (cA - par));
-                const float2* ai = reinterpret_cast<const float2*>(pre_im + rA * SRV + (cA - par));
-                const float2* br = reinterpret_cast<const float2*>(pre_re + rB * SRV + (cB - par));
-                const float2* bi = reinterpret_cast<const float2*>(pre_im + rB * SRV + (cB - par));
-                if (self) {
+                const float* far = pre_re + rA * SRV + (cA - par);
+                const float* fai = pre_im + rA * SRV + (cA - par);
+                const float* fbr = pre_re + rB * SRV + (cB - par);
+                const float* fbi = pre_im + rB * SRV + (cB - par);
+                const float2* ar = reinterpret_cast<const float2*>(far);
+                const float2* ai = reinterpret_cast<const float2*>(fai);
+                const float2* br = reinterpret_cast<const float2*>(fbr);
+                const float2* bi = reinterpret_cast<const float2*>(fbi);
+                if (NC == 1 && odd) {
+                    // single copy, odd shift: two 4-byte loads per pair (warp-uniform branch)
+                    auto ld = [](const float* v, int q) { return make_float2(v[2 * q], v[2 * q + 1]); };
+                    if (self) {
+#pragma unroll
+                        for (int q = 0; q < PPS; ++q) {
+                            const int p = s * PPS + q;
+                            const float2 xr2 = ld(far, q), xi2 = ld(fai, q);
+                            rp[p] = __ffma2_rn(ncr, xr2, __ffma2_rn(pci, xi2, rp[p]));
+                            ip[p] = __ffma2_rn(ncr, xi2, __ffma2_rn(nci, xr2, ip[p]));
+                            kacc_pair(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+                        }
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < PPS; ++q) {
+                            const int p = s * PPS + q;
+                            const float2 xr2 = ld(far, q), xi2 = ld(fai, q), yr2 = ld(fbr, q), yi2 = ld(fbi, q);
+                            rp[p] = __ffma2_rn(nci, yi2, __ffma2_rn(ncr, yr2, __ffma2_rn(pci, xi2, __ffma2_rn(ncr, xr2, rp[p]))));
+                            ip[p] = __ffma2_rn(pci, yr2, __ffma2_rn(ncr, yi2, __ffma2_rn(nci, xr2, __ffma2_rn(ncr, xi2, ip[p]))));
+                            kacc_pair(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+                        }
+                    }
+                } else if (self) {
 #pragma unroll
                     for (int q = 0; q < PPS; ++q) {
                         const int p = s * PPS + q;
@@ -1023,12 +1056,19 @@ static int v2r_variant() {
 template <int T, int PATH>
 static int k2v2_launch_t(const K2Args& a, int32_t ntiles, cudaStream_t s) {
     if constexpr (PATH == PATH_F32_COMPLEX) {
-        using Cf = V2PCfg<T>;
-        cudaError_t e = cudaFuncSetAttribute(k2v2c_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
-        if (e != cudaSuccess) return e;
-        if (ntiles <= 0) return cudaSuccess;
-        k2v2c_kernel<T><<<ntiles, 32 * Cf::WARPS, Cf::SMEM, s>>>(a);
-        return cudaGetLastError();
+        // single-copy W planes by default (FOFSE_V2C_COPIES=2: even/odd copies)
+        static const int nc = [] {
+            const char* e = getenv("FOFSE_V2C_COPIES");
+            return (e && e[0] == '2') ? 2 : 1;
+        }();
+        auto launch = [&](auto* fn, size_t smem) -> int {
+            cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+            if (ntiles <= 0) return cudaSuccess;
+            fn<<<ntiles, 32 * V2PCfg<T>::WARPS, smem, s>>>(a);
+            return cudaGetLastError();
+        };
+        return nc == 2 ? launch(k2v2c_kernel<T, 2>, V2PCfg<T, 2>::SMEM) : launch(k2v2c_kernel<T, 1>, V2PCfg<T, 1>::SMEM);
     } else {
         using Cf = V2Cfg<T, PATH>;
         auto* fn = v2r_variant() == 3   ? k2v2r_kernel<T, 3>

@@ -39,8 +39,8 @@ __device__ __forceinline__ void v2_stage(const K2Args& a, const Tile& tile, unsi
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Cf::OFF_BAR);
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
-        const uint32_t bytes = static_cast<uint32_t>(Cf::IMG_BYTES);
-        const char* src = static_cast<const char*>(a.wimg) + (size_t)tile.cls * bytes;
+        const uint32_t bytes = static_cast<uint32_t>(Cf::IMG_BYTES);  // staged prefix of the class image
+        const char* src = static_cast<const char*>(a.wimg) + (size_t)tile.cls * Cf::CLASS_BYTES;
         mbar_expect_tx(bar, bytes);
         for (uint32_t off = 0; off < bytes; off += 32768)
             bulk_g2s(smem + off, src + off, bytes - off < 32768u ? bytes - off : 32768u, bar);
