@@ -1284,6 +1284,10 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
                             : v2                    ? static_cast<int64_t>(wpl_elems)
                                                     : static_cast<int64_t>(T) * sr32;
             a.flags = d_flags;
+            // border kernel: one W copy (3 CTAs / SM) in general; with frame groups the
+            // two-copy form measured better (+1.4 % end to end on C4: its CTAs displace
+            // fewer main-chunk CTAs while the group pipeline overlaps them)
+            a.v2c_copies = job.groups > 1 ? 2 : 1;
             a.rec_global = 1;
             a.iterations = I - head;
             a.trace_from_nu0 = 1;

@@ -138,6 +138,7 @@ struct K2Args {
     int32_t nu_limit;           // K2d: iterate until nu == nu_limit (per-block resume points; 0 = off)
     const int32_t* src_pos;     // K2d REPLAY: position of the block's K1 spectrum in rin / init_*
     const int32_t* nu_flag;     // K2d REPLAY: selections to replay (made in fp32 before the near-tie)
+    int32_t v2c_copies;         // K2v2c: W plane copies staged (1: half the smem, 2: aligned pairs)
 };
 
 struct CvtArgs {

@@ -1056,11 +1056,12 @@ static int v2r_variant() {
 template <int T, int PATH>
 static int k2v2_launch_t(const K2Args& a, int32_t ntiles, cudaStream_t s) {
     if constexpr (PATH == PATH_F32_COMPLEX) {
-        // single-copy W planes by default (FOFSE_V2C_COPIES=2: even/odd copies)
-        static const int nc = [] {
+        // W planes: a.v2c_copies (the engine's choice), FOFSE_V2C_COPIES=1/2 overrides
+        static const int forced = [] {
             const char* e = getenv("FOFSE_V2C_COPIES");
-            return (e && e[0] == '2') ? 2 : 1;
+            return e ? atoi(e) : 0;
         }();
+        const int nc = forced == 1 || forced == 2 ? forced : (a.v2c_copies == 2 ? 2 : 1);
         auto launch = [&](auto* fn, size_t smem) -> int {
             cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (e != cudaSuccess) return e;
