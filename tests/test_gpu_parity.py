@@ -500,6 +500,31 @@ def test_frames_u8_matches_f64_and_is_deterministic(gpu):
     assert rep.device["blocks"] == offs[-1]
 
 
+@pytest.mark.parametrize("nframes", [40, 130])
+def test_frame_groups_match_single_frames(gpu, nframes):
+    """The pipelined frames API with frame groups (40 frames: 2 groups; 130: 8
+    groups, first/last a quarter of the others; lazily queued uploads, per-group
+    downloads, two-copy border kernel) gives, frame by frame, the bytes and block
+    errors of concealing each frame on its own."""
+    rng = np.random.default_rng(487)
+    H = W = 160
+    frames = np.stack([np.clip(smooth_test_image(rng, H) + 0.0, 0, 255).astype(np.uint8) for _ in range(nframes)])
+    pats = []
+    for f in range(nframes):
+        rr = P.gen_losses(500 + f, W // 16, H // 16, 0.12, 16, 16)
+        pats.append(P.LossPattern(W, H, 16, 16, [P.Rect(*map(int, (r["row"], r["col"], 16, 16))) for r in rr]))
+    cfg = WL.C4.config("fp32")
+    out, sq, rep = P.conceal_frames(frames, pats, cfg)
+    k = 0
+    for f in range(0, nframes, 7):
+        one, sq1, _ = P.conceal_frames(frames[f:f + 1], pats[f:f + 1], cfg)
+        np.testing.assert_array_equal(one[0], out[f])
+        n0 = sum(len(p.blocks) for p in pats[:f])
+        np.testing.assert_array_equal(sq1, sq[n0:n0 + len(pats[f].blocks)])
+        k += 1
+    assert k > 3 and rep.device["blocks"] == sum(len(p.blocks) for p in pats)
+
+
 def test_shards_reassemble_the_full_run(gpu):
     """fofse_conceal_shard_f64: disjoint shards (every block still lost) reproduce
     the single-call result bit for bit — the multi-GPU decomposition."""
