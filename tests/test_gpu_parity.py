@@ -286,6 +286,25 @@ def test_conceal_fp64_small_transforms(gpu, orc, t, b, sw):
     assert np.abs(out.restored - ref["restored"]).max() <= FP64_PX_TOL
 
 
+@pytest.mark.parametrize("t,b,sw", [(8, 4, 2), (16, 8, 4), (32, 16, 8)])
+def test_conceal_fp32_small_transforms(gpu, orc, t, b, sw):
+    """fp32 fast mode at T = 8/16/32 (K2v2r with idle lanes for T < 32, the
+    fp64 head, the guard) vs the fp64 oracle: <= 0.5 px, <= 0.05 dB."""
+    rng = np.random.default_rng(503 + t + b)
+    img = smooth_test_image(rng, 128)
+    cells = [(r, c) for r in range(0, 128 - b + 1, 3 * b) for c in range(0, 128 - b + 1, 3 * b)]
+    pat = P.LossPattern(128, 128, b, b, [P.Rect(r, c, b, b) for r, c in cells])
+    cfg = P.ConcealConfig(gamma=0.5, iterations=60, transform_size=t, support_width=sw, precision="fp32")
+    out = P.conceal(img, pat, cfg)
+    ref = _oracle_conceal(orc, img, pat, P.ConcealConfig(gamma=0.5, iterations=60, transform_size=t,
+                                                         support_width=sw), traces=False)
+    lost = np.zeros(img.shape, bool)
+    for r, c in cells:
+        lost[r:r + b, c:c + b] = True
+    assert _fp32_vs_ref(out.restored, ref["restored"], lost) <= FP32_PX_TOL
+    assert abs(out.report.psnr_db - ref["psnr_db"]) <= FP32_PSNR_TOL
+
+
 def test_conceal_ofse_vs_oracle(gpu, orc):
     """pipeline ofse (fast_iterate_full_od per window, pipeline.cpp:194-196): K2d with
     the rotated-frame d reduction (interior masks) and the strict kernel (border and
