@@ -305,6 +305,40 @@ def test_conceal_fp32_small_transforms(gpu, orc, t, b, sw):
     assert abs(out.report.psnr_db - ref["psnr_db"]) <= FP32_PSNR_TOL
 
 
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+@pytest.mark.parametrize("case", ["zero_iterations", "constant", "black", "white", "corners"])
+def test_conceal_edge_cases_vs_oracle(gpu, orc, precision, case):
+    """Edge inputs through the whole path in both precisions, against the oracle:
+    I = 0 (empty model: the hole is 0 after the clamp), constant / black /
+    saturated images (black: zero energy converges at once; constant: the
+    selections approach the DC value), and lost blocks in all four corners
+    (every border class)."""
+    rng = np.random.default_rng(509)
+    img = smooth_test_image(rng, 96)
+    iters = 0 if case == "zero_iterations" else 40
+    if case == "constant":
+        img = np.full((96, 96), 137.0)
+    elif case == "black":
+        img = np.zeros((96, 96))
+    elif case == "white":
+        img = np.full((96, 96), 255.0)
+    blocks = [(0, 0), (0, 80), (80, 0), (80, 80), (40, 40)] if case == "corners" else [(16, 16), (48, 64)]
+    pat = P.LossPattern(96, 96, 16, 16, [P.Rect(r, c, 16, 16) for r, c in blocks])
+    cfg = P.ConcealConfig(gamma=0.5, iterations=iters, precision=precision)
+    out = P.conceal(img, pat, cfg)
+    ref = _oracle_conceal(orc, img, pat, P.ConcealConfig(gamma=0.5, iterations=iters), traces=False)
+    lost = np.zeros(img.shape, bool)
+    for r, c in blocks:
+        lost[r:r + 16, c:c + 16] = True
+    tol = FP64_PX_TOL if precision == "fp64" else FP32_PX_TOL
+    assert np.abs(out.restored - ref["restored"]).max() <= tol
+    np.testing.assert_array_equal(out.restored[~lost], img[~lost])
+    if case == "black":  # zero residual energy: converged before the first selection
+        assert not out.restored[lost].any()
+    elif case in ("constant", "white"):  # the DC-led selections approach the constant
+        np.testing.assert_allclose(out.restored[lost], img[lost], atol=1e-3)
+
+
 def test_conceal_ofse_vs_oracle(gpu, orc):
     """pipeline ofse (fast_iterate_full_od per window, pipeline.cpp:194-196): K2d with
     the rotated-frame d reduction (interior masks) and the strict kernel (border and
