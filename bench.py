@@ -356,7 +356,8 @@ def main():
             pass
         peak = peaks.get("smem_gbs")
         T = wl.transform_size
-        k32 = f"fofse::k2v2h_kernel<{T}>" if T == 128 else f"fofse::k2v2r_kernel<{T}>"
+        k32 = (f"fofse::k2v2h_kernel<{T}>" if T == 128
+               else f"fofse::k2v2r_kernel<{T}>" + (" or k2v2h_kernel<64> (jobs of about one wave)" if T == 64 and n_blocks < 8192 else ""))
         kname = (f"{k32} (fp32 rotated-frame iterate + fused synthesis)" if prec == "fp32"
                  else f"fofse::k2d_kernel<{T}> / k2_kernel (fp64 iterate + fused synthesis)")
         roof = {"bound": "smem", "kernel": kname,

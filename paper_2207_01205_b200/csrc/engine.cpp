@@ -820,7 +820,21 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
     // from seg_for(T, 0); K2v2 uses v2_seg(T) — equal for every T).
     double2* d_wimg64 = ctx->buf("wimg64").as<double2>(static_cast<size_t>(ncls) * T * sr64);
     float2* d_wimg32 = fp32 ? ctx->buf("wimg32").as<float2>(static_cast<size_t>(ncls) * T * sr32) : nullptr;
-    const int vcopies = v2r ? v2_real_copies(T) : 1;
+    // K2v2r vs K2v2h at T = 64 for this job (its real-path block count)
+    int real_gw = 1;
+    if (v2 && T == 64) {
+        int64_t n_real = 0;
+        if (n <= 65536) {
+            std::vector<int64_t> cc(static_cast<size_t>(ncls), 0);
+            for (const BlockDesc& d : job.blocks) ++cc[static_cast<size_t>(d.cls)];
+            for (int c = 0; c < ncls; ++c)
+                if (sym[static_cast<size_t>(c)]) n_real += cc[static_cast<size_t>(c)];
+        } else {
+            n_real = n;  // large jobs: the throughput form regardless of the border share
+        }
+        real_gw = v2_choose_real_gw(T, n_real, ctx->device);
+    }
+    const int vcopies = v2r ? v2_real_copies(T, real_gw) : 1;
     const size_t vimg_elems = !v2r ? static_cast<size_t>(T) * sr32
                               : vcopies == 4 ? 4 * static_cast<size_t>(T) * v2_srv4(T)
                                              : 2 * static_cast<size_t>(T) * v2_srv(T);
@@ -1041,7 +1055,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
     auto soa_of = [&](int path) {
         return ((v2r && path == PATH_F32_REAL) || (v2 && path == PATH_F32_COMPLEX)) ? 1 : 0;
     };
-    auto spt_of = [&](int path) { return (v2r && path == PATH_F32_REAL) ? v2_real_spt(T) : spt32; };
+    auto spt_of = [&](int path) { return (v2r && path == PATH_F32_REAL) ? v2_real_spt(T, real_gw) : spt32; };
     const BinLayout L32r = BinLayout::make(T, seg32, spt_of(PATH_F32_REAL));
     const int64_t s32 = static_cast<int64_t>(std::max(packed32_floats(L32, 0), packed32_floats(L32r, soa_of(PATH_F32_REAL))));
     if (fp32) d_R32 = ctx->buf("R32").as<char>(static_cast<size_t>(n) * sizeof(float) * s32);
@@ -1119,7 +1133,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         const int64_t one_wave = 2LL * nsm;  // a border range this small goes on the high-priority stream
         // real ranges: chunks of a whole number of the fp32 kernel's waves (the
         // last takes the remainder), at least chunk_min blocks, at most 8 per range
-        const int64_t wave = v2r ? k2v2_real_wave(T, ctx->device) : 0;
+        const int64_t wave = v2r ? k2v2_real_wave(T, ctx->device, real_gw) : 0;
         for (const Range& r : ranges) {
             const bool on_side = r.path == PATH_F32_COMPLEX && ranges.size() > 1;
             const int64_t len = r.end - r.begin;
@@ -1288,6 +1302,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             // two-copy form measured better (+1.4 % end to end on C4: its CTAs displace
             // fewer main-chunk CTAs while the group pipeline overlaps them)
             a.v2c_copies = job.groups > 1 ? 2 : 1;
+            a.real_gw = real_gw;
             a.rec_global = 1;
             a.iterations = I - head;
             a.trace_from_nu0 = 1;

@@ -139,6 +139,7 @@ struct K2Args {
     const int32_t* src_pos;     // K2d REPLAY: position of the block's K1 spectrum in rin / init_*
     const int32_t* nu_flag;     // K2d REPLAY: selections to replay (made in fp32 before the near-tie)
     int32_t v2c_copies;         // K2v2c: W plane copies staged (1: half the smem, 2: aligned pairs)
+    int32_t real_gw;            // K2v2 real path at T = 64: warps per lost block (1: K2v2r, 2: K2v2h)
 };
 
 struct CvtArgs {
@@ -174,7 +175,7 @@ int k2d_blocks_per_cta(int T);
 bool k2d_replay_fits(int T, int rstride);
 int k2v2_warps_per_cta(int t);
 // Lost blocks per full wave of the fp32 real-path kernel on device dev (0 = unknown).
-int64_t k2v2_real_wave(int t, int dev);
+int64_t k2v2_real_wave(int t, int dev, int gw);
 int cvt_launch(const CvtArgs& a, cudaStream_t s);
 
 // Tile lists on the device: `runs` = nruns (begin, end, cls, first tile) rows of

@@ -1097,7 +1097,7 @@ static int k2v2h_launch(const K2Args& a, int32_t ntiles, cudaStream_t s) {
 template <int T>
 static int k2v2_T(const K2Args& a, int32_t ntiles, cudaStream_t s) {
     if constexpr (T == 64)
-        if (a.path == PATH_F32_REAL && v2_real_gw(T) == 2) return k2v2h_launch<64>(a, ntiles, s);
+        if (a.path == PATH_F32_REAL && a.real_gw == 2) return k2v2h_launch<64>(a, ntiles, s);
     if (a.path == PATH_F32_REAL) return k2v2_launch_t<T, PATH_F32_REAL>(a, ntiles, s);
     if (a.path == PATH_F32_COMPLEX) return k2v2_launch_t<T, PATH_F32_COMPLEX>(a, ntiles, s);
     return cudaErrorInvalidValue;
@@ -1138,8 +1138,8 @@ static int64_t wave_t(int dev) {
     }
 }
 
-int64_t k2v2_real_wave(int t, int dev) {
-    if (v2_real_gw(t) == 2 || v2r_variant() != 0) return 0;  // experiments: no alignment
+int64_t k2v2_real_wave(int t, int dev, int gw) {
+    if ((t == 64 && gw == 2) || v2r_variant() != 0) return 0;  // K2v2h at T = 64 / experiments: no alignment
     switch (t) {
         case 8: return wave_t<8>(dev);
         case 16: return wave_t<16>(dev);
@@ -1150,9 +1150,9 @@ int64_t k2v2_real_wave(int t, int dev) {
     return 0;
 }
 
-int v2_real_copies(int t) {
+int v2_real_copies(int t, int gw) {
     if (t == 128) return V2HCfg<128>::NCOPY;
-    if (v2_real_gw(t) == 2) return 4;  // K2v2h: quad layout
+    if (t == 64 && gw == 2) return 4;  // K2v2h: quad layout
     return (v2r_variant() == 3 || v2r_variant() == 9) ? 4 : 2;
 }
 
@@ -1165,13 +1165,29 @@ bool v2h128_enabled() {
     return on != 0;
 }
 
-static int g_real_gw = -1;
-int v2_real_gw(int t) {
-    if (g_real_gw < 0) {
+int v2_choose_real_gw(int t, int64_t real_blocks, int dev) {
+    if (t != 64) return 1;
+    static const int forced = [] {
         const char* e = getenv("FOFSE_V2_REAL_GW");
-        g_real_gw = e ? atoi(e) : 1;
-    }
-    return (t == 64 && g_real_gw == 2) ? 2 : 1;
+        return e ? atoi(e) : 0;
+    }();
+    if (forced == 1 || forced == 2) return forced;
+    if (v2r_variant() != 0 || real_blocks <= 0) return 1;
+    // makespan in per-block latencies: K2v2r ceil(N / W1) x 1, K2v2h ceil(N / W2) x 0.7
+    // (the latency ratio measured on C4: 21 K2v2h waves take 1.04 x 14 K2v2r waves)
+    int nsm = 0, p1 = 0, p2 = 0;
+    if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 1;
+    using C1 = V2Cfg<64, PATH_F32_REAL>;
+    using C2 = V2HCfg<64>;
+    cudaFuncSetAttribute(k2v2r_kernel<64, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C1::SMEM);
+    cudaFuncSetAttribute(k2v2h_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C2::SMEM);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p1, k2v2r_kernel<64, 0>, 32 * C1::WARPS, C1::SMEM) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2, k2v2h_kernel<64>, C2::THREADS, C2::SMEM) != cudaSuccess)
+        return 1;
+    const int64_t w1 = (int64_t)nsm * p1 * C1::WARPS, w2 = (int64_t)nsm * p2 * C2::GROUPS;
+    if (w1 <= 0 || w2 <= 0) return 1;
+    const double m1 = (double)((real_blocks + w1 - 1) / w1), m2 = 0.7 * (double)((real_blocks + w2 - 1) / w2);
+    return m2 < m1 ? 2 : 1;
 }
 
 template <int T>

@@ -19,6 +19,7 @@
 #pragma once
 
 #include <stddef.h>
+#include <stdint.h>
 
 #ifdef __CUDACC__
 #define FOFSE_HD __host__ __device__ __forceinline__
@@ -126,13 +127,15 @@ FOFSE_HDC int v2_srv(int t) { return t + v2_seg(t) + 2; }
 // Quad layout: four copies C_k[c] = V[c + k] with a row stride that is a
 // multiple of 4, so any 4 consecutive columns are one aligned 16-byte load.
 FOFSE_HDC int v2_srv4(int t) { return ((t + v2_seg(t) + 4 + 3) / 4) * 4; }
-// Warps per lost block of the K2v2 real path: T = 64 splits the block over two
-// warps (one 32-column segment each), smaller T keep one warp.
-// (host override for experiments: v2_set_real_gw)
-int v2_real_gw(int t);
-inline int v2_real_spt(int t) { return v2_real_gw(t) == 2 ? 1 : v2_spt(t); }
+// Warps per lost block of the K2v2 real path at T = 64, chosen per job: 1 (K2v2r,
+// the throughput form) or 2 (K2v2h: a 32-column segment per warp, ~0.7x the
+// per-block latency at 2/3 of the blocks per wave — better when the job is a
+// wave or two, where the partial last wave sets the time). v2_choose_real_gw
+// decides from the job's real-path block count; FOFSE_V2_REAL_GW=1/2 forces.
+int v2_choose_real_gw(int t, int64_t real_blocks, int dev);
+inline int v2_real_spt(int t, int gw) { return (t == 64 && gw == 2) ? 1 : v2_spt(t); }
 // Copies of V in the K2v2 real path's class image (2: even/odd pairs, 4: quads).
-int v2_real_copies(int t);
+int v2_real_copies(int t, int gw);
 // T = 128 fp32 real path on K2v2h (8 warps per lost block); FOFSE_K2_128=v1
 // keeps the older K2 kernel (experiments).
 bool v2h128_enabled();
