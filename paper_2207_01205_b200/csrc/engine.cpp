@@ -1023,18 +1023,21 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
                       d_R64 + static_cast<size_t>(r.begin) * r64_bytes, d_e0 + r.begin, d_imax + r.begin);
     }
     // one fp64 iteration launch over positions [b0, b1) of `descs` (K2d or strict)
-    auto ng_f64 = [&](int hp) {
-        return (hp == PATH_F64_REAL || hp == PATH_F64_CPLX) ? k2d_blocks_per_cta(T) : k2_groups_per_cta(T, PATH_F64_STRICT);
+    auto ng_f64 = [&](int hp, bool wide = false) {
+        return (hp == PATH_F64_REAL || hp == PATH_F64_CPLX) ? k2d_blocks_per_cta(T, wide && hp == PATH_F64_REAL)
+                                                            : k2_groups_per_cta(T, PATH_F64_STRICT);
     };
     // pre: tiles already on the device (the chunk pipeline uploads all of its tile
     // lists in one copy up front)
     auto k2_f64 = [&](K2Args a, int hp, int64_t b0, int64_t b1, const std::vector<BlockDesc>& descs,
-                      const std::string& tag, cudaStream_t s, const Tile* pre = nullptr, size_t npre = 0) {
+                      const std::string& tag, cudaStream_t s, const Tile* pre = nullptr, size_t npre = 0,
+                      bool wide = false) {
         const bool fast = hp == PATH_F64_REAL || hp == PATH_F64_CPLX;
+        a.d_wide = (wide && hp == PATH_F64_REAL) ? 1 : 0;
         std::vector<Tile> tl;
         const Tile* d_tl = pre;
         if (!pre) {
-            tl = make_tiles(b0, b1, descs, ng_f64(hp));
+            tl = make_tiles(b0, b1, descs, ng_f64(hp, wide));
             d_tl = upload(ctx, "tiles64" + tag, tl.data(), tl.size(), s);
             npre = tl.size();
         }
@@ -1217,6 +1220,10 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             const char* e = std::getenv("FOFSE_RESUME");
             return !(e && e[0] == '0');
         }();
+        const bool wide_reruns = [] {  // FOFSE_WIDE_RERUNS=0: re-runs on the standard K2d form
+            const char* e = std::getenv("FOFSE_WIDE_RERUNS");
+            return !(e && e[0] == '0');
+        }();
         ck(cudaStreamWaitEvent(ctx->aux, ctx->ev[4], 0), "wait");
         std::vector<char> waited(static_cast<size_t>(2 * ngroups), 0);  // [group][main/side] upload waits
         // per chunk: events [3i] after K1, [3i+1] before the fp32 iteration, [3i+2] done
@@ -1365,7 +1372,13 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             // re-run buffers are sized for the largest chunk and reused in stream order (aux)
             BlockDesc* d_rdesc = ctx->buf("rdesc").as<BlockDesc>(static_cast<size_t>(max_chunk));
             int32_t* d_rr = ctx->buf("rr").as<int32_t>(static_cast<size_t>(max_chunk));
-            char* d_Rr = ctx->buf("Rr").as<char>(static_cast<size_t>(max_chunk) * r64_bytes);
+            // the last chunk's re-runs are the job's tail: K2d's WIDE form there (half the
+            // bins per thread: ~0.65x the latency); earlier re-runs overlap later chunks,
+            // where the standard form's throughput is better (measured: C2 +5 %, C4
+            // -2 % with WIDE everywhere). Its packed layout has more slots.
+            const bool wide = wide_reruns && T <= 64 && ci + 1 == chunks.size();
+            const size_t rr_bytes = std::max(r64_bytes, sizeof(double2) * BinLayout::make(T, k2d_wide_seg(T)).SLOTS);
+            char* d_Rr = ctx->buf("Rr").as<char>(static_cast<size_t>(max_chunk) * rr_bytes);
             double* d_re0 = ctx->buf("re0").as<double>(static_cast<size_t>(max_chunk));
             double* d_rimax = ctx->buf("rimax").as<double>(static_cast<size_t>(max_chunk));
             if (!rr.empty()) {  // from scratch: K1 + all I selections in fp64
@@ -1382,8 +1395,9 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
                 a.init_max = d_rimax;
                 a.rec_global = 0;  // strict: smem records (or the per-block global scratch when I > cap)
                 const int hp = hi_path(ch.path);
-                k1_packed(d_rdesc, m, hp, seg64, 1, d_Rr, d_re0, d_rimax, 0, 0, ctx->aux);
-                k2_f64(a, hp, 0, m, rdesc, tag, ctx->aux);
+                const bool w = wide && hp == PATH_F64_REAL;
+                k1_packed(d_rdesc, m, hp, w ? k2d_wide_seg(T) : seg64, 1, d_Rr, d_re0, d_rimax, 0, 0, ctx->aux);
+                k2_f64(a, hp, 0, m, rdesc, tag, ctx->aux, nullptr, 0, w);
             }
             if (!rs.empty()) {  // resumed: K2d REPLAY rebuilds the fp64 state at the near-tie and goes on
                 const int64_t m = static_cast<int64_t>(rs.size());
@@ -1405,7 +1419,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
                 a.nu_limit = I;
                 a.rec_global = 1;
                 a.trace_from_nu0 = 1;
-                k2_f64(a, PATH_F64_REAL, 0, m, sdesc, tag, ctx->aux);
+                k2_f64(a, PATH_F64_REAL, 0, m, sdesc, tag, ctx->aux, nullptr, 0, wide);
             }
             // a frame group is complete once its last chunk and its re-runs are done
             const bool last_of_group = ci + 1 == chunks.size() || chunks[ci + 1].grp != ch.grp;

@@ -140,6 +140,7 @@ struct K2Args {
     const int32_t* nu_flag;     // K2d REPLAY: selections to replay (made in fp32 before the near-tie)
     int32_t v2c_copies;         // K2v2c: W plane copies staged (1: half the smem, 2: aligned pairs)
     int32_t real_gw;            // K2v2 real path at T = 64: warps per lost block (1: K2v2r, 2: K2v2h)
+    int32_t d_wide;             // K2d: WIDE form (T <= 64; guard re-runs)
 };
 
 struct CvtArgs {
@@ -169,7 +170,10 @@ int fft2d_launch(double2* data, int64_t n, int32_t T, int32_t dir, const double2
 int k2v2_launch(const K2Args& a, int32_t ntiles, cudaStream_t s);
 // K2d: fp64 rotated-frame iteration (PATH_F64_REAL), groups of d_group_threads(T).
 int k2d_launch(const K2Args& a, int32_t ntiles, cudaStream_t s);
-int k2d_blocks_per_cta(int T);
+int k2d_blocks_per_cta(int T, bool wide = false);
+// K2d WIDE form (a.d_wide, T <= 64): half the bins per thread; its fp64 packed
+// input layout uses this SEG.
+int k2d_wide_seg(int T);
 // K2d REPLAY mode (a.src_pos set): rebuilds a near-tie block's fp64 state after
 // its first nu_flag[pos] recorded selections, then iterates on to nu_limit.
 bool k2d_replay_fits(int T, int rstride);

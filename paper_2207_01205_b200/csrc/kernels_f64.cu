@@ -29,9 +29,11 @@
 
 namespace fofse {
 
-template <int T>
+// WIDE: half the bins per thread (twice the threads per lost block) — lower
+// per-selection latency for small launches (guard re-runs, the tail).
+template <int T, bool WIDE = false>
 struct DCfg {
-    static constexpr int SEG = seg_for(T, 1);
+    static constexpr int SEG = WIDE ? seg_for(T, 1) / 2 : seg_for(T, 1);
     static constexpr int HT = T / 2;
     static constexpr int QN = T / SEG;
     static constexpr int NT = HT * QN;             // threads holding bins
@@ -129,7 +131,10 @@ __device__ __forceinline__ void d_replay(const K2Args& a, const double* vE, cons
                                          double (&re)[Cf::SEG + 1], double (&im)[Cf::SEG + 1], double& energy_out,
                                          int& nf_out, int& conv_out) {
     constexpr int T = Cf::HT * 2, SEG = Cf::SEG, NT = Cf::NT, PPS = Cf::PPS, SRV = Cf::SRV, GT = Cf::GT;
-    const double2* R0 = static_cast<const double2*>(a.rin) + (size_t)src * L.SLOTS;
+    // R0 is stored in the fp64 packed layout of K1 (SEG = seg_for(T, 1)), which
+    // differs from the kernel's own layout in the WIDE form
+    const BinLayout Ls = BinLayout::make(T, seg_for(T, 1), 1);
+    const double2* R0 = static_cast<const double2*>(a.rin) + (size_t)src * Ls.SLOTS;
     const int* rec_u = a.rec_u_g + (size_t)b * rstride;
     double2* rec_c = a.rec_c_g + (size_t)b * rstride;
     const double e_init = a.init_energy[src], imax = a.init_max[src];
@@ -148,8 +153,8 @@ __device__ __forceinline__ void d_replay(const K2Args& a, const double* vE, cons
         for (int q = lane; q < nf; q += 32) {  // R'_0 at every selected bin, in parallel
             const int u = rec_u[q], u1 = u >> 16, u2 = u & 0xffff;
             int slot, tid;
-            bin_slot(L, u1, u2, &slot, &tid);
-            pend[q] = R0[slot * NT + tid];
+            bin_slot(Ls, u1, u2, &slot, &tid);
+            pend[q] = R0[slot * Ls.NT + tid];
             sel[q].u1 = u1;
             sel[q].u2 = u2;
         }
@@ -216,12 +221,22 @@ __device__ __forceinline__ void d_replay(const K2Args& a, const double* vE, cons
     const int nf = nf_out;
 #pragma unroll
     for (int q = 0; q < SEG; ++q) {
-        const double2 v = active ? R0[q * NT + ltid] : make_double2(0.0, 0.0);
+        double2 v = make_double2(0.0, 0.0);
+        if (active) {
+            int slot, tid;
+            bin_slot(Ls, k1, c0 + q, &slot, &tid);
+            v = R0[slot * Ls.NT + tid];
+        }
         re[q] = v.x;
         im[q] = v.y;
     }
     {
-        const double2 v = (active && ex) ? R0[SEG * NT + ltid] : make_double2(0.0, 0.0);
+        double2 v = make_double2(0.0, 0.0);
+        if (active && ex) {
+            int slot, tid;
+            bin_slot(Ls, k1, T / 2, &slot, &tid);
+            v = R0[slot * Ls.NT + tid];
+        }
         re[SEG] = v.x;
         im[SEG] = v.y;
     }
@@ -276,9 +291,9 @@ __device__ __forceinline__ void d_replay(const K2Args& a, const double* vE, cons
     }
 }
 
-template <int T, bool FOD, bool REPLAY = false>
-__global__ void __launch_bounds__(DCfg<T>::THREADS, DCfg<T>::MINB) k2d_kernel(K2Args a) {
-    using Cf = DCfg<T>;
+template <int T, bool FOD, bool REPLAY = false, bool WIDE = false>
+__global__ void __launch_bounds__(DCfg<T, WIDE>::THREADS, DCfg<T, WIDE>::MINB) k2d_kernel(K2Args a) {
+    using Cf = DCfg<T, WIDE>;
     constexpr int SEG = Cf::SEG, NT = Cf::NT, GT = Cf::GT, NW = Cf::NW, PPS = Cf::PPS, SRV = Cf::SRV;
     constexpr int NB = SEG + 1;
     constexpr unsigned long long KM = Cf::KMASK;
@@ -826,11 +841,12 @@ static int k2dc_t(const K2Args& a, int32_t ntiles, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-template <int T>
-static int k2d_t(const K2Args& a, int32_t ntiles, cudaStream_t s) {
-    using Cf = DCfg<T>;
+template <int T, bool WIDE>
+static int k2d_tw(const K2Args& a, int32_t ntiles, cudaStream_t s) {
+    using Cf = DCfg<T, WIDE>;
     const bool replay = a.src_pos != nullptr;
-    auto* fn = replay ? k2d_kernel<T, false, true> : a.full_od ? k2d_kernel<T, true> : k2d_kernel<T, false>;
+    auto* fn = replay ? k2d_kernel<T, false, true, WIDE>
+                      : a.full_od ? k2d_kernel<T, true, false, WIDE> : k2d_kernel<T, false, false, WIDE>;
     const int rstride = a.rec_stride > 0 ? a.rec_stride : a.iterations;
     const size_t smem = replay ? ((Cf::SMEM + 31) & ~size_t(31)) +
                                      (sizeof(RSel) + sizeof(double2)) * (size_t)Cf::GROUPS * rstride
@@ -841,6 +857,13 @@ static int k2d_t(const K2Args& a, int32_t ntiles, cudaStream_t s) {
     if (ntiles <= 0) return cudaSuccess;
     fn<<<ntiles, Cf::THREADS, smem, s>>>(a);
     return cudaGetLastError();
+}
+
+template <int T>
+static int k2d_t(const K2Args& a, int32_t ntiles, cudaStream_t s) {
+    if constexpr (T <= 64)
+        if (a.d_wide) return k2d_tw<T, true>(a, ntiles, s);
+    return k2d_tw<T, false>(a, ntiles, s);
 }
 
 bool k2d_replay_fits(int T, int rstride) {
@@ -877,15 +900,17 @@ int k2d_launch(const K2Args& a, int32_t ntiles, cudaStream_t s) {
     return cudaErrorInvalidValue;
 }
 
-int k2d_blocks_per_cta(int T) {
+int k2d_blocks_per_cta(int T, bool wide) {
     switch (T) {
-        case 8: return DCfg<8>::GROUPS;
-        case 16: return DCfg<16>::GROUPS;
-        case 32: return DCfg<32>::GROUPS;
-        case 64: return DCfg<64>::GROUPS;
+        case 8: return wide ? DCfg<8, true>::GROUPS : DCfg<8>::GROUPS;
+        case 16: return wide ? DCfg<16, true>::GROUPS : DCfg<16>::GROUPS;
+        case 32: return wide ? DCfg<32, true>::GROUPS : DCfg<32>::GROUPS;
+        case 64: return wide ? DCfg<64, true>::GROUPS : DCfg<64>::GROUPS;
         case 128: return DCfg<128>::GROUPS;
     }
     return 1;
 }
+
+int k2d_wide_seg(int T) { return T <= 64 ? seg_for(T, 1) / 2 : seg_for(T, 1); }
 
 }  // namespace fofse

@@ -557,8 +557,8 @@ def test_frames_u8_matches_f64_and_is_deterministic(gpu):
 def test_frame_groups_match_single_frames(gpu, nframes):
     """The pipelined frames API with frame groups (40 frames: 2 groups; 130: 8
     groups, first/last a quarter of the others; lazily queued uploads, per-group
-    downloads, two-copy border kernel) gives, frame by frame, the bytes and block
-    errors of concealing each frame on its own."""
+    downloads, two-copy border kernel) gives, frame by frame, the bytes (and the
+    block errors to rounding) of concealing each frame on its own."""
     rng = np.random.default_rng(487)
     H = W = 160
     frames = np.stack([np.clip(smooth_test_image(rng, H) + 0.0, 0, 255).astype(np.uint8) for _ in range(nframes)])
@@ -573,7 +573,9 @@ def test_frame_groups_match_single_frames(gpu, nframes):
         one, sq1, _ = P.conceal_frames(frames[f:f + 1], pats[f:f + 1], cfg)
         np.testing.assert_array_equal(one[0], out[f])
         n0 = sum(len(p.blocks) for p in pats[:f])
-        np.testing.assert_array_equal(sq1, sq[n0:n0 + len(pats[f].blocks)])
+        # per-block squared errors: fp64 sums whose reduction order follows the
+        # kernel form chosen for the job (e.g. the tail's WIDE re-runs)
+        np.testing.assert_allclose(sq1, sq[n0:n0 + len(pats[f].blocks)], rtol=1e-12)
         k += 1
     assert k > 3 and rep.device["blocks"] == sum(len(p.blocks) for p in pats)
 
