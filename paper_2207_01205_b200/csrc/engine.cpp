@@ -1335,7 +1335,10 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         for (size_t ci = 0; ci < chunks.size(); ++ci) {
             const Chunk& ch = chunks[ci];
             ck(cudaEventSynchronize(ctx->event(3 * ci + 2)), "sync chunk");
-            ck(cudaMemcpyAsync(h_flags, d_flags, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, ctx->cpy), "D2H flags");
+            // guard flags are indexed by position: read back this chunk's range only
+            ck(cudaMemcpyAsync(h_flags + ch.b0, d_flags + ch.b0, sizeof(int32_t) * (ch.b1 - ch.b0),
+                               cudaMemcpyDeviceToHost, ctx->cpy),
+               "D2H flags");
             ck(cudaStreamSynchronize(ctx->cpy), "sync");
             std::vector<int32_t> rr, rs;  // caller ids (from scratch / resumed), grouped by class
             std::vector<BlockDesc> rdesc, sdesc;
@@ -1345,9 +1348,9 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             const bool can_resume = resume_on && head > 0 && hi_path(ch.path) == PATH_F64_REAL && soa_of(ch.path) &&
                                     k2d_replay_fits(T, I);
             for (int64_t i = ch.b0; i < ch.b1; ++i) {
-                const int32_t b = ids[static_cast<size_t>(i)];
-                const int32_t f = h_flags[b];
+                const int32_t f = h_flags[i];
                 if (!f) continue;
+                const int32_t b = ids[static_cast<size_t>(i)];
                 if (can_resume && f - 1 > head) {
                     rs.push_back(b);
                     sdesc.push_back(job.blocks[static_cast<size_t>(b)]);
@@ -1362,8 +1365,8 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             out.resumed += static_cast<int64_t>(rs.size());
             if (hp_.on && !(rr.empty() && rs.empty())) {  // where the near-ties stop the fp32 iteration
                 int hist[10] = {0};
-                for (int32_t b : rr) hist[std::min(9, (std::max(h_flags[b], 1) - 1) * 10 / std::max(1, I))]++;
-                for (int32_t b : rs) hist[std::min(9, (h_flags[b] - 1) * 10 / std::max(1, I))]++;
+                for (int64_t i = ch.b0; i < ch.b1; ++i)
+                    if (h_flags[i]) hist[std::min(9, (h_flags[i] - 1) * 10 / std::max(1, I))]++;
                 std::fprintf(stderr, "[fofse guard] chunk %zu: %zu flagged (%zu resumed); by tenth of I:", ci,
                              rr.size() + rs.size(), rs.size());
                 for (int q = 0; q < 10; ++q) std::fprintf(stderr, " %d", hist[q]);

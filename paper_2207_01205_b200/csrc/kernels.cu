@@ -794,7 +794,7 @@ __global__ void __launch_bounds__(K2Cfg<T, PATH>::THREADS) k2_kernel(K2Args a) {
             if (a.energy_out) a.energy_out[sb] = energy;
             if (a.nu_out) a.nu_out[sb] = nu;
             if (a.conv_out) a.conv_out[sb] = conv;
-            if (a.flags) a.flags[b] = flagged;
+            if (a.flags) a.flags[pos] = flagged;  // by position: the host reads a chunk's range
             if (a.trace_count) a.trace_count[b] = ntrace;  // == nu when trace_from_nu0
         }
         if constexpr (NW == 1)

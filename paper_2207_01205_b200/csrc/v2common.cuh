@@ -112,7 +112,7 @@ __device__ __forceinline__ void v2_finish(const K2Args& a, const BlockDesc& desc
         if (a.energy_out) a.energy_out[sb] = energy;
         if (a.nu_out) a.nu_out[sb] = nu;
         if (a.conv_out) a.conv_out[sb] = conv;
-        if (a.flags) a.flags[b] = flagged;
+        if (a.flags) a.flags[pos] = flagged;  // by position: the host reads a chunk's range
         if (a.trace_count) a.trace_count[b] = ntrace;
     }
     __syncwarp();
