@@ -365,7 +365,19 @@ def main():
                 "frac": (achieved / peak) if peak else None, "traffic": peaks.get("k2_dram_bytes"),
                 "per_unit": f"4*s*H = {4 * s * H} B per block-iteration (s={s}, H={H}); "
                             f"{its} fp32 iterations x {real_blocks if prec == 'fp32' else n_blocks} blocks per step",
-                "peak_source": peaks.get("smem_source")}
+                "peak_source": peaks.get("smem_source"),
+                "note": "the iteration kernel is bound by on-chip shared-memory bandwidth / issue, not by HBM or "
+                        "tensor cores (GEMM-free: shifted complex updates + argmax); hbm_check shows its DRAM share"}
+        try:  # HBM side of the same kernel: ncu DRAM bytes of one chunk launch, scaled to the step
+            with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+                hbm_peak = json.load(f).get("hbm_gbs")
+        except Exception:
+            hbm_peak = None
+        tr = peaks.get("k2_dram_bytes")
+        if prec == "fp32" and tr and real_avg > 0 and hbm_peak:
+            hbm = tr * (real_blocks / 24906.0) / (real_avg * 1e-3) / 1e9
+            roof["hbm_check"] = {"achieved": hbm, "peak": hbm_peak, "unit": "GB/s", "frac": hbm / hbm_peak,
+                                 "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             try:
