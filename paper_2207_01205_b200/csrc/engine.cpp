@@ -229,6 +229,7 @@ struct fofse_ctx {
     cudaStream_t side = nullptr;     // concurrent launches (asymmetric-mask blocks)
     cudaStream_t side_hi = nullptr;  // the same at high priority (a border range under one wave)
     cudaStream_t aux = nullptr;   // fp32 guard re-runs, overlapping the later chunks
+    cudaStream_t aux2 = nullptr;  // host-driven re-runs (border chunks), kept off aux's device-driven queue
     cudaStream_t cpy = nullptr;   // guard-flag read-back
     cudaStream_t io = nullptr;    // frame uploads / downloads of the pipelined host API
     cudaStream_t pre = nullptr;   // per-chunk spectra + fp64 head, running ahead of the fp32 iteration
@@ -248,7 +249,7 @@ struct fofse_ctx {
         const size_t need = (bytes + 255) & ~size_t(255);
         if (pin_used + need > pin_cap) {
             // earlier staged copies of this call must land before the arena moves
-            for (cudaStream_t x : {stream, side, side_hi, aux, cpy, io, pre})
+            for (cudaStream_t x : {stream, side, side_hi, aux, aux2, cpy, io, pre})
                 if (x) ck(cudaStreamSynchronize(x), "sync");
             const size_t cap = std::max<size_t>({need, 2 * pin_cap, size_t(8) << 20});
             if (pin) cudaFreeHost(pin);
@@ -952,8 +953,10 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         d_rec_c = ctx->buf("rec_c").as<double2>(static_cast<size_t>(n) * I);
     }
     auto k1_packed = [&](const BlockDesc* descs, int64_t cnt, int path, int seg, int spt, void* outp,
-                         double* e, double* m, int soa = 0, int64_t stride = 0, cudaStream_t ks = nullptr) {
+                         double* e, double* m, int soa = 0, int64_t stride = 0, cudaStream_t ks = nullptr,
+                         const int32_t* n_dev = nullptr) {
         K1Args a{};
+        a.n_dev = n_dev;
         a.T = T;
         a.Lh = g.Lh;
         a.Lw = g.Lw;
@@ -1224,6 +1227,99 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             const char* e = std::getenv("FOFSE_WIDE_RERUNS");
             return !(e && e[0] == '0');
         }();
+        // Small real-path chunks plan and launch their guard re-runs on the device
+        // (guard plan kernel + device-sized K1 / K2d launches on aux, enqueued with
+        // the chunk — no host round trip); the other chunks keep the host-driven
+        // path on aux2. FOFSE_DEVICE_GUARD=0: host-driven everywhere.
+        const bool dev_guard_on = [] {
+            const char* e = std::getenv("FOFSE_DEVICE_GUARD");
+            return !(e && e[0] == '0');
+        }();
+        int64_t max_chunk = 0;
+        for (const Chunk& ch : chunks) max_chunk = std::max(max_chunk, ch.b1 - ch.b0);
+        const size_t rr_bytes = std::max(r64_bytes, sizeof(double2) * BinLayout::make(T, k2d_wide_seg(T)).SLOTS);
+        // (device-sized launches cover the whole chunk: grids of chunk-size CTAs that mostly
+        // exit at once — cheap for small chunks, measurable for 25k-block ones, whose host
+        // round trip overlaps the following chunks anyway: C2 +3 %, C4 -0.7 % if used there)
+        auto dev_guard = [&](const Chunk& ch) {
+            return dev_guard_on && hi_path(ch.path) == PATH_F64_REAL && ch.b1 - ch.b0 <= 8192;
+        };
+        auto can_resume_of = [&](const Chunk& ch) {
+            return resume_on && head > 0 && hi_path(ch.path) == PATH_F64_REAL && soa_of(ch.path) && k2d_replay_fits(T, I);
+        };
+        GuardPlan* d_plans = ctx->buf("gp_plan").as<GuardPlan>(std::max<size_t>(chunks.size(), 1));
+        const size_t mc = static_cast<size_t>(std::max<int64_t>(max_chunk, 1));
+        int32_t* g_rr_ids = ctx->buf("gp_rr_ids").as<int32_t>(mc);
+        BlockDesc* g_rr_desc = ctx->buf("gp_rr_desc").as<BlockDesc>(mc);
+        Tile* g_rr_tiles = ctx->buf("gp_rr_tiles").as<Tile>(mc);
+        int32_t* g_rs_ids = ctx->buf("gp_rs_ids").as<int32_t>(mc);
+        int32_t* g_rs_pos = ctx->buf("gp_rs_pos").as<int32_t>(mc);
+        int32_t* g_rs_nuf = ctx->buf("gp_rs_nuf").as<int32_t>(mc);
+        BlockDesc* g_rs_desc = ctx->buf("gp_rs_desc").as<BlockDesc>(mc);
+        Tile* g_rs_tiles = ctx->buf("gp_rs_tiles").as<Tile>(mc);
+        char* g_Rr = ctx->buf("gp_Rr").as<char>(mc * rr_bytes);
+        double* g_re0 = ctx->buf("gp_re0").as<double>(mc);
+        double* g_rimax = ctx->buf("gp_rimax").as<double>(mc);
+        // event slots after the chunks' three: [3 * nchunks + ci] = chunk ci's guard re-runs done
+        const size_t ev_guard = 3 * chunks.size();
+        auto enqueue_device_guard = [&](size_t ci) {
+            const Chunk& ch = chunks[ci];
+            const int64_t cn = ch.b1 - ch.b0;
+            const bool wide = wide_reruns && T <= 64 && ci + 1 == chunks.size();
+            ck(cudaStreamWaitEvent(ctx->aux, ctx->event(3 * ci + 2), 0), "wait");
+            GuardPlanArgs gp{};
+            gp.flags = d_flags;
+            gp.b0 = ch.b0;
+            gp.b1 = ch.b1;
+            gp.head = head;
+            gp.can_resume = can_resume_of(ch) ? 1 : 0;
+            gp.ng_rr = ng_f64(PATH_F64_REAL, wide);
+            gp.ng_rs = ng_f64(PATH_F64_REAL, wide);
+            gp.order = d_ids;
+            gp.descs = d_sorted;
+            gp.rr_ids = g_rr_ids;
+            gp.rr_desc = g_rr_desc;
+            gp.rr_tiles = g_rr_tiles;
+            gp.rs_ids = g_rs_ids;
+            gp.rs_pos = g_rs_pos;
+            gp.rs_nuf = g_rs_nuf;
+            gp.rs_desc = g_rs_desc;
+            gp.rs_tiles = g_rs_tiles;
+            gp.plan = d_plans + ci;
+            ck(guard_plan_launch(gp, ctx->aux), "guard plan");
+            ++ctx->launches;
+            std::vector<BlockDesc> none;
+            {  // from scratch: K1 (device count) + K2d over the device tiles
+                K2Args a = base_args();
+                a.order = g_rr_ids;
+                a.blocks = g_rr_desc;
+                a.rin = g_Rr;
+                a.energy0 = g_re0;
+                a.init_energy = g_re0;
+                a.init_max = g_rimax;
+                a.rec_global = 0;
+                a.ntiles_dev = &d_plans[ci].nt_rr;
+                k1_packed(g_rr_desc, cn, PATH_F64_REAL, wide ? k2d_wide_seg(T) : seg64, 1, g_Rr, g_re0, g_rimax, 0, 0,
+                          ctx->aux, &d_plans[ci].n_rr);
+                k2_f64(a, PATH_F64_REAL, 0, cn, none, "gr", ctx->aux, g_rr_tiles, static_cast<size_t>(cn), wide);
+            }
+            if (can_resume_of(ch)) {  // resumed at the near-tie (K2d REPLAY)
+                K2Args a = base_args();
+                a.order = g_rs_ids;
+                a.blocks = g_rs_desc;
+                a.rin = d_R64;
+                a.src_pos = g_rs_pos;
+                a.nu_flag = g_rs_nuf;
+                a.init_energy = d_e0;
+                a.init_max = d_imax;
+                a.nu_limit = I;
+                a.rec_global = 1;
+                a.trace_from_nu0 = 1;
+                a.ntiles_dev = &d_plans[ci].nt_rs;
+                k2_f64(a, PATH_F64_REAL, 0, cn, none, "gs", ctx->aux, g_rs_tiles, static_cast<size_t>(cn), wide);
+            }
+            ck(cudaEventRecord(ctx->event(ev_guard + ci), ctx->aux), "event");
+        };
         ck(cudaStreamWaitEvent(ctx->aux, ctx->ev[4], 0), "wait");
         std::vector<char> waited(static_cast<size_t>(2 * ngroups), 0);  // [group][main/side] upload waits
         // per chunk: events [3i] after K1, [3i+1] before the fp32 iteration, [3i+2] done
@@ -1323,17 +1419,32 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
                "K2 fp32");
             ++ctx->launches;
             ck(cudaEventRecord(ctx->event(3 * ci + 2), ch.s), "event");
+            if (dev_guard(ch)) enqueue_device_guard(ci);
         }
         ck(cudaEventRecord(ctx->ev[1], st), "event");  // all fp32 work enqueued
         hp_.mark("fp32 chunks enqueued");
 
-        // ---- near-tie guard: re-run flagged blocks in fp64 from scratch, per chunk ----
-        int64_t max_chunk = 0;
-        for (const Chunk& ch : chunks) max_chunk = std::max(max_chunk, ch.b1 - ch.b0);
+        // ---- near-tie guard, host-driven chunks: read the flags, re-run in fp64 ----
         std::vector<int32_t> flags(static_cast<size_t>(n));
         int32_t* h_flags = flags.data();
+        const size_t ev_host = ev_guard + chunks.size();  // [ev_host + ci]: host-driven re-runs of ci done
         for (size_t ci = 0; ci < chunks.size(); ++ci) {
             const Chunk& ch = chunks[ci];
+            const bool last_of_group = ci + 1 == chunks.size() || chunks[ci + 1].grp != ch.grp;
+            auto group_done = [&]() {  // a frame group is complete once its chunks and their re-runs are done
+                if (!(gio && last_of_group)) return;
+                for (size_t cj = 0; cj <= ci; ++cj) {
+                    if (chunks[cj].grp != ch.grp) continue;
+                    ck(cudaStreamWaitEvent(ctx->io, ctx->event(3 * cj + 2), 0), "wait");
+                    ck(cudaStreamWaitEvent(ctx->io, ctx->event(dev_guard(chunks[cj]) ? ev_guard + cj : ev_host + cj), 0),
+                       "wait");
+                }
+                gio->on_done(ch.grp, ctx->io);
+            };
+            if (dev_guard(ch)) {
+                group_done();
+                continue;
+            }
             ck(cudaEventSynchronize(ctx->event(3 * ci + 2)), "sync chunk");
             // guard flags are indexed by position: read back this chunk's range only
             ck(cudaMemcpyAsync(h_flags + ch.b0, d_flags + ch.b0, sizeof(int32_t) * (ch.b1 - ch.b0),
@@ -1345,8 +1456,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             std::vector<int32_t> spos, snuf;  // resumed: position of the K1 spectrum, selections made
             // resume at the near-tie when the fp64 K1 spectrum is still in place (direct
             // head hand-off) and the fp32 phase had made selections beyond the head
-            const bool can_resume = resume_on && head > 0 && hi_path(ch.path) == PATH_F64_REAL && soa_of(ch.path) &&
-                                    k2d_replay_fits(T, I);
+            const bool can_resume = can_resume_of(ch);
             for (int64_t i = ch.b0; i < ch.b1; ++i) {
                 const int32_t f = h_flags[i];
                 if (!f) continue;
@@ -1380,15 +1490,14 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             // where the standard form's throughput is better (measured: C2 +5 %, C4
             // -2 % with WIDE everywhere). Its packed layout has more slots.
             const bool wide = wide_reruns && T <= 64 && ci + 1 == chunks.size();
-            const size_t rr_bytes = std::max(r64_bytes, sizeof(double2) * BinLayout::make(T, k2d_wide_seg(T)).SLOTS);
             char* d_Rr = ctx->buf("Rr").as<char>(static_cast<size_t>(max_chunk) * rr_bytes);
             double* d_re0 = ctx->buf("re0").as<double>(static_cast<size_t>(max_chunk));
             double* d_rimax = ctx->buf("rimax").as<double>(static_cast<size_t>(max_chunk));
             if (!rr.empty()) {  // from scratch: K1 + all I selections in fp64
                 const int64_t m = static_cast<int64_t>(rr.size());
                 const std::string tag = "r" + std::to_string(ci);
-                upload_to(ctx, d_rdesc, rdesc.data(), rdesc.size(), ctx->aux);
-                upload_to(ctx, d_rr, rr.data(), rr.size(), ctx->aux);
+                upload_to(ctx, d_rdesc, rdesc.data(), rdesc.size(), ctx->aux2);
+                upload_to(ctx, d_rr, rr.data(), rr.size(), ctx->aux2);
                 K2Args a = base_args();
                 a.order = d_rr;
                 a.blocks = d_rdesc;
@@ -1399,18 +1508,18 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
                 a.rec_global = 0;  // strict: smem records (or the per-block global scratch when I > cap)
                 const int hp = hi_path(ch.path);
                 const bool w = wide && hp == PATH_F64_REAL;
-                k1_packed(d_rdesc, m, hp, w ? k2d_wide_seg(T) : seg64, 1, d_Rr, d_re0, d_rimax, 0, 0, ctx->aux);
-                k2_f64(a, hp, 0, m, rdesc, tag, ctx->aux, nullptr, 0, w);
+                k1_packed(d_rdesc, m, hp, w ? k2d_wide_seg(T) : seg64, 1, d_Rr, d_re0, d_rimax, 0, 0, ctx->aux2);
+                k2_f64(a, hp, 0, m, rdesc, tag, ctx->aux2, nullptr, 0, w);
             }
             if (!rs.empty()) {  // resumed: K2d REPLAY rebuilds the fp64 state at the near-tie and goes on
                 const int64_t m = static_cast<int64_t>(rs.size());
                 const std::string tag = "s" + std::to_string(ci);
                 int32_t* d_rpos = ctx->buf("rpos").as<int32_t>(static_cast<size_t>(max_chunk));
                 int32_t* d_rnuf = ctx->buf("rnuf").as<int32_t>(static_cast<size_t>(max_chunk));
-                upload_to(ctx, d_rdesc, sdesc.data(), sdesc.size(), ctx->aux);
-                upload_to(ctx, d_rr, rs.data(), rs.size(), ctx->aux);
-                upload_to(ctx, d_rpos, spos.data(), spos.size(), ctx->aux);
-                upload_to(ctx, d_rnuf, snuf.data(), snuf.size(), ctx->aux);
+                upload_to(ctx, d_rdesc, sdesc.data(), sdesc.size(), ctx->aux2);
+                upload_to(ctx, d_rr, rs.data(), rs.size(), ctx->aux2);
+                upload_to(ctx, d_rpos, spos.data(), spos.size(), ctx->aux2);
+                upload_to(ctx, d_rnuf, snuf.data(), snuf.size(), ctx->aux2);
                 K2Args a = base_args();
                 a.order = d_rr;
                 a.blocks = d_rdesc;
@@ -1422,17 +1531,10 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
                 a.nu_limit = I;
                 a.rec_global = 1;
                 a.trace_from_nu0 = 1;
-                k2_f64(a, PATH_F64_REAL, 0, m, sdesc, tag, ctx->aux, nullptr, 0, wide);
+                k2_f64(a, PATH_F64_REAL, 0, m, sdesc, tag, ctx->aux2, nullptr, 0, wide);
             }
-            // a frame group is complete once its last chunk and its re-runs are done
-            const bool last_of_group = ci + 1 == chunks.size() || chunks[ci + 1].grp != ch.grp;
-            if (gio && last_of_group) {
-                ck(cudaEventRecord(ctx->ev[5], ctx->aux), "event");
-                ck(cudaStreamWaitEvent(ctx->io, ctx->ev[5], 0), "wait");
-                for (size_t cj = 0; cj <= ci; ++cj)
-                    if (chunks[cj].grp == ch.grp) ck(cudaStreamWaitEvent(ctx->io, ctx->event(3 * cj + 2), 0), "wait");
-                gio->on_done(ch.grp, ctx->io);
-            }
+            ck(cudaEventRecord(ctx->event(ev_host + ci), ctx->aux2), "event");
+            group_done();
         }
         hp_.mark("re-runs enqueued");
         ck(cudaEventRecord(ctx->ev[5], ctx->side), "event");
@@ -1441,6 +1543,8 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         ck(cudaStreamWaitEvent(st, ctx->ev[5], 0), "wait");
         ck(cudaEventRecord(ctx->ev[5], ctx->aux), "event");
         ck(cudaStreamWaitEvent(st, ctx->ev[5], 0), "wait");
+        ck(cudaEventRecord(ctx->ev[5], ctx->aux2), "event");
+        ck(cudaStreamWaitEvent(st, ctx->ev[5], 0), "wait");
         ck(cudaEventRecord(ctx->ev[2], st), "event");
         ck(cudaEventRecord(ctx->ev[3], st), "event");
         if (!chunks.empty()) {
@@ -1448,6 +1552,28 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             float ms = 0;
             ck(cudaEventElapsedTime(&ms, ctx->event(3 * (chunks.size() - 1) + 2), ctx->ev[3]), "elapsed");
             out.rerun_tail_ms = ms;
+            // device-planned re-runs: counts from the plans (and, with FOFSE_HOST_PROF, where
+            // the near-ties stopped the fp32 iteration)
+            std::vector<GuardPlan> plans(chunks.size());
+            ck(cudaMemcpy(plans.data(), d_plans, sizeof(GuardPlan) * chunks.size(), cudaMemcpyDeviceToHost), "D2H plans");
+            for (size_t ci = 0; ci < chunks.size(); ++ci) {
+                if (!dev_guard(chunks[ci])) continue;
+                out.reruns += plans[ci].n_rr + plans[ci].n_rs;
+                out.resumed += plans[ci].n_rs;
+                if (hp_.on) {
+                    const Chunk& ch = chunks[ci];
+                    ck(cudaMemcpy(h_flags + ch.b0, d_flags + ch.b0, sizeof(int32_t) * (ch.b1 - ch.b0),
+                                  cudaMemcpyDeviceToHost),
+                       "D2H flags");
+                    int hist[10] = {0};
+                    for (int64_t i = ch.b0; i < ch.b1; ++i)
+                        if (h_flags[i]) hist[std::min(9, (h_flags[i] - 1) * 10 / std::max(1, I))]++;
+                    std::fprintf(stderr, "[fofse guard] chunk %zu (device plan): %d flagged (%d resumed); by tenth of I:",
+                                 ci, plans[ci].n_rr + plans[ci].n_rs, plans[ci].n_rs);
+                    for (int q = 0; q < 10; ++q) std::fprintf(stderr, " %d", hist[q]);
+                    std::fprintf(stderr, "\n");
+                }
+            }
         }
         // device-time breakdown from the chunk events (overlapping chunks add up)
         for (size_t ci = 0; ci < chunks.size(); ++ci) {
@@ -1626,6 +1752,7 @@ int fofse_create(int32_t device, fofse_ctx** out) {
         ck(cudaStreamCreateWithPriority(&ctx->side_hi, cudaStreamNonBlocking, prio ? prio_hi : prio_lo), "cudaStreamCreate");
         ck(cudaStreamCreateWithFlags(&ctx->pre, cudaStreamNonBlocking), "cudaStreamCreate");
         ck(cudaStreamCreateWithPriority(&ctx->aux, cudaStreamNonBlocking, prio ? prio_hi : prio_lo), "cudaStreamCreate");
+        ck(cudaStreamCreateWithPriority(&ctx->aux2, cudaStreamNonBlocking, prio ? prio_hi : prio_lo), "cudaStreamCreate");
         ck(cudaStreamCreateWithFlags(&ctx->cpy, cudaStreamNonBlocking), "cudaStreamCreate");
         ck(cudaStreamCreateWithFlags(&ctx->io, cudaStreamNonBlocking), "cudaStreamCreate");
         ctx->own_stream = true;
@@ -1642,7 +1769,7 @@ void fofse_destroy(fofse_ctx* ctx) {
         if (e) cudaEventDestroy(e);
     for (auto e : ctx->evpool) cudaEventDestroy(e);
     if (ctx->pin) cudaFreeHost(ctx->pin);
-    for (cudaStream_t x : {ctx->side, ctx->side_hi, ctx->aux, ctx->cpy, ctx->io, ctx->pre})
+    for (cudaStream_t x : {ctx->side, ctx->side_hi, ctx->aux, ctx->aux2, ctx->cpy, ctx->io, ctx->pre})
         if (x) {
             cudaStreamSynchronize(x);
             cudaStreamDestroy(x);

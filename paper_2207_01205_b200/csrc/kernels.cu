@@ -10,6 +10,8 @@
 // No tensor cores: the path is not a contraction. K2 is bound by
 // shared-memory bandwidth and FP/issue throughput; K1 by FP64 + SMEM.
 #include <cuda_runtime.h>
+
+#include <cub/block/block_scan.cuh>
 #include <stdint.h>
 
 #include <climits>
@@ -62,6 +64,7 @@ __global__ void __launch_bounds__(256) k1_kernel(K1Args a) {
     double* red = reinterpret_cast<double*>(zbuf + C::ZCH * T);
 
     const int b = blockIdx.x;
+    if (a.n_dev && b >= *a.n_dev) return;  // device-sized launch (guard re-runs)
     const bool class_mode = a.mode == K1_CLASS;
     BlockDesc d;
     if (class_mode) {
@@ -957,6 +960,111 @@ static int k2_launch_T(const K2Args& a, int32_t ntiles, cudaStream_t s) {
         case PATH_F32_REAL: return k2_launch_t<T, PATH_F32_REAL>(a, ntiles, s);
     }
     return cudaErrorInvalidValue;
+}
+
+// ---------------------------------------------------------------------------
+// Guard plan of one fp32 chunk, one CTA: stable compaction of the flagged
+// positions into the resumed / from-scratch lists (block-wide prefix sums over
+// a blocked arrangement), then the tiles of each list (a tile starts at a class
+// change or every ng blocks inside a class run).
+// ---------------------------------------------------------------------------
+constexpr int GP_THREADS = 1024;
+
+__device__ __forceinline__ int gp_exclusive_sum(int v, int* tmp, int* total) {
+    using Scan = cub::BlockScan<int, GP_THREADS>;
+    __shared__ typename Scan::TempStorage ts;
+    int out, agg;
+    Scan(ts).ExclusiveSum(v, out, agg);
+    __syncthreads();
+    (void)tmp;
+    *total = agg;
+    return out;
+}
+__device__ __forceinline__ int gp_inclusive_max(int v) {
+    using Scan = cub::BlockScan<int, GP_THREADS>;
+    __shared__ typename Scan::TempStorage ts;
+    int out;
+    Scan(ts).InclusiveScan(v, out, cub::Max());
+    __syncthreads();
+    return out;
+}
+
+// tiles of list [0, n) with classes cls(i): write tiles, return the tile count
+template <class ClsOf>
+__device__ int gp_tiles(int n, int ng, ClsOf cls_of, Tile* tiles) {
+    const int ipt = (n + GP_THREADS - 1) / GP_THREADS;
+    const int i0 = threadIdx.x * ipt, i1 = min(n, i0 + ipt);
+    // segment (class run) start of each element: inclusive max-scan of run starts
+    int last = -1;
+    for (int i = i0; i < i1; ++i)
+        if (i == 0 || cls_of(i) != cls_of(i - 1)) last = i;
+    const int carry_in = gp_inclusive_max(last);  // run start at the end of this thread's items
+    // the run start entering this thread's range: the previous threads' maximum
+    __shared__ int prev_max[GP_THREADS];
+    prev_max[threadIdx.x] = carry_in;
+    __syncthreads();
+    int seg = threadIdx.x > 0 ? prev_max[threadIdx.x - 1] : -1;
+    int cnt = 0;
+    for (int i = i0; i < i1; ++i) {
+        if (i == 0 || cls_of(i) != cls_of(i - 1)) seg = i;
+        cnt += ((i - seg) % ng == 0) ? 1 : 0;
+    }
+    int total;
+    int t = gp_exclusive_sum(cnt, nullptr, &total);
+    seg = threadIdx.x > 0 ? prev_max[threadIdx.x - 1] : -1;
+    for (int i = i0; i < i1; ++i) {
+        if (i == 0 || cls_of(i) != cls_of(i - 1)) seg = i;
+        if ((i - seg) % ng == 0) tiles[t++] = Tile{cls_of(i), i, 0, 0};
+    }
+    __syncthreads();
+    // counts: up to the next tile's begin, within ng and the run
+    for (int k = threadIdx.x; k < total; k += GP_THREADS) {
+        const int b = tiles[k].begin, e = k + 1 < total ? tiles[k + 1].begin : n;
+        tiles[k].count = min(ng, e - b);
+    }
+    __syncthreads();
+    return total;
+}
+
+__global__ void __launch_bounds__(GP_THREADS) guard_plan_kernel(GuardPlanArgs a) {
+    const int len = (int)(a.b1 - a.b0);
+    const int ipt = (len + GP_THREADS - 1) / GP_THREADS;
+    const int i0 = threadIdx.x * ipt, i1 = min(len, i0 + ipt);
+    auto resumable = [&](int f) { return a.can_resume && f - 1 > a.head; };
+    int nrs = 0, nrr = 0;
+    for (int i = i0; i < i1; ++i) {
+        const int f = a.flags[a.b0 + i];
+        if (!f) continue;
+        if (resumable(f)) ++nrs; else ++nrr;
+    }
+    int tot_rs, tot_rr;
+    int ors = gp_exclusive_sum(nrs, nullptr, &tot_rs);
+    int orr = gp_exclusive_sum(nrr, nullptr, &tot_rr);
+    for (int i = i0; i < i1; ++i) {
+        const int64_t pos = a.b0 + i;
+        const int f = a.flags[pos];
+        if (!f) continue;
+        if (resumable(f)) {
+            a.rs_ids[ors] = a.order[pos];
+            a.rs_pos[ors] = (int32_t)pos;
+            a.rs_nuf[ors] = f - 1;
+            a.rs_desc[ors] = a.descs[pos];
+            ++ors;
+        } else {
+            a.rr_ids[orr] = a.order[pos];
+            a.rr_desc[orr] = a.descs[pos];
+            ++orr;
+        }
+    }
+    __syncthreads();
+    const int nt_rr = gp_tiles(tot_rr, a.ng_rr, [&](int i) { return a.rr_desc[i].cls; }, a.rr_tiles);
+    const int nt_rs = gp_tiles(tot_rs, a.ng_rs, [&](int i) { return a.rs_desc[i].cls; }, a.rs_tiles);
+    if (threadIdx.x == 0) *a.plan = GuardPlan{tot_rr, tot_rs, nt_rr, nt_rs};
+}
+
+int guard_plan_launch(const GuardPlanArgs& a, cudaStream_t s) {
+    guard_plan_kernel<<<1, GP_THREADS, 0, s>>>(a);
+    return cudaGetLastError();
 }
 
 // One thread per tile: find its run (a list has a handful), cut the tile.

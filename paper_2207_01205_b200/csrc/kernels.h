@@ -80,6 +80,7 @@ struct K1Args {
     double* w0;                // [ncls]
     const double2* twid;       // e^{-j 2 pi k / T}, k < T
     const double2* ptab;       // e^{-j pi m / T}, m < 2T (rotation phases; NULL = computed)
+    const int32_t* n_dev;      // optional: block count on the device (grid = an upper bound)
 };
 enum { K1_PACKED = 0, K1_FULL = 1, K1_CLASS = 2 };
 
@@ -141,6 +142,7 @@ struct K2Args {
     int32_t v2c_copies;         // K2v2c: W plane copies staged (1: half the smem, 2: aligned pairs)
     int32_t real_gw;            // K2v2 real path at T = 64: warps per lost block (1: K2v2r, 2: K2v2h)
     int32_t d_wide;             // K2d: WIDE form (T <= 64; guard re-runs)
+    const int32_t* ntiles_dev;  // K2d: optional tile count on the device (grid = an upper bound)
 };
 
 struct CvtArgs {
@@ -174,6 +176,31 @@ int k2d_blocks_per_cta(int T, bool wide = false);
 // K2d WIDE form (a.d_wide, T <= 64): half the bins per thread; its fp64 packed
 // input layout uses this SEG.
 int k2d_wide_seg(int T);
+// Device-side guard plan of one fp32 chunk (positions [b0, b1)): the flagged
+// blocks split into resumed (flag - 1 > head, when can_resume) and from-scratch
+// lists in position order (class runs), their tiles (<= ng blocks of one
+// class) and the counts — so the re-runs launch without a host round trip.
+struct GuardPlan {
+    int32_t n_rr, n_rs, nt_rr, nt_rs;
+};
+struct GuardPlanArgs {
+    const int32_t* flags;       // by position
+    int64_t b0, b1;
+    int32_t head, can_resume, ng_rr, ng_rs;
+    const int32_t* order;       // caller id by position
+    const BlockDesc* descs;     // by position
+    int32_t* rr_ids;            // from scratch: ids, descs, tiles
+    BlockDesc* rr_desc;
+    Tile* rr_tiles;
+    int32_t* rs_ids;            // resumed: ids, spectrum positions, selections made, descs, tiles
+    int32_t* rs_pos;
+    int32_t* rs_nuf;
+    BlockDesc* rs_desc;
+    Tile* rs_tiles;
+    GuardPlan* plan;
+};
+int guard_plan_launch(const GuardPlanArgs& a, cudaStream_t s);
+
 // K2d REPLAY mode (a.src_pos set): rebuilds a near-tie block's fp64 state after
 // its first nu_flag[pos] recorded selections, then iterates on to nu_limit.
 bool k2d_replay_fits(int T, int rstride);

@@ -300,6 +300,7 @@ __global__ void __launch_bounds__(DCfg<T, WIDE>::THREADS, DCfg<T, WIDE>::MINB) k
     constexpr int KTOP = static_cast<int>(Cf::KTOP);
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    if (a.ntiles_dev && (int)blockIdx.x >= *a.ntiles_dev) return;  // device-sized launch
     const Tile tile = a.tiles[blockIdx.x];
     v2_stage<Cf>(a, tile, smem_raw);
     const double* vE = reinterpret_cast<const double*>(smem_raw);

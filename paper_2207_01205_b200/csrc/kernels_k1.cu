@@ -149,6 +149,7 @@ __global__ void __launch_bounds__(K1fCfg<FT>::THREADS, FT == 64 ? 3 : 8) k1f_ker
     double2* tile = reinterpret_cast<double2*>(smem_raw + C::sc) + g * 8 * SS;
 
     const int b = blockIdx.x;
+    if (a.n_dev && b >= *a.n_dev) return;  // device-sized launch (guard re-runs)
     const BlockDesc d = a.blocks[b];
     const double* wc = a.wcls + (size_t)d.cls * a.Lh * a.Lw;
     for (int i = threadIdx.x; i < FT; i += blockDim.x) tw[i] = a.twid[i];
