@@ -529,6 +529,18 @@ def test_guard_resume_matches_rerun_from_scratch(gpu, monkeypatch, name):
     assert abs(resumed.report.psnr_db - o64.report.psnr_db) <= FP32_PSNR_TOL
 
 
+def test_device_planned_guard_matches_host_planned(gpu, monkeypatch):
+    """C2 (one chunk): the re-runs planned on the device (guard plan kernel,
+    device-sized launches) equal the host-planned ones bit for bit."""
+    img, pat = WL.C2.frame(seed=31)
+    cfg = WL.C2.config("fp32")
+    dev = P.conceal(img.astype(np.float64), pat, cfg)
+    monkeypatch.setenv("FOFSE_DEVICE_GUARD", "0")
+    host = P.conceal(img.astype(np.float64), pat, cfg)
+    assert dev.report.device["guard_reruns"] == host.report.device["guard_reruns"] > 0
+    np.testing.assert_array_equal(dev.restored, host.restored)
+
+
 def test_frames_u8_matches_f64_and_is_deterministic(gpu):
     """Video entry point: u8 frames give write_pgm-rounded results of the f64 path;
     repeated runs and frame-order changes are bitwise identical."""
