@@ -1020,10 +1020,28 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
     char* d_R32 = nullptr;
     const size_t r64_bytes = sizeof(double2) * L64.SLOTS;  // per block
     if (!fp32 || head > 0) d_R64 = ctx->buf("R64").as<char>(static_cast<size_t>(n) * r64_bytes);
-    if (!fp32) {
+    // fp64 mode, a job within one wave of the WIDE K2d (e.g. one small image): its real
+    // ranges run the WIDE form (lower per-selection latency; own packed layout / buffer)
+    const size_t r64w_bytes = sizeof(double2) * BinLayout::make(T, k2d_wide_seg(T)).SLOTS;
+    bool f64_wide = false;
+    if (!fp32 && use_d && T <= 64 && !full_od(cfg)) {
+        int64_t n_real = 0;
         for (const Range& r : ranges)
-            k1_packed(d_sorted + r.begin, r.end - r.begin, hi_path(r.path), seg64, 1,
-                      d_R64 + static_cast<size_t>(r.begin) * r64_bytes, d_e0 + r.begin, d_imax + r.begin);
+            if (hi_path(r.path) == PATH_F64_REAL) n_real += r.end - r.begin;
+        int nsm = 148;
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device);
+        f64_wide = n_real > 0 && n_real <= 2LL * nsm * k2d_blocks_per_cta(T, true);
+    }
+    char* d_R64w = f64_wide ? ctx->buf("R64w").as<char>(static_cast<size_t>(n) * r64w_bytes) : nullptr;
+    auto range_wide = [&](const Range& r) { return f64_wide && hi_path(r.path) == PATH_F64_REAL; };
+    if (!fp32) {
+        for (const Range& r : ranges) {
+            const bool w = range_wide(r);
+            k1_packed(d_sorted + r.begin, r.end - r.begin, hi_path(r.path), w ? k2d_wide_seg(T) : seg64, 1,
+                      w ? d_R64w + static_cast<size_t>(r.begin) * r64w_bytes
+                        : d_R64 + static_cast<size_t>(r.begin) * r64_bytes,
+                      d_e0 + r.begin, d_imax + r.begin);
+        }
     }
     // one fp64 iteration launch over positions [b0, b1) of `descs` (K2d or strict)
     auto ng_f64 = [&](int hp, bool wide = false) {
@@ -1073,8 +1091,13 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         a.rin = d_R64;
         a.rec_global = 0;
         if (!ckpts) {
-            for (size_t i = 0; i < ranges.size(); ++i)
-                k2_f64(a, hi_path(ranges[i].path), ranges[i].begin, ranges[i].end, sorted, std::to_string(i), st);
+            for (size_t i = 0; i < ranges.size(); ++i) {
+                const bool w = range_wide(ranges[i]);
+                K2Args ar = a;
+                if (w) ar.rin = d_R64w;
+                k2_f64(ar, hi_path(ranges[i].path), ranges[i].begin, ranges[i].end, sorted, std::to_string(i), st,
+                       nullptr, 0, w);
+            }
         } else {
             // checkpointed curves (pipeline.cpp:264-369): resumable phases up to each
             // checkpoint, state carried by position in place, records at nu-1, then
@@ -1103,8 +1126,13 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
                 a.iterations = (*ckpts)[c] - done;
                 a.block_sq = d_block_sq + c * static_cast<size_t>(n);
                 for (size_t i = 0; i < ranges.size(); ++i)
-                    k2_f64(a, hi_path(ranges[i].path), ranges[i].begin, ranges[i].end, sorted,
-                           std::to_string(i), st);
+                {
+                    const bool w = range_wide(ranges[i]);
+                    K2Args ar = a;
+                    if (w) ar.rin = ar.rout = d_R64w;
+                    k2_f64(ar, hi_path(ranges[i].path), ranges[i].begin, ranges[i].end, sorted,
+                           std::to_string(i), st, nullptr, 0, w);
+                }
                 done = (*ckpts)[c];
             }
         }
