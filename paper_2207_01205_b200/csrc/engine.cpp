@@ -1269,8 +1269,12 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         // (device-sized launches cover the whole chunk: grids of chunk-size CTAs that mostly
         // exit at once — cheap for small chunks, measurable for 25k-block ones, whose host
         // round trip overlaps the following chunks anyway: C2 +3 %, C4 -0.7 % if used there)
+        static const int64_t dev_guard_max = [] {  // experiments: FOFSE_DEVICE_GUARD_MAX=<blocks>
+            const char* e = std::getenv("FOFSE_DEVICE_GUARD_MAX");
+            return e ? static_cast<int64_t>(std::atoll(e)) : int64_t(8192);
+        }();
         auto dev_guard = [&](const Chunk& ch) {
-            return dev_guard_on && hi_path(ch.path) == PATH_F64_REAL && ch.b1 - ch.b0 <= 8192;
+            return dev_guard_on && hi_path(ch.path) == PATH_F64_REAL && ch.b1 - ch.b0 <= dev_guard_max;
         };
         auto can_resume_of = [&](const Chunk& ch) {
             return resume_on && head > 0 && hi_path(ch.path) == PATH_F64_REAL && soa_of(ch.path) && k2d_replay_fits(T, I);
