@@ -305,9 +305,202 @@ __global__ void __launch_bounds__(K1fCfg<FT>::THREADS, FT == 64 ? 3 : 8) k1f_ker
     }
 }
 
+// ============================================================================
+// T = 128 (windows up to 64 x 64): 128 = 8 x 16 with 16 lanes x 8 elements per
+// transform. Stage 1: radix-8 in registers over m (n = t + 16 m), twiddles
+// W128^{t k1}; transpose; stage 2: the 16-point DFTs over t split by output
+// parity — lane t' (k1' = t'/2, h = t' % 2) forms z[s] = (Y[s] +- Y[s+8]) W16^{s h}
+// and runs one more radix-8, ending with X[tout + 16 q], tout = k1' + 8 h.
+// Row pass: <= 32 row pairs (one per 16-lane group, 512 threads); column pass:
+// the 63 complex columns + the packed (0, 64) pair, two per group; the column
+// results go straight to the packed canonical half (bin (k1, c) or the partner
+// (128 - k1, 128 - c)), no second tile.
+// ============================================================================
+constexpr int WT = 128, WLG = 16, WGR = 32;  // transform, lanes per transform, groups
+constexpr int WCS = WT / 2 + 1;             // spectrum tile: [65 columns][65 rows] (window rows <= 64)
+constexpr int WSS = WLG + 1;                // transpose tile row stride (double2)
+struct K1wSmem {
+    static constexpr size_t tw = 0;                                  // W128^e, e < 128
+    static constexpr size_t ph = tw + sizeof(double2) * WT;          // e^{+j pi m / T}, m < 256
+    static constexpr size_t cb = ph + sizeof(double2) * 2 * WT;      // [65][65]
+    static constexpr size_t sc = cb + sizeof(double2) * WCS * WCS;   // [32 groups][8][17]
+    static constexpr size_t red = sc + sizeof(double2) * WGR * 8 * WSS;
+    static constexpr size_t total = red + 32 * sizeof(double);
+};
+
+// 128-point forward DFT of v[n] = x_t[m], n = t + 16 m, over the 16 lanes t of a
+// group; on return lane t holds X[tout + 16 q] in x[q], tout = (t >> 1) + 8 (t & 1).
+__device__ __forceinline__ void fft128_group(double2 (&x)[8], int t, const double2* tw, double2* tile,
+                                             unsigned gmask) {
+    fft8(x);  // Y[t][k1] = sum_m x[t + 16 m] W8^{m k1}
+#pragma unroll
+    for (int k1 = 1; k1 < 8; ++k1) x[k1] = c_mul(x[k1], tw[t * k1]);  // * W128^{t k1}
+#pragma unroll
+    for (int k1 = 0; k1 < 8; ++k1) tile[k1 * WSS + t] = x[k1];
+    __syncwarp(gmask);
+    const int k1p = t >> 1, h = t & 1;
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+        const double2 y0 = tile[k1p * WSS + s], y1 = tile[k1p * WSS + s + 8];
+        x[s] = h ? c_mul(c_sub(y0, y1), tw[8 * s]) : c_add(y0, y1);  // W16^{s} = W128^{8 s}
+    }
+    __syncwarp(gmask);
+    fft8(x);  // X[k1p + 8 (2 q + h)]
+}
+
+template <class SRC>
+__global__ void __launch_bounds__(WGR * WLG, 1) k1w_kernel(K1Args a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double2* tw = reinterpret_cast<double2*>(smem_raw + K1wSmem::tw);
+    double2* ph = reinterpret_cast<double2*>(smem_raw + K1wSmem::ph);
+    double2* cb = reinterpret_cast<double2*>(smem_raw + K1wSmem::cb);
+    double* red = reinterpret_cast<double*>(smem_raw + K1wSmem::red);
+    const int g = threadIdx.x / WLG, t = threadIdx.x % WLG;
+    const unsigned gmask = 0xFFFFu << (WLG * (g & 1));
+    double2* tile = reinterpret_cast<double2*>(smem_raw + K1wSmem::sc) + g * 8 * WSS;
+    const int tout = (t >> 1) + 8 * (t & 1);
+
+    const int b = blockIdx.x;
+    if (a.n_dev && b >= *a.n_dev) return;  // device-sized launch (guard re-runs)
+    const BlockDesc d = a.blocks[b];
+    const double* wc = a.wcls + (size_t)d.cls * a.Lh * a.Lw;
+    for (int i = threadIdx.x; i < WT; i += blockDim.x) tw[i] = a.twid[i];
+    for (int i = threadIdx.x; i < 2 * WT; i += blockDim.x) {
+        if (a.ptab) {
+            const double2 p = a.ptab[i];
+            ph[i] = make_double2(p.x, -p.y);
+        } else {
+            ph[i] = phase_pos<WT>(i);
+        }
+    }
+    __syncthreads();
+
+    // ---- row pass: row pair g ----
+    double energy = 0.0;
+    const int npairs = (a.Lh + 1) / 2;
+    if (g < npairs) {
+        const int ra = 2 * g, rb = ra + 1;
+        const bool hasb = rb < a.Lh;
+        const SRC* pa = k1f_row<SRC>(a, d, ra);
+        const SRC* pb = hasb ? k1f_row<SRC>(a, d, rb) : nullptr;
+        const double* wra = wc + ra * a.Lw;
+        const double* wrb = wc + (hasb ? rb : ra) * a.Lw;
+        const int c_lo = -d.col0, c_hi = a.fr.width - d.col0;
+        double2 x[8];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            const int n = t + WLG * m;
+            const bool in = n < a.Lw;
+            const bool inf = in && n >= c_lo && n < c_hi;
+            const double wa = in ? wra[n] : 0.0, wb = (in && hasb) ? wrb[n] : 0.0;
+            const double fa = (inf && pa) ? static_cast<double>(pa[n]) : 0.0;
+            const double fb = (inf && pb) ? static_cast<double>(pb[n]) : 0.0;
+            const double va = wa * fa, vb = wb * fb;
+            energy += va * fa;
+            energy += vb * fb;
+            x[m] = make_double2(va, vb);
+        }
+        fft128_group(x, t, tw, tile, gmask);
+        // lane t holds Z[k], k = tout + 16 q; unpack needs Z[-k]
+#pragma unroll
+        for (int q = 0; q < 8; ++q) tile[q * WSS + tout] = x[q];
+        __syncwarp(gmask);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int k = tout + WLG * q;
+            if (k > WT / 2) continue;
+            const int nk = (WT - k) & (WT - 1);
+            const double2 zc = tile[(nk >> 4) * WSS + (nk & 15)];
+            const double2 z = x[q];
+            cb[k * WCS + ra] = make_double2(0.5 * (z.x + zc.x), 0.5 * (z.y - zc.y));
+            cb[k * WCS + rb] = make_double2(0.5 * (z.y + zc.y), -0.5 * (z.x - zc.x));
+        }
+        __syncwarp(gmask);
+    }
+    energy = block_reduce<double>(energy, red, false);  // (its __syncthreads orders cb)
+    const int nrows = 2 * npairs;
+
+    // ---- column pass + the canonical half, written from the registers ----
+    const BinLayout L = BinLayout::make(WT, a.seg, a.spt > 0 ? a.spt : 1);
+    const bool rotate = path_is_rotated(a.path);
+    const bool f64 = path_is_f64(a.path);
+    const size_t per = a.out_stride > 0 ? (size_t)a.out_stride : packed32_floats(L, a.soa);
+    double vmax2 = 0.0;
+    auto emit = [&](int k1, int k2, double2 v) {
+        vmax2 = fmax(vmax2, fma(v.x, v.x, v.y * v.y));
+        if (rotate) v = c_mul(v, ph[(k1 * (a.Lh - 1) + k2 * (a.Lw - 1)) & (2 * WT - 1)]);
+        int i, tid;
+        bin_slot(L, k1, k2, &i, &tid);
+        if (f64)
+            static_cast<double2*>(a.out)[(size_t)b * L.SLOTS + (size_t)i * L.NT + tid] = v;
+        else
+            put_packed32(static_cast<float*>(a.out) + (size_t)b * per, L, a.soa, i, tid, static_cast<float>(v.x),
+                         static_cast<float>(v.y));
+    };
+#pragma unroll 1
+    for (int jj = 0; jj < 2; ++jj) {
+        const int tr = g + WGR * jj;  // 0..63: columns 1..63, then the packed pair (0, 64)
+        double2 x[8];
+        if (tr < WT / 2 - 1) {
+            const int col = tr + 1;
+#pragma unroll
+            for (int m = 0; m < 8; ++m)
+                x[m] = (t + WLG * m < nrows) ? cb[col * WCS + t + WLG * m] : make_double2(0.0, 0.0);
+            fft128_group(x, t, tw, tile, gmask);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int k1 = tout + WLG * q;
+                if (k1 <= WT / 2)
+                    emit(k1, col, x[q]);
+                else
+                    emit(WT - k1, WT - col, make_double2(x[q].x, -x[q].y));
+            }
+        } else {
+#pragma unroll
+            for (int m = 0; m < 8; ++m)
+                x[m] = (t + WLG * m < nrows) ? make_double2(cb[t + WLG * m].x, cb[(WT / 2) * WCS + t + WLG * m].x)
+                                              : make_double2(0.0, 0.0);
+            fft128_group(x, t, tw, tile, gmask);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) tile[q * WSS + tout] = x[q];
+            __syncwarp(gmask);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int k1 = tout + WLG * q;
+                if (k1 > WT / 2) continue;
+                const int nk = (WT - k1) & (WT - 1);
+                const double2 zc = tile[(nk >> 4) * WSS + (nk & 15)];
+                const double2 z = x[q];
+                emit(k1, 0, make_double2(0.5 * (z.x + zc.x), 0.5 * (z.y - zc.y)));
+                emit(k1, WT / 2, make_double2(0.5 * (z.y + zc.y), -0.5 * (z.x - zc.x)));
+            }
+        }
+        __syncwarp(gmask);
+    }
+    // unused extra slots (segments without the self-conjugate extra bin) read as 0
+    for (int tid = threadIdx.x; tid < L.NT * L.SPT; tid += blockDim.x) {
+        const int th = tid % L.NT, sg = tid / L.NT;
+        int k1, c0, ex;
+        L.thread_segment(th, sg, &k1, &c0, &ex);
+        if (ex) continue;
+        const int i = sg * (L.SEG + 1) + L.SEG;
+        if (f64)
+            static_cast<double2*>(a.out)[(size_t)b * L.SLOTS + (size_t)i * L.NT + th] = make_double2(0.0, 0.0);
+        else
+            put_packed32(static_cast<float*>(a.out) + (size_t)b * per, L, a.soa, i, th, 0.f, 0.f);
+    }
+    vmax2 = block_reduce<double>(vmax2, red, true);
+    if (threadIdx.x == 0) {
+        a.energy[b] = energy;
+        a.init_max[b] = sqrt(vmax2);
+    }
+}
+
 }  // namespace
 
 bool k1f_supported(const K1Args& a) {
+    if (a.T == 128)  // windows of at most 64 x 64 (the spectrum tile holds 64 rows)
+        return a.mode == K1_PACKED && a.Lh <= 64 && a.Lw <= 64 && (a.spt <= 1);
     if ((a.T != 32 && a.T != 64) || a.mode != K1_PACKED || a.Lh > a.T || a.Lw > a.T) return false;
     const int threads = a.T * a.T / 16;
     const BinLayout L = BinLayout::make(a.T, a.seg, a.spt > 0 ? a.spt : 1);
@@ -330,7 +523,22 @@ static int k1f_launch_t(const K1Args& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+static int k1w_launch(const K1Args& a, cudaStream_t s) {
+    cudaError_t e = cudaFuncSetAttribute(k1w_kernel<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)K1wSmem::total);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k1w_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K1wSmem::total);
+    if (e != cudaSuccess) return e;
+    if (a.n <= 0) return cudaSuccess;
+    if (a.fr.type == SRC_U8)
+        k1w_kernel<uint8_t><<<a.n, WGR * WLG, K1wSmem::total, s>>>(a);
+    else
+        k1w_kernel<double><<<a.n, WGR * WLG, K1wSmem::total, s>>>(a);
+    return cudaGetLastError();
+}
+
 int k1f_launch(const K1Args& a, cudaStream_t s) {
+    if (a.T == 128) return k1w_launch(a, s);
     return a.T == 32 ? k1f_launch_t<32>(a, s) : k1f_launch_t<64>(a, s);
 }
 
