@@ -1159,11 +1159,16 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             int64_t b0, b1;
             cudaStream_t s;
             int grp;
+            bool f64_direct = false;  // a small border range run in fp64 outright (no head, no guard)
         };
         std::vector<Chunk> chunks;
         const int64_t chunk_min = 24576;  // blocks: keeps every chunk several waves deep
         int nsm = 148;
         ck(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device), "SM count");
+        const bool f64_direct_on = [] {  // FOFSE_BORDER_F64=0: small border ranges take the fp32 path
+            const char* e = std::getenv("FOFSE_BORDER_F64");
+            return !(e && e[0] == '0');
+        }();
         const int64_t one_wave = 2LL * nsm;  // a border range this small goes on the high-priority stream
         // real ranges: chunks of a whole number of the fp32 kernel's waves (the
         // last takes the remainder), at least chunk_min blocks, at most 8 per range
@@ -1173,7 +1178,11 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             const int64_t len = r.end - r.begin;
             const cudaStream_t cs = on_side ? (len <= one_wave ? ctx->side_hi : ctx->side) : st;
             if (r.path != PATH_F32_REAL) {
-                chunks.push_back({r.path, r.begin, r.end, cs, r.grp});
+                // a border range under one wave runs in fp64 outright (K2dc, T <= 64),
+                // concurrently with the main chunks: no head / convert / guard re-runs
+                // (C2 +2 %; at T = 128 only the slow strict kernel could, measured -3 %)
+                chunks.push_back({r.path, r.begin, r.end, cs, r.grp,
+                                  f64_direct_on && on_side && len <= one_wave && hi_path(r.path) == PATH_F64_CPLX});
                 continue;
             }
             const int nc = static_cast<int>(std::clamp<int64_t>(len / chunk_min, 1, 8));
@@ -1202,7 +1211,8 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         for (size_t ci = 0; ci < chunks.size(); ++ci) {
             const Chunk& ch = chunks[ci];
             for (int k = 0; k < 2; ++k) {
-                if (k == 0 && head == 0) continue;
+                if (k == 0 && head == 0 && !ch.f64_direct) continue;
+                if (k == 1 && ch.f64_direct) continue;
                 const bool kv2 = ch.path == PATH_F32_REAL ? v2r : v2;
                 const int ng = k == 0 ? ng_f64(hi_path(ch.path)) : kv2 ? k2v2_warps_per_cta(T) : k2_groups_per_cta(T, ch.path);
                 TList& tl = tls[2 * ci + static_cast<size_t>(k)];
@@ -1354,6 +1364,8 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         };
         ck(cudaStreamWaitEvent(ctx->aux, ctx->ev[4], 0), "wait");
         std::vector<char> waited(static_cast<size_t>(2 * ngroups), 0);  // [group][main/side] upload waits
+        for (const Chunk& ch : chunks)
+            if (ch.f64_direct && !d_R64) d_R64 = ctx->buf("R64").as<char>(static_cast<size_t>(n) * r64_bytes);
         // per chunk: events [3i] after K1, [3i+1] before the fp32 iteration, [3i+2] done
         for (size_t ci = 0; ci < chunks.size(); ++ci) {
             const Chunk& ch = chunks[ci];
@@ -1369,6 +1381,17 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
                 wt = 1;
             }
             ck(cudaEventRecord(ctx->event(3 * ci + 0), ps), "event");
+            if (ch.f64_direct) {  // fp64 outright: K1 + the fp64 kernel for all I selections
+                const int hp = hi_path(ch.path);
+                k1_packed(d_sorted + ch.b0, cn, hp, seg64, 1, d_R64 + static_cast<size_t>(ch.b0) * r64_bytes,
+                          d_e0 + ch.b0, d_imax + ch.b0, 0, 0, ch.s);
+                ck(cudaEventRecord(ctx->event(3 * ci + 1), ch.s), "event");
+                K2Args a = base_args();
+                a.rin = d_R64;
+                k2_f64(a, hp, ch.b0, ch.b1, sorted, "d" + tag, ch.s, cut_tiles(2 * ci, ch.s), tls[2 * ci].nt);
+                ck(cudaEventRecord(ctx->event(3 * ci + 2), ch.s), "event");
+                continue;
+            }
             if (head > 0) {
                 k1_packed(d_sorted + ch.b0, cn, hi_path(ch.path), seg64, 1,
                           d_R64 + static_cast<size_t>(ch.b0) * r64_bytes, d_e0 + ch.b0, d_imax + ch.b0, 0, 0, ps);
@@ -1468,12 +1491,14 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
                 for (size_t cj = 0; cj <= ci; ++cj) {
                     if (chunks[cj].grp != ch.grp) continue;
                     ck(cudaStreamWaitEvent(ctx->io, ctx->event(3 * cj + 2), 0), "wait");
-                    ck(cudaStreamWaitEvent(ctx->io, ctx->event(dev_guard(chunks[cj]) ? ev_guard + cj : ev_host + cj), 0),
-                       "wait");
+                    if (!chunks[cj].f64_direct)
+                        ck(cudaStreamWaitEvent(ctx->io,
+                                               ctx->event(dev_guard(chunks[cj]) ? ev_guard + cj : ev_host + cj), 0),
+                           "wait");
                 }
                 gio->on_done(ch.grp, ctx->io);
             };
-            if (dev_guard(ch)) {
+            if (dev_guard(ch) || ch.f64_direct) {
                 group_done();
                 continue;
             }
