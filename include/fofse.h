@@ -40,8 +40,8 @@ enum {
 };
 
 /* fse::Algorithm (include/fse/pipeline.hpp:13). fse == fofse with gamma 1
- * (pipeline.cpp:188-190); ofse (full-OD compensation) is FOFSE_EUNSUPPORTED
- * in this build. */
+ * (pipeline.cpp:188-190); ofse (full-OD compensation, engine_spectral.cpp:
+ * 79-97) runs in fp64 (an fp32 request is promoted). */
 enum { FOFSE_ALGO_FSE = 0, FOFSE_ALGO_OFSE = 1, FOFSE_ALGO_FOFSE = 2 };
 
 /* Arithmetic of the iteration. FP64 reproduces the reference's selected-basis
