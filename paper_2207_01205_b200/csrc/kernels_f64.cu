@@ -146,11 +146,14 @@ __device__ __forceinline__ void d_replay(const K2Args& a, const double* vE, cons
         const double s = ((p1 + q1 >= T) ? sgn_r : 1.0) * ((p2 + q2 >= T) ? sgn_c : 1.0);
         return s * vE[((p1 + q1) & (T - 1)) * SRV + ((p2 + q2) & (T - 1))];
     };
-    if (w == 0) {
+    // every thread of the group: the scalar part replicated, the fold of each new a_q
+    // into the later selections split across the group (thread l keeps R'[u_q] for
+    // q = l mod GT), one group barrier per selection
+    {
         double energy = e_init;
         const double thr_e = 1e-12 * e_init, thr_m = (1e-12 * imax) * (1e-12 * imax);
         int nf = min(a.nu_flag[pos], rstride), conv = e_init <= 0.0;
-        for (int q = lane; q < nf; q += 32) {  // R'_0 at every selected bin, in parallel
+        for (int q = ltid; q < nf; q += GT) {  // R'_0 at every selected bin, in parallel
             const int u = rec_u[q], u1 = u >> 16, u2 = u & 0xffff;
             int slot, tid;
             bin_slot(Ls, u1, u2, &slot, &tid);
@@ -158,7 +161,7 @@ __device__ __forceinline__ void d_replay(const K2Args& a, const double* vE, cons
             sel[q].u1 = u1;
             sel[q].u2 = u2;
         }
-        __syncwarp();
+        named_bar_sync(bar, GT);
         for (int q = 0; q < nf && !conv; ++q) {
             const int u1 = sel[q].u1, u2 = sel[q].u2;
             const double pr = pend[q].x, pi = pend[q].y;
@@ -188,14 +191,14 @@ __device__ __forceinline__ void d_replay(const K2Args& a, const double* vE, cons
             }
             const double e = energy + delta;
             energy = 0.0 < e ? e : 0.0;
-            if (lane == 0) {
+            if (ltid == 0) {
                 sel[q].ar = a_re;
                 sel[q].ai = a_im;
                 sel[q].self = self;
                 rec_c[q] = self ? make_double2(c_re, 0.0) : make_double2(2.0 * c_re, 2.0 * c_im);
             }
-            // fold a_q into this lane's later selections (the K2d update at bin u_t)
-            for (int t = q + 1 + ((lane - q - 1) & 31); t < nf; t += 32) {
+            // fold a_q into this thread's later selections (the K2d update at bin u_t)
+            for (int t = q + 1 + ((ltid - q - 1) % GT + GT) % GT; t < nf; t += GT) {
                 const int t1 = sel[t].u1, t2 = sel[t].u2;
                 const double v1 = vdiff(t1, t2, u1, u2);
                 double dr = a_re * v1, di = a_im * v1;
@@ -206,9 +209,9 @@ __device__ __forceinline__ void d_replay(const K2Args& a, const double* vE, cons
                 }
                 pend[t] = make_double2(pend[t].x - dr, pend[t].y - di);
             }
-            __syncwarp();
+            named_bar_sync(bar, GT);
         }
-        if (lane == 0) {
+        if (ltid == 0) {
             bcast[0] = energy;
             bcast[1] = (double)nf;
             bcast[2] = (double)conv;
