@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(128, VAR == 0 ? 3 : 2) k2v2r_kernel(K2Args a) 
             if (lane == 0) {
                 if (nu - 1 < rstride) {
                     rec_u[nu - 1] = (u1 << 16) | u2;
-                    rec_c[nu - 1] = self ? make_double2(c_re, 0.0) : make_double2(2.0 * c_re, 2.0 * c_im);
+                    rec_c[nu - 1] = make_double2(self ? c_re : 2.f * c_re, self ? 0.f : 2.f * c_im);  // exact doubling in fp32
                 }
                 st->energy = en;
                 st->nu = nu;
