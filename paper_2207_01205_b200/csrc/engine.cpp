@@ -237,6 +237,7 @@ struct fofse_ctx {
     std::map<std::string, DevBuf> bufs;
     cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     std::vector<cudaEvent_t> evpool;  // per-chunk events of the fp32 pipeline
+    size_t total_mem = 0;  // device memory (bytes), queried once
     // job storage of fofse_conceal_frames_u8, reused from call to call
     std::unique_ptr<fofse_plan, void (*)(fofse_plan*)> frames_plan{nullptr, fofse_plan_destroy};
     int64_t launches = 0;
@@ -2115,14 +2116,12 @@ int fofse_plan_execute_device(fofse_plan* plan, uint8_t* d_frames, double* d_blo
     });
 }
 
-int fofse_conceal_frames_u8(fofse_ctx* ctx, const uint8_t* frames, int32_t n_frames, int32_t width,
-                            int32_t height, const fofse_rect* blocks, const int64_t* offs,
-                            int32_t bh, int32_t bw, const fofse_params* params, uint8_t* restored,
-                            double* block_sq, fofse_report* report) {
-    return guarded([&] {
-        if (!ctx || !frames || !restored || !offs || n_frames < 1)
-            throw std::invalid_argument("conceal_frames: bad argument");
-        if (width < 1 || height < 1) throw std::invalid_argument("grid dimensions must be >= 1");
+// One batch of frames through the pipelined frames path (see fofse_conceal_frames_u8).
+static void conceal_frames_batch(fofse_ctx* ctx, const uint8_t* frames, int32_t n_frames, int32_t width,
+                                 int32_t height, const fofse_rect* blocks, const int64_t* offs, int32_t bh,
+                                 int32_t bw, const fofse_params* params, uint8_t* restored, double* block_sq,
+                                 fofse_report* report) {
+    {
         ctx->activate();
         // Frames are processed as G groups: group uploads are queued up front on
         // the io stream (overlapping the host-side validation + classification of
@@ -2224,6 +2223,87 @@ int fofse_conceal_frames_u8(fofse_ctx* ctx, const uint8_t* frames, int32_t n_fra
         if (block_sq && n) std::memcpy(block_sq, sq.data(), sizeof(double) * n);
         fill_report(report, ro, n, static_cast<int64_t>(plan->job.cls_labels.size()), tot,
                     n * static_cast<int64_t>(bh) * bw, ctx->launches - l0);
+    }
+}
+
+int fofse_conceal_frames_u8(fofse_ctx* ctx, const uint8_t* frames, int32_t n_frames, int32_t width,
+                            int32_t height, const fofse_rect* blocks, const int64_t* offs,
+                            int32_t bh, int32_t bw, const fofse_params* params, uint8_t* restored,
+                            double* block_sq, fofse_report* report) {
+    return guarded([&] {
+        if (!ctx || !frames || !restored || !offs || n_frames < 1)
+            throw std::invalid_argument("conceal_frames: bad argument");
+        if (width < 1 || height < 1) throw std::invalid_argument("grid dimensions must be >= 1");
+        if (offs[0] != 0) throw std::invalid_argument("frame_offsets[0] must be 0");
+        for (int f = 0; f < n_frames; ++f)
+            if (offs[f + 1] - offs[f] < 0) throw std::invalid_argument("frame_offsets must be non-decreasing");
+        ctx->activate();
+        // A request larger than device memory runs as consecutive batches of whole
+        // frames (each a full pipelined call): the per-block device state is about
+        // 14 T^2 + 20 I bytes, kept under half of the device memory.
+        const Cfg cfg = to_cfg(params);
+        const int64_t per_block = 14LL * cfg.T * cfg.T + 20LL * std::max(cfg.iterations, 0) + 512;
+        if (ctx->total_mem == 0) {  // once per context (cudaMemGetInfo is not free)
+            size_t free_b = 0, total_b = 0;
+            ck(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+            ctx->total_mem = total_b;
+        }
+        const int64_t fs = static_cast<int64_t>(width) * height;
+        int64_t max_blocks = static_cast<int64_t>(ctx->total_mem / 2) / per_block;
+        if (const char* e = std::getenv("FOFSE_MAX_BATCH_BLOCKS")) max_blocks = std::max<int64_t>(1, std::atoll(e));
+        const int64_t n_all = offs[n_frames];
+        if (n_all <= max_blocks) {
+            conceal_frames_batch(ctx, frames, n_frames, width, height, blocks, offs, bh, bw, params, restored, block_sq,
+                                 report);
+            return;
+        }
+        {  // validate the whole request first: errors name the caller's frame index
+            Job check;
+            fill_image_job(check, cfg, width, height, bh, bw, blocks, offs, n_frames);
+        }
+        fofse_report agg{};
+        double sq_total = 0.0;
+        std::vector<double> sq_all;
+        double* sq_out = block_sq;
+        if (!sq_out) {
+            sq_all.resize(static_cast<size_t>(n_all));
+            sq_out = sq_all.data();
+        }
+        std::vector<int64_t> boffs;
+        for (int f0 = 0; f0 < n_frames;) {
+            int f1 = f0 + 1;  // at least one frame per batch
+            while (f1 < n_frames && offs[f1 + 1] - offs[f0] <= max_blocks) ++f1;
+            boffs.assign(offs + f0, offs + f1 + 1);
+            for (auto& o : boffs) o -= offs[f0];
+            fofse_report r{};
+            conceal_frames_batch(ctx, frames + f0 * fs, f1 - f0, width, height, blocks + offs[f0], boffs.data(), bh,
+                                 bw, params, restored + f0 * fs, sq_out + offs[f0], &r);
+            agg.blocks += r.blocks;
+            agg.classes = std::max(agg.classes, r.classes);
+            agg.guard_reruns += r.guard_reruns;
+            agg.converged_blocks += r.converged_blocks;
+            agg.init_ms += r.init_ms;
+            agg.iterate_ms += r.iterate_ms;
+            agg.total_ms += r.total_ms;
+            agg.kernel_launches += r.kernel_launches;
+            agg.rerun_ms += r.rerun_ms;
+            agg.fp64_head = r.fp64_head;
+            agg.real_blocks += r.real_blocks;
+            agg.real_iterate_ms += r.real_iterate_ms;
+            f0 = f1;
+        }
+        for (int64_t i = 0; i < n_all; ++i) sq_total += sq_out[i];
+        if (report) {
+            *report = agg;
+            report->mean_seconds_per_block = agg.blocks ? agg.total_ms * 1e-3 / static_cast<double>(agg.blocks) : 0.0;
+            const int64_t missing = n_all * static_cast<int64_t>(bh) * bw;
+            if (n_all == 0 || sq_total == 0.0) {
+                report->psnr_identical = 1;
+                report->psnr_db = 0.0;
+            } else {
+                report->psnr_db = 10.0 * std::log10(255.0 * 255.0 / (sq_total / static_cast<double>(missing)));
+            }
+        }
     });
 }
 

@@ -599,6 +599,26 @@ def test_frame_groups_match_single_frames(gpu, nframes):
     assert k > 3 and rep.device["blocks"] == sum(len(p.blocks) for p in pats)
 
 
+def test_frames_api_batches_large_requests(gpu, monkeypatch):
+    """A request above the device-memory budget runs as consecutive batches of
+    whole frames (forced here with FOFSE_MAX_BATCH_BLOCKS): same bytes, same
+    per-block errors and the same PSNR as one call."""
+    rng = np.random.default_rng(491)
+    frames = np.stack([np.clip(smooth_test_image(rng, 128), 0, 255).astype(np.uint8) for _ in range(12)])
+    pats = []
+    for f in range(12):
+        rr = P.gen_losses(700 + f, 8, 8, 0.15, 16, 16)
+        pats.append(P.LossPattern(128, 128, 16, 16, [P.Rect(*map(int, (r["row"], r["col"], 16, 16))) for r in rr]))
+    cfg = WL.C4.config("fp32")
+    one, sq1, rep1 = P.conceal_frames(frames, pats, cfg)
+    monkeypatch.setenv("FOFSE_MAX_BATCH_BLOCKS", "20")
+    many, sqn, repn = P.conceal_frames(frames, pats, cfg)
+    np.testing.assert_array_equal(one, many)
+    np.testing.assert_allclose(sq1, sqn, rtol=1e-12)
+    assert repn.device["blocks"] == rep1.device["blocks"] == sum(len(p.blocks) for p in pats)
+    assert repn.psnr_db == pytest.approx(rep1.psnr_db, rel=1e-12)
+
+
 def test_shards_reassemble_the_full_run(gpu):
     """fofse_conceal_shard_f64: disjoint shards (every block still lost) reproduce
     the single-call result bit for bit — the multi-GPU decomposition."""
