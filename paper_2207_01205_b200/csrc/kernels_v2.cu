@@ -18,6 +18,8 @@
 #include <stdint.h>
 
 #include <climits>
+#include <map>
+#include <mutex>
 #include <cstdlib>
 #include <type_traits>
 
@@ -1138,8 +1140,7 @@ static int64_t wave_t(int dev) {
     }
 }
 
-int64_t k2v2_real_wave(int t, int dev, int gw) {
-    if ((t == 64 && gw == 2) || v2r_variant() != 0) return 0;  // K2v2h at T = 64 / experiments: no alignment
+static int64_t k2v2_real_wave_q(int t, int dev) {
     switch (t) {
         case 8: return wave_t<8>(dev);
         case 16: return wave_t<16>(dev);
@@ -1165,6 +1166,19 @@ bool v2h128_enabled() {
     return on != 0;
 }
 
+// per (T, device) once: the occupancy query is not free and run_job asks every call
+int64_t k2v2_real_wave(int t, int dev, int gw) {
+    if ((t == 64 && gw == 2) || v2r_variant() != 0) return 0;  // K2v2h at T = 64 / experiments: no alignment
+    static std::mutex mu;
+    static std::map<std::pair<int, int>, int64_t> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find({t, dev});
+    if (it != cache.end()) return it->second;
+    const int64_t w = k2v2_real_wave_q(t, dev);
+    cache[{t, dev}] = w;
+    return w;
+}
+
 int v2_choose_real_gw(int t, int64_t real_blocks, int dev) {
     if (t != 64) return 1;
     static const int forced = [] {
@@ -1175,16 +1189,31 @@ int v2_choose_real_gw(int t, int64_t real_blocks, int dev) {
     if (v2r_variant() != 0 || real_blocks <= 0) return 1;
     // makespan in per-block latencies: K2v2r ceil(N / W1) x 1, K2v2h ceil(N / W2) x 0.7
     // (the latency ratio measured on C4: 21 K2v2h waves take 1.04 x 14 K2v2r waves)
-    int nsm = 0, p1 = 0, p2 = 0;
-    if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 1;
-    using C1 = V2Cfg<64, PATH_F32_REAL>;
-    using C2 = V2HCfg<64>;
-    cudaFuncSetAttribute(k2v2r_kernel<64, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C1::SMEM);
-    cudaFuncSetAttribute(k2v2h_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C2::SMEM);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p1, k2v2r_kernel<64, 0>, 32 * C1::WARPS, C1::SMEM) != cudaSuccess ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2, k2v2h_kernel<64>, C2::THREADS, C2::SMEM) != cudaSuccess)
-        return 1;
-    const int64_t w1 = (int64_t)nsm * p1 * C1::WARPS, w2 = (int64_t)nsm * p2 * C2::GROUPS;
+    static std::mutex mu;
+    static std::map<int, std::pair<int64_t, int64_t>> cache;  // device -> (W1, W2)
+    int64_t w1 = 0, w2 = 0;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find(dev);
+        if (it != cache.end()) {
+            w1 = it->second.first;
+            w2 = it->second.second;
+        } else {
+            int nsm = 0, p1 = 0, p2 = 0;
+            if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 1;
+            using C1 = V2Cfg<64, PATH_F32_REAL>;
+            using C2 = V2HCfg<64>;
+            cudaFuncSetAttribute(k2v2r_kernel<64, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C1::SMEM);
+            cudaFuncSetAttribute(k2v2h_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C2::SMEM);
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p1, k2v2r_kernel<64, 0>, 32 * C1::WARPS, C1::SMEM) !=
+                    cudaSuccess ||
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2, k2v2h_kernel<64>, C2::THREADS, C2::SMEM) != cudaSuccess)
+                return 1;
+            w1 = (int64_t)nsm * p1 * C1::WARPS;
+            w2 = (int64_t)nsm * p2 * C2::GROUPS;
+            cache[dev] = {w1, w2};
+        }
+    }
     if (w1 <= 0 || w2 <= 0) return 1;
     const double m1 = (double)((real_blocks + w1 - 1) / w1), m2 = 0.7 * (double)((real_blocks + w2 - 1) / w2);
     return m2 < m1 ? 2 : 1;
