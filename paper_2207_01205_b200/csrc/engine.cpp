@@ -921,15 +921,16 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
     hp_.mark("upload order");
     struct Range { int path; int64_t begin, end; int grp; };
     std::vector<Range> ranges;
-    for (int64_t p0 = 0; p0 < n;) {
-        const int p = path_of(sorted[static_cast<size_t>(p0)].cls);
-        const int gq = job.group_of(sorted[static_cast<size_t>(p0)]);
-        int64_t p1 = p0;
-        while (p1 < n && path_of(sorted[static_cast<size_t>(p1)].cls) == p &&
-               job.group_of(sorted[static_cast<size_t>(p1)]) == gq)
-            ++p1;
-        ranges.push_back({p, p0, p1, gq});
-        p0 = p1;
+    // (group, path) ranges from the key runs of the execution order (each run has
+    // one group, path and class): O(runs), not O(blocks)
+    for (size_t k = 0; k < job.runs.size(); ++k) {
+        const int64_t p0 = job.runs[k], p1 = k + 1 < job.runs.size() ? job.runs[k + 1] : n;
+        const BlockDesc& d = sorted[static_cast<size_t>(p0)];
+        const int p = path_of(d.cls), gq = job.group_of(d);
+        if (!ranges.empty() && ranges.back().path == p && ranges.back().grp == gq && ranges.back().end == p0)
+            ranges.back().end = p1;
+        else
+            ranges.push_back({p, p0, p1, gq});
     }
     const int ngroups = job.groups;
     for (const Range& r : ranges)
