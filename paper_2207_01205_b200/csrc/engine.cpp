@@ -527,11 +527,20 @@ struct Job {
     std::vector<BlockDesc> blocks;          // caller order
     std::vector<std::vector<uint8_t>> cls_labels;
     std::vector<double> wfull;
-    // frame groups of the pipelined frames API (group-major execution order)
+    // row groups of the pipelined frames API (group-major execution order): the
+    // frames' rows, concatenated, cut into `groups` bands; group g = rows
+    // [group_row_end[g-1], group_row_end[g]). A block belongs to the band holding
+    // the last row its window reads (so its group's upload covers its window).
     int groups = 1;
-    std::vector<int32_t> frame_group;  // group of each frame (groups > 1)
+    int frame_rows = 0;                   // frame height
+    std::vector<int64_t> group_row_end;  // (groups > 1)
+    std::vector<int32_t> frame_group;    // bands on frame boundaries: each frame's group
     int group_of(const BlockDesc& d) const {
-        return groups > 1 ? frame_group[static_cast<size_t>(d.frame)] : 0;
+        if (groups <= 1) return 0;
+        if (!frame_group.empty()) return frame_group[static_cast<size_t>(d.frame)];
+        const int64_t last = static_cast<int64_t>(d.frame) * frame_rows + std::min(d.row0 + geo.Lh, frame_rows) - 1;
+        return static_cast<int>(std::upper_bound(group_row_end.begin(), group_row_end.end(), last) -
+                                group_row_end.begin());
     }
     // cached execution order (run_job): caller ids by position and their descs,
     // start positions of the (group, path, class) key runs
@@ -1714,6 +1723,7 @@ void fill_image_job(Job& job, const Cfg& cfg, int W, int H, int bh, int bw, cons
     const HostProf hp_;
     job.order_key = -1;
     job.groups = 1;
+    job.group_row_end.clear();
     job.frame_group.clear();
     job.cls_labels.clear();
     job.geo = Geometry{cfg.T, bh, bw, cfg.S, bh + 2 * cfg.S, bw + 2 * cfg.S};
@@ -2131,22 +2141,32 @@ static void conceal_frames_batch(fofse_ctx* ctx, const uint8_t* frames, int32_t 
         // are done — transfers overlap the iteration of the other groups.
         const size_t fs = static_cast<size_t>(width) * height;
         const size_t bytes = static_cast<size_t>(n_frames) * fs;
-        const int G = (params && params->precision == FOFSE_PREC_FP32)
-                          ? static_cast<int>(std::clamp<int32_t>(n_frames / 16, 1, 8)) : 1;
-        // group boundaries: the first and last groups are a quarter of the others —
-        // the first upload and the last download are the only transfers that
-        // nothing overlaps
-        std::vector<size_t> gb(static_cast<size_t>(G) + 1, 0);
+        // Groups are bands of the frames' concatenated rows: whole frames for
+        // frame batches (>= 16 frames). Row bands of fewer, big frames
+        // (FOFSE_ROW_GROUPS) overlap a frame's transfers with its iteration, but
+        // measured slower on C3/C5 (each band's chunk runs its K1 + fp64 head
+        // after the previous band's iteration, in partial waves) — off by default.
+        const bool fp32 = params && params->precision == FOFSE_PREC_FP32;
+        const bool by_frame = n_frames >= 16;
+        int G = fp32 && by_frame ? std::clamp<int32_t>(n_frames / 16, 1, 8) : 1;
+        if (const char* e = std::getenv("FOFSE_ROW_GROUPS"); e && fp32 && !by_frame)
+            G = std::clamp(std::atoi(e), 1, std::max(1, height / 64));
+        // group boundaries (rows): the first and last groups are a quarter of the
+        // others — the first upload and the last download are the only transfers
+        // that nothing overlaps
+        const int64_t unit_rows = by_frame ? height : 1;
+        const int64_t nunits = static_cast<int64_t>(n_frames) * height / unit_rows;
+        std::vector<int64_t> gb(static_cast<size_t>(G) + 1, 0);  // row boundaries
         {
             const int units = G <= 2 ? G : 4 * (G - 2) + 2;
             int u = 0;
             for (int gq = 0; gq < G; ++gq) {
                 u += (G <= 2 || gq == 0 || gq == G - 1) ? 1 : 4;
-                gb[static_cast<size_t>(gq) + 1] = static_cast<size_t>((static_cast<int64_t>(u) * n_frames + units - 1) / units);
+                gb[static_cast<size_t>(gq) + 1] = (static_cast<int64_t>(u) * nunits + units - 1) / units * unit_rows;
             }
-            gb[static_cast<size_t>(G)] = static_cast<size_t>(n_frames);
+            gb[static_cast<size_t>(G)] = static_cast<int64_t>(n_frames) * height;
         }
-        auto f0 = [&](int gq) { return gb[static_cast<size_t>(gq)]; };
+        auto f0 = [&](int gq) { return static_cast<size_t>(gb[static_cast<size_t>(gq)]) * width; };  // byte offset
         uint8_t* d_fr = ctx->buf("frames_u8").as<uint8_t>(bytes);
         std::vector<cudaEvent_t> h2d(static_cast<size_t>(G), nullptr);
         struct EvHold {
@@ -2161,7 +2181,7 @@ static void conceal_frames_batch(fofse_ctx* ctx, const uint8_t* frames, int32_t 
             for (; h2d_next <= g && h2d_next < G; ++h2d_next) {
                 const int gq = h2d_next;
                 ck(cudaEventCreateWithFlags(&h2d[static_cast<size_t>(gq)], cudaEventDisableTiming), "cudaEventCreate");
-                const size_t a0 = f0(gq) * fs, a1 = f0(gq + 1) * fs;
+                const size_t a0 = f0(gq), a1 = f0(gq + 1);
                 if (a1 > a0)
                     ck(cudaMemcpyAsync(d_fr + a0, frames + a0, a1 - a0, cudaMemcpyHostToDevice, ctx->io), "H2D frames");
                 ck(cudaEventRecord(h2d[static_cast<size_t>(gq)], ctx->io), "event");
@@ -2182,10 +2202,30 @@ static void conceal_frames_batch(fofse_ctx* ctx, const uint8_t* frames, int32_t 
         }
         hp_.mark("conceal_frames: plan (validate + classify)");
         plan->job.groups = G;
-        plan->job.frame_group.assign(static_cast<size_t>(n_frames), 0);
-        for (int gq = 0; gq < G; ++gq)
-            for (size_t f = f0(gq); f < f0(gq + 1); ++f) plan->job.frame_group[f] = gq;
+        plan->job.frame_rows = height;
+        plan->job.group_row_end.assign(gb.begin() + 1, gb.end() - 1);
+        if (by_frame && G > 1) {
+            plan->job.frame_group.resize(static_cast<size_t>(n_frames));
+            for (int gq = 0; gq < G; ++gq)
+                for (int64_t f = gb[static_cast<size_t>(gq)] / height; f < gb[static_cast<size_t>(gq) + 1] / height; ++f)
+                    plan->job.frame_group[static_cast<size_t>(f)] = gq;
+        }
         const int64_t n = static_cast<int64_t>(plan->job.blocks.size());
+        // downloads: once groups <= g are done, the rows above the first row any
+        // later group's block writes (and inside the uploaded bands) are final
+        std::vector<int64_t> final_after(static_cast<size_t>(G), static_cast<int64_t>(n_frames) * height);
+        if (G > 1 && !by_frame) {  // (frame bands: a block writes inside its own band)
+            std::vector<int64_t> first_write(static_cast<size_t>(G), static_cast<int64_t>(n_frames) * height);
+            for (const BlockDesc& d : plan->job.blocks) {
+                int64_t& fw = first_write[static_cast<size_t>(plan->job.group_of(d))];
+                fw = std::min<int64_t>(fw, static_cast<int64_t>(d.frame) * height + d.row0 + plan->job.geo.S);
+            }
+            for (int gq = G - 2; gq >= 0; --gq)
+                final_after[static_cast<size_t>(gq)] =
+                    std::min(final_after[static_cast<size_t>(gq) + 1], first_write[static_cast<size_t>(gq) + 1]);
+        }
+        for (int gq = 0; gq < G; ++gq)
+            final_after[static_cast<size_t>(gq)] = std::min(final_after[static_cast<size_t>(gq)], gb[static_cast<size_t>(gq) + 1]);
         double* d_sq = ctx->buf("sq").as<double>(static_cast<size_t>(std::max<int64_t>(n, 1)));
         const int64_t l0 = ctx->launches;
         GroupIO gio;
@@ -2194,12 +2234,15 @@ static void conceal_frames_batch(fofse_ctx* ctx, const uint8_t* frames, int32_t 
             ensure_h2d(g);
             gio.h2d_done = h2d;
         };
-        std::vector<char> down(static_cast<size_t>(G), 0);
-        gio.on_done = [&](int gq, cudaStream_t s) {
-            const size_t a0 = f0(gq) * fs, a1 = f0(gq + 1) * fs;
-            if (a1 > a0) ck(cudaMemcpyAsync(restored + a0, d_fr + a0, a1 - a0, cudaMemcpyDeviceToHost, s), "D2H frames");
-            down[static_cast<size_t>(gq)] = 1;
+        int64_t down_rows = 0;  // rows [0, down_rows) have their download enqueued
+        auto download_to = [&](int64_t r1, cudaStream_t s) {
+            if (r1 <= down_rows) return;
+            const size_t a0 = static_cast<size_t>(down_rows) * width, a1 = static_cast<size_t>(r1) * width;
+            ck(cudaMemcpyAsync(restored + a0, d_fr + a0, a1 - a0, cudaMemcpyDeviceToHost, s), "D2H frames");
+            down_rows = r1;
         };
+        // group g done (groups complete in order)
+        gio.on_done = [&](int gq, cudaStream_t s) { download_to(final_after[static_cast<size_t>(gq)], s); };
         RunOut ro;
         fofse::Frames fr{d_fr, d_fr, fofse::SRC_U8, width, height, static_cast<int64_t>(fs)};
         try {
@@ -2207,8 +2250,7 @@ static void conceal_frames_batch(fofse_ctx* ctx, const uint8_t* frames, int32_t 
                 ro = run_job(ctx, plan->job, plan->cfg, fr, fofse::SYN_IMAGE, d_sq, nullptr, nullptr, nullptr, nullptr,
                              &gio);
             ensure_h2d(G - 1);
-            for (int gq = 0; gq < G; ++gq)  // groups without lost blocks come back unchanged
-                if (!down[static_cast<size_t>(gq)]) gio.on_done(gq, ctx->io);
+            download_to(static_cast<int64_t>(n_frames) * height, ctx->io);  // the rest (and unchanged groups)
         } catch (...) {
             // the caller's host buffers may still be in flight on the copy streams
             cudaStreamSynchronize(ctx->io);

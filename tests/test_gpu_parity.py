@@ -599,6 +599,34 @@ def test_frame_groups_match_single_frames(gpu, nframes):
     assert k > 3 and rep.device["blocks"] == sum(len(p.blocks) for p in pats)
 
 
+@pytest.mark.parametrize("nframes,groups", [(1, 3), (1, 8), (3, 5)])
+def test_row_groups_match_one_group(gpu, monkeypatch, nframes, groups):
+    """Fewer than 16 frames: the frames' rows are cut into bands (first/last a
+    quarter of the others; band uploads overlap iteration, each row range comes
+    back once no later band's block writes into it). Forced band counts
+    (FOFSE_ROW_GROUPS) give the bytes of one group, including bands without
+    losses (the bottom quarter of frame 0 is loss-free)."""
+    rng = np.random.default_rng(497 + nframes)
+    H, W = 512, 384
+    frames = np.stack([np.clip(smooth_test_image(rng, H)[:, :W] + 0.0, 0, 255).astype(np.uint8)
+                       for _ in range(nframes)])
+    pats = []
+    for f in range(nframes):
+        rr = P.gen_losses(900 + f, W // 16, H // 16, 0.15, 16, 16)
+        rects = [P.Rect(*map(int, (r["row"], r["col"], 16, 16))) for r in rr]
+        if f == 0:
+            rects = [r for r in rects if r.row < 3 * H // 4]
+        pats.append(P.LossPattern(W, H, 16, 16, rects))
+    cfg = WL.C4.config("fp32")
+    monkeypatch.setenv("FOFSE_ROW_GROUPS", "1")
+    one, sq1, rep1 = P.conceal_frames(frames, pats, cfg)
+    monkeypatch.setenv("FOFSE_ROW_GROUPS", str(groups))
+    out, sq, rep = P.conceal_frames(frames, pats, cfg)
+    np.testing.assert_array_equal(one, out)
+    np.testing.assert_allclose(sq1, sq, rtol=1e-12)
+    assert rep.device["blocks"] == rep1.device["blocks"] == sum(len(p.blocks) for p in pats)
+
+
 def test_frames_api_batches_large_requests(gpu, monkeypatch):
     """A request above the device-memory budget runs as consecutive batches of
     whole frames (forced here with FOFSE_MAX_BATCH_BLOCKS): same bytes, same
