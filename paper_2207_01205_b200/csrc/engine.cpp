@@ -2158,10 +2158,18 @@ static void conceal_frames_batch(fofse_ctx* ctx, const uint8_t* frames, int32_t 
         const int64_t nunits = static_cast<int64_t>(n_frames) * height / unit_rows;
         std::vector<int64_t> gb(static_cast<size_t>(G) + 1, 0);  // row boundaries
         {
-            const int units = G <= 2 ? G : 4 * (G - 2) + 2;
+            // weights in eighths of a middle group (FOFSE_GROUP_EDGES=first,last)
+            int wf = 2, wl = 2;
+            if (const char* e = std::getenv("FOFSE_GROUP_EDGES"); e && std::sscanf(e, "%d,%d", &wf, &wl) == 2) {
+                wf = std::clamp(wf, 1, 8);
+                wl = std::clamp(wl, 1, 8);
+            }
+            if (G <= 2) wf = wl = 1;
+            const int wm = G <= 2 ? 1 : 8;
+            const int units = G == 1 ? 1 : wf + wl + wm * (G - 2);
             int u = 0;
             for (int gq = 0; gq < G; ++gq) {
-                u += (G <= 2 || gq == 0 || gq == G - 1) ? 1 : 4;
+                u += gq == 0 ? wf : gq == G - 1 ? wl : wm;
                 gb[static_cast<size_t>(gq) + 1] = (static_cast<int64_t>(u) * nunits + units - 1) / units * unit_rows;
             }
             gb[static_cast<size_t>(G)] = static_cast<int64_t>(n_frames) * height;
