@@ -72,7 +72,7 @@ typedef struct {
     int32_t record_traces; /* fill per-block IterationRecord traces */
     int32_t precision;     /* FOFSE_PREC_* */
     double guard_tau;      /* FP32 near-tie guard on |R|^2; < 0 = default, 0 = off */
-    int32_t fp64_head;     /* FP32 mode: first selections run in FP64; < 0 = default */
+    int32_t fp64_head;     /* FP32 mode: first selections run in FP64; < 0 = default (4) */
     int32_t pad0;
 } fofse_params;
 

@@ -736,10 +736,9 @@ bool f64_strict_forced() {
 // dominate the late-iteration residual).
 int resolve_head(const Cfg& c) {
     if (c.precision != FOFSE_PREC_FP32 || c.iterations <= 0) return 0;
-    // default: max(5, ceil(I/20)); at T = 128 a short head of 4 (C5 sweep over
-    // 1..15: 4 is +2.8 % with the same re-run count, the head dominating the
-    // front of the one big chunk)
-    const int h = c.head >= 0 ? c.head : c.T == 128 ? 4 : std::max(5, (c.iterations + 19) / 20);
+    // default: 4 selections (sweeps: C4 +2.2 % over the earlier max(5, ceil(I/20))
+    // = 10 with 1 % more re-runs; C5 +2.8 % over 15; C3 level)
+    const int h = c.head >= 0 ? c.head : 4;
     return std::min(h, c.iterations);
 }
 
