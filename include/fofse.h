@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define FOFSE_ABI_VERSION 2
+#define FOFSE_ABI_VERSION 3
 
 enum {
     FOFSE_OK = 0,
@@ -72,7 +72,7 @@ typedef struct {
     int32_t record_traces; /* fill per-block IterationRecord traces */
     int32_t precision;     /* FOFSE_PREC_* */
     double guard_tau;      /* FP32 near-tie guard on |R|^2; < 0 = default, 0 = off */
-    int32_t fp64_head;     /* FP32 mode: first selections run in FP64; < 0 = default (4) */
+    int32_t fp64_head;     /* FP32 mode: first selections run in FP64; < 0 = default */
     int32_t pad0;
 } fofse_params;
 
@@ -102,6 +102,8 @@ typedef struct {
     int64_t fp64_head;         /* FP32 mode: selections run in FP64 per block */
     int64_t real_blocks;       /* blocks on the rotated-frame real path (point-symmetric masks) */
     double real_iterate_ms;    /* FP32 mode: summed durations of the real-path iteration launches */
+    double k1_ms;              /* FP32 mode: summed durations of the real-path residual-spectrum
+                                  (K1: window gather + weighted forward FFT) launches */
 } fofse_report;
 
 typedef struct fofse_ctx fofse_ctx;
@@ -133,6 +135,18 @@ int fofse_conceal_shard_f64(fofse_ctx* ctx, const double* image, int32_t width, 
                             const fofse_rect* blocks, int64_t n_blocks, int64_t first,
                             int64_t count, int32_t block_height, int32_t block_width,
                             const fofse_params* params, double* restored, fofse_report* report);
+
+/* The same shard, with the concealed tiles packed for a gather instead of a
+ * whole image: tiles receives count*block_height*block_width f64 (shard block
+ * order), packed on the device. tiles_on_device != 0: tiles is a device
+ * pointer on the context's device (e.g. an NCCL send buffer); else host.
+ * This is the send side of the multi-GPU gather that replaces the reference's
+ * parallel_blocks workers (pipeline.cpp:136-162). */
+int fofse_conceal_shard_tiles_f64(fofse_ctx* ctx, const double* image, int32_t width, int32_t height,
+                                  const fofse_rect* blocks, int64_t n_blocks, int64_t first,
+                                  int64_t count, int32_t block_height, int32_t block_width,
+                                  const fofse_params* params, double* tiles, int32_t tiles_on_device,
+                                  fofse_report* report);
 
 /* Batched uint8 frames (the video workload): frames n_frames*height*width,
  * frame f owns blocks[frame_offsets[f] .. frame_offsets[f+1]). restored is
@@ -248,17 +262,6 @@ int fofse_diag_spectral_iterate(fofse_ctx* ctx, int32_t t, int64_t n, int32_t wi
                                 int32_t* nu, int32_t* converged, double gamma, int32_t iterations,
                                 int32_t precision, fofse_record* traces, int32_t* trace_counts,
                                 float* gap_trace);
-
-/* Synthetic inputs (host C++, deterministic, multi-threaded).
- * gen_image: sum of 3 low-frequency cosines (amp 40), 4 piecewise-constant
- * regions from 2 random half-plane edges (levels U[30,220]), one oriented
- * stripe texture (period U[4,16], amp 20), Gaussian noise sigma 2, rounded
- * and clipped to [0,255]. gen_losses: isolated block losses on a random
- * parity sublattice (no two lost cells 8-adjacent), round(frac*grid_w*grid_h)
- * of them, row-major order; returns the count or -1. */
-int fofse_gen_image_u8(uint64_t seed, int32_t width, int32_t height, uint8_t* out);
-int64_t fofse_gen_losses(uint64_t seed, int32_t grid_w, int32_t grid_h, double frac,
-                         int32_t block_h, int32_t block_w, fofse_rect* out, int64_t cap);
 
 #ifdef __cplusplus
 }

@@ -12,6 +12,10 @@ import os
 import numpy as np
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libfofse.so")
+# synthetic-input generator (include/fofse_gen.h): its own host-only library, so
+# generating a workload never maps the product library
+GEN_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libfofse_gen.so")
+GEN_EXPORTS = ["fofse_gen_image_u8", "fofse_gen_losses"]
 
 OK, EINVAL, ERUNTIME, ECUDA, EUNSUPPORTED = 0, 1, 2, 3, 4
 ALGO_FSE, ALGO_OFSE, ALGO_FOFSE = 0, 1, 2
@@ -24,10 +28,10 @@ EXPORTS = [
     "fofse_destroy", "fofse_set_stream", "fofse_conceal_f64", "fofse_conceal_frames_u8",
     "fofse_plan_frames_u8", "fofse_plan_execute_device", "fofse_plan_destroy",
     "fofse_extrapolate_windows", "fofse_spectral_init", "fofse_spectral_iterate",
-    "fofse_spectral_synthesize", "fofse_gen_image_u8", "fofse_gen_losses",
+    "fofse_spectral_synthesize",
     "fofse_validate_conceal", "fofse_plan_info", "fofse_plan_block_labels", "fofse_microbench",
     "fofse_diag_conceal_f64", "fofse_diag_spectral_iterate",
-    "fofse_conceal_shard_f64", "fofse_spectral_iterate_full_od", "fofse_psnr_curves",
+    "fofse_conceal_shard_f64", "fofse_conceal_shard_tiles_f64", "fofse_spectral_iterate_full_od", "fofse_psnr_curves",
 ]
 
 
@@ -59,7 +63,7 @@ class Report(C.Structure):
         ("guard_reruns", C.c_int64), ("converged_blocks", C.c_int64), ("init_ms", C.c_double),
         ("iterate_ms", C.c_double), ("total_ms", C.c_double), ("kernel_launches", C.c_int64),
         ("rerun_ms", C.c_double), ("fp64_head", C.c_int64), ("real_blocks", C.c_int64),
-        ("real_iterate_ms", C.c_double),
+        ("real_iterate_ms", C.c_double), ("k1_ms", C.c_double),
     ]
 
     def as_dict(self):
@@ -85,12 +89,26 @@ def lib():
             raise FofseCudaError(f"{LIB_PATH} is not built; run paper_2207_01205_b200.build.build()")
         L = C.CDLL(LIB_PATH)
         L.fofse_last_error.restype = C.c_char_p
-        L.fofse_gen_losses.restype = C.c_int64
         L.fofse_plan_destroy.restype = None
         L.fofse_destroy.restype = None
         L.fofse_params_default.restype = None
         _lib = L
     return _lib
+
+
+_gen = None
+
+
+def gen_lib():
+    """Load libfofse_gen.so (host-only synthetic inputs)."""
+    global _gen
+    if _gen is None:
+        if not os.path.exists(GEN_LIB_PATH):
+            raise FofseError(f"{GEN_LIB_PATH} is not built; run paper_2207_01205_b200.build.build()")
+        G = C.CDLL(GEN_LIB_PATH)
+        G.fofse_gen_losses.restype = C.c_int64
+        _gen = G
+    return _gen
 
 
 def check(rc: int):
@@ -171,17 +189,18 @@ def rects_array(blocks) -> np.ndarray:
 
 def gen_image_u8(seed: int, width: int, height: int) -> np.ndarray:
     out = np.empty((height, width), np.uint8)
-    check(lib().fofse_gen_image_u8(C.c_uint64(seed), width, height, ptr(out, C.c_uint8)))
+    if gen_lib().fofse_gen_image_u8(C.c_uint64(seed), width, height, ptr(out, C.c_uint8)) != OK:
+        raise ValueError("gen_image_u8: bad arguments")
     return out
 
 
 def gen_losses(seed: int, grid_w: int, grid_h: int, frac: float, block_h: int, block_w: int):
-    n = lib().fofse_gen_losses(C.c_uint64(seed), grid_w, grid_h, C.c_double(frac), block_h, block_w,
+    n = gen_lib().fofse_gen_losses(C.c_uint64(seed), grid_w, grid_h, C.c_double(frac), block_h, block_w,
                                None, 0)
     if n < 0:
         raise ValueError("gen_losses: bad arguments")
     out = np.zeros(n, RECT_DTYPE)
-    lib().fofse_gen_losses(C.c_uint64(seed), grid_w, grid_h, C.c_double(frac), block_h, block_w,
+    gen_lib().fofse_gen_losses(C.c_uint64(seed), grid_w, grid_h, C.c_double(frac), block_h, block_w,
                            out.ctypes.data_as(C.POINTER(Rect_)), n)
     return out
 

@@ -19,7 +19,7 @@ OBJ = os.path.join(PKG, "_build")
 LIB_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIB_DIR, "libfofse.so")
 
-SOURCES = ["kernels.cu", "kernels_v2.cu", "kernels_f64.cu", "kernels_k1.cu", "engine.cpp", "gen.cpp", "microbench.cu"]
+SOURCES = ["kernels.cu", "kernels_v2.cu", "kernels_f64.cu", "kernels_k1.cu", "engine.cpp", "microbench.cu"]
 HEADERS = ["kernels.h", "layout.h", "kcommon.cuh", "v2common.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "nvcc")
@@ -53,10 +53,25 @@ def build(verbose: bool = False) -> str:
     if _newer(LIB, objs):
         cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs, "-lpthread", "-ldl", "-lrt"]
         subprocess.run(cmd, check=True)
+    build_gen()
     build_cli()
     if verbose:
         print(LIB)
     return LIB
+
+
+GEN_SRC = os.path.join(CSRC, "gen.cpp")
+GEN_LIB = os.path.join(LIB_DIR, "libfofse_gen.so")
+
+
+def build_gen() -> str:
+    """Synthetic-input generator (csrc/gen.cpp), host-only, its own library."""
+    deps = [GEN_SRC, os.path.join(ROOT, "include", "fofse_gen.h"), os.path.join(ROOT, "include", "fofse.h")]
+    if _newer(GEN_LIB, deps):
+        cmd = [os.environ.get("CXX", "g++"), "-O2", "-std=c++17", "-fPIC", "-shared", "-Wall",
+               "-I" + os.path.join(ROOT, "include"), GEN_SRC, "-o", GEN_LIB, "-lpthread"]
+        subprocess.run(cmd, check=True)
+    return GEN_LIB
 
 
 CLI_SRC = os.path.join(PKG, "cli", "fofse_cli.cpp")

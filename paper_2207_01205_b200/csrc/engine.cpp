@@ -708,6 +708,7 @@ struct RunOut {
     double init_ms = 0, iter_ms = 0, total_ms = 0, rerun_ms = 0;
     double chunk_pre_ms = 0, chunk_iter_ms = 0, rerun_tail_ms = 0;  // fp32 pipeline
     double real_iter_ms = 0;                                         // fp32 real-path launches
+    double k1_ms = 0;                                                // fp32 real-path K1 launches
     int64_t real_blocks = 0;
     int64_t reruns = 0, converged = 0, head = 0, resumed = 0;
 };
@@ -736,9 +737,12 @@ bool f64_strict_forced() {
 // dominate the late-iteration residual).
 int resolve_head(const Cfg& c) {
     if (c.precision != FOFSE_PREC_FP32 || c.iterations <= 0) return 0;
-    // default: 4 selections (sweeps: C4 +2.2 % over the earlier max(5, ceil(I/20))
-    // = 10 with 1 % more re-runs; C5 +2.8 % over 15; C3 level)
-    const int h = c.head >= 0 ? c.head : 4;
+    // default: 8 selections for T <= 64, 16 for T = 128 — the shortest heads with
+    // which the guard (tau = 1e-5) catches every selection that leaves the fp64
+    // sequence (tools/divergence_study.py: head 4 misses 3 of 229 divergent C4
+    // blocks, head 8 none of 204; C5 head 8 misses 1 of 255, head 16 none of 233)
+    // and no block of the full-scale studies ends above 0.5 px
+    const int h = c.head >= 0 ? c.head : (c.T > 64 ? 16 : 8);
     return std::min(h, c.iterations);
 }
 
@@ -1379,7 +1383,9 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         std::vector<char> waited(static_cast<size_t>(2 * ngroups), 0);  // [group][main/side] upload waits
         for (const Chunk& ch : chunks)
             if (ch.f64_direct && !d_R64) d_R64 = ctx->buf("R64").as<char>(static_cast<size_t>(n) * r64_bytes);
-        // per chunk: events [3i] after K1, [3i+1] before the fp32 iteration, [3i+2] done
+        // per chunk: events [3i] before K1, [3i+1] before the fp32 iteration, [3i+2] done;
+        // [ev_k1 + i] after K1 (the K1 share of the chunk's preparation)
+        const size_t ev_k1 = 5 * chunks.size();
         for (size_t ci = 0; ci < chunks.size(); ++ci) {
             const Chunk& ch = chunks[ci];
             const int64_t cn = ch.b1 - ch.b0;
@@ -1408,6 +1414,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             if (head > 0) {
                 k1_packed(d_sorted + ch.b0, cn, hi_path(ch.path), seg64, 1,
                           d_R64 + static_cast<size_t>(ch.b0) * r64_bytes, d_e0 + ch.b0, d_imax + ch.b0, 0, 0, ps);
+                ck(cudaEventRecord(ctx->event(ev_k1 + ci), ps), "event");
                 K2Args a = base_args();
                 a.rin = d_R64;
                 a.rec_global = 1;
@@ -1451,6 +1458,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
                 k1_packed(d_sorted + ch.b0, cn, ch.path, seg32, spt_of(ch.path),
                           d_R32 + static_cast<size_t>(ch.b0) * sizeof(float) * s32, d_e0 + ch.b0, d_imax + ch.b0,
                           soa_of(ch.path), s32, ps);
+                ck(cudaEventRecord(ctx->event(ev_k1 + ci), ps), "event");
             }
             ck(cudaEventRecord(ctx->event(3 * ci + 1), ps), "event");
             if (ps != ch.s) ck(cudaStreamWaitEvent(ch.s, ctx->event(3 * ci + 1), 0), "wait");
@@ -1653,6 +1661,10 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             ck(cudaEventElapsedTime(&ms, ctx->event(3 * ci + 1), ctx->event(3 * ci + 2)), "elapsed");
             out.chunk_iter_ms += ms;
             if (chunks[ci].path == PATH_F32_REAL) out.real_iter_ms += ms;
+            if (chunks[ci].path == PATH_F32_REAL && !chunks[ci].f64_direct) {
+                ck(cudaEventElapsedTime(&ms, ctx->event(3 * ci + 0), ctx->event(ev_k1 + ci)), "elapsed");
+                out.k1_ms += ms;
+            }
         }
         if (hp_.on) {  // chunk timeline (FOFSE_HOST_PROF): start / iterate / done vs the job start
             for (size_t ci = 0; ci < chunks.size(); ++ci) {
@@ -1706,6 +1718,7 @@ void fill_report(fofse_report* rep, const RunOut& ro, int64_t n, int64_t ncls, d
     rep->fp64_head = ro.head;
     rep->real_blocks = ro.real_blocks;
     rep->real_iterate_ms = ro.real_iter_ms;
+    rep->k1_ms = ro.k1_ms;
     rep->mean_seconds_per_block = n ? ro.total_ms * 1e-3 / static_cast<double>(n) : 0.0;
     rep->kernel_launches = launches;
     // pipeline.cpp:252-260 + grid.cpp:117-120
@@ -1867,8 +1880,9 @@ int fofse_set_stream(fofse_ctx* ctx, void* s) {
 static void conceal_f64_impl(fofse_ctx* ctx, const double* image, int32_t width, int32_t height,
                              const fofse_rect* blocks, int64_t n_all, int64_t first, int64_t count,
                              int32_t bh, int32_t bw, const fofse_params* params, double* restored,
-                             fofse_record* traces, int32_t* trace_counts, fofse_report* report) {
-        if (!ctx || !image || !restored || (n_all && !blocks))
+                             fofse_record* traces, int32_t* trace_counts, fofse_report* report,
+                             double* tiles = nullptr, bool tiles_on_device = false) {
+        if (!ctx || !image || !(restored || tiles) || (n_all && !blocks))
             throw std::invalid_argument("conceal: NULL argument");
         if (width < 1 || height < 1) throw std::invalid_argument("grid dimensions must be >= 1");
         if (first < 0 || count < 0 || first + count > n_all)
@@ -1896,7 +1910,23 @@ static void conceal_f64_impl(fofse_ctx* ctx, const double* image, int32_t width,
         if (n > 0) ro = run_job(ctx, job, cfg, fr, fofse::SYN_IMAGE, d_sq, nullptr, d_tr, d_tc);
         std::vector<double> sq(static_cast<size_t>(n));
         if (n) ck(cudaMemcpyAsync(sq.data(), d_sq, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream), "D2H sq");
-        ck(cudaMemcpyAsync(restored, d_img, npx * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H image");
+        if (restored)
+            ck(cudaMemcpyAsync(restored, d_img, npx * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H image");
+        if (tiles && n > 0) {
+            // the shard's tiles packed on the device (block order of the shard)
+            std::vector<int4> rc(static_cast<size_t>(n));
+            for (int64_t i = 0; i < n; ++i) {
+                const fofse_rect& r = blocks[first + i];
+                rc[static_cast<size_t>(i)] = make_int4(r.row, r.col, r.height, r.width);
+            }
+            const int4* d_rc = upload(ctx, "tile_rects", rc.data(), rc.size());
+            const size_t tb = static_cast<size_t>(n) * bh * bw;
+            double* d_out = tiles_on_device ? tiles : ctx->buf("tiles").as<double>(tb);
+            ck(fofse::pack_tiles_launch(d_img, width, d_rc, n, bh, bw, d_out, ctx->stream), "pack tiles");
+            ++ctx->launches;
+            if (!tiles_on_device)
+                ck(cudaMemcpyAsync(tiles, d_out, tb * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H tiles");
+        }
         if (d_tr) {
             ck(cudaMemcpyAsync(traces, d_tr, sizeof(fofse_record) * n * cfg.iterations, cudaMemcpyDeviceToHost, ctx->stream), "D2H trace");
             if (trace_counts)
@@ -1975,6 +2005,17 @@ int fofse_conceal_shard_f64(fofse_ctx* ctx, const double* image, int32_t width, 
     return guarded([&] {
         conceal_f64_impl(ctx, image, width, height, blocks, n_blocks, first, count, bh, bw, params,
                          restored, nullptr, nullptr, report);
+    });
+}
+
+int fofse_conceal_shard_tiles_f64(fofse_ctx* ctx, const double* image, int32_t width, int32_t height,
+                                  const fofse_rect* blocks, int64_t n_blocks, int64_t first, int64_t count,
+                                  int32_t bh, int32_t bw, const fofse_params* params, double* tiles,
+                                  int32_t tiles_on_device, fofse_report* report) {
+    return guarded([&] {
+        if (!tiles && count > 0) throw std::invalid_argument("conceal: NULL argument");
+        conceal_f64_impl(ctx, image, width, height, blocks, n_blocks, first, count, bh, bw, params, nullptr,
+                         nullptr, nullptr, report, tiles, tiles_on_device != 0);
     });
 }
 
@@ -2343,6 +2384,7 @@ int fofse_conceal_frames_u8(fofse_ctx* ctx, const uint8_t* frames, int32_t n_fra
             agg.fp64_head = r.fp64_head;
             agg.real_blocks += r.real_blocks;
             agg.real_iterate_ms += r.real_iterate_ms;
+            agg.k1_ms += r.k1_ms;
             f0 = f1;
         }
         for (int64_t i = 0; i < n_all; ++i) sq_total += sq_out[i];

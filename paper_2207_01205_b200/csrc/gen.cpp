@@ -21,7 +21,7 @@
 #include <thread>
 #include <vector>
 
-#include "../../include/fofse.h"
+#include "../../include/fofse_gen.h"
 
 namespace {
 

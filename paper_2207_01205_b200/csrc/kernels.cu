@@ -1131,6 +1131,26 @@ static int fft2d_t(double2* data, int64_t n, int dir, const double2* tw, cudaStr
     return cudaGetLastError();
 }
 
+// Packs the concealed B x B tiles of n blocks out of an f64 image into
+// tiles[n][bh][bw] (the multi-GPU gather's send buffer): one CTA per block,
+// coalesced along rows.
+__global__ void pack_tiles_kernel(const double* __restrict__ img, int64_t width, const int4* __restrict__ rects,
+                                  int32_t bh, int32_t bw, double* __restrict__ out) {
+    const int4 r = rects[blockIdx.x];  // (row, col, height, width)
+    double* o = out + (size_t)blockIdx.x * bh * bw;
+    for (int i = threadIdx.x; i < bh * bw; i += blockDim.x) {
+        const int y = i / bw, x = i - y * bw;
+        o[i] = img[(size_t)(r.x + y) * width + r.y + x];
+    }
+}
+
+int pack_tiles_launch(const double* img, int64_t width, const int4* rects, int64_t n, int32_t bh, int32_t bw,
+                      double* out, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    pack_tiles_kernel<<<(unsigned)n, 128, 0, s>>>(img, width, rects, bh, bw, out);
+    return cudaGetLastError();
+}
+
 int fft2d_launch(double2* data, int64_t n, int32_t T, int32_t dir, const double2* tw, cudaStream_t s) {
     switch (T) {
         case 8: return fft2d_t<8>(data, n, dir, tw, s);

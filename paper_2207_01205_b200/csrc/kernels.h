@@ -168,6 +168,10 @@ int k2_launch(const K2Args& a, int32_t ntiles, cudaStream_t s);
 int fft2d_launch(double2* data, int64_t n, int32_t T, int32_t dir, const double2* twid_fwd,
                  cudaStream_t s);
 
+// tiles[n][bh][bw] <- the B x B regions rects[i] = (row, col, h, w) of an f64 image.
+int pack_tiles_launch(const double* img, int64_t width, const int4* rects, int64_t n, int32_t bh, int32_t bw,
+                      double* out, cudaStream_t s);
+
 // K2v2: single-warp fp32 iteration kernel (T <= 64); convert fp64 head state.
 int k2v2_launch(const K2Args& a, int32_t ntiles, cudaStream_t s);
 // K2d: fp64 rotated-frame iteration (PATH_F64_REAL), groups of d_group_threads(T).

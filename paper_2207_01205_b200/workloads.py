@@ -48,14 +48,15 @@ class Workload:
                            for r in rects])
         return img, pat
 
-    def batch(self, seed: int, frames: int | None = None):
-        """Frames (F, H, W) u8, rects (structured), frame offsets (F+1,)."""
+    def batch(self, seed: int, frames: int | None = None, first: int = 0, out: np.ndarray | None = None):
+        """Frames first .. first+F-1 of the batch: (F, H, W) u8 (written into `out`
+        when given), rects (structured), frame offsets (F+1,)."""
         nf = self.frames if frames is None else frames
-        imgs = np.empty((nf, self.height, self.width), np.uint8)
+        imgs = np.empty((nf, self.height, self.width), np.uint8) if out is None else out
         rects, offs = [], [0]
         for f in range(nf):
-            imgs[f] = capi.gen_image_u8(seed + f, self.width, self.height)
-            r = capi.gen_losses(seed + f, self.width // self.block, self.height // self.block,
+            imgs[f] = capi.gen_image_u8(seed + first + f, self.width, self.height)
+            r = capi.gen_losses(seed + first + f, self.width // self.block, self.height // self.block,
                                 self.loss_frac, self.block, self.block)
             rects.append(r)
             offs.append(offs[-1] + len(r))

@@ -41,7 +41,7 @@ def test_reference_arm_line():
 def test_our_arm_line(gpu):
     d = run_bench("--workload", "C2", "--steps", "3", "--warmup", "3", "--no-cpu-baseline")
     assert BASE_KEYS <= set(d) and "impl" not in d
-    assert d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] == 3 and d["scaling"] == "weak"
+    assert d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] == 3 and d["scaling"] == "strong"
     assert d["value"] > 0 and d["ms_per_step"] > 0 and d["dtype"] == "f32" and d["vs_baseline"] is None
     e = d["e2e"]
     assert e["value"] > 0 and e["unit"] == d["unit"] and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0

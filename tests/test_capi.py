@@ -22,7 +22,19 @@ def test_library_exports_every_declared_symbol(lib):
     assert declared == set(capi.EXPORTS)
     for name in declared:
         assert hasattr(lib, name), name
-    assert lib.fofse_abi_version() == 2
+    assert lib.fofse_abi_version() == 3
+
+
+def test_generator_library_is_separate(lib):
+    """The synthetic-input generator lives in libfofse_gen.so (include/fofse_gen.h),
+    so generating a workload (the reference arm of bench.py) never maps libfofse.so."""
+    header = open(os.path.join(ROOT, "include", "fofse_gen.h")).read()
+    declared = set(re.findall(r"\b(fofse_[a-z0-9_]+)\s*\(", header))
+    assert declared == set(capi.GEN_EXPORTS)
+    g = capi.gen_lib()
+    for name in declared:
+        assert hasattr(g, name), name
+        assert not hasattr(lib, name), name
 
 
 def test_params_default_match_conceal_config(lib):
@@ -36,7 +48,7 @@ def test_params_default_match_conceal_config(lib):
 def test_struct_layouts_match_header(lib):
     assert C.sizeof(capi.Params) == 64
     assert capi.RECORD_DTYPE.itemsize == 72
-    assert C.sizeof(capi.Report) == 120
+    assert C.sizeof(capi.Report) == 128
 
 
 def test_generators_deterministic(lib):

@@ -466,6 +466,31 @@ def test_conceal_fp32_vs_fp64_full_C2(gpu):
     assert abs(o32.report.psnr_db - o64.report.psnr_db) <= FP32_PSNR_TOL
 
 
+def test_fp32_default_on_c4_frames_vs_fp64(gpu):
+    """The shipped fp32 default (fp64 head, guard tau) on 48 whole C4 frames
+    (39,168 blocks) against the fp64 path: no block above 0.5 px, |dPSNR| of the
+    concealed blocks <= 0.05 dB (north_star fp32 bar; bench.py reports the same
+    check over all 256 frames of the timed batch)."""
+    import dataclasses
+
+    from paper_2207_01205_b200 import parity
+    r = parity.fp32_vs_fp64(dataclasses.replace(WL.C4, frames=48), seed=4242)
+    assert r["blocks"] == 48 * 816
+    assert r["blocks_over_0.5"] == 0 and r["max_px"] <= FP32_PX_TOL, r
+    assert r["dpsnr_db"] <= FP32_PSNR_TOL and r["max_frame_dpsnr_db"] <= FP32_PSNR_TOL, r
+
+
+def test_fp32_default_on_c5_vs_fp64(gpu):
+    """T = 128 (C5, 3,277 blocks of one 8192^2 image, 300 iterations) at the shipped
+    fp32 default against the fp64 path."""
+    import dataclasses
+
+    from paper_2207_01205_b200 import parity
+    r = parity.fp32_vs_fp64(dataclasses.replace(WL.C5, frames=2), seed=777)
+    assert r["blocks_over_0.5"] == 0 and r["max_px"] <= FP32_PX_TOL, r
+    assert r["dpsnr_db"] <= FP32_PSNR_TOL, r
+
+
 def test_extrapolate_windows_vs_oracle(gpu, orc):
     """Window level (pipeline.cpp:181-203) with arbitrary per-window masks."""
     rng = np.random.default_rng(99)
