@@ -152,3 +152,57 @@ def test_extrapolate_writes_model_and_trace(cli, gpu, tmp_path):
     assert len(rows) == 25
     assert [int(x[1]) for x in rows] == list(runs[0].trace["u1"])
     assert r.stdout.startswith("iterations=25 converged=false ")
+
+
+# ---- JSON config (main.cpp:66-110,274-293): flags beat the file, the file beats defaults ----
+def test_dump_config_defaults_and_flag_precedence(cli, tmp_path):
+    import json
+    r = run(cli, "conceal", "--input", "in.pgm", "--dump-config", "-")
+    assert r.returncode == 0, r.stderr
+    d = json.loads(r.stdout)
+    assert d == {"algorithm": "fofse", "block": 16, "count_limit": 81, "fft_size": 64, "gamma": 0.2,
+                 "input": "in.pgm", "iterations": 200, "out_dir": "", "pattern": "", "rho_hat": 0.8, "seed": 0,
+                 "spacing": 48, "stride": 5, "support": 16, "threads": 1}
+    assert list(d) == sorted(d) and r.stdout.startswith('{\n  "algorithm": "fofse",\n')
+    cfg = tmp_path / "c.json"
+    cfg.write_text('{"gamma": 0.5, "iterations": 50, "pattern": "p.txt", "seed": 7, "rho_hat": 1e-1}')
+    out = tmp_path / "eff.json"
+    r = run(cli, "conceal", "--input", "in.pgm", "--config", cfg, "--iterations", "80", "--dump-config", out)
+    assert r.returncode == 0, r.stderr
+    d = json.loads(out.read_text())
+    assert (d["gamma"], d["iterations"], d["pattern"], d["seed"], d["rho_hat"]) == (0.5, 80, "p.txt", 7, 0.1)
+
+
+def test_config_file_errors(cli, tmp_path):
+    bad = tmp_path / "bad.json"
+    bad.write_text('{"gamma": 0.5, "colour": 3}')
+    r = run(cli, "conceal", "--input", "in.pgm", "--config", bad)
+    assert r.returncode == 1 and "unknown key 'colour'" in r.stderr
+    bad.write_text('{"gamma": 0.5,,}')
+    r = run(cli, "conceal", "--input", "in.pgm", "--config", bad)
+    assert r.returncode == 1 and "invalid JSON" in r.stderr
+    bad.write_text('[1, 2]')
+    r = run(cli, "conceal", "--input", "in.pgm", "--config", bad)
+    assert r.returncode == 1 and "config must be a JSON object" in r.stderr
+    r = run(cli, "conceal", "--input", "in.pgm", "--config", tmp_path / "nope.json")
+    assert r.returncode == 2 and "cannot open config file" in r.stderr
+
+
+def test_pattern_file_parsing_and_validation(cli, tmp_path):
+    """pattern.cpp:55-96: comments and blank lines skipped, short lines rejected with
+    the line number, bounds / overlap checked in load order (before any device work)."""
+    img = tmp_path / "img.pgm"
+    write_pgm(img, np.full((64, 64), 90.0))
+    pat = tmp_path / "p.txt"
+    pat.write_text("# lost blocks\n\n0 0 16 16\n16 16 16\n")
+    r = run(cli, "conceal", "--input", img, "--pattern", pat, "--out-dir", tmp_path / "o")
+    assert r.returncode == 2 and f"{pat}:4: expected 'row col height width'" in r.stderr
+    pat.write_text("0 0 16 16  # first\n8 8 16 16\n")
+    r = run(cli, "conceal", "--input", img, "--pattern", pat, "--out-dir", tmp_path / "o")
+    assert r.returncode == 1 and "pattern: blocks 0 and 1 overlap" in r.stderr
+    pat.write_text("0 0 16 16\n56 56 16 16\n")
+    r = run(cli, "conceal", "--input", img, "--pattern", pat, "--out-dir", tmp_path / "o")
+    assert r.returncode == 1 and "pattern: block 1 exceeds image bounds" in r.stderr
+    pat.write_text("0 0 16 16\n32 32 8 8\n")
+    r = run(cli, "conceal", "--input", img, "--pattern", pat, "--out-dir", tmp_path / "o")
+    assert r.returncode == 1 and "pattern: blocks must share one size" in r.stderr
