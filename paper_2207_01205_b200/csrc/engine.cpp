@@ -752,6 +752,18 @@ double effective_tau(const Cfg& c, int head) {
     return head > 0 ? 1e-5 : 5e-5;
 }
 
+// fp64 mode's near-tie guard: a block whose two largest canonical
+// |R|^2 come within tau (relative) re-runs on the exact path (K1x + the strict
+// kernel with the hypot argmax), bit-identical to the reference, so the selected-
+// basis sequence does not depend on K1's / K2d's last-bit rounding. guard_tau in
+// fp64 mode overrides the default 1e-9 (0 = off, 1 = every block on the exact path).
+// OFSE keeps the fast kernels only (its block-wide d-reduction has no
+// reference-order form).
+double fp64_tie_tau(const Cfg& c) {
+    if (c.precision != FOFSE_PREC_FP64 || c.algorithm == FOFSE_ALGO_OFSE) return 0.0;
+    return c.tau >= 0.0 ? c.tau : 1e-9;
+}
+
 // Frame-group I/O hooks of the pipelined frames API: group g's first kernel
 // waits for h2d_done[g]; once all of group g's work (iteration, re-runs) is
 // enqueued, on_done(g, s) enqueues its download on stream s after it.
@@ -1069,7 +1081,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
     // lists in one copy up front)
     auto k2_f64 = [&](K2Args a, int hp, int64_t b0, int64_t b1, const std::vector<BlockDesc>& descs,
                       const std::string& tag, cudaStream_t s, const Tile* pre = nullptr, size_t npre = 0,
-                      bool wide = false) {
+                      bool wide = false, double tau = 0.0) {
         const bool fast = hp == PATH_F64_REAL || hp == PATH_F64_CPLX;
         a.d_wide = (wide && hp == PATH_F64_REAL) ? 1 : 0;
         std::vector<Tile> tl;
@@ -1081,7 +1093,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         }
         a.path = hp;
         a.seg = seg64;
-        a.tau = 0.0;
+        a.tau = tau;  // > 0 only for the fp64 mode's near-tie guard
         a.tiles = d_tl;
         a.wimg = hp == PATH_F64_REAL ? (const void*)d_vimg64 : (const void*)d_wimg64;
         a.wimg_stride = hp == PATH_F64_REAL ? static_cast<int64_t>(vimg64_elems) : static_cast<int64_t>(T) * sr64;
@@ -1108,12 +1120,75 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         a.rin = d_R64;
         a.rec_global = 0;
         if (!ckpts) {
+            const double tau64 = fp64_tie_tau(cfg);
+            int32_t* d_tie = tau64 > 0.0 ? ctx->buf("tie").as<int32_t>(static_cast<size_t>(n)) : nullptr;
+            if (d_tie) ck(cudaMemsetAsync(d_tie, 0, sizeof(int32_t) * n, st), "memset");
             for (size_t i = 0; i < ranges.size(); ++i) {
                 const bool w = range_wide(ranges[i]);
                 K2Args ar = a;
                 if (w) ar.rin = d_R64w;
+                ar.flags = d_tie;
                 k2_f64(ar, hi_path(ranges[i].path), ranges[i].begin, ranges[i].end, sorted, std::to_string(i), st,
-                       nullptr, 0, w);
+                       nullptr, 0, w, tau64);
+            }
+            if (d_tie) {
+                // ---- near-tie blocks: the exact path (K1x + strict kernel, hypot argmax) ----
+                std::vector<int32_t> tie(static_cast<size_t>(n));
+                ck(cudaMemcpyAsync(tie.data(), d_tie, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st), "D2H tie");
+                ck(cudaStreamSynchronize(st), "sync");
+                std::vector<BlockDesc> xd;
+                std::vector<int32_t> xid;
+                std::vector<Tile> xt;
+                for (int64_t q = 0; q < n; ++q)
+                    if (tie[static_cast<size_t>(q)]) {
+                        xt.push_back(Tile{static_cast<int32_t>(xd.size()), static_cast<int32_t>(xd.size()), 1, 0});
+                        xd.push_back(sorted[static_cast<size_t>(q)]);
+                        xid.push_back(ids[static_cast<size_t>(q)]);
+                    }
+                const int64_t m = static_cast<int64_t>(xd.size());
+                if (m > 0) {
+                    const size_t tt = static_cast<size_t>(T) * T;
+                    BlockDesc* d_xd = upload(ctx, "x_desc", xd.data(), xd.size());
+                    int32_t* d_xid = upload(ctx, "x_ids", xid.data(), xid.size());
+                    Tile* d_xt = upload(ctx, "x_tiles", xt.data(), xt.size());
+                    K1xArgs k{};
+                    k.T = T;
+                    k.Lh = g.Lh;
+                    k.Lw = g.Lw;
+                    k.n = static_cast<int32_t>(m);
+                    k.seg = seg64;
+                    k.blocks = d_xd;
+                    k.fr = fr;
+                    k.wcls = d_wcls;
+                    k.twid = d_twf;
+                    k.scratch = ctx->buf("x_scr").as<double2>(static_cast<size_t>(m) * 2 * tt);
+                    k.rpacked = ctx->buf("x_R").as<double2>(static_cast<size_t>(m) * L64.SLOTS);
+                    k.wimg = ctx->buf("x_W").as<double2>(static_cast<size_t>(m) * T * sr64);
+                    k.w0 = ctx->buf("x_w0").as<double>(static_cast<size_t>(m));
+                    k.energy = ctx->buf("x_e0").as<double>(static_cast<size_t>(m));
+                    k.init_max = ctx->buf("x_imax").as<double>(static_cast<size_t>(m));
+                    ck(k1x_launch(k, st), "K1x exact init");
+                    ++ctx->launches;
+                    K2Args x = base_args();
+                    x.path = PATH_F64_STRICT;
+                    x.seg = seg64;
+                    x.tau = 0.0;
+                    x.exact_peak = 1;
+                    x.tiles = d_xt;
+                    x.order = d_xid;
+                    x.blocks = d_xd;
+                    x.rin = k.rpacked;
+                    x.wimg = k.wimg;
+                    x.wimg_stride = static_cast<int64_t>(T) * sr64;
+                    x.w0 = k.w0;
+                    x.energy0 = k.energy;
+                    x.init_energy = k.energy;
+                    x.init_max = k.init_max;
+                    x.rec_global = 0;
+                    ck(k2_launch(x, static_cast<int32_t>(m), st), "K2 strict exact re-runs");
+                    ++ctx->launches;
+                    out.reruns += m;
+                }
             }
         } else {
             // checkpointed curves (pipeline.cpp:264-369): resumable phases up to each
@@ -2473,46 +2548,41 @@ int fofse_spectral_init(fofse_ctx* ctx, const double* f, const uint8_t* labels,
         for (size_t q = 0; q < fm.size(); ++q) fm[q] = labels[q] == FOFSE_SUPPORT ? f[q] : 0.0;
         std::vector<BlockDesc> bd(static_cast<size_t>(n));
         for (int64_t i = 0; i < n; ++i) bd[static_cast<size_t>(i)] = BlockDesc{static_cast<int32_t>(i), 0, 0, static_cast<int32_t>(i)};
-        const auto twf = twiddles(t, -1);
+        const auto twf = twiddles(t, -1);  // the FFT stand-in's table (oracle/fft_radix2.h)
         double2* d_tw = upload(ctx, "twf", twf.data(), twf.size());
         double* d_f = upload(ctx, "si_f", fm.data(), fm.size());
         double* d_wg = upload(ctx, "si_wg", wg.data(), wg.size());
         BlockDesc* d_bd = upload(ctx, "si_bd", bd.data(), bd.size());
         const size_t tt = static_cast<size_t>(t) * t;
-        double2* d_rw = ctx->buf("si_rw").as<double2>(std::max<size_t>(static_cast<size_t>(n) * tt, 1));
-        double2* d_ws = ctx->buf("si_ws").as<double2>(std::max<size_t>(static_cast<size_t>(n) * tt, 1));
-        double* d_e = ctx->buf("si_e").as<double>(static_cast<size_t>(std::max<int64_t>(n, 1)));
-        double* d_m = ctx->buf("si_m").as<double>(static_cast<size_t>(std::max<int64_t>(n, 1)));
-        double* d_e2 = ctx->buf("si_e2").as<double>(static_cast<size_t>(std::max<int64_t>(n, 1)));
-        double* d_m2 = ctx->buf("si_m2").as<double>(static_cast<size_t>(std::max<int64_t>(n, 1)));
-        K1Args a{};
-        a.T = t;
-        a.Lh = h;
-        a.Lw = w;
-        a.n = static_cast<int32_t>(n);
-        a.blocks = d_bd;
-        a.fr = Frames{d_f, nullptr, SRC_F64, w, h, static_cast<int64_t>(L)};
-        a.wcls = d_wg;
-        a.mode = K1_FULL;
-        a.out = d_rw;
-        a.energy = d_e;
-        a.init_max = d_m;
-        a.twid = d_tw;
-        ck(k1_launch(a, ctx->stream), "K1 init rw");
-        // W = DFT(w): same kernel with f == 1 on every sample of w
-        std::vector<double> ones(static_cast<size_t>(n) * L, 1.0);
-        double* d_one = upload(ctx, "si_one", ones.data(), ones.size());
-        a.fr.src = d_one;
-        a.out = d_ws;
-        a.energy = d_e2;
-        a.init_max = d_m2;
-        ck(k1_launch(a, ctx->stream), "K1 init W");
-        ck(cudaMemcpyAsync(rw, d_rw, sizeof(double2) * n * tt, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
-        ck(cudaMemcpyAsync(wspec, d_ws, sizeof(double2) * n * tt, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
-        ck(cudaMemcpyAsync(energy, d_e, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
-        ck(cudaMemcpyAsync(imax, d_m, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        const size_t nn = static_cast<size_t>(std::max<int64_t>(n, 1));
+        // K1x: init_spectra in the reference's operation order — the spectra, energy
+        // and initial_max are bit-identical to the reference's (with the stand-in FFT)
+        K1xArgs k{};
+        k.T = t;
+        k.Lh = h;
+        k.Lw = w;
+        k.n = static_cast<int32_t>(n);
+        k.seg = seg_of(t, PATH_F64_STRICT);
+        k.blocks = d_bd;
+        k.fr = Frames{d_f, nullptr, SRC_F64, w, h, static_cast<int64_t>(L)};
+        k.wcls = d_wg;
+        k.twid = d_tw;
+        k.scratch = ctx->buf("si_scr").as<double2>(nn * 2 * tt);
+        k.w0 = ctx->buf("si_w0").as<double>(nn);
+        k.energy = ctx->buf("si_e").as<double>(nn);
+        k.init_max = ctx->buf("si_m").as<double>(nn);
+        ck(k1x_launch(k, ctx->stream), "K1x init");
+        for (int64_t i = 0; i < n; ++i) {
+            const double2* src = k.scratch + static_cast<size_t>(i) * 2 * tt;
+            ck(cudaMemcpyAsync(rw + 2 * static_cast<size_t>(i) * tt, src, sizeof(double2) * tt, cudaMemcpyDeviceToHost,
+                               ctx->stream), "D2H");
+            ck(cudaMemcpyAsync(wspec + 2 * static_cast<size_t>(i) * tt, src + tt, sizeof(double2) * tt,
+                               cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        }
+        ck(cudaMemcpyAsync(energy, k.energy, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        ck(cudaMemcpyAsync(imax, k.init_max, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        ck(cudaMemcpyAsync(w0, k.w0, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
         ck(cudaStreamSynchronize(ctx->stream), "sync");
-        for (int64_t i = 0; i < n; ++i) w0[i] = wspec[2 * static_cast<size_t>(i) * tt];
     });
 }
 
@@ -2620,6 +2690,7 @@ static int spectral_iterate_impl(fofse_ctx* ctx, int32_t t, int64_t n, int32_t w
         double2* d_twi = upload(ctx, "twi", twi.data(), twi.size());
         K2Args a{};
         a.full_od = fod;
+        a.exact_peak = path == PATH_F64_STRICT ? 1 : 0;  // find_peak's hypot compare
         a.T = t;
         a.Lh = wh;
         a.Lw = ww;

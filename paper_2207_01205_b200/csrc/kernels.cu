@@ -369,6 +369,11 @@ __global__ void __launch_bounds__(K2Cfg<T, PATH>::THREADS) k2_kernel(K2Args a) {
     const float sgn_r = ((a.Lh - 1) & 1) ? -1.f : 1.f;
     const float sgn_c = ((a.Lw - 1) & 1) ? -1.f : 1.f;
     const double w0 = a.w0[tile.cls];
+    // exact find_peak (engine_spectral.cpp:20-33): compare |R| as the host's
+    // std::abs computes it (hypot_ref), so equal or near-equal magnitudes resolve
+    // exactly as in the reference; the runner-up is kept for the fp64 near-tie guard
+    const bool exact = !F32 && a.exact_peak;
+    const bool track2 = F32 || a.tau > 0.0;
 
     for (int bi = gid; bi < tile.count; bi += Cf::NG) {
         // inputs are indexed by position (tile order), outputs by block id
@@ -418,17 +423,21 @@ __global__ void __launch_bounds__(K2Cfg<T, PATH>::THREADS) k2_kernel(K2Args a) {
             // ---- local argmax over owned canonical bins (strict '>' in index order) ----
             Real m1 = Real(-1), m2 = Real(-1);
             int j1 = 0;
+            auto magof = [&](Real x, Real y) -> Real {
+                if constexpr (F32) return mag2(x, y);
+                return exact ? hypot_ref(x, y) : mag2(x, y);
+            };
 #pragma unroll
             for (int j = 0; j < SEG; ++j) {
-                const Real m = mag2(re[j], im[j]);
-                if constexpr (F32) m2 = fmaxf(m2, fminf(m, m1));
+                const Real m = magof(re[j], im[j]);
+                if (track2) m2 = fmax(m2, fmin(m, m1));
                 const bool gt = m > m1;
                 m1 = gt ? m : m1;
                 j1 = gt ? j : j1;
             }
             if (ex) {
-                const Real m = mag2(re[SEG], im[SEG]);
-                if constexpr (F32) m2 = fmaxf(m2, fminf(m, m1));
+                const Real m = magof(re[SEG], im[SEG]);
+                if (track2) m2 = fmax(m2, fmin(m, m1));
                 if (m > m1) {
                     m1 = m;
                     j1 = SEG;
@@ -447,9 +456,9 @@ __global__ void __launch_bounds__(K2Cfg<T, PATH>::THREADS) k2_kernel(K2Args a) {
                 const Real om = __shfl_xor_sync(0xffffffffu, wm, o);
                 const int og = __shfl_xor_sync(0xffffffffu, wg, o);
                 const bool take = om > wm || (om == wm && og < wg);
-                if constexpr (F32) {
+                if (track2) {
                     const Real om2 = __shfl_xor_sync(0xffffffffu, wm2, o);
-                    wm2 = fmaxf(fmaxf(wm2, om2), take ? wm : om);
+                    wm2 = fmax(fmax(wm2, om2), take ? wm : om);
                 }
                 wm = take ? om : wm;
                 wg = take ? og : wg;
@@ -463,7 +472,7 @@ __global__ void __launch_bounds__(K2Cfg<T, PATH>::THREADS) k2_kernel(K2Args a) {
                 }
                 Slot s;
                 s.m1 = wm;
-                s.m2 = F32 ? (double)wm2 : -1.0;
+                s.m2 = track2 ? (double)wm2 : -1.0;
                 s.pre_re = pr;
                 s.pre_im = pi;
                 s.g = wg;
@@ -509,14 +518,15 @@ __global__ void __launch_bounds__(K2Cfg<T, PATH>::THREADS) k2_kernel(K2Args a) {
                 p.need_d = 0;
                 p.u1 = p.u2 = 0;
                 p.c_re = p.c_im = 0.0;
-                const double mag = sqrt(M);
+                const double mag = exact ? M : sqrt(M);  // exact: M is |R| itself
                 // engine_spectral.cpp:60-65 early stop
                 if (e_init <= 0.0 || energy < 1e-12 * e_init || !(M > 0.0) || mag < 1e-12 * imax) {
                     p.stop = 1;
                     conv = 1;
-                } else if (F32 && a.tau > 0.0 && M2 > M * (1.0 - a.tau)) {
-                    // near-tie: fp32 cannot certify the reference's selection; abort,
-                    // the host re-runs this block in fp64.
+                } else if (track2 && a.tau > 0.0 && M2 > M * (1.0 - a.tau)) {
+                    // near-tie: fp32 cannot certify the reference's selection (fp64:
+                    // K1's spectra are not the reference's bits); abort, the host
+                    // re-runs this block in fp64 (fp64 mode: on the exact path).
                     p.stop = 1;
                     flagged = 1;
                 } else {

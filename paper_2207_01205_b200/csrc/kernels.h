@@ -143,7 +143,35 @@ struct K2Args {
     int32_t real_gw;            // K2v2 real path at T = 64: warps per lost block (1: K2v2r, 2: K2v2h)
     int32_t d_wide;             // K2d: WIDE form (T <= 64; guard re-runs)
     const int32_t* ntiles_dev;  // K2d: optional tile count on the device (grid = an upper bound)
+    // fp64 mode: tau > 0 on an fp64 kernel is the near-tie guard (top-2 |R|^2 within
+    // tau relative -> flags[pos] = 1 + nu, no write-back; the block re-runs on the exact
+    // path). exact_peak: the strict kernel's argmax compares hypot_ref(|R|) like find_peak.
+    int32_t exact_peak;
 };
+
+// Exact init (the fp64 mode's tie re-runs): init_spectra (engine_spectral.cpp:
+// 148-183) with the reference's operation order — w f products and the energy
+// sum in row-major order, the radix-2 row / column FFT of the FFT stand-in
+// (oracle/fft_radix2.h order; twiddles from the host's libm), initial_max over
+// all T^2 bins with hypot_ref — so the spectra are bit-identical to the
+// reference's. Outputs: the canonical half in the strict kernel's packed layout,
+// the block's own W image ([T][T+SEG+1], SEG of the strict path), w0, energy,
+// initial_max; one CTA of T threads per block, scratch 2 T^2 complex per block.
+struct K1xArgs {
+    int32_t T, Lh, Lw, n;
+    int32_t seg;                // SEG of the strict path (packed layout, W image stride)
+    const BlockDesc* blocks;    // window origin + the class whose weights apply
+    Frames fr;
+    const double* wcls;         // [ncls][Lh*Lw]
+    const double2* twid;        // e^{-j 2 pi k / T}, k < T, host libm (the stand-in's table)
+    double2* scratch;           // [n][2][T*T]
+    double2* rpacked;           // [n][SLOTS] (strict layout)
+    double2* wimg;              // [n][T*(T+SEG+1)]
+    double* w0;                 // [n]
+    double* energy;             // [n]
+    double* init_max;           // [n]
+};
+int k1x_launch(const K1xArgs& a, cudaStream_t s);
 
 struct CvtArgs {
     int32_t T, Lh, Lw, n;

@@ -78,10 +78,59 @@ constexpr unsigned long long DKEY_MASK = 0xFFFFFFFFFFFFF000ull;
 constexpr int DKEY_TOP = 4095;
 
 template <unsigned long long MASK = DKEY_MASK>
-__device__ __forceinline__ void dscan(unsigned long long& K, double re, double im, unsigned kidx) {
+__device__ __forceinline__ unsigned long long dkey(double re, double im, unsigned kidx) {
     const double m = fma(im, im, re * re);
-    const unsigned long long key = (static_cast<unsigned long long>(__double_as_longlong(m)) & MASK) | kidx;
+    return (static_cast<unsigned long long>(__double_as_longlong(m)) & MASK) | kidx;
+}
+// TIE (the fp64 mode's near-tie guard): S2 tracks the high word of the
+// runner-up of the chain — the smaller of (new key, old best) on every bin.
+template <unsigned long long MASK = DKEY_MASK, bool TIE = false>
+__device__ __forceinline__ void dscan(unsigned long long& K, unsigned& S2, double re, double im, unsigned kidx) {
+    const unsigned long long key = dkey<MASK>(re, im, kidx);
+    if constexpr (TIE) S2 = max(S2, min(static_cast<unsigned>(key >> 32), static_cast<unsigned>(K >> 32)));
     K = key > K ? key : K;
+}
+
+// The exact runner-up key of a thread: the largest key of its bins other than
+// the group winner's (second stage of the near-tie guard, run only when the
+// high words of the two largest keys are within one step).
+template <int NB, unsigned long long MASK>
+__device__ __forceinline__ unsigned long long dsecond(const double (&re)[NB], const double (&im)[NB], bool active,
+                                                      int ex, unsigned kbase, unsigned long long Mk) {
+    unsigned long long S = 0;
+    if (!active) return S;
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+        if (j == NB - 1 && !ex) break;
+        const unsigned long long k = dkey<MASK>(re[j], im[j], kbase - j);
+        S = (k != Mk && k > S) ? k : S;
+    }
+    return S;
+}
+
+// Near-tie guard of the fp64 kernels (fp64 mode): true when the
+// runner-up is within tau of the maximum (relative, on |R|^2). s2hi is the group
+// runner-up's high word; the exact check (second pass over the bins, one extra
+// group barrier) runs only when it is within one step of the maximum's high word.
+template <int NB, int NW, int GT, unsigned long long MASK>
+__device__ __forceinline__ bool dtie(const K2Args& a, const double (&re)[NB], const double (&im)[NB], bool active,
+                                     int ex, unsigned kbase, unsigned Mhi, unsigned Mlo, unsigned s2hi,
+                                     unsigned long long* scratch, int w, int lane, int bar) {
+    if (s2hi + 1u < Mhi) return false;
+    const unsigned long long Mk = (static_cast<unsigned long long>(Mhi) << 32) | Mlo;
+    unsigned long long S = dsecond<NB, MASK>(re, im, active, ex, kbase, Mk);
+    const unsigned shi = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(S >> 32));
+    const unsigned slo = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(S >> 32) == shi ? static_cast<unsigned>(S) : 0u);
+    S = (static_cast<unsigned long long>(shi) << 32) | slo;
+    if constexpr (NW > 1) {
+        if (lane == 0) scratch[w] = S;
+        named_bar_sync(bar, GT);
+#pragma unroll
+        for (int k = 0; k < NW; ++k) S = scratch[k] > S ? scratch[k] : S;
+    }
+    const double Mv = __longlong_as_double(static_cast<long long>(Mk & MASK));
+    const double Sv = __longlong_as_double(static_cast<long long>(S & MASK));
+    return Sv >= Mv * (1.0 - a.tau);
 }
 
 // R'[j] of the winner lane by a (lane-local) jump on j.
@@ -294,7 +343,7 @@ __device__ __forceinline__ void d_replay(const K2Args& a, const double* vE, cons
     }
 }
 
-template <int T, bool FOD, bool REPLAY = false, bool WIDE = false>
+template <int T, bool FOD, bool REPLAY = false, bool WIDE = false, bool TIE = false>
 __global__ void __launch_bounds__(DCfg<T, WIDE>::THREADS, DCfg<T, WIDE>::MINB) k2d_kernel(K2Args a) {
     using Cf = DCfg<T, WIDE>;
     constexpr int SEG = Cf::SEG, NT = Cf::NT, GT = Cf::GT, NW = Cf::NW, PPS = Cf::PPS, SRV = Cf::SRV;
@@ -372,9 +421,11 @@ __global__ void __launch_bounds__(DCfg<T, WIDE>::THREADS, DCfg<T, WIDE>::MINB) k
         int ntrace = a.trace_from_nu0 ? nu : 0;
 
         unsigned long long KA = 0, KB = 0;  // two independent max chains
+        unsigned S2 = 0;                    // TIE: runner-up high word
+        int flagged = 0;
 #pragma unroll
-        for (int j = 0; j < SEG; ++j) dscan<KM>((j & 1) ? KB : KA, re[j], im[j], kbase - j);
-        if (ex) dscan<KM>(KA, re[SEG], im[SEG], kbase - SEG);
+        for (int j = 0; j < SEG; ++j) dscan<KM, TIE>((j & 1) ? KB : KA, S2, re[j], im[j], kbase - j);
+        if (ex) dscan<KM, TIE>(KA, S2, re[SEG], im[SEG], kbase - SEG);
 
         const int nu_end = a.nu_limit > 0 ? a.nu_limit : nu + a.iterations;  // per-block resume points
         for (int it = 0; nu < nu_end && !conv; ++it) {
@@ -385,10 +436,16 @@ __global__ void __launch_bounds__(DCfg<T, WIDE>::THREADS, DCfg<T, WIDE>::MINB) k
             const unsigned hi = static_cast<unsigned>(K >> 32), lo = static_cast<unsigned>(K);
             const unsigned Mhi = __reduce_max_sync(0xffffffffu, hi);
             const unsigned Mlo = __reduce_max_sync(0xffffffffu, hi == Mhi ? lo : 0u);
-            if (hi == Mhi && lo == Mlo) {
+            const bool win = hi == Mhi && lo == Mlo;
+            unsigned ws2 = 0;  // TIE: the warp's runner-up high word
+            if constexpr (TIE) {
+                const unsigned t2 = active ? max(S2, min(static_cast<unsigned>(KA >> 32), static_cast<unsigned>(KB >> 32))) : 0u;
+                ws2 = __reduce_max_sync(0xffffffffu, win ? t2 : hi);
+            }
+            if (win) {
                 const int g = KTOP - static_cast<int>(Mlo & Cf::KTOP);
                 const double2 pre = dpick<NB>(g - gbase, re, im);
-                slots[par * NW + w] = DSlot{Mhi, Mlo, g, 0, pre.x, pre.y};
+                slots[par * NW + w] = DSlot{Mhi, Mlo, g, static_cast<int>(ws2), pre.x, pre.y};
             }
             if constexpr (NW == 1)
                 __syncwarp();
@@ -414,6 +471,17 @@ __global__ void __launch_bounds__(DCfg<T, WIDE>::THREADS, DCfg<T, WIDE>::MINB) k
             if (energy < thr_e || !(M > 0.0) || M < thr_m) {
                 conv = 1;
                 break;
+            }
+            if constexpr (TIE) {
+                unsigned s2 = static_cast<unsigned>(s.pad);  // the winner warp's own runner-up
+#pragma unroll
+                for (int k = 0; k < NW; ++k)
+                    if (k != wb) s2 = max(s2, slots[par * NW + k].hi);
+                if (dtie<NB, NW, GT, KM>(a, re, im, active, ex, kbase, s.hi, s.lo, s2,
+                                         reinterpret_cast<unsigned long long*>(dred + par * NW), w, ltid & 31, bar)) {
+                    flagged = 1 + nu;  // near-tie: the block re-runs on the exact path
+                    break;
+                }
             }
             const int G = s.g;
             const int u1 = G / T, u2 = G % T;
@@ -519,6 +587,7 @@ __global__ void __launch_bounds__(DCfg<T, WIDE>::THREADS, DCfg<T, WIDE>::MINB) k
             const double n2r = -s2 * a_re, n2i = s2 * a_im;
             KA = 0;
             KB = 0;
+            S2 = 0;
             if (self) {
 #pragma unroll
                 for (int q = 0; q < PPS; ++q) {
@@ -527,8 +596,8 @@ __global__ void __launch_bounds__(DCfg<T, WIDE>::THREADS, DCfg<T, WIDE>::MINB) k
                     im[2 * q] = fma(n1i, x.x, im[2 * q]);
                     re[2 * q + 1] = fma(n1r, x.y, re[2 * q + 1]);
                     im[2 * q + 1] = fma(n1i, x.y, im[2 * q + 1]);
-                    dscan<KM>(KA, re[2 * q], im[2 * q], kbase - 2 * q);
-                    dscan<KM>(KB, re[2 * q + 1], im[2 * q + 1], kbase - 2 * q - 1);
+                    dscan<KM, TIE>(KA, S2, re[2 * q], im[2 * q], kbase - 2 * q);
+                    dscan<KM, TIE>(KB, S2, re[2 * q + 1], im[2 * q + 1], kbase - 2 * q - 1);
                 }
             } else {
 #pragma unroll
@@ -538,8 +607,8 @@ __global__ void __launch_bounds__(DCfg<T, WIDE>::THREADS, DCfg<T, WIDE>::MINB) k
                     im[2 * q] = fma(n2i, y.x, fma(n1i, x.x, im[2 * q]));
                     re[2 * q + 1] = fma(n2r, y.y, fma(n1r, x.y, re[2 * q + 1]));
                     im[2 * q + 1] = fma(n2i, y.y, fma(n1i, x.y, im[2 * q + 1]));
-                    dscan<KM>(KA, re[2 * q], im[2 * q], kbase - 2 * q);
-                    dscan<KM>(KB, re[2 * q + 1], im[2 * q + 1], kbase - 2 * q - 1);
+                    dscan<KM, TIE>(KA, S2, re[2 * q], im[2 * q], kbase - 2 * q);
+                    dscan<KM, TIE>(KB, S2, re[2 * q + 1], im[2 * q + 1], kbase - 2 * q - 1);
                 }
             }
             if (ex) {
@@ -551,7 +620,7 @@ __global__ void __launch_bounds__(DCfg<T, WIDE>::THREADS, DCfg<T, WIDE>::MINB) k
                     re[SEG] = fma(n2r, y, re[SEG]);
                     im[SEG] = fma(n2i, y, im[SEG]);
                 }
-                dscan<KM>(KA, re[SEG], im[SEG], kbase - SEG);
+                dscan<KM, TIE>(KA, S2, re[SEG], im[SEG], kbase - SEG);
             }
         }
 
@@ -589,7 +658,7 @@ __global__ void __launch_bounds__(DCfg<T, WIDE>::THREADS, DCfg<T, WIDE>::MINB) k
             __syncwarp();
         else
             named_bar_sync(bar, GT);
-        v2_finish<T, GT, double2>(a, a.blocks[pos], pos, b, ltid, energy, nu, conv, 0, ntrace, rec_u, rec_c,
+        v2_finish<T, GT, double2>(a, a.blocks[pos], pos, b, ltid, energy, nu, conv, flagged, ntrace, rec_u, rec_c,
                                   rstride, twi, red, bar);
         if constexpr (NW == 1)
             __syncwarp();
@@ -632,7 +701,7 @@ struct DCCfg {
     static_assert(T * T <= 4096, "key index bits");
 };
 
-template <int T, bool FOD>
+template <int T, bool FOD, bool TIE = false>
 __global__ void __launch_bounds__(256, 2) k2dc_kernel(K2Args a) {
     using Cf = DCCfg<T>;
     constexpr int SEG = Cf::SEG, NT = Cf::NT, GT = Cf::GT, NW = Cf::NW, SR = Cf::SR;
@@ -690,9 +759,11 @@ __global__ void __launch_bounds__(256, 2) k2dc_kernel(K2Args a) {
         int conv = (a.conv0 ? a.conv0[pos] : 0) | (e_init <= 0.0);
 
         unsigned long long KA = 0, KB = 0;
+        unsigned S2 = 0;  // TIE: runner-up high word
+        int flagged = 0;
 #pragma unroll
-        for (int j = 0; j < SEG; ++j) dscan((j & 1) ? KB : KA, re[j], im[j], kbase - j);
-        if (ex) dscan(KA, re[SEG], im[SEG], kbase - SEG);
+        for (int j = 0; j < SEG; ++j) dscan<DKEY_MASK, TIE>((j & 1) ? KB : KA, S2, re[j], im[j], kbase - j);
+        if (ex) dscan<DKEY_MASK, TIE>(KA, S2, re[SEG], im[SEG], kbase - SEG);
 
         const int nu_end = a.nu_limit > 0 ? a.nu_limit : nu + a.iterations;  // per-block resume points
         for (int it = 0; nu < nu_end && !conv; ++it) {
@@ -702,26 +773,48 @@ __global__ void __launch_bounds__(256, 2) k2dc_kernel(K2Args a) {
             const unsigned hi = static_cast<unsigned>(K >> 32), lo = static_cast<unsigned>(K);
             const unsigned Mhi = __reduce_max_sync(0xffffffffu, hi);
             const unsigned Mlo = __reduce_max_sync(0xffffffffu, hi == Mhi ? lo : 0u);
-            if (hi == Mhi && lo == Mlo) {
+            const bool win = hi == Mhi && lo == Mlo;
+            unsigned ws2 = 0;  // TIE: the warp's runner-up high word
+            if constexpr (TIE) {
+                const unsigned t2 = active ? max(S2, min(static_cast<unsigned>(KA >> 32), static_cast<unsigned>(KB >> 32))) : 0u;
+                ws2 = __reduce_max_sync(0xffffffffu, win ? t2 : hi);
+            }
+            if (win) {
                 const int g = DKEY_TOP - static_cast<int>(Mlo & 0xFFFu);
                 const double2 pre = dpick<NB>(g - gbase, re, im);
-                slots[par * NW + w] = DSlot{Mhi, Mlo, g, 0, pre.x, pre.y};
+                slots[par * NW + w] = DSlot{Mhi, Mlo, g, static_cast<int>(ws2), pre.x, pre.y};
             }
             if constexpr (NW == 1)
                 __syncwarp();
             else
                 named_bar_sync(bar, GT);
             DSlot s = slots[par * NW];
+            int wwin = 0;
 #pragma unroll
             for (int k = 1; k < NW; ++k) {
                 const DSlot o = slots[par * NW + k];
-                if (o.hi > s.hi || (o.hi == s.hi && o.lo > s.lo)) s = o;
+                if (o.hi > s.hi || (o.hi == s.hi && o.lo > s.lo)) {
+                    s = o;
+                    wwin = k;
+                }
             }
             const double pr = s.pre_re, pi = s.pre_im;
             const double M = fma(pi, pi, pr * pr);
             if (energy < thr_e || !(M > 0.0) || M < thr_m) {
                 conv = 1;
                 break;
+            }
+            if constexpr (TIE) {
+                unsigned s2 = static_cast<unsigned>(s.pad);
+#pragma unroll
+                for (int k = 0; k < NW; ++k)
+                    if (k != wwin) s2 = max(s2, slots[par * NW + k].hi);
+                if (dtie<NB, NW, GT, DKEY_MASK>(a, re, im, active, ex, kbase, s.hi, s.lo, s2,
+                                                reinterpret_cast<unsigned long long*>(dred + par * NW), w, ltid & 31,
+                                                bar)) {
+                    flagged = 1 + nu;
+                    break;
+                }
             }
             const int G = s.g;
             const int u1 = G / T, u2 = G % T;
@@ -795,6 +888,7 @@ __global__ void __launch_bounds__(256, 2) k2dc_kernel(K2Args a) {
             // ---- R[k] -= c W[k-u] + conj(c) W[k+u] (engine_spectral.cpp:112-125), next scan ----
             KA = 0;
             KB = 0;
+            S2 = 0;
 #pragma unroll
             for (int j = 0; j < NB; ++j) {
                 if (j == SEG && !ex) break;
@@ -809,9 +903,9 @@ __global__ void __launch_bounds__(256, 2) k2dc_kernel(K2Args a) {
                 re[j] = r;
                 im[j] = m;
                 if (j < SEG)
-                    dscan((j & 1) ? KB : KA, r, m, kbase - j);
+                    dscan<DKEY_MASK, TIE>((j & 1) ? KB : KA, S2, r, m, kbase - j);
                 else
-                    dscan(KA, r, m, kbase - SEG);
+                    dscan<DKEY_MASK, TIE>(KA, S2, r, m, kbase - SEG);
             }
         }
 
@@ -825,7 +919,7 @@ __global__ void __launch_bounds__(256, 2) k2dc_kernel(K2Args a) {
             __syncwarp();
         else
             named_bar_sync(bar, GT);
-        v2_finish<T, GT, double2>(a, a.blocks[pos], pos, b, ltid, energy, nu, conv, 0, ntrace, rec_u, rec_c,
+        v2_finish<T, GT, double2>(a, a.blocks[pos], pos, b, ltid, energy, nu, conv, flagged, ntrace, rec_u, rec_c,
                                   rstride, twi, red, bar);
         if constexpr (NW == 1)
             __syncwarp();
@@ -837,7 +931,7 @@ __global__ void __launch_bounds__(256, 2) k2dc_kernel(K2Args a) {
 template <int T>
 static int k2dc_t(const K2Args& a, int32_t ntiles, cudaStream_t s) {
     using Cf = DCCfg<T>;
-    auto* fn = a.full_od ? k2dc_kernel<T, true> : k2dc_kernel<T, false>;
+    auto* fn = a.full_od ? k2dc_kernel<T, true> : a.tau > 0.0 ? k2dc_kernel<T, false, true> : k2dc_kernel<T, false>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
     if (e != cudaSuccess) return e;
     if (ntiles <= 0) return cudaSuccess;
@@ -849,8 +943,10 @@ template <int T, bool WIDE>
 static int k2d_tw(const K2Args& a, int32_t ntiles, cudaStream_t s) {
     using Cf = DCfg<T, WIDE>;
     const bool replay = a.src_pos != nullptr;
-    auto* fn = replay ? k2d_kernel<T, false, true, WIDE>
-                      : a.full_od ? k2d_kernel<T, true, false, WIDE> : k2d_kernel<T, false, false, WIDE>;
+    auto* fn = replay      ? k2d_kernel<T, false, true, WIDE>
+               : a.full_od ? k2d_kernel<T, true, false, WIDE>
+               : a.tau > 0.0 ? k2d_kernel<T, false, false, WIDE, true>  // fp64 mode: near-tie guard
+                             : k2d_kernel<T, false, false, WIDE>;
     const int rstride = a.rec_stride > 0 ? a.rec_stride : a.iterations;
     const size_t smem = replay ? ((Cf::SMEM + 31) & ~size_t(31)) +
                                      (sizeof(RSel) + sizeof(double2)) * (size_t)Cf::GROUPS * rstride
