@@ -55,6 +55,7 @@ def build(verbose: bool = False) -> str:
         subprocess.run(cmd, check=True)
     build_gen()
     build_cli()
+    build_adapter()
     if verbose:
         print(LIB)
     return LIB
@@ -72,6 +73,27 @@ def build_gen() -> str:
                "-I" + os.path.join(ROOT, "include"), GEN_SRC, "-o", GEN_LIB, "-lpthread"]
         subprocess.run(cmd, check=True)
     return GEN_LIB
+
+
+REF_INCLUDE = os.environ.get("FOFSE_REF_INCLUDE", "/root/reference/proj/include")
+ADAPTER_SRC = os.path.join(PKG, "adapter", "fse_b200.cpp")
+ADAPTER_LIB = os.path.join(LIB_DIR, "libfse_b200.so")
+
+
+def build_adapter() -> str | None:
+    """The link-level drop-in (adapter/fse_b200.cpp -> _lib/libfse_b200.so): the
+    reference's hot-path symbols over its own types, compiled against the
+    reference's public headers. Built where those headers exist (this
+    container); elsewhere the prebuilt library is used as is."""
+    if not os.path.isdir(os.path.join(REF_INCLUDE, "fse")):
+        return ADAPTER_LIB if os.path.exists(ADAPTER_LIB) else None
+    deps = [ADAPTER_SRC, LIB, os.path.join(ROOT, "include", "fofse.h")]
+    if _newer(ADAPTER_LIB, deps):
+        cmd = [os.environ.get("CXX", "g++"), "-O2", "-std=c++20", "-fPIC", "-shared", "-Wall", "-Wextra",
+               "-I" + os.path.join(ROOT, "include"), "-I" + REF_INCLUDE, ADAPTER_SRC, "-o", ADAPTER_LIB,
+               "-L" + LIB_DIR, "-lfofse", "-Wl,-rpath,$ORIGIN", "-Wl,--no-undefined"]
+        subprocess.run(cmd, check=True)
+    return ADAPTER_LIB
 
 
 CLI_SRC = os.path.join(PKG, "cli", "fofse_cli.cpp")

@@ -116,7 +116,8 @@ template <int NB, int NW, int GT, unsigned long long MASK>
 __device__ __forceinline__ bool dtie(const K2Args& a, const double (&re)[NB], const double (&im)[NB], bool active,
                                      int ex, unsigned kbase, unsigned Mhi, unsigned Mlo, unsigned s2hi,
                                      unsigned long long* scratch, int w, int lane, int bar) {
-    if (s2hi + 1u < Mhi) return false;
+    // two or more high-word steps apart = a gap of at least 2^-20 relative (> tau up to 5e-7)
+    if (a.tau < 5e-7 && s2hi + 1u < Mhi) return false;
     const unsigned long long Mk = (static_cast<unsigned long long>(Mhi) << 32) | Mlo;
     unsigned long long S = dsecond<NB, MASK>(re, im, active, ex, kbase, Mk);
     const unsigned shi = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(S >> 32));
