@@ -152,12 +152,21 @@ int fofse_conceal_shard_tiles_f64(fofse_ctx* ctx, const double* image, int32_t w
  * frame f owns blocks[frame_offsets[f] .. frame_offsets[f+1]). restored is
  * written like the reference's write_pgm (std::round + clamp,
  * src/image_io.cpp:73-77); it may alias frames. block_sq (optional, n_blocks)
- * receives each block's squared error vs the input over its MISSING samples. */
+ * receives each block's squared error vs the input over its MISSING samples.
+ * frames / restored should be page-locked (fofse_host_register, or memory from
+ * cudaHostAlloc): the call pipelines each frame group's upload and download
+ * with the other groups' kernels, and copies to or from pageable memory are
+ * synchronous — correct, but without that overlap. */
 int fofse_conceal_frames_u8(fofse_ctx* ctx, const uint8_t* frames, int32_t n_frames,
                             int32_t width, int32_t height, const fofse_rect* blocks,
                             const int64_t* frame_offsets, int32_t block_height,
                             int32_t block_width, const fofse_params* params, uint8_t* restored,
                             double* block_sq, fofse_report* report);
+
+/* Page-lock (cudaHostRegister) / release a caller buffer for the frames API's
+ * overlapped transfers, for callers without the CUDA runtime (FFI / ctypes). */
+int fofse_host_register(void* ptr, size_t bytes);
+int fofse_host_unregister(void* ptr);
 
 /* Plan/execute split of fofse_conceal_frames_u8 for inputs already resident
  * in device memory: plan = validation, window classes, tiles, device

@@ -203,6 +203,8 @@ inline ConcealOutput conceal(const SampleGrid& image, const LossPattern& pattern
                                                        {f.c_re, f.c_im}, f.gamma_effective,
                                                        f.weighted_energy, f.degenerate != 0});
         }
+        // the reference sets Trace::converged on an early stop (engine_spectral.cpp:60-64)
+        br.trace.converged = tc[static_cast<size_t>(i)] < config.iterations;
     }
     return out;
 }

@@ -31,7 +31,7 @@ EXPORTS = [
     "fofse_spectral_synthesize",
     "fofse_validate_conceal", "fofse_plan_info", "fofse_plan_block_labels", "fofse_microbench",
     "fofse_diag_conceal_f64", "fofse_diag_spectral_iterate",
-    "fofse_conceal_shard_f64", "fofse_conceal_shard_tiles_f64", "fofse_spectral_iterate_full_od", "fofse_psnr_curves",
+    "fofse_conceal_shard_f64", "fofse_conceal_shard_tiles_f64", "fofse_host_register", "fofse_host_unregister", "fofse_spectral_iterate_full_od", "fofse_psnr_curves",
 ]
 
 

@@ -2083,6 +2083,19 @@ int fofse_conceal_shard_f64(fofse_ctx* ctx, const double* image, int32_t width, 
     });
 }
 
+int fofse_host_register(void* ptr, size_t bytes) {
+    return guarded([&] {
+        if (!ptr && bytes) throw std::invalid_argument("host_register: NULL pointer");
+        if (bytes) ck(cudaHostRegister(ptr, bytes, cudaHostRegisterDefault), "cudaHostRegister");
+    });
+}
+
+int fofse_host_unregister(void* ptr) {
+    return guarded([&] {
+        if (ptr) ck(cudaHostUnregister(ptr), "cudaHostUnregister");
+    });
+}
+
 int fofse_conceal_shard_tiles_f64(fofse_ctx* ctx, const double* image, int32_t width, int32_t height,
                                   const fofse_rect* blocks, int64_t n_blocks, int64_t first, int64_t count,
                                   int32_t bh, int32_t bw, const fofse_params* params, double* tiles,

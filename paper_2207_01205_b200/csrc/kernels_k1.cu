@@ -185,8 +185,11 @@ __global__ void __launch_bounds__(K1fCfg<FT>::THREADS, FT == 64 ? 3 : 8) k1f_ker
             const bool inf = in && n >= c_lo && n < c_hi;
             wa[m] = in ? wra[n] : 0.0;
             wb[m] = (in && hasb) ? wrb[n] : 0.0;
-            fa[m] = (inf && pa) ? static_cast<double>(pa[n]) : 0.0;
-            fb[m] = (inf && pb) ? static_cast<double>(pb[n]) : 0.0;
+            // samples with w = 0 (MISSING / OUTSIDE) are never read as values, like the
+            // reference's `if (wv == 0.0) continue` (init_spectra:165): a NaN or Inf in a
+            // lost block cannot reach the spectrum through 0 * NaN
+            fa[m] = (inf && pa && wa[m] != 0.0) ? static_cast<double>(pa[n]) : 0.0;
+            fb[m] = (inf && pb && wb[m] != 0.0) ? static_cast<double>(pb[n]) : 0.0;
         }
 #pragma unroll
         for (int m = 0; m < 8; ++m) {
@@ -393,8 +396,8 @@ __global__ void __launch_bounds__(WGR * WLG, 1) k1w_kernel(K1Args a) {
             const bool in = n < a.Lw;
             const bool inf = in && n >= c_lo && n < c_hi;
             const double wa = in ? wra[n] : 0.0, wb = (in && hasb) ? wrb[n] : 0.0;
-            const double fa = (inf && pa) ? static_cast<double>(pa[n]) : 0.0;
-            const double fb = (inf && pb) ? static_cast<double>(pb[n]) : 0.0;
+            const double fa = (inf && pa && wa != 0.0) ? static_cast<double>(pa[n]) : 0.0;  // w = 0: not read
+            const double fb = (inf && pb && wb != 0.0) ? static_cast<double>(pb[n]) : 0.0;
             const double va = wa * fa, vb = wb * fb;
             energy += va * fa;
             energy += vb * fb;
