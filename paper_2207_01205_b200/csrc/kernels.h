@@ -129,6 +129,7 @@ struct K2Args {
     int32_t trace_from_nu0;     // trace index continues from nu0 (multi-phase calls)
     int32_t trace_stride;       // trace records per block (0 = iterations)
     int32_t state_by_pos;       // energy_out / nu_out / conv_out indexed by position
+    float tau1f;                // (float)(1 - tau), precomputed (K2v2: one constant load per selection)
     uint32_t kmask;             // K2v2 packed-key mantissa mask (0xffffffc0), a runtime value so
                                 // the key is one LOP3 (mask in a register, index immediate)
     int32_t full_od;            // OFSE: full orthogonality-deficiency compensation (engine_spectral.cpp:79-97)
