@@ -50,6 +50,10 @@ enum { FOFSE_ALGO_FSE = 0, FOFSE_ALGO_OFSE = 1, FOFSE_ALGO_FOFSE = 2 };
  * FP64). */
 enum { FOFSE_PREC_FP64 = 0, FOFSE_PREC_FP32 = 1 };
 
+/* fse::BasisKind (include/fse/basis.hpp:17). DCT runs the spatial engine
+ * (engine_spatial.cpp:254-381) in fp64 with the reference's operation order. */
+enum { FOFSE_BASIS_DFT = 0, FOFSE_BASIS_DCT = 1 };
+
 /* Region labels, fse::Region order (include/fse/grid.hpp:26-30). */
 enum { FOFSE_SUPPORT = 0, FOFSE_MISSING = 1, FOFSE_OUTSIDE = 2 };
 
@@ -73,7 +77,7 @@ typedef struct {
     int32_t precision;     /* FOFSE_PREC_* */
     double guard_tau;      /* FP32 near-tie guard on |R|^2; < 0 = default, 0 = off */
     int32_t fp64_head;     /* FP32 mode: first selections run in FP64; < 0 = default */
-    int32_t pad0;
+    int32_t basis;         /* FOFSE_BASIS_* (ConcealConfig::basis, pipeline.hpp:28) */
 } fofse_params;
 
 /* fse::IterationRecord (include/fse/trace.hpp:13-21), 72 bytes. */

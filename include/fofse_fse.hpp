@@ -50,6 +50,7 @@ struct LossPattern {
 
 enum class Algorithm { fse = FOFSE_ALGO_FSE, ofse = FOFSE_ALGO_OFSE, fofse = FOFSE_ALGO_FOFSE };
 enum class Precision { fp64 = FOFSE_PREC_FP64, fp32 = FOFSE_PREC_FP32 };
+enum class BasisKind { dft2d = FOFSE_BASIS_DFT, dct2d = FOFSE_BASIS_DCT };  // basis.hpp:17
 
 struct ConcealConfig {
     Algorithm algorithm = Algorithm::fofse;
@@ -63,6 +64,7 @@ struct ConcealConfig {
     Precision precision = Precision::fp64;  // fp64 reproduces the reference selections
     double guard_tau = -1.0;
     int fp64_head = -1;
+    BasisKind basis = BasisKind::dft2d;
 
     fofse_params params() const {
         fofse_params p;
@@ -78,6 +80,7 @@ struct ConcealConfig {
         p.precision = static_cast<int32_t>(precision);
         p.guard_tau = guard_tau;
         p.fp64_head = fp64_head;
+        p.basis = static_cast<int32_t>(basis);
         return p;
     }
 };

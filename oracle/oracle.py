@@ -184,7 +184,7 @@ class _Lib:
         return self._iterate("fast_iterate_full_od", s, iterations)
 
     def conceal(self, image, blocks, block_h, block_w, *, algorithm=ALGO_FOFSE, gamma=0.2,
-                iterations=200, t=64, rho_hat=0.8, support=16, threads=1, traces=False):
+                iterations=200, t=64, rho_hat=0.8, support=16, threads=1, traces=False, basis=0):
         image = np.ascontiguousarray(image, np.float64)
         h, w = image.shape
         rects = (OrRect * max(len(blocks), 1))(*[OrRect(*map(int, b)) for b in blocks])
@@ -194,7 +194,12 @@ class _Lib:
         counts = np.zeros(n, np.int32)
         db, ident = C.c_double(0), C.c_int(0)
         extra = self._conceal_extra()
-        rc = self._fn("conceal")(
+        fn = "conceal"
+        if basis:  # DCT (spatial engine): the compiled reference only
+            if not isinstance(self, Reference):
+                raise OracleError("the DCT basis is pinned on the compiled reference (oracle/_ref) only")
+            fn, extra = "conceal_basis", extra + (int(basis),)
+        rc = self._fn(fn)(
             _dp(image), w, h, rects, n, block_h, block_w, algorithm, C.c_double(gamma),
             iterations, t, C.c_double(rho_hat), support, threads, _dp(restored),
             recs.ctypes.data_as(C.POINTER(OrRecord)) if traces else None,

@@ -248,11 +248,28 @@ int ref_extract_windows(const double* image, int img_w, int img_h, const or_rect
 }
 
 // fse::conceal through its public API (pipeline.hpp:83-84).
+int ref_conceal_basis(const double* image, int img_w, int img_h, const or_rect* blocks, int n,
+                      int block_h, int block_w, int algorithm, double gamma, int iterations, int t,
+                      double rho_hat, int support, int threads, double* restored, or_record* traces,
+                      int* trace_counts, double* psnr_db, int* psnr_identical,
+                      double* mean_seconds_per_block, int basis);
+
 int ref_conceal(const double* image, int img_w, int img_h, const or_rect* blocks, int n,
                 int block_h, int block_w, int algorithm, double gamma, int iterations, int t,
                 double rho_hat, int support, int threads, double* restored, or_record* traces,
                 int* trace_counts, double* psnr_db, int* psnr_identical,
                 double* mean_seconds_per_block) {
+    return ref_conceal_basis(image, img_w, img_h, blocks, n, block_h, block_w, algorithm, gamma, iterations, t,
+                             rho_hat, support, threads, restored, traces, trace_counts, psnr_db, psnr_identical,
+                             mean_seconds_per_block, 0);
+}
+
+// ConcealConfig::basis (pipeline.hpp:28): 0 dft2d, 1 dct2d (the spatial engine)
+int ref_conceal_basis(const double* image, int img_w, int img_h, const or_rect* blocks, int n,
+                      int block_h, int block_w, int algorithm, double gamma, int iterations, int t,
+                      double rho_hat, int support, int threads, double* restored, or_record* traces,
+                      int* trace_counts, double* psnr_db, int* psnr_identical,
+                      double* mean_seconds_per_block, int basis) {
     return guarded([&] {
         fse::LossPattern p;
         p.image_width = img_w;
@@ -271,6 +288,7 @@ int ref_conceal(const double* image, int img_w, int img_h, const or_rect* blocks
         cfg.support_width = support;
         cfg.threads = threads;
         cfg.record_traces = traces != nullptr;
+        cfg.basis = basis ? fse::BasisKind::dct2d : fse::BasisKind::dft2d;
         const auto out = fse::conceal(make_grid(image, img_h, img_w), p, cfg);
         std::memcpy(restored, out.restored.samples.data(),
                     sizeof(double) * out.restored.samples.size());

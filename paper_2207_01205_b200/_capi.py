@@ -20,6 +20,7 @@ GEN_EXPORTS = ["fofse_gen_image_u8", "fofse_gen_losses"]
 OK, EINVAL, ERUNTIME, ECUDA, EUNSUPPORTED = 0, 1, 2, 3, 4
 ALGO_FSE, ALGO_OFSE, ALGO_FOFSE = 0, 1, 2
 PREC_FP64, PREC_FP32 = 0, 1
+BASIS_DFT, BASIS_DCT = 0, 1
 SUPPORT, MISSING, OUTSIDE = 0, 1, 2
 
 # Every symbol include/fofse.h declares (checked by tests/test_capi.py).
@@ -52,7 +53,7 @@ class Params(C.Structure):
         ("algorithm", C.c_int32), ("gamma", C.c_double), ("iterations", C.c_int32),
         ("transform_size", C.c_int32), ("rho_hat", C.c_double), ("support_width", C.c_int32),
         ("threads", C.c_int32), ("record_traces", C.c_int32), ("precision", C.c_int32),
-        ("guard_tau", C.c_double), ("fp64_head", C.c_int32), ("pad0", C.c_int32),
+        ("guard_tau", C.c_double), ("fp64_head", C.c_int32), ("basis", C.c_int32),
     ]
 
 

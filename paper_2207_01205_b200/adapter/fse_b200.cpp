@@ -75,13 +75,8 @@ fofse_params params_of(const fse::ConcealConfig& c) {
     p.threads = c.threads;
     p.record_traces = c.record_traces ? 1 : 0;
     p.precision = FOFSE_PREC_FP64;  // the reference's arithmetic: same selected-basis sequence
+    p.basis = c.basis == fse::BasisKind::dct2d ? FOFSE_BASIS_DCT : FOFSE_BASIS_DFT;
     return p;
-}
-
-void require_dft(const fse::ConcealConfig& c) {
-    if (c.basis != fse::BasisKind::dft2d)
-        throw std::runtime_error("basis dct: the DCT family runs on the reference's spatial engine, "
-                                 "not on this GPU build (use the reference library for it)");
 }
 
 fse::IterationRecord to_record(const fofse_record& r) {
@@ -125,7 +120,6 @@ ConcealOutput conceal(const SampleGrid& image, const LossPattern& pattern, const
                                  pattern.block_width));
     if (pattern.image_width != image.width || pattern.image_height != image.height)
         throw std::invalid_argument("conceal: pattern dimensions do not match the image");
-    require_dft(config);
     ConcealOutput out;
     out.restored = grid(image.width, image.height);
     std::vector<fofse_record> tr;
@@ -161,7 +155,6 @@ ConcealOutput conceal(const SampleGrid& image, const LossPattern& pattern, const
 
 WindowRun extrapolate_window(const SampleGrid& window, const RegionMask& mask, const ConcealConfig& config) {
     const fofse_params p = params_of(config);
-    require_dft(config);
     if (mask.width != window.width || mask.height != window.height)
         throw std::invalid_argument("init_spectra: signal, mask and weight shapes differ");
     WindowRun run;

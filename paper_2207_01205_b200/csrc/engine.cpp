@@ -306,13 +306,14 @@ struct Cfg {
     int S, threads, traces, precision;
     double tau;
     int head;
+    int basis;
 };
 
 Cfg to_cfg(const fofse_params* p) {
     if (!p) throw std::invalid_argument("params must not be NULL");
     Cfg c{p->algorithm,      p->gamma,     p->iterations,    p->transform_size,
           p->rho_hat,        p->support_width, p->threads,   p->record_traces,
-          p->precision,      p->guard_tau,     p->fp64_head};
+          p->precision,      p->guard_tau,     p->fp64_head,     p->basis};
     return c;
 }
 
@@ -330,9 +331,15 @@ void validate_config(const Cfg& c) {
     if (c.threads < 1) throw std::invalid_argument("config: thread count must be >= 1");
     if (c.precision != FOFSE_PREC_FP64 && c.precision != FOFSE_PREC_FP32)
         throw std::invalid_argument("config: precision must be FOFSE_PREC_FP64 or FOFSE_PREC_FP32");
+    if (c.basis != FOFSE_BASIS_DFT && c.basis != FOFSE_BASIS_DCT)
+        throw std::invalid_argument("config: basis must be FOFSE_BASIS_DFT or FOFSE_BASIS_DCT");
 }
 
 void check_gpu_support(const Cfg& c) {
+    if (c.basis == FOFSE_BASIS_DCT) {  // the spatial engine takes any T (kernels_dct.cu)
+        if (c.T > 512) throw Unsupported("transform_size must be <= 512 for the DCT basis on the GPU path");
+        return;
+    }
     if (!(c.T == 8 || c.T == 16 || c.T == 32 || c.T == 64 || c.T == 128))
         throw Unsupported("transform_size must be a power of two in [8, 128] on the GPU path");
 }
@@ -807,6 +814,73 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         for (size_t i = 0; i < L; ++i)
             if (lab[i] == FOFSE_SUPPORT) wcls[static_cast<size_t>(c) * L + i] = job.wfull[i];
         sym[static_cast<size_t>(c)] = point_symmetric(lab, g.Lh, g.Lw) ? 1 : 0;
+    }
+    if (cfg.basis == FOFSE_BASIS_DCT) {
+        // ---- the DCT family: the spatial engine (engine_spatial.cpp:254-381) in the
+        // reference's operation order, fp64, every block (kernels_dct.cu) ----
+        if (ckpts) throw Unsupported("PSNR curves are built for the DFT basis only");
+        std::vector<double> axis(static_cast<size_t>(T) * T);  // basis.cpp:19-27
+        const double a0 = std::sqrt(1.0 / T), ak = std::sqrt(2.0 / T);
+        for (int k = 0; k < T; ++k)
+            for (int m = 0; m < T; ++m)
+                axis[static_cast<size_t>(k) * T + m] = (k == 0 ? a0 : ak) * std::cos(M_PI * (2 * m + 1) * k / (2.0 * T));
+        const double* d_axis = upload(ctx, "ks_axis", axis.data(), axis.size());
+        const double* d_w = upload(ctx, "wcls", wcls.data(), wcls.size());
+        const BlockDesc* d_bl = upload(ctx, "ks_blocks", job.blocks.data(), job.blocks.size());
+        std::vector<int32_t> idv(static_cast<size_t>(n));
+        for (int64_t i = 0; i < n; ++i) idv[static_cast<size_t>(i)] = static_cast<int32_t>(i);
+        const int32_t* d_idv = upload(ctx, "ks_ids", idv.data(), idv.size());
+        if (gio)
+            for (int gq = 0; gq < job.groups; ++gq) {
+                gio->ensure_h2d(gq);
+                ck(cudaStreamWaitEvent(st, gio->h2d_done[static_cast<size_t>(gq)], 0), "wait");
+            }
+        ck(cudaEventRecord(ctx->ev[1], st), "event");
+        const int64_t chunk = std::min<int64_t>(std::max<int64_t>(n, 1), 4096);
+        double* d_scr = ctx->buf("ks_scr").as<double>(static_cast<size_t>(chunk) * ks_scratch_doubles(T));
+        const bool img_region = synth == SYN_IMAGE || synth == SYN_ERR;
+        for (int64_t b0 = 0; b0 < n; b0 += chunk) {
+            DctArgs a{};
+            a.T = T;
+            a.Lh = g.Lh;
+            a.Lw = g.Lw;
+            a.n = static_cast<int32_t>(std::min(chunk, n - b0));
+            a.blocks = d_bl + b0;
+            a.order = d_idv + b0;
+            a.fr = fr;
+            a.wcls = d_w;
+            a.axis = d_axis;
+            a.iterations = I;
+            // ConcealConfig::engine_config (pipeline.cpp:40-60)
+            a.selection = cfg.algorithm == FOFSE_ALGO_FOFSE ? 0 : 1;
+            a.compensation = cfg.algorithm == FOFSE_ALGO_FSE ? 0 : cfg.algorithm == FOFSE_ALGO_FOFSE ? 1 : 2;
+            a.gamma = cfg.gamma;
+            a.scratch = d_scr;
+            a.synth = synth;
+            a.reg_r0 = img_region ? g.S : 0;
+            a.reg_c0 = img_region ? g.S : 0;
+            a.reg_nr = img_region ? g.bh : g.Lh;
+            a.reg_nc = img_region ? g.bw : g.Lw;
+            a.models = d_models;
+            a.block_sq = d_block_sq;
+            a.trace = d_trace;
+            a.trace_count = d_trace_count;
+            a.trace_stride = I;
+            ck(ks_launch(a, st), "KS spatial DCT engine");
+            ++ctx->launches;
+        }
+        ck(cudaEventRecord(ctx->ev[2], st), "event");
+        ck(cudaEventRecord(ctx->ev[3], st), "event");
+        if (gio)
+            for (int gq = 0; gq < job.groups; ++gq) gio->on_done(gq, st);
+        ck(cudaEventSynchronize(ctx->ev[3]), "sync");
+        float ms = 0;
+        ck(cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[3]), "elapsed");
+        out.total_ms = ms;
+        ck(cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]), "elapsed");
+        out.init_ms = ms;
+        out.iter_ms = out.total_ms - out.init_ms;
+        return out;
     }
     // fp64 only: OFSE and the checkpointed curves (resumable fp64 phases)
     const bool fp32 = cfg.precision == FOFSE_PREC_FP32 && !full_od(cfg) && !ckpts;

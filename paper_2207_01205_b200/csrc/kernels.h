@@ -174,6 +174,31 @@ struct K1xArgs {
 };
 int k1x_launch(const K1xArgs& a, cudaStream_t s);
 
+// KS: the spatial engine for the DCT basis (kernels_dct.cu), reference op order.
+struct DctArgs {
+    int32_t T, Lh, Lw, n;
+    const BlockDesc* blocks;    // by position
+    const int32_t* order;       // position -> caller id (NULL = identity)
+    Frames fr;
+    const double* wcls;         // [ncls][Lh*Lw]
+    const double* axis;         // [T][T] dct_axis(k, m) (basis.cpp:19-27, host libm)
+    int32_t iterations;
+    int32_t selection;          // 0 max weighted portion (fofse), 1 min distance (fse, ofse)
+    int32_t compensation;       // 0 none (fse), 1 constant gamma (fofse), 2 full OD (ofse)
+    double gamma;
+    double* scratch;            // [n][ks_scratch_doubles(T)]
+    int32_t synth;              // SYN_IMAGE / SYN_WINDOW
+    int32_t reg_r0, reg_c0, reg_nr, reg_nc;
+    double* models;             // SYN_WINDOW: [id][Lh*Lw]
+    double* block_sq;           // SYN_IMAGE: [id]
+    fofse_record* trace;        // [id][trace_stride] (optional)
+    int32_t* trace_count;       // [id] (optional)
+    int32_t trace_stride;
+    int32_t* conv_out;          // [id] (optional)
+};
+size_t ks_scratch_doubles(int T);
+int ks_launch(const DctArgs& a, cudaStream_t s);
+
 struct CvtArgs {
     int32_t T, Lh, Lw, n;
     const double2* in;          // packed fp64 residuals (strict layout: seg_of(T, F64), SPT 1)

@@ -74,6 +74,7 @@ class ConcealConfig:
     precision: str = "fp64"
     guard_tau: float = -1.0
     fp64_head: int = -1
+    basis: str = "dft2d"  # fse::BasisKind (basis.hpp:17): dft2d or dct2d
 
     def validate(self):
         """pipeline.cpp:34-38 + engine_spatial.cpp:8-15 (same messages)."""
@@ -106,6 +107,9 @@ class ConcealConfig:
         p.precision = _PRECS[self.precision]
         p.guard_tau = self.guard_tau
         p.fp64_head = self.fp64_head
+        if self.basis not in ("dft2d", "dct2d"):
+            raise ValueError("config: basis must be 'dft2d' or 'dct2d'")
+        p.basis = capi.BASIS_DCT if self.basis == "dct2d" else capi.BASIS_DFT
         return p
 
 
