@@ -34,7 +34,7 @@ def test_conceal_dct_bit_exact_vs_reference(gpu, ref, algo, t, blk, sup, its):
         for k in ("u1", "u2", "p_re", "p_im", "c_re", "c_im", "gamma_effective", "weighted_energy", "degenerate"):
             np.testing.assert_array_equal(a[k], b[k], err_msg=k)
     np.testing.assert_array_equal(out.restored, r["restored"])
-    assert out.report.psnr_db == r["psnr_db"]
+    assert out.report.psnr_db == pytest.approx(r["psnr_db"], rel=1e-13)  # summation order of the MSE
 
 
 def test_dct_window_level_and_frames(gpu, ref):
