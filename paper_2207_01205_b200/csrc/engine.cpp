@@ -37,6 +37,8 @@
 #include <unordered_map>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only; a no-op unless a profiler attaches
+
 #include "../../include/fofse.h"
 #include "kernels.h"
 #include "layout.h"
@@ -720,12 +722,24 @@ struct RunOut {
     int64_t reruns = 0, converged = 0, head = 0, resumed = 0;
 };
 
-// FOFSE_HOST_PROF=1 prints host-side checkpoints of run_job to stderr.
+// NVTX ranges of the host-side phases (nsys / ncu --nvtx): the B200 counterpart
+// of the reference's per-block timing (pipeline.cpp:224-233); device time per
+// phase comes from the CUDA events of run_job.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
+// FOFSE_HOST_PROF=1 prints host-side checkpoints of run_job to stderr (every
+// checkpoint is also an NVTX marker).
 struct HostProf {
     bool on;
     std::chrono::steady_clock::time_point t0;
     HostProf() : on(std::getenv("FOFSE_HOST_PROF") != nullptr), t0(std::chrono::steady_clock::now()) {}
     void mark(const char* what) const {
+        nvtxMarkA(what);
         if (!on) return;
         const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         std::fprintf(stderr, "[fofse host] %8.2f ms  %s\n", ms, what);
@@ -793,6 +807,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
                float* d_gap = nullptr, const GroupIO* gio = nullptr,
                const std::vector<int>* ckpts = nullptr) {
     using namespace fofse;
+    const NvtxRange nv_job("fofse::run_job");
     const Geometry& g = job.geo;
     const int T = g.T;
     const int64_t n = static_cast<int64_t>(job.blocks.size());
@@ -818,6 +833,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
     if (cfg.basis == FOFSE_BASIS_DCT) {
         // ---- the DCT family: the spatial engine (engine_spatial.cpp:254-381) in the
         // reference's operation order, fp64, every block (kernels_dct.cu) ----
+        const NvtxRange nv("fofse::DCT spatial engine");
         if (ckpts) throw Unsupported("PSNR curves are built for the DFT basis only");
         std::vector<double> axis(static_cast<size_t>(T) * T);  // basis.cpp:19-27
         const double a0 = std::sqrt(1.0 / T), ak = std::sqrt(2.0 / T);
@@ -1189,6 +1205,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
 
     if (!fp32) {
         // ---- fp64: K2d (symmetric masks) / strict kernel, every block ----
+        const NvtxRange nv("fofse::fp64 iterate");
         ck(cudaEventRecord(ctx->ev[1], st), "event");
         K2Args a = base_args();
         a.rin = d_R64;
@@ -1207,6 +1224,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             }
             if (d_tie) {
                 // ---- near-tie blocks: the exact path (K1x + strict kernel, hypot argmax) ----
+                const NvtxRange nv("fofse::fp64 near-tie exact re-runs");
                 std::vector<int32_t> tie(static_cast<size_t>(n));
                 ck(cudaMemcpyAsync(tie.data(), d_tie, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st), "D2H tie");
                 ck(cudaStreamSynchronize(st), "sync");
@@ -1308,6 +1326,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             for (int gq = 0; gq < ngroups; ++gq) gio->on_done(gq, st);
     } else {
         // ---- fp32 fast mode: a pipeline over chunks of blocks ----
+        const NvtxRange nv("fofse::fp32 chunk pipeline (K1 + fp64 head + fp32 iterate + guard re-runs)");
         // chunk = K1 (+ fp64 head + convert) + the fp32 iteration; once a chunk
         // is done its near-tie re-runs (fp64, from scratch) are launched on the
         // aux stream, where they overlap the following chunks. Asymmetric-mask
@@ -1924,6 +1943,7 @@ void fill_image_job(Job& job, const Cfg& cfg, int W, int H, int bh, int bw, cons
 
 Job make_image_job(const Cfg& cfg, int W, int H, int bh, int bw, const fofse_rect* blocks,
                    const int64_t* offs, int nframes) {
+    const NvtxRange nv("fofse::plan (validate + window classes)");
     Job job;
     fill_image_job(job, cfg, W, H, bh, bw, blocks, offs, nframes);
     job.grids = {};

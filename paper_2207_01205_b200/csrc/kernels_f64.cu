@@ -19,6 +19,7 @@
 //    scalar part of iterate redundantly (no controller hand-off);
 //  * the next scan is fused into the update (one pass over the registers).
 // Used for fp64 concealment, the fp32 mode's fp64 head and its guard re-runs.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -929,6 +930,236 @@ __global__ void __launch_bounds__(256, 2) k2dc_kernel(K2Args a) {
     }
 }
 
+// ============================================================================
+// K2dcx: K2dc at T = 128 on a 2-CTA thread-block cluster (north_star: "a
+// thread-block cluster with DSMEM for 128x128 FFTs"). The complex fp64 W image
+// of an asymmetric window (128 x 145 x 16 B = 297 KB) exceeds one SM's shared
+// memory, so the pair splits it by rows — CTA r stages rows [64 r, 64 r + 64)
+// (148 KB, TMA bulk copy) — and every W gather goes through the cluster's
+// distributed shared memory: the row (k1 -+ u1) mod 128 is read from whichever
+// CTA holds it (generic loads on map_shared_rank addresses). The block's 8,194
+// canonical bins are split across the pair by the K2dc thread layout (512
+// threads, CTA r = threads [256 r, 256 r + 256): columns [64 r, 64 r + 64) of
+// every row). Argmax: every warp's winner slot is written to BOTH CTAs' slot
+// arrays (parity double-buffered), one cluster barrier per selection, then every
+// thread resolves the same winner and runs the scalar part redundantly — the
+// K2d / K2dc protocol with the barrier stretched over the pair. The synthesis
+// epilogue runs on CTA 0.
+// ============================================================================
+struct DCXCfg {
+    static constexpr int T = 128, SEG = 16, HT = 64, NT = 512, CT = 256, NWC = 8, NWG = 16;
+    static constexpr int SR = T + SEG + 1;  // the class image row stride (K1 class mode)
+    static constexpr int HROWS = T / 2;
+    static constexpr size_t HALF_BYTES = (size_t)HROWS * SR * sizeof(double2);
+    static constexpr size_t OFF_P = HALF_BYTES;                             // ptab: 2T double2
+    static constexpr size_t OFF_TW = OFF_P + sizeof(double2) * 2 * T;      // twi: T double2
+    static constexpr size_t OFF_S = OFF_TW + sizeof(double2) * T;           // slots [2][16] DSlot
+    static constexpr size_t OFF_RED = OFF_S + 2 * NWG * sizeof(DSlot);      // red[8]
+    static constexpr size_t OFF_BAR = OFF_RED + NWC * sizeof(double);
+    static constexpr size_t SMEM = OFF_BAR + 16;
+    static_assert(HALF_BYTES % 16 == 0, "bulk copy granularity");
+    static_assert(SMEM <= 227 * 1024, "shared memory");
+};
+
+template <bool TIE>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) k2dcx_kernel(K2Args a) {
+    namespace cg = cooperative_groups;
+    using Cf = DCXCfg;
+    constexpr int T = Cf::T, SEG = Cf::SEG, NT = Cf::NT, SR = Cf::SR, NB = SEG + 1;
+    cg::cluster_group cl = cg::this_cluster();
+    const int rank = static_cast<int>(cl.block_rank());
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const Tile tile = a.tiles[blockIdx.x / 2];
+
+    // ---- stage this CTA's half of the class image + the phase / twiddle tables ----
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(smem_raw + Cf::OFF_BAR);
+    if (threadIdx.x == 0) {
+        mbar_init(mbar, 1);
+        const char* src = static_cast<const char*>(a.wimg) + (size_t)tile.cls * a.wimg_stride * sizeof(double2) +
+                          (size_t)rank * Cf::HALF_BYTES;
+        constexpr uint32_t bytes = static_cast<uint32_t>(Cf::HALF_BYTES);
+        mbar_expect_tx(mbar, bytes);
+        for (uint32_t off = 0; off < bytes; off += 32768)
+            bulk_g2s(smem_raw + off, src + off, bytes - off < 32768u ? bytes - off : 32768u, mbar);
+    }
+    double2* twi = reinterpret_cast<double2*>(smem_raw + Cf::OFF_TW);
+    for (int i = threadIdx.x; i < T; i += blockDim.x) twi[i] = a.twid_inv[i];
+    __syncthreads();
+    mbar_wait(mbar, 0);
+    cl.sync();  // both halves resident before any remote read
+    const double2* whalf0 = cl.map_shared_rank(reinterpret_cast<double2*>(smem_raw), 0);
+    const double2* whalf1 = cl.map_shared_rank(reinterpret_cast<double2*>(smem_raw), 1);
+    auto wrow = [&](int row) { return (row >= 64 ? whalf1 : whalf0) + (row & 63) * SR; };  // W row (either CTA)
+    DSlot* slots = reinterpret_cast<DSlot*>(smem_raw + Cf::OFF_S);
+    DSlot* pslots = cl.map_shared_rank(slots, rank ^ 1);  // the partner's copy
+    double* red = reinterpret_cast<double*>(smem_raw + Cf::OFF_RED);
+
+    const int ltid = rank * Cf::CT + static_cast<int>(threadIdx.x);
+    const int w = static_cast<int>(threadIdx.x) >> 5, gw = rank * Cf::NWC + w;
+    const BinLayout L = BinLayout::make(T, SEG, 1);
+    int k1 = 0, c0 = 0, ex = 0;
+    L.segment(ltid, &k1, &c0, &ex);
+    const int gbase = k1 * T + c0;
+    constexpr unsigned long long KM = DCfg<128>::KMASK;
+    constexpr int KTOP = static_cast<int>(DCfg<128>::KTOP);
+    const unsigned kbase = static_cast<unsigned>(KTOP - gbase);
+    const int rstride = a.rec_stride > 0 ? a.rec_stride : a.iterations;
+    const int tstride = a.trace_stride > 0 ? a.trace_stride : a.iterations;
+    const double w0 = a.w0[tile.cls], iw = 1.0 / w0;
+
+    for (int bi = 0; bi < tile.count; ++bi) {
+        const int pos = tile.begin + bi;
+        const int b = a.order[pos];
+        double re[NB], im[NB];
+        {
+            const double2* R = static_cast<const double2*>(a.rin) + (size_t)pos * L.SLOTS;
+#pragma unroll
+            for (int j = 0; j < SEG; ++j) {
+                const double2 v = R[j * NT + ltid];
+                re[j] = v.x;
+                im[j] = v.y;
+            }
+            const double2 v = ex ? R[SEG * NT + ltid] : make_double2(0.0, 0.0);
+            re[SEG] = v.x;
+            im[SEG] = v.y;
+        }
+        int* rec_u = a.rec_u_g + (size_t)b * rstride;
+        double2* rec_c = a.rec_c_g + (size_t)b * rstride;
+        double energy = a.energy0[pos];
+        const double e_init = a.init_energy[pos];
+        const double thr_e = 1e-12 * e_init;
+        const double thr_m = (1e-12 * a.init_max[pos]) * (1e-12 * a.init_max[pos]);
+        int nu = a.nu0 ? a.nu0[pos] : 0;
+        int ntrace = a.trace_from_nu0 ? nu : 0;
+        int conv = (a.conv0 ? a.conv0[pos] : 0) | (e_init <= 0.0);
+        unsigned long long KA = 0, KB = 0;
+        unsigned S2 = 0;
+        int flagged = 0;
+#pragma unroll
+        for (int j = 0; j < SEG; ++j) dscan<KM, TIE>((j & 1) ? KB : KA, S2, re[j], im[j], kbase - j);
+        if (ex) dscan<KM, TIE>(KA, S2, re[SEG], im[SEG], kbase - SEG);
+
+        const int nu_end = a.nu_limit > 0 ? a.nu_limit : nu + a.iterations;
+        for (int it = 0; nu < nu_end && !conv; ++it) {
+            const int par = it & 1;
+            const unsigned long long K = KA > KB ? KA : KB;
+            const unsigned hi = static_cast<unsigned>(K >> 32), lo = static_cast<unsigned>(K);
+            const unsigned Mhi = __reduce_max_sync(0xffffffffu, hi);
+            const unsigned Mlo = __reduce_max_sync(0xffffffffu, hi == Mhi ? lo : 0u);
+            const bool win = hi == Mhi && lo == Mlo;
+            unsigned ws2 = 0;
+            if constexpr (TIE) {
+                const unsigned t2 = max(S2, min(static_cast<unsigned>(KA >> 32), static_cast<unsigned>(KB >> 32)));
+                ws2 = __reduce_max_sync(0xffffffffu, win ? t2 : hi);
+            }
+            if (win) {  // the warp's candidate, into both CTAs' slot arrays
+                const int g = KTOP - static_cast<int>(Mlo & DCfg<128>::KTOP);
+                const double2 pre = dpick<NB>(g - gbase, re, im);
+                const DSlot ds{Mhi, Mlo, g, static_cast<int>(ws2), pre.x, pre.y};
+                slots[par * Cf::NWG + gw] = ds;
+                pslots[par * Cf::NWG + gw] = ds;
+            }
+            cl.sync();  // one cluster barrier per selection
+            int wb = 0;
+            {
+                uint2 kb = *reinterpret_cast<const uint2*>(&slots[par * Cf::NWG]);
+#pragma unroll
+                for (int k = 1; k < Cf::NWG; ++k) {
+                    const uint2 o = *reinterpret_cast<const uint2*>(&slots[par * Cf::NWG + k]);
+                    const bool gt = o.x > kb.x || (o.x == kb.x && o.y > kb.y);
+                    kb = gt ? o : kb;
+                    wb = gt ? k : wb;
+                }
+            }
+            const DSlot s = slots[par * Cf::NWG + wb];
+            const double pr = s.pre_re, pi = s.pre_im;
+            const double M = fma(pi, pi, pr * pr);
+            if (energy < thr_e || !(M > 0.0) || M < thr_m) {
+                conv = 1;
+                break;
+            }
+            if constexpr (TIE) {
+                // the runner-up's high word within one step of the maximum: flag (the exact
+                // path resolves the selection; no second pass over the pair)
+                unsigned s2 = static_cast<unsigned>(s.pad);
+#pragma unroll
+                for (int k = 0; k < Cf::NWG; ++k)
+                    if (k != wb) s2 = max(s2, slots[par * Cf::NWG + k].hi);
+                if (s2 + 1u >= s.hi) {
+                    flagged = 1 + nu;
+                    break;
+                }
+            }
+            const int G = s.g;
+            const int u1 = G / T, u2 = G % T;
+            const int self = ((T - u1) % T == u1) && ((T - u2) % T == u2);
+            const double2* wa = wrow((k1 - u1) & (T - 1)) + ((c0 - u2) & (T - 1));  // W[k-u] (DSMEM)
+            const double2* wb2 = wrow((k1 + u1) & (T - 1)) + ((c0 + u2) & (T - 1));  // W[k+u]
+            const double geff = a.gamma;
+            const double p_re = pr * iw, p_im = pi * iw;
+            const double c_re = p_re * geff, c_im = self ? 0.0 : p_im * geff;
+            double delta;
+            if (self) {
+                delta = -2.0 * c_re * pr + c_re * c_re * w0;
+            } else {
+                const double2 w2 = wrow((2 * u1) & (T - 1))[(2 * u2) & (T - 1)];
+                const double cc_r = c_re * c_re - c_im * c_im, cc_i = 2.0 * c_re * c_im;
+                delta = -4.0 * (c_re * pr + c_im * pi) + 2.0 * (c_re * c_re + c_im * c_im) * w0 +
+                        2.0 * (cc_r * w2.x + cc_i * w2.y);
+            }
+            const double e = energy + delta;
+            energy = 0.0 < e ? e : 0.0;
+            nu += 1;
+            if (ltid == 0)
+                v2_record(a, b, nu, ntrace, rstride, tstride, rec_u, rec_c, u1, u2, self, p_re, p_im, c_re, c_im,
+                          energy, M, 0.0, geff, 0);
+            ntrace += 1;
+            KA = 0;
+            KB = 0;
+            S2 = 0;
+#pragma unroll
+            for (int j = 0; j < NB; ++j) {
+                if (j == SEG && !ex) break;
+                const double2 x = wa[j];
+                double r = fma(-c_re, x.x, fma(c_im, x.y, re[j]));
+                double m = fma(-c_re, x.y, fma(-c_im, x.x, im[j]));
+                if (!self) {
+                    const double2 y = wb2[j];
+                    r = fma(-c_re, y.x, fma(-c_im, y.y, r));
+                    m = fma(-c_re, y.y, fma(c_im, y.x, m));
+                }
+                re[j] = r;
+                im[j] = m;
+                if (j < SEG)
+                    dscan<KM, TIE>((j & 1) ? KB : KA, S2, r, m, kbase - j);
+                else
+                    dscan<KM, TIE>(KA, S2, r, m, kbase - SEG);
+            }
+        }
+        if (a.rout) {
+            double2* R = static_cast<double2*>(a.rout) + (size_t)pos * L.SLOTS;
+#pragma unroll
+            for (int j = 0; j < SEG; ++j) R[j * NT + ltid] = make_double2(re[j], im[j]);
+            if (ex) R[SEG * NT + ltid] = make_double2(re[SEG], im[SEG]);
+        }
+        cl.sync();  // records visible; the pair leaves the block's remote reads together
+        if (rank == 0)
+            v2_finish<T, Cf::CT, double2>(a, a.blocks[pos], pos, b, ltid, energy, nu, conv, flagged, ntrace, rec_u,
+                                          rec_c, rstride, twi, red, 1);
+        cl.sync();
+    }
+}
+
+static int k2dcx_launch(const K2Args& a, int32_t ntiles, cudaStream_t s) {
+    if (a.full_od) return cudaErrorInvalidValue;  // OFSE at T = 128 keeps the strict kernel
+    auto* fn = a.tau > 0.0 ? k2dcx_kernel<true> : k2dcx_kernel<false>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DCXCfg::SMEM);
+    if (e != cudaSuccess) return e;
+    if (ntiles <= 0) return cudaSuccess;
+    fn<<<2 * ntiles, DCXCfg::CT, DCXCfg::SMEM, s>>>(a);
+    return cudaGetLastError();
+}
+
 template <int T>
 static int k2dc_t(const K2Args& a, int32_t ntiles, cudaStream_t s) {
     using Cf = DCCfg<T>;
@@ -988,6 +1219,7 @@ int k2d_launch(const K2Args& a, int32_t ntiles, cudaStream_t s) {
             case 16: return k2dc_t<16>(a, ntiles, s);
             case 32: return k2dc_t<32>(a, ntiles, s);
             case 64: return k2dc_t<64>(a, ntiles, s);
+            case 128: return k2dcx_launch(a, ntiles, s);  // 2-CTA cluster
         }
         return cudaErrorInvalidValue;
     }

@@ -148,7 +148,7 @@ bool v2h128_enabled();
 // conflict free. K2dc (complex W, asymmetric masks) stops at T = 64: the fp64
 // complex image of T = 128 exceeds shared memory (the strict kernel serves it).
 FOFSE_HDC bool d_supported(int t) { return t >= 8 && t <= 128; }
-FOFSE_HDC bool dc_supported(int t) { return t >= 8 && t <= 64; }
+FOFSE_HDC bool dc_supported(int t) { return t >= 8 && t <= 128; }  // T = 128: the 2-CTA cluster form
 FOFSE_HDC int d_ncopy(int t) { return t <= 64 ? 2 : 1; }
 FOFSE_HDC int d_srv(int t) { return t <= 64 ? t + seg_for(t, 1) + 2 : t + seg_for(t, 1) + 1; }
 

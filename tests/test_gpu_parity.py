@@ -257,6 +257,49 @@ def test_conceal_fp64_T128_k2d_matches_strict(gpu, monkeypatch):
     assert np.abs(fast.restored - strict.restored).max() <= FP64_PX_TOL
 
 
+def _c5_border_crop(seed, size=1024):
+    """32 x 32 blocks on all four image edges (asymmetric windows, 300 iterations)."""
+    img = P.gen_image_u8(seed, size, size)
+    blocks = set()
+    for x in range(0, size - 31, 96):
+        blocks |= {(0, x), (size - 32, x), (x, 0), (x, size - 32)}
+    pat = P.LossPattern(size, size, 32, 32, [P.Rect(r, c, 32, 32) for r, c in sorted(blocks)])
+    return img, pat
+
+
+def test_conceal_fp64_T128_border_cluster_matches_strict(gpu, monkeypatch):
+    """T = 128 asymmetric (border) windows run K2dcx — the 2-CTA cluster kernel with
+    the W image split across the pair's shared memory (DSMEM gathers): identical
+    selections to the strict kernel (reference op order), pixels within 1e-9."""
+    img, pat = _c5_border_crop(61)
+    cfg = WL.C5.config("fp64", record_traces=True)
+    fast = P.conceal(img.astype(np.float64), pat, cfg)
+    monkeypatch.setenv("FOFSE_F64_KERNEL", "strict")
+    strict = P.conceal(img.astype(np.float64), pat, cfg)
+    _assert_same_selections(fast.report.traces, strict.report.traces)
+    assert np.abs(fast.restored - strict.restored).max() <= FP64_PX_TOL
+
+
+def test_conceal_T128_border_cluster_vs_oracle_both_precisions(gpu, orc):
+    """Border windows at T = 128 against the oracle: fp64 selections + 1e-9 px; the
+    fp32 mode (borders run fp64 outright on K2dcx, interior fp32) within 0.5 px."""
+    img, pat = _c5_border_crop(62, 512)
+    pat = P.LossPattern(pat.image_width, pat.image_height, 32, 32, pat.blocks[:8])
+    cfg = WL.C5.config("fp64", record_traces=True)
+    cfg.iterations = 150
+    out = P.conceal(img.astype(np.float64), pat, cfg)
+    ref = _oracle_conceal(orc, img, pat, cfg)
+    _assert_same_selections(out.report.traces, ref["traces"])
+    assert np.abs(out.restored - ref["restored"]).max() <= FP64_PX_TOL
+    cfg32 = WL.C5.config("fp32")
+    cfg32.iterations = 150
+    o32 = P.conceal(img.astype(np.float64), pat, cfg32)
+    lost = np.zeros(img.shape, bool)
+    for b in pat.blocks:
+        lost[b.row:b.row + 32, b.col:b.col + 32] = True
+    assert _fp32_vs_ref(o32.restored, ref["restored"], lost) <= FP32_PX_TOL
+
+
 @pytest.mark.parametrize("name", ["C2", "C3", "C5"])
 def test_k1_register_fft_matches_radix2(gpu, monkeypatch, name):
     """The register K1 (T = 64: radix-8x8; T = 32: radix-8 then two radix-4 per
