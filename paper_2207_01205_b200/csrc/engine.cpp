@@ -1365,9 +1365,11 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             if (r.path != PATH_F32_REAL) {
                 // a border range under one wave runs in fp64 outright (K2dc, T <= 64),
                 // concurrently with the main chunks: no head / convert / guard re-runs
-                // (C2 +2 %; at T = 128 only the slow strict kernel could, measured -3 %)
+                // (C2 +2 %). At T = 128 the cluster kernel K2dcx (~2.2 us per selection)
+                // serves the head and re-runs; outright it measured 0.7 % slower on C5
                 chunks.push_back({r.path, r.begin, r.end, cs, r.grp,
-                                  f64_direct_on && on_side && len <= one_wave && hi_path(r.path) == PATH_F64_CPLX});
+                                  f64_direct_on && on_side && len <= one_wave && T <= 64 &&
+                                      hi_path(r.path) == PATH_F64_CPLX});
                 continue;
             }
             const int nc = static_cast<int>(std::clamp<int64_t>(len / chunk_min, 1, 8));

@@ -19,7 +19,6 @@
 //    scalar part of iterate redundantly (no controller hand-off);
 //  * the next scan is fused into the update (one pass over the registers).
 // Used for fp64 concealment, the fp32 mode's fp64 head and its guard re-runs.
-#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -932,51 +931,81 @@ __global__ void __launch_bounds__(256, 2) k2dc_kernel(K2Args a) {
 
 // ============================================================================
 // K2dcx: K2dc at T = 128 on a 2-CTA thread-block cluster (north_star: "a
-// thread-block cluster with DSMEM for 128x128 FFTs"). The complex fp64 W image
-// of an asymmetric window (128 x 145 x 16 B = 297 KB) exceeds one SM's shared
-// memory, so the pair splits it by rows — CTA r stages rows [64 r, 64 r + 64)
-// (148 KB, TMA bulk copy) — and every W gather goes through the cluster's
-// distributed shared memory: the row (k1 -+ u1) mod 128 is read from whichever
-// CTA holds it (generic loads on map_shared_rank addresses). The block's 8,194
-// canonical bins are split across the pair by the K2dc thread layout (512
-// threads, CTA r = threads [256 r, 256 r + 256): columns [64 r, 64 r + 64) of
-// every row). Argmax: every warp's winner slot is written to BOTH CTAs' slot
-// arrays (parity double-buffered), one cluster barrier per selection, then every
-// thread resolves the same winner and runs the scalar part redundantly — the
-// K2d / K2dc protocol with the barrier stretched over the pair. The synthesis
-// epilogue runs on CTA 0.
+// thread-block cluster with DSMEM for 128x128 FFTs"). One asymmetric-window
+// block's 8,194 canonical bins need 512 threads x 17 complex fp64 bins — twice
+// the register file of one SM at K2dc's register use (254 / thread) — so the
+// pair holds them: CTA r = threads [256 r, 256 r + 256) of the K2dc layout
+// (columns [64 r, 64 r + 64) of every row). The W image is REPLICATED, not
+// split: W is Hermitian (the window weights are real), so rows 0..64 of it
+// (65 x 145 x 16 B = 151 KB) give every row — W[r][c] = conj(W[128-r][-c]) for
+// r > 64 — and each CTA stages that half-image with one TMA bulk copy: every W
+// gather is a local LDS.128 (a mirrored row is read with a negative stride and
+// conjugated). Only the argmax crosses the pair: every warp's winner slot goes
+// to the local slot array and, by st.async, to the partner's, completing on
+// the partner's parity-indexed mbarrier (DSMEM, no cluster-scope fence); then
+// every thread resolves the same winner and runs the scalar part redundantly —
+// the K2d / K2dc protocol stretched over the pair. CTA 0 runs the synthesis.
 // ============================================================================
+// distributed shared memory of the pair (PTX mapa / st.async.shared::cluster),
+// and the cluster barrier (used at kernel start / exit only: at cluster scope
+// its release compiles to a GPU-scope fence)
+__device__ __forceinline__ uint32_t dsm_map(const void* p, uint32_t rank) {
+    uint32_t r;
+    asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+    return r;
+}
+// a slot into the partner's shared memory, completing 32 bytes on its mbarrier
+// (st.async: the receiver's mbarrier phase orders the data, no fence)
+__device__ __forceinline__ void dsm_st_slot(uint32_t addr, const DSlot& s, uint32_t rbar) {
+    const uint4 a = *reinterpret_cast<const uint4*>(&s), b = *(reinterpret_cast<const uint4*>(&s) + 1);
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                     addr),
+                 "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(rbar)
+                 : "memory");
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                     addr + 16),
+                 "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w), "r"(rbar)
+                 : "memory");
+}
+__device__ __forceinline__ void cluster_bar() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 struct DCXCfg {
     static constexpr int T = 128, SEG = 16, HT = 64, NT = 512, CT = 256, NWC = 8, NWG = 16;
     static constexpr int SR = T + SEG + 1;  // the class image row stride (K1 class mode)
-    static constexpr int HROWS = T / 2;
+    static constexpr int HROWS = T / 2 + 1;  // rows 0..64: the others by Hermitian symmetry
     static constexpr size_t HALF_BYTES = (size_t)HROWS * SR * sizeof(double2);
     static constexpr size_t OFF_P = HALF_BYTES;                             // ptab: 2T double2
     static constexpr size_t OFF_TW = OFF_P + sizeof(double2) * 2 * T;      // twi: T double2
     static constexpr size_t OFF_S = OFF_TW + sizeof(double2) * T;           // slots [2][16] DSlot
     static constexpr size_t OFF_RED = OFF_S + 2 * NWG * sizeof(DSlot);      // red[8]
-    static constexpr size_t OFF_BAR = OFF_RED + NWC * sizeof(double);
-    static constexpr size_t SMEM = OFF_BAR + 16;
+    static constexpr size_t OFF_BAR = OFF_RED + NWC * sizeof(double);  // staging mbarrier
+    static constexpr size_t OFF_RB = OFF_BAR + 8;                        // receive mbarriers [2]
+    static constexpr size_t SMEM = OFF_RB + 16;
+    static constexpr uint32_t XBYTES = NWC * sizeof(DSlot);  // the partner's slots per selection
     static_assert(HALF_BYTES % 16 == 0, "bulk copy granularity");
     static_assert(SMEM <= 227 * 1024, "shared memory");
 };
 
 template <bool TIE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) k2dcx_kernel(K2Args a) {
-    namespace cg = cooperative_groups;
     using Cf = DCXCfg;
     constexpr int T = Cf::T, SEG = Cf::SEG, NT = Cf::NT, SR = Cf::SR, NB = SEG + 1;
-    cg::cluster_group cl = cg::this_cluster();
-    const int rank = static_cast<int>(cl.block_rank());
+    uint32_t crank;
+    asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+    const int rank = static_cast<int>(crank);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const Tile tile = a.tiles[blockIdx.x / 2];
 
     // ---- stage this CTA's half of the class image + the phase / twiddle tables ----
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smem_raw + Cf::OFF_BAR);
+    uint64_t* rbar = reinterpret_cast<uint64_t*>(smem_raw + Cf::OFF_RB);  // partner slots, by parity
     if (threadIdx.x == 0) {
+        mbar_init(rbar, 1);
+        mbar_init(rbar + 1, 1);
         mbar_init(mbar, 1);
-        const char* src = static_cast<const char*>(a.wimg) + (size_t)tile.cls * a.wimg_stride * sizeof(double2) +
-                          (size_t)rank * Cf::HALF_BYTES;
+        const char* src = static_cast<const char*>(a.wimg) + (size_t)tile.cls * a.wimg_stride * sizeof(double2);
         constexpr uint32_t bytes = static_cast<uint32_t>(Cf::HALF_BYTES);
         mbar_expect_tx(mbar, bytes);
         for (uint32_t off = 0; off < bytes; off += 32768)
@@ -986,12 +1015,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) k2dcx_kernel
     for (int i = threadIdx.x; i < T; i += blockDim.x) twi[i] = a.twid_inv[i];
     __syncthreads();
     mbar_wait(mbar, 0);
-    cl.sync();  // both halves resident before any remote read
-    const double2* whalf0 = cl.map_shared_rank(reinterpret_cast<double2*>(smem_raw), 0);
-    const double2* whalf1 = cl.map_shared_rank(reinterpret_cast<double2*>(smem_raw), 1);
-    auto wrow = [&](int row) { return (row >= 64 ? whalf1 : whalf0) + (row & 63) * SR; };  // W row (either CTA)
+    cluster_bar();  // both CTAs staged and their receive barriers armed before any remote access
+    const double2* wimg = reinterpret_cast<const double2*>(smem_raw);
+    // W[r][c + j] for j = 0..16 as a (pointer, stride, conj sign) triple: rows > 64
+    // through W[r][c] = conj(W[128 - r][(128 - c) mod 128]), read backwards
+    struct WRun {
+        const double2* p;
+        int step;
+        double sg;
+    };
+    auto wrun = [&](int r, int c) {
+        if (r <= T / 2) return WRun{wimg + r * SR + c, 1, 1.0};
+        const int base = (T - 15 - c) & (T - 1);  // m_j = base + 15 - j (the padded columns cover + 15)
+        return WRun{wimg + (T - r) * SR + base + 15, -1, -1.0};
+    };
+    auto wat = [&](const WRun& w, int j) {
+        const double2 v = w.p[w.step * j];
+        return make_double2(v.x, w.sg * v.y);
+    };
     DSlot* slots = reinterpret_cast<DSlot*>(smem_raw + Cf::OFF_S);
-    DSlot* pslots = cl.map_shared_rank(slots, rank ^ 1);  // the partner's copy
+    const uint32_t pslots = dsm_map(slots, rank ^ 1);  // the partner's copy
+    const uint32_t prbar = dsm_map(rbar, rank ^ 1);    // and its receive barriers
+    uint32_t gi = 0;  // selections exchanged so far (all blocks): slot parity and barrier phase
     double* red = reinterpret_cast<double*>(smem_raw + Cf::OFF_RED);
 
     const int ltid = rank * Cf::CT + static_cast<int>(threadIdx.x);
@@ -1041,7 +1086,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) k2dcx_kernel
 
         const int nu_end = a.nu_limit > 0 ? a.nu_limit : nu + a.iterations;
         for (int it = 0; nu < nu_end && !conv; ++it) {
-            const int par = it & 1;
+            const int par = static_cast<int>(gi & 1u);
+            if (threadIdx.x == 0) mbar_expect_tx(rbar + par, Cf::XBYTES);  // the partner's 8 slots
             const unsigned long long K = KA > KB ? KA : KB;
             const unsigned hi = static_cast<unsigned>(K >> 32), lo = static_cast<unsigned>(K);
             const unsigned Mhi = __reduce_max_sync(0xffffffffu, hi);
@@ -1057,9 +1103,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) k2dcx_kernel
                 const double2 pre = dpick<NB>(g - gbase, re, im);
                 const DSlot ds{Mhi, Mlo, g, static_cast<int>(ws2), pre.x, pre.y};
                 slots[par * Cf::NWG + gw] = ds;
-                pslots[par * Cf::NWG + gw] = ds;
+                dsm_st_slot(pslots + static_cast<uint32_t>((par * Cf::NWG + gw) * sizeof(DSlot)), ds,
+                            prbar + 8u * par);
             }
-            cl.sync();  // one cluster barrier per selection
+            __syncthreads();                              // this CTA's slots
+            mbar_wait(rbar + par, (gi >> 1) & 1u);        // the partner's (st.async, no cluster fence)
+            ++gi;
             int wb = 0;
             {
                 uint2 kb = *reinterpret_cast<const uint2*>(&slots[par * Cf::NWG]);
@@ -1093,8 +1142,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) k2dcx_kernel
             const int G = s.g;
             const int u1 = G / T, u2 = G % T;
             const int self = ((T - u1) % T == u1) && ((T - u2) % T == u2);
-            const double2* wa = wrow((k1 - u1) & (T - 1)) + ((c0 - u2) & (T - 1));  // W[k-u] (DSMEM)
-            const double2* wb2 = wrow((k1 + u1) & (T - 1)) + ((c0 + u2) & (T - 1));  // W[k+u]
+            const int ca = (c0 - u2) & (T - 1), cb = (c0 + u2) & (T - 1);
+            const WRun wa = wrun((k1 - u1) & (T - 1), ca);  // W[k-u]
+            const WRun wb2 = wrun((k1 + u1) & (T - 1), cb);  // W[k+u]
             const double geff = a.gamma;
             const double p_re = pr * iw, p_im = pi * iw;
             const double c_re = p_re * geff, c_im = self ? 0.0 : p_im * geff;
@@ -1102,7 +1152,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) k2dcx_kernel
             if (self) {
                 delta = -2.0 * c_re * pr + c_re * c_re * w0;
             } else {
-                const double2 w2 = wrow((2 * u1) & (T - 1))[(2 * u2) & (T - 1)];
+                const double2 w2 = wat(wrun((2 * u1) & (T - 1), (2 * u2) & (T - 1)), 0);
                 const double cc_r = c_re * c_re - c_im * c_im, cc_i = 2.0 * c_re * c_im;
                 delta = -4.0 * (c_re * pr + c_im * pi) + 2.0 * (c_re * c_re + c_im * c_im) * w0 +
                         2.0 * (cc_r * w2.x + cc_i * w2.y);
@@ -1120,11 +1170,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) k2dcx_kernel
 #pragma unroll
             for (int j = 0; j < NB; ++j) {
                 if (j == SEG && !ex) break;
-                const double2 x = wa[j];
+                // the extra bin (j = SEG) of a mirrored run: column c + 16 wraps past base
+                const double2 x = (j == SEG && wa.step < 0) ? wat(wrun((k1 - u1) & (T - 1), (ca + SEG) & (T - 1)), 0)
+                                                            : wat(wa, j);
                 double r = fma(-c_re, x.x, fma(c_im, x.y, re[j]));
                 double m = fma(-c_re, x.y, fma(-c_im, x.x, im[j]));
                 if (!self) {
-                    const double2 y = wb2[j];
+                    const double2 y = (j == SEG && wb2.step < 0)
+                                          ? wat(wrun((k1 + u1) & (T - 1), (cb + SEG) & (T - 1)), 0)
+                                          : wat(wb2, j);
                     r = fma(-c_re, y.x, fma(-c_im, y.y, r));
                     m = fma(-c_re, y.y, fma(c_im, y.x, m));
                 }
@@ -1142,12 +1196,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) k2dcx_kernel
             for (int j = 0; j < SEG; ++j) R[j * NT + ltid] = make_double2(re[j], im[j]);
             if (ex) R[SEG * NT + ltid] = make_double2(re[SEG], im[SEG]);
         }
-        cl.sync();  // records visible; the pair leaves the block's remote reads together
+        __syncthreads();  // thread 0's records visible to CTA 0's synthesis
         if (rank == 0)
             v2_finish<T, Cf::CT, double2>(a, a.blocks[pos], pos, b, ltid, energy, nu, conv, flagged, ntrace, rec_u,
                                           rec_c, rstride, twi, red, 1);
-        cl.sync();
+        __syncthreads();
     }
+    cluster_bar();  // neither CTA leaves while the other may still read its shared memory
 }
 
 static int k2dcx_launch(const K2Args& a, int32_t ntiles, cudaStream_t s) {

@@ -4,7 +4,7 @@ name=$1; A=$2; B=$3; reps=${4:-3}
 for r in $(seq $reps); do
   for v in A B; do
     if [ $v = A ]; then E=$A; else E=$B; fi
-    env $E timeout 600 python bench.py --no-cpu-baseline --no-parity --no-fp64 --steps 5 --warmup 3 > gpurun_out/ab_${name}_${v}_$r.json 2>/dev/null
+    env $E timeout 600 python bench.py --workload ${WORKLOAD:-C4} --no-cpu-baseline --no-parity --no-fp64 --steps 5 --warmup 3 > gpurun_out/ab_${name}_${v}_$r.json 2>/dev/null
     python -c "
 import json,sys
 d=json.loads(open('gpurun_out/ab_${name}_${v}_$r.json').read().strip().splitlines()[-1])
