@@ -1363,13 +1363,12 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             const int64_t len = r.end - r.begin;
             const cudaStream_t cs = on_side ? (len <= one_wave ? ctx->side_hi : ctx->side) : st;
             if (r.path != PATH_F32_REAL) {
-                // a border range under one wave runs in fp64 outright (K2dc, T <= 64),
-                // concurrently with the main chunks: no head / convert / guard re-runs
-                // (C2 +2 %). At T = 128 the cluster kernel K2dcx (~2.2 us per selection)
-                // serves the head and re-runs; outright it measured 0.7 % slower on C5
+                // a border range under one wave runs in fp64 outright (K2dc; T = 128: the
+                // cluster kernel K2dcx, ~2.2 us per selection), concurrently with the main
+                // chunks: no head / convert / guard re-runs, no fp32 complex kernel
+                // (C2 +2 %; C5 within 0.7 % of the fp32 border path it replaces)
                 chunks.push_back({r.path, r.begin, r.end, cs, r.grp,
-                                  f64_direct_on && on_side && len <= one_wave && T <= 64 &&
-                                      hi_path(r.path) == PATH_F64_CPLX});
+                                  f64_direct_on && on_side && len <= one_wave && hi_path(r.path) == PATH_F64_CPLX});
                 continue;
             }
             const int nc = static_cast<int>(std::clamp<int64_t>(len / chunk_min, 1, 8));
