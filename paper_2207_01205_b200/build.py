@@ -19,7 +19,7 @@ OBJ = os.path.join(PKG, "_build")
 LIB_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIB_DIR, "libfofse.so")
 
-SOURCES = ["kernels.cu", "kernels_v2.cu", "kernels_f64.cu", "kernels_k1.cu", "kernels_exact.cu", "kernels_dct.cu", "engine.cpp", "microbench.cu"]
+SOURCES = ["kernels.cu", "kernels_v2.cu", "kernels_f64.cu", "kernels_k1.cu", "kernels_exact.cu", "kernels_dct.cu", "kernels_generic.cu", "engine.cpp", "microbench.cu"]
 HEADERS = ["kernels.h", "layout.h", "kcommon.cuh", "v2common.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "nvcc")

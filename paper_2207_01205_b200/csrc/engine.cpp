@@ -337,13 +337,18 @@ void validate_config(const Cfg& c) {
         throw std::invalid_argument("config: basis must be FOFSE_BASIS_DFT or FOFSE_BASIS_DCT");
 }
 
+// T in {8, 16, 32, 64, 128}: the specialised kernels; any other T <= 512 runs the
+// generic path (DFT: kernels_generic.cu; DCT: kernels_dct.cu takes every T)
+bool specialised_T(int T) { return T == 8 || T == 16 || T == 32 || T == 64 || T == 128; }
+
 void check_gpu_support(const Cfg& c) {
-    if (c.basis == FOFSE_BASIS_DCT) {  // the spatial engine takes any T (kernels_dct.cu)
-        if (c.T > 512) throw Unsupported("transform_size must be <= 512 for the DCT basis on the GPU path");
-        return;
-    }
-    if (!(c.T == 8 || c.T == 16 || c.T == 32 || c.T == 64 || c.T == 128))
-        throw Unsupported("transform_size must be a power of two in [8, 128] on the GPU path");
+    if (c.T > 512) throw Unsupported("transform_size must be <= 512 on the GPU path");
+}
+
+// the engine-level API (fofse_spectral_*) exchanges the specialised layouts
+void check_engine_support(const Cfg& c) {
+    if (!specialised_T(c.T))
+        throw Unsupported("the engine-level API supports transform sizes 8, 16, 32, 64 and 128 on the GPU path");
 }
 
 double effective_gamma(const Cfg& c) { return c.algorithm == FOFSE_ALGO_FSE ? 1.0 : c.gamma; }
@@ -883,6 +888,76 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             a.trace_count = d_trace_count;
             a.trace_stride = I;
             ck(ks_launch(a, st), "KS spatial DCT engine");
+            ++ctx->launches;
+        }
+        ck(cudaEventRecord(ctx->ev[2], st), "event");
+        ck(cudaEventRecord(ctx->ev[3], st), "event");
+        if (gio)
+            for (int gq = 0; gq < job.groups; ++gq) gio->on_done(gq, st);
+        ck(cudaEventSynchronize(ctx->ev[3]), "sync");
+        float ms = 0;
+        ck(cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[3]), "elapsed");
+        out.total_ms = ms;
+        ck(cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]), "elapsed");
+        out.init_ms = ms;
+        out.iter_ms = out.total_ms - out.init_ms;
+        return out;
+    }
+    if (!specialised_T(T)) {
+        // ---- DFT at a transform size without specialised kernels: the generic path
+        // in the reference's arithmetic (kernels_generic.cu), fp64, every block ----
+        const NvtxRange nv("fofse::generic-T spectral engine");
+        if (ckpts) throw Unsupported("PSNR curves need a transform size of 8, 16, 32, 64 or 128");
+        const auto twf = twiddles(T, -1), twi = twiddles(T, +1);
+        const double2* d_twf = upload(ctx, "twf", twf.data(), twf.size());
+        const double2* d_twi = upload(ctx, "twi", twi.data(), twi.size());
+        const double* d_w = upload(ctx, "wcls", wcls.data(), wcls.size());
+        const BlockDesc* d_bl = upload(ctx, "kg_blocks", job.blocks.data(), job.blocks.size());
+        std::vector<int32_t> idv(static_cast<size_t>(n));
+        for (int64_t i = 0; i < n; ++i) idv[static_cast<size_t>(i)] = static_cast<int32_t>(i);
+        const int32_t* d_idv = upload(ctx, "kg_ids", idv.data(), idv.size());
+        int32_t* d_ru = ctx->buf("rec_u").as<int32_t>(static_cast<size_t>(std::max<int64_t>(n, 1)) * std::max(I, 1));
+        double2* d_rc = ctx->buf("rec_c").as<double2>(static_cast<size_t>(std::max<int64_t>(n, 1)) * std::max(I, 1));
+        if (gio)
+            for (int gq = 0; gq < job.groups; ++gq) {
+                gio->ensure_h2d(gq);
+                ck(cudaStreamWaitEvent(st, gio->h2d_done[static_cast<size_t>(gq)], 0), "wait");
+            }
+        ck(cudaEventRecord(ctx->ev[1], st), "event");
+        const size_t per = kg_scratch_complex(T);
+        const int64_t chunk = std::clamp<int64_t>(static_cast<int64_t>((size_t(1) << 30) / (per * sizeof(double2))), 1, 1024);
+        double2* d_scr = ctx->buf("kg_scr").as<double2>(static_cast<size_t>(std::min(chunk, std::max<int64_t>(n, 1))) * per);
+        const bool img_region = synth == SYN_IMAGE || synth == SYN_ERR;
+        for (int64_t b0 = 0; b0 < n; b0 += chunk) {
+            KgArgs a{};
+            a.T = T;
+            a.Lh = g.Lh;
+            a.Lw = g.Lw;
+            a.n = static_cast<int32_t>(std::min(chunk, n - b0));
+            a.blocks = d_bl + b0;
+            a.order = d_idv + b0;
+            a.fr = fr;
+            a.wcls = d_w;
+            a.twid = d_twf;
+            a.twid_inv = d_twi;
+            a.iterations = I;
+            a.full_od = full_od(cfg) ? 1 : 0;
+            a.gamma = effective_gamma(cfg);
+            a.scratch = d_scr;
+            a.rec_u = d_ru;
+            a.rec_c = d_rc;
+            a.synth = synth;
+            a.reg_r0 = img_region ? g.S : 0;
+            a.reg_c0 = img_region ? g.S : 0;
+            a.reg_nr = img_region ? g.bh : g.Lh;
+            a.reg_nc = img_region ? g.bw : g.Lw;
+            a.models = d_models;
+            a.block_sq = d_block_sq;
+            a.trace = d_trace;
+            a.trace_count = d_trace_count;
+            a.trace_stride = I;
+            a.conv_out = nullptr;
+            ck(kg_launch(a, st), "KG generic-T engine");
             ++ctx->launches;
         }
         ck(cudaEventRecord(ctx->ev[2], st), "event");
@@ -2644,7 +2719,7 @@ int fofse_spectral_init(fofse_ctx* ctx, const double* f, const uint8_t* labels,
         Cfg c{};
         c.T = t;
         c.algorithm = FOFSE_ALGO_FOFSE;
-        check_gpu_support(c);
+        check_engine_support(c);
         ctx->activate();
         const size_t L = static_cast<size_t>(h) * w;
         // per-spectrum class = its own weight field masked by SUPPORT
@@ -2711,7 +2786,7 @@ static int spectral_iterate_impl(fofse_ctx* ctx, int32_t t, int64_t n, int32_t w
         Cfg c{};
         c.T = t;
         c.algorithm = FOFSE_ALGO_FOFSE;
-        check_gpu_support(c);
+        check_engine_support(c);
         if (precision != FOFSE_PREC_FP64 && precision != FOFSE_PREC_FP32)
             throw std::invalid_argument("precision must be FOFSE_PREC_FP64 or FOFSE_PREC_FP32");
         ctx->activate();
@@ -2920,7 +2995,7 @@ int fofse_spectral_synthesize(fofse_ctx* ctx, int32_t t, int64_t n, const double
         Cfg c{};
         c.T = t;
         c.algorithm = FOFSE_ALGO_FOFSE;
-        check_gpu_support(c);
+        check_engine_support(c);
         if (h > t || w > t) throw std::invalid_argument("synthesize: window exceeds the transform grid");
         ctx->activate();
         const size_t tt = static_cast<size_t>(t) * t;

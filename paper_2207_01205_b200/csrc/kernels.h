@@ -199,6 +199,33 @@ struct DctArgs {
 size_t ks_scratch_doubles(int T);
 int ks_launch(const DctArgs& a, cudaStream_t s);
 
+// KG: the DFT path for any transform size (kernels_generic.cu), reference op order.
+struct KgArgs {
+    int32_t T, Lh, Lw, n;
+    const BlockDesc* blocks;    // by position
+    const int32_t* order;       // position -> caller id
+    Frames fr;
+    const double* wcls;         // [ncls][Lh*Lw]
+    const double2* twid;        // e^{-j 2 pi k / T} (host libm, the stand-in's table)
+    const double2* twid_inv;    // e^{+j 2 pi k / T}
+    int32_t iterations;
+    int32_t full_od;            // OFSE (gamma_eff from d = sum R W)
+    double gamma;               // effective gamma (1 for fse)
+    double2* scratch;           // [n][kg_scratch_complex(T)]
+    int32_t* rec_u;             // [id][iterations]
+    double2* rec_c;             // [id][iterations]
+    int32_t synth;              // SYN_IMAGE / SYN_WINDOW
+    int32_t reg_r0, reg_c0, reg_nr, reg_nc;
+    double* models;
+    double* block_sq;
+    fofse_record* trace;
+    int32_t* trace_count;
+    int32_t trace_stride;
+    int32_t* conv_out;
+};
+size_t kg_scratch_complex(int T);
+int kg_launch(const KgArgs& a, cudaStream_t s);
+
 struct CvtArgs {
     int32_t T, Lh, Lw, n;
     const double2* in;          // packed fp64 residuals (strict layout: seg_of(T, F64), SPT 1)
