@@ -763,12 +763,13 @@ bool f64_strict_forced() {
 // dominate the late-iteration residual).
 int resolve_head(const Cfg& c) {
     if (c.precision != FOFSE_PREC_FP32 || c.iterations <= 0) return 0;
-    // default: 8 selections for T <= 64, 16 for T = 128 — the shortest heads with
-    // which the guard (tau = 1e-5) catches every selection that leaves the fp64
-    // sequence (tools/divergence_study.py: head 4 misses 3 of 229 divergent C4
-    // blocks, head 8 none of 204; C5 head 8 misses 1 of 255, head 16 none of 233)
-    // and no block of the full-scale studies ends above 0.5 px
-    const int h = c.head >= 0 ? c.head : (c.T > 64 ? 16 : 8);
+    // default: 4 selections for T <= 32, 8 for T = 64, 16 for T = 128 — the shortest
+    // heads with which the guard (tau = 1e-5) catches every selection that leaves
+    // the fp64 sequence (tools/divergence_study.py: C3 head 4 misses none of 25
+    // divergent blocks; C4 head 4 misses 3 of 229, head 8 none of 204; C5 head 8
+    // misses 1 of 255, head 16 none of 233) and no block of the full-scale studies
+    // ends above 0.5 px
+    const int h = c.head >= 0 ? c.head : (c.T > 64 ? 16 : c.T > 32 ? 8 : 4);
     return std::min(h, c.iterations);
 }
 
