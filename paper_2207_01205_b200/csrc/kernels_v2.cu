@@ -80,10 +80,19 @@ __device__ __forceinline__ unsigned key_mask(const K2Args& a) {
 __device__ __forceinline__ float pkey(float m, int p, unsigned mask) {
     return __uint_as_float((__float_as_uint(m) & mask) | static_cast<unsigned>(63 - p));
 }
+// LO = false: the runner-up is tracked over the pairs' larger bins only; every
+// other pair's smaller bin is <= its larger one, so the global runner-up is the
+// larger of that and the WINNING pair's smaller bin, which the controller adds
+// from the spilled pair (one FMNMX per pair less in the scan)
+template <bool LO = true>
 __device__ __forceinline__ void kacc_pair(KAcc& A, float2 mp, int p, unsigned mask) {
-    const float hi = fmaxf(mp.x, mp.y), lo = fminf(mp.x, mp.y);
+    const float hi = fmaxf(mp.x, mp.y);
     const float k = pkey(hi, p, mask);
-    A.m2 = fmax3(A.m2, lo, fminf(k, A.m1));
+    if constexpr (LO) {
+        A.m2 = fmax3(A.m2, fminf(mp.x, mp.y), fminf(k, A.m1));
+    } else {
+        A.m2 = fmaxf(A.m2, fminf(k, A.m1));
+    }
     A.m1 = fmaxf(A.m1, k);
 }
 __device__ __forceinline__ void kacc_one(KAcc& A, float m, int p, unsigned mask) {
@@ -142,6 +151,7 @@ __global__ void __launch_bounds__(128, VAR == 0 ? 3 : 2) k2v2r_kernel(K2Args a) 
     // VAR 9: diagnostic — the update + scan alone (one REDUX, synthetic selections).
     // The next scan is fused into the update in every variant.
     constexpr int ACC = VAR == 0 ? 2 : 4;  // independent argmax chains
+    constexpr bool LO = false;  // the winning pair's smaller bin is added in the controller
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const Tile tile = a.tiles[blockIdx.x];
@@ -222,7 +232,7 @@ __global__ void __launch_bounds__(128, VAR == 0 ? 3 : 2) k2v2r_kernel(K2Args a) 
 #pragma unroll
         for (int k = 0; k <= ACC; ++k) A[k] = KAcc{0.f, 0.f};
 #pragma unroll
-        for (int p = 0; p < NP; ++p) kacc_pair(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+        for (int p = 0; p < NP; ++p) kacc_pair<LO>(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
 #pragma unroll
         for (int s = 0; s < SPT; ++s)
             if (exs[s]) kacc_one(A[ACC], fmaf(xi[s], xi[s], xr[s] * xr[s]), NP + s, kmask);
@@ -259,10 +269,12 @@ __global__ void __launch_bounds__(128, VAR == 0 ? 3 : 2) k2v2r_kernel(K2Args a) 
             __syncwarp();
             float2 pre;
             int jw, sw;
+            float lo_w = 0.f;  // LO = false: the winning pair's smaller bin
             {
                 const float4 q = spill[0];
                 if (pw < NP) {
                     const float ma = fmaf(q.z, q.z, q.x * q.x), mb = fmaf(q.w, q.w, q.y * q.y);
+                    lo_w = fminf(ma, mb);
                     const int half = mb > ma ? 1 : 0;  // ties to the lower column
                     pre = half ? make_float2(q.y, q.w) : make_float2(q.x, q.z);
                     sw = pw / PPS;
@@ -277,7 +289,7 @@ __global__ void __launch_bounds__(128, VAR == 0 ? 3 : 2) k2v2r_kernel(K2Args a) 
 
             // ---- scalar part of iterate (engine_spectral.cpp:58-110), fp32 (the
             // update it feeds is fp32); the energy bookkeeping accumulates in fp64 ----
-            const float Mf = __uint_as_float(M), Sf = __uint_as_float(S);
+            const float Mf = __uint_as_float(M), Sf = fmaxf(__uint_as_float(S), lo_w);
             const double energy = st->energy;
             const float w0 = st->w0, gw = st->gw;
             if (energy < st->thr_e || !(Mf > 0.f) || Mf < st->thr_m) {
@@ -364,8 +376,8 @@ __global__ void __launch_bounds__(128, VAR == 0 ? 3 : 2) k2v2r_kernel(K2Args a) 
                             ip[p] = __ffma2_rn(n1i, make_float2(x.x, x.y), ip[p]);
                             rp[p + 1] = __ffma2_rn(n1r, make_float2(x.z, x.w), rp[p + 1]);
                             ip[p + 1] = __ffma2_rn(n1i, make_float2(x.z, x.w), ip[p + 1]);
-                            kacc_pair(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
-                            kacc_pair(A[(p + 1) % ACC], __ffma2_rn(ip[p + 1], ip[p + 1], __fmul2_rn(rp[p + 1], rp[p + 1])),
+                            kacc_pair<LO>(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+                            kacc_pair<LO>(A[(p + 1) % ACC], __ffma2_rn(ip[p + 1], ip[p + 1], __fmul2_rn(rp[p + 1], rp[p + 1])),
                                       p + 1, kmask);
                         }
                     } else {
@@ -377,8 +389,8 @@ __global__ void __launch_bounds__(128, VAR == 0 ? 3 : 2) k2v2r_kernel(K2Args a) 
                             ip[p] = __ffma2_rn(n2i, make_float2(y.x, y.y), __ffma2_rn(n1i, make_float2(x.x, x.y), ip[p]));
                             rp[p + 1] = __ffma2_rn(n2r, make_float2(y.z, y.w), __ffma2_rn(n1r, make_float2(x.z, x.w), rp[p + 1]));
                             ip[p + 1] = __ffma2_rn(n2i, make_float2(y.z, y.w), __ffma2_rn(n1i, make_float2(x.z, x.w), ip[p + 1]));
-                            kacc_pair(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
-                            kacc_pair(A[(p + 1) % ACC], __ffma2_rn(ip[p + 1], ip[p + 1], __fmul2_rn(rp[p + 1], rp[p + 1])),
+                            kacc_pair<LO>(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+                            kacc_pair<LO>(A[(p + 1) % ACC], __ffma2_rn(ip[p + 1], ip[p + 1], __fmul2_rn(rp[p + 1], rp[p + 1])),
                                       p + 1, kmask);
                         }
                     }
@@ -389,7 +401,7 @@ __global__ void __launch_bounds__(128, VAR == 0 ? 3 : 2) k2v2r_kernel(K2Args a) 
                         const float2 x = va[q];
                         rp[p] = __ffma2_rn(n1r, x, rp[p]);
                         ip[p] = __ffma2_rn(n1i, x, ip[p]);
-                        kacc_pair(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+                        kacc_pair<LO>(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
                     }
                 } else {
 #pragma unroll
@@ -398,7 +410,7 @@ __global__ void __launch_bounds__(128, VAR == 0 ? 3 : 2) k2v2r_kernel(K2Args a) 
                         const float2 x = va[q], y = vb[q];
                         rp[p] = __ffma2_rn(n2r, y, __ffma2_rn(n1r, x, rp[p]));
                         ip[p] = __ffma2_rn(n2i, y, __ffma2_rn(n1i, x, ip[p]));
-                        kacc_pair(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+                        kacc_pair<LO>(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
                     }
                 }
                 if (exs[s]) {
@@ -549,7 +561,7 @@ __global__ void __launch_bounds__(V2HCfg<T>::THREADS, V2HCfg<T>::MINB) k2v2h_ker
 #pragma unroll
         for (int k = 0; k <= ACC; ++k) A[k] = KAcc{0.f, 0.f};
 #pragma unroll
-        for (int p = 0; p < NP; ++p) kacc_pair(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+        for (int p = 0; p < NP; ++p) kacc_pair<false>(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
         if (ex) kacc_one(A[ACC], fmaf(xi, xi, xr * xr), NP, kmask);
 
         for (int it = 0; it < a.iterations && !conv; ++it) {
@@ -590,13 +602,14 @@ __global__ void __launch_bounds__(V2HCfg<T>::THREADS, V2HCfg<T>::MINB) k2v2h_ker
             }
             const HSlot& sw = slots[par * GW + wsel];
             const float Mf = __uint_as_float(M);
-            const float Sf = fmaxf(sw.second, __uint_as_float(S2));
             const int pw = 63 - static_cast<int>(M & 63u);
             float2 pre;
             int jw;
+            float lo_w = 0.f;  // the winning pair's smaller bin (kacc_pair<false>)
             if (pw < NP) {
                 const float4 q = sw.pair;
                 const float ma = fmaf(q.z, q.z, q.x * q.x), mb = fmaf(q.w, q.w, q.y * q.y);
+                lo_w = fminf(ma, mb);
                 const int half = mb > ma ? 1 : 0;  // ties to the lower column
                 pre = half ? make_float2(q.y, q.w) : make_float2(q.x, q.z);
                 jw = 2 * pw + half;
@@ -611,6 +624,7 @@ __global__ void __launch_bounds__(V2HCfg<T>::THREADS, V2HCfg<T>::MINB) k2v2h_ker
                 conv = 1;
                 break;
             }
+            const float Sf = fmaxf(fmaxf(sw.second, __uint_as_float(S2)), lo_w);
             if (Sf > Mf * tau1) {
                 flagged = 1 + nu;  // near-tie: the host re-runs this block in fp64
                 break;
@@ -686,8 +700,8 @@ __global__ void __launch_bounds__(V2HCfg<T>::THREADS, V2HCfg<T>::MINB) k2v2h_ker
                     ip[p] = __ffma2_rn(n1i, make_float2(x.x, x.y), ip[p]);
                     rp[p + 1] = __ffma2_rn(n1r, make_float2(x.z, x.w), rp[p + 1]);
                     ip[p + 1] = __ffma2_rn(n1i, make_float2(x.z, x.w), ip[p + 1]);
-                    kacc_pair(A[0], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
-                    kacc_pair(A[1], __ffma2_rn(ip[p + 1], ip[p + 1], __fmul2_rn(rp[p + 1], rp[p + 1])), p + 1, kmask);
+                    kacc_pair<false>(A[0], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+                    kacc_pair<false>(A[1], __ffma2_rn(ip[p + 1], ip[p + 1], __fmul2_rn(rp[p + 1], rp[p + 1])), p + 1, kmask);
                 }
             } else {
 #pragma unroll
@@ -698,8 +712,8 @@ __global__ void __launch_bounds__(V2HCfg<T>::THREADS, V2HCfg<T>::MINB) k2v2h_ker
                     ip[p] = __ffma2_rn(n2i, make_float2(y.x, y.y), __ffma2_rn(n1i, make_float2(x.x, x.y), ip[p]));
                     rp[p + 1] = __ffma2_rn(n2r, make_float2(y.z, y.w), __ffma2_rn(n1r, make_float2(x.z, x.w), rp[p + 1]));
                     ip[p + 1] = __ffma2_rn(n2i, make_float2(y.z, y.w), __ffma2_rn(n1i, make_float2(x.z, x.w), ip[p + 1]));
-                    kacc_pair(A[0], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
-                    kacc_pair(A[1], __ffma2_rn(ip[p + 1], ip[p + 1], __fmul2_rn(rp[p + 1], rp[p + 1])), p + 1, kmask);
+                    kacc_pair<false>(A[0], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+                    kacc_pair<false>(A[1], __ffma2_rn(ip[p + 1], ip[p + 1], __fmul2_rn(rp[p + 1], rp[p + 1])), p + 1, kmask);
                 }
             }
             if (ex) {
@@ -849,7 +863,7 @@ __global__ void __launch_bounds__(128, 3) k2v2c_kernel(K2Args a) {
 #pragma unroll
         for (int k = 0; k <= ACC; ++k) A[k] = KAcc{0.f, 0.f};
 #pragma unroll
-        for (int p = 0; p < NP; ++p) kacc_pair(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+        for (int p = 0; p < NP; ++p) kacc_pair<false>(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
 #pragma unroll
         for (int s = 0; s < SPT; ++s)
             if (exs[s]) kacc_one(A[ACC], fmaf(xi[s], xi[s], xr[s] * xr[s]), NP + s, kmask);
@@ -871,10 +885,12 @@ __global__ void __launch_bounds__(128, 3) k2v2c_kernel(K2Args a) {
             __syncwarp();
             float2 pre;
             int jw, sw;
+            float lo_w = 0.f;  // the winning pair's smaller bin (kacc_pair<false>)
             {
                 const float4 q = spill[0];
                 if (pw < NP) {
                     const float ma = fmaf(q.z, q.z, q.x * q.x), mb = fmaf(q.w, q.w, q.y * q.y);
+                    lo_w = fminf(ma, mb);
                     const int half = mb > ma ? 1 : 0;
                     pre = half ? make_float2(q.y, q.w) : make_float2(q.x, q.z);
                     sw = pw / PPS;
@@ -888,7 +904,7 @@ __global__ void __launch_bounds__(128, 3) k2v2c_kernel(K2Args a) {
             const int G = __shfl_sync(0xffffffffu, (SPT == 2 && sw == 1) ? gb1 : gb0, wl) + jw;
 
             // ---- scalar part of iterate (engine_spectral.cpp:58-110), fp32; energy in fp64 ----
-            const float Mf = __uint_as_float(M), Sf = __uint_as_float(S);
+            const float Mf = __uint_as_float(M), Sf = fmaxf(__uint_as_float(S), lo_w);
             const double energy = st->energy;
             const float w0 = st->w0, gw = st->gw;
             if (energy < st->thr_e || !(Mf > 0.f) || Mf < st->thr_m) {
@@ -964,7 +980,7 @@ __global__ void __launch_bounds__(128, 3) k2v2c_kernel(K2Args a) {
                             const float2 xr2 = ld(far, q), xi2 = ld(fai, q);
                             rp[p] = __ffma2_rn(ncr, xr2, __ffma2_rn(pci, xi2, rp[p]));
                             ip[p] = __ffma2_rn(ncr, xi2, __ffma2_rn(nci, xr2, ip[p]));
-                            kacc_pair(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+                            kacc_pair<false>(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
                         }
                     } else {
 #pragma unroll
@@ -973,7 +989,7 @@ __global__ void __launch_bounds__(128, 3) k2v2c_kernel(K2Args a) {
                             const float2 xr2 = ld(far, q), xi2 = ld(fai, q), yr2 = ld(fbr, q), yi2 = ld(fbi, q);
                             rp[p] = __ffma2_rn(nci, yi2, __ffma2_rn(ncr, yr2, __ffma2_rn(pci, xi2, __ffma2_rn(ncr, xr2, rp[p]))));
                             ip[p] = __ffma2_rn(pci, yr2, __ffma2_rn(ncr, yi2, __ffma2_rn(nci, xr2, __ffma2_rn(ncr, xi2, ip[p]))));
-                            kacc_pair(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+                            kacc_pair<false>(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
                         }
                     }
                 } else if (self) {
@@ -983,7 +999,7 @@ __global__ void __launch_bounds__(128, 3) k2v2c_kernel(K2Args a) {
                         const float2 xr2 = ar[q], xi2 = ai[q];
                         rp[p] = __ffma2_rn(ncr, xr2, __ffma2_rn(pci, xi2, rp[p]));
                         ip[p] = __ffma2_rn(ncr, xi2, __ffma2_rn(nci, xr2, ip[p]));
-                        kacc_pair(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+                        kacc_pair<false>(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
                     }
                 } else {
 #pragma unroll
@@ -992,7 +1008,7 @@ __global__ void __launch_bounds__(128, 3) k2v2c_kernel(K2Args a) {
                         const float2 xr2 = ar[q], xi2 = ai[q], yr2 = br[q], yi2 = bi[q];
                         rp[p] = __ffma2_rn(nci, yi2, __ffma2_rn(ncr, yr2, __ffma2_rn(pci, xi2, __ffma2_rn(ncr, xr2, rp[p]))));
                         ip[p] = __ffma2_rn(pci, yr2, __ffma2_rn(ncr, yi2, __ffma2_rn(nci, xr2, __ffma2_rn(ncr, xi2, ip[p]))));
-                        kacc_pair(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+                        kacc_pair<false>(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
                     }
                 }
                 if (exs[s]) {
