@@ -1290,13 +1290,25 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             const double tau64 = fp64_tie_tau(cfg);
             int32_t* d_tie = tau64 > 0.0 ? ctx->buf("tie").as<int32_t>(static_cast<size_t>(n)) : nullptr;
             if (d_tie) ck(cudaMemsetAsync(d_tie, 0, sizeof(int32_t) * n, st), "memset");
+            // the ranges (interior / border paths) are independent: the first on the
+            // main stream, the others concurrently on the side streams (C1: the
+            // border K2dc no longer waits for the interior K2d), joined before the
+            // tie flags are read
+            const cudaStream_t rs[3] = {st, ctx->side, ctx->side_hi};
+            ck(cudaEventRecord(ctx->event(0), st), "event");
+            for (size_t i = 1; i < std::min<size_t>(ranges.size(), 3); ++i)
+                ck(cudaStreamWaitEvent(rs[i], ctx->event(0), 0), "wait");
             for (size_t i = 0; i < ranges.size(); ++i) {
                 const bool w = range_wide(ranges[i]);
                 K2Args ar = a;
                 if (w) ar.rin = d_R64w;
                 ar.flags = d_tie;
-                k2_f64(ar, hi_path(ranges[i].path), ranges[i].begin, ranges[i].end, sorted, std::to_string(i), st,
-                       nullptr, 0, w, tau64);
+                k2_f64(ar, hi_path(ranges[i].path), ranges[i].begin, ranges[i].end, sorted, std::to_string(i),
+                       rs[i % 3], nullptr, 0, w, tau64);
+            }
+            for (size_t i = 1; i < std::min<size_t>(ranges.size(), 3); ++i) {
+                ck(cudaEventRecord(ctx->event(i), rs[i]), "event");
+                ck(cudaStreamWaitEvent(st, ctx->event(i), 0), "wait");
             }
             if (d_tie) {
                 // ---- near-tie blocks: the exact path (K1x + strict kernel, hypot argmax) ----
