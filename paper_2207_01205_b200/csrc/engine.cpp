@@ -802,6 +802,9 @@ struct GroupIO {
     // on the copy engine
     std::function<void(int)> ensure_h2d;
     std::function<void(int, cudaStream_t)> on_done;
+    // the rectangle (frame, row, col, rows, cols) was rewritten after its group's
+    // download: copy it again on stream s
+    std::function<void(int32_t, int32_t, int32_t, int32_t, int32_t, cudaStream_t)> on_patch;
 };
 
 // Device run of a job. fr: source (and destination) frames on device.
@@ -1128,7 +1131,10 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
     const int ngroups = job.groups;
     for (const Range& r : ranges)
         if (r.path == PATH_F32_REAL || r.path == PATH_F64_REAL) out.real_blocks += r.end - r.begin;
-    if (gio && !fp32)
+    // fp64 frames API: each group's K1 waits for its own upload and its download
+    // follows its last iteration launch (the copies overlap the kernels)
+    const bool f64_pipe = gio && !fp32 && !ckpts && ngroups > 1;
+    if (gio && !fp32 && !f64_pipe)
         for (int gq = 0; gq < ngroups; ++gq)
         {
             gio->ensure_h2d(gq);
@@ -1229,20 +1235,47 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
     }
     char* d_R64w = f64_wide ? ctx->buf("R64w").as<char>(static_cast<size_t>(n) * r64w_bytes) : nullptr;
     auto range_wide = [&](const Range& r) { return f64_wide && hi_path(r.path) == PATH_F64_REAL; };
-    if (!fp32) {
-        for (const Range& r : ranges) {
-            const bool w = range_wide(r);
-            k1_packed(d_sorted + r.begin, r.end - r.begin, hi_path(r.path), w ? k2d_wide_seg(T) : seg64, 1,
-                      w ? d_R64w + static_cast<size_t>(r.begin) * r64w_bytes
-                        : d_R64 + static_cast<size_t>(r.begin) * r64_bytes,
-                      d_e0 + r.begin, d_imax + r.begin);
-        }
-    }
-    // one fp64 iteration launch over positions [b0, b1) of `descs` (K2d or strict)
     auto ng_f64 = [&](int hp, bool wide = false) {
         return (hp == PATH_F64_REAL || hp == PATH_F64_CPLX) ? k2d_blocks_per_cta(T, wide && hp == PATH_F64_REAL)
                                                             : k2_groups_per_cta(T, PATH_F64_STRICT);
     };
+    // f64_pipe: every range's tile list in one upload, enqueued before the later
+    // groups' frames so that it is not queued behind them on the copy engine;
+    // K1 on the `pre` stream, range by range, [ev_k1f + i] after range i's K1
+    std::vector<size_t> pipe_toff;
+    const Tile* d_pipe_tiles = nullptr;
+    const size_t ev_k1f = 8, ev_k2f = 8 + ranges.size();
+    if (f64_pipe) {
+        std::vector<Tile> all;
+        for (const Range& r : ranges) {
+            pipe_toff.push_back(all.size());
+            const std::vector<Tile> tl = make_tiles(r.begin, r.end, sorted, ng_f64(hi_path(r.path), range_wide(r)));
+            all.insert(all.end(), tl.begin(), tl.end());
+        }
+        pipe_toff.push_back(all.size());
+        d_pipe_tiles = upload(ctx, "tiles64pipe", all.data(), all.size());
+        ck(cudaEventRecord(ctx->event(0), st), "event");
+        ck(cudaStreamWaitEvent(ctx->pre, ctx->event(0), 0), "wait");
+    }
+    if (!fp32) {
+        const cudaStream_t ks = f64_pipe ? ctx->pre : st;
+        int waited = -1;
+        for (size_t i = 0; i < ranges.size(); ++i) {
+            const Range& r = ranges[i];
+            if (f64_pipe && r.grp != waited) {
+                gio->ensure_h2d(r.grp);
+                ck(cudaStreamWaitEvent(ks, gio->h2d_done[static_cast<size_t>(r.grp)], 0), "wait");
+                waited = r.grp;
+            }
+            const bool w = range_wide(r);
+            k1_packed(d_sorted + r.begin, r.end - r.begin, hi_path(r.path), w ? k2d_wide_seg(T) : seg64, 1,
+                      w ? d_R64w + static_cast<size_t>(r.begin) * r64w_bytes
+                        : d_R64 + static_cast<size_t>(r.begin) * r64_bytes,
+                      d_e0 + r.begin, d_imax + r.begin, 0, 0, ks);
+            if (f64_pipe) ck(cudaEventRecord(ctx->event(ev_k1f + i), ks), "event");
+        }
+    }
+    // one fp64 iteration launch over positions [b0, b1) of `descs` (K2d or strict)
     // pre: tiles already on the device (the chunk pipeline uploads all of its tile
     // lists in one copy up front)
     auto k2_f64 = [&](K2Args a, int hp, int64_t b0, int64_t b1, const std::vector<BlockDesc>& descs,
@@ -1282,7 +1315,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
     if (!fp32) {
         // ---- fp64: K2d (symmetric masks) / strict kernel, every block ----
         const NvtxRange nv("fofse::fp64 iterate");
-        ck(cudaEventRecord(ctx->ev[1], st), "event");
+        ck(cudaEventRecord(ctx->ev[1], f64_pipe ? ctx->pre : st), "event");
         K2Args a = base_args();
         a.rin = d_R64;
         a.rec_global = 0;
@@ -1290,21 +1323,41 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             const double tau64 = fp64_tie_tau(cfg);
             int32_t* d_tie = tau64 > 0.0 ? ctx->buf("tie").as<int32_t>(static_cast<size_t>(n)) : nullptr;
             if (d_tie) ck(cudaMemsetAsync(d_tie, 0, sizeof(int32_t) * n, st), "memset");
+            if (f64_pipe) {
+                ck(cudaEventRecord(ctx->event(3), st), "event");
+                for (cudaStream_t x : {ctx->side, ctx->side_hi}) ck(cudaStreamWaitEvent(x, ctx->event(3), 0), "wait");
+            }
             // the ranges (interior / border paths) are independent: the first on the
             // main stream, the others concurrently on the side streams (C1: the
             // border K2dc no longer waits for the interior K2d), joined before the
             // tie flags are read
             const cudaStream_t rs[3] = {st, ctx->side, ctx->side_hi};
-            ck(cudaEventRecord(ctx->event(0), st), "event");
-            for (size_t i = 1; i < std::min<size_t>(ranges.size(), 3); ++i)
-                ck(cudaStreamWaitEvent(rs[i], ctx->event(0), 0), "wait");
+            if (!f64_pipe) {
+                ck(cudaEventRecord(ctx->event(0), st), "event");
+                for (size_t i = 1; i < std::min<size_t>(ranges.size(), 3); ++i)
+                    ck(cudaStreamWaitEvent(rs[i], ctx->event(0), 0), "wait");
+            }
             for (size_t i = 0; i < ranges.size(); ++i) {
                 const bool w = range_wide(ranges[i]);
                 K2Args ar = a;
                 if (w) ar.rin = d_R64w;
                 ar.flags = d_tie;
-                k2_f64(ar, hi_path(ranges[i].path), ranges[i].begin, ranges[i].end, sorted, std::to_string(i),
-                       rs[i % 3], nullptr, 0, w, tau64);
+                const cudaStream_t s = rs[i % 3];
+                if (f64_pipe) ck(cudaStreamWaitEvent(s, ctx->event(ev_k1f + i), 0), "wait");
+                k2_f64(ar, hi_path(ranges[i].path), ranges[i].begin, ranges[i].end, sorted, std::to_string(i), s,
+                       f64_pipe ? d_pipe_tiles + pipe_toff[i] : nullptr,
+                       f64_pipe ? pipe_toff[i + 1] - pipe_toff[i] : 0, w, tau64);
+                if (f64_pipe) {
+                    ck(cudaEventRecord(ctx->event(ev_k2f + i), s), "event");
+                    const int gq = ranges[i].grp;
+                    if (i + 1 == ranges.size() || ranges[i + 1].grp != gq) {
+                        // the group's ranges done (and, by stream order, the earlier groups'):
+                        // its download; near-tie blocks are patched after their re-run
+                        for (size_t j = i + 1; j-- > 0 && ranges[j].grp == gq;)
+                            ck(cudaStreamWaitEvent(ctx->io, ctx->event(ev_k2f + j), 0), "wait");
+                        gio->on_done(gq, ctx->io);
+                    }
+                }
             }
             for (size_t i = 1; i < std::min<size_t>(ranges.size(), 3); ++i) {
                 ck(cudaEventRecord(ctx->event(i), rs[i]), "event");
@@ -1368,6 +1421,13 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
                     ck(k2_launch(x, static_cast<int32_t>(m), st), "K2 strict exact re-runs");
                     ++ctx->launches;
                     out.reruns += m;
+                    if (f64_pipe && gio->on_patch) {
+                        // their groups were downloaded without them: copy their blocks again
+                        ck(cudaEventRecord(ctx->event(ev_k2f + ranges.size()), st), "event");
+                        ck(cudaStreamWaitEvent(ctx->io, ctx->event(ev_k2f + ranges.size()), 0), "wait");
+                        for (const BlockDesc& d : xd)
+                            gio->on_patch(d.frame, d.row0 + g.S, d.col0 + g.S, g.bh, g.bw, ctx->io);
+                    }
                 }
             }
         } else {
@@ -2462,7 +2522,7 @@ static void conceal_frames_batch(fofse_ctx* ctx, const uint8_t* frames, int32_t 
         // after the previous band's iteration, in partial waves) — off by default.
         const bool fp32 = params && params->precision == FOFSE_PREC_FP32;
         const bool by_frame = n_frames >= 16;
-        int G = fp32 && by_frame ? std::clamp<int32_t>(n_frames / 16, 1, 8) : 1;
+        int G = by_frame ? std::clamp<int32_t>(n_frames / 16, 1, 8) : 1;
         if (const char* e = std::getenv("FOFSE_ROW_GROUPS"); e && fp32 && !by_frame)
             G = std::clamp(std::atoi(e), 1, std::max(1, height / 64));
         // group boundaries (rows): the first and last groups are a quarter of the
@@ -2565,6 +2625,14 @@ static void conceal_frames_batch(fofse_ctx* ctx, const uint8_t* frames, int32_t 
         };
         // group g done (groups complete in order)
         gio.on_done = [&](int gq, cudaStream_t s) { download_to(final_after[static_cast<size_t>(gq)], s); };
+        gio.on_patch = [&](int32_t f, int32_t r, int32_t c, int32_t nr, int32_t nc, cudaStream_t s) {
+            const int32_t r0 = std::max(r, 0), c0 = std::max(c, 0);
+            const int32_t r1 = std::min(r + nr, height), c1 = std::min(c + nc, width);
+            if (r1 <= r0 || c1 <= c0) return;
+            const size_t off = static_cast<size_t>(f) * fs + static_cast<size_t>(r0) * width + c0;
+            ck(cudaMemcpy2DAsync(restored + off, width, d_fr + off, width, c1 - c0, r1 - r0, cudaMemcpyDeviceToHost, s),
+               "D2H patch");
+        };
         RunOut ro;
         fofse::Frames fr{d_fr, d_fr, fofse::SRC_U8, width, height, static_cast<int64_t>(fs)};
         try {

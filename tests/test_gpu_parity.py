@@ -667,6 +667,54 @@ def test_frame_groups_match_single_frames(gpu, nframes):
     assert k > 3 and rep.device["blocks"] == sum(len(p.blocks) for p in pats)
 
 
+@pytest.mark.parametrize("nframes", [40, 130])
+def test_fp64_frame_groups_match_single_frames(gpu, nframes):
+    """fp64 mode through the frames API: each group's K1 waits for its own upload
+    and its download follows its last iteration launch (the copies overlap the
+    kernels). Frame by frame, the bytes of concealing each frame on its own."""
+    rng = np.random.default_rng(587)
+    H = W = 128
+    frames = np.stack([np.clip(smooth_test_image(rng, H) + 0.0, 0, 255).astype(np.uint8) for _ in range(nframes)])
+    pats = []
+    for f in range(nframes):
+        rr = P.gen_losses(800 + f, W // 16, H // 16, 0.12, 16, 16)
+        pats.append(P.LossPattern(W, H, 16, 16, [P.Rect(*map(int, (r["row"], r["col"], 16, 16))) for r in rr]))
+    cfg = WL.C4.config("fp64")
+    out, sq, rep = P.conceal_frames(frames, pats, cfg)
+    for f in range(0, nframes, 9):
+        one, sq1, _ = P.conceal_frames(frames[f:f + 1], pats[f:f + 1], cfg)
+        np.testing.assert_array_equal(one[0], out[f])
+        n0 = sum(len(p.blocks) for p in pats[:f])
+        np.testing.assert_allclose(sq1, sq[n0:n0 + len(pats[f].blocks)], rtol=1e-12)
+    assert rep.device["blocks"] == sum(len(p.blocks) for p in pats)
+
+
+@pytest.mark.parametrize("tau", [None, 1.0])
+def test_fp64_frame_groups_patch_exact_reruns(gpu, tau):
+    """Near-tie blocks skip the fast kernel's write-back and are re-run on the
+    exact path after their group was downloaded: the frames API copies their
+    blocks again. Transpose-symmetric frames (exact ties on the diagonal) and
+    guard_tau = 1 (every block re-run): the bytes of one frame at a time."""
+    n = 36
+    frames, pats = [], []
+    for f in range(n):
+        a = np.random.default_rng(f).normal(0.0, 12.0, (128, 128))
+        x = np.arange(128)
+        base = 110 + 40 * np.cos(2 * np.pi * x / 37.0)[:, None] * np.cos(2 * np.pi * x / 37.0)[None, :]
+        frames.append(np.clip(np.round(base + a + a.T), 0, 255).astype(np.uint8))
+        rr = [(r, r, 16, 16) for r in (16, 48, 80)] + [(16, 80, 16, 16), (96, 32, 16, 16)]
+        pats.append(P.LossPattern(128, 128, 16, 16, [P.Rect(*b) for b in rr]))
+    frames = np.stack(frames)
+    kw = {} if tau is None else {"guard_tau": tau}
+    cfg = P.ConcealConfig(gamma=0.5, iterations=80, transform_size=64, rho_hat=0.8, support_width=16, **kw)
+    out, sq, rep = P.conceal_frames(frames, pats, cfg)
+    assert rep.device["guard_reruns"] > 0 if tau is None else rep.device["guard_reruns"] == 5 * n
+    for f in range(0, n, 5):
+        one, sq1, _ = P.conceal_frames(frames[f:f + 1], pats[f:f + 1], cfg)
+        np.testing.assert_array_equal(one[0], out[f])
+        np.testing.assert_allclose(sq1, sq[5 * f:5 * f + 5], rtol=1e-12)
+
+
 @pytest.mark.parametrize("nframes,groups", [(1, 3), (1, 8), (3, 5)])
 def test_row_groups_match_one_group(gpu, monkeypatch, nframes, groups):
     """Fewer than 16 frames: the frames' rows are cut into bands (first/last a
