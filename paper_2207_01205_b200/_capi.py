@@ -11,7 +11,9 @@ import os
 
 import numpy as np
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libfofse.so")
+# FOFSE_LIB_PATH: another build of the library (same-box A/B of kernel variants)
+LIB_PATH = os.environ.get("FOFSE_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib",
+                                                            "libfofse.so")
 # synthetic-input generator (include/fofse_gen.h): its own host-only library, so
 # generating a workload never maps the product library
 GEN_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libfofse_gen.so")

@@ -1548,7 +1548,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
                 if (k == 0 && head == 0 && !ch.f64_direct) continue;
                 if (k == 1 && ch.f64_direct) continue;
                 const bool kv2 = ch.path == PATH_F32_REAL ? v2r : v2;
-                const int ng = k == 0 ? ng_f64(hi_path(ch.path)) : kv2 ? k2v2_warps_per_cta(T) : k2_groups_per_cta(T, ch.path);
+                const int ng = k == 0 ? ng_f64(hi_path(ch.path)) : kv2 ? k2v2_blocks_per_cta(T, ch.path) : k2_groups_per_cta(T, ch.path);
                 TList& tl = tls[2 * ci + static_cast<size_t>(k)];
                 tl.ng = ng;
                 tl.r0 = all_runs.size();

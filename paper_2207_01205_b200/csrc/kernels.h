@@ -289,7 +289,7 @@ int guard_plan_launch(const GuardPlanArgs& a, cudaStream_t s);
 // K2d REPLAY mode (a.src_pos set): rebuilds a near-tie block's fp64 state after
 // its first nu_flag[pos] recorded selections, then iterates on to nu_limit.
 bool k2d_replay_fits(int T, int rstride);
-int k2v2_warps_per_cta(int t);
+int k2v2_blocks_per_cta(int t, int path);
 // Lost blocks per full wave of the fp32 real-path kernel on device dev (0 = unknown).
 int64_t k2v2_real_wave(int t, int dev, int gw);
 int cvt_launch(const CvtArgs& a, cudaStream_t s);

@@ -254,12 +254,17 @@ __global__ void __launch_bounds__(K1fCfg<FT>::THREADS, FT == 64 ? 3 : 8) k1f_ker
             }
         }
     }
-    energy = block_reduce<double>(energy, red, false);  // (its __syncthreads orders the tile)
+    // the block's energy and max are needed by thread 0 only: warp partials here,
+    // one pass over the warps' slots at the end
+#pragma unroll
+    for (int o = 16; o; o >>= 1) energy += __shfl_xor_sync(0xffffffffu, energy, o);
+    __syncthreads();  // the column pass's tile writes before the pack
 
     // ---- pack the canonical half ----
     double vmax2 = 0.0;
     const BinLayout L = BinLayout::make(FT, a.seg, a.spt > 0 ? a.spt : 1);
     const bool rotate = path_is_rotated(a.path);
+    constexpr int SEG16 = 16;  // seg_for(FT, fp64): the fp64 AoS layout of K2d / the strict kernel
     const size_t per = a.out_stride > 0 ? (size_t)a.out_stride : packed32_floats(L, a.soa);
     // thread -> (tid, first slot): the segment(s) of tid are fixed, no divisions
     const int NT = L.NT, tid = threadIdx.x % NT, step = blockDim.x / NT;
@@ -275,7 +280,47 @@ __global__ void __launch_bounds__(K1fCfg<FT>::THREADS, FT == 64 ? 3 : 8) k1f_ker
         if (rotate) v = c_mul(v, ph[(k1 * (a.Lh - 1) + k2 * (a.Lw - 1)) & (2 * FT - 1)]);
         return v;
     };
-    if (L.SPT == 1 && path_is_f64(a.path)) {
+    if (a.spt <= 1 && a.seg == SEG16 && path_is_f64(a.path)) {
+        // fp64 AoS, the common layout, with compile-time geometry: slot j of
+        // thread tid at j * NT + tid; a thread's slots are j0, j0 + STEP, ...
+        // (j0 is warp-uniform); the rotation phase index advances by Lw - 1 per column
+        constexpr int HT = FT / 2, QN = FT / SEG16, NT16 = HT * QN, STEP = C::THREADS / NT16;
+        static_assert(C::THREADS % NT16 == 0, "whole slot rows per pass");
+        const int tid16 = threadIdx.x % NT16, j0 = threadIdx.x / NT16;
+        const int vr = tid16 % HT, q = tid16 / HT;
+        int k1, c0, ex;
+        if (vr == 0) {
+            k1 = q < QN / 2 ? 0 : HT;
+            c0 = (q < QN / 2 ? q : q - QN / 2) * SEG16;
+            ex = q == QN / 2 - 1 || q == QN - 1;
+        } else {
+            k1 = vr;
+            c0 = q * SEG16;
+            ex = 0;
+        }
+        const int lw1 = a.Lw - 1;
+        const int nk1 = (FT - k1) & (FT - 1);
+        const int pbase = k1 * (a.Lh - 1);
+        double2* o = static_cast<double2*>(a.out) + (size_t)b * ((SEG16 + 1) * NT16) + tid16;
+#pragma unroll
+        for (int i = 0; i < (SEG16 + STEP) / STEP; ++i) {
+            const int j = j0 + STEP * i;
+            if (j > SEG16) break;
+            double2 v = make_double2(0.0, 0.0);
+            if (j < SEG16 || ex) {
+                const int k2 = c0 + j;
+                if (k2 <= FT / 2) {
+                    v = cb[k2 * CS + k1];
+                } else {
+                    const double2 u = cb[(FT - k2) * CS + nk1];
+                    v = make_double2(u.x, -u.y);
+                }
+                vmax2 = fmax(vmax2, fma(v.x, v.x, v.y * v.y));
+                if (rotate) v = c_mul(v, ph[(pbase + k2 * lw1) & (2 * FT - 1)]);
+            }
+            o[(size_t)j * NT16] = v;
+        }
+    } else if (L.SPT == 1 && path_is_f64(a.path)) {
         // fp64 AoS (K2d / strict input): slot j of tid at j * NT + tid
         int k1, c0, ex;
         L.thread_segment(tid, 0, &k1, &c0, &ex);
@@ -301,10 +346,24 @@ __global__ void __launch_bounds__(K1fCfg<FT>::THREADS, FT == 64 ? 3 : 8) k1f_ker
                              static_cast<float>(v.x), static_cast<float>(v.y));
         }
     }
-    vmax2 = block_reduce<double>(vmax2, red, true);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) vmax2 = fmax(vmax2, __shfl_xor_sync(0xffffffffu, vmax2, o));
+    constexpr int NW = C::THREADS / 32;
+    static_assert(2 * NW <= 16, "red holds 16 doubles");
+    if ((threadIdx.x & 31) == 0) {
+        red[threadIdx.x >> 5] = energy;
+        red[NW + (threadIdx.x >> 5)] = vmax2;
+    }
+    __syncthreads();
     if (threadIdx.x == 0) {
-        a.energy[b] = energy;
-        a.init_max[b] = sqrt(vmax2);
+        double e = red[0], m = red[NW];
+#pragma unroll
+        for (int w = 1; w < NW; ++w) {
+            e += red[w];
+            m = fmax(m, red[NW + w]);
+        }
+        a.energy[b] = e;
+        a.init_max[b] = sqrt(m);
     }
 }
 

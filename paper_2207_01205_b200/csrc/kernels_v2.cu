@@ -443,6 +443,296 @@ __global__ void __launch_bounds__(128, VAR == 0 ? 3 : 2) k2v2r_kernel(K2Args a) 
 }
 
 // ============================================================================
+// Real path, SEVERAL LOST BLOCKS PER WARP (T <= 32): K2v2t. A team of NT lanes
+// owns one lost block (T = 32: 16 lanes x 2 segments x 16 bins; T = 16: 8 lanes),
+// BPW = 32 / NT teams share the warp's instruction stream, so the per-selection
+// controller (team-masked REDUX argmax + runner-up, scalar part, record) and
+// the fused synthesis are issued once for BPW blocks — at T = 32 the controller
+// outweighs the update (8 bin pairs per lane in the one-block-per-warp form).
+// A team whose block has stopped (converged / near-tie flag) rides along with a
+// zero update until every team of the warp is done.
+// ============================================================================
+template <int T>
+struct V2TCfg {
+    static constexpr int SEG = v2_seg(T);
+    static constexpr int SPT = v2_team_spt(T);
+    static constexpr int HT = T / 2;
+    static constexpr int QN = T / SEG;
+    static constexpr int NT = HT * QN / SPT;  // lanes per team (lost block)
+    static constexpr int BPW = 32 / NT;       // lost blocks per warp
+    static constexpr int NP = SPT * SEG / 2;  // bin pairs per lane
+    static constexpr int SRV = v2_srv(T);
+    static constexpr int NCOPY = 2;
+    static constexpr int WARPS = 4;
+    static constexpr int BLOCKS = WARPS * BPW;  // lost blocks per CTA (tile)
+    static constexpr bool REAL = true;
+    static constexpr size_t WELEMS = (size_t)NCOPY * T * SRV;
+    static constexpr size_t IMG_BYTES = WELEMS * 4;
+    static constexpr size_t CLASS_BYTES = IMG_BYTES;  // the K2v2r class image
+    static constexpr bool TW64 = false;
+    static constexpr bool P32 = true;
+    static constexpr size_t WBYTES = ((IMG_BYTES + 15) / 16) * 16;
+    static constexpr size_t OFF_P = WBYTES;
+    static constexpr size_t OFF_TW = OFF_P + sizeof(double2) * 2 * T;
+    static constexpr size_t OFF_SP = OFF_TW + sizeof(float2) * T;             // one float4 per team
+    static constexpr size_t OFF_ST = OFF_SP + sizeof(float4) * WARPS * BPW;   // one V2State per team
+    static constexpr size_t OFF_BAR = OFF_ST + 64 * WARPS * BPW;
+    static constexpr size_t SMEM = OFF_BAR + 16;
+    static_assert(32 % NT == 0 && NT >= 4, "whole teams per warp");
+    static_assert(NP + SPT <= 64, "pair index must fit the 6 key bits");
+    static_assert(SEG % 2 == 0, "bin pairs");
+};
+
+// max of v over the lanes of team `sub` (BPW teams of 32 / BPW lanes): one
+// uniform full-warp REDUX per team, keys are non-negative float bits
+template <int BPW>
+__device__ __forceinline__ unsigned team_max(unsigned v, int sub) {
+    unsigned m = 0;
+#pragma unroll
+    for (int j = 0; j < BPW; ++j) {
+        const unsigned r = __reduce_max_sync(0xffffffffu, sub == j ? v : 0u);
+        m = sub == j ? r : m;
+    }
+    return m;
+}
+
+template <int T>
+__global__ void __launch_bounds__(128, 4) k2v2t_kernel(K2Args a) {
+    using Cf = V2TCfg<T>;
+    constexpr int SEG = Cf::SEG, SPT = Cf::SPT, NT = Cf::NT, NP = Cf::NP, SRV = Cf::SRV, BPW = Cf::BPW;
+    constexpr int PPS = SEG / 2;
+    constexpr int ACC = 2;
+    constexpr bool LO = false;
+
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const Tile tile = a.tiles[blockIdx.x];
+    v2_stage<Cf>(a, tile, smem_raw);
+    const float* vE = reinterpret_cast<const float*>(smem_raw);
+    const float2* ptab = reinterpret_cast<const float2*>(smem_raw + Cf::OFF_P);
+    const float2* twi = reinterpret_cast<const float2*>(smem_raw + Cf::OFF_TW);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int sub = lane / NT, sl = lane % NT;  // team, lane in the team
+    const unsigned tmask = NT == 32 ? 0xffffffffu : (((1u << NT) - 1u) << (sub * NT));
+    const int team = warp * BPW + sub;
+    float4* spill = reinterpret_cast<float4*>(smem_raw + Cf::OFF_SP) + team;
+    V2State* st = reinterpret_cast<V2State*>(smem_raw + Cf::OFF_ST + 64 * team);
+
+    const BinLayout L = BinLayout::make(T, SEG, SPT);
+    int k1s[SPT], c0s[SPT], exs[SPT];
+#pragma unroll
+    for (int s = 0; s < SPT; ++s) L.thread_segment(sl, s, &k1s[s], &c0s[s], &exs[s]);
+    const int gb0 = k1s[0] * T + c0s[0];
+    const int gb1 = k1s[SPT - 1] * T + c0s[SPT - 1];
+    const float sgn_r = ((a.Lh - 1) & 1) ? -1.f : 1.f;
+    const float sgn_c = ((a.Lw - 1) & 1) ? -1.f : 1.f;
+    constexpr unsigned kmask = 0xffffffc0u;
+    const float tau1 = a.tau1f;
+    const int rstride = a.rec_stride > 0 ? a.rec_stride : a.iterations;
+    const int lh1 = a.Lh - 1, lw1 = a.Lw - 1;
+    const bool diag = a.trace != nullptr || a.gap_trace != nullptr;
+
+    for (int bw = warp * BPW; bw < tile.count; bw += Cf::WARPS * BPW) {  // warp-uniform
+        const int bi = bw + sub;
+        const bool has = bi < tile.count;
+        const int pos = tile.begin + (has ? bi : bw);  // a team without a block reads its warp's first
+        const int b = a.order[pos];
+        float2 rp[NP], ip[NP];
+        float xr[SPT], xi[SPT];
+        {
+            const size_t rs = a.rin_stride > 0 ? (size_t)a.rin_stride : (size_t)(NP + SPT) * NT * 4;
+            const float4* R = reinterpret_cast<const float4*>(static_cast<const float*>(a.rin) + (size_t)pos * rs);
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+                const float4 u = R[p * NT + sl];
+                rp[p] = make_float2(u.x, u.y);
+                ip[p] = make_float2(u.z, u.w);
+            }
+#pragma unroll
+            for (int s = 0; s < SPT; ++s) {
+                const float4 u = R[(NP + s) * NT + sl];
+                xr[s] = u.x;
+                xi[s] = u.z;
+            }
+        }
+        const double e_init = a.init_energy[pos];
+        if (sl == 0) {
+            const double im = 1e-12 * a.init_max[pos];
+            const double w0 = a.w0[tile.cls];
+            st->energy = a.energy0[pos];
+            st->thr_e = 1e-12 * e_init;
+            st->thr_m = (float)(im * im);
+            st->w0 = (float)w0;
+            st->gw = (float)(a.gamma / w0);
+            st->nu = a.nu0 ? a.nu0[pos] : 0;
+            st->ntrace = a.trace_from_nu0 ? st->nu : 0;
+        }
+        int conv = (a.conv0 ? a.conv0[pos] : 0) | (e_init <= 0.0) | (has ? 0 : 1);
+        int flagged = 0;
+        int* rec_u = a.rec_u_g + (size_t)b * rstride;
+        double2* rec_c = a.rec_c_g + (size_t)b * rstride;
+        __syncwarp();
+
+        KAcc A[ACC + 1];
+#pragma unroll
+        for (int k = 0; k <= ACC; ++k) A[k] = KAcc{0.f, 0.f};
+#pragma unroll
+        for (int p = 0; p < NP; ++p) kacc_pair<LO>(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+#pragma unroll
+        for (int s = 0; s < SPT; ++s)
+            if (exs[s]) kacc_one(A[ACC], fmaf(xi[s], xi[s], xr[s] * xr[s]), NP + s, kmask);
+
+        for (int it = 0; it < a.iterations; ++it) {
+            if (__all_sync(0xffffffffu, conv | flagged)) break;
+            float bm1 = A[0].m1, bm2 = A[0].m2;
+#pragma unroll
+            for (int k = 1; k <= ACC; ++k) {
+                bm2 = fmax3(bm2, A[k].m2, fminf(bm1, A[k].m1));
+                bm1 = fmaxf(bm1, A[k].m1);
+            }
+            // ---- team argmax + runner-up: full-warp REDUX per team (a team mask is
+            // not warp-uniform, and REDUX with a divergent mask falls back to a loop) ----
+            const unsigned M = team_max<BPW>(fbits(bm1), sub);
+            const bool cand = fbits(bm1) == M;
+            const int wl = __ffs(__ballot_sync(0xffffffffu, cand) & tmask) - 1;
+            const unsigned S = team_max<BPW>(fbits(lane == wl ? bm2 : bm1), sub);
+            const int pw = 63 - static_cast<int>(M & 63u);
+            __syncwarp();
+            if (lane == wl) *spill = pick_pair<NP, SPT>(pw, rp, ip, xr, xi);
+            __syncwarp();
+            float2 pre;
+            int jw, sw;
+            float lo_w = 0.f;
+            {
+                const float4 q = *spill;
+                if (pw < NP) {
+                    const float ma = fmaf(q.z, q.z, q.x * q.x), mb = fmaf(q.w, q.w, q.y * q.y);
+                    lo_w = fminf(ma, mb);
+                    const int half = mb > ma ? 1 : 0;
+                    pre = half ? make_float2(q.y, q.w) : make_float2(q.x, q.z);
+                    sw = pw / PPS;
+                    jw = 2 * (pw % PPS) + half;
+                } else {
+                    pre = make_float2(q.x, q.z);
+                    sw = pw - NP;
+                    jw = SEG;
+                }
+            }
+            const int G = __shfl_sync(0xffffffffu, (SPT == 2 && sw == 1) ? gb1 : gb0, wl) + jw;
+
+            const float Mf = __uint_as_float(M), Sf = fmaxf(__uint_as_float(S), lo_w);
+            const double energy = st->energy;
+            const float w0 = st->w0, gw = st->gw;
+            bool stop = (conv | flagged) != 0;
+            if (!stop) {
+                if (energy < st->thr_e || !(Mf > 0.f) || Mf < st->thr_m) {
+                    conv = 1;
+                    stop = true;
+                } else if (Sf > Mf * tau1) {
+                    flagged = 1 + st->nu;  // near-tie: the host re-runs this block in fp64
+                    stop = true;
+                }
+            }
+            const int u1 = G / T, u2 = G % T;
+            const int self = ((u1 & (T / 2 - 1)) == 0) && ((u2 & (T / 2 - 1)) == 0);
+            const float pr = pre.x, pi = pre.y;
+            const float2 P = ptab[(u1 * lh1 + u2 * lw1) & (2 * T - 1)];
+            const float ar = pr * gw, ai = pi * gw;
+            float c_re = ar * P.x - ai * P.y, c_im = ar * P.y + ai * P.x;
+            float delta;
+            float a_re = ar, a_im = ai;
+            if (self) {
+                c_im = 0.f;
+                a_re = c_re * P.x;
+                a_im = -c_re * P.y;
+                delta = c_re * (c_re * w0 - 2.f * (pr * P.x - pi * P.y));
+            } else {
+                const int mi1 = 2 * u1, mi2 = 2 * u2;
+                const float v2 = vE[(mi1 & (T - 1)) * SRV + (mi2 & (T - 1))];
+                const float sig = ((mi1 >= T) ? sgn_r : 1.f) * ((mi2 >= T) ? sgn_c : 1.f);
+                delta = -4.f * (a_re * pr + a_im * pi) + 2.f * (a_re * a_re + a_im * a_im) * w0 +
+                        2.f * sig * v2 * (a_re * a_re - a_im * a_im);
+            }
+            __syncwarp();
+            if (!stop && sl == 0) {
+                const double e = energy + (double)delta;
+                const double en = 0.0 < e ? e : 0.0;
+                const int nu = st->nu + 1;
+                if (nu - 1 < rstride) {
+                    rec_u[nu - 1] = (u1 << 16) | u2;
+                    rec_c[nu - 1] = make_double2(self ? c_re : 2.f * c_re, self ? 0.f : 2.f * c_im);
+                }
+                st->energy = en;
+                st->nu = nu;
+                st->ntrace += 1;
+                if (diag) {
+                    const int tstride = a.trace_stride > 0 ? a.trace_stride : a.iterations;
+                    const float iw = 1.f / w0;
+                    v2_record(a, b, nu, st->ntrace - 1, 0, tstride, nullptr, nullptr, u1, u2, self,
+                              (pr * P.x - pi * P.y) * iw, (pr * P.y + pi * P.x) * iw, c_re, c_im, en, Mf, Sf);
+                }
+            }
+            if (stop) {  // a stopped team rides along: R -= 0
+                a_re = 0.f;
+                a_im = 0.f;
+            }
+            // ---- residual update: R' -= s1 a V[k-u] + s2 conj(a) V[k+u] (+ next scan) ----
+            const float fr = a_re, fi = a_im;
+            const int par = u2 & 1;
+            const float* vimg = vE + par * (T * SRV);
+#pragma unroll
+            for (int k = 0; k <= ACC; ++k) A[k] = KAcc{0.f, 0.f};
+#pragma unroll
+            for (int s = 0; s < SPT; ++s) {
+                const int k1 = k1s[s], c0 = c0s[s];
+                const int rA = (k1 - u1) & (T - 1), rB = (k1 + u1) & (T - 1);
+                const int cA = (c0 - u2) & (T - 1), cB = (c0 + u2) & (T - 1);
+                const float s1 = ((k1 < u1) ? sgn_r : 1.f) * ((c0 < u2) ? sgn_c : 1.f);
+                const float s2 = ((k1 + u1 >= T) ? sgn_r : 1.f) * ((c0 + u2 >= T) ? sgn_c : 1.f);
+                const float2* va = reinterpret_cast<const float2*>(vimg + rA * SRV + (cA - par));
+                const float2* vb = reinterpret_cast<const float2*>(vimg + rB * SRV + (cB - par));
+                const float2 n1r = make_float2(-s1 * fr, -s1 * fr), n1i = make_float2(-s1 * fi, -s1 * fi);
+                // self-conjugate selections have no second term: s2 = 0 folds it away
+                const float t2 = self ? 0.f : s2;
+                const float2 n2r = make_float2(-t2 * fr, -t2 * fr), n2i = make_float2(t2 * fi, t2 * fi);
+#pragma unroll
+                for (int q = 0; q < PPS; ++q) {
+                    const int p = s * PPS + q;
+                    const float2 x = va[q], y = vb[q];
+                    rp[p] = __ffma2_rn(n2r, y, __ffma2_rn(n1r, x, rp[p]));
+                    ip[p] = __ffma2_rn(n2i, y, __ffma2_rn(n1i, x, ip[p]));
+                    kacc_pair<LO>(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+                }
+                if (exs[s]) {
+                    const float x = vE[rA * SRV + cA + SEG];
+                    xr[s] = fmaf(-s1 * fr, x, xr[s]);
+                    xi[s] = fmaf(-s1 * fi, x, xi[s]);
+                    if (!self) {
+                        const float y = vE[rB * SRV + cB + SEG];
+                        xr[s] = fmaf(-s2 * fr, y, xr[s]);
+                        xi[s] = fmaf(s2 * fi, y, xi[s]);
+                    }
+                    kacc_one(A[ACC], fmaf(xi[s], xi[s], xr[s] * xr[s]), NP + s, kmask);
+                }
+            }
+        }
+
+        if (a.rout && has) {
+            const size_t rs = a.rin_stride > 0 ? (size_t)a.rin_stride : (size_t)(NP + SPT) * NT * 4;
+            float4* R = reinterpret_cast<float4*>(static_cast<float*>(a.rout) + (size_t)pos * rs);
+#pragma unroll
+            for (int p = 0; p < NP; ++p) R[p * NT + sl] = make_float4(rp[p].x, rp[p].y, ip[p].x, ip[p].y);
+#pragma unroll
+            for (int s = 0; s < SPT; ++s) R[(NP + s) * NT + sl] = make_float4(xr[s], 0.f, xi[s], 0.f);
+        }
+        __syncwarp();
+        v2_finish_teams<T, NT>(a, a.blocks[pos], pos, b, sl, has, st->energy, st->nu, conv, flagged, st->ntrace,
+                               rec_u, rec_c, rstride, twi);
+        __syncwarp();
+    }
+}
+
+// ============================================================================
 // Real path, TWO WARPS PER LOST BLOCK (T = 64): each warp owns one 32-column
 // segment of every canonical row (16 bin pairs + the self-conjugate extra for
 // lane 0) — half the registers of the one-warp form, so twice the warps per SM
@@ -1092,6 +1382,14 @@ static int k2v2_launch_t(const K2Args& a, int32_t ntiles, cudaStream_t s) {
             return cudaGetLastError();
         };
         return nc == 2 ? launch(k2v2c_kernel<T, 2>, V2PCfg<T, 2>::SMEM) : launch(k2v2c_kernel<T, 1>, V2PCfg<T, 1>::SMEM);
+    } else if constexpr (T <= 32) {
+        // several lost blocks per warp (K2v2t)
+        using Cf = V2TCfg<T>;
+        cudaError_t e = cudaFuncSetAttribute(k2v2t_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
+        if (e != cudaSuccess) return e;
+        if (ntiles <= 0) return cudaSuccess;
+        k2v2t_kernel<T><<<ntiles, 32 * Cf::WARPS, Cf::SMEM, s>>>(a);
+        return cudaGetLastError();
     } else {
         using Cf = V2Cfg<T, PATH>;
         auto* fn = v2r_variant() == 3   ? k2v2r_kernel<T, 3>
@@ -1139,7 +1437,17 @@ int k2v2_launch(const K2Args& args, int32_t ntiles, cudaStream_t s) {
     return cudaErrorInvalidValue;
 }
 
-int k2v2_warps_per_cta(int t) { return t == 128 ? V2HCfg<128>::GROUPS : 4; }  // lost blocks per CTA
+// lost blocks per CTA (one tile) of the fp32 iteration kernel of a path
+int k2v2_blocks_per_cta(int t, int path) {
+    if (path == PATH_F32_REAL) {
+        switch (t) {
+            case 8: return V2TCfg<8>::BLOCKS;
+            case 16: return V2TCfg<16>::BLOCKS;
+            case 32: return V2TCfg<32>::BLOCKS;
+        }
+    }
+    return t == 128 ? V2HCfg<128>::GROUPS : 4;
+}
 
 // Lost blocks resident at once on the device for the fp32 real-path kernel
 // (SMs x CTAs per SM x blocks per CTA): chunk sizes are multiples of it, so no
@@ -1154,6 +1462,11 @@ static int64_t wave_t(int dev) {
         cudaFuncSetAttribute(k2v2h_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2v2h_kernel<128>, Cf::THREADS, Cf::SMEM);
         return e == cudaSuccess ? (int64_t)nsm * per_sm * Cf::GROUPS : 0;
+    } else if constexpr (T <= 32) {
+        using Cf = V2TCfg<T>;
+        cudaFuncSetAttribute(k2v2t_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2v2t_kernel<T>, 32 * Cf::WARPS, Cf::SMEM);
+        return e == cudaSuccess ? (int64_t)nsm * per_sm * Cf::BLOCKS : 0;
     } else {
         using Cf = V2Cfg<T, PATH_F32_REAL>;
         cudaFuncSetAttribute(k2v2r_kernel<T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);

@@ -133,7 +133,10 @@ FOFSE_HDC int v2_srv4(int t) { return ((t + v2_seg(t) + 4 + 3) / 4) * 4; }
 // wave or two, where the partial last wave sets the time). v2_choose_real_gw
 // decides from the job's real-path block count; FOFSE_V2_REAL_GW=1/2 forces.
 int v2_choose_real_gw(int t, int64_t real_blocks, int dev);
-inline int v2_real_spt(int t, int gw) { return (t == 64 && gw == 2) ? 1 : v2_spt(t); }
+// Segments per lane of the team kernel K2v2t (T <= 32, several lost blocks per
+// warp): T = 32 and 16 hold two segments, so a block is a team of 16 / 8 lanes.
+FOFSE_HDC int v2_team_spt(int t) { return (t == 32 || t == 16) ? 2 : 1; }
+inline int v2_real_spt(int t, int gw) { return t <= 32 ? v2_team_spt(t) : ((t == 64 && gw == 2) ? 1 : v2_spt(t)); }
 // Copies of V in the K2v2 real path's class image (2: even/odd pairs, 4: quads).
 int v2_real_copies(int t, int gw);
 // T = 128 fp32 real path on K2v2h (8 warps per lost block); FOFSE_K2_128=v1

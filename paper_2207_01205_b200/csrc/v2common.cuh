@@ -194,4 +194,94 @@ __device__ __forceinline__ void v2_finish(const K2Args& a, const BlockDesc& desc
     }
 }
 
+// v2_finish for a warp of BPW teams of NT lanes (K2v2t: one lost block per
+// team). Every loop runs to the warp's largest count so the shuffles stay
+// convergent; a team past its own record count reads zero records, a team
+// without a block (or with a near-tie flag) writes nothing.
+template <int T, int NT>
+__device__ __forceinline__ void v2_finish_teams(const K2Args& a, const BlockDesc& desc, int pos, int b, int t,
+                                                bool has, double energy, int nu, int conv, int flagged, int ntrace,
+                                                const int* rec_u, const double2* rec_c, int rstride,
+                                                const float2* twi) {
+    constexpr int PX = NT >= 16 ? 4 : 8;  // pixels per lane per pass
+    const int base = (threadIdx.x & 31) - t;  // the team's first lane
+    if (t == 0 && has) {
+        const int sb = a.state_by_pos ? pos : b;
+        if (a.energy_out) a.energy_out[sb] = energy;
+        if (a.nu_out) a.nu_out[sb] = nu;
+        if (a.conv_out) a.conv_out[sb] = conv;
+        if (a.flags) a.flags[pos] = flagged;
+        if (a.trace_count) a.trace_count[b] = ntrace;
+    }
+    __syncwarp();
+    const bool skip = !has || a.synth == SYN_NONE || flagged;
+    if (__all_sync(0xffffffffu, skip)) return;
+    const int nr = skip ? 0 : (nu < rstride ? nu : rstride);
+    const int nrmax = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(nr)));
+    const int npx = a.reg_nr * a.reg_nc;
+    double sq = 0.0;
+    for (int p0 = 0; p0 < npx; p0 += NT * PX) {
+        float acc[PX];
+        int mm[PX], nn[PX];
+#pragma unroll
+        for (int k = 0; k < PX; ++k) {
+            acc[k] = 0.f;
+            const int px = p0 + k * NT + t;
+            mm[k] = a.reg_r0 + (px < npx ? px / a.reg_nc : 0);
+            nn[k] = a.reg_c0 + (px < npx ? px % a.reg_nc : 0);
+        }
+        for (int q0 = 0; q0 < nrmax; q0 += NT) {
+            int uq = 0;
+            float cxq = 0.f, cyq = 0.f;
+            if (q0 + t < nr) {
+                uq = rec_u[q0 + t];
+                const double2 cd = rec_c[q0 + t];
+                cxq = (float)cd.x;
+                cyq = (float)cd.y;
+            }
+            const int nq = nrmax - q0 < NT ? nrmax - q0 : NT;
+            for (int q = 0; q < nq; ++q) {
+                const int u = __shfl_sync(0xffffffffu, uq, base + q);
+                const float cx = __shfl_sync(0xffffffffu, cxq, base + q), cy = __shfl_sync(0xffffffffu, cyq, base + q);
+                const int uu1 = u >> 16, uu2 = u & 0xffff;
+#pragma unroll
+                for (int k = 0; k < PX; ++k) {
+                    const float2 tw = twi[(uu1 * mm[k] + uu2 * nn[k]) & (T - 1)];
+                    acc[k] = fmaf(cx, tw.x, fmaf(-cy, tw.y, acc[k]));
+                }
+            }
+        }
+        if (!skip) {
+#pragma unroll
+            for (int k = 0; k < PX; ++k) {
+                const int px = p0 + k * NT + t;
+                if (px >= npx) continue;
+                const int m = mm[k], n = nn[k];
+                if (a.synth == SYN_WINDOW) {
+                    a.models[(size_t)b * a.Lh * a.Lw + m * a.Lw + n] = acc[k];
+                } else {
+                    const double v0 = acc[k];
+                    const double v = v0 < 0.0 ? 0.0 : (v0 > 255.0 ? 255.0 : v0);
+                    const int64_t gi = (int64_t)desc.frame * a.fr.frame_stride +
+                                       (int64_t)(desc.row0 + m) * a.fr.width + (desc.col0 + n);
+                    double orig;
+                    if (a.fr.type == SRC_U8) {
+                        orig = (double)static_cast<const uint8_t*>(a.fr.src)[gi];
+                        if (a.synth == SYN_IMAGE) static_cast<uint8_t*>(a.fr.dst)[gi] = static_cast<uint8_t>(round(v));
+                    } else {
+                        orig = static_cast<const double*>(a.fr.src)[gi];
+                        if (a.synth == SYN_IMAGE) static_cast<double*>(a.fr.dst)[gi] = v;
+                    }
+                    sq += (orig - v) * (orig - v);
+                }
+            }
+        }
+    }
+    if (a.block_sq && (a.synth == SYN_IMAGE || a.synth == SYN_ERR)) {
+#pragma unroll
+        for (int o = NT / 2; o; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);  // within the team
+        if (t == 0 && !skip) a.block_sq[b] = sq;
+    }
+}
+
 }  // namespace fofse

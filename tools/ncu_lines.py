@@ -1,44 +1,44 @@
-"""Per-source-line hot spots of an ncu report (needs -lineinfo + --import-source).
+"""Per-source-line instruction / stall-sample shares of an ncu report captured
+with --import-source on (kernels compiled with -lineinfo).
 
-Uses the combined CUDA+SASS source view (one row per SASS instruction with its
-CUDA line) and aggregates stall samples and executed instructions per line."""
-import csv, io, subprocess, sys
-from collections import defaultdict
+usage: python tools/ncu_lines.py REPORT [TOP]
+"""
+import csv
+import io
+import subprocess
+import sys
 
 
-def main(path, top=30):
-    out = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+def main(rep, top=40):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                          capture_output=True, text=True).stdout
-    agg = defaultdict(lambda: [0.0, 0.0, ""])
-    fname, hdr = "", None
+    cur, hdr, agg = None, None, {}
     for r in csv.reader(io.StringIO(out)):
         if not r:
             continue
-        if r[0] in ("File Path", "File Name"):
-            fname = r[1].split("/")[-1]
+        if r[0] == "File Path":
+            cur = r[1].split("/")[-1]
             continue
         if r[0] == "Line No":
             hdr = r
             continue
-        if not hdr or len(r) < len(hdr):
+        if hdr is None or not r[0].isdigit():
             continue
         try:
-            samp = float(r[4] or 0)
-            inst = float(r[7] or 0)
-        except ValueError:
+            inst = float(r[hdr.index("Instructions Executed")] or 0)
+            samp = float(r[hdr.index("Warp Stall Sampling (All Samples)")] or 0)
+        except (ValueError, IndexError):
             continue
-        a = agg[(fname, r[0])]
-        a[0] += samp
-        a[1] += inst
-        if r[1].strip():
-            a[2] = r[1].strip()[:90]
-    res = sorted(((v[0], v[1], k[0], k[1], v[2]) for k, v in agg.items()), reverse=True)
-    tot = sum(x[0] for x in res) or 1
-    toti = sum(x[1] for x in res) or 1
-    print(f"total samples {tot:.0f}, instructions {toti:.3e}")
-    for s, i, f, ln, src in res[:top]:
-        print(f"{100*s/tot:5.1f}% samp {100*i/toti:5.1f}% inst  {f}:{ln}  {src}")
+        k = (cur, int(r[0]))
+        a = agg.setdefault(k, [0.0, 0.0, r[1].strip()[:80]])
+        a[0] += inst
+        a[1] += samp
+    ti = sum(v[0] for v in agg.values()) or 1
+    ts = sum(v[1] for v in agg.values()) or 1
+    print(f"report {rep}: {ti:.4g} warp instructions, {ts:.4g} stall samples")
+    for (f, ln), (i, s, src) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
+        print(f"{100 * i / ti:5.1f}% inst {100 * s / ts:5.1f}% samp  {f}:{ln}  {src}")
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 30)
+    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 40)
