@@ -63,7 +63,7 @@ struct V2Cfg {
 };
 
 // fp32 argmax on packed keys: |R|^2 with its 6 low mantissa bits replaced by
-// (63 - pair index). Truncation merges values within 2^-17 relative into ties;
+// (63 - pair index) — or, in K2v2r, (63 - quad index) over the larger of four. Truncation merges values within 2^-17 relative into ties;
 // every tie leaves the runner-up equal to the maximum, which the near-tie guard
 // (tau >= 1e-5 > 2^-17) flags for an fp64 re-run, so the key order never
 // decides an unflagged selection.
@@ -125,6 +125,42 @@ __device__ __forceinline__ float4 pick_pair(int pw, const float2* rp, const floa
     return q;
 }
 
+// Quad keys (K2v2r VAR 5): one key per two adjacent bin pairs (four bins); the
+// runner-up chain runs over the quads' maxima, the winning quad's other three
+// bins join in the controller (the LO = false argument, one level up).
+__device__ __forceinline__ void kacc_quad(KAcc& A, float2 ma, float2 mb, int q, unsigned mask) {
+    const float hi = fmax3(fmaxf(ma.x, ma.y), mb.x, mb.y);
+    const float k = pkey(hi, q, mask);
+    A.m2 = fmaxf(A.m2, fminf(k, A.m1));
+    A.m1 = fmaxf(A.m1, k);
+}
+// The winning quad of a lane (warp-uniform index): pairs 2q, 2q+1 as two float4
+// (re_a, re_b, im_a, im_b); q >= NQ: the segment's extra bin (re, 0, im, 0).
+template <int NQ, int SPT>
+__device__ __forceinline__ void pick_quad(int qw, const float2* rp, const float2* ip, const float* xr,
+                                          const float* xi, float4& o0, float4& o1) {
+    o0 = make_float4(0.f, 0.f, 0.f, 0.f);
+    o1 = o0;
+    switch (qw) {
+#define PICKQ_CASE(Q)                                                                                    \
+    case Q:                                                                                              \
+        if (Q < NQ) {                                                                                    \
+            constexpr int P0 = Q < NQ ? 2 * Q : 0;                                                       \
+            o0 = make_float4(rp[P0].x, rp[P0].y, ip[P0].x, ip[P0].y);                                    \
+            o1 = make_float4(rp[P0 + 1].x, rp[P0 + 1].y, ip[P0 + 1].x, ip[P0 + 1].y);                    \
+        } else {                                                                                         \
+            constexpr int E = (Q >= NQ && Q - NQ < SPT) ? Q - NQ : 0;                                    \
+            o0 = make_float4(xr[E], 0.f, xi[E], 0.f);                                                    \
+        }                                                                                                \
+        break;
+        PICKQ_CASE(0) PICKQ_CASE(1) PICKQ_CASE(2) PICKQ_CASE(3) PICKQ_CASE(4) PICKQ_CASE(5) PICKQ_CASE(6)
+        PICKQ_CASE(7) PICKQ_CASE(8) PICKQ_CASE(9) PICKQ_CASE(10) PICKQ_CASE(11) PICKQ_CASE(12) PICKQ_CASE(13)
+        PICKQ_CASE(14) PICKQ_CASE(15) PICKQ_CASE(16) PICKQ_CASE(17)
+#undef PICKQ_CASE
+        default: break;
+    }
+}
+
 // (value, index) argmax merge: larger value wins, ties to the lower index.
 __device__ __forceinline__ void am_merge(float& m1, int& i1, float& m2, float om1, int oi1, float om2) {
     const bool take = om1 > m1 || (om1 == m1 && oi1 < i1);
@@ -140,17 +176,23 @@ __device__ __forceinline__ void am_merge(float& m1, int& i1, float& m2, float om
 // update / magnitude is an FFMA2 / FMUL2 on a pair.
 // ============================================================================
 template <int T, int VAR>
-__global__ void __launch_bounds__(128, VAR == 0 ? 3 : 2) k2v2r_kernel(K2Args a) {
+__global__ void __launch_bounds__(128, (VAR == 3 || VAR == 9) ? 2 : 3) k2v2r_kernel(K2Args a) {
     // VAR 3: quad V layout, one LDS.128 per two bin pairs
     constexpr bool Q4 = VAR == 3 || VAR == 9;
     using Cf = V2Cfg<T, PATH_F32_REAL, Q4>;
     constexpr int SEG = Cf::SEG, SPT = Cf::SPT, NT = Cf::NT, NP = Cf::NP, SRV = Cf::SRV;
     constexpr int PPS = SEG / 2;  // pairs per segment
-    // VAR 0 (production): even/odd V pairs, 168 registers, 3 CTAs/SM;
+    // VAR 0 (production): even/odd V pairs, quad keys, 168 registers, 3 CTAs/SM; VAR 1: keys per pair;
     // VAR 3: quad V layout (LDS.128 per two pairs), 2 CTAs/SM — measured ~2 % slower;
     // VAR 9: diagnostic — the update + scan alone (one REDUX, synthetic selections).
     // The next scan is fused into the update in every variant.
-    constexpr int ACC = VAR == 0 ? 2 : 4;  // independent argmax chains
+    // independent argmax chains (quad keys: 1 chain -0.3 %, 3 chains -6 %)
+    constexpr int ACC = (VAR == 3 || VAR == 9) ? 4 : 2;
+    // argmax keys per bin QUAD (two adjacent pairs): one key, one max and one
+    // runner-up step per quad, the winning quad's other three bins join in the
+    // controller — C4 K2v2r 48.9 -> 48.4 ms; VAR 1 keeps the key per pair
+    constexpr bool QK = VAR == 0;
+    constexpr int NQ = NP / 2;
     constexpr bool LO = false;  // the winning pair's smaller bin is added in the controller
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -178,7 +220,7 @@ __global__ void __launch_bounds__(128, VAR == 0 ? 3 : 2) k2v2r_kernel(K2Args a) 
     const float sgn_c = ((a.Lw - 1) & 1) ? -1.f : 1.f;
     // VAR 0 keeps the mask an immediate (two LOP3 per key): the register form saves
     // 32 instructions per block-iteration but measured 7 % slower on C4 (same-box A/B)
-    const unsigned kmask = key_mask<VAR != 0>(a);
+    const unsigned kmask = key_mask<VAR == 3 || VAR == 9>(a);
     V2State* st = reinterpret_cast<V2State*>(smem_raw + Cf::OFF_ST + 64 * warp);
     // loop invariants of the controller (kept out of the per-selection path)
     const float tau1 = a.tau1f;  // 1 - tau (tau == 0 disables the guard: S <= M)
@@ -231,11 +273,19 @@ __global__ void __launch_bounds__(128, VAR == 0 ? 3 : 2) k2v2r_kernel(K2Args a) 
         KAcc A[ACC + 1];
 #pragma unroll
         for (int k = 0; k <= ACC; ++k) A[k] = KAcc{0.f, 0.f};
+        if constexpr (QK) {
 #pragma unroll
-        for (int p = 0; p < NP; ++p) kacc_pair<LO>(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+            for (int q = 0; q < NQ; ++q)
+                kacc_quad(A[q % ACC], __ffma2_rn(ip[2 * q], ip[2 * q], __fmul2_rn(rp[2 * q], rp[2 * q])),
+                          __ffma2_rn(ip[2 * q + 1], ip[2 * q + 1], __fmul2_rn(rp[2 * q + 1], rp[2 * q + 1])), q, kmask);
+        } else {
+#pragma unroll
+            for (int p = 0; p < NP; ++p) kacc_pair<LO>(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+        }
+        constexpr int XKEY = QK ? NQ : NP;  // key index of a segment's extra bin
 #pragma unroll
         for (int s = 0; s < SPT; ++s)
-            if (exs[s]) kacc_one(A[ACC], fmaf(xi[s], xi[s], xr[s] * xr[s]), NP + s, kmask);
+            if (exs[s]) kacc_one(A[ACC], fmaf(xi[s], xi[s], xr[s] * xr[s]), XKEY + s, kmask);
 
         for (int it = 0; it < a.iterations && !conv; ++it) {
             int u1, u2, self;
@@ -263,14 +313,45 @@ __global__ void __launch_bounds__(128, VAR == 0 ? 3 : 2) k2v2r_kernel(K2Args a) 
             const bool cand = fbits(bm1) == M;
             const int wl = __ffs(__ballot_sync(0xffffffffu, cand)) - 1;
             const unsigned S = __reduce_max_sync(0xffffffffu, fbits(lane == wl ? bm2 : bm1));
-            const int pw = 63 - static_cast<int>(M & 63u);  // winning pair (or NP + segment)
+            const int pw = 63 - static_cast<int>(M & 63u);  // winning pair / quad (or NP / NQ + segment)
             __syncwarp();
-            if (lane == wl) spill[0] = pick_pair<NP, SPT>(pw, rp, ip, xr, xi);  // uniform jump table
+            if constexpr (QK) {
+                if (lane == wl) {
+                    float4 o0, o1;
+                    pick_quad<NQ, SPT>(pw, rp, ip, xr, xi, o0, o1);
+                    spill[0] = o0;
+                    spill[1] = o1;
+                }
+            } else {
+                if (lane == wl) spill[0] = pick_pair<NP, SPT>(pw, rp, ip, xr, xi);  // uniform jump table
+            }
             __syncwarp();
             float2 pre;
             int jw, sw;
-            float lo_w = 0.f;  // LO = false: the winning pair's smaller bin
-            {
+            float lo_w = 0.f;  // LO = false: the winning pair's (quad's) other bins
+            if constexpr (QK) {
+                const float4 q0 = spill[0], q1 = spill[1];
+                if (pw < NQ) {
+                    const float m0 = fmaf(q0.z, q0.z, q0.x * q0.x), m1 = fmaf(q0.w, q0.w, q0.y * q0.y);
+                    const float m2 = fmaf(q1.z, q1.z, q1.x * q1.x), m3 = fmaf(q1.w, q1.w, q1.y * q1.y);
+                    // the largest bin, ties to the lowest column; lo_w = the largest of the others
+                    const bool b1 = m1 > m0, b3 = m3 > m2;
+                    const float ma = b1 ? m1 : m0, oa = b1 ? m0 : m1;
+                    const float mb = b3 ? m3 : m2, ob = b3 ? m2 : m3;
+                    const bool hb = mb > ma;
+                    const int bi = hb ? (b3 ? 3 : 2) : (b1 ? 1 : 0);
+                    lo_w = fmax3(oa, ob, hb ? ma : mb);
+                    const float4 qq = (bi & 2) ? q1 : q0;
+                    pre = (bi & 1) ? make_float2(qq.y, qq.w) : make_float2(qq.x, qq.z);
+                    const int p0 = 2 * pw;
+                    sw = p0 / PPS;
+                    jw = 2 * (p0 % PPS) + bi;
+                } else {
+                    pre = make_float2(q0.x, q0.z);
+                    sw = pw - NQ;
+                    jw = SEG;
+                }
+            } else {
                 const float4 q = spill[0];
                 if (pw < NP) {
                     const float ma = fmaf(q.z, q.z, q.x * q.x), mb = fmaf(q.w, q.w, q.y * q.y);
@@ -394,6 +475,38 @@ __global__ void __launch_bounds__(128, VAR == 0 ? 3 : 2) k2v2r_kernel(K2Args a) 
                                       p + 1, kmask);
                         }
                     }
+                } else if constexpr (QK) {
+                    // quad keys: two pairs updated, one key step
+                    static_assert(PPS % 2 == 0, "whole quads per segment");
+                    if (self) {
+#pragma unroll
+                        for (int q = 0; q < PPS; q += 2) {
+                            const int p = s * PPS + q;
+                            const float2 x0 = va[q], x1 = va[q + 1];
+                            rp[p] = __ffma2_rn(n1r, x0, rp[p]);
+                            ip[p] = __ffma2_rn(n1i, x0, ip[p]);
+                            rp[p + 1] = __ffma2_rn(n1r, x1, rp[p + 1]);
+                            ip[p + 1] = __ffma2_rn(n1i, x1, ip[p + 1]);
+                            kacc_quad(A[(p / 2) % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])),
+                                      __ffma2_rn(ip[p + 1], ip[p + 1], __fmul2_rn(rp[p + 1], rp[p + 1])), p / 2, kmask);
+                        }
+                    } else {
+                        // the pair loop, the key every second pair (two pairs updated
+                        // before one key step measured 5 % slower: LDS latency exposed)
+                        float2 mprev = make_float2(0.f, 0.f);
+#pragma unroll
+                        for (int q = 0; q < PPS; ++q) {
+                            const int p = s * PPS + q;
+                            const float2 x = va[q], y = vb[q];
+                            rp[p] = __ffma2_rn(n2r, y, __ffma2_rn(n1r, x, rp[p]));
+                            ip[p] = __ffma2_rn(n2i, y, __ffma2_rn(n1i, x, ip[p]));
+                            const float2 m = __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p]));
+                            if (q & 1)
+                                kacc_quad(A[(p / 2) % ACC], mprev, m, p / 2, kmask);
+                            else
+                                mprev = m;
+                        }
+                    }
                 } else if (self) {
 #pragma unroll
                     for (int q = 0; q < PPS; ++q) {
@@ -422,7 +535,7 @@ __global__ void __launch_bounds__(128, VAR == 0 ? 3 : 2) k2v2r_kernel(K2Args a) 
                         xr[s] = fmaf(-s2 * fr, y, xr[s]);
                         xi[s] = fmaf(s2 * fi, y, xi[s]);
                     }
-                    kacc_one(A[ACC], fmaf(xi[s], xi[s], xr[s] * xr[s]), NP + s, kmask);
+                    kacc_one(A[ACC], fmaf(xi[s], xi[s], xr[s] * xr[s]), XKEY + s, kmask);
                 }
             }
         }
@@ -1394,6 +1507,7 @@ static int k2v2_launch_t(const K2Args& a, int32_t ntiles, cudaStream_t s) {
         using Cf = V2Cfg<T, PATH>;
         auto* fn = v2r_variant() == 3   ? k2v2r_kernel<T, 3>
                    : v2r_variant() == 9 ? k2v2r_kernel<T, 9>
+                   : v2r_variant() == 1 ? k2v2r_kernel<T, 1>
                                         : k2v2r_kernel<T, 0>;
         const size_t smem = (v2r_variant() == 3 || v2r_variant() == 9) ? V2Cfg<T, PATH, true>::SMEM : Cf::SMEM;
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1503,7 +1617,7 @@ bool v2h128_enabled() {
 
 // per (T, device) once: the occupancy query is not free and run_job asks every call
 int64_t k2v2_real_wave(int t, int dev, int gw) {
-    if ((t == 64 && gw == 2) || v2r_variant() != 0) return 0;  // K2v2h at T = 64 / experiments: no alignment
+    if ((t == 64 && gw == 2) || (v2r_variant() == 3 || v2r_variant() == 9)) return 0;  // K2v2h at T = 64 / experiments: no alignment
     static std::mutex mu;
     static std::map<std::pair<int, int>, int64_t> cache;
     std::lock_guard<std::mutex> lk(mu);
@@ -1521,7 +1635,7 @@ int v2_choose_real_gw(int t, int64_t real_blocks, int dev) {
         return e ? atoi(e) : 0;
     }();
     if (forced == 1 || forced == 2) return forced;
-    if (v2r_variant() != 0 || real_blocks <= 0) return 1;
+    if ((v2r_variant() == 3 || v2r_variant() == 9) || real_blocks <= 0) return 1;
     // makespan in per-block latencies: K2v2r ceil(N / W1) x 1, K2v2h ceil(N / W2) x 0.7
     // (the latency ratio measured on C4: 21 K2v2h waves take 1.04 x 14 K2v2r waves)
     static std::mutex mu;
