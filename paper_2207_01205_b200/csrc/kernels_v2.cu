@@ -587,8 +587,8 @@ struct V2TCfg {
     static constexpr size_t WBYTES = ((IMG_BYTES + 15) / 16) * 16;
     static constexpr size_t OFF_P = WBYTES;
     static constexpr size_t OFF_TW = OFF_P + sizeof(double2) * 2 * T;
-    static constexpr size_t OFF_SP = OFF_TW + sizeof(float2) * T;             // one float4 per team
-    static constexpr size_t OFF_ST = OFF_SP + sizeof(float4) * WARPS * BPW;   // one V2State per team
+    static constexpr size_t OFF_SP = OFF_TW + sizeof(float2) * T;             // two float4 rows, one slot per team
+    static constexpr size_t OFF_ST = OFF_SP + sizeof(float4) * 2 * WARPS * BPW;  // one V2State per team
     static constexpr size_t OFF_BAR = OFF_ST + 64 * WARPS * BPW;
     static constexpr size_t SMEM = OFF_BAR + 16;
     static_assert(32 % NT == 0 && NT >= 4, "whole teams per warp");
@@ -609,13 +609,17 @@ __device__ __forceinline__ unsigned team_max(unsigned v, int sub) {
     return m;
 }
 
-template <int T>
+// QK: argmax keys per bin quad (as K2v2r); false: per pair
+template <int T, bool QK>
 __global__ void __launch_bounds__(128, 4) k2v2t_kernel(K2Args a) {
     using Cf = V2TCfg<T>;
     constexpr int SEG = Cf::SEG, SPT = Cf::SPT, NT = Cf::NT, NP = Cf::NP, SRV = Cf::SRV, BPW = Cf::BPW;
     constexpr int PPS = SEG / 2;
     constexpr int ACC = 2;
     constexpr bool LO = false;
+    constexpr int NQ = NP / 2;
+    constexpr int XKEY = QK ? NQ : NP;  // key index of a segment's extra bin
+    static_assert(!QK || PPS % 2 == 0, "whole quads per segment");
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const Tile tile = a.tiles[blockIdx.x];
@@ -689,11 +693,18 @@ __global__ void __launch_bounds__(128, 4) k2v2t_kernel(K2Args a) {
         KAcc A[ACC + 1];
 #pragma unroll
         for (int k = 0; k <= ACC; ++k) A[k] = KAcc{0.f, 0.f};
+        if constexpr (QK) {
 #pragma unroll
-        for (int p = 0; p < NP; ++p) kacc_pair<LO>(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+            for (int q = 0; q < NQ; ++q)
+                kacc_quad(A[q % ACC], __ffma2_rn(ip[2 * q], ip[2 * q], __fmul2_rn(rp[2 * q], rp[2 * q])),
+                          __ffma2_rn(ip[2 * q + 1], ip[2 * q + 1], __fmul2_rn(rp[2 * q + 1], rp[2 * q + 1])), q, kmask);
+        } else {
+#pragma unroll
+            for (int p = 0; p < NP; ++p) kacc_pair<LO>(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+        }
 #pragma unroll
         for (int s = 0; s < SPT; ++s)
-            if (exs[s]) kacc_one(A[ACC], fmaf(xi[s], xi[s], xr[s] * xr[s]), NP + s, kmask);
+            if (exs[s]) kacc_one(A[ACC], fmaf(xi[s], xi[s], xr[s] * xr[s]), XKEY + s, kmask);
 
         for (int it = 0; it < a.iterations; ++it) {
             if (__all_sync(0xffffffffu, conv | flagged)) break;
@@ -711,12 +722,42 @@ __global__ void __launch_bounds__(128, 4) k2v2t_kernel(K2Args a) {
             const unsigned S = team_max<BPW>(fbits(lane == wl ? bm2 : bm1), sub);
             const int pw = 63 - static_cast<int>(M & 63u);
             __syncwarp();
-            if (lane == wl) *spill = pick_pair<NP, SPT>(pw, rp, ip, xr, xi);
+            if constexpr (QK) {
+                if (lane == wl) {
+                    float4 o0, o1;
+                    pick_quad<NQ, SPT>(pw, rp, ip, xr, xi, o0, o1);
+                    spill[0] = o0;
+                    spill[Cf::WARPS * BPW] = o1;  // the second slot row
+                }
+            } else {
+                if (lane == wl) *spill = pick_pair<NP, SPT>(pw, rp, ip, xr, xi);
+            }
             __syncwarp();
             float2 pre;
             int jw, sw;
             float lo_w = 0.f;
-            {
+            if constexpr (QK) {
+                const float4 q0 = spill[0], q1 = spill[Cf::WARPS * BPW];
+                if (pw < NQ) {
+                    const float m0 = fmaf(q0.z, q0.z, q0.x * q0.x), m1 = fmaf(q0.w, q0.w, q0.y * q0.y);
+                    const float m2 = fmaf(q1.z, q1.z, q1.x * q1.x), m3 = fmaf(q1.w, q1.w, q1.y * q1.y);
+                    const bool b1 = m1 > m0, b3 = m3 > m2;
+                    const float ma = b1 ? m1 : m0, oa = b1 ? m0 : m1;
+                    const float mb = b3 ? m3 : m2, ob = b3 ? m2 : m3;
+                    const bool hb = mb > ma;
+                    const int bi = hb ? (b3 ? 3 : 2) : (b1 ? 1 : 0);
+                    lo_w = fmax3(oa, ob, hb ? ma : mb);
+                    const float4 qq = (bi & 2) ? q1 : q0;
+                    pre = (bi & 1) ? make_float2(qq.y, qq.w) : make_float2(qq.x, qq.z);
+                    const int p0 = 2 * pw;
+                    sw = p0 / PPS;
+                    jw = 2 * (p0 % PPS) + bi;
+                } else {
+                    pre = make_float2(q0.x, q0.z);
+                    sw = pw - NQ;
+                    jw = SEG;
+                }
+            } else {
                 const float4 q = *spill;
                 if (pw < NP) {
                     const float ma = fmaf(q.z, q.z, q.x * q.x), mb = fmaf(q.w, q.w, q.y * q.y);
@@ -808,13 +849,22 @@ __global__ void __launch_bounds__(128, 4) k2v2t_kernel(K2Args a) {
                 // self-conjugate selections have no second term: s2 = 0 folds it away
                 const float t2 = self ? 0.f : s2;
                 const float2 n2r = make_float2(-t2 * fr, -t2 * fr), n2i = make_float2(t2 * fi, t2 * fi);
+                float2 mprev = make_float2(0.f, 0.f);
 #pragma unroll
                 for (int q = 0; q < PPS; ++q) {
                     const int p = s * PPS + q;
                     const float2 x = va[q], y = vb[q];
                     rp[p] = __ffma2_rn(n2r, y, __ffma2_rn(n1r, x, rp[p]));
                     ip[p] = __ffma2_rn(n2i, y, __ffma2_rn(n1i, x, ip[p]));
-                    kacc_pair<LO>(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+                    const float2 m = __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p]));
+                    if constexpr (QK) {
+                        if (q & 1)
+                            kacc_quad(A[(p / 2) % ACC], mprev, m, p / 2, kmask);
+                        else
+                            mprev = m;
+                    } else {
+                        kacc_pair<LO>(A[p % ACC], m, p, kmask);
+                    }
                 }
                 if (exs[s]) {
                     const float x = vE[rA * SRV + cA + SEG];
@@ -825,7 +875,7 @@ __global__ void __launch_bounds__(128, 4) k2v2t_kernel(K2Args a) {
                         xr[s] = fmaf(-s2 * fr, y, xr[s]);
                         xi[s] = fmaf(s2 * fi, y, xi[s]);
                     }
-                    kacc_one(A[ACC], fmaf(xi[s], xi[s], xr[s] * xr[s]), NP + s, kmask);
+                    kacc_one(A[ACC], fmaf(xi[s], xi[s], xr[s] * xr[s]), XKEY + s, kmask);
                 }
             }
         }
@@ -1498,10 +1548,15 @@ static int k2v2_launch_t(const K2Args& a, int32_t ntiles, cudaStream_t s) {
     } else if constexpr (T <= 32) {
         // several lost blocks per warp (K2v2t)
         using Cf = V2TCfg<T>;
-        cudaError_t e = cudaFuncSetAttribute(k2v2t_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
+        static const bool qk = [] {
+            const char* e = getenv("FOFSE_V2T_QK");
+            return !(e && e[0] == '0');
+        }();
+        auto* fn = qk ? k2v2t_kernel<T, true> : k2v2t_kernel<T, false>;
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
         if (e != cudaSuccess) return e;
         if (ntiles <= 0) return cudaSuccess;
-        k2v2t_kernel<T><<<ntiles, 32 * Cf::WARPS, Cf::SMEM, s>>>(a);
+        fn<<<ntiles, 32 * Cf::WARPS, Cf::SMEM, s>>>(a);
         return cudaGetLastError();
     } else {
         using Cf = V2Cfg<T, PATH>;
@@ -1578,8 +1633,8 @@ static int64_t wave_t(int dev) {
         return e == cudaSuccess ? (int64_t)nsm * per_sm * Cf::GROUPS : 0;
     } else if constexpr (T <= 32) {
         using Cf = V2TCfg<T>;
-        cudaFuncSetAttribute(k2v2t_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2v2t_kernel<T>, 32 * Cf::WARPS, Cf::SMEM);
+        cudaFuncSetAttribute(k2v2t_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2v2t_kernel<T, true>, 32 * Cf::WARPS, Cf::SMEM);
         return e == cudaSuccess ? (int64_t)nsm * per_sm * Cf::BLOCKS : 0;
     } else {
         using Cf = V2Cfg<T, PATH_F32_REAL>;
