@@ -928,7 +928,7 @@ struct V2HCfg {
     static constexpr size_t OFF_P = WBYTES;
     static constexpr size_t OFF_TW = OFF_P + sizeof(double2) * 2 * T;
     // per group: slots [2 parity][GW warps] x 32 B, red GW doubles
-    static constexpr size_t GRP = 2 * GW * 32 + 8 * GW;
+    static constexpr size_t GRP = 2 * GW * 48 + 8 * GW;  // [2][GW] slots (HSlotQ) + red
     static constexpr size_t OFF_G = OFF_TW + sizeof(float2) * T;
     static constexpr size_t OFF_BAR = OFF_G + GRP * GROUPS;
     static constexpr size_t SMEM = OFF_BAR + 16;
@@ -944,12 +944,23 @@ struct HSlot {
     float4 pair;    // the winning bin pair (re_a, re_b, im_a, im_b) or the extra bin
 };
 static_assert(sizeof(HSlot) == 32, "slot");
+struct HSlotQ {     // quad keys: the winning quad as two pairs
+    unsigned key;
+    float second;
+    int gbase;
+    int pad;
+    float4 pair, pair2;
+};
+static_assert(sizeof(HSlotQ) == 48, "slot");
 
-template <int T>
+// QK: argmax keys per bin quad (as K2v2r); false: per pair
+template <int T, bool QK>
 __global__ void __launch_bounds__(V2HCfg<T>::THREADS, V2HCfg<T>::MINB) k2v2h_kernel(K2Args a) {
     using Cf = V2HCfg<T>;
     constexpr int SEG = Cf::SEG, NT = Cf::NT, NP = Cf::NP, PPS = Cf::PPS, SRV = Cf::SRV, GW = Cf::GW;
     constexpr int ACC = 2;
+    constexpr int NQ = NP / 2;
+    using Slot = std::conditional_t<QK, HSlotQ, HSlot>;
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const Tile tile = a.tiles[blockIdx.x];
@@ -961,8 +972,8 @@ __global__ void __launch_bounds__(V2HCfg<T>::THREADS, V2HCfg<T>::MINB) k2v2h_ker
     const int grp = threadIdx.x / NT, tid = threadIdx.x % NT;
     const int w = tid >> 5, lane = tid & 31;
     unsigned char* gsm = smem_raw + Cf::OFF_G + Cf::GRP * grp;
-    HSlot* slots = reinterpret_cast<HSlot*>(gsm);  // [2 parity][GW]
-    double* red = reinterpret_cast<double*>(gsm + 2 * GW * 32);
+    Slot* slots = reinterpret_cast<Slot*>(gsm);  // [2 parity][GW]
+    double* red = reinterpret_cast<double*>(gsm + 2 * GW * sizeof(Slot));
     const int bar = 1 + grp;
 
     const BinLayout L = BinLayout::make(T, SEG, 1);
@@ -1013,9 +1024,17 @@ __global__ void __launch_bounds__(V2HCfg<T>::THREADS, V2HCfg<T>::MINB) k2v2h_ker
         KAcc A[ACC + 1];
 #pragma unroll
         for (int k = 0; k <= ACC; ++k) A[k] = KAcc{0.f, 0.f};
+        if constexpr (QK) {
 #pragma unroll
-        for (int p = 0; p < NP; ++p) kacc_pair<false>(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
-        if (ex) kacc_one(A[ACC], fmaf(xi, xi, xr * xr), NP, kmask);
+            for (int q = 0; q < NQ; ++q)
+                kacc_quad(A[q % ACC], __ffma2_rn(ip[2 * q], ip[2 * q], __fmul2_rn(rp[2 * q], rp[2 * q])),
+                          __ffma2_rn(ip[2 * q + 1], ip[2 * q + 1], __fmul2_rn(rp[2 * q + 1], rp[2 * q + 1])), q, kmask);
+        } else {
+#pragma unroll
+            for (int p = 0; p < NP; ++p) kacc_pair<false>(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+        }
+        constexpr int XKEY = QK ? NQ : NP;
+        if (ex) kacc_one(A[ACC], fmaf(xi, xi, xr * xr), XKEY, kmask);
 
         for (int it = 0; it < a.iterations && !conv; ++it) {
             const int par = it & 1;
@@ -1037,7 +1056,13 @@ __global__ void __launch_bounds__(V2HCfg<T>::THREADS, V2HCfg<T>::MINB) k2v2h_ker
             if (lane == wl) {
                 const int pw = 63 - static_cast<int>(Mw & 63u);
                 float xra[1] = {xr}, xia[1] = {xi};
-                slots[par * GW + w] = HSlot{Mw, __uint_as_float(Sw), gb, 0, pick_pair<NP, 1>(pw, rp, ip, xra, xia)};
+                if constexpr (QK) {
+                    float4 o0, o1;
+                    pick_quad<NQ, 1>(pw, rp, ip, xra, xia, o0, o1);
+                    slots[par * GW + w] = HSlotQ{Mw, __uint_as_float(Sw), gb, 0, o0, o1};
+                } else {
+                    slots[par * GW + w] = HSlot{Mw, __uint_as_float(Sw), gb, 0, pick_pair<NP, 1>(pw, rp, ip, xra, xia)};
+                }
             }
             named_bar_sync(bar, NT);
             // merge the GW warps: the winner is the largest key (keys are distinct
@@ -1053,13 +1078,31 @@ __global__ void __launch_bounds__(V2HCfg<T>::THREADS, V2HCfg<T>::MINB) k2v2h_ker
                 wsel = kv > M ? v : wsel;
                 M = max(M, kv);
             }
-            const HSlot& sw = slots[par * GW + wsel];
+            const Slot& sw = slots[par * GW + wsel];
             const float Mf = __uint_as_float(M);
             const int pw = 63 - static_cast<int>(M & 63u);
             float2 pre;
             int jw;
-            float lo_w = 0.f;  // the winning pair's smaller bin (kacc_pair<false>)
-            if (pw < NP) {
+            float lo_w = 0.f;  // the winning pair's (quad's) other bins
+            if constexpr (QK) {
+                if (pw < NQ) {
+                    const float4 q0 = sw.pair, q1 = sw.pair2;
+                    const float m0 = fmaf(q0.z, q0.z, q0.x * q0.x), m1 = fmaf(q0.w, q0.w, q0.y * q0.y);
+                    const float m2 = fmaf(q1.z, q1.z, q1.x * q1.x), m3 = fmaf(q1.w, q1.w, q1.y * q1.y);
+                    const bool b1 = m1 > m0, b3 = m3 > m2;
+                    const float ma = b1 ? m1 : m0, oa = b1 ? m0 : m1;
+                    const float mb = b3 ? m3 : m2, ob = b3 ? m2 : m3;
+                    const bool hb = mb > ma;
+                    const int bi = hb ? (b3 ? 3 : 2) : (b1 ? 1 : 0);
+                    lo_w = fmax3(oa, ob, hb ? ma : mb);
+                    const float4 qq = (bi & 2) ? q1 : q0;
+                    pre = (bi & 1) ? make_float2(qq.y, qq.w) : make_float2(qq.x, qq.z);
+                    jw = 4 * pw + bi;
+                } else {
+                    pre = make_float2(sw.pair.x, sw.pair.z);
+                    jw = SEG;
+                }
+            } else if (pw < NP) {
                 const float4 q = sw.pair;
                 const float ma = fmaf(q.z, q.z, q.x * q.x), mb = fmaf(q.w, q.w, q.y * q.y);
                 lo_w = fminf(ma, mb);
@@ -1153,8 +1196,13 @@ __global__ void __launch_bounds__(V2HCfg<T>::THREADS, V2HCfg<T>::MINB) k2v2h_ker
                     ip[p] = __ffma2_rn(n1i, make_float2(x.x, x.y), ip[p]);
                     rp[p + 1] = __ffma2_rn(n1r, make_float2(x.z, x.w), rp[p + 1]);
                     ip[p + 1] = __ffma2_rn(n1i, make_float2(x.z, x.w), ip[p + 1]);
-                    kacc_pair<false>(A[0], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
-                    kacc_pair<false>(A[1], __ffma2_rn(ip[p + 1], ip[p + 1], __fmul2_rn(rp[p + 1], rp[p + 1])), p + 1, kmask);
+                    if constexpr (QK) {
+                        kacc_quad(A[q % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])),
+                                  __ffma2_rn(ip[p + 1], ip[p + 1], __fmul2_rn(rp[p + 1], rp[p + 1])), q, kmask);
+                    } else {
+                        kacc_pair<false>(A[0], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+                        kacc_pair<false>(A[1], __ffma2_rn(ip[p + 1], ip[p + 1], __fmul2_rn(rp[p + 1], rp[p + 1])), p + 1, kmask);
+                    }
                 }
             } else {
 #pragma unroll
@@ -1165,8 +1213,13 @@ __global__ void __launch_bounds__(V2HCfg<T>::THREADS, V2HCfg<T>::MINB) k2v2h_ker
                     ip[p] = __ffma2_rn(n2i, make_float2(y.x, y.y), __ffma2_rn(n1i, make_float2(x.x, x.y), ip[p]));
                     rp[p + 1] = __ffma2_rn(n2r, make_float2(y.z, y.w), __ffma2_rn(n1r, make_float2(x.z, x.w), rp[p + 1]));
                     ip[p + 1] = __ffma2_rn(n2i, make_float2(y.z, y.w), __ffma2_rn(n1i, make_float2(x.z, x.w), ip[p + 1]));
-                    kacc_pair<false>(A[0], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
-                    kacc_pair<false>(A[1], __ffma2_rn(ip[p + 1], ip[p + 1], __fmul2_rn(rp[p + 1], rp[p + 1])), p + 1, kmask);
+                    if constexpr (QK) {
+                        kacc_quad(A[q % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])),
+                                  __ffma2_rn(ip[p + 1], ip[p + 1], __fmul2_rn(rp[p + 1], rp[p + 1])), q, kmask);
+                    } else {
+                        kacc_pair<false>(A[0], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+                        kacc_pair<false>(A[1], __ffma2_rn(ip[p + 1], ip[p + 1], __fmul2_rn(rp[p + 1], rp[p + 1])), p + 1, kmask);
+                    }
                 }
             }
             if (ex) {
@@ -1178,7 +1231,7 @@ __global__ void __launch_bounds__(V2HCfg<T>::THREADS, V2HCfg<T>::MINB) k2v2h_ker
                     xr = fmaf(-s2f * fr, y, xr);
                     xi = fmaf(s2f * fi, y, xi);
                 }
-                kacc_one(A[ACC], fmaf(xi, xi, xr * xr), NP, kmask);
+                kacc_one(A[ACC], fmaf(xi, xi, xr * xr), XKEY, kmask);
             }
         }
 
@@ -1576,10 +1629,15 @@ static int k2v2_launch_t(const K2Args& a, int32_t ntiles, cudaStream_t s) {
 template <int T>
 static int k2v2h_launch(const K2Args& a, int32_t ntiles, cudaStream_t s) {
     using Cf = V2HCfg<T>;
-    cudaError_t e = cudaFuncSetAttribute(k2v2h_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
+    static const bool qk = [] {
+        const char* e = getenv("FOFSE_V2H_QK");
+        return !(e && e[0] == '0');
+    }();
+    auto* fn = qk ? k2v2h_kernel<T, true> : k2v2h_kernel<T, false>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
     if (e != cudaSuccess) return e;
     if (ntiles <= 0) return cudaSuccess;
-    k2v2h_kernel<T><<<ntiles, Cf::NT * Cf::GROUPS, Cf::SMEM, s>>>(a);
+    fn<<<ntiles, Cf::NT * Cf::GROUPS, Cf::SMEM, s>>>(a);
     return cudaGetLastError();
 }
 
@@ -1628,8 +1686,8 @@ static int64_t wave_t(int dev) {
     cudaError_t e;
     if constexpr (T == 128) {
         using Cf = V2HCfg<128>;
-        cudaFuncSetAttribute(k2v2h_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2v2h_kernel<128>, Cf::THREADS, Cf::SMEM);
+        cudaFuncSetAttribute(k2v2h_kernel<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2v2h_kernel<128, true>, Cf::THREADS, Cf::SMEM);
         return e == cudaSuccess ? (int64_t)nsm * per_sm * Cf::GROUPS : 0;
     } else if constexpr (T <= 32) {
         using Cf = V2TCfg<T>;
@@ -1708,10 +1766,10 @@ int v2_choose_real_gw(int t, int64_t real_blocks, int dev) {
             using C1 = V2Cfg<64, PATH_F32_REAL>;
             using C2 = V2HCfg<64>;
             cudaFuncSetAttribute(k2v2r_kernel<64, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C1::SMEM);
-            cudaFuncSetAttribute(k2v2h_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C2::SMEM);
+            cudaFuncSetAttribute(k2v2h_kernel<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C2::SMEM);
             if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p1, k2v2r_kernel<64, 0>, 32 * C1::WARPS, C1::SMEM) !=
                     cudaSuccess ||
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2, k2v2h_kernel<64>, C2::THREADS, C2::SMEM) != cudaSuccess)
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2, k2v2h_kernel<64, true>, C2::THREADS, C2::SMEM) != cudaSuccess)
                 return 1;
             w1 = (int64_t)nsm * p1 * C1::WARPS;
             w2 = (int64_t)nsm * p2 * C2::GROUPS;
