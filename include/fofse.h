@@ -167,6 +167,15 @@ int fofse_conceal_frames_u8(fofse_ctx* ctx, const uint8_t* frames, int32_t n_fra
                             int32_t block_width, const fofse_params* params, uint8_t* restored,
                             double* block_sq, fofse_report* report);
 
+/* The same pipeline on fp64 frames: restored holds the unrounded concealed
+ * pixels (clamped to [0, 255]) — the batch path's output at full precision
+ * (e.g. the fp32 vs fp64 parity measurement over a whole video batch). */
+int fofse_conceal_frames_f64(fofse_ctx* ctx, const double* frames, int32_t n_frames,
+                             int32_t width, int32_t height, const fofse_rect* blocks,
+                             const int64_t* frame_offsets, int32_t block_height,
+                             int32_t block_width, const fofse_params* params, double* restored,
+                             double* block_sq, fofse_report* report);
+
 /* Page-lock (cudaHostRegister) / release a caller buffer for the frames API's
  * overlapped transfers, for callers without the CUDA runtime (FFI / ctypes). */
 int fofse_host_register(void* ptr, size_t bytes);

@@ -28,7 +28,7 @@ SUPPORT, MISSING, OUTSIDE = 0, 1, 2
 # Every symbol include/fofse.h declares (checked by tests/test_capi.py).
 EXPORTS = [
     "fofse_abi_version", "fofse_last_error", "fofse_params_default", "fofse_create",
-    "fofse_destroy", "fofse_set_stream", "fofse_conceal_f64", "fofse_conceal_frames_u8",
+    "fofse_destroy", "fofse_set_stream", "fofse_conceal_f64", "fofse_conceal_frames_u8", "fofse_conceal_frames_f64",
     "fofse_plan_frames_u8", "fofse_plan_execute_device", "fofse_plan_destroy",
     "fofse_extrapolate_windows", "fofse_spectral_init", "fofse_spectral_iterate",
     "fofse_spectral_synthesize",

@@ -28,6 +28,7 @@
 #include <limits>
 #include <map>
 #include <memory>
+#include <type_traits>
 #include <mutex>
 #include <numeric>
 #include <random>
@@ -1623,6 +1624,19 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         auto can_resume_of = [&](const Chunk& ch) {
             return resume_on && head > 0 && hi_path(ch.path) == PATH_F64_REAL && soa_of(ch.path) && k2d_replay_fits(T, I);
         };
+        // exact near-tie resolution (K2v2x) for the host-driven real chunks of the
+        // K2v2r path: the flagged block goes on in fp32 from its own state, each tie
+        // decided from fp64 coefficients rebuilt in O(nu^2) (FOFSE_ETR=0: the fp64
+        // REPLAY re-run instead)
+        const bool etr_on = [] {
+            const char* e = std::getenv("FOFSE_ETR");
+            return !(e && e[0] == '0');
+        }();
+        auto etr_of = [&](const Chunk& ch) {
+            return etr_on && can_resume_of(ch) && ch.path == PATH_F32_REAL && v2r && real_gw == 1 &&
+                   k2v2x_supported(T) && d_vimg64;
+        };
+        double* d_enf = ctx->buf("enf").as<double>(static_cast<size_t>(std::max<int64_t>(n, 1)));
         GuardPlan* d_plans = ctx->buf("gp_plan").as<GuardPlan>(std::max<size_t>(chunks.size(), 1));
         const size_t mc = static_cast<size_t>(std::max<int64_t>(max_chunk, 1));
         int32_t* g_rr_ids = ctx->buf("gp_rr_ids").as<int32_t>(mc);
@@ -1650,7 +1664,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             gp.head = head;
             gp.can_resume = can_resume_of(ch) ? 1 : 0;
             gp.ng_rr = ng_f64(PATH_F64_REAL, wide);
-            gp.ng_rs = ng_f64(PATH_F64_REAL, wide);
+            gp.ng_rs = etr_of(ch) ? 4 : ng_f64(PATH_F64_REAL, wide);  // K2v2x: 4 blocks per CTA
             gp.order = d_ids;
             gp.descs = d_sorted;
             gp.rr_ids = g_rr_ids;
@@ -1679,7 +1693,33 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
                           ctx->aux, &d_plans[ci].n_rr);
                 k2_f64(a, PATH_F64_REAL, 0, cn, none, "gr", ctx->aux, g_rr_tiles, static_cast<size_t>(cn), wide);
             }
-            if (can_resume_of(ch)) {  // resumed at the near-tie (K2d REPLAY)
+            if (etr_of(ch)) {  // resumed at the near-tie, exact resolution + fp32 (K2v2x)
+                K2Args a = base_args();
+                a.path = PATH_F32_REAL;
+                a.seg = seg32;
+                a.tau = effective_tau(cfg, head);
+                a.tiles = g_rs_tiles;
+                a.ntiles_dev = &d_plans[ci].nt_rs;
+                a.order = g_rs_ids;
+                a.blocks = g_rs_desc;
+                a.src_pos = g_rs_pos;
+                a.nu_flag = g_rs_nuf;
+                a.rin = d_R32;
+                a.rin_stride = s32;
+                a.wimg = d_vimg32;
+                a.wimg_stride = static_cast<int64_t>(vimg_elems);
+                a.flag_energy = d_enf;
+                a.init_energy = d_e0;
+                a.init_max = d_imax;
+                a.rec_global = 1;
+                a.flags = nullptr;
+                a.vimg64x = d_vimg64;
+                a.vimg64x_stride = static_cast<int64_t>(vimg64_elems);
+                a.r64x = reinterpret_cast<const double2*>(d_R64);
+                a.r64x_seg = seg64;
+                ck(k2v2x_launch(a, static_cast<int32_t>(cn), ctx->aux), "K2v2x exact near-tie resolution");  // grid: an upper bound
+                ++ctx->launches;
+            } else if (can_resume_of(ch)) {  // resumed at the near-tie (K2d REPLAY)
                 K2Args a = base_args();
                 a.order = g_rs_ids;
                 a.blocks = g_rs_desc;
@@ -1807,6 +1847,11 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
                 a.nu0 = d_nu;
                 a.conv0 = d_cvh;
             }
+            if (etr_of(ch)) {  // a near-tie block leaves its fp32 state in place for K2v2x
+                a.rout = d_R32;
+                a.rout_flagged = 1;
+                a.flag_energy = d_enf;
+            }
             ck(kv2 ? k2v2_launch(a, static_cast<int32_t>(ntl), ch.s)
                   : k2_launch(a, static_cast<int32_t>(ntl), ch.s),
                "K2 fp32");
@@ -1906,7 +1951,41 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
                 k1_packed(d_rdesc, m, hp, w ? k2d_wide_seg(T) : seg64, 1, d_Rr, d_re0, d_rimax, 0, 0, ctx->aux2);
                 k2_f64(a, hp, 0, m, rdesc, tag, ctx->aux2, nullptr, 0, w);
             }
-            if (!rs.empty()) {  // resumed: K2d REPLAY rebuilds the fp64 state at the near-tie and goes on
+            if (!rs.empty() && etr_of(ch)) {  // exact resolution at the near-tie, then fp32 (K2v2x)
+                const int64_t m = static_cast<int64_t>(rs.size());
+                int32_t* d_rpos = ctx->buf("rpos").as<int32_t>(static_cast<size_t>(max_chunk));
+                int32_t* d_rnuf = ctx->buf("rnuf").as<int32_t>(static_cast<size_t>(max_chunk));
+                upload_to(ctx, d_rdesc, sdesc.data(), sdesc.size(), ctx->aux2);
+                upload_to(ctx, d_rr, rs.data(), rs.size(), ctx->aux2);
+                upload_to(ctx, d_rpos, spos.data(), spos.size(), ctx->aux2);
+                upload_to(ctx, d_rnuf, snuf.data(), snuf.size(), ctx->aux2);
+                const std::vector<Tile> xt = make_tiles(0, m, sdesc, 4);
+                const Tile* d_xt = upload(ctx, "xtiles" + std::to_string(ci), xt.data(), xt.size(), ctx->aux2);
+                K2Args a = base_args();
+                a.path = PATH_F32_REAL;
+                a.seg = seg32;
+                a.tau = effective_tau(cfg, head);
+                a.tiles = d_xt;
+                a.order = d_rr;
+                a.blocks = d_rdesc;
+                a.src_pos = d_rpos;
+                a.nu_flag = d_rnuf;
+                a.rin = d_R32;
+                a.rin_stride = s32;
+                a.wimg = d_vimg32;
+                a.wimg_stride = static_cast<int64_t>(vimg_elems);
+                a.flag_energy = d_enf;
+                a.init_energy = d_e0;
+                a.init_max = d_imax;
+                a.rec_global = 1;
+                a.flags = nullptr;
+                a.vimg64x = d_vimg64;
+                a.vimg64x_stride = static_cast<int64_t>(vimg64_elems);
+                a.r64x = reinterpret_cast<const double2*>(d_R64);
+                a.r64x_seg = seg64;
+                ck(k2v2x_launch(a, static_cast<int32_t>(xt.size()), ctx->aux2), "K2v2x exact near-tie resolution");
+                ++ctx->launches;
+            } else if (!rs.empty()) {  // resumed: K2d REPLAY rebuilds the fp64 state at the near-tie and goes on
                 const int64_t m = static_cast<int64_t>(rs.size());
                 const std::string tag = "s" + std::to_string(ci);
                 int32_t* d_rpos = ctx->buf("rpos").as<int32_t>(static_cast<size_t>(max_chunk));
@@ -2502,9 +2581,13 @@ int fofse_plan_execute_device(fofse_plan* plan, uint8_t* d_frames, double* d_blo
 }
 
 // One batch of frames through the pipelined frames path (see fofse_conceal_frames_u8).
-static void conceal_frames_batch(fofse_ctx* ctx, const uint8_t* frames, int32_t n_frames, int32_t width,
+// P: the pixel type of the frames (uint8_t: fofse_conceal_frames_u8; double:
+// fofse_conceal_frames_f64, the same pipeline with unrounded pixels out)
+extern "C++" {
+template <class P>
+static void conceal_frames_batch(fofse_ctx* ctx, const P* frames, int32_t n_frames, int32_t width,
                                  int32_t height, const fofse_rect* blocks, const int64_t* offs, int32_t bh,
-                                 int32_t bw, const fofse_params* params, uint8_t* restored, double* block_sq,
+                                 int32_t bw, const fofse_params* params, P* restored, double* block_sq,
                                  fofse_report* report) {
     {
         ctx->activate();
@@ -2548,8 +2631,9 @@ static void conceal_frames_batch(fofse_ctx* ctx, const uint8_t* frames, int32_t 
             }
             gb[static_cast<size_t>(G)] = static_cast<int64_t>(n_frames) * height;
         }
-        auto f0 = [&](int gq) { return static_cast<size_t>(gb[static_cast<size_t>(gq)]) * width; };  // byte offset
-        uint8_t* d_fr = ctx->buf("frames_u8").as<uint8_t>(bytes);
+        auto f0 = [&](int gq) { return static_cast<size_t>(gb[static_cast<size_t>(gq)]) * width; };  // pixel offset
+        constexpr bool U8 = std::is_same<P, uint8_t>::value;
+        P* d_fr = ctx->buf(U8 ? "frames_u8" : "frames_f64").as<P>(bytes);
         std::vector<cudaEvent_t> h2d(static_cast<size_t>(G), nullptr);
         struct EvHold {
             std::vector<cudaEvent_t>& v;
@@ -2565,7 +2649,8 @@ static void conceal_frames_batch(fofse_ctx* ctx, const uint8_t* frames, int32_t 
                 ck(cudaEventCreateWithFlags(&h2d[static_cast<size_t>(gq)], cudaEventDisableTiming), "cudaEventCreate");
                 const size_t a0 = f0(gq), a1 = f0(gq + 1);
                 if (a1 > a0)
-                    ck(cudaMemcpyAsync(d_fr + a0, frames + a0, a1 - a0, cudaMemcpyHostToDevice, ctx->io), "H2D frames");
+                    ck(cudaMemcpyAsync(d_fr + a0, frames + a0, (a1 - a0) * sizeof(P), cudaMemcpyHostToDevice, ctx->io),
+                       "H2D frames");
                 ck(cudaEventRecord(h2d[static_cast<size_t>(gq)], ctx->io), "event");
             }
         };
@@ -2620,7 +2705,7 @@ static void conceal_frames_batch(fofse_ctx* ctx, const uint8_t* frames, int32_t 
         auto download_to = [&](int64_t r1, cudaStream_t s) {
             if (r1 <= down_rows) return;
             const size_t a0 = static_cast<size_t>(down_rows) * width, a1 = static_cast<size_t>(r1) * width;
-            ck(cudaMemcpyAsync(restored + a0, d_fr + a0, a1 - a0, cudaMemcpyDeviceToHost, s), "D2H frames");
+            ck(cudaMemcpyAsync(restored + a0, d_fr + a0, (a1 - a0) * sizeof(P), cudaMemcpyDeviceToHost, s), "D2H frames");
             down_rows = r1;
         };
         // group g done (groups complete in order)
@@ -2630,11 +2715,12 @@ static void conceal_frames_batch(fofse_ctx* ctx, const uint8_t* frames, int32_t 
             const int32_t r1 = std::min(r + nr, height), c1 = std::min(c + nc, width);
             if (r1 <= r0 || c1 <= c0) return;
             const size_t off = static_cast<size_t>(f) * fs + static_cast<size_t>(r0) * width + c0;
-            ck(cudaMemcpy2DAsync(restored + off, width, d_fr + off, width, c1 - c0, r1 - r0, cudaMemcpyDeviceToHost, s),
+            ck(cudaMemcpy2DAsync(restored + off, width * sizeof(P), d_fr + off, width * sizeof(P), (c1 - c0) * sizeof(P),
+                                 r1 - r0, cudaMemcpyDeviceToHost, s),
                "D2H patch");
         };
         RunOut ro;
-        fofse::Frames fr{d_fr, d_fr, fofse::SRC_U8, width, height, static_cast<int64_t>(fs)};
+        fofse::Frames fr{d_fr, d_fr, U8 ? fofse::SRC_U8 : fofse::SRC_F64, width, height, static_cast<int64_t>(fs)};
         try {
             if (n > 0)
                 ro = run_job(ctx, plan->job, plan->cfg, fr, fofse::SYN_IMAGE, d_sq, nullptr, nullptr, nullptr, nullptr,
@@ -2659,10 +2745,14 @@ static void conceal_frames_batch(fofse_ctx* ctx, const uint8_t* frames, int32_t 
     }
 }
 
-int fofse_conceal_frames_u8(fofse_ctx* ctx, const uint8_t* frames, int32_t n_frames, int32_t width,
-                            int32_t height, const fofse_rect* blocks, const int64_t* offs,
-                            int32_t bh, int32_t bw, const fofse_params* params, uint8_t* restored,
-                            double* block_sq, fofse_report* report) {
+}  // extern "C++"
+
+extern "C++" {
+template <class P>
+static int conceal_frames_impl(fofse_ctx* ctx, const P* frames, int32_t n_frames, int32_t width,
+                               int32_t height, const fofse_rect* blocks, const int64_t* offs,
+                               int32_t bh, int32_t bw, const fofse_params* params, P* restored,
+                               double* block_sq, fofse_report* report) {
     return guarded([&] {
         if (!ctx || !frames || !restored || !offs || n_frames < 1)
             throw std::invalid_argument("conceal_frames: bad argument");
@@ -2739,6 +2829,24 @@ int fofse_conceal_frames_u8(fofse_ctx* ctx, const uint8_t* frames, int32_t n_fra
             }
         }
     });
+}
+
+}  // extern "C++"
+
+int fofse_conceal_frames_u8(fofse_ctx* ctx, const uint8_t* frames, int32_t n_frames, int32_t width,
+                            int32_t height, const fofse_rect* blocks, const int64_t* offs,
+                            int32_t bh, int32_t bw, const fofse_params* params, uint8_t* restored,
+                            double* block_sq, fofse_report* report) {
+    return conceal_frames_impl(ctx, frames, n_frames, width, height, blocks, offs, bh, bw, params, restored, block_sq,
+                               report);
+}
+
+int fofse_conceal_frames_f64(fofse_ctx* ctx, const double* frames, int32_t n_frames, int32_t width,
+                             int32_t height, const fofse_rect* blocks, const int64_t* offs,
+                             int32_t bh, int32_t bw, const fofse_params* params, double* restored,
+                             double* block_sq, fofse_report* report) {
+    return conceal_frames_impl(ctx, frames, n_frames, width, height, blocks, offs, bh, bw, params, restored, block_sq,
+                               report);
 }
 
 int fofse_extrapolate_windows(fofse_ctx* ctx, const double* windows, const uint8_t* labels,

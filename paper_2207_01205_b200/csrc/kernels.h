@@ -148,6 +148,17 @@ struct K2Args {
     // tau relative -> flags[pos] = 1 + nu, no write-back; the block re-runs on the exact
     // path). exact_peak: the strict kernel's argmax compares hypot_ref(|R|) like find_peak.
     int32_t exact_peak;
+    // exact near-tie resolution (fp32 mode, K2v2x): the flagged block's fp32 residual
+    // is written back in place (rout = rin, rout_flagged) with its energy at the flag
+    // (flag_energy, by position); K2v2x resolves each near-tie from the fp64 K1
+    // spectrum (r64x, K2d packed layout of segment r64x_seg, by src_pos) and the fp64
+    // rotated V image (vimg64x, copy 0 rows of stride d_srv(T)) and goes on in fp32
+    int32_t rout_flagged;
+    double* flag_energy;
+    const double* vimg64x;
+    int64_t vimg64x_stride;
+    const double2* r64x;
+    int32_t r64x_seg;
 };
 
 // Exact init (the fp64 mode's tie re-runs): init_spectra (engine_spectral.cpp:
@@ -255,6 +266,12 @@ int pack_tiles_launch(const double* img, int64_t width, const int4* rects, int64
 
 // K2v2: single-warp fp32 iteration kernel (T <= 64); convert fp64 head state.
 int k2v2_launch(const K2Args& a, int32_t ntiles, cudaStream_t s);
+// K2v2x (T = 64 real path): guard-flagged blocks resumed at their near-tie, each
+// tie decided exactly in fp64 (O(nu^2) coefficient replay on the tie's candidate
+// bins), the iteration going on in fp32; tiles over the flagged list (order /
+// blocks / nu_flag by list index, data by src_pos)
+int k2v2x_launch(const K2Args& a, int32_t ntiles, cudaStream_t s);
+bool k2v2x_supported(int t);
 // K2d: fp64 rotated-frame iteration (PATH_F64_REAL), groups of d_group_threads(T).
 int k2d_launch(const K2Args& a, int32_t ntiles, cudaStream_t s);
 int k2d_blocks_per_cta(int T, bool wide = false);

@@ -540,19 +540,424 @@ __global__ void __launch_bounds__(128, (VAR == 3 || VAR == 9) ? 2 : 3) k2v2r_ker
             }
         }
 
-        if (a.rout && active) {
+        // rout_flagged: only a near-tie block's residual (in place, for K2v2x) and its energy
+        if (a.rout && active && (!a.rout_flagged || flagged)) {
             const size_t rs = a.rin_stride > 0 ? (size_t)a.rin_stride : (size_t)(NP + SPT) * NT * 4;
             float4* R = reinterpret_cast<float4*>(static_cast<float*>(a.rout) + (size_t)pos * rs);
 #pragma unroll
             for (int p = 0; p < NP; ++p) R[p * NT + lane] = make_float4(rp[p].x, rp[p].y, ip[p].x, ip[p].y);
 #pragma unroll
             for (int s = 0; s < SPT; ++s) R[(NP + s) * NT + lane] = make_float4(xr[s], 0.f, xi[s], 0.f);
+            if (flagged && a.flag_energy && lane == 0) a.flag_energy[pos] = st->energy;
         }
         __syncwarp();
         v2_finish<T, 32>(a, a.blocks[pos], pos, b, lane, st->energy, st->nu, conv, flagged, st->ntrace, rec_u, rec_c,
                          rstride, twi);
         __syncwarp();
     }
+}
+
+// ============================================================================
+// K2v2x: guard re-runs without the fp64 replay (fp32 mode, real path, T = 64).
+// A block flagged by K2v2r at selection nu_f (its top-2 |R'|^2 within tau) is
+// resumed from the fp32 residual K2v2r left in place at the flag. Each near-tie
+// (the first one, and any later one) is decided EXACTLY: the fp64 coefficients
+// of the selections made so far are rebuilt from K1's fp64 spectrum —
+//   R'_s[u_s] = R'_0[u_s] - sum_{r<s} (s1 a_r V[u_s - u_r] + s2 conj(a_r) V[u_s + u_r])
+// (the rotated-frame update of K2v2r / K2d restricted to one bin, O(s) per
+// coefficient, the warp's lanes splitting r) — and every candidate bin (fp32
+// |R'|^2 within 2 tau of the maximum) is evaluated the same way; the largest
+// (ties to the lowest index) is the selection, its coefficient and energy step
+// are fp64. The iteration then goes on in fp32 with the same guard. Cost per
+// block O(nu^2 / 32) instead of the fp64 replay's O(nu * H).
+// ============================================================================
+template <int T>
+__device__ __forceinline__ double2 x_exact(int k1, int c, int s, int lane, const double2* xa, const int* xu,
+                                           const double* V64, double sgn_r, double sgn_c, double2 r0) {
+    constexpr int SRV64 = d_srv(T);
+    double tr = 0.0, ti = 0.0;
+    for (int r = lane; r < s; r += 32) {
+        const int u = xu[r];
+        const int u1 = u >> 16, u2 = u & 0xffff;
+        const double2 av = xa[r];
+        const bool self = ((u1 & (T / 2 - 1)) == 0) && ((u2 & (T / 2 - 1)) == 0);
+        const int rA = (k1 - u1) & (T - 1), cA = (c - u2) & (T - 1);
+        const double s1 = ((k1 < u1) ? sgn_r : 1.0) * ((c < u2) ? sgn_c : 1.0);
+        const double va = s1 * V64[rA * SRV64 + cA];
+        tr = fma(va, av.x, tr);
+        ti = fma(va, av.y, ti);
+        if (!self) {
+            const int rB = (k1 + u1) & (T - 1), cB = (c + u2) & (T - 1);
+            const double s2 = ((k1 + u1 >= T) ? sgn_r : 1.0) * ((c + u2 >= T) ? sgn_c : 1.0);
+            const double vb = s2 * V64[rB * SRV64 + cB];
+            tr = fma(vb, av.x, tr);
+            ti = fma(-vb, av.y, ti);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        tr += __shfl_xor_sync(0xffffffffu, tr, o);
+        ti += __shfl_xor_sync(0xffffffffu, ti, o);
+    }
+    return make_double2(r0.x - tr, r0.y - ti);
+}
+
+// K1's fp64 rotated spectrum at canonical bin (k1, c) of the block at position pos
+__device__ __forceinline__ double2 x_r0(const K2Args& a, const BinLayout& L64, int pos, int k1, int c) {
+    int i, t;
+    bin_slot(L64, k1, c, &i, &t);
+    return a.r64x[(size_t)pos * L64.SLOTS + (size_t)i * L64.NT + t];
+}
+
+template <int T>
+__global__ void __launch_bounds__(128, 2) k2v2x_kernel(K2Args a) {
+    using Cf = V2Cfg<T, PATH_F32_REAL>;
+    constexpr int SEG = Cf::SEG, SPT = Cf::SPT, NT = Cf::NT, NP = Cf::NP, SRV = Cf::SRV;
+    constexpr int PPS = SEG / 2;
+    constexpr int ACC = 2;
+    constexpr int NQ = NP / 2, XKEY = NQ;
+    constexpr unsigned kmask = 0xffffffc0u;
+    static_assert(NT == 32 && NP <= 32, "one warp per block, 64 pair bins per lane");
+
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    if (a.ntiles_dev && (int)blockIdx.x >= *a.ntiles_dev) return;  // device-sized launch
+    const Tile tile = a.tiles[blockIdx.x];
+    v2_stage<Cf>(a, tile, smem_raw);
+    const float* vE = reinterpret_cast<const float*>(smem_raw);
+    const float2* ptab = reinterpret_cast<const float2*>(smem_raw + Cf::OFF_P);
+    const float2* twi = reinterpret_cast<const float2*>(smem_raw + Cf::OFF_TW);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float4* spill = reinterpret_cast<float4*>(smem_raw + Cf::OFF_SP) + warp * (NP + SPT + 1);
+    V2State* st = reinterpret_cast<V2State*>(smem_raw + Cf::OFF_ST + 64 * warp);
+    const int imax = a.iterations;
+    unsigned char* xbase = smem_raw + ((Cf::SMEM + 15) & ~size_t(15));
+    double2* xa = reinterpret_cast<double2*>(xbase) + (size_t)warp * imax;   // exact coefficients a_s
+    int* xu = reinterpret_cast<int*>(xbase + sizeof(double2) * Cf::WARPS * imax) + (size_t)warp * imax;
+
+    const BinLayout L = BinLayout::make(T, SEG, SPT);
+    int k1s[SPT], c0s[SPT], exs[SPT];
+#pragma unroll
+    for (int s = 0; s < SPT; ++s) L.thread_segment(lane, s, &k1s[s], &c0s[s], &exs[s]);
+    const int gb0 = k1s[0] * T + c0s[0];
+    const int gb1 = k1s[SPT - 1] * T + c0s[SPT - 1];
+    const float sgn_r = ((a.Lh - 1) & 1) ? -1.f : 1.f;
+    const float sgn_c = ((a.Lw - 1) & 1) ? -1.f : 1.f;
+    const double sgn_rd = sgn_r, sgn_cd = sgn_c;
+    const float tau1 = a.tau1f;
+    const float tau2 = (float)(1.0 - 2.0 * a.tau);  // candidates: within 2 tau of the maximum
+    const int rstride = a.rec_stride > 0 ? a.rec_stride : a.iterations;
+    const int lh1 = a.Lh - 1, lw1 = a.Lw - 1;
+    const BinLayout L64 = BinLayout::make(T, a.r64x_seg, 1);
+    const double* V64 = a.vimg64x + (size_t)tile.cls * a.vimg64x_stride;
+    constexpr int SRV64 = d_srv(T);
+    const double w0d = a.w0[tile.cls], gwd = a.gamma / w0d;
+
+    for (int bi = warp; bi < tile.count; bi += Cf::WARPS) {
+        const int j = tile.begin + bi;  // index into the flagged list
+        const int b = a.order[j];
+        const int pos = a.src_pos[j];
+        const int nuf = a.nu_flag[j];
+        float2 rp[NP], ip[NP];
+        float xr[SPT], xi[SPT];
+        {
+            const size_t rs = a.rin_stride > 0 ? (size_t)a.rin_stride : (size_t)(NP + SPT) * NT * 4;
+            const float4* R = reinterpret_cast<const float4*>(static_cast<const float*>(a.rin) + (size_t)pos * rs);
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+                const float4 u = R[p * NT + lane];
+                rp[p] = make_float2(u.x, u.y);
+                ip[p] = make_float2(u.z, u.w);
+            }
+#pragma unroll
+            for (int s = 0; s < SPT; ++s) {
+                const float4 u = R[(NP + s) * NT + lane];
+                xr[s] = u.x;
+                xi[s] = u.z;
+            }
+        }
+        const double e_init = a.init_energy[pos];
+        if (lane == 0) {
+            const double im = 1e-12 * a.init_max[pos];
+            st->energy = a.flag_energy[pos];
+            st->thr_e = 1e-12 * e_init;
+            st->thr_m = (float)(im * im);
+            st->w0 = (float)w0d;
+            st->gw = (float)gwd;
+            st->nu = nuf;
+            st->ntrace = nuf;
+        }
+        int* rec_u = a.rec_u_g + (size_t)b * rstride;
+        double2* rec_c = a.rec_c_g + (size_t)b * rstride;
+        for (int r = lane; r < nuf; r += 32) xu[r] = rec_u[r];
+        int conv = e_init <= 0.0;
+        int nu = nuf;
+        int nex = 0;           // exact coefficients known for selections [0, nex)
+        bool pending = true;   // the flagged selection: decided exactly first
+        __syncwarp();
+
+        KAcc A[ACC + 1];
+#pragma unroll
+        for (int k = 0; k <= ACC; ++k) A[k] = KAcc{0.f, 0.f};
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+            kacc_quad(A[q % ACC], __ffma2_rn(ip[2 * q], ip[2 * q], __fmul2_rn(rp[2 * q], rp[2 * q])),
+                      __ffma2_rn(ip[2 * q + 1], ip[2 * q + 1], __fmul2_rn(rp[2 * q + 1], rp[2 * q + 1])), q, kmask);
+#pragma unroll
+        for (int s = 0; s < SPT; ++s)
+            if (exs[s]) kacc_one(A[ACC], fmaf(xi[s], xi[s], xr[s] * xr[s]), XKEY + s, kmask);
+
+        while (nu < a.iterations && !conv) {
+            float bm1 = A[0].m1, bm2 = A[0].m2;
+#pragma unroll
+            for (int k = 1; k <= ACC; ++k) {
+                bm2 = fmax3(bm2, A[k].m2, fminf(bm1, A[k].m1));
+                bm1 = fmaxf(bm1, A[k].m1);
+            }
+            const unsigned M = __reduce_max_sync(0xffffffffu, fbits(bm1));
+            const bool cand = fbits(bm1) == M;
+            const int wl = __ffs(__ballot_sync(0xffffffffu, cand)) - 1;
+            const unsigned S = __reduce_max_sync(0xffffffffu, fbits(lane == wl ? bm2 : bm1));
+            const int pw = 63 - static_cast<int>(M & 63u);
+            __syncwarp();
+            if (lane == wl) {
+                float4 o0, o1;
+                pick_quad<NQ, SPT>(pw, rp, ip, xr, xi, o0, o1);
+                spill[0] = o0;
+                spill[1] = o1;
+            }
+            __syncwarp();
+            float2 pre;
+            int jw, sw;
+            float lo_w = 0.f;
+            {
+                const float4 q0 = spill[0], q1 = spill[1];
+                if (pw < NQ) {
+                    const float m0 = fmaf(q0.z, q0.z, q0.x * q0.x), m1 = fmaf(q0.w, q0.w, q0.y * q0.y);
+                    const float m2 = fmaf(q1.z, q1.z, q1.x * q1.x), m3 = fmaf(q1.w, q1.w, q1.y * q1.y);
+                    const bool b1 = m1 > m0, b3 = m3 > m2;
+                    const float ma = b1 ? m1 : m0, oa = b1 ? m0 : m1;
+                    const float mb = b3 ? m3 : m2, ob = b3 ? m2 : m3;
+                    const bool hb = mb > ma;
+                    const int bq = hb ? (b3 ? 3 : 2) : (b1 ? 1 : 0);
+                    lo_w = fmax3(oa, ob, hb ? ma : mb);
+                    const float4 qq = (bq & 2) ? q1 : q0;
+                    pre = (bq & 1) ? make_float2(qq.y, qq.w) : make_float2(qq.x, qq.z);
+                    const int p0 = 2 * pw;
+                    sw = p0 / PPS;
+                    jw = 2 * (p0 % PPS) + bq;
+                } else {
+                    pre = make_float2(q0.x, q0.z);
+                    sw = pw - NQ;
+                    jw = SEG;
+                }
+            }
+            int G = __shfl_sync(0xffffffffu, (SPT == 2 && sw == 1) ? gb1 : gb0, wl) + jw;
+            const float Mf = __uint_as_float(M), Sf = fmaxf(__uint_as_float(S), lo_w);
+            const double energy = st->energy;
+            if (energy < st->thr_e || !(Mf > 0.f) || Mf < st->thr_m) {
+                conv = 1;
+                break;
+            }
+            int u1, u2, self;
+            float fr, fi;
+            double delta, cre, cim;
+            if (pending || Sf > Mf * tau1) {
+                // ---- exact decision: fp64 coefficients of selections [nex, nu) ----
+                for (int s = nex; s < nu; ++s) {
+                    const int u = xu[s];
+                    const int su1 = u >> 16, su2 = u & 0xffff;
+                    const double2 r0 = x_r0(a, L64, pos, su1, su2);
+                    const double2 rs = x_exact<T>(su1, su2, s, lane, xa, xu, V64, sgn_rd, sgn_cd, r0);
+                    const int sself = ((su1 & (T / 2 - 1)) == 0) && ((su2 & (T / 2 - 1)) == 0);
+                    const double2 P = a.ptab[(su1 * lh1 + su2 * lw1) & (2 * T - 1)];
+                    double ar = rs.x * gwd, ai = rs.y * gwd;
+                    if (sself) {
+                        const double c_re = ar * P.x - ai * P.y;
+                        ar = c_re * P.x;
+                        ai = -c_re * P.y;
+                    }
+                    if (lane == 0) xa[s] = make_double2(ar, ai);
+                    __syncwarp();
+                }
+                nex = nu;
+                // candidates: bins whose fp32 |R'|^2 is within 2 tau of the maximum
+                const float thr = Mf * tau2;
+                unsigned long long cm = 0ull;
+                unsigned cx = 0u;
+#pragma unroll
+                for (int p = 0; p < NP; ++p) {
+                    const float2 m = __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p]));
+                    if (m.x >= thr) cm |= 1ull << (2 * p);
+                    if (m.y >= thr) cm |= 1ull << (2 * p + 1);
+                }
+#pragma unroll
+                for (int s = 0; s < SPT; ++s)
+                    if (exs[s] && fmaf(xi[s], xi[s], xr[s] * xr[s]) >= thr) cx |= 1u << s;
+                double bestv = -1.0;
+                int bestG = 0x7fffffff;
+                double2 bestR = make_double2(0.0, 0.0);
+                while (true) {
+                    const unsigned has = __ballot_sync(0xffffffffu, (cm | cx) != 0ull);
+                    if (!has) break;
+                    const int src = __ffs(has) - 1;
+                    int Gc = 0;
+                    if (lane == src) {
+                        if (cm) {
+                            const int bit = __ffsll(static_cast<long long>(cm)) - 1;
+                            cm &= cm - 1;
+                            const int p = bit >> 1, s = p / PPS;
+                            Gc = k1s[s] * T + c0s[s] + 2 * (p % PPS) + (bit & 1);
+                        } else {
+                            const int s = __ffs(cx) - 1;
+                            cx &= cx - 1;
+                            Gc = k1s[s] * T + c0s[s] + SEG;
+                        }
+                    }
+                    Gc = __shfl_sync(0xffffffffu, Gc, src);
+                    const int ck1 = Gc / T, cc = Gc % T;
+                    const double2 r0 = x_r0(a, L64, pos, ck1, cc);
+                    const double2 R = x_exact<T>(ck1, cc, nu, lane, xa, xu, V64, sgn_rd, sgn_cd, r0);
+                    const double v = fma(R.y, R.y, R.x * R.x);
+                    if (v > bestv || (v == bestv && Gc < bestG)) {
+                        bestv = v;
+                        bestG = Gc;
+                        bestR = R;
+                    }
+                }
+                G = bestG;
+                u1 = G / T;
+                u2 = G % T;
+                self = ((u1 & (T / 2 - 1)) == 0) && ((u2 & (T / 2 - 1)) == 0);
+                const double pr = bestR.x, pi = bestR.y;
+                const double2 P = a.ptab[(u1 * lh1 + u2 * lw1) & (2 * T - 1)];
+                const double ar = pr * gwd, ai = pi * gwd;
+                cre = ar * P.x - ai * P.y;
+                cim = ar * P.y + ai * P.x;
+                double a_re = ar, a_im = ai;
+                if (self) {
+                    cim = 0.0;
+                    a_re = cre * P.x;
+                    a_im = -cre * P.y;
+                    delta = cre * (cre * w0d - 2.0 * (pr * P.x - pi * P.y));
+                } else {
+                    const int mi1 = 2 * u1, mi2 = 2 * u2;
+                    const double v2 = V64[(mi1 & (T - 1)) * SRV64 + (mi2 & (T - 1))];
+                    const double sig = ((mi1 >= T) ? sgn_rd : 1.0) * ((mi2 >= T) ? sgn_cd : 1.0);
+                    delta = -4.0 * (a_re * pr + a_im * pi) + 2.0 * (a_re * a_re + a_im * a_im) * w0d +
+                            2.0 * sig * v2 * (a_re * a_re - a_im * a_im);
+                }
+                if (lane == 0) xa[nu] = make_double2(a_re, a_im);
+                nex = nu + 1;
+                fr = (float)a_re;
+                fi = (float)a_im;
+                pending = false;
+            } else {
+                // ---- fp32 scalar part (K2v2r) ----
+                u1 = G / T;
+                u2 = G % T;
+                self = ((u1 & (T / 2 - 1)) == 0) && ((u2 & (T / 2 - 1)) == 0);
+                const float pr = pre.x, pi = pre.y;
+                const float w0 = st->w0, gw = st->gw;
+                const float2 P = ptab[(u1 * lh1 + u2 * lw1) & (2 * T - 1)];
+                const float ar = pr * gw, ai = pi * gw;
+                float c_re = ar * P.x - ai * P.y, c_im = ar * P.y + ai * P.x;
+                float a_re = ar, a_im = ai;
+                float d32;
+                if (self) {
+                    c_im = 0.f;
+                    a_re = c_re * P.x;
+                    a_im = -c_re * P.y;
+                    d32 = c_re * (c_re * w0 - 2.f * (pr * P.x - pi * P.y));
+                } else {
+                    const int mi1 = 2 * u1, mi2 = 2 * u2;
+                    const float v2 = vE[(mi1 & (T - 1)) * SRV + (mi2 & (T - 1))];
+                    const float sig = ((mi1 >= T) ? sgn_r : 1.f) * ((mi2 >= T) ? sgn_c : 1.f);
+                    d32 = -4.f * (a_re * pr + a_im * pi) + 2.f * (a_re * a_re + a_im * a_im) * w0 +
+                          2.f * sig * v2 * (a_re * a_re - a_im * a_im);
+                }
+                delta = (double)d32;
+                cre = c_re;
+                cim = c_im;
+                fr = a_re;
+                fi = a_im;
+            }
+            __syncwarp();
+            if (lane == 0) {
+                const double e = energy + delta;
+                if (nu < rstride) {
+                    rec_u[nu] = (u1 << 16) | u2;
+                    rec_c[nu] = self ? make_double2(cre, 0.0) : make_double2(2.0 * cre, 2.0 * cim);
+                }
+                xu[nu] = (u1 << 16) | u2;
+                st->energy = 0.0 < e ? e : 0.0;
+                st->nu = nu + 1;
+                st->ntrace = nu + 1;
+            }
+            nu += 1;
+            __syncwarp();
+            // ---- residual update in fp32 (K2v2r) + the next scan ----
+            const int par = u2 & 1;
+            const float* vimg = vE + par * (T * SRV);
+#pragma unroll
+            for (int k = 0; k <= ACC; ++k) A[k] = KAcc{0.f, 0.f};
+#pragma unroll
+            for (int s = 0; s < SPT; ++s) {
+                const int k1 = k1s[s], c0 = c0s[s];
+                const int rA = (k1 - u1) & (T - 1), rB = (k1 + u1) & (T - 1);
+                const int cA = (c0 - u2) & (T - 1), cB = (c0 + u2) & (T - 1);
+                const float s1 = ((k1 < u1) ? sgn_r : 1.f) * ((c0 < u2) ? sgn_c : 1.f);
+                const float s2 = ((k1 + u1 >= T) ? sgn_r : 1.f) * ((c0 + u2 >= T) ? sgn_c : 1.f);
+                const float t2 = self ? 0.f : s2;
+                const float2* va = reinterpret_cast<const float2*>(vimg + rA * SRV + (cA - par));
+                const float2* vb = reinterpret_cast<const float2*>(vimg + rB * SRV + (cB - par));
+                const float2 n1r = make_float2(-s1 * fr, -s1 * fr), n1i = make_float2(-s1 * fi, -s1 * fi);
+                const float2 n2r = make_float2(-t2 * fr, -t2 * fr), n2i = make_float2(t2 * fi, t2 * fi);
+                float2 mprev = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int q = 0; q < PPS; ++q) {
+                    const int p = s * PPS + q;
+                    const float2 x = va[q], y = vb[q];
+                    rp[p] = __ffma2_rn(n2r, y, __ffma2_rn(n1r, x, rp[p]));
+                    ip[p] = __ffma2_rn(n2i, y, __ffma2_rn(n1i, x, ip[p]));
+                    const float2 m = __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p]));
+                    if (q & 1)
+                        kacc_quad(A[(p / 2) % ACC], mprev, m, p / 2, kmask);
+                    else
+                        mprev = m;
+                }
+                if (exs[s]) {
+                    const float x = vE[rA * SRV + cA + SEG];
+                    xr[s] = fmaf(-s1 * fr, x, xr[s]);
+                    xi[s] = fmaf(-s1 * fi, x, xi[s]);
+                    if (!self) {
+                        const float y = vE[rB * SRV + cB + SEG];
+                        xr[s] = fmaf(-s2 * fr, y, xr[s]);
+                        xi[s] = fmaf(s2 * fi, y, xi[s]);
+                    }
+                    kacc_one(A[ACC], fmaf(xi[s], xi[s], xr[s] * xr[s]), XKEY + s, kmask);
+                }
+            }
+        }
+        __syncwarp();
+        v2_finish<T, 32>(a, a.blocks[j], j, b, lane, st->energy, st->nu, conv, 0, st->ntrace, rec_u, rec_c,
+                         rstride, twi);
+        __syncwarp();
+    }
+}
+
+bool k2v2x_supported(int t) { return t == 64; }
+
+int k2v2x_launch(const K2Args& args, int32_t ntiles, cudaStream_t s) {
+    if (args.T != 64) return cudaErrorInvalidValue;
+    K2Args a = args;
+    a.tau1f = (float)(1.0 - a.tau);
+    using Cf = V2Cfg<64, PATH_F32_REAL>;
+    const size_t smem = ((Cf::SMEM + 15) & ~size_t(15)) + (sizeof(double2) + sizeof(int)) * Cf::WARPS * (size_t)a.iterations;
+    cudaError_t e = cudaFuncSetAttribute(k2v2x_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    if (ntiles <= 0) return cudaSuccess;
+    k2v2x_kernel<64><<<ntiles, 32 * Cf::WARPS, smem, s>>>(a);
+    return cudaGetLastError();
 }
 
 // ============================================================================

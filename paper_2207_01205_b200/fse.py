@@ -236,9 +236,12 @@ def conceal_shard(image: np.ndarray, pattern: LossPattern, first: int, count: in
 
 def conceal_frames(frames: np.ndarray, patterns: list, config: ConcealConfig | None = None,
                    device: int = 0, inplace: bool = False):
-    """Batched uint8 frames (video). Returns (restored u8 frames, per-block sq errors, report)."""
+    """Batched frames (video). uint8 frames: restored uint8 (rounded like write_pgm);
+    float64 frames: the same pipeline with the unrounded concealed pixels.
+    Returns (restored frames, per-block sq errors, report)."""
     config = config or ConcealConfig()
-    frames = np.ascontiguousarray(frames, np.uint8)
+    f64 = np.asarray(frames).dtype == np.float64
+    frames = np.ascontiguousarray(frames, np.float64 if f64 else np.uint8)
     f, h, w = frames.shape
     if len(patterns) != f:
         raise ValueError("one LossPattern per frame is required")
@@ -256,10 +259,16 @@ def conceal_frames(frames: np.ndarray, patterns: list, config: ConcealConfig | N
     sq = np.zeros(len(rects), np.float64)
     rep = capi.Report()
     ctx = capi.context(device)
-    capi.check(capi.lib().fofse_conceal_frames_u8(
-        ctx.handle, capi.ptr(frames, C.c_uint8), f, w, h,
-        rects.ctypes.data_as(C.POINTER(capi.Rect_)), capi.ptr(offs, C.c_int64), bh, bw,
-        C.byref(config.params()), capi.ptr(out, C.c_uint8), capi.ptr(sq), C.byref(rep)))
+    if f64:
+        capi.check(capi.lib().fofse_conceal_frames_f64(
+            ctx.handle, capi.ptr(frames), f, w, h,
+            rects.ctypes.data_as(C.POINTER(capi.Rect_)), capi.ptr(offs, C.c_int64), bh, bw,
+            C.byref(config.params()), capi.ptr(out), capi.ptr(sq), C.byref(rep)))
+    else:
+        capi.check(capi.lib().fofse_conceal_frames_u8(
+            ctx.handle, capi.ptr(frames, C.c_uint8), f, w, h,
+            rects.ctypes.data_as(C.POINTER(capi.Rect_)), capi.ptr(offs, C.c_int64), bh, bw,
+            C.byref(config.params()), capi.ptr(out, C.c_uint8), capi.ptr(sq), C.byref(rep)))
     return out, sq, _report(config, rep)
 
 

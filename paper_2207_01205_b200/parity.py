@@ -1,11 +1,13 @@
 """fp32 fast mode vs the fp64 path on whole workloads (north_star fp32 bar:
 max |pixel error| <= 0.5 and PSNR of the concealed blocks within 0.05 dB).
 
-Both arms run on the GPU through ``fse.conceal`` (fofse_conceal_f64: the same
-kernels and parameters as the frames API, with unrounded f64 pixels out).
-The fp64 arm is the path pinned to the oracle by the GPU parity tests, so a
-block within 0.5 px of it is within 0.5 px of the reference up to the fp64
-path's own 1e-9.
+Both arms run on the GPU through the batch path the bench times
+(``fse.conceal_frames`` on fp64 frames = fofse_conceal_frames_f64: the same
+plan, chunk pipeline, kernels — K2v2r / K2v2h / K2v2t, guard, exact near-tie
+resolution — and parameters as the u8 frames API, with the unrounded pixels
+out), ``per_call`` frames at a time. The fp64 arm is the path pinned to the
+oracle by the GPU parity tests, so a block within 0.5 px of it is within
+0.5 px of the reference up to the fp64 path's own 1e-9.
 """
 from __future__ import annotations
 
@@ -24,10 +26,12 @@ def _block_max(d: np.ndarray, rects, bh: int, bw: int) -> np.ndarray:
     return np.array([d[r.row:r.row + bh, r.col:r.col + bw].max() for r in rects], np.float64)
 
 
-def fp32_vs_fp64(wl, seed: int, frames: int | None = None, cfg32=None, device: int = 0) -> dict:
+def fp32_vs_fp64(wl, seed: int, frames: int | None = None, cfg32=None, device: int = 0,
+                 per_call: int = 32) -> dict:
     """Run every frame of workload `wl` (frame f from seed + f) in fp32 (``cfg32``,
     default: the workload's fp32 config with the library's default head / guard)
-    and in fp64; compare pixel by pixel over all lost blocks."""
+    and in fp64, ``per_call`` frames per batch call; compare pixel by pixel over
+    all lost blocks."""
     nf = wl.frames if frames is None else frames
     cfg64 = wl.config("fp64")
     cfg32 = cfg32 or wl.config("fp32")
@@ -38,31 +42,41 @@ def fp32_vs_fp64(wl, seed: int, frames: int | None = None, cfg32=None, device: i
     npx = 0
     dpsnr_frame = 0.0
     worst = None
-    for f in range(nf):
-        img, pat = wl.frame(seed, f)
-        img = img.astype(np.float64)
-        o64 = fse.conceal(img, pat, cfg64, device)
-        o32 = fse.conceal(img, pat, cfg32, device)
-        d = np.abs(o32.restored - o64.restored)
-        bm = _block_max(d, pat.blocks, bh, bw)
-        blocks += len(bm)
-        over += int((bm > 0.5).sum())
-        if len(bm) and bm.max() > max_px:
-            max_px = float(bm.max())
-            worst = {"frame": f, "block": int(bm.argmax())}
-        reruns += int(o32.report.device["guard_reruns"])
-        e32 = o32.restored - img
-        e64 = o64.restored - img
-        sq32 += float((e32 * e32).sum())  # restored == image outside the lost blocks
-        sq64 += float((e64 * e64).sum())
-        npx += len(pat.blocks) * bh * bw
-        if not (o32.report.psnr_identical or o64.report.psnr_identical):
-            dpsnr_frame = max(dpsnr_frame, abs(o32.report.psnr_db - o64.report.psnr_db))
 
-    def db(sq):
-        return math.inf if sq == 0.0 else 10.0 * math.log10(255.0 * 255.0 / (sq / max(npx, 1)))
+    def db(sq, n):
+        return math.inf if sq == 0.0 else 10.0 * math.log10(255.0 * 255.0 / (sq / max(n, 1)))
+
+    for f0 in range(0, nf, max(1, per_call)):
+        nb = min(nf - f0, max(1, per_call))
+        imgs, rects, offs = wl.batch(seed, frames=nb, first=f0)
+        imgs = imgs.astype(np.float64)
+        pats = []
+        for f in range(nb):
+            rr = rects[offs[f]:offs[f + 1]]
+            pats.append(fse.LossPattern(wl.width, wl.height, bh, bw,
+                                        [fse.Rect(int(r["row"]), int(r["col"]), bh, bw) for r in rr]))
+        o64, s64, _ = fse.conceal_frames(imgs, pats, cfg64, device)
+        o32, s32, rep32 = fse.conceal_frames(imgs, pats, cfg32, device)
+        reruns += int(rep32.device["guard_reruns"])
+        for f in range(nb):
+            pat = pats[f]
+            d = np.abs(o32[f] - o64[f])
+            bm = _block_max(d, pat.blocks, bh, bw)
+            blocks += len(bm)
+            over += int((bm > 0.5).sum())
+            if len(bm) and bm.max() > max_px:
+                max_px = float(bm.max())
+                worst = {"frame": f0 + f, "block": int(bm.argmax())}
+            e32 = float(s32[offs[f]:offs[f + 1]].sum())  # per-block squared errors vs the input
+            e64 = float(s64[offs[f]:offs[f + 1]].sum())
+            sq32 += e32
+            sq64 += e64
+            n = len(pat.blocks) * bh * bw
+            npx += n
+            if e32 > 0.0 and e64 > 0.0:
+                dpsnr_frame = max(dpsnr_frame, abs(db(e32, n) - db(e64, n)))
 
     return {"frames": nf, "blocks": blocks, "max_px": max_px, "blocks_over_0.5": over,
-            "dpsnr_db": abs(db(sq32) - db(sq64)), "max_frame_dpsnr_db": dpsnr_frame,
+            "dpsnr_db": abs(db(sq32, npx) - db(sq64, npx)), "max_frame_dpsnr_db": dpsnr_frame,
             "guard_reruns": reruns, "rerun_frac": reruns / max(blocks, 1), "worst": worst,
-            "psnr_fp32_db": db(sq32), "psnr_fp64_db": db(sq64)}
+            "psnr_fp32_db": db(sq32, npx), "psnr_fp64_db": db(sq64, npx), "per_call": per_call}

@@ -1,0 +1,4 @@
+set -x
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/etr_tests.log 2>&1; echo tests rc=$?
+tail -3 gpurun_out/etr_tests.log
+bash tools/gpu/abn.sh etr4 3 FOFSE_ETR=0 FOFSE_ETR=1
