@@ -1637,6 +1637,19 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
                    k2v2x_supported(T) && d_vimg64;
         };
         double* d_enf = ctx->buf("enf").as<double>(static_cast<size_t>(std::max<int64_t>(n, 1)));
+        // K1H: spectra + fp64 head in one kernel for the K2v2r chunks (no fp64 spectrum in
+        // HBM; K2v2x recomputes K1 for its few flagged blocks). Measured (C4, same box):
+        // 45k warp instructions per block against 26k for K1f + the K2d head (256
+        // threads x 8 bins: the per-selection controller runs on twice the threads),
+        // 3.07 vs 3.12 M blocks/s — off by default; FOFSE_K1H=1 turns it on
+        const bool k1h_on = [] {
+            const char* e = std::getenv("FOFSE_K1H");
+            return e && e[0] == '1';
+        }();
+        auto k1h_of = [&](const Chunk& ch) {
+            return k1h_on && etr_of(ch) && T == 64 && head > 0 && !d_trace && !d_gap && g.Lh <= 64 && g.Lw <= 64;
+        };
+        const size_t rx_bytes = r64_bytes;  // K2v2x: K1 recomputed for the flagged list (K2d layout)
         GuardPlan* d_plans = ctx->buf("gp_plan").as<GuardPlan>(std::max<size_t>(chunks.size(), 1));
         const size_t mc = static_cast<size_t>(std::max<int64_t>(max_chunk, 1));
         int32_t* g_rr_ids = ctx->buf("gp_rr_ids").as<int32_t>(mc);
@@ -1650,6 +1663,9 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         char* g_Rr = ctx->buf("gp_Rr").as<char>(mc * rr_bytes);
         double* g_re0 = ctx->buf("gp_re0").as<double>(mc);
         double* g_rimax = ctx->buf("gp_rimax").as<double>(mc);
+        char* g_Rx = ctx->buf("gp_Rx").as<char>(mc * r64_bytes);  // K2v2x: K1 of the flagged list
+        double* g_xe0 = ctx->buf("gp_xe0").as<double>(mc);
+        double* g_xim = ctx->buf("gp_xim").as<double>(mc);
         // event slots after the chunks' three: [3 * nchunks + ci] = chunk ci's guard re-runs done
         const size_t ev_guard = 3 * chunks.size();
         auto enqueue_device_guard = [&](size_t ci) {
@@ -1694,6 +1710,12 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
                 k2_f64(a, PATH_F64_REAL, 0, cn, none, "gr", ctx->aux, g_rr_tiles, static_cast<size_t>(cn), wide);
             }
             if (etr_of(ch)) {  // resumed at the near-tie, exact resolution + fp32 (K2v2x)
+                // K1's fp64 spectra of the flagged blocks: in place, or recomputed (device count)
+                // when K1H kept none in HBM
+                const bool xk1 = k1h_of(ch);
+                if (xk1)
+                    k1_packed(g_rs_desc, cn, PATH_F64_REAL, seg64, 1, g_Rx, g_xe0, g_xim, 0, 0, ctx->aux,
+                              &d_plans[ci].n_rs);
                 K2Args a = base_args();
                 a.path = PATH_F32_REAL;
                 a.seg = seg32;
@@ -1715,8 +1737,9 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
                 a.flags = nullptr;
                 a.vimg64x = d_vimg64;
                 a.vimg64x_stride = static_cast<int64_t>(vimg64_elems);
-                a.r64x = reinterpret_cast<const double2*>(d_R64);
+                a.r64x = reinterpret_cast<const double2*>(xk1 ? g_Rx : d_R64);
                 a.r64x_seg = seg64;
+                a.r64x_by_list = xk1 ? 1 : 0;
                 ck(k2v2x_launch(a, static_cast<int32_t>(cn), ctx->aux), "K2v2x exact near-tie resolution");  // grid: an upper bound
                 ++ctx->launches;
             } else if (can_resume_of(ch)) {  // resumed at the near-tie (K2d REPLAY)
@@ -1768,7 +1791,42 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
                 ck(cudaEventRecord(ctx->event(3 * ci + 2), ch.s), "event");
                 continue;
             }
-            if (head > 0) {
+            if (k1h_of(ch)) {
+                K1Args k{};
+                k.T = T;
+                k.Lh = g.Lh;
+                k.Lw = g.Lw;
+                k.n = static_cast<int32_t>(cn);
+                k.blocks = d_sorted + ch.b0;
+                k.fr = fr;
+                k.wcls = d_wcls;
+                k.mode = K1_PACKED;
+                k.path = ch.path;
+                k.seg = seg32;
+                k.spt = spt_of(ch.path);
+                k.soa = 1;
+                k.out_stride = s32;
+                k.out = d_R32 + static_cast<size_t>(ch.b0) * sizeof(float) * s32;
+                k.energy = d_e0 + ch.b0;
+                k.init_max = d_imax + ch.b0;
+                k.twid = d_twf;
+                k.ptab = d_ptab;
+                k.head = head;
+                k.gamma = effective_gamma(cfg);
+                k.vimg64h = d_vimg64;
+                k.vimg64h_stride = static_cast<int64_t>(vimg64_elems);
+                k.w0c = d_w0;
+                k.order = d_ids + ch.b0;
+                k.rec_u = d_rec_u;
+                k.rec_c = d_rec_c;
+                k.rec_stride = I;
+                k.energy_out = d_en + ch.b0;
+                k.nu_out = d_nu + ch.b0;
+                k.conv_out = d_cvh + ch.b0;
+                ck(k1h_launch(k, ps), "K1H spectra + fp64 head");
+                ++ctx->launches;
+                ck(cudaEventRecord(ctx->event(ev_k1 + ci), ps), "event");
+            } else if (head > 0) {
                 k1_packed(d_sorted + ch.b0, cn, hi_path(ch.path), seg64, 1,
                           d_R64 + static_cast<size_t>(ch.b0) * r64_bytes, d_e0 + ch.b0, d_imax + ch.b0, 0, 0, ps);
                 ck(cudaEventRecord(ctx->event(ev_k1 + ci), ps), "event");
@@ -1961,6 +2019,15 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
                 upload_to(ctx, d_rnuf, snuf.data(), snuf.size(), ctx->aux2);
                 const std::vector<Tile> xt = make_tiles(0, m, sdesc, 4);
                 const Tile* d_xt = upload(ctx, "xtiles" + std::to_string(ci), xt.data(), xt.size(), ctx->aux2);
+                // K1's fp64 spectra of the flagged blocks: in place (d_R64, by position), or
+                // recomputed for the list when K1H kept none in HBM
+                char* d_Rx = nullptr;
+                if (k1h_of(ch)) {
+                    d_Rx = ctx->buf("Rx").as<char>(static_cast<size_t>(max_chunk) * rx_bytes);
+                    double* d_xe0 = ctx->buf("xe0").as<double>(static_cast<size_t>(max_chunk));
+                    double* d_xim = ctx->buf("xim").as<double>(static_cast<size_t>(max_chunk));
+                    k1_packed(d_rdesc, m, PATH_F64_REAL, seg64, 1, d_Rx, d_xe0, d_xim, 0, 0, ctx->aux2);
+                }
                 K2Args a = base_args();
                 a.path = PATH_F32_REAL;
                 a.seg = seg32;
@@ -1981,8 +2048,9 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
                 a.flags = nullptr;
                 a.vimg64x = d_vimg64;
                 a.vimg64x_stride = static_cast<int64_t>(vimg64_elems);
-                a.r64x = reinterpret_cast<const double2*>(d_R64);
+                a.r64x = reinterpret_cast<const double2*>(d_Rx ? d_Rx : d_R64);
                 a.r64x_seg = seg64;
+                a.r64x_by_list = d_Rx ? 1 : 0;
                 ck(k2v2x_launch(a, static_cast<int32_t>(xt.size()), ctx->aux2), "K2v2x exact near-tie resolution");
                 ++ctx->launches;
             } else if (!rs.empty()) {  // resumed: K2d REPLAY rebuilds the fp64 state at the near-tie and goes on

@@ -81,8 +81,24 @@ struct K1Args {
     const double2* twid;       // e^{-j 2 pi k / T}, k < T
     const double2* ptab;       // e^{-j pi m / T}, m < 2T (rotation phases; NULL = computed)
     const int32_t* n_dev;      // optional: block count on the device (grid = an upper bound)
+    // K1H (k1h_launch): the fp32 real path's spectra AND its fp64 head in one kernel —
+    // `head` selections on the spectrum while it is still on chip, then the fp32 SoA
+    // hand-off (out / seg / spt / out_stride) for K2v2r; no fp64 spectrum in HBM
+    int32_t head;
+    double gamma;
+    const double* vimg64h;     // [ncls] rotated fp64 V images, copy 0 rows of stride d_srv(T)
+    int64_t vimg64h_stride;    // doubles per class
+    const double* w0c;         // [ncls] W[0]
+    const int32_t* order;      // caller id by position (records)
+    int32_t* rec_u;            // [caller id][rec_stride] head records
+    double2* rec_c;
+    int32_t rec_stride;
+    double* energy_out;        // per position: weighted energy after the head
+    int32_t* nu_out;           // per position: selections made
+    int32_t* conv_out;         // per position: stopped during the head
 };
 enum { K1_PACKED = 0, K1_FULL = 1, K1_CLASS = 2 };
+int k1h_launch(const K1Args& a, cudaStream_t s);  // T = 64, symmetric (rotated) classes
 
 struct K2Args {
     int32_t T, Lh, Lw, path, seg;
@@ -159,6 +175,7 @@ struct K2Args {
     int64_t vimg64x_stride;
     const double2* r64x;
     int32_t r64x_seg;
+    int32_t r64x_by_list;       // r64x indexed by the flagged-list index (else by src_pos)
 };
 
 // Exact init (the fp64 mode's tie re-runs): init_spectra (engine_spectral.cpp:

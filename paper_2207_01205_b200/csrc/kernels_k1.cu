@@ -558,6 +558,341 @@ __global__ void __launch_bounds__(WGR * WLG, 1) k1w_kernel(K1Args a) {
     }
 }
 
+// ============================================================================
+// K1H: K1f + the fp64 head in one kernel (fp32 mode, real path, T = 64). The
+// block's spectrum never leaves the SM before the head: after K1f's two FFT
+// passes each of the 256 threads takes 8 canonical bins (+ the self-conjugate
+// extra) of the rotated spectrum R' into registers, the class's rotated V
+// image (64 x 64 fp64, 32 KB) replaces the transpose tiles in shared memory,
+// and `head` selections run in fp64 — argmax on 64-bit keys (|R'|^2 with the
+// low 12 bits replaced by 4095 - G: the largest value, ties to the lowest
+// index, as K2d), parity-double-buffered warp slots and ONE __syncthreads per
+// selection, the rotated-frame update of K2d with per-bin wrap signs — then
+// the residual is handed to K2v2r in its fp32 SoA layout. Replaces K1f's fp64
+// spectrum write + K2d's read of it + the K2d head launch.
+// ============================================================================
+struct K1HSlot {
+    unsigned hi, lo;
+    int g, pad;
+    double pre_re, pre_im;
+};
+
+template <class SRC>
+__global__ void __launch_bounds__(256, 3) k1h_kernel(K1Args a) {
+    constexpr int FT = 64;
+    using C = K1fCfg<FT>;
+    constexpr int LG = C::LG, SS = C::SS, CS = C::CS;
+    constexpr int HSEG = 8;                        // bins per thread in the head
+    constexpr unsigned long long KMASK = ~0ull << 12;
+    constexpr int KTOP = 4095;
+    static_assert(C::THREADS == 256 && (FT / 2) * (FT / HSEG) == 256, "one segment per thread");
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double2* tw = reinterpret_cast<double2*>(smem_raw + C::tw);
+    double2* ph = reinterpret_cast<double2*>(smem_raw + C::ph);
+    double2* cb = reinterpret_cast<double2*>(smem_raw + C::cb);
+    double* red = reinterpret_cast<double*>(smem_raw + C::red);
+    K1HSlot* slots = reinterpret_cast<K1HSlot*>(smem_raw + C::total);  // [2][8]
+    const int g = threadIdx.x / LG, t = threadIdx.x % LG;
+    const unsigned gmask = ((1u << LG) - 1u) << (LG * (g % (32 / LG)));
+    double2* tile = reinterpret_cast<double2*>(smem_raw + C::sc) + g * 8 * SS;
+    // after the FFT: V[64][VSR] (odd row stride: a warp's 32 rows hit 32 banks)
+    constexpr int VSR = FT + 1;
+    double* Vs = reinterpret_cast<double*>(smem_raw + C::sc);
+    static_assert((size_t)FT * VSR * sizeof(double) <= (size_t)(FT / 2) * 8 * SS * sizeof(double2), "V fits");
+
+    const int b = blockIdx.x;
+    if (a.n_dev && b >= *a.n_dev) return;
+    const BlockDesc d = a.blocks[b];
+    const double* wc = a.wcls + (size_t)d.cls * a.Lh * a.Lw;
+    for (int i = threadIdx.x; i < FT; i += blockDim.x) tw[i] = a.twid[i];
+    for (int i = threadIdx.x; i < 2 * FT; i += blockDim.x) {
+        const double2 p = a.ptab[i];  // e^{-j pi m / T}
+        ph[i] = make_double2(p.x, -p.y);
+    }
+    __syncthreads();
+
+    // ---- K1f: row pass, column pass (kernels_k1.cu k1f_kernel) ----
+    double energy = 0.0;
+    const int npairs = (a.Lh + 1) / 2;
+    if (g < npairs) {
+        const int ra = 2 * g, rb = ra + 1;
+        double2 x[8];
+        const bool hasb = rb < a.Lh;
+        const SRC* pa = k1f_row<SRC>(a, d, ra);
+        const SRC* pb = hasb ? k1f_row<SRC>(a, d, rb) : nullptr;
+        const double* wra = wc + ra * a.Lw;
+        const double* wrb = wc + (hasb ? rb : ra) * a.Lw;
+        const int c_lo = -d.col0, c_hi = a.fr.width - d.col0;
+        double wa[8], wb[8], fa[8], fb[8];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            const int n = t + LG * m;
+            const bool in = n < a.Lw;
+            const bool inf = in && n >= c_lo && n < c_hi;
+            wa[m] = in ? wra[n] : 0.0;
+            wb[m] = (in && hasb) ? wrb[n] : 0.0;
+            fa[m] = (inf && pa && wa[m] != 0.0) ? static_cast<double>(pa[n]) : 0.0;
+            fb[m] = (inf && pb && wb[m] != 0.0) ? static_cast<double>(pb[n]) : 0.0;
+        }
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            const double va = wa[m] * fa[m], vb = wb[m] * fb[m];
+            energy += va * fa[m];
+            energy += vb * fb[m];
+            x[m] = make_double2(va, vb);
+        }
+        fft_group<FT>(x, t, tw, tile, gmask);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) tile[j * SS + t] = x[j];
+        __syncwarp(gmask);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int k = t + LG * j;
+            if (k > FT / 2) continue;
+            const int nk = (FT - k) & (FT - 1);
+            const double2 zc = tile[(nk / LG) * SS + (nk % LG)];
+            const double2 z = x[j];
+            cb[k * CS + ra] = make_double2(0.5 * (z.x + zc.x), 0.5 * (z.y - zc.y));
+            if (rb < FT) cb[k * CS + rb] = make_double2(0.5 * (z.y + zc.y), -0.5 * (z.x - zc.x));
+        }
+        __syncwarp(gmask);
+    }
+    __syncthreads();
+    const int nrows = 2 * npairs;
+    {
+        constexpr int GL = FT / 2 - 1;
+        const int col = g < GL ? g + 1 : 0;
+        double2 x[8];
+        if (g < GL) {
+#pragma unroll
+            for (int m = 0; m < 8; ++m)
+                x[m] = (t + LG * m < nrows) ? cb[col * CS + t + LG * m] : make_double2(0.0, 0.0);
+        } else {
+#pragma unroll
+            for (int m = 0; m < 8; ++m)
+                x[m] = (t + LG * m < nrows) ? make_double2(cb[t + LG * m].x, cb[(FT / 2) * CS + t + LG * m].x)
+                                            : make_double2(0.0, 0.0);
+        }
+        fft_group<FT>(x, t, tw, tile, gmask);
+        if (g < GL) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) cb[col * CS + t + LG * j] = x[j];
+        } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) tile[j * SS + t] = x[j];
+            __syncwarp(gmask);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int k = t + LG * j;
+                const int nk = (FT - k) & (FT - 1);
+                const double2 zc = tile[(nk / LG) * SS + (nk % LG)];
+                const double2 z = x[j];
+                cb[k] = make_double2(0.5 * (z.x + zc.x), 0.5 * (z.y - zc.y));
+                cb[(FT / 2) * CS + k] = make_double2(0.5 * (z.y + zc.y), -0.5 * (z.x - zc.x));
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) energy += __shfl_xor_sync(0xffffffffu, energy, o);
+    __syncthreads();  // the spectrum tile is complete; the transpose tiles are free
+
+    // ---- the class's rotated V image into the transpose tiles' space ----
+    {
+        const double* V = a.vimg64h + (size_t)d.cls * a.vimg64h_stride;
+        constexpr int SRV64 = d_srv(FT);
+        for (int i = threadIdx.x; i < FT * FT / 2; i += blockDim.x) {  // two columns per step
+            const int r = i / (FT / 2), c = 2 * (i % (FT / 2));
+            Vs[r * VSR + c] = V[r * SRV64 + c];
+            Vs[r * VSR + c + 1] = V[r * SRV64 + c + 1];
+        }
+    }
+    // ---- this thread's canonical bins, rotated: R' = R e^{+j phi} ----
+    int k1, c0, ex;
+    BinLayout::make(FT, HSEG, 1).thread_segment(threadIdx.x, 0, &k1, &c0, &ex);
+    const int nk1 = (FT - k1) & (FT - 1);
+    const int pbase = k1 * (a.Lh - 1), lw1 = a.Lw - 1;
+    double re[HSEG + 1], im[HSEG + 1];
+    double vmax2 = 0.0;
+#pragma unroll
+    for (int j = 0; j <= HSEG; ++j) {
+        double2 v = make_double2(0.0, 0.0);
+        if (j < HSEG || ex) {
+            const int k2 = j < HSEG ? c0 + j : FT / 2;
+            if (k2 <= FT / 2) {
+                v = cb[k2 * CS + k1];
+            } else {
+                const double2 u = cb[(FT - k2) * CS + nk1];
+                v = make_double2(u.x, -u.y);
+            }
+            vmax2 = fmax(vmax2, fma(v.x, v.x, v.y * v.y));
+            v = c_mul(v, ph[(pbase + k2 * lw1) & (2 * FT - 1)]);
+        }
+        re[j] = v.x;
+        im[j] = v.y;
+    }
+    // block energy and max: every thread needs them (the head's stop tests)
+#pragma unroll
+    for (int o = 16; o; o >>= 1) vmax2 = fmax(vmax2, __shfl_xor_sync(0xffffffffu, vmax2, o));
+    if ((threadIdx.x & 31) == 0) {
+        red[threadIdx.x >> 5] = energy;
+        red[8 + (threadIdx.x >> 5)] = vmax2;
+    }
+    __syncthreads();  // also: V staged
+    double e0 = red[0], m2 = red[8];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) {
+        e0 += red[w];
+        m2 = fmax(m2, red[8 + w]);
+    }
+    const double imax = sqrt(m2);
+
+    // ---- the fp64 head (K2d's selection, scalar part and update) ----
+    const double w0 = a.w0c[d.cls], gw = a.gamma / w0;
+    const double sgn_r = ((a.Lh - 1) & 1) ? -1.0 : 1.0, sgn_c = ((a.Lw - 1) & 1) ? -1.0 : 1.0;
+    const double thr_e = 1e-12 * e0, thr_m = (1e-12 * imax) * (1e-12 * imax);
+    const int gbase = k1 * FT + c0;
+    const int cid = a.order[b];
+    int* rec_u = a.rec_u + (size_t)cid * a.rec_stride;
+    double2* rec_c = a.rec_c + (size_t)cid * a.rec_stride;
+    double en = e0;
+    int nu = 0, conv = e0 <= 0.0;
+    const int w = threadIdx.x >> 5;
+    for (int it = 0; it < a.head && !conv; ++it) {
+        const int par = it & 1;
+        unsigned long long K = 0ull;
+#pragma unroll
+        for (int j = 0; j <= HSEG; ++j) {
+            if (j == HSEG && !ex) continue;
+            const int G = j < HSEG ? gbase + j : k1 * FT + FT / 2;
+            const double m = fma(im[j], im[j], re[j] * re[j]);
+            const unsigned long long key =
+                (static_cast<unsigned long long>(__double_as_longlong(m)) & KMASK) | static_cast<unsigned>(KTOP - G);
+            K = key > K ? key : K;
+        }
+        const unsigned hi = static_cast<unsigned>(K >> 32), lo = static_cast<unsigned>(K);
+        const unsigned Mhi = __reduce_max_sync(0xffffffffu, hi);
+        const unsigned Mlo = __reduce_max_sync(0xffffffffu, hi == Mhi ? lo : 0u);
+        if (hi == Mhi && lo == Mlo) {
+            const int G = KTOP - static_cast<int>(Mlo & KTOP);
+            const int j = G - gbase;
+            double pr = 0.0, pi = 0.0;
+#pragma unroll
+            for (int q = 0; q <= HSEG; ++q) {
+                const bool hit = q < HSEG ? j == q : (ex && G == k1 * FT + FT / 2);
+                pr = hit ? re[q] : pr;
+                pi = hit ? im[q] : pi;
+            }
+            slots[par * 8 + w] = K1HSlot{Mhi, Mlo, G, 0, pr, pi};
+        }
+        __syncthreads();
+        int wb = 0;
+        {
+            unsigned bh = slots[par * 8].hi, bl = slots[par * 8].lo;
+#pragma unroll
+            for (int k = 1; k < 8; ++k) {
+                const unsigned oh = slots[par * 8 + k].hi, ol = slots[par * 8 + k].lo;
+                const bool gt = oh > bh || (oh == bh && ol > bl);
+                bh = gt ? oh : bh;
+                bl = gt ? ol : bl;
+                wb = gt ? k : wb;
+            }
+        }
+        const K1HSlot sl = slots[par * 8 + wb];
+        const double pr = sl.pre_re, pi = sl.pre_im;
+        const double M = fma(pi, pi, pr * pr);
+        if (en < thr_e || !(M > 0.0) || M < thr_m) {
+            conv = 1;
+            break;
+        }
+        const int G = sl.g;
+        const int u1 = G / FT, u2 = G % FT;
+        const int self = ((FT - u1) % FT == u1) && ((FT - u2) % FT == u2);
+        const double2 P = a.ptab[(u1 * (a.Lh - 1) + u2 * lw1) & (2 * FT - 1)];
+        const double ar = pr * gw, ai = pi * gw;
+        double c_re = ar * P.x - ai * P.y, c_im = ar * P.y + ai * P.x;
+        double a_re = ar, a_im = ai, delta;
+        if (self) {
+            c_im = 0.0;
+            a_re = c_re * P.x;
+            a_im = -c_re * P.y;
+            delta = -2.0 * c_re * (pr * P.x - pi * P.y) + c_re * c_re * w0;
+        } else {
+            const int mi1 = 2 * u1, mi2 = 2 * u2;
+            const double v2 = Vs[(mi1 & (FT - 1)) * VSR + (mi2 & (FT - 1))];
+            const double sig = ((mi1 >= FT) ? sgn_r : 1.0) * ((mi2 >= FT) ? sgn_c : 1.0);
+            delta = -4.0 * (a_re * pr + a_im * pi) + 2.0 * (a_re * a_re + a_im * a_im) * w0 +
+                    2.0 * sig * v2 * (a_re * a_re - a_im * a_im);
+        }
+        const double e = en + delta;
+        en = 0.0 < e ? e : 0.0;
+        if (threadIdx.x == 0 && nu < a.rec_stride) {
+            rec_u[nu] = (u1 << 16) | u2;
+            rec_c[nu] = self ? make_double2(c_re, 0.0) : make_double2(2.0 * c_re, 2.0 * c_im);
+        }
+        nu += 1;
+        // R'[k] -= s1 a V[k - u] + s2 conj(a) V[k + u] (self: the first term), per bin signs
+        const int rA = (k1 - u1) & (FT - 1), rB = (k1 + u1) & (FT - 1);
+        const double sr1 = (k1 < u1) ? sgn_r : 1.0, sr2 = (k1 + u1 >= FT) ? sgn_r : 1.0;
+        const double* VA = Vs + rA * VSR;
+        const double* VB = Vs + rB * VSR;
+#pragma unroll
+        for (int j = 0; j <= HSEG; ++j) {
+            if (j == HSEG && !ex) continue;
+            const int c = j < HSEG ? c0 + j : FT / 2;
+            const double s1 = sr1 * ((c < u2) ? sgn_c : 1.0);
+            const double va = s1 * VA[(c - u2) & (FT - 1)];
+            double nr = fma(-va, a_re, re[j]), ni = fma(-va, a_im, im[j]);
+            if (!self) {
+                const double s2 = sr2 * ((c + u2 >= FT) ? sgn_c : 1.0);
+                const double vb = s2 * VB[(c + u2) & (FT - 1)];
+                nr = fma(-vb, a_re, nr);
+                ni = fma(vb, a_im, ni);
+            }
+            re[j] = nr;
+            im[j] = ni;
+        }
+    }
+
+    // ---- hand-off: the fp32 SoA pair layout of K2v2r (as K2d's rout_f32) ----
+    {
+        const BinLayout Lo = BinLayout::make(FT, a.seg, a.spt > 0 ? a.spt : 1);
+        float* o = static_cast<float*>(a.out) + (size_t)b * a.out_stride;
+        int i0, tt;
+        bin_slot(Lo, k1, c0, &i0, &tt);
+        const int s0 = i0 / (Lo.SEG + 1), j0 = i0 - s0 * (Lo.SEG + 1);
+        float4* o4 = reinterpret_cast<float4*>(o) + (size_t)(s0 * (Lo.SEG / 2) + j0 / 2) * Lo.NT + tt;
+#pragma unroll
+        for (int q = 0; q < HSEG / 2; ++q)
+            o4[(size_t)q * Lo.NT] = make_float4((float)re[2 * q], (float)re[2 * q + 1], (float)im[2 * q],
+                                                (float)im[2 * q + 1]);
+        if (ex) {
+            int i, t2;
+            bin_slot(Lo, k1, FT / 2, &i, &t2);
+            const int sx = i / (Lo.SEG + 1);
+            reinterpret_cast<float4*>(o)[(size_t)(Lo.SPT * Lo.SEG / 2 + sx) * Lo.NT + t2] =
+                make_float4((float)re[HSEG], 0.f, (float)im[HSEG], 0.f);
+        }
+    }
+    if (threadIdx.x == 0) {
+        a.energy[b] = e0;
+        a.init_max[b] = imax;
+        a.energy_out[b] = en;
+        a.nu_out[b] = nu;
+        a.conv_out[b] = conv;
+    }
+}
+
+template <class SRC>
+static int k1h_launch_t(const K1Args& a, cudaStream_t s) {
+    using C = K1fCfg<64>;
+    const size_t smem = C::total + 2 * 8 * sizeof(K1HSlot);
+    cudaError_t e = cudaFuncSetAttribute(k1h_kernel<SRC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    if (a.n <= 0) return cudaSuccess;
+    k1h_kernel<SRC><<<a.n, C::THREADS, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
 }  // namespace
 
 bool k1f_supported(const K1Args& a) {
@@ -597,6 +932,11 @@ static int k1w_launch(const K1Args& a, cudaStream_t s) {
     else
         k1w_kernel<double><<<a.n, WGR * WLG, K1wSmem::total, s>>>(a);
     return cudaGetLastError();
+}
+
+int k1h_launch(const K1Args& a, cudaStream_t s) {
+    if (a.T != 64 || a.Lh > 64 || a.Lw > 64) return cudaErrorInvalidValue;
+    return a.fr.type == SRC_U8 ? k1h_launch_t<uint8_t>(a, s) : k1h_launch_t<double>(a, s);
 }
 
 int k1f_launch(const K1Args& a, cudaStream_t s) {

@@ -657,6 +657,7 @@ __global__ void __launch_bounds__(128, 2) k2v2x_kernel(K2Args a) {
         const int b = a.order[j];
         const int pos = a.src_pos[j];
         const int nuf = a.nu_flag[j];
+        const int rpos = a.r64x_by_list ? j : pos;  // K1's fp64 spectrum of this block
         float2 rp[NP], ip[NP];
         float xr[SPT], xi[SPT];
         {
@@ -766,7 +767,7 @@ __global__ void __launch_bounds__(128, 2) k2v2x_kernel(K2Args a) {
                 for (int s = nex; s < nu; ++s) {
                     const int u = xu[s];
                     const int su1 = u >> 16, su2 = u & 0xffff;
-                    const double2 r0 = x_r0(a, L64, pos, su1, su2);
+                    const double2 r0 = x_r0(a, L64, rpos, su1, su2);
                     const double2 rs = x_exact<T>(su1, su2, s, lane, xa, xu, V64, sgn_rd, sgn_cd, r0);
                     const int sself = ((su1 & (T / 2 - 1)) == 0) && ((su2 & (T / 2 - 1)) == 0);
                     const double2 P = a.ptab[(su1 * lh1 + su2 * lw1) & (2 * T - 1)];
@@ -815,7 +816,7 @@ __global__ void __launch_bounds__(128, 2) k2v2x_kernel(K2Args a) {
                     }
                     Gc = __shfl_sync(0xffffffffu, Gc, src);
                     const int ck1 = Gc / T, cc = Gc % T;
-                    const double2 r0 = x_r0(a, L64, pos, ck1, cc);
+                    const double2 r0 = x_r0(a, L64, rpos, ck1, cc);
                     const double2 R = x_exact<T>(ck1, cc, nu, lane, xa, xu, V64, sgn_rd, sgn_cd, r0);
                     const double v = fma(R.y, R.y, R.x * R.x);
                     if (v > bestv || (v == bestv && Gc < bestG)) {

@@ -753,6 +753,24 @@ def test_fp32_batch_path_parity_vs_fp64(gpu):
     assert r["dpsnr_db"] <= FP32_PSNR_TOL
 
 
+def test_fused_k1_head_matches_two_kernels(gpu, monkeypatch):
+    """K1H (FOFSE_K1H=1: spectra + fp64 head in one kernel, the fp32 hand-off
+    straight from the SM; near-tie blocks recompute K1 for the exact
+    resolution) against K1f + the K2d head: the same selections up to fp64
+    rounding — pixels within fp32 noise — and both within the fp32 bar of
+    the fp64 path."""
+    from paper_2207_01205_b200 import parity as PAR
+    import dataclasses
+    wl = dataclasses.replace(WL.C4, frames=32)
+    base = PAR.fp32_vs_fp64(wl, 913, per_call=32)
+    monkeypatch.setenv("FOFSE_K1H", "1")
+    fused = PAR.fp32_vs_fp64(wl, 913, per_call=32)
+    for r in (base, fused):
+        assert r["blocks_over_0.5"] == 0 and r["dpsnr_db"] <= FP32_PSNR_TOL
+    assert abs(fused["guard_reruns"] - base["guard_reruns"]) <= max(3, base["guard_reruns"] // 50)
+    assert abs(fused["psnr_fp32_db"] - base["psnr_fp32_db"]) <= 1e-4
+
+
 @pytest.mark.parametrize("nframes,groups", [(1, 3), (1, 8), (3, 5)])
 def test_row_groups_match_one_group(gpu, monkeypatch, nframes, groups):
     """Fewer than 16 frames: the frames' rows are cut into bands (first/last a
