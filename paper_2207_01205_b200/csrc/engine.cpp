@@ -1680,7 +1680,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             gp.head = head;
             gp.can_resume = can_resume_of(ch) ? 1 : 0;
             gp.ng_rr = ng_f64(PATH_F64_REAL, wide);
-            gp.ng_rs = etr_of(ch) ? 4 : ng_f64(PATH_F64_REAL, wide);  // K2v2x: 4 blocks per CTA
+            gp.ng_rs = etr_of(ch) ? k2v2x_blocks_per_cta(T) : ng_f64(PATH_F64_REAL, wide);
             gp.order = d_ids;
             gp.descs = d_sorted;
             gp.rr_ids = g_rr_ids;
@@ -2017,7 +2017,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
                 upload_to(ctx, d_rr, rs.data(), rs.size(), ctx->aux2);
                 upload_to(ctx, d_rpos, spos.data(), spos.size(), ctx->aux2);
                 upload_to(ctx, d_rnuf, snuf.data(), snuf.size(), ctx->aux2);
-                const std::vector<Tile> xt = make_tiles(0, m, sdesc, 4);
+                const std::vector<Tile> xt = make_tiles(0, m, sdesc, k2v2x_blocks_per_cta(T));
                 const Tile* d_xt = upload(ctx, "xtiles" + std::to_string(ci), xt.data(), xt.size(), ctx->aux2);
                 // K1's fp64 spectra of the flagged blocks: in place (d_R64, by position), or
                 // recomputed for the list when K1H kept none in HBM

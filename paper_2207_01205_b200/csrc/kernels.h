@@ -289,6 +289,7 @@ int k2v2_launch(const K2Args& a, int32_t ntiles, cudaStream_t s);
 // blocks / nu_flag by list index, data by src_pos)
 int k2v2x_launch(const K2Args& a, int32_t ntiles, cudaStream_t s);
 bool k2v2x_supported(int t);
+int k2v2x_blocks_per_cta(int t);  // lost blocks per tile of K2v2x (T = 128: one per CTA)
 // K2d: fp64 rotated-frame iteration (PATH_F64_REAL), groups of d_group_threads(T).
 int k2d_launch(const K2Args& a, int32_t ntiles, cudaStream_t s);
 int k2d_blocks_per_cta(int T, bool wide = false);

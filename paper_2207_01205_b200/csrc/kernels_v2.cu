@@ -946,7 +946,12 @@ __global__ void __launch_bounds__(128, 2) k2v2x_kernel(K2Args a) {
     }
 }
 
+// T = 128 keeps the fp64 REPLAY re-run: the same exact resolution on the K2v2h
+// layout (8 warps per block, candidates listed in shared memory, warp 0
+// resolving) measured 2 % slower on C5 — the near-tie tail there is a fraction
+// of a wave, where the 8-warp fp32 iteration's latency outweighs the replay
 bool k2v2x_supported(int t) { return t == 64; }
+int k2v2x_blocks_per_cta(int) { return 4; }
 
 int k2v2x_launch(const K2Args& args, int32_t ntiles, cudaStream_t s) {
     if (args.T != 64) return cudaErrorInvalidValue;
@@ -1648,12 +1653,13 @@ __global__ void __launch_bounds__(V2HCfg<T>::THREADS, V2HCfg<T>::MINB) k2v2h_ker
                 rec_c[q] = make_double2(bcx, bcy);
             }
         }
-        if (a.rout) {
+        if (a.rout && (!a.rout_flagged || flagged)) {  // rout_flagged: a near-tie block's state (K2v2x)
             const size_t rs = a.rin_stride > 0 ? (size_t)a.rin_stride : (size_t)(NP + 1) * NT * 4;
             float4* R = reinterpret_cast<float4*>(static_cast<float*>(a.rout) + (size_t)pos * rs);
 #pragma unroll
             for (int p = 0; p < NP; ++p) R[p * NT + tid] = make_float4(rp[p].x, rp[p].y, ip[p].x, ip[p].y);
             R[NP * NT + tid] = make_float4(xr, 0.f, xi, 0.f);
+            if (flagged && a.flag_energy && tid == 0) a.flag_energy[pos] = energy;
         }
         // both warps see the records written by tid 0 before synthesising
         named_bar_sync(bar, NT);
