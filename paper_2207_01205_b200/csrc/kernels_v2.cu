@@ -571,29 +571,33 @@ __global__ void __launch_bounds__(128, (VAR == 3 || VAR == 9) ? 2 : 3) k2v2r_ker
 // are fp64. The iteration then goes on in fp32 with the same guard. Cost per
 // block O(nu^2 / 32) instead of the fp64 replay's O(nu * H).
 // ============================================================================
+// one rotated-frame term of selection (u, a) at canonical bin (k1, c): the sum
+// s1 a V[k - u] + s2 conj(a) V[k + u] (self-conjugate u: the first term)
+template <int T>
+__device__ __forceinline__ void x_term(int k1, int c, int u, double2 av, const double* V, int vs, double sgn_r,
+                                       double sgn_c, double& tr, double& ti) {
+    const int u1 = u >> 16, u2 = u & 0xffff;
+    const bool self = ((u1 & (T / 2 - 1)) == 0) && ((u2 & (T / 2 - 1)) == 0);
+    const int rA = (k1 - u1) & (T - 1), cA = (c - u2) & (T - 1);
+    const double s1 = ((k1 < u1) ? sgn_r : 1.0) * ((c < u2) ? sgn_c : 1.0);
+    const double va = s1 * V[rA * vs + cA];
+    tr = fma(va, av.x, tr);
+    ti = fma(va, av.y, ti);
+    if (!self) {
+        const int rB = (k1 + u1) & (T - 1), cB = (c + u2) & (T - 1);
+        const double s2 = ((k1 + u1 >= T) ? sgn_r : 1.0) * ((c + u2 >= T) ? sgn_c : 1.0);
+        const double vb = s2 * V[rB * vs + cB];
+        tr = fma(vb, av.x, tr);
+        ti = fma(-vb, av.y, ti);
+    }
+}
+
 template <int T>
 __device__ __forceinline__ double2 x_exact(int k1, int c, int s, int lane, const double2* xa, const int* xu,
-                                           const double* V64, double sgn_r, double sgn_c, double2 r0) {
-    constexpr int SRV64 = d_srv(T);
+                                           const double* V64, double sgn_r, double sgn_c, double2 r0,
+                                           int vs = d_srv(T)) {
     double tr = 0.0, ti = 0.0;
-    for (int r = lane; r < s; r += 32) {
-        const int u = xu[r];
-        const int u1 = u >> 16, u2 = u & 0xffff;
-        const double2 av = xa[r];
-        const bool self = ((u1 & (T / 2 - 1)) == 0) && ((u2 & (T / 2 - 1)) == 0);
-        const int rA = (k1 - u1) & (T - 1), cA = (c - u2) & (T - 1);
-        const double s1 = ((k1 < u1) ? sgn_r : 1.0) * ((c < u2) ? sgn_c : 1.0);
-        const double va = s1 * V64[rA * SRV64 + cA];
-        tr = fma(va, av.x, tr);
-        ti = fma(va, av.y, ti);
-        if (!self) {
-            const int rB = (k1 + u1) & (T - 1), cB = (c + u2) & (T - 1);
-            const double s2 = ((k1 + u1 >= T) ? sgn_r : 1.0) * ((c + u2 >= T) ? sgn_c : 1.0);
-            const double vb = s2 * V64[rB * SRV64 + cB];
-            tr = fma(vb, av.x, tr);
-            ti = fma(-vb, av.y, ti);
-        }
-    }
+    for (int r = lane; r < s; r += 32) x_term<T>(k1, c, xu[r], xa[r], V64, vs, sgn_r, sgn_c, tr, ti);
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
         tr += __shfl_xor_sync(0xffffffffu, tr, o);
@@ -630,8 +634,13 @@ __global__ void __launch_bounds__(128, 2) k2v2x_kernel(K2Args a) {
     float4* spill = reinterpret_cast<float4*>(smem_raw + Cf::OFF_SP) + warp * (NP + SPT + 1);
     V2State* st = reinterpret_cast<V2State*>(smem_raw + Cf::OFF_ST + 64 * warp);
     const int imax = a.iterations;
-    unsigned char* xbase = smem_raw + ((Cf::SMEM + 15) & ~size_t(15));
-    double2* xa = reinterpret_cast<double2*>(xbase) + (size_t)warp * imax;   // exact coefficients a_s
+    // the class's fp64 rotated V (64 x 64, odd row stride) for the exact evaluations,
+    // then per warp: xa[s] (the partial residual at u_s while s is pending, then the
+    // exact coefficient a_s) and xu[s] (the selections)
+    constexpr int XVS = T + 1;
+    double* Vx = reinterpret_cast<double*>(smem_raw + ((Cf::SMEM + 15) & ~size_t(15)));
+    unsigned char* xbase = reinterpret_cast<unsigned char*>(Vx + T * XVS);
+    double2* xa = reinterpret_cast<double2*>(xbase) + (size_t)warp * imax;
     int* xu = reinterpret_cast<int*>(xbase + sizeof(double2) * Cf::WARPS * imax) + (size_t)warp * imax;
 
     const BinLayout L = BinLayout::make(T, SEG, SPT);
@@ -648,9 +657,13 @@ __global__ void __launch_bounds__(128, 2) k2v2x_kernel(K2Args a) {
     const int rstride = a.rec_stride > 0 ? a.rec_stride : a.iterations;
     const int lh1 = a.Lh - 1, lw1 = a.Lw - 1;
     const BinLayout L64 = BinLayout::make(T, a.r64x_seg, 1);
-    const double* V64 = a.vimg64x + (size_t)tile.cls * a.vimg64x_stride;
-    constexpr int SRV64 = d_srv(T);
     const double w0d = a.w0[tile.cls], gwd = a.gamma / w0d;
+    {
+        const double* V64 = a.vimg64x + (size_t)tile.cls * a.vimg64x_stride;
+        constexpr int SRV64 = d_srv(T);
+        for (int i = threadIdx.x; i < T * T; i += blockDim.x) Vx[(i / T) * XVS + (i % T)] = V64[(i / T) * SRV64 + (i % T)];
+        __syncthreads();
+    }
 
     for (int bi = warp; bi < tile.count; bi += Cf::WARPS) {
         const int j = tile.begin + bi;  // index into the flagged list
@@ -764,11 +777,22 @@ __global__ void __launch_bounds__(128, 2) k2v2x_kernel(K2Args a) {
             double delta, cre, cim;
             if (pending || Sf > Mf * tau1) {
                 // ---- exact decision: fp64 coefficients of selections [nex, nu) ----
-                for (int s = nex; s < nu; ++s) {
+                // (1) lanes over s: xa[s] = R'_0[u_s] - sum_{r < nex} term(r, u_s)
+                for (int s = nex + lane; s < nu; s += 32) {
                     const int u = xu[s];
                     const int su1 = u >> 16, su2 = u & 0xffff;
+                    double tr = 0.0, ti = 0.0;
+                    for (int r = 0; r < nex; ++r) x_term<T>(su1, su2, xu[r], xa[r], Vx, XVS, sgn_rd, sgn_cd, tr, ti);
                     const double2 r0 = x_r0(a, L64, rpos, su1, su2);
-                    const double2 rs = x_exact<T>(su1, su2, s, lane, xa, xu, V64, sgn_rd, sgn_cd, r0);
+                    xa[s] = make_double2(r0.x - tr, r0.y - ti);
+                }
+                __syncwarp();
+                // (2) wavefront: a_r from its completed partial residual, then its term
+                // joins every later pending one (lanes over s)
+                for (int r = nex; r < nu; ++r) {
+                    const int u = xu[r];
+                    const int su1 = u >> 16, su2 = u & 0xffff;
+                    const double2 rs = xa[r];
                     const int sself = ((su1 & (T / 2 - 1)) == 0) && ((su2 & (T / 2 - 1)) == 0);
                     const double2 P = a.ptab[(su1 * lh1 + su2 * lw1) & (2 * T - 1)];
                     double ar = rs.x * gwd, ai = rs.y * gwd;
@@ -777,7 +801,16 @@ __global__ void __launch_bounds__(128, 2) k2v2x_kernel(K2Args a) {
                         ar = c_re * P.x;
                         ai = -c_re * P.y;
                     }
-                    if (lane == 0) xa[s] = make_double2(ar, ai);
+                    const double2 av = make_double2(ar, ai);
+                    for (int s = r + 1 + lane; s < nu; s += 32) {
+                        const int us = xu[s];
+                        double tr = 0.0, ti = 0.0;
+                        x_term<T>(us >> 16, us & 0xffff, u, av, Vx, XVS, sgn_rd, sgn_cd, tr, ti);
+                        const double2 q = xa[s];
+                        xa[s] = make_double2(q.x - tr, q.y - ti);
+                    }
+                    __syncwarp();
+                    if (lane == 0) xa[r] = av;
                     __syncwarp();
                 }
                 nex = nu;
@@ -817,7 +850,7 @@ __global__ void __launch_bounds__(128, 2) k2v2x_kernel(K2Args a) {
                     Gc = __shfl_sync(0xffffffffu, Gc, src);
                     const int ck1 = Gc / T, cc = Gc % T;
                     const double2 r0 = x_r0(a, L64, rpos, ck1, cc);
-                    const double2 R = x_exact<T>(ck1, cc, nu, lane, xa, xu, V64, sgn_rd, sgn_cd, r0);
+                    const double2 R = x_exact<T>(ck1, cc, nu, lane, xa, xu, Vx, sgn_rd, sgn_cd, r0, XVS);
                     const double v = fma(R.y, R.y, R.x * R.x);
                     if (v > bestv || (v == bestv && Gc < bestG)) {
                         bestv = v;
@@ -842,7 +875,7 @@ __global__ void __launch_bounds__(128, 2) k2v2x_kernel(K2Args a) {
                     delta = cre * (cre * w0d - 2.0 * (pr * P.x - pi * P.y));
                 } else {
                     const int mi1 = 2 * u1, mi2 = 2 * u2;
-                    const double v2 = V64[(mi1 & (T - 1)) * SRV64 + (mi2 & (T - 1))];
+                    const double v2 = Vx[(mi1 & (T - 1)) * XVS + (mi2 & (T - 1))];
                     const double sig = ((mi1 >= T) ? sgn_rd : 1.0) * ((mi2 >= T) ? sgn_cd : 1.0);
                     delta = -4.0 * (a_re * pr + a_im * pi) + 2.0 * (a_re * a_re + a_im * a_im) * w0d +
                             2.0 * sig * v2 * (a_re * a_re - a_im * a_im);
@@ -958,7 +991,8 @@ int k2v2x_launch(const K2Args& args, int32_t ntiles, cudaStream_t s) {
     K2Args a = args;
     a.tau1f = (float)(1.0 - a.tau);
     using Cf = V2Cfg<64, PATH_F32_REAL>;
-    const size_t smem = ((Cf::SMEM + 15) & ~size_t(15)) + (sizeof(double2) + sizeof(int)) * Cf::WARPS * (size_t)a.iterations;
+    const size_t smem = ((Cf::SMEM + 15) & ~size_t(15)) + sizeof(double) * 64 * 65 +
+                        (sizeof(double2) + sizeof(int)) * Cf::WARPS * (size_t)a.iterations;
     cudaError_t e = cudaFuncSetAttribute(k2v2x_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     if (ntiles <= 0) return cudaSuccess;
