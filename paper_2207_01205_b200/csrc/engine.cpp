@@ -1632,9 +1632,9 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             const char* e = std::getenv("FOFSE_ETR");
             return !(e && e[0] == '0');
         }();
-        auto etr_of = [&](const Chunk& ch) {
+        auto etr_of = [&](const Chunk& ch) {  // (traces requested: the REPLAY re-run records every selection)
             return etr_on && can_resume_of(ch) && ch.path == PATH_F32_REAL && v2r && real_gw == 1 &&
-                   k2v2x_supported(T) && d_vimg64;
+                   k2v2x_supported(T, I) && d_vimg64 && !d_trace && !d_gap;
         };
         double* d_enf = ctx->buf("enf").as<double>(static_cast<size_t>(std::max<int64_t>(n, 1)));
         // K1H: spectra + fp64 head in one kernel for the K2v2r chunks (no fp64 spectrum in

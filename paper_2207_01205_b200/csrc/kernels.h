@@ -288,7 +288,7 @@ int k2v2_launch(const K2Args& a, int32_t ntiles, cudaStream_t s);
 // bins), the iteration going on in fp32; tiles over the flagged list (order /
 // blocks / nu_flag by list index, data by src_pos)
 int k2v2x_launch(const K2Args& a, int32_t ntiles, cudaStream_t s);
-bool k2v2x_supported(int t);
+bool k2v2x_supported(int t, int iterations);
 int k2v2x_blocks_per_cta(int t);  // lost blocks per tile of K2v2x (T = 128: one per CTA)
 // K2d: fp64 rotated-frame iteration (PATH_F64_REAL), groups of d_group_threads(T).
 int k2d_launch(const K2Args& a, int32_t ntiles, cudaStream_t s);

@@ -983,7 +983,13 @@ __global__ void __launch_bounds__(128, 2) k2v2x_kernel(K2Args a) {
 // layout (8 warps per block, candidates listed in shared memory, warp 0
 // resolving) measured 2 % slower on C5 — the near-tie tail there is a fraction
 // of a wave, where the 8-warp fp32 iteration's latency outweighs the replay
-bool k2v2x_supported(int t) { return t == 64; }
+bool k2v2x_supported(int t, int iterations) {
+    if (t != 64) return false;
+    using Cf = V2Cfg<64, PATH_F32_REAL>;
+    const size_t smem = ((Cf::SMEM + 15) & ~size_t(15)) + sizeof(double) * 64 * 65 +
+                        (sizeof(double2) + sizeof(int)) * Cf::WARPS * (size_t)iterations;
+    return smem <= 227 * 1024;
+}
 int k2v2x_blocks_per_cta(int) { return 4; }
 
 int k2v2x_launch(const K2Args& args, int32_t ntiles, cudaStream_t s) {

@@ -611,6 +611,33 @@ def test_guard_resume_matches_rerun_from_scratch(gpu, monkeypatch, name):
         assert abs(out.report.psnr_db - o64.report.psnr_db) <= FP32_PSNR_TOL
 
 
+def test_fp32_traces_are_complete_with_guard_reruns(gpu):
+    """fp32 mode with record_traces: near-tie blocks re-run on a path that records
+    every selection (the exact-resolution continuation records none, so traces
+    route those blocks to the fp64 re-run): each block's trace is 1..nu without
+    gaps, selections on the canonical half."""
+    img, pat = WL.C2.frame(seed=29)
+    cfg = WL.C2.config("fp32", record_traces=True)
+    out = P.conceal(img.astype(np.float64), pat, cfg)
+    assert out.report.device["guard_reruns"] > 0
+    for tr in out.report.traces:
+        assert len(tr) >= 1
+        np.testing.assert_array_equal(tr["nu"], np.arange(1, len(tr) + 1))
+        assert (tr["u1"] >= 0).all() and (tr["u1"] <= 32).all() and (tr["u2"] >= 0).all() and (tr["u2"] < 64).all()
+
+
+@pytest.mark.parametrize("iters", [24, 400])
+def test_fp32_batch_parity_short_and_long_runs(gpu, iters):
+    """The batch path (K2v2r, head, guard, exact near-tie resolution) at a short
+    run (the head is a third of it) and a long one (records / exact coefficients
+    sized by the iteration count): within the fp32 bar of the fp64 path."""
+    from paper_2207_01205_b200 import parity as PAR
+    import dataclasses
+    wl = dataclasses.replace(WL.C4, frames=24, iterations=iters)
+    r = PAR.fp32_vs_fp64(wl, 933, per_call=24)
+    assert r["blocks_over_0.5"] == 0 and r["dpsnr_db"] <= FP32_PSNR_TOL
+
+
 def test_device_planned_guard_matches_host_planned(gpu, monkeypatch):
     """C2 (one chunk): the re-runs planned on the device (guard plan kernel,
     device-sized launches) equal the host-planned ones bit for bit."""
