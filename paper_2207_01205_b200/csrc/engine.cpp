@@ -986,12 +986,15 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
     // the fp32 real path: K2v2 (T <= 64) or its multi-warp form K2v2h (T = 128)
     const bool v2r = v2 || (fp32 && T == 128 && v2h128_enabled());
     const bool use_d = d_supported(T) && !f64_strict_forced();  // K2d for symmetric masks
+    // asymmetric masks in fp64: K2dc / K2dcx, except OFSE at T = 128 (the cluster
+    // kernel has no full-OD reduction: the strict kernel)
+    const bool dc_ok = dc_supported(T) && !(T == 128 && full_od(cfg));
     auto path_of = [&](int cls) {
         const bool sy = sym[static_cast<size_t>(cls)] != 0;
         if (!fp32)
             return !use_d ? (int)PATH_F64_STRICT
                    : sy   ? (int)PATH_F64_REAL
-                          : (dc_supported(T) ? (int)PATH_F64_CPLX : (int)PATH_F64_STRICT);
+                          : (dc_ok ? (int)PATH_F64_CPLX : (int)PATH_F64_STRICT);
         return sy ? (int)PATH_F32_REAL : (int)PATH_F32_COMPLEX;
     };
     // the fp64 kernel serving a range (fp64 mode, the fp32 mode's head and re-runs):
@@ -999,7 +1002,7 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
     auto hi_path = [&](int p) {
         if (!use_d) return (int)PATH_F64_STRICT;
         if (p == PATH_F32_REAL || p == PATH_F64_REAL) return (int)PATH_F64_REAL;
-        return dc_supported(T) ? (int)PATH_F64_CPLX : (int)PATH_F64_STRICT;
+        return dc_ok ? (int)PATH_F64_CPLX : (int)PATH_F64_STRICT;
     };
 
     const auto twf = twiddles(T, -1), twi = twiddles(T, +1);

@@ -421,6 +421,23 @@ def test_conceal_ofse_C1(gpu, orc):
     assert np.abs(out.restored - ref["restored"]).max() <= FP64_PX_TOL
 
 
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_conceal_ofse_T128_borders_vs_oracle(gpu, orc, precision):
+    """OFSE at T = 128 with border (asymmetric) windows: the strict kernel serves
+    them (the cluster kernel has no full-OD reduction) — oracle selections,
+    pixels <= 1e-9; an fp32 request runs the same fp64 OFSE kernels."""
+    rng = np.random.default_rng(557)
+    img = smooth_test_image(rng, 256)
+    blocks = [(0, 0, 32, 32), (96, 64, 32, 32), (224, 128, 32, 32), (128, 224, 32, 32)]
+    pat = P.LossPattern(256, 256, 32, 32, [P.Rect(*b) for b in blocks])
+    cfg = P.ConcealConfig(algorithm="ofse", gamma=0.5, iterations=40, transform_size=128, rho_hat=0.85,
+                          support_width=16, record_traces=True, precision=precision)
+    out = P.conceal(img, pat, cfg)
+    ref = _oracle_conceal(orc, img, pat, cfg)
+    _assert_same_selections(out.report.traces, ref["traces"])
+    assert np.abs(out.restored - ref["restored"]).max() <= FP64_PX_TOL
+
+
 def test_psnr_curves_vs_oracle(gpu, orc):
     """psnr_vs_iterations (pipeline.cpp:264-369): checkpointed PSNR after every
     `stride` selections for a gamma sweep + fse + ofse equals, point by point, the

@@ -48,10 +48,12 @@ def main(cases=60, seed=1):
         its = int(rng.choice([1, 7, 50, 150]))
         gamma = float(rng.choice([0.2, 0.5, 1.0]))
         rho = float(rng.choice([0.7, 0.8, 0.9]))
-        kw = dict(gamma=gamma, iterations=its, transform_size=t, rho_hat=rho, support_width=s)
+        algo = "ofse" if rng.random() < 0.2 else "fofse"
+        kw = dict(algorithm=algo, gamma=gamma, iterations=its, transform_size=t, rho_hat=rho, support_width=s)
         try:
             o64 = P.conceal(img, pat, P.ConcealConfig(**kw))
-            ref = orc.conceal(img, rects, b, b, gamma=gamma, iterations=its, t=t, rho_hat=rho, support=s)
+            ref = orc.conceal(img, rects, b, b, algorithm=oracle.ALGO_OFSE if algo == "ofse" else oracle.ALGO_FOFSE,
+                              gamma=gamma, iterations=its, t=t, rho_hat=rho, support=s)
             d64 = float(np.abs(o64.restored - ref["restored"]).max())
             o32 = P.conceal(img, pat, P.ConcealConfig(precision="fp32", **kw))
             d32 = float(np.abs(o32.restored - o64.restored).max())
@@ -62,7 +64,7 @@ def main(cases=60, seed=1):
             continue
         worst64, worst32, worstb = max(worst64, d64), max(worst32, d32), max(worstb, db)
         bad = d64 > 1e-9 or d32 > 0.5 or db > 0.05
-        print(f"case {c:3d} T={t:3d} b={b:2d} S={s:2d} {size}x{size} blocks={len(rects):4d} I={its:3d} "
+        print(f"case {c:3d} {algo:5s} T={t:3d} b={b:2d} S={s:2d} {size}x{size} blocks={len(rects):4d} I={its:3d} "
               f"g={gamma} rho={rho}: fp64-oracle {d64:.2e} fp32-fp64 {d32:.3f} batch-image {db:.2e}"
               f"{'  <-- FAIL' if bad else ''}", flush=True)
         if bad:
