@@ -142,14 +142,31 @@ __device__ __forceinline__ void v2_finish(const K2Args& a, const BlockDesc& desc
                 cyq = (Acc)cd.y;
             }
             const int nq = nr - q0 < 32 ? nr - q0 : 32;
-            for (int q = 0; q < nq; ++q) {
-                const int u = __shfl_sync(0xffffffffu, uq, q);
-                const Acc cx = __shfl_sync(0xffffffffu, cxq, q), cy = __shfl_sync(0xffffffffu, cyq, q);
-                const int uu1 = u >> 16, uu2 = u & 0xffff;
+            if (NTH % a.reg_nc == 0) {
+                // a lane's pixels share a column and step NTH / reg_nc rows: the twiddle
+                // index of pixel k is base + k d (one add per pixel instead of two products)
+                const int dm = NTH / a.reg_nc;
+                for (int q = 0; q < nq; ++q) {
+                    const int u = __shfl_sync(0xffffffffu, uq, q);
+                    const Acc cx = __shfl_sync(0xffffffffu, cxq, q), cy = __shfl_sync(0xffffffffu, cyq, q);
+                    const int uu1 = u >> 16, uu2 = u & 0xffff;
+                    const int base = uu1 * mm[0] + uu2 * nn[0], d = uu1 * dm;
 #pragma unroll
-                for (int k = 0; k < PX; ++k) {
-                    const TW tw = twi[(uu1 * mm[k] + uu2 * nn[k]) & (T - 1)];
-                    acc[k] = fma(cx, tw.x, fma(-cy, tw.y, acc[k]));
+                    for (int k = 0; k < PX; ++k) {
+                        const TW tw = twi[(base + k * d) & (T - 1)];
+                        acc[k] = fma(cx, tw.x, fma(-cy, tw.y, acc[k]));
+                    }
+                }
+            } else {
+                for (int q = 0; q < nq; ++q) {
+                    const int u = __shfl_sync(0xffffffffu, uq, q);
+                    const Acc cx = __shfl_sync(0xffffffffu, cxq, q), cy = __shfl_sync(0xffffffffu, cyq, q);
+                    const int uu1 = u >> 16, uu2 = u & 0xffff;
+#pragma unroll
+                    for (int k = 0; k < PX; ++k) {
+                        const TW tw = twi[(uu1 * mm[k] + uu2 * nn[k]) & (T - 1)];
+                        acc[k] = fma(cx, tw.x, fma(-cy, tw.y, acc[k]));
+                    }
                 }
             }
         }
