@@ -53,6 +53,7 @@ struct DCfg {
     static constexpr size_t IMG_BYTES = (size_t)NCOPY * T * SRV * sizeof(double);
     static constexpr size_t CLASS_BYTES = IMG_BYTES;  // class stride of the image array
     static constexpr bool TW64 = true;
+    static constexpr int TWX = 1;  // synthesis twiddle table: TWX * T entries
     static constexpr bool P32 = false;
     static constexpr size_t WBYTES = ((IMG_BYTES + 15) / 16) * 16;
     static constexpr size_t OFF_P = WBYTES;                            // 2T double2
@@ -691,6 +692,7 @@ struct DCCfg {
     static constexpr size_t IMG_BYTES = (size_t)T * SR * sizeof(double2);
     static constexpr size_t CLASS_BYTES = IMG_BYTES;  // class stride of the image array
     static constexpr bool TW64 = true;
+    static constexpr int TWX = 1;  // synthesis twiddle table: TWX * T entries
     static constexpr bool P32 = false;
     static constexpr size_t WBYTES = ((IMG_BYTES + 15) / 16) * 16;
     static constexpr size_t OFF_P = WBYTES;

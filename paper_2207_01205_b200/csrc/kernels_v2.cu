@@ -50,11 +50,12 @@ struct V2Cfg {
     static constexpr size_t IMG_BYTES = WELEMS * (REAL ? 4 : 8);
     static constexpr size_t CLASS_BYTES = IMG_BYTES;  // class stride of the image array
     static constexpr bool TW64 = false;
+    static constexpr int TWX = 8;  // synthesis twiddle table: TWX * T entries
     static constexpr bool P32 = true;  // fp32 rotated-frame phase table
     static constexpr size_t WBYTES = ((IMG_BYTES + 15) / 16) * 16;
     static constexpr size_t OFF_P = WBYTES;                            // 2T double2
     static constexpr size_t OFF_TW = OFF_P + sizeof(double2) * 2 * T;  // T float2
-    static constexpr size_t OFF_SP = OFF_TW + sizeof(float2) * T;      // spill: WARPS x (NP+SPT) float4
+    static constexpr size_t OFF_SP = OFF_TW + sizeof(float2) * T * TWX;  // spill: WARPS x (NP+SPT) float4
     static constexpr size_t OFF_ST = OFF_SP + sizeof(float4) * WARPS * (NP + SPT + 1);  // WARPS x V2State
     static constexpr size_t OFF_BAR = OFF_ST + 64 * WARPS;
     static constexpr size_t SMEM = OFF_BAR + 16;
@@ -551,8 +552,8 @@ __global__ void __launch_bounds__(128, (VAR == 3 || VAR == 9) ? 2 : 3) k2v2r_ker
             if (flagged && a.flag_energy && lane == 0) a.flag_energy[pos] = st->energy;
         }
         __syncwarp();
-        v2_finish<T, 32>(a, a.blocks[pos], pos, b, lane, st->energy, st->nu, conv, flagged, st->ntrace, rec_u, rec_c,
-                         rstride, twi);
+        v2_finish<T, 32, float2, Cf::TWX>(a, a.blocks[pos], pos, b, lane, st->energy, st->nu, conv, flagged, st->ntrace,
+                                          rec_u, rec_c, rstride, twi);
         __syncwarp();
     }
 }
@@ -973,7 +974,7 @@ __global__ void __launch_bounds__(128, 2) k2v2x_kernel(K2Args a) {
             }
         }
         __syncwarp();
-        v2_finish<T, 32>(a, a.blocks[j], j, b, lane, st->energy, st->nu, conv, 0, st->ntrace, rec_u, rec_c,
+        v2_finish<T, 32, float2, Cf::TWX>(a, a.blocks[j], j, b, lane, st->energy, st->nu, conv, 0, st->ntrace, rec_u, rec_c,
                          rstride, twi);
         __syncwarp();
     }
@@ -1034,11 +1035,12 @@ struct V2TCfg {
     static constexpr size_t IMG_BYTES = WELEMS * 4;
     static constexpr size_t CLASS_BYTES = IMG_BYTES;  // the K2v2r class image
     static constexpr bool TW64 = false;
+    static constexpr int TWX = 8;  // synthesis twiddle table: TWX * T entries
     static constexpr bool P32 = true;
     static constexpr size_t WBYTES = ((IMG_BYTES + 15) / 16) * 16;
     static constexpr size_t OFF_P = WBYTES;
     static constexpr size_t OFF_TW = OFF_P + sizeof(double2) * 2 * T;
-    static constexpr size_t OFF_SP = OFF_TW + sizeof(float2) * T;             // two float4 rows, one slot per team
+    static constexpr size_t OFF_SP = OFF_TW + sizeof(float2) * T * TWX;       // two float4 rows, one slot per team
     static constexpr size_t OFF_ST = OFF_SP + sizeof(float4) * 2 * WARPS * BPW;  // one V2State per team
     static constexpr size_t OFF_BAR = OFF_ST + 64 * WARPS * BPW;
     static constexpr size_t SMEM = OFF_BAR + 16;
@@ -1340,7 +1342,7 @@ __global__ void __launch_bounds__(128, 4) k2v2t_kernel(K2Args a) {
             for (int s = 0; s < SPT; ++s) R[(NP + s) * NT + sl] = make_float4(xr[s], 0.f, xi[s], 0.f);
         }
         __syncwarp();
-        v2_finish_teams<T, NT>(a, a.blocks[pos], pos, b, sl, has, st->energy, st->nu, conv, flagged, st->ntrace,
+        v2_finish_teams<T, NT, Cf::TWX>(a, a.blocks[pos], pos, b, sl, has, st->energy, st->nu, conv, flagged, st->ntrace,
                                rec_u, rec_c, rstride, twi);
         __syncwarp();
     }
@@ -1374,6 +1376,7 @@ struct V2HCfg {
     static constexpr size_t IMG_BYTES = WELEMS * 4;
     static constexpr size_t CLASS_BYTES = IMG_BYTES;  // class stride of the image array
     static constexpr bool TW64 = false;
+    static constexpr int TWX = 1;  // synthesis twiddle table: TWX * T entries
     static constexpr bool P32 = true;
     static constexpr size_t WBYTES = ((IMG_BYTES + 15) / 16) * 16;
     static constexpr size_t OFF_P = WBYTES;
@@ -1736,6 +1739,7 @@ struct V2PCfg {
     static constexpr size_t IMG_BYTES = 2 * NC * PLANE * 4;
     static constexpr size_t CLASS_BYTES = 4 * PLANE * 4;
     static constexpr bool TW64 = false;
+    static constexpr int TWX = 1;  // synthesis twiddle table: TWX * T entries
     static constexpr bool P32 = true;
     static constexpr size_t WBYTES = ((IMG_BYTES + 15) / 16) * 16;
     static constexpr size_t OFF_P = WBYTES;

@@ -52,8 +52,8 @@ __device__ __forceinline__ void v2_stage(const K2Args& a, const Tile& tile, unsi
         else
             reinterpret_cast<double2*>(smem + Cf::OFF_P)[i] = p;
     }
-    for (int i = threadIdx.x; i < T_of<Cf>(); i += blockDim.x) {
-        const double2 t = a.twid_inv[i];
+    for (int i = threadIdx.x; i < T_of<Cf>() * Cf::TWX; i += blockDim.x) {  // TWX periods (index without a wrap)
+        const double2 t = a.twid_inv[i & (T_of<Cf>() - 1)];
         if constexpr (Cf::TW64)
             reinterpret_cast<double2*>(smem + Cf::OFF_TW)[i] = t;
         else
@@ -98,7 +98,9 @@ __device__ __forceinline__ void v2_record(const K2Args& a, int b, int nu, int nt
 // 195-208) over the MISSING region, clamp + write-back (pipeline.cpp:226-232).
 // A team of NTH threads (t = 0..NTH-1, whole warps) shares the pixels; for
 // NTH > 32 the teams' partial squared errors meet in red[] behind named barrier bar.
-template <int T, int NTH, class TW = float2>
+// TWX >= 8: the twiddle table holds TWX periods, so the fast path's index
+// (base mod T) + k (d mod T) needs no wrap (k < PX <= 8)
+template <int T, int NTH, class TW = float2, int TWX = 1>
 __device__ __forceinline__ void v2_finish(const K2Args& a, const BlockDesc& desc, int pos, int b,
                                           int t, double energy, int nu, int conv, int flagged,
                                           int ntrace, const int* rec_u, const double2* rec_c,
@@ -151,10 +153,19 @@ __device__ __forceinline__ void v2_finish(const K2Args& a, const BlockDesc& desc
                     const Acc cx = __shfl_sync(0xffffffffu, cxq, q), cy = __shfl_sync(0xffffffffu, cyq, q);
                     const int uu1 = u >> 16, uu2 = u & 0xffff;
                     const int base = uu1 * mm[0] + uu2 * nn[0], d = uu1 * dm;
+                    if constexpr (TWX >= PX) {
+                        const int b0 = base & (T - 1), d0 = d & (T - 1);
 #pragma unroll
-                    for (int k = 0; k < PX; ++k) {
-                        const TW tw = twi[(base + k * d) & (T - 1)];
-                        acc[k] = fma(cx, tw.x, fma(-cy, tw.y, acc[k]));
+                        for (int k = 0; k < PX; ++k) {
+                            const TW tw = twi[b0 + k * d0];
+                            acc[k] = fma(cx, tw.x, fma(-cy, tw.y, acc[k]));
+                        }
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < PX; ++k) {
+                            const TW tw = twi[(base + k * d) & (T - 1)];
+                            acc[k] = fma(cx, tw.x, fma(-cy, tw.y, acc[k]));
+                        }
                     }
                 }
             } else {
@@ -215,7 +226,7 @@ __device__ __forceinline__ void v2_finish(const K2Args& a, const BlockDesc& desc
 // team). Every loop runs to the warp's largest count so the shuffles stay
 // convergent; a team past its own record count reads zero records, a team
 // without a block (or with a near-tie flag) writes nothing.
-template <int T, int NT>
+template <int T, int NT, int TWX = 1>
 __device__ __forceinline__ void v2_finish_teams(const K2Args& a, const BlockDesc& desc, int pos, int b, int t,
                                                 bool has, double energy, int nu, int conv, int flagged, int ntrace,
                                                 const int* rec_u, const double2* rec_c, int rstride,
@@ -257,14 +268,29 @@ __device__ __forceinline__ void v2_finish_teams(const K2Args& a, const BlockDesc
                 cyq = (float)cd.y;
             }
             const int nq = nrmax - q0 < NT ? nrmax - q0 : NT;
-            for (int q = 0; q < nq; ++q) {
-                const int u = __shfl_sync(0xffffffffu, uq, base + q);
-                const float cx = __shfl_sync(0xffffffffu, cxq, base + q), cy = __shfl_sync(0xffffffffu, cyq, base + q);
-                const int uu1 = u >> 16, uu2 = u & 0xffff;
+            if (TWX >= PX && NT % a.reg_nc == 0) {  // linear pixel rows, extended table (v2_finish)
+                const int dm = NT / a.reg_nc;
+                for (int q = 0; q < nq; ++q) {
+                    const int u = __shfl_sync(0xffffffffu, uq, base + q);
+                    const float cx = __shfl_sync(0xffffffffu, cxq, base + q), cy = __shfl_sync(0xffffffffu, cyq, base + q);
+                    const int uu1 = u >> 16, uu2 = u & 0xffff;
+                    const int b0 = (uu1 * mm[0] + uu2 * nn[0]) & (T - 1), d0 = (uu1 * dm) & (T - 1);
 #pragma unroll
-                for (int k = 0; k < PX; ++k) {
-                    const float2 tw = twi[(uu1 * mm[k] + uu2 * nn[k]) & (T - 1)];
-                    acc[k] = fmaf(cx, tw.x, fmaf(-cy, tw.y, acc[k]));
+                    for (int k = 0; k < PX; ++k) {
+                        const float2 tw = twi[b0 + k * d0];
+                        acc[k] = fmaf(cx, tw.x, fmaf(-cy, tw.y, acc[k]));
+                    }
+                }
+            } else {
+                for (int q = 0; q < nq; ++q) {
+                    const int u = __shfl_sync(0xffffffffu, uq, base + q);
+                    const float cx = __shfl_sync(0xffffffffu, cxq, base + q), cy = __shfl_sync(0xffffffffu, cyq, base + q);
+                    const int uu1 = u >> 16, uu2 = u & 0xffff;
+#pragma unroll
+                    for (int k = 0; k < PX; ++k) {
+                        const float2 tw = twi[(uu1 * mm[k] + uu2 * nn[k]) & (T - 1)];
+                        acc[k] = fmaf(cx, tw.x, fmaf(-cy, tw.y, acc[k]));
+                    }
                 }
             }
         }
