@@ -192,7 +192,11 @@ __global__ void __launch_bounds__(128, (VAR == 3 || VAR == 9) ? 2 : 3) k2v2r_ker
     // argmax keys per bin QUAD (two adjacent pairs): one key, one max and one
     // runner-up step per quad, the winning quad's other three bins join in the
     // controller — C4 K2v2r 48.9 -> 48.4 ms; VAR 1 keeps the key per pair
-    constexpr bool QK = VAR == 0;
+    constexpr bool QK = VAR == 0 || VAR == 4;
+    // VAR 0 carries no trace / gap diagnostics code (the launcher picks VAR 4 — the
+    // same kernel with it — when traces are requested): 1.7 % on C4, the loop's
+    // schedule at 168 registers is that sensitive
+    constexpr bool NODIAG = VAR == 0;
     constexpr int NQ = NP / 2;
     constexpr bool LO = false;  // the winning pair's smaller bin is added in the controller
 
@@ -227,7 +231,7 @@ __global__ void __launch_bounds__(128, (VAR == 3 || VAR == 9) ? 2 : 3) k2v2r_ker
     const float tau1 = a.tau1f;  // 1 - tau (tau == 0 disables the guard: S <= M)
     const int rstride = a.rec_stride > 0 ? a.rec_stride : a.iterations;
     const int lh1 = a.Lh - 1, lw1 = a.Lw - 1;
-    const bool diag = a.trace != nullptr || a.gap_trace != nullptr;
+    const bool diag = !NODIAG && (a.trace != nullptr || a.gap_trace != nullptr);
 
     for (int bi = warp; bi < tile.count; bi += Cf::WARPS) {
         const int pos = tile.begin + bi;
@@ -1062,8 +1066,9 @@ __device__ __forceinline__ unsigned team_max(unsigned v, int sub) {
     return m;
 }
 
-// QK: argmax keys per bin quad (as K2v2r); false: per pair
-template <int T, bool QK>
+// QK: argmax keys per bin quad (as K2v2r); false: per pair. DIAG: the trace /
+// gap diagnostics code (instantiated only when traces are requested)
+template <int T, bool QK, bool DIAG = false>
 __global__ void __launch_bounds__(128, 4) k2v2t_kernel(K2Args a) {
     using Cf = V2TCfg<T>;
     constexpr int SEG = Cf::SEG, SPT = Cf::SPT, NT = Cf::NT, NP = Cf::NP, SRV = Cf::SRV, BPW = Cf::BPW;
@@ -1100,7 +1105,7 @@ __global__ void __launch_bounds__(128, 4) k2v2t_kernel(K2Args a) {
     const float tau1 = a.tau1f;
     const int rstride = a.rec_stride > 0 ? a.rec_stride : a.iterations;
     const int lh1 = a.Lh - 1, lw1 = a.Lw - 1;
-    const bool diag = a.trace != nullptr || a.gap_trace != nullptr;
+    const bool diag = DIAG && (a.trace != nullptr || a.gap_trace != nullptr);
 
     for (int bw = warp * BPW; bw < tile.count; bw += Cf::WARPS * BPW) {  // warp-uniform
         const int bi = bw + sub;
@@ -1407,8 +1412,9 @@ struct HSlotQ {     // quad keys: the winning quad as two pairs
 };
 static_assert(sizeof(HSlotQ) == 48, "slot");
 
-// QK: argmax keys per bin quad (as K2v2r); false: per pair
-template <int T, bool QK>
+// QK: argmax keys per bin quad (as K2v2r); false: per pair. DIAG: the trace /
+// gap diagnostics code (instantiated only when traces are requested)
+template <int T, bool QK, bool DIAG = false>
 __global__ void __launch_bounds__(V2HCfg<T>::THREADS, V2HCfg<T>::MINB) k2v2h_kernel(K2Args a) {
     using Cf = V2HCfg<T>;
     constexpr int SEG = Cf::SEG, NT = Cf::NT, NP = Cf::NP, PPS = Cf::PPS, SRV = Cf::SRV, GW = Cf::GW;
@@ -1613,7 +1619,7 @@ __global__ void __launch_bounds__(V2HCfg<T>::THREADS, V2HCfg<T>::MINB) k2v2h_ker
                     rec_c[nu - 32 + lane] = make_double2(bcx, bcy);
                 }
             }
-            if (a.trace || a.gap_trace) {  // diagnostics only
+            if (DIAG && (a.trace || a.gap_trace)) {  // diagnostics only
                 if (tid == 0)
                     v2_record(a, b, nu, ntrace, 0, tstride, nullptr, nullptr, u1, u2, self,
                               (pr * P.x - pi * P.y) * iw, (pr * P.y + pi * P.x) * iw, c_re, c_im, energy, Mf, Sf);
@@ -2061,7 +2067,9 @@ static int k2v2_launch_t(const K2Args& a, int32_t ntiles, cudaStream_t s) {
             const char* e = getenv("FOFSE_V2T_QK");
             return !(e && e[0] == '0');
         }();
-        auto* fn = qk ? k2v2t_kernel<T, true> : k2v2t_kernel<T, false>;
+        const bool dg = a.trace || a.gap_trace;
+        auto* fn = dg ? (qk ? k2v2t_kernel<T, true, true> : k2v2t_kernel<T, false, true>)
+                      : (qk ? k2v2t_kernel<T, true> : k2v2t_kernel<T, false>);
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
         if (e != cudaSuccess) return e;
         if (ntiles <= 0) return cudaSuccess;
@@ -2072,6 +2080,7 @@ static int k2v2_launch_t(const K2Args& a, int32_t ntiles, cudaStream_t s) {
         auto* fn = v2r_variant() == 3   ? k2v2r_kernel<T, 3>
                    : v2r_variant() == 9 ? k2v2r_kernel<T, 9>
                    : v2r_variant() == 1 ? k2v2r_kernel<T, 1>
+                   : (v2r_variant() == 4 || a.trace || a.gap_trace) ? k2v2r_kernel<T, 4>
                                         : k2v2r_kernel<T, 0>;
         const size_t smem = (v2r_variant() == 3 || v2r_variant() == 9) ? V2Cfg<T, PATH, true>::SMEM : Cf::SMEM;
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -2089,7 +2098,9 @@ static int k2v2h_launch(const K2Args& a, int32_t ntiles, cudaStream_t s) {
         const char* e = getenv("FOFSE_V2H_QK");
         return !(e && e[0] == '0');
     }();
-    auto* fn = qk ? k2v2h_kernel<T, true> : k2v2h_kernel<T, false>;
+    const bool dg = a.trace || a.gap_trace;
+    auto* fn = dg ? (qk ? k2v2h_kernel<T, true, true> : k2v2h_kernel<T, false, true>)
+                  : (qk ? k2v2h_kernel<T, true> : k2v2h_kernel<T, false>);
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
     if (e != cudaSuccess) return e;
     if (ntiles <= 0) return cudaSuccess;
