@@ -345,7 +345,8 @@ __device__ __forceinline__ void d_replay(const K2Args& a, const double* vE, cons
     }
 }
 
-template <int T, bool FOD, bool REPLAY = false, bool WIDE = false, bool TIE = false>
+// DIAG: the trace / gap diagnostics code (instantiated only when traces are requested)
+template <int T, bool FOD, bool REPLAY = false, bool WIDE = false, bool TIE = false, bool DIAG = false>
 __global__ void __launch_bounds__(DCfg<T, WIDE>::THREADS, DCfg<T, WIDE>::MINB) k2d_kernel(K2Args a) {
     using Cf = DCfg<T, WIDE>;
     constexpr int SEG = Cf::SEG, NT = Cf::NT, GT = Cf::GT, NW = Cf::NW, PPS = Cf::PPS, SRV = Cf::SRV;
@@ -578,9 +579,9 @@ __global__ void __launch_bounds__(DCfg<T, WIDE>::THREADS, DCfg<T, WIDE>::MINB) k
             energy = 0.0 < e ? e : 0.0;
             nu += 1;
             if (ltid == 0) {
-                v2_record(a, b, nu, ntrace, rstride, tstride, rec_u, rec_c, u1, u2, self,
-                          (pr * P.x - pi * P.y) * iw, (pr * P.y + pi * P.x) * iw, c_re, c_im, energy, M, 0.0, geff,
-                          degen);
+                v2_record<DIAG>(a, b, nu, ntrace, rstride, tstride, rec_u, rec_c, u1, u2, self,
+                                (pr * P.x - pi * P.y) * iw, (pr * P.y + pi * P.x) * iw, c_re, c_im, energy, M, 0.0,
+                                geff, degen);
             }
             ntrace += 1;
 
@@ -1232,10 +1233,12 @@ template <int T, bool WIDE>
 static int k2d_tw(const K2Args& a, int32_t ntiles, cudaStream_t s) {
     using Cf = DCfg<T, WIDE>;
     const bool replay = a.src_pos != nullptr;
-    auto* fn = replay      ? k2d_kernel<T, false, true, WIDE>
-               : a.full_od ? k2d_kernel<T, true, false, WIDE>
-               : a.tau > 0.0 ? k2d_kernel<T, false, false, WIDE, true>  // fp64 mode: near-tie guard
-                             : k2d_kernel<T, false, false, WIDE>;
+    const bool dg = a.trace || a.gap_trace;
+    auto* fn = replay      ? (dg ? k2d_kernel<T, false, true, WIDE, false, true> : k2d_kernel<T, false, true, WIDE>)
+               : a.full_od ? (dg ? k2d_kernel<T, true, false, WIDE, false, true> : k2d_kernel<T, true, false, WIDE>)
+               : a.tau > 0.0 ? (dg ? k2d_kernel<T, false, false, WIDE, true, true>  // fp64 mode: near-tie guard
+                                   : k2d_kernel<T, false, false, WIDE, true>)
+                             : (dg ? k2d_kernel<T, false, false, WIDE, false, true> : k2d_kernel<T, false, false, WIDE>);
     const int rstride = a.rec_stride > 0 ? a.rec_stride : a.iterations;
     const size_t smem = replay ? ((Cf::SMEM + 31) & ~size_t(31)) +
                                      (sizeof(RSel) + sizeof(double2)) * (size_t)Cf::GROUPS * rstride

@@ -65,6 +65,8 @@ __device__ __forceinline__ void v2_stage(const K2Args& a, const Tile& tile, unsi
 
 // Lane 0 records a selection: synthesis record (pair factor folded in), the
 // IterationRecord trace (trace.hpp:13-21) and the guard diagnostics.
+// DIAG = false: the selection record only (kernels instantiated without the trace code)
+template <bool DIAG = true>
 __device__ __forceinline__ void v2_record(const K2Args& a, int b, int nu, int ntrace, int rstride,
                                           int tstride, int* rec_u, double2* rec_c, int u1, int u2,
                                           int self, double p_re, double p_im, double c_re,
@@ -74,6 +76,7 @@ __device__ __forceinline__ void v2_record(const K2Args& a, int b, int nu, int nt
         rec_u[nu - 1] = (u1 << 16) | u2;
         rec_c[nu - 1] = self ? make_double2(c_re, 0.0) : make_double2(2.0 * c_re, 2.0 * c_im);
     }
+    if (!DIAG) return;
     if (a.trace && ntrace < tstride) {
         fofse_record rr;
         rr.nu = nu;
