@@ -705,7 +705,7 @@ struct DCCfg {
     static_assert(T * T <= 4096, "key index bits");
 };
 
-template <int T, bool FOD, bool TIE = false>
+template <int T, bool FOD, bool TIE = false, bool DIAG = false>
 __global__ void __launch_bounds__(256, 2) k2dc_kernel(K2Args a) {
     using Cf = DCCfg<T>;
     constexpr int SEG = Cf::SEG, NT = Cf::NT, GT = Cf::GT, NW = Cf::NW, SR = Cf::SR;
@@ -885,8 +885,8 @@ __global__ void __launch_bounds__(256, 2) k2dc_kernel(K2Args a) {
             energy = 0.0 < e ? e : 0.0;
             nu += 1;
             if (ltid == 0)
-                v2_record(a, b, nu, ntrace, rstride, tstride, rec_u, rec_c, u1, u2, self, p_re, p_im, c_re, c_im,
-                          energy, M, 0.0, geff, degen);
+                v2_record<DIAG>(a, b, nu, ntrace, rstride, tstride, rec_u, rec_c, u1, u2, self, p_re, p_im, c_re, c_im,
+                                energy, M, 0.0, geff, degen);
             ntrace += 1;
 
             // ---- R[k] -= c W[k-u] + conj(c) W[k+u] (engine_spectral.cpp:112-125), next scan ----
@@ -991,7 +991,7 @@ struct DCXCfg {
     static_assert(SMEM <= 227 * 1024, "shared memory");
 };
 
-template <bool TIE>
+template <bool TIE, bool DIAG = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) k2dcx_kernel(K2Args a) {
     using Cf = DCXCfg;
     constexpr int T = Cf::T, SEG = Cf::SEG, NT = Cf::NT, SR = Cf::SR, NB = SEG + 1;
@@ -1164,8 +1164,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) k2dcx_kernel
             energy = 0.0 < e ? e : 0.0;
             nu += 1;
             if (ltid == 0)
-                v2_record(a, b, nu, ntrace, rstride, tstride, rec_u, rec_c, u1, u2, self, p_re, p_im, c_re, c_im,
-                          energy, M, 0.0, geff, 0);
+                v2_record<DIAG>(a, b, nu, ntrace, rstride, tstride, rec_u, rec_c, u1, u2, self, p_re, p_im, c_re, c_im,
+                                energy, M, 0.0, geff, 0);
             ntrace += 1;
             KA = 0;
             KB = 0;
@@ -1210,7 +1210,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) k2dcx_kernel
 
 static int k2dcx_launch(const K2Args& a, int32_t ntiles, cudaStream_t s) {
     if (a.full_od) return cudaErrorInvalidValue;  // OFSE at T = 128 keeps the strict kernel
-    auto* fn = a.tau > 0.0 ? k2dcx_kernel<true> : k2dcx_kernel<false>;
+    const bool dg = a.trace || a.gap_trace;
+    auto* fn = a.tau > 0.0 ? (dg ? k2dcx_kernel<true, true> : k2dcx_kernel<true>)
+                           : (dg ? k2dcx_kernel<false, true> : k2dcx_kernel<false>);
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DCXCfg::SMEM);
     if (e != cudaSuccess) return e;
     if (ntiles <= 0) return cudaSuccess;
@@ -1221,7 +1223,10 @@ static int k2dcx_launch(const K2Args& a, int32_t ntiles, cudaStream_t s) {
 template <int T>
 static int k2dc_t(const K2Args& a, int32_t ntiles, cudaStream_t s) {
     using Cf = DCCfg<T>;
-    auto* fn = a.full_od ? k2dc_kernel<T, true> : a.tau > 0.0 ? k2dc_kernel<T, false, true> : k2dc_kernel<T, false>;
+    const bool dg = a.trace || a.gap_trace;
+    auto* fn = a.full_od ? (dg ? k2dc_kernel<T, true, false, true> : k2dc_kernel<T, true>)
+               : a.tau > 0.0 ? (dg ? k2dc_kernel<T, false, true, true> : k2dc_kernel<T, false, true>)
+                             : (dg ? k2dc_kernel<T, false, false, true> : k2dc_kernel<T, false>);
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
     if (e != cudaSuccess) return e;
     if (ntiles <= 0) return cudaSuccess;
