@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(128, (VAR == 3 || VAR == 9) ? 2 : 3) k2v2r_ker
                 }
                 st->energy = en;
                 st->nu = nu;
-                st->ntrace += 1;
+                if constexpr (!NODIAG) st->ntrace += 1;  // NODIAG: ntrace = nu - (trace_from_nu0 ? 0 : nu0)
                 if (diag) {  // diagnostics only
                     const int tstride = a.trace_stride > 0 ? a.trace_stride : a.iterations;
                     const float iw = 1.f / w0;
@@ -556,7 +556,8 @@ __global__ void __launch_bounds__(128, (VAR == 3 || VAR == 9) ? 2 : 3) k2v2r_ker
             if (flagged && a.flag_energy && lane == 0) a.flag_energy[pos] = st->energy;
         }
         __syncwarp();
-        v2_finish<T, 32, float2, Cf::TWX>(a, a.blocks[pos], pos, b, lane, st->energy, st->nu, conv, flagged, st->ntrace,
+        const int ntr = NODIAG ? st->nu - (a.trace_from_nu0 ? 0 : (a.nu0 ? a.nu0[pos] : 0)) : st->ntrace;
+        v2_finish<T, 32, float2, Cf::TWX>(a, a.blocks[pos], pos, b, lane, st->energy, st->nu, conv, flagged, ntr,
                                           rec_u, rec_c, rstride, twi);
         __syncwarp();
     }
