@@ -460,7 +460,10 @@ def main():
                           "frac": k1_ach / peaks["dfma_tflops"] if peaks.get("dfma_tflops") else None,
                           "per_unit": f"{k1_flops:.0f} flop per block x {real_blocks} blocks",
                           "ms_per_step": k1_avg,
-                          "peak_source": "measured live by fofse_microbench(kind=3): DFMA, 148 SMs"}
+                          "peak_source": "measured live by fofse_microbench(kind=3): DFMA, 148 SMs",
+                          "timing": "CUDA events around K1 inside the concurrent chunk pipeline (it shares the SMs "
+                                    "with the border chunks and guard re-runs): a lower bound of its own rate; "
+                                    "K1 alone, serialised under ncu: profiles/r02_launches_C4.txt"}
             roof["k3"] = {"kernel": "fused into the iteration kernel's epilogue (sparse synthesis of the B x B hole "
                                     "from <= 2I records + clamp + write-back); no separate launch — its time is "
                                     "inside the K2 figure above, its share is in profiles/r02_k3_share.txt"}
