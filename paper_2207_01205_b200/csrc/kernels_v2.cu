@@ -1758,7 +1758,8 @@ struct V2PCfg {
     static_assert(NT <= 32, "one warp per block");
 };
 
-template <int T, int NC>
+// DIAG: the trace / gap diagnostics code (instantiated only when traces are requested)
+template <int T, int NC, bool DIAG = false>
 __global__ void __launch_bounds__(128, 3) k2v2c_kernel(K2Args a) {
     using Cf = V2PCfg<T, NC>;
     constexpr int SEG = Cf::SEG, SPT = Cf::SPT, NT = Cf::NT, NP = Cf::NP, SRV = Cf::SRV;
@@ -1911,7 +1912,7 @@ __global__ void __launch_bounds__(128, 3) k2v2c_kernel(K2Args a) {
                 st->energy = en;
                 st->nu = nu;
                 st->ntrace += 1;
-                if (a.trace || a.gap_trace) {
+                if (DIAG && (a.trace || a.gap_trace)) {
                     const float iw = 1.f / w0;
                     v2_record(a, b, nu, st->ntrace - 1, 0, tstride, nullptr, nullptr, u1, u2, self, pr * iw, pi * iw,
                               c_re, c_im, en, Mf, Sf);
@@ -2060,6 +2061,9 @@ static int k2v2_launch_t(const K2Args& a, int32_t ntiles, cudaStream_t s) {
             fn<<<ntiles, 32 * V2PCfg<T>::WARPS, smem, s>>>(a);
             return cudaGetLastError();
         };
+        if (a.trace || a.gap_trace)
+            return nc == 2 ? launch(k2v2c_kernel<T, 2, true>, V2PCfg<T, 2>::SMEM)
+                           : launch(k2v2c_kernel<T, 1, true>, V2PCfg<T, 1>::SMEM);
         return nc == 2 ? launch(k2v2c_kernel<T, 2>, V2PCfg<T, 2>::SMEM) : launch(k2v2c_kernel<T, 1>, V2PCfg<T, 1>::SMEM);
     } else if constexpr (T <= 32) {
         // several lost blocks per warp (K2v2t)
