@@ -1766,6 +1766,10 @@ __global__ void __launch_bounds__(128, 3) k2v2c_kernel(K2Args a) {
     constexpr int PPS = SEG / 2;
     constexpr size_t PL = Cf::PLANE;
     constexpr int ACC = 2;
+    // argmax keys per bin quad (as K2v2r): the key every second pair, the winning
+    // quad's other bins join in the controller
+    constexpr int NQ = NP / 2, XKEY = NQ;
+    static_assert(PPS % 2 == 0, "whole quads per segment");
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const Tile tile = a.tiles[blockIdx.x];
@@ -1833,10 +1837,12 @@ __global__ void __launch_bounds__(128, 3) k2v2c_kernel(K2Args a) {
 #pragma unroll
         for (int k = 0; k <= ACC; ++k) A[k] = KAcc{0.f, 0.f};
 #pragma unroll
-        for (int p = 0; p < NP; ++p) kacc_pair<false>(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+        for (int q = 0; q < NQ; ++q)
+            kacc_quad(A[q % ACC], __ffma2_rn(ip[2 * q], ip[2 * q], __fmul2_rn(rp[2 * q], rp[2 * q])),
+                      __ffma2_rn(ip[2 * q + 1], ip[2 * q + 1], __fmul2_rn(rp[2 * q + 1], rp[2 * q + 1])), q, kmask);
 #pragma unroll
         for (int s = 0; s < SPT; ++s)
-            if (exs[s]) kacc_one(A[ACC], fmaf(xi[s], xi[s], xr[s] * xr[s]), NP + s, kmask);
+            if (exs[s]) kacc_one(A[ACC], fmaf(xi[s], xi[s], xr[s] * xr[s]), XKEY + s, kmask);
 
         for (int it = 0; it < a.iterations && !conv; ++it) {
             float bm1 = A[0].m1, bm2 = A[0].m2;
@@ -1851,23 +1857,35 @@ __global__ void __launch_bounds__(128, 3) k2v2c_kernel(K2Args a) {
             const unsigned S = __reduce_max_sync(0xffffffffu, fbits(lane == wl ? bm2 : bm1));
             const int pw = 63 - static_cast<int>(M & 63u);
             __syncwarp();
-            if (lane == wl) spill[0] = pick_pair<NP, SPT>(pw, rp, ip, xr, xi);
+            if (lane == wl) {
+                float4 o0, o1;
+                pick_quad<NQ, SPT>(pw, rp, ip, xr, xi, o0, o1);
+                spill[0] = o0;
+                spill[1] = o1;
+            }
             __syncwarp();
             float2 pre;
             int jw, sw;
-            float lo_w = 0.f;  // the winning pair's smaller bin (kacc_pair<false>)
+            float lo_w = 0.f;  // the winning quad's other bins
             {
-                const float4 q = spill[0];
-                if (pw < NP) {
-                    const float ma = fmaf(q.z, q.z, q.x * q.x), mb = fmaf(q.w, q.w, q.y * q.y);
-                    lo_w = fminf(ma, mb);
-                    const int half = mb > ma ? 1 : 0;
-                    pre = half ? make_float2(q.y, q.w) : make_float2(q.x, q.z);
-                    sw = pw / PPS;
-                    jw = 2 * (pw % PPS) + half;
+                const float4 q0 = spill[0], q1 = spill[1];
+                if (pw < NQ) {
+                    const float m0 = fmaf(q0.z, q0.z, q0.x * q0.x), m1 = fmaf(q0.w, q0.w, q0.y * q0.y);
+                    const float m2 = fmaf(q1.z, q1.z, q1.x * q1.x), m3 = fmaf(q1.w, q1.w, q1.y * q1.y);
+                    const bool b1 = m1 > m0, b3 = m3 > m2;
+                    const float ma = b1 ? m1 : m0, oa = b1 ? m0 : m1;
+                    const float mb = b3 ? m3 : m2, ob = b3 ? m2 : m3;
+                    const bool hb = mb > ma;
+                    const int bq = hb ? (b3 ? 3 : 2) : (b1 ? 1 : 0);
+                    lo_w = fmax3(oa, ob, hb ? ma : mb);
+                    const float4 qq = (bq & 2) ? q1 : q0;
+                    pre = (bq & 1) ? make_float2(qq.y, qq.w) : make_float2(qq.x, qq.z);
+                    const int p0 = 2 * pw;
+                    sw = p0 / PPS;
+                    jw = 2 * (p0 % PPS) + bq;
                 } else {
-                    pre = make_float2(q.x, q.z);
-                    sw = pw - NP;
+                    pre = make_float2(q0.x, q0.z);
+                    sw = pw - NQ;
                     jw = SEG;
                 }
             }
@@ -1929,6 +1947,7 @@ __global__ void __launch_bounds__(128, 3) k2v2c_kernel(K2Args a) {
             for (int k = 0; k <= ACC; ++k) A[k] = KAcc{0.f, 0.f};
 #pragma unroll
             for (int s = 0; s < SPT; ++s) {
+                float2 mprev = make_float2(0.f, 0.f);
                 const int k1 = k1s[s], c0 = c0s[s];
                 const int rA = (k1 - u1) & (T - 1), rB = (k1 + u1) & (T - 1);
                 const int cA = (c0 - u2) & (T - 1), cB = (c0 + u2) & (T - 1);
@@ -1950,7 +1969,13 @@ __global__ void __launch_bounds__(128, 3) k2v2c_kernel(K2Args a) {
                             const float2 xr2 = ld(far, q), xi2 = ld(fai, q);
                             rp[p] = __ffma2_rn(ncr, xr2, __ffma2_rn(pci, xi2, rp[p]));
                             ip[p] = __ffma2_rn(ncr, xi2, __ffma2_rn(nci, xr2, ip[p]));
-                            kacc_pair<false>(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+                            {
+                                const float2 m = __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p]));
+                                if (q & 1)
+                                    kacc_quad(A[(p / 2) % ACC], mprev, m, p / 2, kmask);
+                                else
+                                    mprev = m;
+                            }
                         }
                     } else {
 #pragma unroll
@@ -1959,7 +1984,13 @@ __global__ void __launch_bounds__(128, 3) k2v2c_kernel(K2Args a) {
                             const float2 xr2 = ld(far, q), xi2 = ld(fai, q), yr2 = ld(fbr, q), yi2 = ld(fbi, q);
                             rp[p] = __ffma2_rn(nci, yi2, __ffma2_rn(ncr, yr2, __ffma2_rn(pci, xi2, __ffma2_rn(ncr, xr2, rp[p]))));
                             ip[p] = __ffma2_rn(pci, yr2, __ffma2_rn(ncr, yi2, __ffma2_rn(nci, xr2, __ffma2_rn(ncr, xi2, ip[p]))));
-                            kacc_pair<false>(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+                            {
+                                const float2 m = __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p]));
+                                if (q & 1)
+                                    kacc_quad(A[(p / 2) % ACC], mprev, m, p / 2, kmask);
+                                else
+                                    mprev = m;
+                            }
                         }
                     }
                 } else if (self) {
@@ -1969,7 +2000,13 @@ __global__ void __launch_bounds__(128, 3) k2v2c_kernel(K2Args a) {
                         const float2 xr2 = ar[q], xi2 = ai[q];
                         rp[p] = __ffma2_rn(ncr, xr2, __ffma2_rn(pci, xi2, rp[p]));
                         ip[p] = __ffma2_rn(ncr, xi2, __ffma2_rn(nci, xr2, ip[p]));
-                        kacc_pair<false>(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+                        {
+                            const float2 m = __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p]));
+                            if (q & 1)
+                                kacc_quad(A[(p / 2) % ACC], mprev, m, p / 2, kmask);
+                            else
+                                mprev = m;
+                        }
                     }
                 } else {
 #pragma unroll
@@ -1978,7 +2015,13 @@ __global__ void __launch_bounds__(128, 3) k2v2c_kernel(K2Args a) {
                         const float2 xr2 = ar[q], xi2 = ai[q], yr2 = br[q], yi2 = bi[q];
                         rp[p] = __ffma2_rn(nci, yi2, __ffma2_rn(ncr, yr2, __ffma2_rn(pci, xi2, __ffma2_rn(ncr, xr2, rp[p]))));
                         ip[p] = __ffma2_rn(pci, yr2, __ffma2_rn(ncr, yi2, __ffma2_rn(nci, xr2, __ffma2_rn(ncr, xi2, ip[p]))));
-                        kacc_pair<false>(A[p % ACC], __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p])), p, kmask);
+                        {
+                            const float2 m = __ffma2_rn(ip[p], ip[p], __fmul2_rn(rp[p], rp[p]));
+                            if (q & 1)
+                                kacc_quad(A[(p / 2) % ACC], mprev, m, p / 2, kmask);
+                            else
+                                mprev = m;
+                        }
                     }
                 }
                 if (exs[s]) {
@@ -1993,7 +2036,7 @@ __global__ void __launch_bounds__(128, 3) k2v2c_kernel(K2Args a) {
                     }
                     xr[s] = r;
                     xi[s] = m;
-                    kacc_one(A[ACC], fmaf(m, m, r * r), NP + s, kmask);
+                    kacc_one(A[ACC], fmaf(m, m, r * r), XKEY + s, kmask);
                 }
             }
         }
