@@ -53,14 +53,14 @@ struct DCfg {
     static constexpr size_t IMG_BYTES = (size_t)NCOPY * T * SRV * sizeof(double);
     static constexpr size_t CLASS_BYTES = IMG_BYTES;  // class stride of the image array
     static constexpr bool TW64 = true;
-    static constexpr int TWX = 1;  // synthesis twiddle table: TWX * T entries
+    static constexpr int TWX = GT >= 128 ? 2 : (GT >= 64 ? 4 : 8);  // synthesis twiddle table: TWX * T entries
     static constexpr bool P32 = false;
     static constexpr size_t WBYTES = ((IMG_BYTES + 15) / 16) * 16;
     static constexpr size_t OFF_P = WBYTES;                            // 2T double2
     static constexpr size_t OFF_TW = OFF_P + sizeof(double2) * 2 * T;  // T double2
     // per group: slots[2][NW] (32 B) + full-OD partials dred[2][NW] (16 B) + red[NW] (8 B)
     static constexpr size_t GRP = ((2 * NW * 32 + 2 * NW * 16 + 8 * NW + 15) / 16) * 16;
-    static constexpr size_t OFF_G = OFF_TW + sizeof(double2) * T;
+    static constexpr size_t OFF_G = OFF_TW + sizeof(double2) * T * TWX;
     static constexpr size_t OFF_BAR = OFF_G + GRP * GROUPS;
     static constexpr size_t SMEM = OFF_BAR + 16;
     static_assert(T * T <= (1 << KBITS), "key index bits");
@@ -661,7 +661,7 @@ __global__ void __launch_bounds__(DCfg<T, WIDE>::THREADS, DCfg<T, WIDE>::MINB) k
             __syncwarp();
         else
             named_bar_sync(bar, GT);
-        v2_finish<T, GT, double2>(a, a.blocks[pos], pos, b, ltid, energy, nu, conv, flagged, ntrace, rec_u, rec_c,
+        v2_finish<T, GT, double2, Cf::TWX>(a, a.blocks[pos], pos, b, ltid, energy, nu, conv, flagged, ntrace, rec_u, rec_c,
                                   rstride, twi, red, bar);
         if constexpr (NW == 1)
             __syncwarp();
@@ -693,13 +693,13 @@ struct DCCfg {
     static constexpr size_t IMG_BYTES = (size_t)T * SR * sizeof(double2);
     static constexpr size_t CLASS_BYTES = IMG_BYTES;  // class stride of the image array
     static constexpr bool TW64 = true;
-    static constexpr int TWX = 1;  // synthesis twiddle table: TWX * T entries
+    static constexpr int TWX = GT >= 128 ? 2 : (GT >= 64 ? 4 : 8);  // synthesis twiddle table: TWX * T entries
     static constexpr bool P32 = false;
     static constexpr size_t WBYTES = ((IMG_BYTES + 15) / 16) * 16;
     static constexpr size_t OFF_P = WBYTES;
     static constexpr size_t OFF_TW = OFF_P + sizeof(double2) * 2 * T;
     static constexpr size_t GRP = ((2 * NW * 32 + 2 * NW * 16 + 8 * NW + 15) / 16) * 16;
-    static constexpr size_t OFF_G = OFF_TW + sizeof(double2) * T;
+    static constexpr size_t OFF_G = OFF_TW + sizeof(double2) * T * TWX;
     static constexpr size_t OFF_BAR = OFF_G + GRP * GROUPS;
     static constexpr size_t SMEM = OFF_BAR + 16;
     static_assert(T * T <= 4096, "key index bits");
@@ -923,7 +923,7 @@ __global__ void __launch_bounds__(256, 2) k2dc_kernel(K2Args a) {
             __syncwarp();
         else
             named_bar_sync(bar, GT);
-        v2_finish<T, GT, double2>(a, a.blocks[pos], pos, b, ltid, energy, nu, conv, flagged, ntrace, rec_u, rec_c,
+        v2_finish<T, GT, double2, Cf::TWX>(a, a.blocks[pos], pos, b, ltid, energy, nu, conv, flagged, ntrace, rec_u, rec_c,
                                   rstride, twi, red, bar);
         if constexpr (NW == 1)
             __syncwarp();

@@ -1382,14 +1382,14 @@ struct V2HCfg {
     static constexpr size_t IMG_BYTES = WELEMS * 4;
     static constexpr size_t CLASS_BYTES = IMG_BYTES;  // class stride of the image array
     static constexpr bool TW64 = false;
-    static constexpr int TWX = 1;  // synthesis twiddle table: TWX * T entries
+    static constexpr int TWX = NT >= 128 ? 2 : (NT >= 64 ? 4 : 8);  // synthesis twiddle table: TWX * T entries
     static constexpr bool P32 = true;
     static constexpr size_t WBYTES = ((IMG_BYTES + 15) / 16) * 16;
     static constexpr size_t OFF_P = WBYTES;
     static constexpr size_t OFF_TW = OFF_P + sizeof(double2) * 2 * T;
     // per group: slots [2 parity][GW warps] x 32 B, red GW doubles
     static constexpr size_t GRP = 2 * GW * 48 + 8 * GW;  // [2][GW] slots (HSlotQ) + red
-    static constexpr size_t OFF_G = OFF_TW + sizeof(float2) * T;
+    static constexpr size_t OFF_G = OFF_TW + sizeof(float2) * T * TWX;
     static constexpr size_t OFF_BAR = OFF_G + GRP * GROUPS;
     static constexpr size_t SMEM = OFF_BAR + 16;
     static_assert(NT % 32 == 0 && GW >= 2 && GW <= 8, "whole warps per block");
@@ -1713,7 +1713,7 @@ __global__ void __launch_bounds__(V2HCfg<T>::THREADS, V2HCfg<T>::MINB) k2v2h_ker
         }
         // both warps see the records written by tid 0 before synthesising
         named_bar_sync(bar, NT);
-        v2_finish<T, NT>(a, a.blocks[pos], pos, b, tid, energy, nu, conv, flagged, ntrace, rec_u, rec_c, rstride,
+        v2_finish<T, NT, float2, Cf::TWX>(a, a.blocks[pos], pos, b, tid, energy, nu, conv, flagged, ntrace, rec_u, rec_c, rstride,
                          twi, red, bar);
         named_bar_sync(bar, NT);
     }
@@ -1746,12 +1746,12 @@ struct V2PCfg {
     static constexpr size_t IMG_BYTES = 2 * NC * PLANE * 4;
     static constexpr size_t CLASS_BYTES = 4 * PLANE * 4;
     static constexpr bool TW64 = false;
-    static constexpr int TWX = 1;  // synthesis twiddle table: TWX * T entries
+    static constexpr int TWX = 8;  // synthesis twiddle table: TWX * T entries
     static constexpr bool P32 = true;
     static constexpr size_t WBYTES = ((IMG_BYTES + 15) / 16) * 16;
     static constexpr size_t OFF_P = WBYTES;
     static constexpr size_t OFF_TW = OFF_P + sizeof(double2) * 2 * T;
-    static constexpr size_t OFF_SP = OFF_TW + sizeof(float2) * T;
+    static constexpr size_t OFF_SP = OFF_TW + sizeof(float2) * T * TWX;
     static constexpr size_t OFF_ST = OFF_SP + sizeof(float4) * WARPS * (NP + SPT + 1);
     static constexpr size_t OFF_BAR = OFF_ST + 64 * WARPS;
     static constexpr size_t SMEM = OFF_BAR + 16;
@@ -2050,7 +2050,7 @@ __global__ void __launch_bounds__(128, 3) k2v2c_kernel(K2Args a) {
             for (int s = 0; s < SPT; ++s) R[(NP + s) * NT + lane] = make_float4(xr[s], 0.f, xi[s], 0.f);
         }
         __syncwarp();
-        v2_finish<T, 32>(a, a.blocks[pos], pos, b, lane, st->energy, st->nu, conv, flagged, st->ntrace,
+        v2_finish<T, 32, float2, Cf::TWX>(a, a.blocks[pos], pos, b, lane, st->energy, st->nu, conv, flagged, st->ntrace,
                          a.rec_u_g + (size_t)b * rstride, a.rec_c_g + (size_t)b * rstride, rstride, twi);
         __syncwarp();
     }
