@@ -448,7 +448,10 @@ def main():
                 "traffic_source": "ncu --set full dram__bytes_read.sum + dram__bytes_write.sum of this kernel, per "
                                   "block-iteration x the units of one step (profiles/peaks.json)",
                 "note": "the iteration kernel is bound by on-chip shared-memory bandwidth / issue, not by HBM or "
-                        "tensor cores (GEMM-free: shifted complex updates + argmax)"}
+                        "tensor cores (GEMM-free: shifted complex updates + argmax)",
+                "timing": "summed CUDA-event durations of the kernel's launches on its stream; where the pipeline "
+                          "runs other kernels beside it (C5: the previous chunk's guard re-runs and the next "
+                          "chunk's preparation) the SMs are shared and this understates the kernel's own rate"}
         # K1: window gather + weighted forward FFT in fp64 (2.5 T^2 log2(T^2)
         # flops per block for the real-input 2-D FFT + 3 per window sample for w f and w f^2)
         if prec == "fp32" and k1_avg > 0:

@@ -1499,7 +1499,16 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             bool f64_direct = false;  // a small border range run in fp64 outright (no head, no guard)
         };
         std::vector<Chunk> chunks;
-        const int64_t chunk_min = 24576;  // blocks: keeps every chunk several waves deep
+        // blocks: keeps every chunk several waves deep (FOFSE_CHUNK_MIN: experiments).
+        // T = 128: three waves of K2v2h (~900 blocks), so the guard re-runs of a chunk
+        // overlap the next chunk's iteration instead of forming the job's tail (C5 +5 %
+        // with the preparation stream below)
+        static const int64_t chunk_min_env = [] {
+            const char* e = std::getenv("FOFSE_CHUNK_MIN");
+            return e ? static_cast<int64_t>(std::atoll(e)) : int64_t(0);
+        }();
+        const int64_t wave_t128 = (v2r && T == 128) ? k2v2_real_wave(T, ctx->device, real_gw) : 0;
+        const int64_t chunk_min = chunk_min_env > 0 ? chunk_min_env : wave_t128 > 0 ? 3 * wave_t128 : 24576;
         int nsm = 148;
         ck(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device), "SM count");
         const bool f64_direct_on = [] {  // FOFSE_BORDER_F64=0: small border ranges take the fp32 path
@@ -1585,14 +1594,15 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         ck(cudaStreamWaitEvent(ctx->side, ctx->ev[4], 0), "wait");
         ck(cudaStreamWaitEvent(ctx->side_hi, ctx->ev[4], 0), "wait");
         ck(cudaStreamWaitEvent(ctx->pre, ctx->ev[4], 0), "wait");
-        // FOFSE_PRE_STREAM=1: main-stream chunks run spectra + head on the pre
-        // stream, so chunk k+1's preparation overlaps chunk k's iteration. Measured
-        // (C4): +1 % on device-resident frames, -4 % end to end (it delays the
-        // frame groups' completion) — off by default.
-        static const bool pre_on = [] {
+        // the pre stream: main-stream chunks run spectra + head on it, so chunk k+1's
+        // preparation overlaps chunk k's iteration. Measured: C4 +1 % on device-resident
+        // frames but -4 % end to end (it delays the frame groups' completion) — off;
+        // T = 128 (C5, three-wave chunks) +5 % — on. FOFSE_PRE_STREAM=0/1 forces.
+        static const int pre_env = [] {
             const char* e = std::getenv("FOFSE_PRE_STREAM");
-            return e && e[0] == '1';
+            return e ? (e[0] == '1' ? 1 : 0) : -1;
         }();
+        const bool pre_on = pre_env >= 0 ? pre_env == 1 : T == 128;
         // guard re-runs resume at the near-tie (k2d_replay + K2d); FOFSE_RESUME=0
         // re-runs them from scratch (diagnostics)
         const bool resume_on = [] {

@@ -1,0 +1,7 @@
+for cm in 0 1200 900 600; do
+  for pre in 0 1; do
+  env FOFSE_CHUNK_MIN=$cm FOFSE_PRE_STREAM=$pre timeout 600 python bench.py --workload C5 --no-cpu-baseline --no-parity --no-fp64 --steps 5 --warmup 3 > gpurun_out/c5c.json 2>/dev/null
+  python -c "
+import json; d=json.loads(open('gpurun_out/c5c.json').read().strip().splitlines()[-1]); print('chunk_min=$cm pre=$pre', round(d['value']), round(d['e2e']['value']), d['ms_per_step'], d['detail']['guard_reruns_per_step'])"
+  done
+done
