@@ -575,6 +575,13 @@ void classify_frames(Job& job, const fofse_rect* blocks, const int64_t* offs, in
                      int H, std::vector<CellGrid>& grids) {
     const Geometry& g = job.geo;
     const int64_t n = offs[nframes];
+    static const bool prof = std::getenv("FOFSE_HOST_PROF") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what) {
+        if (prof)
+            std::fprintf(stderr, "[fofse host]   classify %7.3f ms  %s\n",
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(), what);
+    };
     job.blocks.resize(static_cast<size_t>(n));
     // Work pieces of <= 2048 blocks of one frame. Each piece dedupes its class
     // keys locally (first-appearance order; a window has few distinct keys), the
@@ -592,6 +599,16 @@ void classify_frames(Job& job, const fofse_rect* blocks, const int64_t* offs, in
             pieces.push_back({f, i0, std::min<int64_t>(i0 + 2048, offs[f + 1]), {}, {}});
     std::vector<uint16_t>& lid = job.lid;  // piece-local key index per block (< 2048)
     lid.resize(static_cast<size_t>(n));
+    // frames whose blocks all sit on the block grid: a window's neighbours are then
+    // exactly the cells it covers (no anchor one cell up / left can reach into it)
+    std::vector<char> aligned(static_cast<size_t>(nframes), 1);
+    parallel_for(nframes, [&](int64_t f) {
+        for (int64_t i = offs[f]; i < offs[f + 1]; ++i)
+            if (blocks[i].row % g.bh || blocks[i].col % g.bw) {
+                aligned[static_cast<size_t>(f)] = 0;
+                return;
+            }
+    }, 1);
     parallel_for(static_cast<int64_t>(pieces.size()), [&](int64_t pi) {
         Piece& pc = pieces[static_cast<size_t>(pi)];
         const int f = pc.f;
@@ -611,9 +628,10 @@ void classify_frames(Job& job, const fofse_rect* blocks, const int64_t* offs, in
             const int top = std::max(0, -r0), left = std::max(0, -c0);
             const int bottom = std::max(0, r0 + g.Lh - H), right = std::max(0, c0 + g.Lw - W);
             rects.clear();
-            const int cr0 = std::max(0, (std::max(r0, 0)) / g.bh - 1);
+            const int back = aligned[static_cast<size_t>(f)] ? 0 : 1;
+            const int cr0 = std::max(0, (std::max(r0, 0)) / g.bh - back);
             const int cr1 = std::min(cg.gh - 1, (std::min(r0 + g.Lh, H) - 1) / g.bh);
-            const int cc0 = std::max(0, (std::max(c0, 0)) / g.bw - 1);
+            const int cc0 = std::max(0, (std::max(c0, 0)) / g.bw - back);
             const int cc1 = std::min(cg.gw - 1, (std::min(c0 + g.Lw, W) - 1) / g.bw);
             for (int cr = cr0; cr <= cr1; ++cr)
                 for (int cc = cc0; cc <= cc1; ++cc) {
@@ -641,6 +659,7 @@ void classify_frames(Job& job, const fofse_rect* blocks, const int64_t* offs, in
             lid[static_cast<size_t>(i)] = static_cast<uint16_t>(u);
         }
     }, 1);
+    mark("pieces keyed");
     ClassTable tab;
     for (Piece& pc : pieces) {
         pc.gid.resize(pc.uniq.size());
@@ -649,12 +668,14 @@ void classify_frames(Job& job, const fofse_rect* blocks, const int64_t* offs, in
             pc.gid[u] = tab.intern(std::vector<int32_t>(k), [&] { return labels_from_key(g, k); });
         }
     }
+    mark("classes interned");
     parallel_for(static_cast<int64_t>(pieces.size()), [&](int64_t pi) {
         const Piece& pc = pieces[static_cast<size_t>(pi)];
         for (int64_t i = pc.i0; i < pc.i1; ++i)
             job.blocks[static_cast<size_t>(i)].cls = pc.gid[lid[static_cast<size_t>(i)]];
     }, 1);
     job.cls_labels = std::move(tab.labels);
+    mark("ids assigned");
 }
 
 // Window-mode classes: key = the label bytes themselves.
