@@ -181,7 +181,7 @@ __device__ __forceinline__ void d_replay(const K2Args& a, const double* vE, cons
                                          int src, double sgn_r, double sgn_c, double w0, double gw, int rstride,
                                          double (&re)[Cf::SEG + 1], double (&im)[Cf::SEG + 1], double& energy_out,
                                          int& nf_out, int& conv_out) {
-    constexpr int T = Cf::HT * 2, SEG = Cf::SEG, NT = Cf::NT, PPS = Cf::PPS, SRV = Cf::SRV, GT = Cf::GT;
+    constexpr int T = Cf::HT * 2, SEG = Cf::SEG, PPS = Cf::PPS, SRV = Cf::SRV, GT = Cf::GT;
     // R0 is stored in the fp64 packed layout of K1 (SEG = seg_for(T, 1)), which
     // differs from the kernel's own layout in the WIDE form
     const BinLayout Ls = BinLayout::make(T, seg_for(T, 1), 1);

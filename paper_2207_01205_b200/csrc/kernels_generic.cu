@@ -325,7 +325,6 @@ __global__ void __launch_bounds__(KG_THREADS) kg_kernel(KgArgs a) {
         }
     }
     if (a.block_sq && a.synth != SYN_WINDOW) {
-        int dummy = 0;
         double s = sq;
 #pragma unroll
         for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -336,7 +335,6 @@ __global__ void __launch_bounds__(KG_THREADS) kg_kernel(KgArgs a) {
             for (int k = 0; k < KG_THREADS / 32; ++k) tot += redv[k];
             a.block_sq[b] = tot;
         }
-        (void)dummy;
     }
 }
 
