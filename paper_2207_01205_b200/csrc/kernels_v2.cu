@@ -176,7 +176,9 @@ __device__ __forceinline__ void am_merge(float& m1, int& i1, float& m2, float om
 // so one LDS.64 from the even/odd-aligned V copy feeds two bins and every
 // update / magnitude is an FFMA2 / FMUL2 on a pair.
 // ============================================================================
-template <int T, int VAR>
+// ODD: the window's (Lh - 1) and (Lw - 1) are both odd (every interior window of
+// an even block + 2 S, e.g. 48 x 48): the wrap signs are compile-time -1
+template <int T, int VAR, bool ODD = false>
 __global__ void __launch_bounds__(128, (VAR == 3 || VAR == 9) ? 2 : 3) k2v2r_kernel(K2Args a) {
     // VAR 3: quad V layout, one LDS.128 per two bin pairs
     constexpr bool Q4 = VAR == 3 || VAR == 9;
@@ -221,8 +223,8 @@ __global__ void __launch_bounds__(128, (VAR == 3 || VAR == 9) ? 2 : 3) k2v2r_ker
     const int gb0 = k1s[0] * T + c0s[0];
     const int gb1 = k1s[SPT - 1] * T + c0s[SPT - 1];
     static_assert(NP + SPT <= 64, "pair index must fit the 6 key bits");
-    const float sgn_r = ((a.Lh - 1) & 1) ? -1.f : 1.f;
-    const float sgn_c = ((a.Lw - 1) & 1) ? -1.f : 1.f;
+    const float sgn_r = ODD ? -1.f : (((a.Lh - 1) & 1) ? -1.f : 1.f);
+    const float sgn_c = ODD ? -1.f : (((a.Lw - 1) & 1) ? -1.f : 1.f);
     // VAR 0 keeps the mask an immediate (two LOP3 per key): the register form saves
     // 32 instructions per block-iteration but measured 7 % slower on C4 (same-box A/B)
     const unsigned kmask = key_mask<VAR == 3 || VAR == 9>(a);
@@ -2129,6 +2131,7 @@ static int k2v2_launch_t(const K2Args& a, int32_t ntiles, cudaStream_t s) {
                    : v2r_variant() == 9 ? k2v2r_kernel<T, 9>
                    : v2r_variant() == 1 ? k2v2r_kernel<T, 1>
                    : (v2r_variant() == 4 || a.trace || a.gap_trace) ? k2v2r_kernel<T, 4>
+                   : (((a.Lh - 1) & 1) && ((a.Lw - 1) & 1) && v2r_variant() != 5) ? k2v2r_kernel<T, 0, true>
                                         : k2v2r_kernel<T, 0>;
         const size_t smem = (v2r_variant() == 3 || v2r_variant() == 9) ? V2Cfg<T, PATH, true>::SMEM : Cf::SMEM;
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
