@@ -1582,7 +1582,21 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
                 if (k == 0 && head == 0 && !ch.f64_direct) continue;
                 if (k == 1 && ch.f64_direct) continue;
                 const bool kv2 = ch.path == PATH_F32_REAL ? v2r : v2;
-                const int ng = k == 0 ? ng_f64(hi_path(ch.path)) : kv2 ? k2v2_blocks_per_cta(T, ch.path) : k2_groups_per_cta(T, ch.path);
+                // tile multipliers (blocks per group / warp per CTA; the kernels loop over a tile)
+                // head tiles of two rounds per group when the chunk fills the GPU many times
+                // over: the class image is staged once per two blocks (C4 +0.4 %)
+                static const int head_tm_env = [] {
+                    const char* e = std::getenv("FOFSE_HEAD_TM");
+                    return e ? std::max(1, std::atoi(e)) : 0;
+                }();
+                const int ng_h = ng_f64(hi_path(ch.path));
+                const int head_tm = head_tm_env > 0 ? head_tm_env : (ch.b1 - ch.b0 >= 8LL * nsm * ng_h ? 2 : 1);
+                static const int iter_tm = [] {
+                    const char* e = std::getenv("FOFSE_ITER_TM");
+                    return e ? std::max(1, std::atoi(e)) : 1;
+                }();
+                const int ng = k == 0 ? (ch.f64_direct ? 1 : head_tm) * ng_h
+                                      : iter_tm * (kv2 ? k2v2_blocks_per_cta(T, ch.path) : k2_groups_per_cta(T, ch.path));
                 TList& tl = tls[2 * ci + static_cast<size_t>(k)];
                 tl.ng = ng;
                 tl.r0 = all_runs.size();

@@ -530,7 +530,7 @@ __global__ void __launch_bounds__(K2Cfg<T, PATH>::THREADS) k2_kernel(K2Args a) {
                     p.stop = 1;
                     flagged = 1;
                 } else {
-                    const int u1 = G / T, u2 = G % T;
+                    const int u1 = static_cast<int>(static_cast<unsigned>(G) / T), u2 = static_cast<int>(static_cast<unsigned>(G) % T);  // G >= 0
                     const int v1 = (T - u1) % T, v2 = (T - u2) % T;
                     const int self = (u1 == v1 && u2 == v2);
                     double c_re, c_im, p_re, p_im, upd_re, upd_im, delta;

@@ -89,7 +89,9 @@ template <unsigned long long MASK = DKEY_MASK, bool TIE = false>
 __device__ __forceinline__ void dscan(unsigned long long& K, unsigned& S2, double re, double im, unsigned kidx) {
     const unsigned long long key = dkey<MASK>(re, im, kidx);
     if constexpr (TIE) S2 = max(S2, min(static_cast<unsigned>(key >> 32), static_cast<unsigned>(K >> 32)));
-    K = key > K ? key : K;
+    // keys are non-negative finite doubles: their order as doubles is their order as
+    // u64 — one DSETP instead of a two-word integer compare
+    K = __longlong_as_double(static_cast<long long>(key)) > __longlong_as_double(static_cast<long long>(K)) ? key : K;
 }
 
 // The exact runner-up key of a thread: the largest key of its bins other than
@@ -357,7 +359,9 @@ __global__ void __launch_bounds__(DCfg<T, WIDE>::THREADS, DCfg<T, WIDE>::MINB) k
     extern __shared__ __align__(16) unsigned char smem_raw[];
     if (a.ntiles_dev && (int)blockIdx.x >= *a.ntiles_dev) return;  // device-sized launch
     const Tile tile = a.tiles[blockIdx.x];
-    v2_stage<Cf>(a, tile, smem_raw);
+    // the image copy completes while the first block's spectrum loads (REPLAY reads V at once)
+    v2_stage<Cf, REPLAY>(a, tile, smem_raw);
+    bool staged = REPLAY;
     const double* vE = reinterpret_cast<const double*>(smem_raw);
     const double2* ptab = reinterpret_cast<const double2*>(smem_raw + Cf::OFF_P);
     const double2* twi = reinterpret_cast<const double2*>(smem_raw + Cf::OFF_TW);
@@ -417,6 +421,10 @@ __global__ void __launch_bounds__(DCfg<T, WIDE>::THREADS, DCfg<T, WIDE>::MINB) k
             const double2 v = (active && ex) ? R[SEG * NT + ltid] : make_double2(0.0, 0.0);
             re[SEG] = v.x;
             im[SEG] = v.y;
+            if (!staged) {
+                v2_stage_wait<Cf>(smem_raw);
+                staged = true;
+            }
             energy = a.energy0[pos];
             nu = a.nu0 ? a.nu0[pos] : 0;
             conv = (a.conv0 ? a.conv0[pos] : 0) | (e_init <= 0.0);
@@ -487,7 +495,7 @@ __global__ void __launch_bounds__(DCfg<T, WIDE>::THREADS, DCfg<T, WIDE>::MINB) k
                 }
             }
             const int G = s.g;
-            const int u1 = G / T, u2 = G % T;
+            const int u1 = static_cast<int>(static_cast<unsigned>(G) / T), u2 = static_cast<int>(static_cast<unsigned>(G) % T);  // G >= 0
             const int self = ((T - u1) % T == u1) && ((T - u2) % T == u2);
             const double2 P = ptab[(u1 * (a.Lh - 1) + u2 * (a.Lw - 1)) & (2 * T - 1)];  // e^{-j phi(u)}
             // gathers of this selection: V[k-u] (sign s1) and V[k+u] (sign s2) per owned bin
@@ -821,7 +829,7 @@ __global__ void __launch_bounds__(256, 2) k2dc_kernel(K2Args a) {
                 }
             }
             const int G = s.g;
-            const int u1 = G / T, u2 = G % T;
+            const int u1 = static_cast<int>(static_cast<unsigned>(G) / T), u2 = static_cast<int>(static_cast<unsigned>(G) % T);  // G >= 0
             const int self = ((T - u1) % T == u1) && ((T - u2) % T == u2);
             const double2* wa = wimg + ((k1 - u1) & (T - 1)) * SR + ((c0 - u2) & (T - 1));  // W[k-u]
             const double2* wb = wimg + ((k1 + u1) & (T - 1)) * SR + ((c0 + u2) & (T - 1));  // W[k+u]
@@ -1143,7 +1151,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) k2dcx_kernel
                 }
             }
             const int G = s.g;
-            const int u1 = G / T, u2 = G % T;
+            const int u1 = static_cast<int>(static_cast<unsigned>(G) / T), u2 = static_cast<int>(static_cast<unsigned>(G) % T);  // G >= 0
             const int self = ((T - u1) % T == u1) && ((T - u2) % T == u2);
             const int ca = (c0 - u2) & (T - 1), cb = (c0 + u2) & (T - 1);
             const WRun wa = wrun((k1 - u1) & (T - 1), ca);  // W[k-u]

@@ -262,12 +262,8 @@ __global__ void __launch_bounds__(K1fCfg<FT>::THREADS, FT == 64 ? 3 : 8) k1f_ker
 
     // ---- pack the canonical half ----
     double vmax2 = 0.0;
-    const BinLayout L = BinLayout::make(FT, a.seg, a.spt > 0 ? a.spt : 1);
     const bool rotate = path_is_rotated(a.path);
     constexpr int SEG16 = 16;  // seg_for(FT, fp64): the fp64 AoS layout of K2d / the strict kernel
-    const size_t per = a.out_stride > 0 ? (size_t)a.out_stride : packed32_floats(L, a.soa);
-    // thread -> (tid, first slot): the segment(s) of tid are fixed, no divisions
-    const int NT = L.NT, tid = threadIdx.x % NT, step = blockDim.x / NT;
     auto spec = [&](int k1, int k2) {
         double2 v;
         if (k2 <= FT / 2) {
@@ -320,7 +316,13 @@ __global__ void __launch_bounds__(K1fCfg<FT>::THREADS, FT == 64 ? 3 : 8) k1f_ker
             }
             o[(size_t)j * NT16] = v;
         }
-    } else if (L.SPT == 1 && path_is_f64(a.path)) {
+    } else {
+    // runtime layouts (divisions by runtime values: kept off the common path above)
+    const BinLayout L = BinLayout::make(FT, a.seg, a.spt > 0 ? a.spt : 1);
+    const size_t per = a.out_stride > 0 ? (size_t)a.out_stride : packed32_floats(L, a.soa);
+    // thread -> (tid, first slot): the segment(s) of tid are fixed, no divisions
+    const int NT = L.NT, tid = threadIdx.x % NT, step = blockDim.x / NT;
+    if (L.SPT == 1 && path_is_f64(a.path)) {
         // fp64 AoS (K2d / strict input): slot j of tid at j * NT + tid
         int k1, c0, ex;
         L.thread_segment(tid, 0, &k1, &c0, &ex);
@@ -345,6 +347,7 @@ __global__ void __launch_bounds__(K1fCfg<FT>::THREADS, FT == 64 ? 3 : 8) k1f_ker
                 put_packed32(static_cast<float*>(a.out) + (size_t)b * per, L, a.soa, j, tid,
                              static_cast<float>(v.x), static_cast<float>(v.y));
         }
+    }
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) vmax2 = fmax(vmax2, __shfl_xor_sync(0xffffffffu, vmax2, o));

@@ -33,8 +33,9 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
 }
 
 // Stage the class image (TMA bulk copy), the rotated-frame phase table and the
-// synthesis twiddles; returns once everything is resident.
-template <class Cf>
+// synthesis twiddles; returns once everything is resident (WAIT = false: the
+// tables are resident, the image copy is still in flight — v2_stage_wait).
+template <class Cf, bool WAIT = true>
 __device__ __forceinline__ void v2_stage(const K2Args& a, const Tile& tile, unsigned char* smem) {
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Cf::OFF_BAR);
     if (threadIdx.x == 0) {
@@ -60,7 +61,11 @@ __device__ __forceinline__ void v2_stage(const K2Args& a, const Tile& tile, unsi
             reinterpret_cast<float2*>(smem + Cf::OFF_TW)[i] = make_float2((float)t.x, (float)t.y);
     }
     __syncthreads();
-    mbar_wait(bar, 0);
+    if constexpr (WAIT) mbar_wait(bar, 0);
+}
+template <class Cf>
+__device__ __forceinline__ void v2_stage_wait(unsigned char* smem) {
+    mbar_wait(reinterpret_cast<uint64_t*>(smem + Cf::OFF_BAR), 0);
 }
 
 // Lane 0 records a selection: synthesis record (pair factor folded in), the

@@ -9,6 +9,6 @@ for r in $(seq $reps); do
     python -c "
 import json
 d=json.loads(open('gpurun_out/abn_${name}_${i}_$r.json').read().strip().splitlines()[-1])
-print('$i', '$E', round(d['value']), round(d['e2e']['value']), round(d['roofline']['frac'],4), round(d['detail']['real_iterate_ms'],2))"
+print('$i', '$E', round(d['value']), round(d['e2e']['value']), round(d['roofline']['frac'],4), round(d['detail']['real_iterate_ms'],2), round(d['detail'].get('k1_ms',0),2), round(d['detail'].get('init_ms',0),2))"
   done
 done
