@@ -21,6 +21,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "kcommon.cuh"
 #include "kernels.h"
 #include "layout.h"
@@ -367,6 +370,310 @@ __global__ void __launch_bounds__(K1fCfg<FT>::THREADS, FT == 64 ? 3 : 8) k1f_ker
         }
         a.energy[b] = e;
         a.init_max[b] = sqrt(m);
+    }
+}
+
+// ============================================================================
+// K1p: K1f for the headline input (T = 64, u8 frames, windows <= 48 x 48, the
+// fp64 AoS layout of K2d), persistent: a CTA walks its blocks (b += grid) with
+// the twiddle / phase tables staged once, the NEXT block's window copied into
+// shared memory by cp.async while the current one is transformed (no gather
+// latency on the row pass), and three CTA barriers per block. Row and column
+// FFTs as in K1f with the first radix-8 stage pruned (inputs n >= 48 are zero)
+// and XOR-swizzled 8 x 8 transposes (64 slots, conflict-free): the column pass
+// transposes in its own spectrum column, so only the row pass needs tiles.
+// ============================================================================
+struct K1pCfg {
+    static constexpr int FT = 64, LG = 8, THREADS = 256, NC = 33, CS = 65;
+    static constexpr int LMAX = 48;           // window rows / columns
+    static constexpr int NWR = 13;            // 4-byte words per staged window row (shift <= 3)
+    static constexpr int WROW = 4 * NWR;      // bytes per staged row
+    static constexpr size_t tw = 0;                                   // W_T^e, e < T
+    static constexpr size_t ph = tw + sizeof(double2) * FT;           // rotation phases, m < 2T
+    static constexpr size_t cb = ph + sizeof(double2) * 2 * FT;       // [NC][CS] spectrum tile
+    static constexpr size_t rt = cb + sizeof(double2) * NC * CS;      // [LMAX/2][64] row-pass tiles
+    static constexpr size_t win = rt + sizeof(double2) * (LMAX / 2) * 64;  // [2][LMAX][WROW] windows
+    static constexpr size_t red = win + 2 * LMAX * WROW;              // [2][16] doubles
+    static constexpr size_t total = red + 2 * 16 * sizeof(double);
+    static_assert(total <= 75 * 1024, "three CTAs per SM");
+};
+
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// element (row, col) of an 8 x 8 transpose tile: XOR swizzle, conflict-free both ways
+__device__ __forceinline__ int swz(int row, int col) { return row * 8 + (col ^ row); }
+
+// Forward 8-point DFT with x[6] = x[7] = 0 (natural order in and out).
+__device__ __forceinline__ void fft8_p6(double2 (&x)[8]) {
+    constexpr double H = 0.70710678118654752440;
+    const double2 a0 = c_add(x[0], x[4]), a1 = c_sub(x[0], x[4]);
+    const double2 a2 = x[2], a3 = x[2];
+    const double2 b0 = c_add(x[1], x[5]), b1 = c_sub(x[1], x[5]);
+    const double2 b2 = x[3], b3 = x[3];
+    const double2 E0 = c_add(a0, a2), E2 = c_sub(a0, a2);
+    const double2 E1 = c_add(a1, c_mj(a3)), E3 = c_sub(a1, c_mj(a3));
+    const double2 O0 = c_add(b0, b2), O2 = c_sub(b0, b2);
+    const double2 O1 = c_add(b1, c_mj(b3)), O3 = c_sub(b1, c_mj(b3));
+    const double2 t1 = make_double2(H * (O1.x + O1.y), H * (O1.y - O1.x));
+    const double2 t2 = c_mj(O2);
+    const double2 t3 = make_double2(H * (O3.y - O3.x), -H * (O3.x + O3.y));
+    x[0] = c_add(E0, O0);
+    x[4] = c_sub(E0, O0);
+    x[1] = c_add(E1, t1);
+    x[5] = c_sub(E1, t1);
+    x[2] = c_add(E2, t2);
+    x[6] = c_sub(E2, t2);
+    x[3] = c_add(E3, t3);
+    x[7] = c_sub(E3, t3);
+}
+
+// 64-point forward DFT of v[n] = x_t[m], n = t + 8 m (x_t[6], x_t[7] = 0), by the
+// 8 lanes t of a group; tile: the group's 64 swizzled slots. Lane t ends with X[t + 8 j].
+__device__ __forceinline__ void fft64_p6(double2 (&x)[8], int t, const double2* tw, double2* tile, unsigned gmask) {
+    fft8_p6(x);
+#pragma unroll
+    for (int k1 = 1; k1 < 8; ++k1) x[k1] = c_mul(x[k1], tw[t * k1]);
+#pragma unroll
+    for (int k1 = 0; k1 < 8; ++k1) tile[swz(k1, t)] = x[k1];
+    __syncwarp(gmask);
+#pragma unroll
+    for (int s = 0; s < 8; ++s) x[s] = tile[swz(t, s)];  // lane s's x[t]: Y[s][k1 = t]
+    __syncwarp(gmask);
+    fft8(x);
+}
+
+__global__ void __launch_bounds__(K1pCfg::THREADS, 3) k1p_kernel(K1Args a) {
+    using C = K1pCfg;
+    constexpr int FT = C::FT, LG = C::LG, CS = C::CS;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double2* tw = reinterpret_cast<double2*>(smem_raw + C::tw);
+    double2* ph = reinterpret_cast<double2*>(smem_raw + C::ph);
+    double2* cb = reinterpret_cast<double2*>(smem_raw + C::cb);
+    double* red = reinterpret_cast<double*>(smem_raw + C::red);
+    const int g = threadIdx.x / LG, t = threadIdx.x % LG;
+    const unsigned gmask = ((1u << LG) - 1u) << (LG * (g % (32 / LG)));
+    const int n = a.n_dev ? min(*a.n_dev, a.n) : a.n;
+    const uint8_t* src = static_cast<const uint8_t*>(a.fr.src);
+    const int Lh = a.Lh, Lw = a.Lw, W = a.fr.width, H = a.fr.height;
+    const bool rotate = path_is_rotated(a.path);
+
+    for (int i = threadIdx.x; i < FT; i += blockDim.x) tw[i] = a.twid[i];
+    for (int i = threadIdx.x; i < 2 * FT; i += blockDim.x) {
+        if (a.ptab) {
+            const double2 p = a.ptab[i];  // e^{-j pi m / T}
+            ph[i] = make_double2(p.x, -p.y);
+        } else {
+            ph[i] = phase_pos<FT>(i);
+        }
+    }
+    // row r of block d's window: its byte offset in the source and the alignment shift
+    auto row_off = [&](const BlockDesc& d, int r) -> int64_t {
+        return (int64_t)d.frame * a.fr.frame_stride + (int64_t)(d.row0 + r) * W + d.col0;
+    };
+    // stage block b's window into buffer buf: aligned words fully inside the frame
+    // row by cp.async, words straddling its left / right edge byte by byte, rows
+    // outside the frame and words left / right of it as zeros
+    auto stage = [&](int b, int buf) {
+        const BlockDesc d = a.blocks[b];
+        unsigned char* wb = smem_raw + C::win + (size_t)buf * C::LMAX * C::WROW;
+        for (int i = threadIdx.x; i < Lh * C::NWR; i += blockDim.x) {
+            const int r = i / C::NWR, w = i - r * C::NWR;
+            uint32_t* dst = reinterpret_cast<uint32_t*>(wb + r * C::WROW) + w;
+            const int gr = d.row0 + r;
+            if (gr < 0 || gr >= H) {
+                *dst = 0u;
+                continue;
+            }
+            const int64_t off = row_off(d, r);
+            const int shift = static_cast<int>((reinterpret_cast<uintptr_t>(src) + off) & 3);
+            const int fc = d.col0 - shift + 4 * w;  // frame column of the word's first byte
+            if (fc >= 0 && fc + 4 <= W) {
+                cp_async4(dst, src + off - shift + 4 * w);
+            } else if (fc + 4 <= 0 || fc >= W) {
+                *dst = 0u;
+            } else {
+                uint32_t v = 0u;
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (fc + j >= 0 && fc + j < W) v |= static_cast<uint32_t>(src[off - shift + 4 * w + j]) << (8 * j);
+                *dst = v;
+            }
+        }
+        cp_async_commit();
+    };
+
+    int b = blockIdx.x;
+    if (b < n) stage(b, 0);
+    cp_async_wait_all();
+    __syncthreads();
+    const int npairs = (Lh + 1) / 2;
+    const int nrows = 2 * npairs;  // rows >= nrows are zero (never stored)
+    for (int it = 0; b < n; b += gridDim.x, ++it) {
+        const int buf = it & 1;
+        const BlockDesc d = a.blocks[b];
+        if (b + (int)gridDim.x < n) stage(b + gridDim.x, buf ^ 1);  // lands during this block
+        const double* wc = a.wcls + (size_t)d.cls * Lh * Lw;
+        const unsigned char* wb = smem_raw + C::win + (size_t)buf * C::LMAX * C::WROW;
+
+        // ---- row pass: row pair g (rows 2g, 2g+1) ----
+        double energy = 0.0;
+        if (g < npairs) {
+            const int ra = 2 * g, rb = ra + 1;
+            const bool hasb = rb < Lh;
+            const double* wra = wc + ra * Lw;
+            const double* wrb = wc + (hasb ? rb : ra) * Lw;
+            const int sa = static_cast<int>((reinterpret_cast<uintptr_t>(src) + row_off(d, ra)) & 3);
+            const int sb = hasb ? static_cast<int>((reinterpret_cast<uintptr_t>(src) + row_off(d, rb)) & 3) : 0;
+            const unsigned char* pa = wb + ra * C::WROW + sa;
+            const unsigned char* pb = wb + (hasb ? rb : ra) * C::WROW + sb;
+            double2 x[8];
+#pragma unroll
+            for (int m = 0; m < 6; ++m) {
+                const int nn = t + LG * m;
+                const bool in = nn < Lw;
+                // samples off the frame / lost carry w = 0; u8 values are finite, so
+                // w * f = 0 for them whatever byte the staging holds
+                const double wa = in ? wra[nn] : 0.0, wbv = (in && hasb) ? wrb[nn] : 0.0;
+                const double fa = static_cast<double>(pa[nn]), fb = static_cast<double>(pb[nn]);
+                const double va = wa * fa, vb = wbv * fb;
+                energy = fma(va, fa, energy);
+                energy = fma(vb, fb, energy);
+                x[m] = make_double2(va, vb);
+            }
+            x[6] = make_double2(0.0, 0.0);
+            x[7] = x[6];
+            double2* tile = reinterpret_cast<double2*>(smem_raw + C::rt) + g * 64;
+            fft64_p6(x, t, tw, tile, gmask);
+            // lane t holds Z[k], k = t + 8 j; the unpack needs Z[-k]
+#pragma unroll
+            for (int j = 0; j < 8; ++j) tile[swz(j, t)] = x[j];
+            __syncwarp(gmask);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int k = t + LG * j;
+                if (k > FT / 2) continue;
+                const int nk = (FT - k) & (FT - 1);
+                const double2 zc = tile[swz(nk / LG, nk % LG)];
+                const double2 z = x[j];
+                cb[k * CS + ra] = make_double2(0.5 * (z.x + zc.x), 0.5 * (z.y - zc.y));
+                if (rb < FT) cb[k * CS + rb] = make_double2(0.5 * (z.y + zc.y), -0.5 * (z.x - zc.x));
+            }
+        }
+        __syncthreads();
+
+        // ---- column pass: group g < 31 -> column g + 1; group 31 -> columns 0 and 32 packed;
+        // each group transposes in its own column (64 swizzled slots of its CS = 65) ----
+        {
+            constexpr int GL = FT / 2 - 1;
+            const int col = g < GL ? g + 1 : 0;
+            double2 x[8];
+            if (g < GL) {
+#pragma unroll
+                for (int m = 0; m < 6; ++m) x[m] = (t + LG * m < nrows) ? cb[col * CS + t + LG * m] : make_double2(0.0, 0.0);
+            } else {
+#pragma unroll
+                for (int m = 0; m < 6; ++m)
+                    x[m] = (t + LG * m < nrows) ? make_double2(cb[t + LG * m].x, cb[(FT / 2) * CS + t + LG * m].x)
+                                                : make_double2(0.0, 0.0);
+            }
+            x[6] = make_double2(0.0, 0.0);
+            x[7] = x[6];
+            __syncwarp(gmask);  // the column's reads before the in-place transpose
+            // the packed group transposes in the (otherwise unused) slots of column 32
+            // only after both real columns are read: column 0's slots hold its input
+            double2* tile = cb + (g < GL ? col : FT / 2) * CS;
+            fft64_p6(x, t, tw, tile, gmask);
+            if (g < GL) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) cb[col * CS + t + LG * j] = x[j];
+            } else {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) tile[swz(j, t)] = x[j];
+                __syncwarp(gmask);
+                double2 z[8], zc[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int k = t + LG * j, nk = (FT - k) & (FT - 1);
+                    z[j] = x[j];
+                    zc[j] = tile[swz(nk / LG, nk % LG)];
+                }
+                __syncwarp(gmask);  // all lanes' reads of column 32's slots before the writes
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int k = t + LG * j;
+                    cb[k] = make_double2(0.5 * (z[j].x + zc[j].x), 0.5 * (z[j].y - zc[j].y));
+                    cb[(FT / 2) * CS + k] = make_double2(0.5 * (z[j].y + zc[j].y), -0.5 * (z[j].x - zc[j].x));
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) energy += __shfl_xor_sync(0xffffffffu, energy, o);
+        __syncthreads();  // the column pass's writes before the pack
+
+        // ---- pack the canonical half: fp64 AoS, SEG 16 (K2d / strict input) ----
+        double vmax2 = 0.0;
+        {
+            constexpr int SEG16 = 16, HT = FT / 2, QN = FT / SEG16, NT16 = HT * QN, STEP = C::THREADS / NT16;
+            const int tid16 = threadIdx.x % NT16, j0 = threadIdx.x / NT16;
+            const int vr = tid16 % HT, q = tid16 / HT;
+            int k1, c0, ex;
+            if (vr == 0) {
+                k1 = q < QN / 2 ? 0 : HT;
+                c0 = (q < QN / 2 ? q : q - QN / 2) * SEG16;
+                ex = q == QN / 2 - 1 || q == QN - 1;
+            } else {
+                k1 = vr;
+                c0 = q * SEG16;
+                ex = 0;
+            }
+            const int lw1 = Lw - 1;
+            const int nk1 = (FT - k1) & (FT - 1);
+            const int pbase = k1 * (Lh - 1);
+            double2* o = static_cast<double2*>(a.out) + (size_t)b * ((SEG16 + 1) * NT16) + tid16;
+#pragma unroll
+            for (int i = 0; i < (SEG16 + STEP) / STEP; ++i) {
+                const int j = j0 + STEP * i;
+                if (j > SEG16) break;
+                double2 v = make_double2(0.0, 0.0);
+                if (j < SEG16 || ex) {
+                    const int k2 = c0 + j;
+                    if (k2 <= FT / 2) {
+                        v = cb[k2 * CS + k1];
+                    } else {
+                        const double2 u = cb[(FT - k2) * CS + nk1];
+                        v = make_double2(u.x, -u.y);
+                    }
+                    vmax2 = fmax(vmax2, fma(v.x, v.x, v.y * v.y));
+                    if (rotate) v = c_mul(v, ph[(pbase + k2 * lw1) & (2 * FT - 1)]);
+                }
+                o[(size_t)j * NT16] = v;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) vmax2 = fmax(vmax2, __shfl_xor_sync(0xffffffffu, vmax2, o));
+        constexpr int NW = C::THREADS / 32;
+        double* rd = red + buf * 16;
+        if ((threadIdx.x & 31) == 0) {
+            rd[threadIdx.x >> 5] = energy;
+            rd[NW + (threadIdx.x >> 5)] = vmax2;
+        }
+        cp_async_wait_all();  // the next block's window (this thread's copies)
+        __syncthreads();      // ... everyone's; the pack's reads of cb before the next row pass
+        if (threadIdx.x == 0) {
+            double e = rd[0], m = rd[NW];
+#pragma unroll
+            for (int w = 1; w < NW; ++w) {
+                e += rd[w];
+                m = fmax(m, rd[NW + w]);
+            }
+            a.energy[b] = e;
+            a.init_max[b] = sqrt(m);
+        }
     }
 }
 
@@ -942,8 +1249,38 @@ int k1h_launch(const K1Args& a, cudaStream_t s) {
     return a.fr.type == SRC_U8 ? k1h_launch_t<uint8_t>(a, s) : k1h_launch_t<double>(a, s);
 }
 
+// K1p (persistent, cp.async-staged windows) for the headline input; FOFSE_K1P=0: K1f
+static bool k1p_usable(const K1Args& a) {
+    static const bool on = [] {
+        const char* e = std::getenv("FOFSE_K1P");
+        return !(e && e[0] == '0');
+    }();
+    return on && a.T == 64 && a.fr.type == SRC_U8 && a.blocks && a.Lh <= K1pCfg::LMAX && a.Lw <= K1pCfg::LMAX &&
+           (a.spt <= 1) && a.seg == 16 && path_is_f64(a.path);
+}
+
+static int k1p_launch(const K1Args& a, cudaStream_t s) {
+    static int grid_max = 0;
+    if (grid_max == 0) {
+        int dev = 0, nsm = 148, per = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaFuncSetAttribute(k1p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K1pCfg::total);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k1p_kernel, K1pCfg::THREADS, K1pCfg::total) != cudaSuccess ||
+            per < 1)
+            per = 1;
+        grid_max = nsm * per;
+    }
+    cudaError_t e = cudaFuncSetAttribute(k1p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K1pCfg::total);
+    if (e != cudaSuccess) return e;
+    if (a.n <= 0) return cudaSuccess;
+    k1p_kernel<<<std::min(a.n, grid_max), K1pCfg::THREADS, K1pCfg::total, s>>>(a);
+    return cudaGetLastError();
+}
+
 int k1f_launch(const K1Args& a, cudaStream_t s) {
     if (a.T == 128) return k1w_launch(a, s);
+    if (k1p_usable(a)) return k1p_launch(a, s);
     return a.T == 32 ? k1f_launch_t<32>(a, s) : k1f_launch_t<64>(a, s);
 }
 
