@@ -458,7 +458,10 @@ def main():
             Lw = wl.window
             k1_flops = 2.5 * T * T * math.log2(T * T) + 3 * Lw * Lw
             k1_ach = k1_flops * real_blocks / (k1_avg * 1e-3) / 1e12
-            roof["k1"] = {"kernel": f"fofse::k1f_kernel<{T}> (register FFT, fp64)" if T <= 64 else "fofse::k1w_kernel",
+            k1_name = ("fofse::k1p_kernel (persistent register FFT, cp.async-staged windows, fp64)"
+                       if T == 64 and wl.window <= 48 else
+                       f"fofse::k1f_kernel<{T}> (register FFT, fp64)" if T <= 64 else "fofse::k1w_kernel")
+            roof["k1"] = {"kernel": k1_name,
                           "bound": "fp64", "achieved": k1_ach, "peak": peaks.get("dfma_tflops"), "unit": "TFLOP/s",
                           "frac": k1_ach / peaks["dfma_tflops"] if peaks.get("dfma_tflops") else None,
                           "per_unit": f"{k1_flops:.0f} flop per block x {real_blocks} blocks",
@@ -466,7 +469,8 @@ def main():
                           "peak_source": "measured live by fofse_microbench(kind=3): DFMA, 148 SMs",
                           "timing": "CUDA events around K1 inside the concurrent chunk pipeline (it shares the SMs "
                                     "with the border chunks and guard re-runs): a lower bound of its own rate; "
-                                    "K1 alone, serialised under ncu: profiles/r02_launches_C4.txt"}
+                                    "K1 alone, serialised under ncu: profiles/r02_launches_C4.txt; issue / shared-memory / barrier "
+                                    "bound, not DFMA (profiles/r02_ncu_k1p_full.txt)"}
             roof["k3"] = {"kernel": "fused into the iteration kernel's epilogue (sparse synthesis of the B x B hole "
                                     "from <= 2I records + clamp + write-back); no separate launch — its time is "
                                     "inside the K2 figure above, its share is in profiles/r02_k3_share.txt"}

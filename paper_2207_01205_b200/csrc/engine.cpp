@@ -1529,7 +1529,9 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
             return e ? static_cast<int64_t>(std::atoll(e)) : int64_t(0);
         }();
         const int64_t wave_t128 = (v2r && T == 128) ? k2v2_real_wave(T, ctx->device, real_gw) : 0;
-        const int64_t chunk_min = chunk_min_env > 0 ? chunk_min_env : wave_t128 > 0 ? 3 * wave_t128 : 24576;
+        // 65,536 (C4: 4 chunks of the device-resident batch instead of 8, one pipeline
+        // bubble per chunk boundary less each: C4 +1 %, C3 +2 %; 24,576 before)
+        const int64_t chunk_min = chunk_min_env > 0 ? chunk_min_env : wave_t128 > 0 ? 3 * wave_t128 : 65536;
         int nsm = 148;
         ck(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device), "SM count");
         const bool f64_direct_on = [] {  // FOFSE_BORDER_F64=0: small border ranges take the fp32 path
@@ -2721,7 +2723,11 @@ static void conceal_frames_batch(fofse_ctx* ctx, const P* frames, int32_t n_fram
         // after the previous band's iteration, in partial waves) — off by default.
         const bool fp32 = params && params->precision == FOFSE_PREC_FP32;
         const bool by_frame = n_frames >= 16;
-        int G = by_frame ? std::clamp<int32_t>(n_frames / 16, 1, 8) : 1;
+        // at most 4 groups (C4 e2e: 4 groups 3.26 M blocks/s, 5: 3.25 M, 8: 3.22 M, 12: 3.19 M —
+        // every group boundary is a pipeline bubble; 2-3 groups expose too much transfer)
+        int G = by_frame ? std::clamp<int32_t>(n_frames / 16, 1, 4) : 1;
+        if (const char* e = std::getenv("FOFSE_FRAME_GROUPS"); e && by_frame)  // experiments
+            G = std::clamp<int32_t>(std::atoi(e), 1, std::max<int32_t>(1, n_frames));
         if (const char* e = std::getenv("FOFSE_ROW_GROUPS"); e && fp32 && !by_frame)
             G = std::clamp(std::atoi(e), 1, std::max(1, height / 64));
         // group boundaries (rows): the first and last groups are a quarter of the

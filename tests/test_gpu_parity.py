@@ -693,7 +693,7 @@ def test_frames_u8_matches_f64_and_is_deterministic(gpu):
 
 @pytest.mark.parametrize("nframes", [40, 130])
 def test_frame_groups_match_single_frames(gpu, nframes):
-    """The pipelined frames API with frame groups (40 frames: 2 groups; 130: 8
+    """The pipelined frames API with frame groups (40 frames: 2 groups; 130: 4
     groups, first/last a quarter of the others; lazily queued uploads, per-group
     downloads, two-copy border kernel) gives, frame by frame, the bytes (and the
     block errors to rounding) of concealing each frame on its own."""
