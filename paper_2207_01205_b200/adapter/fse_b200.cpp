@@ -139,11 +139,19 @@ ConcealOutput conceal(const SampleGrid& image, const LossPattern& pattern, const
     r.psnr = PsnrResult{rep.psnr_identical != 0, rep.psnr_db};
     r.mean_seconds_per_block = rep.mean_seconds_per_block;
     r.block_results.resize(static_cast<size_t>(n));
+    int64_t tc_total = 0;
+    if (!tr.empty())
+        for (int64_t i = 0; i < n; ++i) tc_total += tc[static_cast<size_t>(i)];
     for (int64_t i = 0; i < n; ++i) {
         BlockResult& br = r.block_results[static_cast<size_t>(i)];
         br.block = pattern.blocks[static_cast<size_t>(i)];
         // blocks run as one batch on the device: each gets the batch's device time / n
+        // the blocks run as one batch on the device: each gets its share of the batch's
+        // device time — by selections made when the traces give the counts, else equal
         br.seconds = rep.mean_seconds_per_block;
+        if (!tr.empty() && tc_total > 0)
+            br.seconds = rep.mean_seconds_per_block * static_cast<double>(n) *
+                         static_cast<double>(tc[static_cast<size_t>(i)]) / static_cast<double>(tc_total);
         if (tr.empty()) continue;
         const int32_t cnt = tc[static_cast<size_t>(i)];
         for (int32_t k = 0; k < cnt; ++k)
