@@ -22,12 +22,14 @@ freq=collections.Counter(round(r[2]) for r in recs if r[2]>0)
 print("total warp inst", tot)
 print("top exec counts", freq.most_common(8))
 cls=collections.defaultdict(lambda:[0,0.0,0.0])
+# per-unit normaliser: the largest execution count shared by many instructions (every selection)
+NSEL=max((k for k, n in freq.items() if n >= 50), default=1)
 for a,src,ex,s in recs:
     k=round(ex)
     cls[k][0]+=1; cls[k][1]+=ex; cls[k][2]+=s
 print("exec-count classes by total instructions:")
 for k,(n,e,s) in sorted(cls.items(), key=lambda kv:-kv[1][1])[:14]:
-    print(f"  count {k:>10}  static {n:4d}  dyn share {100*e/tot:5.1f}%  per-iter {e/max(cls, key=lambda k: cls[k][1] if k > 1e6 else 0) if False else 12870767:6.1f}")
+    print(f"  count {k:>10}  static {n:4d}  dyn share {100*e/tot:5.1f}%  per-iter {e/NSEL:6.1f}")
 if len(sys.argv)>2:
     want=int(sys.argv[2])
     for a,src,ex,s in recs:
