@@ -443,7 +443,7 @@ def main():
                 "traffic": (peaks["dram_per_unit"][wl.name] * its * (real_blocks if prec == "fp32" else n_blocks)
                             if wl.name in peaks.get("dram_per_unit", {}) and prec == "fp32" else None),
                 "per_unit": f"4*s*H = {4 * s * H} B per block-iteration (s={s}, H={H}); "
-                            f"{its} fp32 iterations x {real_blocks if prec == 'fp32' else n_blocks} blocks per step",
+                            f"{its} {prec} iterations x {real_blocks if prec == 'fp32' else n_blocks} blocks per step",
                 "peak_source": "measured live by fofse_microbench(kind=0): conflict-free LDS.64, 148 SMs",
                 "traffic_source": "ncu --set full dram__bytes_read.sum + dram__bytes_write.sum of this kernel, per "
                                   "block-iteration x the units of one step (profiles/peaks.json)",
