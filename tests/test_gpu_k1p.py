@@ -24,7 +24,7 @@ sys.path.insert(0, {root!r})
 import paper_2207_01205_b200 as P
 from paper_2207_01205_b200 import workloads as WL
 import dataclasses
-wl = dataclasses.replace(WL.C4, width={w}, height={h})
+wl = dataclasses.replace(WL.C4, width={w}, height={h}, loss_frac={lf})
 frames, rects, offs = wl.batch(seed={seed}, frames={nf})
 pats = []
 for f in range({nf}):
@@ -35,9 +35,9 @@ np.savez({path!r}, out=out, sq=sq)
 """
 
 
-def _run(tmp_path, k1p, prec, w, h, seed, nf):
+def _run(tmp_path, k1p, prec, w, h, seed, nf, lf=0.1):
     path = str(tmp_path / f"k1p{k1p}_{prec}_{w}.npz")
-    code = _SCRIPT.format(root=ROOT, w=w, h=h, seed=seed, nf=nf, prec=prec, path=path)
+    code = _SCRIPT.format(root=ROOT, w=w, h=h, seed=seed, nf=nf, prec=prec, path=path, lf=lf)
     env = dict(os.environ, FOFSE_K1P=str(k1p))
     subprocess.run([sys.executable, "-c", code], env=env, check=True, timeout=600)
     d = np.load(path)
@@ -49,5 +49,15 @@ def _run(tmp_path, k1p, prec, w, h, seed, nf):
 def test_k1p_matches_k1f_bitwise(tmp_path, prec, w, h, nf):
     a_out, a_sq = _run(tmp_path, 0, prec, w, h, 77, nf)
     b_out, b_sq = _run(tmp_path, 1, prec, w, h, 77, nf)
+    np.testing.assert_array_equal(a_out, b_out)
+    np.testing.assert_array_equal(a_sq, b_sq)
+
+
+def test_k1p_small_frames_match_k1f(tmp_path):
+    """Frames smaller than the window (57 x 45: every window clipped on two or more
+    sides, misaligned rows), half the cells lost."""
+    a_out, a_sq = _run(tmp_path, 0, "fp64", 57, 45, 5, 8, lf=0.5)
+    b_out, b_sq = _run(tmp_path, 1, "fp64", 57, 45, 5, 8, lf=0.5)
+    assert a_sq.size > 0
     np.testing.assert_array_equal(a_out, b_out)
     np.testing.assert_array_equal(a_sq, b_sq)
