@@ -813,6 +813,24 @@ double fp64_tie_tau(const Cfg& c) {
     return c.tau >= 0.0 ? c.tau : 1e-9;
 }
 
+// The same guard on the fp32 mode's fp64 phases (the head, fp64-outright border
+// ranges): a near-tie there is decided by the exact path too, so an exact
+// mathematical tie (e.g. a transpose-symmetric window over constant content) is
+// broken as the reference breaks it and not by K2d's last-bit rounding — without
+// it, C3 seed 300 has one block 0.63 px from the fp64 path. FOFSE_HEAD_TIE=0: off.
+double fp32_head_tie_tau(const Cfg& c) {
+    static const bool on = [] {
+        const char* e = std::getenv("FOFSE_HEAD_TIE");
+        return !(e && e[0] == '0');
+    }();
+    static const double tau = [] {
+        const char* e = std::getenv("FOFSE_HEAD_TIE_TAU");
+        return e ? std::atof(e) : 1e-9;
+    }();
+    if (!on || c.precision != FOFSE_PREC_FP32 || c.algorithm == FOFSE_ALGO_OFSE) return 0.0;
+    return tau;
+}
+
 // Frame-group I/O hooks of the pipelined frames API: group g's first kernel
 // waits for h2d_done[g]; once all of group g's work (iteration, re-runs) is
 // enqueued, on_done(g, s) enqueues its download on stream s after it.
@@ -1337,6 +1355,83 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
     const int64_t s32 = static_cast<int64_t>(std::max(packed32_floats(L32, 0), packed32_floats(L32r, soa_of(PATH_F32_REAL))));
     if (fp32) d_R32 = ctx->buf("R32").as<char>(static_cast<size_t>(n) * sizeof(float) * s32);
 
+    // Near-tie blocks (flags by position, != 0): the exact path — K1x + the strict
+    // kernel with the hypot argmax, bit-identical to the reference — for the whole
+    // block, its outputs overwriting whatever the fast path wrote; with frame groups
+    // (ev_patch != nullptr) their rectangles are copied again after their group's
+    // download. Used by the fp64 mode (K2d / K2dc near-tie guard) and by the fp32
+    // mode for near-ties inside its fp64 head / fp64-outright border ranges.
+    auto exact_reruns = [&](const int32_t* d_tie_flags, cudaStream_t xs, cudaEvent_t ev_patch, int64_t q0 = 0,
+                            int64_t q1 = -1, const std::string& bt = "", cudaStream_t cs = nullptr) -> int64_t {
+        const NvtxRange nv("fofse::fp64 near-tie exact re-runs");
+        if (q1 < 0) q1 = n;
+        if (!cs) cs = xs;  // the flags' copy stream
+        std::vector<int32_t> tie(static_cast<size_t>(q1 - q0));
+        if (q1 > q0)
+            ck(cudaMemcpyAsync(tie.data(), d_tie_flags + q0, sizeof(int32_t) * (q1 - q0), cudaMemcpyDeviceToHost, cs),
+               "D2H tie");
+        ck(cudaStreamSynchronize(cs), "sync");
+        std::vector<BlockDesc> xd;
+        std::vector<int32_t> xid;
+        std::vector<Tile> xt;
+        for (int64_t q = q0; q < q1; ++q)
+            if (tie[static_cast<size_t>(q - q0)]) {
+                xt.push_back(Tile{static_cast<int32_t>(xd.size()), static_cast<int32_t>(xd.size()), 1, 0});
+                xd.push_back(sorted[static_cast<size_t>(q)]);
+                xid.push_back(ids[static_cast<size_t>(q)]);
+            }
+        const int64_t m = static_cast<int64_t>(xd.size());
+        if (m == 0) return 0;
+        const size_t tt = static_cast<size_t>(T) * T;
+        BlockDesc* d_xd = upload(ctx, "x_desc" + bt, xd.data(), xd.size(), xs);
+        int32_t* d_xid = upload(ctx, "x_ids" + bt, xid.data(), xid.size(), xs);
+        Tile* d_xt = upload(ctx, "x_tiles" + bt, xt.data(), xt.size(), xs);
+        K1xArgs k{};
+        k.T = T;
+        k.Lh = g.Lh;
+        k.Lw = g.Lw;
+        k.n = static_cast<int32_t>(m);
+        k.seg = seg64;
+        k.blocks = d_xd;
+        k.fr = fr;
+        k.wcls = d_wcls;
+        k.twid = d_twf;
+        k.scratch = ctx->buf("x_scr" + bt).as<double2>(static_cast<size_t>(m) * 2 * tt);
+        k.rpacked = ctx->buf("x_R" + bt).as<double2>(static_cast<size_t>(m) * L64.SLOTS);
+        k.wimg = ctx->buf("x_W" + bt).as<double2>(static_cast<size_t>(m) * T * sr64);
+        k.w0 = ctx->buf("x_w0" + bt).as<double>(static_cast<size_t>(m));
+        k.energy = ctx->buf("x_e0" + bt).as<double>(static_cast<size_t>(m));
+        k.init_max = ctx->buf("x_imax" + bt).as<double>(static_cast<size_t>(m));
+        ck(k1x_launch(k, xs), "K1x exact init");
+        ++ctx->launches;
+        K2Args x = base_args();
+        x.path = PATH_F64_STRICT;
+        x.seg = seg64;
+        x.tau = 0.0;
+        x.exact_peak = 1;
+        x.tiles = d_xt;
+        x.order = d_xid;
+        x.blocks = d_xd;
+        x.rin = k.rpacked;
+        x.wimg = k.wimg;
+        x.wimg_stride = static_cast<int64_t>(T) * sr64;
+        x.w0 = k.w0;
+        x.energy0 = k.energy;
+        x.init_energy = k.energy;
+        x.init_max = k.init_max;
+        x.rec_global = 0;
+        ck(k2_launch(x, static_cast<int32_t>(m), xs), "K2 strict exact re-runs");
+        ++ctx->launches;
+        out.reruns += m;
+        if (ev_patch && gio && gio->on_patch) {
+            // their groups were downloaded without them: copy their blocks again
+            ck(cudaEventRecord(ev_patch, xs), "event");
+            ck(cudaStreamWaitEvent(ctx->io, ev_patch, 0), "wait");
+            for (const BlockDesc& d : xd) gio->on_patch(d.frame, d.row0 + g.S, d.col0 + g.S, g.bh, g.bw, ctx->io);
+        }
+        return m;
+    };
+
     if (!fp32) {
         // ---- fp64: K2d (symmetric masks) / strict kernel, every block ----
         const NvtxRange nv("fofse::fp64 iterate");
@@ -1389,71 +1484,8 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
                 ck(cudaStreamWaitEvent(st, ctx->event(i), 0), "wait");
             }
             if (d_tie) {
-                // ---- near-tie blocks: the exact path (K1x + strict kernel, hypot argmax) ----
-                const NvtxRange nv("fofse::fp64 near-tie exact re-runs");
-                std::vector<int32_t> tie(static_cast<size_t>(n));
-                ck(cudaMemcpyAsync(tie.data(), d_tie, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st), "D2H tie");
-                ck(cudaStreamSynchronize(st), "sync");
-                std::vector<BlockDesc> xd;
-                std::vector<int32_t> xid;
-                std::vector<Tile> xt;
-                for (int64_t q = 0; q < n; ++q)
-                    if (tie[static_cast<size_t>(q)]) {
-                        xt.push_back(Tile{static_cast<int32_t>(xd.size()), static_cast<int32_t>(xd.size()), 1, 0});
-                        xd.push_back(sorted[static_cast<size_t>(q)]);
-                        xid.push_back(ids[static_cast<size_t>(q)]);
-                    }
-                const int64_t m = static_cast<int64_t>(xd.size());
-                if (m > 0) {
-                    const size_t tt = static_cast<size_t>(T) * T;
-                    BlockDesc* d_xd = upload(ctx, "x_desc", xd.data(), xd.size());
-                    int32_t* d_xid = upload(ctx, "x_ids", xid.data(), xid.size());
-                    Tile* d_xt = upload(ctx, "x_tiles", xt.data(), xt.size());
-                    K1xArgs k{};
-                    k.T = T;
-                    k.Lh = g.Lh;
-                    k.Lw = g.Lw;
-                    k.n = static_cast<int32_t>(m);
-                    k.seg = seg64;
-                    k.blocks = d_xd;
-                    k.fr = fr;
-                    k.wcls = d_wcls;
-                    k.twid = d_twf;
-                    k.scratch = ctx->buf("x_scr").as<double2>(static_cast<size_t>(m) * 2 * tt);
-                    k.rpacked = ctx->buf("x_R").as<double2>(static_cast<size_t>(m) * L64.SLOTS);
-                    k.wimg = ctx->buf("x_W").as<double2>(static_cast<size_t>(m) * T * sr64);
-                    k.w0 = ctx->buf("x_w0").as<double>(static_cast<size_t>(m));
-                    k.energy = ctx->buf("x_e0").as<double>(static_cast<size_t>(m));
-                    k.init_max = ctx->buf("x_imax").as<double>(static_cast<size_t>(m));
-                    ck(k1x_launch(k, st), "K1x exact init");
-                    ++ctx->launches;
-                    K2Args x = base_args();
-                    x.path = PATH_F64_STRICT;
-                    x.seg = seg64;
-                    x.tau = 0.0;
-                    x.exact_peak = 1;
-                    x.tiles = d_xt;
-                    x.order = d_xid;
-                    x.blocks = d_xd;
-                    x.rin = k.rpacked;
-                    x.wimg = k.wimg;
-                    x.wimg_stride = static_cast<int64_t>(T) * sr64;
-                    x.w0 = k.w0;
-                    x.energy0 = k.energy;
-                    x.init_energy = k.energy;
-                    x.init_max = k.init_max;
-                    x.rec_global = 0;
-                    ck(k2_launch(x, static_cast<int32_t>(m), st), "K2 strict exact re-runs");
-                    ++ctx->launches;
-                    out.reruns += m;
-                    if (f64_pipe && gio->on_patch) {
-                        // their groups were downloaded without them: copy their blocks again
-                        ck(cudaEventRecord(ctx->event(ev_k2f + ranges.size()), st), "event");
-                        ck(cudaStreamWaitEvent(ctx->io, ctx->event(ev_k2f + ranges.size()), 0), "wait");
-                        for (const BlockDesc& d : xd)
-                            gio->on_patch(d.frame, d.row0 + g.S, d.col0 + g.S, g.bh, g.bw, ctx->io);
-                    }
-                }
+                cudaEvent_t evp = f64_pipe && gio && gio->on_patch ? ctx->event(ev_k2f + ranges.size()) : nullptr;
+                exact_reruns(d_tie, st, evp);
             }
         } else {
             // checkpointed curves (pipeline.cpp:264-369): resumable phases up to each
@@ -1500,6 +1532,9 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
     } else {
         // ---- fp32 fast mode: a pipeline over chunks of blocks ----
         const NvtxRange nv("fofse::fp32 chunk pipeline (K1 + fp64 head + fp32 iterate + guard re-runs)");
+        const double tie32 = ckpts ? 0.0 : fp32_head_tie_tau(cfg);
+        int32_t* d_htie = tie32 > 0.0 ? ctx->buf("htie").as<int32_t>(static_cast<size_t>(n)) : nullptr;
+        if (d_htie) ck(cudaMemsetAsync(d_htie, 0, sizeof(int32_t) * n, st), "memset");
         // chunk = K1 (+ fp64 head + convert) + the fp32 iteration; once a chunk
         // is done its near-tie re-runs (fp64, from scratch) are launched on the
         // aux stream, where they overlap the following chunks. Asymmetric-mask
@@ -1837,7 +1872,9 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
                 ck(cudaEventRecord(ctx->event(3 * ci + 1), ch.s), "event");
                 K2Args a = base_args();
                 a.rin = d_R64;
-                k2_f64(a, hp, ch.b0, ch.b1, sorted, "d" + tag, ch.s, cut_tiles(2 * ci, ch.s), tls[2 * ci].nt);
+                a.flags = d_htie;
+                k2_f64(a, hp, ch.b0, ch.b1, sorted, "d" + tag, ch.s, cut_tiles(2 * ci, ch.s), tls[2 * ci].nt, false,
+                       tie32);
                 ck(cudaEventRecord(ctx->event(3 * ci + 2), ch.s), "event");
                 continue;
             }
@@ -1902,7 +1939,9 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
                     a.rout_spt = spt_of(ch.path);
                     a.rout_stride = s32;
                 }
-                k2_f64(a, hi_path(ch.path), ch.b0, ch.b1, sorted, "h" + tag, ps, cut_tiles(2 * ci, ps), tls[2 * ci].nt);
+                a.flags = d_htie;
+                k2_f64(a, hi_path(ch.path), ch.b0, ch.b1, sorted, "h" + tag, ps, cut_tiles(2 * ci, ps), tls[2 * ci].nt,
+                       false, tie32);
                 if (!direct) {
                 CvtArgs c{};
                 c.T = T;
@@ -1974,13 +2013,26 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
         std::vector<int32_t> flags(static_cast<size_t>(n));
         int32_t* h_flags = flags.data();
         const size_t ev_host = ev_guard + chunks.size();  // [ev_host + ci]: host-driven re-runs of ci done
+        const size_t ev_x = 6 * chunks.size() + 2;        // [ev_x + ci]: exact re-runs of ci's head near-ties done
+        std::vector<char> has_x(chunks.size(), 0);
         for (size_t ci = 0; ci < chunks.size(); ++ci) {
             const Chunk& ch = chunks[ci];
             const bool last_of_group = ci + 1 == chunks.size() || chunks[ci + 1].grp != ch.grp;
+            if (d_htie) {
+                // near-ties inside this chunk's fp64 head (or fp64-outright range): the exact
+                // path as soon as the head is done, beside the chunk's fp32 phase (which
+                // leaves those blocks alone) — not as the job's tail
+                ck(cudaEventSynchronize(ctx->event(ch.f64_direct ? 3 * ci + 2 : 3 * ci + 1)), "sync head");
+                if (exact_reruns(d_htie, ctx->aux2, nullptr, ch.b0, ch.b1, std::to_string(ci), ctx->cpy) > 0) {
+                    ck(cudaEventRecord(ctx->event(ev_x + ci), ctx->aux2), "event");
+                    has_x[ci] = 1;
+                }
+            }
             auto group_done = [&]() {  // a frame group is complete once its chunks and their re-runs are done
                 if (!(gio && last_of_group)) return;
                 for (size_t cj = 0; cj <= ci; ++cj) {
                     if (chunks[cj].grp != ch.grp) continue;
+                    if (has_x[cj]) ck(cudaStreamWaitEvent(ctx->io, ctx->event(ev_x + cj), 0), "wait");
                     ck(cudaStreamWaitEvent(ctx->io, ctx->event(3 * cj + 2), 0), "wait");
                     if (!chunks[cj].f64_direct)
                         ck(cudaStreamWaitEvent(ctx->io,

@@ -827,7 +827,7 @@ __global__ void __launch_bounds__(K2Cfg<T, PATH>::THREADS) k2_kernel(K2Args a) {
         }
 
         double sq = 0.0;
-        if (a.synth != SYN_NONE && !fl) {
+        if (a.synth != SYN_NONE && !fl && !(gs->prm.conv & 2)) {
             const int npx = a.reg_nr * a.reg_nc;
             for (int px = ltid; px < npx; px += GT) {
                 const int m = a.reg_r0 + px / a.reg_nc;

@@ -491,6 +491,7 @@ __global__ void __launch_bounds__(DCfg<T, WIDE>::THREADS, DCfg<T, WIDE>::MINB) k
                 if (dtie<NB, NW, GT, KM>(a, re, im, active, ex, kbase, s.hi, s.lo, s2,
                                          reinterpret_cast<unsigned long long*>(dred + par * NW), w, ltid & 31, bar)) {
                     flagged = 1 + nu;  // near-tie: the block re-runs on the exact path
+                    conv = 2;          // fp32 mode's head: the fp32 phase leaves the block alone
                     break;
                 }
             }
@@ -825,6 +826,7 @@ __global__ void __launch_bounds__(256, 2) k2dc_kernel(K2Args a) {
                                                 reinterpret_cast<unsigned long long*>(dred + par * NW), w, ltid & 31,
                                                 bar)) {
                     flagged = 1 + nu;
+                    conv = 2;  // see k2d_kernel
                     break;
                 }
             }
@@ -1147,6 +1149,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) k2dcx_kernel
                     if (k != wb) s2 = max(s2, slots[par * Cf::NWG + k].hi);
                 if (s2 + 1u >= s.hi) {
                     flagged = 1 + nu;
+                    conv = 2;  // see k2d_kernel
                     break;
                 }
             }

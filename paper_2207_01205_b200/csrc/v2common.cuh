@@ -126,7 +126,10 @@ __device__ __forceinline__ void v2_finish(const K2Args& a, const BlockDesc& desc
         if (a.trace_count) a.trace_count[b] = ntrace;
     }
     __syncwarp();
-    if (a.synth == SYN_NONE || flagged) return;
+    // flagged (near-tie: re-run elsewhere) or conv & 2 (a near-tie inside the fp32 mode's
+    // fp64 head: the block goes to the exact path, whose write-back must find the
+    // frame's original pixels): no synthesis, no write-back
+    if (a.synth == SYN_NONE || flagged || (conv & 2)) return;
     const int nr = nu < rstride ? nu : rstride;
     const int npx = a.reg_nr * a.reg_nc;
     double sq = 0.0;
@@ -250,7 +253,7 @@ __device__ __forceinline__ void v2_finish_teams(const K2Args& a, const BlockDesc
         if (a.trace_count) a.trace_count[b] = ntrace;
     }
     __syncwarp();
-    const bool skip = !has || a.synth == SYN_NONE || flagged;
+    const bool skip = !has || a.synth == SYN_NONE || flagged || (conv & 2);
     if (__all_sync(0xffffffffu, skip)) return;
     const int nr = skip ? 0 : (nu < rstride ? nu : rstride);
     const int nrmax = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(nr)));

@@ -540,6 +540,21 @@ def test_fp32_default_on_c4_frames_vs_fp64(gpu):
     assert r["dpsnr_db"] <= FP32_PSNR_TOL and r["max_frame_dpsnr_db"] <= FP32_PSNR_TOL, r
 
 
+def test_fp32_head_exact_ties_follow_the_reference(gpu):
+    """C3 seed 300 (T = 32, 52,429 blocks of one 4096^2 image) holds exact
+    argmax ties inside the fp64 head (windows over saturated content): the
+    head's near-tie guard sends those blocks to the exact path, as the fp64
+    mode does, so no block ends far from the fp64 path (without it: block 212
+    of frame 0 at 0.63 px)."""
+    import dataclasses
+
+    from paper_2207_01205_b200 import parity
+    r = parity.fp32_vs_fp64(dataclasses.replace(WL.C3, frames=1), seed=300, per_call=1)
+    assert r["blocks"] == 52429
+    assert r["blocks_over_0.5"] == 0 and r["max_px"] <= 0.01, r
+    assert r["dpsnr_db"] <= FP32_PSNR_TOL, r
+
+
 def test_fp32_default_on_c5_vs_fp64(gpu):
     """T = 128 (C5, 3,277 blocks of one 8192^2 image, 300 iterations) at the shipped
     fp32 default against the fp64 path."""
