@@ -2023,8 +2023,9 @@ RunOut run_job(fofse_ctx* ctx, Job& job, const Cfg& cfg, fofse::Frames fr, int s
                 // path as soon as the head is done, beside the chunk's fp32 phase (which
                 // leaves those blocks alone) — not as the job's tail
                 ck(cudaEventSynchronize(ctx->event(ch.f64_direct ? 3 * ci + 2 : 3 * ci + 1)), "sync head");
-                if (exact_reruns(d_htie, ctx->aux2, nullptr, ch.b0, ch.b1, std::to_string(ci), ctx->cpy) > 0) {
-                    ck(cudaEventRecord(ctx->event(ev_x + ci), ctx->aux2), "event");
+                // (their own high-priority stream: not ahead of the fp32 guard's re-runs on aux2)
+                if (exact_reruns(d_htie, ctx->side_hi, nullptr, ch.b0, ch.b1, std::to_string(ci), ctx->cpy) > 0) {
+                    ck(cudaEventRecord(ctx->event(ev_x + ci), ctx->side_hi), "event");
                     has_x[ci] = 1;
                 }
             }
